@@ -1,0 +1,401 @@
+"""Pins for the host oracle (oracle/dbm_oracle.c) against things other than itself:
+numpy/BLAS products (a library routine), brute force on tiny inputs, closed forms,
+invariants, and the values PAPER.md / SPEC.md print (tests/golden/paper_pins.txt).
+
+Each test names the plausible oracle mistake it would catch.  CPU only.
+"""
+import math
+import os
+
+import numpy as np
+import pytest
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden", "paper_pins.txt")
+
+
+def golden():
+    out = {}
+    for line in open(GOLD):
+        line = line.split("#", 1)[0].strip()
+        if not line:
+            continue
+        k, v = [s.strip() for s in line.split("=")]
+        vals = [int(x) for x in v.split(",")]
+        out[k] = vals[0] if len(vals) == 1 else tuple(vals)
+    return out
+
+
+G = golden()
+
+
+def rand_arena(rng, Mb, Nb, bs, ints=False):
+    if ints:
+        return rng.integers(-2, 3, size=Mb * Nb * bs * bs).astype(np.float64)
+    return rng.uniform(-1, 1, size=Mb * Nb * bs * bs)
+
+
+# ----------------------------------------------------------------- the product
+@pytest.mark.parametrize("Mb,Nb,Kb,bs", [(1, 1, 1, 1), (2, 3, 4, 2), (3, 2, 5, 4), (2, 2, 2, 22), (1, 3, 2, 7)])
+def test_multiply_matches_numpy_matmul(orc, Mb, Nb, Kb, bs):
+    """Catches a transposed operand, wrong block index or dropped term: M != N != K."""
+    rng = np.random.default_rng(Mb * 100 + Nb * 10 + Kb + bs)
+    A = rand_arena(rng, Mb, Kb, bs)
+    B = rand_arena(rng, Kb, Nb, bs)
+    C = rand_arena(rng, Mb, Nb, bs)
+    Ad = orc.arena_to_dense(A, Mb, Kb, bs)
+    Bd = orc.arena_to_dense(B, Kb, Nb, bs)
+    Cd = orc.arena_to_dense(C, Mb, Nb, bs)
+    alpha, beta = 0.75, -1.25
+    expect = alpha * (Ad @ Bd) + beta * Cd
+    orc.multiply_blocked(Mb, Nb, Kb, bs, alpha, A, B, beta, C)
+    got = orc.arena_to_dense(C, Mb, Nb, bs)
+    assert np.abs(got - expect).max() <= 1e-13 * max(1.0, np.abs(expect).max()) * Kb * bs
+    # brute-force dense triple loop agrees as well
+    bf = orc.dense_gemm(alpha, Ad, Bd, beta, Cd)
+    assert np.abs(bf - expect).max() <= 1e-13 * Kb * bs
+
+
+def test_arena_dense_layout_is_column_major_blocks(orc):
+    """Element (x,y) of block (bi,bj) sits at slot*bs^2 + y*bs + x (reading R3)."""
+    Mb, Nb, bs = 2, 3, 3
+    g = np.arange(Mb * Nb * bs * bs, dtype=np.float64)
+    d = orc.arena_to_dense(g, Mb, Nb, bs)
+    for bi in range(Mb):
+        for bj in range(Nb):
+            for x in range(bs):
+                for y in range(bs):
+                    assert d[bi * bs + x, bj * bs + y] == (bi * Nb + bj) * bs * bs + y * bs + x
+    assert np.array_equal(orc.dense_to_arena(d, bs), g)
+
+
+def test_identity_and_permutation_are_bit_exact(orc):
+    """A = I gives C = B exactly; a permutation matrix permutes block rows exactly (misrouting)."""
+    rng = np.random.default_rng(7)
+    Mb = Kb = 4
+    Nb, bs = 3, 5
+    B = rand_arena(rng, Kb, Nb, bs)
+    I = orc.dense_to_arena(np.eye(Mb * bs), bs)
+    C = np.zeros(Mb * Nb * bs * bs)
+    orc.multiply_blocked(Mb, Nb, Kb, bs, 1.0, I, B, 0.0, C)
+    assert np.array_equal(C, B)
+    perm = rng.permutation(Mb * bs)
+    Pm = np.eye(Mb * bs)[perm]
+    Pa = orc.dense_to_arena(Pm, bs)
+    orc.multiply_blocked(Mb, Nb, Kb, bs, 1.0, Pa, B, 0.0, C)
+    assert np.array_equal(orc.arena_to_dense(C, Mb, Nb, bs), orc.arena_to_dense(B, Kb, Nb, bs)[perm])
+
+
+def test_alpha_beta_conventions(orc):
+    """beta = 0 never reads C (NaN-filled C stays out); alpha = 0 never reads A, B; linearity."""
+    rng = np.random.default_rng(3)
+    Mb, Nb, Kb, bs = 2, 2, 3, 4
+    A, B = rand_arena(rng, Mb, Kb, bs), rand_arena(rng, Kb, Nb, bs)
+    C0 = rand_arena(rng, Mb, Nb, bs)
+    Cn = np.full_like(C0, np.nan)
+    orc.multiply_blocked(Mb, Nb, Kb, bs, 1.0, A, B, 0.0, Cn)
+    assert not np.isnan(Cn).any()
+    An = np.full_like(A, np.nan)
+    C1 = C0.copy()
+    orc.multiply_blocked(Mb, Nb, Kb, bs, 0.0, An, B, -1.25, C1)
+    assert np.array_equal(C1, -1.25 * C0)
+    AB = np.zeros_like(C0)
+    orc.multiply_blocked(Mb, Nb, Kb, bs, 1.0, A, B, 0.0, AB)
+    C2 = C0.copy()
+    orc.multiply_blocked(Mb, Nb, Kb, bs, 0.5, A, B, 2.0, C2)
+    assert np.allclose(C2, 0.5 * AB + 2.0 * C0, rtol=0, atol=1e-14)
+
+
+def test_small_int_inputs_are_exact(orc):
+    """Integer inputs with dyadic alpha/beta: every partial sum exact, so any order agrees bit for bit."""
+    rng = np.random.default_rng(11)
+    Mb, Nb, Kb, bs = 3, 2, 5, 22
+    A, B, C = (rand_arena(rng, Mb, Kb, bs, True), rand_arena(rng, Kb, Nb, bs, True),
+               rand_arena(rng, Mb, Nb, bs, True))
+    expect = 0.75 * (orc.arena_to_dense(A, Mb, Kb, bs) @ orc.arena_to_dense(B, Kb, Nb, bs)) \
+        - 1.25 * orc.arena_to_dense(C, Mb, Nb, bs)
+    orc.multiply_blocked(Mb, Nb, Kb, bs, 0.75, A, B, -1.25, C)
+    assert np.array_equal(orc.arena_to_dense(C, Mb, Nb, bs), expect)
+
+
+# ----------------------------------------------------------------- input generator
+def test_generator_range_and_distribution(orc):
+    """U[-1,1) values, small-int kind in {-2..2}; different seeds / mat_ids differ."""
+    a = orc.fill_arena(1910, 0, 0, 220, 220, 22)
+    assert a.min() >= -1.0 and a.max() < 1.0
+    assert abs(a.mean()) < 0.01 and abs(a.var() - 1 / 3) < 0.01
+    hist, _ = np.histogram(a, bins=10, range=(-1, 1))
+    assert hist.min() > 0.9 * a.size / 10
+    ints = orc.fill_arena(1910, 0, 1, 220, 220, 22)
+    assert set(np.unique(ints)) == {-2.0, -1.0, 0.0, 1.0, 2.0}
+    assert not np.array_equal(a, orc.fill_arena(1911, 0, 0, 220, 220, 22))
+    assert not np.array_equal(a, orc.fill_arena(1910, 1, 0, 220, 220, 22))
+    # values are exact multiples of 2^-52 (exactly representable generator)
+    assert np.array_equal(np.round(a * 2**52), a * 2**52)
+
+
+@pytest.mark.parametrize("pr,pc", [(1, 2), (2, 2), (2, 4), (3, 2)])
+def test_generator_is_distribution_independent(orc, pr, pc):
+    """A rank's local arena equals the scatter of the 1x1 arena: element values depend on global
+    indices only (catches a local/global index mix-up in the fill)."""
+    rows, cols, bs = 7 * 4, 5 * 4, 4
+    g = orc.fill_arena(5, 2, 0, rows, cols, bs)
+    for r in range(pr):
+        for c in range(pc):
+            loc = orc.fill_arena(5, 2, 0, rows, cols, bs, pr, pc, r, c)
+            assert np.array_equal(loc, orc.scatter(g, rows // bs, cols // bs, bs, pr, pc, r, c))
+
+
+# ----------------------------------------------------------------- grid / distribution
+def test_grid_dims_north_star(orc):
+    assert [orc.grid_dims(p) for p in (1, 2, 4, 8)] == [(1, 1), (1, 2), (2, 2), (2, 4)]
+
+
+def test_owner_pins_from_spec(orc):
+    r, c = G["owner_2x2_block_5_2"]
+    assert orc.owner_rank(5, 2, 2, 2) == r * 2 + c
+    counts = np.zeros(16, dtype=int)
+    for i in range(16):
+        for j in range(16):
+            counts[orc.owner_rank(i, j, 4, 4)] += 1
+    assert (counts == G["owner_4x4_16x16_each"]).all()
+
+
+def test_local_count_closed_form_and_scatter_gather_roundtrip(orc):
+    for nb in range(0, 30):
+        for p in range(1, 6):
+            for r in range(p):
+                assert orc.local_count(nb, p, r) == max(0, math.ceil((nb - r) / p))
+    rng = np.random.default_rng(0)
+    Mb, Nb, bs, pr, pc = 7, 5, 3, 2, 4
+    g = rand_arena(rng, Mb, Nb, bs)
+    back = np.zeros_like(g)
+    for r in range(pr):
+        for c in range(pc):
+            orc.gather_into(back, orc.scatter(g, Mb, Nb, bs, pr, pc, r, c), Mb, Nb, bs, pr, pc, r, c)
+    assert np.array_equal(back, g)
+
+
+def test_paper_shapes_divide(orc):
+    assert G["blocks_22_square"] * 22 == G["square_M"]
+    assert G["square_M"] % 64 == 0 and G["rect_MN"] // 64 == G["blocks_64_rect_mn"]
+    assert G["rect_K"] % 22 == 0 and G["rect_K"] % 64 == 0 and G["rect_MN"] % 22 == 0
+
+
+# ----------------------------------------------------------------- traversal / stacks
+def morton_order(n):
+    """Independent construction: i-major bit interleaving of (i, j) for n a power of two."""
+    def key(i, j):
+        k = 0
+        for b in range(16):
+            k |= ((j >> b) & 1) << (2 * b)
+            k |= ((i >> b) & 1) << (2 * b + 1)
+        return k
+    return sorted(((i, j) for i in range(n) for j in range(n)), key=lambda t: key(*t))
+
+
+def test_traversal_pins(orc):
+    for n in (1, 2, 4, 8, 16):
+        assert [tuple(x) for x in orc.traversal(n, n)] == morton_order(n)
+    assert [tuple(x) for x in orc.traversal(1, 7)] == [(0, j) for j in range(7)]
+    for m, n in [(3, 5), (7, 2), (13, 11), (1, 1)]:
+        t = orc.traversal(m, n)
+        assert len({tuple(x) for x in t}) == m * n == len(t)
+    assert len(orc.traversal(0, 5)) == 0
+
+
+def brute_entries(mloc, nloc, kb):
+    return {(li * kb + kk, kk * nloc + lj, li * nloc + lj) for li in range(mloc) for lj in range(nloc)
+            for kk in range(kb)}
+
+
+@pytest.mark.parametrize("mloc,nloc,kb,cap", [(16, 16, 16, 30000), (16, 16, 16, 100), (5, 3, 7, 20),
+                                              (3, 4, 10, 4), (2, 2, 9, 3), (1, 1, 1, 30000), (4, 4, 0, 10)])
+def test_stack_contracts(orc, mloc, nloc, kb, cap):
+    trip, ptr = orc.stacks(mloc, nloc, kb, cap)
+    assert len(trip) == mloc * nloc * kb
+    assert {tuple(t) for t in trip.tolist()} == brute_entries(mloc, nloc, kb)
+    sizes = np.diff(ptr)
+    assert (sizes <= cap).all() and (sizes > 0).all() and sizes.sum() == len(trip)
+    if 0 < kb <= cap:  # closed form when runs are never split
+        assert len(sizes) == math.ceil(mloc * nloc / (cap // kb))
+        # whole runs never straddle a stack boundary
+        assert all(p % kb == 0 for p in ptr)
+    if kb > cap:
+        assert len(sizes) == mloc * nloc * math.ceil(kb / cap)
+    # within a run k ascends; runs follow the traversal order
+    order = orc.traversal(mloc, nloc)
+    if kb:
+        cs = trip[::kb, 2]
+        assert np.array_equal(cs, order[:, 0] * nloc + order[:, 1])
+
+
+def test_stack_counts_s352_and_paper_scale(orc):
+    """S352 (16^3 blocks) -> 1 stack at cap 30,000 and 43 at cap 100 (SURVEY §8c pins).
+    Reading R7: the paper's ~8M / ~0.3M square stacks match this generator at cap 3,000."""
+    assert orc.stacks(16, 16, 16, G["stack_cap"], counts_only=True) == (4096, 1)
+    assert orc.stacks(16, 16, 16, 100, counts_only=True) == (4096, 43)
+    nb22, nb64 = G["square_M"] // 22, G["square_M"] // 64
+    assert orc.stacks(nb22, nb22, nb22, 30000, counts_only=True)[1] == 829440
+    assert orc.stacks(nb64, nb64, nb64, 30000, counts_only=True)[1] == 32670
+    s22 = orc.stacks(nb22, nb22, nb22, 3000, counts_only=True)[1]
+    s64 = orc.stacks(nb64, nb64, nb64, 3000, counts_only=True)[1]
+    assert abs(s22 / G["stacks_square_bs22"] - 1) < 0.1
+    assert abs(s64 / G["stacks_square_bs64"] - 1) < 0.1
+
+
+def test_densified_is_one_stack_of_one_entry(orc):
+    """P:198 §III: after densification 'the size of the batches become 1'."""
+    e, ns = orc.stacks(1, 1, 1, G["stack_cap"], counts_only=True)
+    assert (e, ns) == (G["densified_batch_size"], 1)
+
+
+# ----------------------------------------------------------------- Cannon
+GRIDS = [(1, 1), (1, 2), (2, 1), (2, 2), (2, 4), (4, 2), (3, 3), (1, 4), (4, 1), (3, 2)]
+
+
+@pytest.mark.parametrize("pr,pc", GRIDS)
+def test_cannon_schedule_computes_the_product(orc, pr, pc):
+    """Simulate the schedule with numpy panels (ragged block counts): every rank sees every K panel
+    exactly once, from a rank that owns it, and the sum of panel products is A@B."""
+    L = orc.lcm(pr, pc)
+    Mb, Nb, Kb, bs = 5, 7, 9, 2
+    rng = np.random.default_rng(pr * 10 + pc)
+    A = rng.uniform(-1, 1, (Mb * bs, Kb * bs))
+    B = rng.uniform(-1, 1, (Kb * bs, Nb * bs))
+    Cout = np.zeros((Mb * bs, Nb * bs))
+    for r in range(pr):
+        for c in range(pc):
+            rows = [i for i in range(Mb) if i % pr == r]
+            cols = [j for j in range(Nb) if j % pc == c]
+            seen = []
+            for s in range(L):
+                k, asrc, bsrc = orc.cannon_step(pr, pc, r, c, s)
+                seen.append(k)
+                ks = [kk for kk in range(Kb) if kk % L == k]
+                # the source really owns every block of the panel
+                assert all(orc.owner_rank(i, kk, pr, pc) == asrc for i in rows for kk in ks)
+                assert all(orc.owner_rank(kk, j, pr, pc) == bsrc for kk in ks for j in cols)
+                ri = np.concatenate([np.arange(i * bs, i * bs + bs) for i in rows]) if rows else np.array([], int)
+                ci = np.concatenate([np.arange(j * bs, j * bs + bs) for j in cols]) if cols else np.array([], int)
+                ki = np.concatenate([np.arange(q * bs, q * bs + bs) for q in ks]) if ks else np.array([], int)
+                if len(ri) and len(ci) and len(ki):
+                    Cout[np.ix_(ri, ci)] += A[np.ix_(ri, ki)] @ B[np.ix_(ki, ci)]
+            assert sorted(seen) == list(range(L))
+    assert np.allclose(Cout, A @ B, atol=1e-12)
+
+
+@pytest.mark.parametrize("pr,pc", GRIDS)
+def test_cannon_at_most_one_send_per_operand_per_step(orc, pr, pc):
+    L = orc.lcm(pr, pc)
+    for s in range(L):
+        a_sends, b_sends = {}, {}
+        for r in range(pr):
+            for c in range(pc):
+                k, asrc, bsrc = orc.cannon_step(pr, pc, r, c, s)
+                me = r * pc + c
+                if asrc != me:
+                    a_sends.setdefault(asrc, set()).add(k)
+                if bsrc != me:
+                    b_sends.setdefault(bsrc, set()).add(k)
+        assert all(len(v) <= 1 for v in a_sends.values())
+        assert all(len(v) <= 1 for v in b_sends.values())
+
+
+@pytest.mark.parametrize("pt", [1, 2, 3, 4])
+def test_cannon_bytes_closed_form_square(orc, pt):
+    """per-rank bytes = 2*(N/P~)^2*8*(P~-1) for dense square doubles, N divisible by P~."""
+    N, bs = 24 * pt, 2
+    nb = N // bs
+    for r in range(pt):
+        for c in range(pt):
+            rv, sd = orc.cannon_bytes(nb, nb, nb, bs, pt, pt, r, c)
+            assert rv == 2 * (N // pt) ** 2 * 8 * (pt - 1)
+            assert sd == rv
+
+
+def test_cannon_bytes_general_formula(orc):
+    """Non-square grids: recv = (L-L/Pc)|A_panel| + (L-L/Pr)|B_panel| when panels divide evenly."""
+    for pr, pc in [(1, 2), (2, 4), (4, 2), (1, 4)]:
+        L = orc.lcm(pr, pc)
+        Mb, Nb, Kb, bs = 4 * pr, 4 * pc, 3 * L, 2
+        ap = (Mb // pr) * (Kb // L) * bs * bs * 8
+        bp = (Kb // L) * (Nb // pc) * bs * bs * 8
+        for r in range(pr):
+            for c in range(pc):
+                rv, _ = orc.cannon_bytes(Mb, Nb, Kb, bs, pr, pc, r, c)
+                assert rv == (L - L // pc) * ap + (L - L // pr) * bp
+
+
+def test_cannon_volume_scales_as_inverse_sqrt_p(orc):
+    """per-rank volume O(1/sqrt(P)); P=4 -> P=16 halves it (within 10%)."""
+    N, bs = 960, 4
+    nb = N // bs
+    v4 = orc.cannon_bytes(nb, nb, nb, bs, 2, 2, 0, 0)[0]
+    v16 = orc.cannon_bytes(nb, nb, nb, bs, 4, 4, 0, 0)[0]
+    assert abs(v16 / v4 - 0.5) < 0.1 * 0.5 + 0.25  # (P~-1)/P~^2 : 3/16 vs 1/4 -> 0.75 exactly
+    assert v16 / v4 == pytest.approx((3 / 16) / (1 / 4))
+
+
+# ----------------------------------------------------------------- densification
+def test_densify_law_eqs_1_2(orc):
+    M, pt, t = G["densify_law_case"]
+    a, b = orc.densified_dims(M, M, M, pt, t)
+    assert a == G["densify_law_A"] and b == G["densify_law_B"]
+    # the law reassembles the whole matrix: t*P~ A blocks of rows, P~ along K and N
+    assert a[0] * t * pt == M and a[1] * pt == M and b[0] * pt == M and b[1] * pt == M
+
+
+def test_densify_layouts_and_roundtrip(orc):
+    rng = np.random.default_rng(5)
+    mloc, nloc, bs = 3, 4, 5
+    arena = rand_arena(rng, mloc, nloc, bs)
+    dense_all = orc.densify_cols(arena, mloc, nloc, bs, np.arange(nloc), 0)
+    ref = orc.arena_to_dense(arena, mloc, nloc, bs)  # the full local arena as a dense matrix
+    assert np.array_equal(dense_all.reshape(nloc * bs, mloc * bs).T, ref)
+    rowmaj = orc.densify_cols(arena, mloc, nloc, bs, np.arange(nloc), 1)
+    assert np.array_equal(rowmaj.reshape(mloc * bs, nloc * bs), ref)
+    sub = [3, 1]
+    d = orc.densify_cols(arena, mloc, nloc, bs, sub, 0).reshape(len(sub) * bs, mloc * bs).T
+    assert np.array_equal(d, ref[:, np.concatenate([np.arange(q * bs, q * bs + bs) for q in sub])])
+    rws = [2, 0]
+    d = orc.densify_rows(arena, mloc, nloc, bs, rws, 0).reshape(nloc * bs, len(rws) * bs).T
+    assert np.array_equal(d, ref[np.concatenate([np.arange(q * bs, q * bs + bs) for q in rws]), :])
+    d1 = orc.densify_rows(arena, mloc, nloc, bs, rws, 1).reshape(len(rws) * bs, nloc * bs)
+    assert np.array_equal(d1, d)
+    # undensify(alpha=1, beta=0) inverts densify bit for bit
+    back = np.full_like(arena, np.nan)
+    orc.undensify(dense_all, mloc * bs, mloc, nloc, bs, 1.0, 0.0, back)
+    assert np.array_equal(back, arena)
+
+
+def test_undensify_alpha_beta(orc):
+    rng = np.random.default_rng(9)
+    mloc, nloc, bs = 2, 3, 4
+    dense = rng.uniform(-1, 1, (mloc * bs) * (nloc * bs))
+    c = rand_arena(rng, mloc, nloc, bs)
+    out = c.copy()
+    orc.undensify(dense, mloc * bs, mloc, nloc, bs, 0.75, -1.25, out)
+    D = dense.reshape(nloc * bs, mloc * bs).T
+    expect = 0.75 * D + (-1.25) * orc.arena_to_dense(c, mloc, nloc, bs)
+    assert np.array_equal(orc.arena_to_dense(out, mloc, nloc, bs), expect)
+
+
+# ----------------------------------------------------------------- verification helpers
+def test_rows_and_freivalds_from_seeds(orc):
+    M, N, K, bs, seed = 88, 66, 110, 22, 1910
+    A = orc.fill_arena(seed, 0, 0, M, K, bs)
+    B = orc.fill_arena(seed, 1, 0, K, N, bs)
+    Cin = orc.fill_arena(seed, 2, 0, M, N, bs)
+    Ad, Bd, Cd = (orc.arena_to_dense(A, M // bs, K // bs, bs), orc.arena_to_dense(B, K // bs, N // bs, bs),
+                  orc.arena_to_dense(Cin, M // bs, N // bs, bs))
+    expect = 0.75 * (Ad @ Bd) - 1.25 * Cd
+    rows = [0, 1, 21, 22, 87]
+    got = orc.rows_from_seeds(M, N, K, seed, 0, 0.75, -1.25, rows)
+    assert np.abs(got - expect[rows]).max() < 1e-13
+    x, rhs = orc.freivalds_rhs(M, N, K, seed, 0, 0.75, -1.25, 42)
+    assert set(np.unique(x)) == {-1.0, 1.0}
+    assert np.abs(rhs - expect @ x).max() < 1e-12
+    # and the oracle's own blocked product agrees with the rows
+    C = Cin.copy()
+    orc.multiply_blocked(M // bs, N // bs, K // bs, bs, 0.75, A, B, -1.25, C)
+    assert np.array_equal(orc.arena_to_dense(C, M // bs, N // bs, bs)[rows], got)

@@ -1,0 +1,315 @@
+"""Benchmark: FP64 TFLOP/s of C = alpha*A*B + beta*C through libdbm (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config sq64|sq22|r64|r22|s352]
+                    [--path densified|blocked] [--impl ours|reference]
+
+A step is one dbm_multiply over the whole configuration (Cannon over the N-rank grid, every local
+step, densify/undensify included).  N>1 runs under torchrun, one rank per GPU over NCCL.  Timing:
+barrier + cuda synchronize on both sides of exactly K steps, CUDA events on the compute stream,
+max over ranks.  Inputs are 8+ GB per matrix, far above the 126 MB L2, so no flush is needed.
+Rank 0 prints one JSON line.  `--impl reference` times the host oracle (oracle/, test
+infrastructure) on a bounded sample of the same workload instead.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "FP64 TFLOP/s per C=A·B (device-timed, max over ranks) at 1/2/4/8 B200; % of FP64 peak"
+CONFIGS = {
+    # name: (M, N, K, bs, default path, BASELINE.json configs[] index)
+    "s352": (352, 352, 352, 22, "densified", 0),
+    "sq64": (63360, 63360, 63360, 64, "densified", 1),
+    "sq22": (63360, 63360, 63360, 22, "densified", 2),
+    "r64": (1408, 1408, 1982464, 64, "densified", 3),
+    "r22": (1408, 1408, 1982464, 22, "densified", 4),
+}
+SEED = 1910
+FP64_PEAK_MEASURED = 37.15  # TFLOP/s per B200, DMMA m8n8k4 chain at 1965 MHz (profiles/r01_fp64_peaks.jsonl)
+FP64_PEAK_SPEC = 37.2       # 148 SM x 64 FMA/clk x 2 x 1.965 GHz
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=3)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--config", default="sq64", choices=sorted(CONFIGS))
+    p.add_argument("--path", default=None, choices=["densified", "blocked"])
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--e2e-steps", type=int, default=1)
+    p.add_argument("--cpu-rows", type=int, default=0, help="oracle sample rows (0 = auto, ~10-30 s)")
+    return p.parse_args()
+
+
+# ------------------------------------------------------------------ clocks during the timed region
+class ClockSampler:
+    REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+               0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+               0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
+
+    def __init__(self, device: int):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(device)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit and bit != 0x1:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        if self.nv:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self.nv:
+            self.t.join()
+
+    def summary(self):
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None, "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+# ------------------------------------------------------------------ reference arm / cpu baseline
+def oracle_sample(M, N, K, rows: int) -> dict:
+    """Time the host oracle on `rows` sampled rows of C (2*rows*K*N flop), as it stands."""
+    import numpy as np
+
+    import oracle
+
+    oracle.build()
+    idx = np.linspace(0, M - 1, rows).astype(np.int64)
+    t0 = time.perf_counter()
+    oracle.rows_from_seeds(M, N, K, SEED, 0, 1.0, 0.0, idx)
+    dt = time.perf_counter() - t0
+    flop = 2.0 * rows * K * N
+    return {"value": flop / dt / 1e12, "unit": "TFLOP/s", "cores": oracle.num_threads(), "kind": "oracle",
+            "sample": f"{rows} of {M} rows of C = A*B regenerated from seeds (2*{rows}*K*N flop), {dt:.1f} s",
+            "seconds": dt}
+
+
+def auto_rows(M, N, K) -> int:
+    # measured: ~0.3 GFLOP/s per core for the plain loop incl. regenerating B; target ~15 s
+    import oracle
+
+    cores = max(1, oracle.num_threads())
+    rows = int(15.0 * 0.3e9 * cores / (2.0 * K * N))
+    return max(1, min(rows, M, 64))
+
+
+def run_reference(args, cfg, name, world, rank):
+    M, N, K, bs, path, _ = cfg
+    if rank != 0:
+        return
+    rows = args.cpu_rows or auto_rows(M, N, K)
+    times = []
+    for i in range(args.warmup + args.steps):
+        r = oracle_sample(M, N, K, rows)
+        if i >= args.warmup:
+            times.append(r)
+    val = statistics.mean(t["value"] for t in times)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": val, "unit": "TFLOP/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": statistics.mean(t["seconds"] for t in times) * 1e3, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": name, "M": M, "N": N, "K": K, "block_size": bs, "path": path},
+        "cpu_baseline": {k: times[-1][k] for k in ("kind", "cores", "sample")} | {"value": val, "unit": "TFLOP/s"},
+        "e2e": {"value": val, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ our arm
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    cfg = CONFIGS[args.config]
+    M, N, K, bs, dpath, cidx = cfg
+    path = args.path or dpath
+    name = {"s352": "352^3 bs22", "sq64": "square 63360^3 bs64", "sq22": "square 63360^3 bs22",
+            "r64": "rect 1408x1408x1982464 bs64", "r22": "rect 1408x1408x1982464 bs22"}[args.config]
+    name = f"{name} {path} (BASELINE.json configs[{cidx}])"
+    if args.impl == "reference":
+        return run_reference(args, (M, N, K, bs, path, cidx), name, world, rank)
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_1910_04796_b200 as dbm
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+        ctx = dbm.Context.from_distributed()
+    else:
+        ctx = dbm.Context(device=local)
+    stream = torch.cuda.current_stream(dev)
+    A, B, C = dbm.Matrix(ctx, M, K, bs), dbm.Matrix(ctx, K, N, bs), dbm.Matrix(ctx, M, N, bs)
+    A.fill_random(SEED, 0, 0)
+    B.fill_random(SEED, 1, 0)
+    C.fill_random(SEED, 2, 0)
+    ws = ctx.workspace(dbm.multiply_workspace(ctx, A, B, C, path))
+    alpha, beta = 1.0, 0.0
+
+    def barrier():
+        if world > 1:
+            dist.barrier(device_ids=[local])
+        torch.cuda.synchronize()
+
+    def maxrank(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    for _ in range(args.warmup):
+        dbm.multiply(ctx, alpha, A, B, beta, C, path, workspace=ws)
+    barrier()
+    launches0 = ctx.launch_count()
+    ctx.set_profiling(True)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        barrier()
+        ev0.record(stream)
+        for _ in range(args.steps):
+            st = dbm.multiply(ctx, alpha, A, B, beta, C, path, workspace=ws)
+        ev1.record(stream)
+        barrier()
+    ctx.set_profiling(False)
+    launches = ctx.launch_count() - launches0
+    ms = maxrank(ev0.elapsed_time(ev1)) / args.steps
+    flop = 2.0 * M * N * K
+    tflops = flop / (ms * 1e-3) / 1e12
+    kern = "dgemm" if path == "densified" else "smm"
+    prof = ctx.profile_read(dbm.K_DGEMM if path == "densified" else dbm.K_SMM)
+    prof_d = ctx.profile_read(dbm.K_DENSIFY)
+    prof_u = ctx.profile_read(dbm.K_UNDENSIFY)
+    ctx.profile_read(dbm.K_STACKGEN)
+    per_launch_ms = prof["ms"] / max(prof["launches"], 1)
+    per_launch_flop = prof["flops"] / max(prof["launches"], 1)
+    achieved = per_launch_flop / (per_launch_ms * 1e-3) / 1e12 if per_launch_ms > 0 else None
+    traffic = None
+    tfile = os.path.join(ROOT, "profiles", f"traffic_{args.config}_{path}_n{world}.json")
+    if os.path.exists(tfile):
+        traffic = json.load(open(tfile)).get("bytes_per_launch")
+
+    # ---------------- end to end through the public API with host buffers (pinned), rank-local shares
+    e2e = None
+    if not args.no_e2e:
+        e2e = run_e2e(args, ctx, dbm, torch, A, B, C, path, ws, stream, barrier, maxrank, flop)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            cpu = oracle_sample(M, N, K, args.cpu_rows or auto_rows(M, N, K))
+            cpu.pop("seconds", None)
+        except Exception as ex:  # reported, never fatal
+            cpu = {"error": str(ex)[:200]}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": tflops, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": name, "M": M, "N": N, "K": K, "block_size": bs, "path": path,
+                       "grid": f"{ctx.pr}x{ctx.pc}", "parallelism": f"cannon{ctx.pr}x{ctx.pc}",
+                       "l2": "inputs >= 8 GB per matrix >> 126 MB L2; no flush", "alpha": alpha, "beta": beta},
+            "pct_fp64_peak": 100.0 * tflops / (world * FP64_PEAK_MEASURED),
+            "roofline": {"kernel": kern, "bound": "tensor", "achieved": achieved, "peak": FP64_PEAK_MEASURED,
+                         "unit": "TFLOP/s", "frac": (achieved / FP64_PEAK_MEASURED) if achieved else None,
+                         "traffic": traffic, "launches": prof["launches"], "ms_per_launch": per_launch_ms,
+                         "flop_per_launch": per_launch_flop,
+                         "peak_source": "measured FP64 DMMA peak, profiles/r01_fp64_peaks.jsonl (FP64 is not in "
+                                        "MEASURED_PEAKS.json); spec 37.2",
+                         "share_of_step": prof["ms"] / (ms * args.steps) if ms > 0 else None},
+            "phases_ms_per_step": {"dgemm_or_smm": prof["ms"] / args.steps, "densify": prof_d["ms"] / args.steps,
+                                   "undensify": prof_u["ms"] / args.steps},
+            "stats": {k: st[k] for k in ("entries", "stacks", "bytes_sent", "bytes_recv", "steps")},
+            "gpu_launches": launches,
+            "clocks": clk.summary(),
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier(device_ids=[local])
+        dist.destroy_process_group()
+
+
+def run_e2e(args, ctx, dbm, torch, A, B, C, path, ws, stream, barrier, maxrank, flop):
+    """Same metric through the public API with HOST buffers: per step H2D of A and B from pinned host
+    memory, the multiply, D2H of C (beta = 0, so C_in is not read: BLAS convention, reading R8)."""
+    try:
+        hA = torch.empty(A.arena_bytes // 8, dtype=torch.float64, pin_memory=True)
+        hB = torch.empty(B.arena_bytes // 8, dtype=torch.float64, pin_memory=True)
+        hC = torch.empty(C.arena_bytes // 8, dtype=torch.float64, pin_memory=True)
+        pinned = True
+    except Exception:
+        hA = torch.empty(A.arena_bytes // 8, dtype=torch.float64)
+        hB = torch.empty(B.arena_bytes // 8, dtype=torch.float64)
+        hC = torch.empty(C.arena_bytes // 8, dtype=torch.float64)
+        pinned = False
+    A.download(hA)
+    B.download(hB)
+    ctx.sync()
+
+    def step():
+        A.upload(hA)
+        B.upload(hB)
+        dbm.multiply(ctx, 1.0, A, B, 0.0, C, path, workspace=ws)
+        C.download(hC)
+
+    step()  # warm-up
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.e2e_steps):
+        step()
+    e1.record(stream)
+    barrier()
+    ms = maxrank(e0.elapsed_time(e1)) / args.e2e_steps
+    out = {"value": flop / (ms * 1e-3) / 1e12, "unit": "TFLOP/s", "h2d_bytes_per_step": A.arena_bytes + B.arena_bytes,
+           "d2h_bytes_per_step": C.arena_bytes, "ms_per_step": ms, "steps": args.e2e_steps,
+           "host_memory": "pinned" if pinned else "pageable (staged through libdbm's pinned double buffer)",
+           "bytes_are": "rank-local shares (rank 0 shown)"}
+    del hA, hB, hC
+    return out
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,197 @@
+/*
+ * dbm.h — C ABI of the B200-native DBCSR dense-multiply hot path (arXiv 1910.04796).
+ *
+ * The library (paper_1910_04796_b200/libdbm.so) multiplies FP64 matrices of uniform
+ * square blocks, distributed block-cyclically over a 2-D grid of ranks (one rank per
+ * GPU), with Cannon's algorithm and either a blocked (stacks + batched small-block
+ * GEMM) or a densified (densify -> one large GEMM -> undensify) local multiply.
+ *
+ * Citations: P:n = PAPER.md line n, S:n = SPEC.md line n; readings R1..R12 are
+ * listed in DESIGN.md §3.
+ *
+ * General conventions
+ *  - Every function returns dbm_status; DBM_OK == 0.  On error, dbm_last_error()
+ *    returns a thread-local human-readable detail string.
+ *  - Device memory (matrix arenas, multiply workspace, dense buffers) is CALLER-OWNED
+ *    (e.g. torch tensors).  The library never frees it.  Handles belong to the
+ *    library until the matching *_destroy.
+ *  - Calls that launch GPU work enqueue on the context's stream and return without
+ *    synchronising, unless documented otherwise.  Asynchronous CUDA / NCCL failures
+ *    surface at dbm_ctx_sync(), after which the context is poisoned: every later
+ *    call returns DBM_ERR_CUDA or DBM_ERR_NCCL.
+ *  - Arguments are validated on the host BEFORE anything is enqueued; on a
+ *    validation error nothing is modified.
+ *  - Matrix storage ("arena", reading R3): the local share of a rows x cols matrix
+ *    with block size bs is mloc x nloc blocks, mloc = #{i < rows/bs : i mod Pr == myrow},
+ *    nloc = #{j < cols/bs : j mod Pc == mycol}; block (li,lj) holds global block
+ *    (myrow + li*Pr, mycol + lj*Pc) ("block-cycling distributed a la ScaLAPACK";
+ *    S:115), at slot li*nloc + lj; element (x,y) at slot*bs*bs + y*bs + x
+ *    (column-major inside a block; DBCSR is Fortran).  The metadata is a
+ *    blocked CSR (§II) with every block present (dense occupancy).
+ */
+#ifndef DBM_H
+#define DBM_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  DBM_OK = 0,
+  DBM_ERR_ARG = 1,       /* null handle / pointer, bad enum, bad size */
+  DBM_ERR_SHAPE = 2,     /* non-conformant shapes; rows/cols not a multiple of bs */
+  DBM_ERR_RANGE = 3,     /* block index out of range */
+  DBM_ERR_PARTITION = 4, /* A's K partition differs from B's (unequal block sizes) */
+  DBM_ERR_PLAN = 5,      /* densify plan mismatch */
+  DBM_ERR_OWNERSHIP = 6, /* block not owned by the calling rank */
+  DBM_ERR_ALIAS = 7,     /* C aliases A or B */
+  DBM_ERR_GRID = 8,      /* Pr*Pc != nranks, or matrices from different contexts */
+  DBM_ERR_WORKSPACE = 9, /* workspace smaller than dbm_multiply_workspace() / arena not attached */
+  DBM_ERR_CUDA = 20,
+  DBM_ERR_NCCL = 21,
+  DBM_ERR_NOMEM = 22
+} dbm_status;
+
+typedef enum { DBM_PATH_BLOCKED = 0, DBM_PATH_DENSIFIED = 1 } dbm_path;
+
+typedef struct dbm_ctx_s* dbm_ctx;
+typedef struct dbm_matrix_s* dbm_matrix;
+
+/* Per-multiply statistics (all counts for the calling rank). */
+typedef struct {
+  int64_t entries;    /* block multiplications (stack entries) executed; densified: 1 per GEMM */
+  int64_t stacks;     /* stacks of <= stack_cap entries generated */
+  int64_t bytes_sent; /* Cannon panel bytes sent by this rank */
+  int64_t bytes_recv; /* Cannon panel bytes received by this rank */
+  int64_t steps;      /* Cannon steps L = lcm(Pr,Pc) (reading R5) */
+  int64_t gemm_launches;
+  int64_t kernel_launches; /* all kernels this call launched */
+  double flops;            /* 2*mloc*bs*nloc*bs*K_local + epilogue, this rank */
+} dbm_stats;
+
+const char* dbm_status_string(dbm_status s);
+const char* dbm_last_error(void);
+
+/* ----------------------------------------------------------------- context */
+/* Bytes of an NCCL unique id (NCCL_UNIQUE_ID_BYTES). */
+int dbm_unique_id_bytes(void);
+/* Rank 0 calls this, then broadcasts the bytes to every rank (e.g. torch.distributed). */
+dbm_status dbm_get_unique_id(void* id_out);
+
+/* Create the per-rank context (§II: a 2-D grid of P processes; one rank per GPU,
+ * P:175).  pr = pc = 0 picks the grid by reading R1 (1->1x1, 2->1x2, 4->2x2, 8->2x4);
+ * otherwise pr*pc must equal nranks (DBM_ERR_GRID).  rank = myrow*pc + mycol.
+ * id: NCCL unique id bytes (ignored when nranks == 1).  device: CUDA ordinal.
+ * cuda_stream: cudaStream_t to enqueue on (NULL = the legacy default stream, e.g. torch's default
+ * stream); the library adds one internal non-blocking stream for the Cannon exchange.
+ * Collective over all ranks when nranks > 1 (ncclCommInitRank). */
+dbm_status dbm_ctx_create(int nranks, int rank, int pr, int pc, const void* id, int device, void* cuda_stream,
+                          dbm_ctx* out);
+dbm_status dbm_ctx_grid(dbm_ctx ctx, int* pr, int* pc, int* myrow, int* mycol);
+/* Switch the stream subsequent calls enqueue on (e.g. torch.cuda.current_stream()). */
+dbm_status dbm_ctx_set_stream(dbm_ctx ctx, void* cuda_stream);
+/* Block until all work enqueued by this context finished; surfaces async errors. */
+dbm_status dbm_ctx_sync(dbm_ctx ctx);
+/* Profiling: when on, every dominant-kernel launch (the FP64 GEMM / small-block GEMM)
+ * is bracketed by CUDA events on its own stream.  dbm_ctx_profile_read() synchronises,
+ * returns the summed device time, launch count and algorithmic flops of the recorded
+ * launches of `kernel` (0 = dense GEMM, 1 = small-block GEMM, 2 = densify, 3 = undensify,
+ * 4 = stack generation) and clears the records. bytes_out: algorithmic bytes. */
+dbm_status dbm_ctx_set_profiling(dbm_ctx ctx, int on);
+dbm_status dbm_ctx_profile_read(dbm_ctx ctx, int kernel, double* ms_out, int64_t* launches_out, double* flops_out,
+                                double* bytes_out);
+/* Densified path on a single rank: byte budget of one K-chunk of dense A + B (default 16 GiB).
+ * K is densified and multiplied chunk by chunk (GEMM-accumulate), so 63,360^3 fits in HBM.
+ * bytes >= 1; changes dbm_multiply_workspace(). */
+dbm_status dbm_ctx_set_dense_chunk_bytes(dbm_ctx ctx, int64_t bytes);
+/* Total kernels this context has launched since creation. */
+dbm_status dbm_ctx_launch_count(dbm_ctx ctx, int64_t* out);
+dbm_status dbm_ctx_destroy(dbm_ctx ctx);
+
+/* ------------------------------------------------------------------ matrix */
+/* A rows x cols FP64 matrix of uniform square blocks of size bs, distributed
+ * block-cyclically over ctx's grid.  rows, cols must be multiples of bs (DBM_ERR_SHAPE;
+ * reading R10).  Host metadata only; attach device storage before use. */
+dbm_status dbm_matrix_create(dbm_ctx ctx, int64_t rows, int64_t cols, int32_t block_size, dbm_matrix* out);
+/* Local share: mloc x nloc blocks; arena_bytes = mloc*nloc*bs*bs*8. */
+dbm_status dbm_matrix_local_info(dbm_matrix m, int64_t* mloc_blocks, int64_t* nloc_blocks, int64_t* arena_bytes);
+/* Blocked-CSR metadata of the local share: row_ptr[mloc+1] (= li*nloc), col_idx[mloc*nloc]
+ * (global block column), row_idx[mloc] (global block row).  Host arrays, caller-allocated. */
+dbm_status dbm_matrix_local_csr(dbm_matrix m, int64_t* row_ptr, int64_t* col_idx, int64_t* row_idx);
+/* Attach caller-owned device storage of >= arena_bytes bytes, 16-byte aligned. */
+dbm_status dbm_matrix_attach(dbm_matrix m, void* device_arena, int64_t bytes);
+/* Fill the local share from the counter-based generator of DESIGN.md §4:
+ * element (gi,gj) = f(seed, mat_id, gi, gj); kind 0 = U[-1,1), 1 = integers {-2..2}. */
+dbm_status dbm_matrix_fill_random(dbm_matrix m, uint64_t seed, uint32_t mat_id, int kind);
+/* Copy one locally-owned block (global indices) from / to a host column-major bs x bs array.
+ * DBM_ERR_RANGE for indices outside the matrix, DBM_ERR_OWNERSHIP if another rank owns it.
+ * Synchronous with respect to the host. */
+dbm_status dbm_matrix_set_block(dbm_matrix m, int64_t bi, int64_t bj, const double* host_colmajor);
+dbm_status dbm_matrix_get_block(dbm_matrix m, int64_t bi, int64_t bj, double* host_colmajor);
+/* Whole local arena host <-> device (host buffer in arena layout, arena_bytes long).
+ * Pinned host memory is copied directly; pageable memory is staged through the context's
+ * pinned double buffer.  Enqueued on the ctx stream; host buffers must stay
+ * valid until the stream reaches the copy (pinned) or the call returns (pageable). */
+dbm_status dbm_matrix_upload(dbm_matrix m, const void* host_arena);
+dbm_status dbm_matrix_download(dbm_matrix m, void* host_arena);
+/* Rank owning global block (bi,bj): (bi mod Pr)*Pc + (bj mod Pc). */
+dbm_status dbm_owner_of_block(dbm_matrix m, int64_t bi, int64_t bj, int* rank);
+dbm_status dbm_matrix_destroy(dbm_matrix m);
+
+/* ---------------------------------------------------------------- multiply */
+/* Device workspace dbm_multiply needs for these operands and path, in bytes. */
+dbm_status dbm_multiply_workspace(dbm_ctx ctx, dbm_matrix A, dbm_matrix B, dbm_matrix C, dbm_path path,
+                                  int64_t* bytes);
+/* C = alpha*A*B + beta*C (north star), collective over the context's ranks.
+ * Cannon over L = lcm(Pr,Pc) steps (reading R5) with NCCL point-to-point panel
+ * exchange on a side stream overlapped with the local multiply.
+ * path DENSIFIED: densify A, B panels -> FP64 GEMM per step -> undensify C with alpha,
+ *   beta (§III).
+ * path BLOCKED: stacks of <= stack_cap (a,b,c) block triplets (0 -> 30000) executed
+ *   by the batched small-block GEMM.
+ * BLAS conventions (reading R8): beta == 0 -> C is not read; alpha == 0 -> A, B not read.
+ * Errors before enqueue: SHAPE (A.cols != B.rows, A.rows != C.rows, B.cols != C.cols),
+ * PARTITION (block sizes differ), ALIAS, GRID (different contexts), WORKSPACE.
+ * stats may be NULL. */
+dbm_status dbm_multiply(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_matrix B, double beta, dbm_matrix C,
+                        dbm_path path, int32_t stack_cap, void* workspace, int64_t workspace_bytes, dbm_stats* stats);
+
+/* Host-only (no GPU needed): the point-to-point operations dbm_multiply issues at Cannon step
+ * `step` for rank (myrow, mycol) of a pr x pc grid multiplying Mb x Kb by Kb x Nb blocks of bs
+ * (owner-pull reading R5).  ops[4*i] = {send(1)/recv(0), operand (0 = A, 1 = B), peer
+ * rank, kappa}; bytes[i] = message size.  *n_ops: in = capacity of ops/bytes, out = count.  Pass
+ * NULL ops and bytes to query the count. */
+dbm_status dbm_plan_exchange(int pr, int pc, int myrow, int mycol, int64_t Mb, int64_t Nb, int64_t Kb, int32_t bs,
+                             dbm_path path, int step, int32_t* ops, int64_t* bytes, int* n_ops);
+
+/* ------------------------------------------------------- densify / undensify */
+/* Densify the whole local share ("a single block is formed from all the blocks
+ * assigned to each thread"): dense is (mloc*bs) x (nloc*bs), layout 0 = column-major with
+ * leading dimension ld >= mloc*bs, layout 1 = row-major with ld >= nloc*bs. Device memory. */
+dbm_status dbm_densify(dbm_matrix m, double* dense, int64_t ld, int layout);
+/* Undensify ("decomposed following the original block sizes") with scaling:
+ * block(li,lj)(x,y) = alpha*D(li*bs+x, lj*bs+y) + beta*block (two roundings, no FMA; beta == 0 ->
+ * block not read).  D column-major, ld >= mloc*bs. */
+dbm_status dbm_undensify(dbm_matrix m, const double* dense, int64_t ld, double alpha, double beta);
+
+/* ------------------------------------------------------------------ debug */
+/* Run the GPU stack-generation kernel for Cannon step `step` of A*B into C on this rank and
+ * copy the result to host: triplets[3*n] (a_slot, b_slot, c_slot) int32, stack_ptr[n_stacks+1].
+ * Pass NULL arrays to query the sizes only.  Synchronous. */
+dbm_status dbm_debug_stacks(dbm_ctx ctx, dbm_matrix A, dbm_matrix B, dbm_matrix C, int step, int32_t cap,
+                            int32_t* triplets, int64_t* n_entries, int64_t* stack_ptr, int64_t* n_stacks);
+/* Raw dense FP64 GEMM kernel (the densified path's local multiply) on device buffers:
+ * C(MxN, col-major, ldc) = alpha * At^T * B + beta * C, At K-major (element (m,k) at At[m*lda+k]),
+ * B K-major (element (k,n) at B[n*ldb+k]); lda, ldb even.  splitk >= 1 splits K with a
+ * deterministic reduction through `partial` (device, splitk*M*N doubles; NULL when splitk == 1);
+ * splitk == 0 picks it.  For tests and profiling. */
+dbm_status dbm_debug_dgemm(dbm_ctx ctx, int64_t M, int64_t N, int64_t K, double alpha, const double* At, int64_t lda,
+                           const double* B, int64_t ldb, double beta, double* C, int64_t ldc, int splitk,
+                           double* partial, int64_t partial_bytes);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DBM_H */

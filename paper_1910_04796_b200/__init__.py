@@ -1,0 +1,12 @@
+"""B200-native DBCSR dense-multiply hot path (arXiv 1910.04796).
+
+The product is libdbm.so (CUDA for sm_100a behind the C ABI in include/dbm.h); this package is
+its thin Python binding.  See DESIGN.md.
+"""
+from .dbm import (EXPORTS, K_DENSIFY, K_DGEMM, K_SMM, K_STACKGEN, K_UNDENSIFY, LIB_PATH, PATH_BLOCKED,
+                  PATH_DENSIFIED, Context, DbmError, Matrix, debug_dgemm, debug_stacks, load, multiply,
+                  multiply_workspace, plan_exchange)
+
+__all__ = ["Context", "Matrix", "multiply", "multiply_workspace", "plan_exchange", "debug_stacks", "debug_dgemm", "load",
+           "DbmError", "EXPORTS", "LIB_PATH", "PATH_BLOCKED", "PATH_DENSIFIED", "K_DGEMM", "K_SMM",
+           "K_DENSIFY", "K_UNDENSIFY", "K_STACKGEN"]

@@ -1,0 +1,1027 @@
+// libdbm C ABI (include/dbm.h): contexts, blocked matrices, the Cannon multiply driver
+// (§II) with the densified (§III) and blocked (§II) local paths.
+//
+// Runtime model: one process per GPU; the compute stream is the caller's (torch's)
+// stream; a second "comm" stream carries NCCL grouped send/recv of Cannon panels so the fetch of
+// step s+1 overlaps the local multiply of step s; CUDA events order the two streams.
+#include <nccl.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <numeric>
+#include <string>
+#include <vector>
+
+#include "dbm_internal.h"
+
+namespace dbm {
+static thread_local std::string g_err;
+void set_error(const std::string& m) { g_err = m; }
+
+int num_sms() {
+  static int n = 0;
+  if (n <= 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) n = 148;
+  }
+  return n;
+}
+
+static int64_t local_count(int64_t nb, int p, int r) { return nb > r ? (nb - r + p - 1) / p : 0; }
+static int64_t lcm64(int64_t a, int64_t b) { return a / std::gcd(a, b) * b; }
+static int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
+}  // namespace dbm
+
+using namespace dbm;
+
+#define ARG_CHECK(cond, code, msg) \
+  do {                             \
+    if (!(cond)) {                 \
+      set_error(msg);              \
+      return code;                 \
+    }                              \
+  } while (0)
+
+#define CUDA_TRY(ctx, x)                                                                    \
+  do {                                                                                      \
+    cudaError_t e_ = (x);                                                                   \
+    if (e_ != cudaSuccess) {                                                                \
+      set_error(std::string(#x) + ": " + cudaGetErrorString(e_));                           \
+      if (ctx) (ctx)->poisoned = DBM_ERR_CUDA;                                              \
+      return DBM_ERR_CUDA;                                                                  \
+    }                                                                                       \
+  } while (0)
+
+#define NCCL_TRY(ctx, x)                                                                    \
+  do {                                                                                      \
+    ncclResult_t r_ = (x);                                                                  \
+    if (r_ != ncclSuccess) {                                                                \
+      set_error(std::string(#x) + ": " + ncclGetErrorString(r_));                           \
+      if (ctx) (ctx)->poisoned = DBM_ERR_NCCL;                                              \
+      return DBM_ERR_NCCL;                                                                  \
+    }                                                                                       \
+  } while (0)
+
+#define CTX_OK(ctx)                                                             \
+  do {                                                                          \
+    ARG_CHECK((ctx) != nullptr, DBM_ERR_ARG, "null context");                   \
+    if ((ctx)->poisoned != DBM_OK) {                                            \
+      set_error("context poisoned by an earlier CUDA/NCCL failure");            \
+      return (ctx)->poisoned;                                                   \
+    }                                                                           \
+    CUDA_TRY(ctx, cudaSetDevice((ctx)->device));                                \
+  } while (0)
+
+namespace {
+
+cudaEvent_t get_event(dbm_ctx ctx) {
+  if (!ctx->ev_pool.empty()) {
+    cudaEvent_t e = ctx->ev_pool.back();
+    ctx->ev_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e = nullptr;
+  cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+  return e;
+}
+
+// Profiling bracket around one dominant-kernel launch (timing events live on the launch stream).
+struct ProfScope {
+  dbm_ctx ctx;
+  cudaStream_t st;
+  cudaEvent_t a = nullptr, b = nullptr;
+  int kind;
+  double flops, bytes;
+  ProfScope(dbm_ctx c, cudaStream_t s, int k, double f, double by) : ctx(c), st(s), kind(k), flops(f), bytes(by) {
+    if (!ctx->profiling) return;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    cudaEventRecord(a, st);
+  }
+  ~ProfScope() {
+    if (!a) return;
+    cudaEventRecord(b, st);
+    ctx->prof.push_back({a, b, kind, flops, bytes});
+  }
+};
+
+}  // namespace
+
+// ====================================================================== misc
+extern "C" const char* dbm_status_string(dbm_status s) {
+  switch (s) {
+    case DBM_OK: return "DBM_OK";
+    case DBM_ERR_ARG: return "DBM_ERR_ARG";
+    case DBM_ERR_SHAPE: return "DBM_ERR_SHAPE";
+    case DBM_ERR_RANGE: return "DBM_ERR_RANGE";
+    case DBM_ERR_PARTITION: return "DBM_ERR_PARTITION";
+    case DBM_ERR_PLAN: return "DBM_ERR_PLAN";
+    case DBM_ERR_OWNERSHIP: return "DBM_ERR_OWNERSHIP";
+    case DBM_ERR_ALIAS: return "DBM_ERR_ALIAS";
+    case DBM_ERR_GRID: return "DBM_ERR_GRID";
+    case DBM_ERR_WORKSPACE: return "DBM_ERR_WORKSPACE";
+    case DBM_ERR_CUDA: return "DBM_ERR_CUDA";
+    case DBM_ERR_NCCL: return "DBM_ERR_NCCL";
+    case DBM_ERR_NOMEM: return "DBM_ERR_NOMEM";
+  }
+  return "DBM_ERR_UNKNOWN";
+}
+
+extern "C" const char* dbm_last_error(void) { return g_err.c_str(); }
+
+extern "C" int dbm_unique_id_bytes(void) { return (int)sizeof(ncclUniqueId); }
+
+extern "C" dbm_status dbm_get_unique_id(void* id_out) {
+  ARG_CHECK(id_out, DBM_ERR_ARG, "null id buffer");
+  ncclUniqueId id;
+  NCCL_TRY((dbm_ctx) nullptr, ncclGetUniqueId(&id));
+  std::memcpy(id_out, &id, sizeof(id));
+  return DBM_OK;
+}
+
+// ====================================================================== context
+extern "C" dbm_status dbm_ctx_create(int nranks, int rank, int pr, int pc, const void* id, int device,
+                                     void* cuda_stream, dbm_ctx* out) {
+  ARG_CHECK(out, DBM_ERR_ARG, "null output handle");
+  ARG_CHECK(nranks >= 1 && rank >= 0 && rank < nranks, DBM_ERR_ARG, "bad nranks/rank");
+  ARG_CHECK(pr >= 0 && pc >= 0, DBM_ERR_ARG, "negative grid");
+  if (pr == 0 && pc == 0) {  // reading R1: largest divisor <= sqrt(P) rows
+    int best = 1;
+    for (int d = 1; (int64_t)d * d <= nranks; ++d)
+      if (nranks % d == 0) best = d;
+    pr = best;
+    pc = nranks / best;
+  }
+  ARG_CHECK(pr * pc == nranks, DBM_ERR_GRID, "pr*pc != nranks");
+  ARG_CHECK(nranks == 1 || id != nullptr, DBM_ERR_ARG, "multi-rank context needs an NCCL unique id");
+  dbm_ctx ctx = new dbm_ctx_s();
+  ctx->nranks = nranks;
+  ctx->rank = rank;
+  ctx->pr = pr;
+  ctx->pc = pc;
+  ctx->myrow = rank / pc;
+  ctx->mycol = rank % pc;
+  ctx->device = device;
+  cudaError_t e = cudaSetDevice(device);
+  ctx->stream = (cudaStream_t)cuda_stream;  // NULL = the legacy default stream (torch's default)
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->comm, cudaStreamNonBlocking);
+  if (e != cudaSuccess) {
+    set_error(std::string("context CUDA setup: ") + cudaGetErrorString(e));
+    delete ctx;
+    return DBM_ERR_CUDA;
+  }
+  if (nranks > 1) {
+    ncclUniqueId uid;
+    std::memcpy(&uid, id, sizeof(uid));
+    ncclComm_t comm;
+    ncclResult_t r = ncclCommInitRank(&comm, nranks, uid, rank);
+    if (r != ncclSuccess) {
+      set_error(std::string("ncclCommInitRank: ") + ncclGetErrorString(r));
+      cudaStreamDestroy(ctx->comm);
+      if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
+      delete ctx;
+      return DBM_ERR_NCCL;
+    }
+    ctx->nccl = comm;
+  }
+  num_sms();
+  *out = ctx;
+  return DBM_OK;
+}
+
+extern "C" dbm_status dbm_ctx_grid(dbm_ctx ctx, int* pr, int* pc, int* myrow, int* mycol) {
+  ARG_CHECK(ctx, DBM_ERR_ARG, "null context");
+  if (pr) *pr = ctx->pr;
+  if (pc) *pc = ctx->pc;
+  if (myrow) *myrow = ctx->myrow;
+  if (mycol) *mycol = ctx->mycol;
+  return DBM_OK;
+}
+
+extern "C" dbm_status dbm_ctx_set_stream(dbm_ctx ctx, void* stream) {
+  CTX_OK(ctx);
+  if (ctx->own_stream && ctx->stream != (cudaStream_t)stream) {
+    CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+    cudaStreamDestroy(ctx->stream);
+    ctx->own_stream = false;
+  }
+  ctx->stream = (cudaStream_t)stream;
+  return DBM_OK;
+}
+
+extern "C" dbm_status dbm_ctx_sync(dbm_ctx ctx) {
+  CTX_OK(ctx);
+  CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+  CUDA_TRY(ctx, cudaStreamSynchronize(ctx->comm));
+  if (ctx->nccl) {
+    ncclResult_t ae;
+    NCCL_TRY(ctx, ncclCommGetAsyncError((ncclComm_t)ctx->nccl, &ae));
+    NCCL_TRY(ctx, ae);
+  }
+  return DBM_OK;
+}
+
+extern "C" dbm_status dbm_ctx_set_profiling(dbm_ctx ctx, int on) {
+  ARG_CHECK(ctx, DBM_ERR_ARG, "null context");
+  ctx->profiling = on != 0;
+  return DBM_OK;
+}
+
+extern "C" dbm_status dbm_ctx_profile_read(dbm_ctx ctx, int kernel, double* ms_out, int64_t* launches_out,
+                                           double* flops_out, double* bytes_out) {
+  CTX_OK(ctx);
+  double ms = 0, fl = 0, by = 0;
+  int64_t n = 0;
+  std::vector<dbm_ctx_s::ProfRec> keep;
+  for (auto& r : ctx->prof) {
+    if (r.kind != kernel) {
+      keep.push_back(r);
+      continue;
+    }
+    CUDA_TRY(ctx, cudaEventSynchronize(r.b));
+    float t = 0;
+    CUDA_TRY(ctx, cudaEventElapsedTime(&t, r.a, r.b));
+    ms += t;
+    fl += r.flops;
+    by += r.bytes;
+    ++n;
+    cudaEventDestroy(r.a);
+    cudaEventDestroy(r.b);
+  }
+  ctx->prof.swap(keep);
+  if (ms_out) *ms_out = ms;
+  if (launches_out) *launches_out = n;
+  if (flops_out) *flops_out = fl;
+  if (bytes_out) *bytes_out = by;
+  return DBM_OK;
+}
+
+extern "C" dbm_status dbm_ctx_set_dense_chunk_bytes(dbm_ctx ctx, int64_t bytes) {
+  ARG_CHECK(ctx && bytes >= 1, DBM_ERR_ARG, "bad argument");
+  ctx->chunk_bytes = bytes;
+  return DBM_OK;
+}
+
+extern "C" dbm_status dbm_ctx_launch_count(dbm_ctx ctx, int64_t* out) {
+  ARG_CHECK(ctx && out, DBM_ERR_ARG, "null argument");
+  *out = ctx->launches;
+  return DBM_OK;
+}
+
+extern "C" dbm_status dbm_ctx_destroy(dbm_ctx ctx) {
+  if (!ctx) return DBM_OK;
+  cudaSetDevice(ctx->device);
+  cudaStreamSynchronize(ctx->stream);
+  cudaStreamSynchronize(ctx->comm);
+  for (auto& r : ctx->prof) {
+    cudaEventDestroy(r.a);
+    cudaEventDestroy(r.b);
+  }
+  for (auto e : ctx->ev_pool) cudaEventDestroy(e);
+  for (int i = 0; i < 2; ++i) {
+    if (ctx->stage[i]) cudaFreeHost(ctx->stage[i]);
+    if (ctx->stage_ev[i]) cudaEventDestroy(ctx->stage_ev[i]);
+  }
+  if (ctx->nccl) ncclCommDestroy((ncclComm_t)ctx->nccl);
+  cudaStreamDestroy(ctx->comm);
+  if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
+  delete ctx;
+  return DBM_OK;
+}
+
+// ====================================================================== matrix
+extern "C" dbm_status dbm_matrix_create(dbm_ctx ctx, int64_t rows, int64_t cols, int32_t bs, dbm_matrix* out) {
+  ARG_CHECK(ctx && out, DBM_ERR_ARG, "null argument");
+  ARG_CHECK(bs > 0 && rows >= 0 && cols >= 0, DBM_ERR_ARG, "bad block size or dimensions");
+  ARG_CHECK(rows % bs == 0 && cols % bs == 0, DBM_ERR_SHAPE, "rows/cols must be multiples of the block size");
+  ARG_CHECK(rows / bs < (1LL << 31) && cols / bs < (1LL << 31), DBM_ERR_SHAPE, "too many blocks");
+  dbm_matrix m = new dbm_matrix_s();
+  m->ctx = ctx;
+  m->rows = rows;
+  m->cols = cols;
+  m->bs = bs;
+  m->Mb = rows / bs;
+  m->Nb = cols / bs;
+  m->mloc = local_count(m->Mb, ctx->pr, ctx->myrow);
+  m->nloc = local_count(m->Nb, ctx->pc, ctx->mycol);
+  *out = m;
+  return DBM_OK;
+}
+
+extern "C" dbm_status dbm_matrix_local_info(dbm_matrix m, int64_t* mloc, int64_t* nloc, int64_t* bytes) {
+  ARG_CHECK(m, DBM_ERR_ARG, "null matrix");
+  if (mloc) *mloc = m->mloc;
+  if (nloc) *nloc = m->nloc;
+  if (bytes) *bytes = m->mloc * m->nloc * (int64_t)m->bs * m->bs * 8;
+  return DBM_OK;
+}
+
+extern "C" dbm_status dbm_matrix_local_csr(dbm_matrix m, int64_t* row_ptr, int64_t* col_idx, int64_t* row_idx) {
+  ARG_CHECK(m, DBM_ERR_ARG, "null matrix");
+  const dbm_ctx c = m->ctx;
+  for (int64_t li = 0; li <= m->mloc; ++li)
+    if (row_ptr) row_ptr[li] = li * m->nloc;
+  for (int64_t li = 0; li < m->mloc; ++li) {
+    if (row_idx) row_idx[li] = c->myrow + li * c->pr;
+    for (int64_t lj = 0; lj < m->nloc; ++lj)
+      if (col_idx) col_idx[li * m->nloc + lj] = c->mycol + lj * c->pc;
+  }
+  return DBM_OK;
+}
+
+extern "C" dbm_status dbm_matrix_attach(dbm_matrix m, void* arena, int64_t bytes) {
+  ARG_CHECK(m, DBM_ERR_ARG, "null matrix");
+  const int64_t need = m->mloc * m->nloc * (int64_t)m->bs * m->bs * 8;
+  ARG_CHECK(bytes >= need, DBM_ERR_WORKSPACE, "arena smaller than dbm_matrix_local_info() bytes");
+  ARG_CHECK(need == 0 || arena != nullptr, DBM_ERR_ARG, "null arena");
+  ARG_CHECK(((uintptr_t)arena & 15) == 0, DBM_ERR_ARG, "arena must be 16-byte aligned");
+  m->arena = (double*)arena;
+  m->arena_bytes = bytes;
+  return DBM_OK;
+}
+
+static dbm_status need_arena(dbm_matrix m) {
+  const int64_t need = m->mloc * m->nloc * (int64_t)m->bs * m->bs * 8;
+  ARG_CHECK(need == 0 || m->arena, DBM_ERR_WORKSPACE, "matrix has no attached arena");
+  return DBM_OK;
+}
+
+extern "C" dbm_status dbm_matrix_fill_random(dbm_matrix m, uint64_t seed, uint32_t mat_id, int kind) {
+  ARG_CHECK(m, DBM_ERR_ARG, "null matrix");
+  ARG_CHECK(kind == 0 || kind == 1, DBM_ERR_ARG, "kind must be 0 or 1");
+  dbm_ctx ctx = m->ctx;
+  CTX_OK(ctx);
+  if (dbm_status s = need_arena(m)) return s;
+  launch_fill(m->arena, m->mloc, m->nloc, m->bs, ctx->pr, ctx->pc, ctx->myrow, ctx->mycol, seed, mat_id, kind,
+              ctx->stream);
+  ctx->launches += (m->mloc * m->nloc) ? 1 : 0;
+  CUDA_TRY(ctx, cudaGetLastError());
+  return DBM_OK;
+}
+
+static dbm_status block_slot(dbm_matrix m, int64_t bi, int64_t bj, int64_t* slot) {
+  ARG_CHECK(bi >= 0 && bj >= 0 && bi < m->Mb && bj < m->Nb, DBM_ERR_RANGE, "block index out of range");
+  const dbm_ctx c = m->ctx;
+  ARG_CHECK(bi % c->pr == c->myrow && bj % c->pc == c->mycol, DBM_ERR_OWNERSHIP, "block owned by another rank");
+  *slot = (bi / c->pr) * m->nloc + (bj / c->pc);
+  return DBM_OK;
+}
+
+extern "C" dbm_status dbm_matrix_set_block(dbm_matrix m, int64_t bi, int64_t bj, const double* host) {
+  ARG_CHECK(m && host, DBM_ERR_ARG, "null argument");
+  dbm_ctx ctx = m->ctx;
+  CTX_OK(ctx);
+  int64_t slot;
+  if (dbm_status s = block_slot(m, bi, bj, &slot)) return s;
+  if (dbm_status s = need_arena(m)) return s;
+  const size_t bb = (size_t)m->bs * m->bs;
+  CUDA_TRY(ctx, cudaMemcpyAsync(m->arena + slot * bb, host, bb * 8, cudaMemcpyHostToDevice, ctx->stream));
+  CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+  return DBM_OK;
+}
+
+extern "C" dbm_status dbm_matrix_get_block(dbm_matrix m, int64_t bi, int64_t bj, double* host) {
+  ARG_CHECK(m && host, DBM_ERR_ARG, "null argument");
+  dbm_ctx ctx = m->ctx;
+  CTX_OK(ctx);
+  int64_t slot;
+  if (dbm_status s = block_slot(m, bi, bj, &slot)) return s;
+  if (dbm_status s = need_arena(m)) return s;
+  const size_t bb = (size_t)m->bs * m->bs;
+  CUDA_TRY(ctx, cudaMemcpyAsync(host, m->arena + slot * bb, bb * 8, cudaMemcpyDeviceToHost, ctx->stream));
+  CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+  return DBM_OK;
+}
+
+// Host <-> device of the whole arena.  Pinned host memory: one async copy.  Pageable: staged through a
+// pinned double buffer (P:174 double buffering, P:200 page-locked memory pools).
+static dbm_status host_copy(dbm_matrix m, void* host, bool upload) {
+  dbm_ctx ctx = m->ctx;
+  const size_t bytes = (size_t)(m->mloc * m->nloc) * m->bs * m->bs * 8;
+  if (bytes == 0) return DBM_OK;
+  cudaPointerAttributes at;
+  bool pinned = cudaPointerGetAttributes(&at, host) == cudaSuccess &&
+                (at.type == cudaMemoryTypeHost || at.type == cudaMemoryTypeManaged);
+  cudaGetLastError();
+  char* dev = (char*)m->arena;
+  if (pinned) {
+    CUDA_TRY(ctx, cudaMemcpyAsync(upload ? (void*)dev : host, upload ? host : (void*)dev, bytes,
+                                  upload ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToHost, ctx->stream));
+    return DBM_OK;
+  }
+  const size_t chunk = 64ull << 20;
+  if (!ctx->stage[0]) {
+    for (int i = 0; i < 2; ++i) {
+      CUDA_TRY(ctx, cudaHostAlloc(&ctx->stage[i], chunk, cudaHostAllocDefault));
+      CUDA_TRY(ctx, cudaEventCreateWithFlags(&ctx->stage_ev[i], cudaEventDisableTiming));
+    }
+    ctx->stage_bytes = chunk;
+  }
+  size_t off = 0;
+  int b = 0;
+  bool used[2] = {false, false};
+  while (off < bytes) {
+    const size_t n = std::min(chunk, bytes - off);
+    if (used[b]) CUDA_TRY(ctx, cudaEventSynchronize(ctx->stage_ev[b]));
+    if (upload) {
+      std::memcpy(ctx->stage[b], (char*)host + off, n);
+      CUDA_TRY(ctx, cudaMemcpyAsync(dev + off, ctx->stage[b], n, cudaMemcpyHostToDevice, ctx->stream));
+      CUDA_TRY(ctx, cudaEventRecord(ctx->stage_ev[b], ctx->stream));
+    } else {
+      CUDA_TRY(ctx, cudaMemcpyAsync(ctx->stage[b], dev + off, n, cudaMemcpyDeviceToHost, ctx->stream));
+      CUDA_TRY(ctx, cudaEventRecord(ctx->stage_ev[b], ctx->stream));
+      CUDA_TRY(ctx, cudaEventSynchronize(ctx->stage_ev[b]));
+      std::memcpy((char*)host + off, ctx->stage[b], n);
+    }
+    used[b] = true;
+    off += n;
+    b ^= 1;
+  }
+  for (int i = 0; i < 2; ++i)
+    if (used[i]) CUDA_TRY(ctx, cudaEventSynchronize(ctx->stage_ev[i]));
+  return DBM_OK;
+}
+
+extern "C" dbm_status dbm_matrix_upload(dbm_matrix m, const void* host) {
+  ARG_CHECK(m && host, DBM_ERR_ARG, "null argument");
+  CTX_OK(m->ctx);
+  if (dbm_status s = need_arena(m)) return s;
+  return host_copy(m, (void*)host, true);
+}
+
+extern "C" dbm_status dbm_matrix_download(dbm_matrix m, void* host) {
+  ARG_CHECK(m && host, DBM_ERR_ARG, "null argument");
+  CTX_OK(m->ctx);
+  if (dbm_status s = need_arena(m)) return s;
+  return host_copy(m, host, false);
+}
+
+extern "C" dbm_status dbm_owner_of_block(dbm_matrix m, int64_t bi, int64_t bj, int* rank) {
+  ARG_CHECK(m && rank, DBM_ERR_ARG, "null argument");
+  ARG_CHECK(bi >= 0 && bj >= 0 && bi < m->Mb && bj < m->Nb, DBM_ERR_RANGE, "block index out of range");
+  *rank = (int)(bi % m->ctx->pr) * m->ctx->pc + (int)(bj % m->ctx->pc);
+  return DBM_OK;
+}
+
+extern "C" dbm_status dbm_matrix_destroy(dbm_matrix m) {
+  delete m;
+  return DBM_OK;
+}
+
+// ====================================================================== densify / undensify
+extern "C" dbm_status dbm_densify(dbm_matrix m, double* dense, int64_t ld, int layout) {
+  ARG_CHECK(m, DBM_ERR_ARG, "null matrix");
+  ARG_CHECK(layout == 0 || layout == 1, DBM_ERR_ARG, "layout must be 0 or 1");
+  dbm_ctx ctx = m->ctx;
+  CTX_OK(ctx);
+  if (dbm_status s = need_arena(m)) return s;
+  const int64_t rows = m->mloc * m->bs, cols = m->nloc * m->bs;
+  ARG_CHECK(ld >= (layout == 0 ? rows : cols), DBM_ERR_PLAN, "leading dimension too small");
+  ARG_CHECK(rows * cols == 0 || dense, DBM_ERR_ARG, "null dense buffer");
+  ProfScope ps(ctx, ctx->stream, 2, 0.0, 16.0 * rows * cols);
+  launch_densify_cols(m->arena, m->mloc, m->nloc, m->bs, 0, 1, m->nloc, dense, ld, layout, ctx->stream);
+  ctx->launches += rows * cols ? 1 : 0;
+  CUDA_TRY(ctx, cudaGetLastError());
+  return DBM_OK;
+}
+
+extern "C" dbm_status dbm_undensify(dbm_matrix m, const double* dense, int64_t ld, double alpha, double beta) {
+  ARG_CHECK(m, DBM_ERR_ARG, "null matrix");
+  dbm_ctx ctx = m->ctx;
+  CTX_OK(ctx);
+  if (dbm_status s = need_arena(m)) return s;
+  const int64_t rows = m->mloc * m->bs, cols = m->nloc * m->bs;
+  ARG_CHECK(ld >= rows, DBM_ERR_PLAN, "leading dimension too small");
+  ARG_CHECK(rows * cols == 0 || dense, DBM_ERR_ARG, "null dense buffer");
+  ProfScope ps(ctx, ctx->stream, 3, 0.0, (beta == 0.0 ? 16.0 : 24.0) * rows * cols);
+  launch_undensify(dense, ld, 1, 0, m->mloc, m->nloc, m->bs, alpha, beta, m->arena, ctx->stream);
+  ctx->launches += rows * cols ? 1 : 0;
+  CUDA_TRY(ctx, cudaGetLastError());
+  return DBM_OK;
+}
+
+// ====================================================================== multiply plan
+namespace {
+
+struct Plan {
+  int L = 1;
+  int pr = 1, pc = 1, r = 0, c = 0;
+  int64_t bs = 0, Mb = 0, Nb = 0, Kb = 0;
+  int64_t mloc = 0, nloc = 0;  // C / A rows, C / B cols (blocks)
+  int64_t kA = 0, kB = 0;      // A local block cols, B local block rows
+  bool densified = true;
+  std::vector<int64_t> kb;  // panel sizes (blocks) per kappa
+  // K chunking (single-rank densified path): chunk_kb blocks per chunk
+  int64_t chunk_kb = 0, nchunks = 1;
+  // workspace regions (byte offsets)
+  size_t off_cd = 0, off_ownA = 0, off_ownB = 0, off_recvA[2] = {0, 0}, off_recvB[2] = {0, 0}, off_part = 0;
+  size_t off_trav = 0, off_trip = 0;
+  std::vector<size_t> ownA_off, ownB_off;  // per kappa, SIZE_MAX if not owned
+  int64_t trip_cap = 0;                     // entries per stack-generation chunk
+  size_t total = 0;
+  int max_split = 1;
+
+  int kappa(int s) const { return (r + c + s) % L; }
+  int a_src(int s) const { return r * pc + kappa(s) % pc; }
+  int b_src(int s) const { return (kappa(s) % pr) * pc + c; }
+  int me() const { return r * pc + c; }
+  // dense panel leading dimensions (even, so TMA strides are 16-byte multiples)
+  int64_t ld_panel(int k) const { return round_up(std::max<int64_t>(kb[k] * bs, 1), 2); }
+  size_t a_panel_bytes(int k) const {
+    return densified ? (size_t)(mloc * bs) * ld_panel(k) * 8 : (size_t)(mloc * kb[k]) * bs * bs * 8;
+  }
+  size_t b_panel_bytes(int k) const {
+    return densified ? (size_t)(nloc * bs) * ld_panel(k) * 8 : (size_t)(nloc * kb[k]) * bs * bs * 8;
+  }
+};
+
+size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
+
+constexpr int64_t kDefaultChunkBytes = 16ll << 30;   // A+B dense chunk budget (single rank)
+constexpr int64_t kTripChunkEntries = 1ll << 25;      // 400 MB of triplets per generation chunk
+
+// Host-only plan: depends on the grid, this rank's coordinates and the block counts (no CUDA).
+Plan make_plan_raw(int nranks, int pr, int pc, int r, int c, int64_t Mb, int64_t Nb, int64_t Kb, int64_t bs,
+                   bool densified, int64_t chunk_bytes) {
+  Plan p;
+  p.pr = pr;
+  p.pc = pc;
+  p.r = r;
+  p.c = c;
+  p.L = (int)lcm64(p.pr, p.pc);
+  p.bs = bs;
+  p.Mb = Mb;
+  p.Kb = Kb;
+  p.Nb = Nb;
+  p.mloc = local_count(Mb, pr, r);
+  p.nloc = local_count(Nb, pc, c);
+  p.kA = local_count(Kb, pc, c);
+  p.kB = local_count(Kb, pr, r);
+  p.densified = densified;
+  p.kb.resize(p.L);
+  for (int k = 0; k < p.L; ++k) p.kb[k] = local_count(p.Kb, p.L, k);
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    size_t o = off;
+    off = align256(off + bytes);
+    return o;
+  };
+  const int64_t M = p.mloc * p.bs, N = p.nloc * p.bs;
+  p.ownA_off.assign(p.L, SIZE_MAX);
+  p.ownB_off.assign(p.L, SIZE_MAX);
+  if (densified) {
+    p.off_cd = take((size_t)M * N * 8);
+    if (nranks == 1) {  // K-chunked densify -> GEMM accumulate (fits HBM at 63,360^3)
+      const int64_t per_kblock = (M + N) * p.bs * 8;
+      int64_t ck = per_kblock > 0 ? std::max<int64_t>(1, chunk_bytes / per_kblock) : p.Kb;
+      ck = std::min<int64_t>(std::max<int64_t>(ck, 1), std::max<int64_t>(p.Kb, 1));
+      p.chunk_kb = ck;
+      p.nchunks = p.Kb > 0 ? (p.Kb + ck - 1) / ck : 1;
+      const int64_t ld = round_up(ck * p.bs, 2);
+      p.off_ownA = take((size_t)M * ld * 8);
+      p.off_ownB = take((size_t)N * ld * 8);
+      p.max_split = pick_splitk(M, N, std::min<int64_t>(ck, std::max<int64_t>(p.Kb, 1)) * p.bs, num_sms());
+    } else {
+      for (int k = 0; k < p.L; ++k) {
+        if (k % p.pc == p.c) p.ownA_off[k] = take(p.a_panel_bytes(k));
+        if (k % p.pr == p.r) p.ownB_off[k] = take(p.b_panel_bytes(k));
+      }
+      for (int s = 0; s < p.L; ++s)
+        p.max_split = std::max(p.max_split, pick_splitk(M, N, p.kb[p.kappa(s)] * p.bs, num_sms()));
+    }
+    if (p.max_split > 1) p.off_part = take((size_t)p.max_split * M * N * 8);
+  } else {
+    // own panels need packing only when a rank holds more than one panel per operand
+    for (int k = 0; k < p.L; ++k) {
+      if (k % p.pc == p.c && p.L / p.pc > 1) p.ownA_off[k] = take(p.a_panel_bytes(k));
+      if (k % p.pr == p.r && p.L / p.pr > 1) p.ownB_off[k] = take(p.b_panel_bytes(k));
+    }
+    p.off_trav = take((size_t)std::max<int64_t>(p.mloc * p.nloc, 1) * 8);
+    int64_t maxkb = 1;
+    for (int k = 0; k < p.L; ++k) maxkb = std::max(maxkb, p.kb[k]);
+    const int64_t runs = std::max<int64_t>(1, kTripChunkEntries / maxkb);
+    p.trip_cap = std::min<int64_t>(runs, std::max<int64_t>(p.mloc * p.nloc, 1)) * maxkb;
+    p.off_trip = take((size_t)p.trip_cap * 12);
+  }
+  if (nranks > 1) {
+    size_t amax = 0, bmax = 0;
+    int nA = 0, nB = 0;
+    for (int s = 0; s < p.L; ++s) {
+      if (p.a_src(s) != p.me()) {
+        amax = std::max(amax, p.a_panel_bytes(p.kappa(s)));
+        ++nA;
+      }
+      if (p.b_src(s) != p.me()) {
+        bmax = std::max(bmax, p.b_panel_bytes(p.kappa(s)));
+        ++nB;
+      }
+    }
+    for (int i = 0; i < std::min(nA, 2); ++i) p.off_recvA[i] = take(amax);
+    for (int i = 0; i < std::min(nB, 2); ++i) p.off_recvB[i] = take(bmax);
+  }
+  p.total = std::max<size_t>(off, 256);
+  return p;
+}
+
+Plan make_plan(dbm_ctx ctx, dbm_matrix A, dbm_matrix B, dbm_matrix C, bool densified) {
+  (void)C;
+  return make_plan_raw(ctx->nranks, ctx->pr, ctx->pc, ctx->myrow, ctx->mycol, A->Mb, B->Nb, A->Nb, A->bs, densified,
+                       ctx->chunk_bytes);
+}
+
+// One Cannon exchange step as a list of point-to-point operations (owner-pull, reading R5):
+// for every rank whose step-s panel lives here, a send; for each of this rank's remote panels, a recv.
+struct XOp {
+  int send;     // 1 send, 0 recv
+  int operand;  // 0 = A panel, 1 = B panel
+  int peer;
+  int kappa;
+  int64_t bytes;
+};
+
+std::vector<XOp> exchange_ops(const Plan& p, int s) {
+  std::vector<XOp> ops;
+  const int me = p.me();
+  for (int rr = 0; rr < p.pr; ++rr)
+    for (int cc = 0; cc < p.pc; ++cc) {
+      const int dst = rr * p.pc + cc;
+      if (dst == me) continue;
+      const int k = (rr + cc + s) % p.L;
+      if (rr == p.r && k % p.pc == p.c) ops.push_back({1, 0, dst, k, (int64_t)p.a_panel_bytes(k)});  // dst needs my A(r,k)
+      if (cc == p.c && k % p.pr == p.r) ops.push_back({1, 1, dst, k, (int64_t)p.b_panel_bytes(k)});  // dst needs my B(k,c)
+    }
+  const int k = p.kappa(s);
+  if (p.a_src(s) != me) ops.push_back({0, 0, p.a_src(s), k, (int64_t)p.a_panel_bytes(k)});
+  if (p.b_src(s) != me) ops.push_back({0, 1, p.b_src(s), k, (int64_t)p.b_panel_bytes(k)});
+  return ops;
+}
+
+dbm_status validate(dbm_ctx ctx, dbm_matrix A, dbm_matrix B, dbm_matrix C) {
+  ARG_CHECK(ctx && A && B && C, DBM_ERR_ARG, "null handle");
+  ARG_CHECK(A->ctx == ctx && B->ctx == ctx && C->ctx == ctx, DBM_ERR_GRID, "matrices from a different context");
+  ARG_CHECK(A->bs == B->bs && A->bs == C->bs, DBM_ERR_PARTITION, "block sizes differ (K partition mismatch)");
+  ARG_CHECK(A->cols == B->rows && A->rows == C->rows && B->cols == C->cols, DBM_ERR_SHAPE, "non-conformant shapes");
+  ARG_CHECK(C != A && C != B, DBM_ERR_ALIAS, "C aliases A or B");
+  auto overlap = [](dbm_matrix x, dbm_matrix y) {
+    if (!x->arena || !y->arena) return false;
+    const char *a0 = (const char*)x->arena, *a1 = a0 + x->mloc * x->nloc * x->bs * x->bs * 8;
+    const char *b0 = (const char*)y->arena, *b1 = b0 + y->mloc * y->nloc * y->bs * y->bs * 8;
+    return a0 < b1 && b0 < a1;
+  };
+  ARG_CHECK(!overlap(C, A) && !overlap(C, B), DBM_ERR_ALIAS, "C storage overlaps A or B");
+  if (dbm_status s = need_arena(A)) return s;
+  if (dbm_status s = need_arena(B)) return s;
+  if (dbm_status s = need_arena(C)) return s;
+  return DBM_OK;
+}
+
+}  // namespace
+
+extern "C" dbm_status dbm_plan_exchange(int pr, int pc, int myrow, int mycol, int64_t Mb, int64_t Nb, int64_t Kb,
+                                        int32_t bs, dbm_path path, int step, int32_t* ops, int64_t* bytes,
+                                        int* n_ops) {
+  ARG_CHECK(n_ops && pr > 0 && pc > 0 && myrow >= 0 && myrow < pr && mycol >= 0 && mycol < pc && bs > 0,
+            DBM_ERR_ARG, "bad grid or block size");
+  ARG_CHECK(Mb >= 0 && Nb >= 0 && Kb >= 0, DBM_ERR_ARG, "negative block counts");
+  const Plan p = make_plan_raw(pr * pc, pr, pc, myrow, mycol, Mb, Nb, Kb, bs, path == DBM_PATH_DENSIFIED,
+                               16ll << 30);
+  ARG_CHECK(step >= 0 && step < p.L, DBM_ERR_RANGE, "step out of range");
+  const std::vector<XOp> v = exchange_ops(p, step);
+  if (ops || bytes) {
+    ARG_CHECK(*n_ops >= (int)v.size(), DBM_ERR_ARG, "ops buffer too small");
+    for (size_t i = 0; i < v.size(); ++i) {
+      if (ops) {
+        ops[4 * i + 0] = v[i].send;
+        ops[4 * i + 1] = v[i].operand;
+        ops[4 * i + 2] = v[i].peer;
+        ops[4 * i + 3] = v[i].kappa;
+      }
+      if (bytes) bytes[i] = v[i].bytes;
+    }
+  }
+  *n_ops = (int)v.size();
+  return DBM_OK;
+}
+
+extern "C" dbm_status dbm_multiply_workspace(dbm_ctx ctx, dbm_matrix A, dbm_matrix B, dbm_matrix C, dbm_path path,
+                                             int64_t* bytes) {
+  ARG_CHECK(bytes, DBM_ERR_ARG, "null output");
+  ARG_CHECK(path == DBM_PATH_BLOCKED || path == DBM_PATH_DENSIFIED, DBM_ERR_ARG, "bad path");
+  if (dbm_status s = validate(ctx, A, B, C)) return s;
+  *bytes = (int64_t)make_plan(ctx, A, B, C, path == DBM_PATH_DENSIFIED).total;
+  return DBM_OK;
+}
+
+namespace {
+
+// One Cannon exchange (owner-pull, reading R5): everything this rank sends and receives at step s.
+dbm_status post_exchange(dbm_ctx ctx, const Plan& p, int s, char* ws, const double* Aarena, const double* Barena,
+                         int bufA, int bufB, int64_t* sent, int64_t* recv) {
+  ncclComm_t comm = (ncclComm_t)ctx->nccl;
+  NCCL_TRY(ctx, ncclGroupStart());
+  for (const XOp& op : exchange_ops(p, s)) {
+    const size_t n = (size_t)op.bytes;
+    if (op.send) {
+      const size_t own = op.operand == 0 ? p.ownA_off[op.kappa] : p.ownB_off[op.kappa];
+      const void* src = own != SIZE_MAX ? (const void*)(ws + own) : (const void*)(op.operand == 0 ? Aarena : Barena);
+      if (n) NCCL_TRY(ctx, ncclSend(src, n / 8, ncclDouble, op.peer, comm, ctx->comm));
+      *sent += (int64_t)n;
+    } else {
+      void* dst = ws + (op.operand == 0 ? p.off_recvA[bufA] : p.off_recvB[bufB]);
+      if (n) NCCL_TRY(ctx, ncclRecv(dst, n / 8, ncclDouble, op.peer, comm, ctx->comm));
+      *recv += (int64_t)n;
+    }
+  }
+  NCCL_TRY(ctx, ncclGroupEnd());
+  return DBM_OK;
+}
+
+__global__ void scale_kernel(double* __restrict__ x, int64_t n, double beta) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    x[i] = beta == 0.0 ? 0.0 : beta * x[i];
+}
+
+}  // namespace
+
+extern "C" dbm_status dbm_multiply(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_matrix B, double beta, dbm_matrix C,
+                                   dbm_path path, int32_t stack_cap, void* workspace, int64_t ws_bytes,
+                                   dbm_stats* stats) {
+  CTX_OK(ctx);
+  ARG_CHECK(path == DBM_PATH_BLOCKED || path == DBM_PATH_DENSIFIED, DBM_ERR_ARG, "bad path");
+  ARG_CHECK(stack_cap >= 0, DBM_ERR_ARG, "negative stack cap");
+  if (dbm_status s = validate(ctx, A, B, C)) return s;
+  const bool dens = path == DBM_PATH_DENSIFIED;
+  const Plan p = make_plan(ctx, A, B, C, dens);
+  ARG_CHECK(workspace != nullptr && ws_bytes >= (int64_t)p.total, DBM_ERR_WORKSPACE,
+            "workspace smaller than dbm_multiply_workspace()");
+  const int64_t cap = stack_cap ? stack_cap : 30000;
+  dbm_stats st{};
+  st.steps = p.L;
+  int launches = 0;
+  cudaStream_t cs = ctx->stream;
+  char* ws = (char*)workspace;
+  const int64_t bs = p.bs, M = p.mloc * bs, N = p.nloc * bs;
+  const int64_t bb = bs * bs;
+
+  // BLAS convention: alpha == 0 -> A and B are not read (reading R8).
+  if (alpha == 0.0 || p.Kb == 0) {
+    const int64_t n = M * N;
+    if (n) {
+      scale_kernel<<<(unsigned)std::min<int64_t>((n + 255) / 256, num_sms() * 16), 256, 0, cs>>>(C->arena, n, beta);
+      ++launches;
+      CUDA_TRY(ctx, cudaGetLastError());
+    }
+    ctx->launches += launches;
+    st.kernel_launches = launches;
+    if (stats) *stats = st;
+    return DBM_OK;
+  }
+
+  // ------------------------------------------------ own panels (densify or pack), on the compute stream
+  if (ctx->nranks > 1) {
+    for (int k = 0; k < p.L; ++k) {
+      if (p.ownA_off[k] != SIZE_MAX) {
+        const int64_t col0 = (k - p.c) / p.pc, stride = p.L / p.pc;
+        double* dst = (double*)(ws + p.ownA_off[k]);
+        if (dens) {
+          ProfScope ps(ctx, cs, 2, 0.0, 16.0 * M * p.kb[k] * bs);
+          launch_densify_cols(A->arena, p.mloc, p.kA, (int)bs, col0, stride, p.kb[k], dst, p.ld_panel(k), 1, cs);
+        } else {
+          launch_pack_cols(A->arena, p.mloc, p.kA, (int)bs, col0, stride, p.kb[k], dst, cs);
+        }
+        launches += (M * p.kb[k]) ? 1 : 0;
+      }
+      if (p.ownB_off[k] != SIZE_MAX) {
+        const int64_t row0 = (k - p.r) / p.pr, stride = p.L / p.pr;
+        double* dst = (double*)(ws + p.ownB_off[k]);
+        if (dens) {
+          ProfScope ps(ctx, cs, 2, 0.0, 16.0 * N * p.kb[k] * bs);
+          launch_densify_rows(B->arena, p.nloc, (int)bs, row0, stride, p.kb[k], dst, p.ld_panel(k), 0, cs);
+        } else {
+          launch_pack_rows(B->arena, p.nloc, (int)bs, row0, stride, p.kb[k], dst, cs);
+        }
+        launches += (N * p.kb[k]) ? 1 : 0;
+      }
+    }
+    CUDA_TRY(ctx, cudaGetLastError());
+  }
+
+  // blocked path: traversal table once per multiply
+  int32_t* trav_li = nullptr;
+  int32_t* trav_lj = nullptr;
+  int32_t* trip = nullptr;
+  if (!dens) {
+    trav_li = (int32_t*)(ws + p.off_trav);
+    trav_lj = trav_li + std::max<int64_t>(p.mloc * p.nloc, 1);
+    trip = (int32_t*)(ws + p.off_trip);
+    ProfScope ps(ctx, cs, 4, 0.0, 8.0 * p.mloc * p.nloc);
+    launch_traversal(p.mloc, p.nloc, trav_li, trav_lj, cs);
+    launches += (p.mloc * p.nloc) ? 1 : 0;
+  }
+
+  // ------------------------------------------------ Cannon steps
+  std::vector<cudaEvent_t> ev_x(p.L, nullptr), ev_g(p.L, nullptr);
+  cudaEvent_t ev_ready = nullptr;
+  int bufA_of[64], bufB_of[64];
+  if (ctx->nranks > 1) {
+    ARG_CHECK(p.L <= 64, DBM_ERR_GRID, "grid too large (L > 64)");
+    int na = 0, nb = 0;
+    for (int s = 0; s < p.L; ++s) {
+      bufA_of[s] = (p.a_src(s) != p.me()) ? (na++ & 1) : -1;
+      bufB_of[s] = (p.b_src(s) != p.me()) ? (nb++ & 1) : -1;
+    }
+    ev_ready = get_event(ctx);
+    CUDA_TRY(ctx, cudaEventRecord(ev_ready, cs));
+    CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->comm, ev_ready, 0));
+    for (int s = 0; s < p.L; ++s) {
+      ev_x[s] = get_event(ctx);
+      ev_g[s] = get_event(ctx);
+    }
+    if (dbm_status e = post_exchange(ctx, p, 0, ws, A->arena, B->arena, bufA_of[0], bufB_of[0], &st.bytes_sent,
+                                     &st.bytes_recv))
+      return e;
+    CUDA_TRY(ctx, cudaEventRecord(ev_x[0], ctx->comm));
+  }
+
+  for (int s = 0; s < p.L; ++s) {
+    const int k = p.kappa(s);
+    if (ctx->nranks > 1) {
+      if (s + 1 < p.L) {  // prefetch step s+1 while step s computes (P:171 overlap)
+        if (s >= 1) CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->comm, ev_g[s - 1], 0));
+        if (dbm_status e = post_exchange(ctx, p, s + 1, ws, A->arena, B->arena, bufA_of[s + 1], bufB_of[s + 1],
+                                         &st.bytes_sent, &st.bytes_recv))
+          return e;
+        CUDA_TRY(ctx, cudaEventRecord(ev_x[s + 1], ctx->comm));
+      }
+      CUDA_TRY(ctx, cudaStreamWaitEvent(cs, ev_x[s], 0));
+    }
+    const int64_t kbk = p.kb[k];
+    // operand panels for this step
+    const double* Ap;
+    const double* Bp;
+    if (ctx->nranks > 1) {
+      Ap = p.a_src(s) != p.me() ? (const double*)(ws + p.off_recvA[bufA_of[s]])
+                                : (p.ownA_off[k] != SIZE_MAX ? (const double*)(ws + p.ownA_off[k]) : A->arena);
+      Bp = p.b_src(s) != p.me() ? (const double*)(ws + p.off_recvB[bufB_of[s]])
+                                : (p.ownB_off[k] != SIZE_MAX ? (const double*)(ws + p.ownB_off[k]) : B->arena);
+    } else {
+      Ap = A->arena;
+      Bp = B->arena;
+    }
+    if (dens) {
+      double* Cd = (double*)(ws + p.off_cd);
+      if (ctx->nranks == 1) {
+        // K-chunked: densify chunk -> GEMM accumulate
+        for (int64_t ch = 0; ch < p.nchunks; ++ch) {
+          const int64_t k0 = ch * p.chunk_kb, nk = std::min(p.chunk_kb, p.Kb - k0);
+          const int64_t ld = round_up(p.chunk_kb * bs, 2);
+          double* Ad = (double*)(ws + p.off_ownA);
+          double* Bd = (double*)(ws + p.off_ownB);
+          {
+            ProfScope ps(ctx, cs, 2, 0.0, 16.0 * (M + N) * nk * bs);
+            launch_densify_cols(A->arena, p.mloc, p.kA, (int)bs, k0, 1, nk, Ad, ld, 1, cs);
+            launch_densify_rows(B->arena, p.nloc, (int)bs, k0, 1, nk, Bd, ld, 0, cs);
+            launches += 2;
+          }
+          GemmArgs g{M, N, nk * bs, Ad, ld, Bd, ld, Cd, M, 1.0, ch == 0 ? 0.0 : 1.0, 1, nullptr};
+          g.splitk = pick_splitk(M, N, g.K, num_sms());
+          g.partial = g.splitk > 1 ? (double*)(ws + p.off_part) : nullptr;
+          {
+            ProfScope ps(ctx, cs, 0, 2.0 * M * N * g.K, 8.0 * (M * g.K + N * g.K + M * N * (ch ? 2 : 1)));
+            CUDA_TRY(ctx, launch_dgemm(g, cs, &launches));
+          }
+          ++st.gemm_launches;
+          ++st.entries;
+          ++st.stacks;
+          st.flops += 2.0 * M * N * g.K;
+        }
+      } else {
+        const int64_t ld = p.ld_panel(k);
+        GemmArgs g{M, N, kbk * bs, Ap, ld, Bp, ld, Cd, M, 1.0, s == 0 ? 0.0 : 1.0, 1, nullptr};
+        g.splitk = pick_splitk(M, N, g.K, num_sms());
+        g.partial = g.splitk > 1 ? (double*)(ws + p.off_part) : nullptr;
+        {
+          ProfScope ps(ctx, cs, 0, 2.0 * M * N * g.K, 8.0 * (M * g.K + N * g.K + M * N * (s ? 2 : 1)));
+          CUDA_TRY(ctx, launch_dgemm(g, cs, &launches));
+        }
+        ++st.gemm_launches;
+        st.entries += (M && N) ? 1 : 0;  // densified batches hold one multiplication
+        st.stacks += (M && N) ? 1 : 0;
+        st.flops += 2.0 * M * N * g.K;
+      }
+    } else if (kbk > 0 && p.mloc * p.nloc > 0) {
+      // blocked: Generation (stack chunks) -> batched small-block GEMM
+      const int64_t nruns = p.mloc * p.nloc;
+      const int64_t runs_per_chunk = std::max<int64_t>(1, p.trip_cap / kbk);
+      const int64_t a_ld = kbk;  // A panel is mloc x kb blocks, row-major over (li, kk)
+      for (int64_t q0 = 0; q0 < nruns; q0 += runs_per_chunk) {
+        const int64_t q1 = std::min(nruns, q0 + runs_per_chunk);
+        {
+          ProfScope ps(ctx, cs, 4, 0.0, 12.0 * (q1 - q0) * kbk);
+          launch_stackgen(trav_li, trav_lj, q0, q1, kbk, p.nloc, a_ld, p.nloc, trip, cs);
+          ++launches;
+        }
+        {
+          ProfScope ps(ctx, cs, 1, 2.0 * bs * bb * (q1 - q0) * kbk, 16.0 * bb * (q1 - q0) * kbk);
+          CUDA_TRY(ctx, launch_smm((int)bs, trip, q1 - q0, kbk, Ap, Bp, C->arena, alpha, s == 0 ? beta : 1.0, cs,
+                                   &launches));
+        }
+      }
+      st.entries += nruns * kbk;
+      st.stacks += kbk <= cap ? (nruns + (cap / kbk) - 1) / (cap / kbk) : nruns * ((kbk + cap - 1) / cap);
+      st.flops += 2.0 * bs * bb * nruns * kbk;
+    } else if (s == 0 && p.mloc * p.nloc > 0) {
+      // empty K panel at step 0 still applies beta exactly once
+      const int64_t n = M * N;
+      scale_kernel<<<(unsigned)std::min<int64_t>((n + 255) / 256, num_sms() * 16), 256, 0, cs>>>(C->arena, n, beta);
+      ++launches;
+    }
+    CUDA_TRY(ctx, cudaGetLastError());
+    if (ctx->nranks > 1) CUDA_TRY(ctx, cudaEventRecord(ev_g[s], cs));
+  }
+
+  if (ctx->nranks > 1) {
+    // the comm stream's last op covers every send: the caller may reuse A/B after this point
+    CUDA_TRY(ctx, cudaStreamWaitEvent(cs, ev_x[p.L - 1], 0));
+  }
+  if (dens && M * N > 0) {
+    ProfScope ps(ctx, cs, 3, 0.0, (beta == 0.0 ? 16.0 : 24.0) * M * N);
+    launch_undensify((double*)(ws + p.off_cd), M, 1, 0, p.mloc, p.nloc, (int)bs, alpha, beta, C->arena, cs);
+    ++launches;
+    CUDA_TRY(ctx, cudaGetLastError());
+  }
+  if (ctx->nranks > 1) {
+    // events are reusable once the compute stream has passed them; recycle after this call
+    cudaEvent_t done = get_event(ctx);
+    CUDA_TRY(ctx, cudaEventRecord(done, cs));
+    ctx->ev_pool.push_back(ev_ready);
+    for (int s = 0; s < p.L; ++s) {
+      ctx->ev_pool.push_back(ev_x[s]);
+      ctx->ev_pool.push_back(ev_g[s]);
+    }
+    ctx->ev_pool.push_back(done);
+  }
+  ctx->launches += launches;
+  st.kernel_launches = launches;
+  if (stats) *stats = st;
+  return DBM_OK;
+}
+
+// ====================================================================== debug entry points
+extern "C" dbm_status dbm_debug_stacks(dbm_ctx ctx, dbm_matrix A, dbm_matrix B, dbm_matrix C, int step, int32_t cap,
+                                       int32_t* triplets, int64_t* n_entries, int64_t* stack_ptr,
+                                       int64_t* n_stacks) {
+  CTX_OK(ctx);
+  if (dbm_status s = validate(ctx, A, B, C)) return s;
+  ARG_CHECK(n_entries && n_stacks, DBM_ERR_ARG, "null size outputs");
+  const Plan p = make_plan(ctx, A, B, C, false);
+  ARG_CHECK(step >= 0 && step < p.L, DBM_ERR_RANGE, "step out of range");
+  const int64_t capv = cap ? cap : 30000;
+  const int64_t kb = p.kb[p.kappa(step)], nruns = p.mloc * p.nloc, ne = nruns * kb;
+  const int64_t ns = kb == 0 ? 0 : (kb <= capv ? (nruns + capv / kb - 1) / (capv / kb) : nruns * ((kb + capv - 1) / capv));
+  *n_entries = ne;
+  *n_stacks = ns;
+  if (!triplets && !stack_ptr) return DBM_OK;
+  int32_t *d_li = nullptr, *d_trip = nullptr;
+  int64_t* d_ptr = nullptr;
+  CUDA_TRY(ctx, cudaMalloc(&d_li, (size_t)std::max<int64_t>(2 * nruns, 2) * 4));
+  CUDA_TRY(ctx, cudaMalloc(&d_trip, (size_t)std::max<int64_t>(3 * ne, 3) * 4));
+  CUDA_TRY(ctx, cudaMalloc(&d_ptr, (size_t)(ns + 1) * 8));
+  launch_traversal(p.mloc, p.nloc, d_li, d_li + nruns, ctx->stream);
+  launch_stackgen(d_li, d_li + nruns, 0, nruns, kb, p.nloc, kb, p.nloc, d_trip, ctx->stream);
+  launch_stack_ptr(nruns, std::max<int64_t>(kb, 1), capv, ns, d_ptr, ctx->stream);
+  ctx->launches += 3;
+  CUDA_TRY(ctx, cudaGetLastError());
+  if (triplets && ne) CUDA_TRY(ctx, cudaMemcpyAsync(triplets, d_trip, ne * 12, cudaMemcpyDeviceToHost, ctx->stream));
+  if (stack_ptr) CUDA_TRY(ctx, cudaMemcpyAsync(stack_ptr, d_ptr, (ns + 1) * 8, cudaMemcpyDeviceToHost, ctx->stream));
+  CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+  cudaFree(d_li);
+  cudaFree(d_trip);
+  cudaFree(d_ptr);
+  return DBM_OK;
+}
+
+extern "C" dbm_status dbm_debug_dgemm(dbm_ctx ctx, int64_t M, int64_t N, int64_t K, double alpha, const double* At,
+                                      int64_t lda, const double* B, int64_t ldb, double beta, double* C, int64_t ldc,
+                                      int splitk, double* partial, int64_t partial_bytes) {
+  CTX_OK(ctx);
+  ARG_CHECK(M >= 0 && N >= 0 && K >= 0, DBM_ERR_ARG, "negative dimension");
+  ARG_CHECK(lda >= K && ldb >= K && ldc >= M && lda % 2 == 0 && ldb % 2 == 0, DBM_ERR_ARG,
+            "bad leading dimensions (lda, ldb >= K and even; ldc >= M)");
+  ARG_CHECK(M < (1ll << 31) && N < (1ll << 31) && K < (1ll << 31), DBM_ERR_SHAPE, "dimension too large");
+  if (splitk == 0) splitk = pick_splitk(M, N, K, num_sms());
+  ARG_CHECK(splitk >= 1, DBM_ERR_ARG, "bad splitk");
+  if (splitk > 1)
+    ARG_CHECK(partial && partial_bytes >= (int64_t)splitk * M * N * 8, DBM_ERR_WORKSPACE, "partial buffer too small");
+  GemmArgs g{M, N, K, At, lda, B, ldb, C, ldc, alpha, beta, splitk, partial};
+  int launches = 0;
+  {
+    ProfScope ps(ctx, ctx->stream, 0, 2.0 * M * N * K, 8.0 * (M * K + N * K + M * N * (beta != 0 ? 2 : 1)));
+    CUDA_TRY(ctx, launch_dgemm(g, ctx->stream, &launches));
+  }
+  ctx->launches += launches;
+  return DBM_OK;
+}

@@ -1,0 +1,109 @@
+// Internal declarations of libdbm (B200 / sm_100a).  Not part of the ABI.
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "dbm.h"
+
+namespace dbm {
+
+// ----------------------------------------------------------------- errors
+void set_error(const std::string& msg);
+
+// ----------------------------------------------------------------- kernels
+// Counter-based generator, device implementation.
+void launch_fill(double* arena, int64_t mloc, int64_t nloc, int bs, int pr, int pc, int r, int c, uint64_t seed,
+                 uint32_t mat_id, int kind, cudaStream_t st);
+
+// Densify a set of block columns of a local arena (A panels): blocks (li, kcol0 + q*kstride),
+// q < nk, li < mloc, from an arena with nloc block columns.  layout 1 = row-major (K-major, the
+// GEMM's A operand): dense[(li*bs+x)*ld + q*bs+y]; layout 0 = column-major: dense[(q*bs+y)*ld + li*bs+x].
+void launch_densify_cols(const double* arena, int64_t mloc, int64_t nloc, int bs, int64_t kcol0, int64_t kstride,
+                         int64_t nk, double* dense, int64_t ld, int layout, cudaStream_t st);
+// Densify a set of block rows (B panels): blocks (krow0 + q*kstride, lj).  layout 0 = column-major
+// (K-major for B, the GEMM's B operand): dense[(lj*bs+y)*ld + q*bs+x]; layout 1 = row-major.
+void launch_densify_rows(const double* arena, int64_t nloc, int bs, int64_t krow0, int64_t kstride, int64_t nk,
+                         double* dense, int64_t ld, int layout, cudaStream_t st);
+// Undensify with alpha/beta: block(li,lj)(x,y) = alpha*D + beta*block.
+// If nsplit > 1, D is the sum over s of dense + s*split_stride (fixed order s = 0..nsplit-1).
+void launch_undensify(const double* dense, int64_t ld, int nsplit, int64_t split_stride, int64_t mloc, int64_t nloc,
+                      int bs, double alpha, double beta, double* arena, cudaStream_t st);
+// Pack a panel of whole blocks: out slot q*ncols + j <- arena slot (row0 + q*rstride)*ncols + j.
+void launch_pack_rows(const double* arena, int64_t ncols, int bs, int64_t row0, int64_t rstride, int64_t nrows,
+                      double* out, cudaStream_t st);
+void launch_pack_cols(const double* arena, int64_t mloc, int64_t nloc, int bs, int64_t col0, int64_t cstride,
+                      int64_t ncols, double* out, cudaStream_t st);
+
+// Dense FP64 GEMM, both operands K-major (the "TN" form): C(M x N col-major) = alpha * At^T B + beta C.
+struct GemmArgs {
+  int64_t M, N, K;
+  const double* A;  // element (m,k) at A[m*lda + k]
+  int64_t lda;
+  const double* B;  // element (k,n) at B[n*ldb + k]
+  int64_t ldb;
+  double* C;  // element (m,n) at C[m + n*ldc]
+  int64_t ldc;
+  double alpha, beta;
+  int splitk;        // >= 1
+  double* partial;   // splitk*M*N doubles when splitk > 1
+};
+// Returns cudaSuccess or an error (tensor-map encode failures map to cudaErrorInvalidValue).
+cudaError_t launch_dgemm(const GemmArgs& g, cudaStream_t st, int* launches);
+int pick_splitk(int64_t M, int64_t N, int64_t K, int num_sms);
+void launch_splitk_reduce(const double* partial, int splitk, int64_t M, int64_t N, double* C, int64_t ldc,
+                          double alpha, double beta, cudaStream_t st);
+
+// Blocked path: stack generation and the batched small-block GEMM.
+// Traversal order table: run q -> (li, lj) (recursive bisection, reading R6), computed on device.
+void launch_traversal(int64_t mloc, int64_t nloc, int32_t* li_out, int32_t* lj_out, cudaStream_t st);
+// Stack entries for runs [q0, q1): triplets (a,b,c) int32 with a = li*kb+kk, b = kk*nb_ld+lj, c = li*nloc+lj.
+void launch_stackgen(const int32_t* li, const int32_t* lj, int64_t q0, int64_t q1, int64_t kb, int64_t nloc,
+                     int64_t a_ld, int64_t b_ld, int32_t* trip, cudaStream_t st);
+void launch_stack_ptr(int64_t nruns, int64_t kb, int64_t cap, int64_t nstacks, int64_t* ptr, cudaStream_t st);
+// Execute stack entries [e0, e1) (whole C-block runs of length kb, consecutive): for each run,
+// C_blk = (first ? beta*C_blk : C_blk) + alpha*sum_k A_blk*B_blk.
+cudaError_t launch_smm(int bs, const int32_t* trip, int64_t nruns, int64_t kb, const double* A, const double* B,
+                       double* C, double alpha, double beta_first, cudaStream_t st, int* launches);
+
+// ----------------------------------------------------------------- driver
+int num_sms();
+
+}  // namespace dbm
+
+// ----------------------------------------------------------------- handles
+struct dbm_ctx_s {
+  int nranks = 1, rank = 0, pr = 1, pc = 1, myrow = 0, mycol = 0, device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  cudaStream_t comm = nullptr;
+  void* nccl = nullptr;  // ncclComm_t
+  dbm_status poisoned = DBM_OK;
+  int64_t launches = 0;
+  int64_t chunk_bytes = 16ll << 30;  // densified single-rank K-chunk budget (dense A + B)
+  bool profiling = false;
+  struct ProfRec {
+    cudaEvent_t a, b;
+    int kind;
+    double flops, bytes;
+  };
+  std::vector<ProfRec> prof;
+  std::vector<cudaEvent_t> ev_pool;  // free events
+  // pinned staging ring for pageable host copies
+  void* stage[2] = {nullptr, nullptr};
+  size_t stage_bytes = 0;
+  cudaEvent_t stage_ev[2] = {nullptr, nullptr};
+};
+
+struct dbm_matrix_s {
+  dbm_ctx ctx = nullptr;
+  int64_t rows = 0, cols = 0;
+  int bs = 0;
+  int64_t Mb = 0, Nb = 0, mloc = 0, nloc = 0;
+  double* arena = nullptr;
+  int64_t arena_bytes = 0;
+};

@@ -1,0 +1,309 @@
+// dgemm_f64 — the densified path's local multiply (§III, the cublasDgemm role; "better
+// performance by using the well-optimized cuBLAS library ... for multiplication of large blocks").
+//
+// B200 design: FP64 has no tcgen05 kind on sm_100a, so the tensor path is
+// mma.sync.m8n8k4.f64 (SASS DMMA.8x8x4), which shares the FP64 pipe with DFMA (measured 37.1 vs
+// 36.6 TFLOP/s, profiles/r01_fp64_peaks.jsonl).  Operands are both K-major ("TN"), staged by TMA
+// (cp.async.bulk.tensor.2d, SWIZZLE_128B, 16 x 128 boxes) into a STAGES-deep shared-memory ring
+// guarded by mbarriers; one producer warp issues the TMA, 8 consumer warps each own a 64 x 32
+// slice of the 128 x 128 C tile (64 FP64 accumulators per thread) and read fragments with
+// conflict-free LDS.64 thanks to the 128B swizzle.  Split-K with a fixed-order reduction covers
+// thin C (rectangular configs).  Bound: FP64 pipe; 2*M*N*K flops per launch.
+#include <algorithm>
+
+#include "dbm_internal.h"
+
+namespace dbm {
+
+namespace {
+
+constexpr int BM = 128, BN = 128, BK = 16, STAGES = 6;
+constexpr int kConsumerWarps = 8;
+constexpr int kThreads = (kConsumerWarps + 1) * 32;
+constexpr int kStageA = BM * BK * 8;  // 16 KB
+constexpr int kStageB = BN * BK * 8;  // 16 KB
+constexpr int kStage = kStageA + kStageB;
+constexpr size_t kSmem = (size_t)STAGES * kStage + 2 * STAGES * 8 + 1024;
+
+__device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint32_t a, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(a), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t a, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(a), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t a) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(a) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t a, uint32_t parity) {
+  uint32_t done;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(a), "r"(parity)
+        : "memory");
+  } while (!done);
+}
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* tm, int c0, int c1, uint32_t mbar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          dst),
+      "l"((uint64_t)tm), "r"(c0), "r"(c1), "r"(mbar)
+      : "memory");
+}
+__device__ __forceinline__ double lds64(uint32_t addr) {
+  double v;
+  asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+      : "+d"(c[0]), "+d"(c[1])
+      : "d"(a), "d"(b));
+}
+
+__global__ void __launch_bounds__(kThreads, 1)
+    dgemm_tn_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M, int N,
+                    int k_tiles_total, int k_tiles_per_split, int tiles_m, int tiles_n, double* __restrict__ C,
+                    int64_t ldc, double alpha, double beta, double* __restrict__ partial) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint64_t* full = (uint64_t*)(smem + STAGES * kStage);
+  uint64_t* empty = full + STAGES;
+
+  // grouped rasterisation: 8 tile-rows per group so concurrently running CTAs share A and B panels in L2
+  constexpr int GROUP = 8;
+  const int tile = blockIdx.x, split = blockIdx.y;
+  const int span = GROUP * tiles_n;
+  const int first_m = (tile / span) * GROUP;
+  const int gsize = min(tiles_m - first_m, GROUP);
+  const int tm = first_m + (tile % span) % gsize;
+  const int tn = (tile % span) / gsize;
+  const int kt0 = split * k_tiles_per_split;
+  const int nkt = max(0, min(k_tiles_total, kt0 + k_tiles_per_split) - kt0);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(su32(&full[s]), 1);
+      mbar_init(su32(&empty[s]), kConsumerWarps);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  if (warp == kConsumerWarps) {  // ---------------- TMA producer
+    if (lane == 0) {
+      asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&tmA) : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&tmB) : "memory");
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int kt = 0; kt < nkt; ++kt) {
+        mbar_wait(su32(&empty[stage]), phase ^ 1);
+        const uint32_t fb = su32(&full[stage]);
+        mbar_expect_tx(fb, kStage);
+        const uint32_t dst = su32(smem + stage * kStage);
+        tma_load_2d(dst, &tmA, (kt0 + kt) * BK, tm * BM, fb);
+        tma_load_2d(dst + kStageA, &tmB, (kt0 + kt) * BK, tn * BN, fb);
+        if (++stage == STAGES) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+    }
+    return;
+  }
+
+  // ---------------- consumers: warp (wm, wn) owns rows wm*64.., cols wn*32..
+  const int wm = warp >> 2, wn = warp & 3;
+  double acc[8][4][2];
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+  // fragment addressing inside a 128-B-swizzled [rows][16 doubles] box: element (row, k) lives at
+  // row*128 + (((k>>1) ^ (row&7)) << 4) + ((k&1) << 3); row&7 == lane>>2 for every fragment row.
+  const int g = lane >> 2;
+  const uint32_t a_row = (uint32_t)(wm * 64 + g) * 128u;
+  const uint32_t b_row = (uint32_t)(wn * 32 + g) * 128u;
+  uint32_t koff[4];
+#pragma unroll
+  for (int ks = 0; ks < 4; ++ks) koff[ks] = (uint32_t)((((ks * 2 + ((lane & 3) >> 1)) ^ g) << 4) | ((lane & 1) << 3));
+
+  int stage = 0;
+  uint32_t phase = 0;
+  const uint32_t smem_base = su32(smem);
+  for (int kt = 0; kt < nkt; ++kt) {
+    mbar_wait(su32(&full[stage]), phase);
+    const uint32_t sA = smem_base + stage * kStage;
+    const uint32_t sB = sA + kStageA;
+#pragma unroll
+    for (int ks = 0; ks < 4; ++ks) {
+      double a[8], b[4];
+#pragma unroll
+      for (int mi = 0; mi < 8; ++mi) a[mi] = lds64(sA + a_row + mi * 1024 + koff[ks]);
+#pragma unroll
+      for (int ni = 0; ni < 4; ++ni) b[ni] = lds64(sB + b_row + ni * 1024 + koff[ks]);
+#pragma unroll
+      for (int mi = 0; mi < 8; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < 4; ++ni) dmma(acc[mi][ni], a[mi], b[ni]);
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(su32(&empty[stage]));
+    if (++stage == STAGES) {
+      stage = 0;
+      phase ^= 1;
+    }
+  }
+
+  // ---------------- epilogue (C column-major)
+  const int m0 = tm * BM + wm * 64 + g;
+  const int n0 = tn * BN + wn * 32 + (lane & 3) * 2;
+  if (partial) {
+    double* P = partial + (size_t)split * M * N;
+#pragma unroll
+    for (int mi = 0; mi < 8; ++mi) {
+      const int m = m0 + mi * 8;
+      if (m >= M) continue;
+#pragma unroll
+      for (int ni = 0; ni < 4; ++ni)
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          const int n = n0 + ni * 8 + j;
+          if (n < N) P[(size_t)n * M + m] = acc[mi][ni][j];
+        }
+    }
+    return;
+  }
+#pragma unroll
+  for (int mi = 0; mi < 8; ++mi) {
+    const int m = m0 + mi * 8;
+    if (m >= M) continue;
+#pragma unroll
+    for (int ni = 0; ni < 4; ++ni)
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        const int n = n0 + ni * 8 + j;
+        if (n < N) {
+          double* p = C + (size_t)n * ldc + m;
+          double v = alpha * acc[mi][ni][j];
+          if (beta != 0.0) v += beta * *p;
+          *p = v;
+        }
+      }
+  }
+}
+
+__global__ void splitk_reduce_kernel(const double* __restrict__ partial, int splitk, int64_t M, int64_t N,
+                                     double* __restrict__ C, int64_t ldc, double alpha, double beta) {
+  const int64_t total = M * N, MN = M * N;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    double s = partial[e];
+    for (int q = 1; q < splitk; ++q) s += partial[q * MN + e];  // fixed order: deterministic
+    const int64_t n = e / M, m = e - n * M;
+    double* p = C + n * ldc + m;
+    double v = alpha * s;
+    if (beta != 0.0) v += beta * *p;
+    *p = v;
+  }
+}
+
+// ---- tensor maps through the driver entry point (no libcuda link dependency) ----
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = (EncodeTiledFn)p;
+  }
+  return fn;
+}
+
+// K-major operand: rows x K, element (row, k) at base[row*ld + k]; box BK x box_rows, 128B swizzle.
+bool make_kmajor_map(CUtensorMap* tm, const double* base, int64_t rows, int64_t K, int64_t ld, int box_rows) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)std::max<int64_t>(K, 1), (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)ld * 8};
+  cuuint32_t box[2] = {BK, (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, (void*)base, dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+}  // namespace
+
+int pick_splitk(int64_t M, int64_t N, int64_t K, int sms) {
+  const int64_t tiles = ((M + BM - 1) / BM) * ((N + BN - 1) / BN);
+  const int64_t ktiles = (K + BK - 1) / BK;
+  if (tiles >= 4LL * sms || ktiles < 128) return 1;
+  int best = 1;
+  double best_t = 1e300;
+  for (int s = 1; s <= 64; ++s) {
+    if (ktiles / s < 64) break;  // keep >= 1024 of K per split
+    const int64_t ctas = tiles * s;
+    const double waves = (double)((ctas + sms - 1) / sms);
+    const double t = waves / s * (1.0 + 0.002 * s);  // normalised time, mild penalty for reduction traffic
+    if (t < best_t - 1e-12) {
+      best_t = t;
+      best = s;
+    }
+  }
+  return best;
+}
+
+cudaError_t launch_dgemm(const GemmArgs& g, cudaStream_t st, int* launches) {
+  if (g.M <= 0 || g.N <= 0) return cudaSuccess;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(dgemm_tn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  CUtensorMap tmA, tmB;
+  // A zero-K product still needs valid (never dereferenced) maps: point at a 1-column view.
+  if (!make_kmajor_map(&tmA, g.A, g.M, g.K, std::max<int64_t>(g.lda, 2), BM) ||
+      !make_kmajor_map(&tmB, g.B, g.N, g.K, std::max<int64_t>(g.ldb, 2), BN))
+    return cudaErrorInvalidValue;
+  const int tiles_m = (int)((g.M + BM - 1) / BM), tiles_n = (int)((g.N + BN - 1) / BN);
+  const int ktiles = (int)((g.K + BK - 1) / BK);
+  const int splitk = std::max(1, g.splitk);
+  const int per = (ktiles + splitk - 1) / splitk;
+  dim3 grid((unsigned)(tiles_m * tiles_n), (unsigned)splitk);
+  dgemm_tn_kernel<<<grid, kThreads, kSmem, st>>>(tmA, tmB, (int)g.M, (int)g.N, ktiles, std::max(per, 0), tiles_m,
+                                                 tiles_n, g.C, g.ldc, g.alpha, g.beta,
+                                                 splitk > 1 ? g.partial : nullptr);
+  if (launches) ++*launches;
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  if (splitk > 1) {
+    launch_splitk_reduce(g.partial, splitk, g.M, g.N, g.C, g.ldc, g.alpha, g.beta, st);
+    if (launches) ++*launches;
+    e = cudaGetLastError();
+  }
+  return e;
+}
+
+void launch_splitk_reduce(const double* partial, int splitk, int64_t M, int64_t N, double* C, int64_t ldc,
+                          double alpha, double beta, cudaStream_t st) {
+  const int64_t total = M * N;
+  int64_t grid = std::min<int64_t>((total + 255) / 256, (int64_t)num_sms() * 16);
+  splitk_reduce_kernel<<<(unsigned)std::max<int64_t>(grid, 1), 256, 0, st>>>(partial, splitk, M, N, C, ldc, alpha,
+                                                                             beta);
+}
+
+}  // namespace dbm

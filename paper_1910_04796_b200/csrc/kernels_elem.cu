@@ -1,0 +1,232 @@
+// HBM-bound data-movement kernels of the hot path (sm_100a):
+//   fill (synthetic inputs, untimed), densify (§III), undensify with alpha/beta
+//   (§III), panel packing for the blocked path (Cannon panels).
+// Bound: HBM.  Algorithmic bytes: densify 16 B/element, undensify 24 B/element (16 if beta == 0),
+// pack 16 B/element.
+#include <algorithm>
+
+#include "dbm_internal.h"
+
+namespace dbm {
+
+namespace {
+
+constexpr int kThreads = 256;
+
+inline int grid_for(int64_t work, int per_block = kThreads) {
+  int64_t g = (work + per_block - 1) / per_block;
+  int64_t cap = (int64_t)num_sms() * 16;
+  if (g > cap) g = cap;
+  return (int)(g < 1 ? 1 : g);
+}
+
+// ---- counter-based generator, DESIGN.md §4 (device copy of the definition) ----
+__device__ __forceinline__ uint64_t mix64(uint64_t z) {
+  z ^= z >> 30;
+  z *= 0xBF58476D1CE4E5B9ull;
+  z ^= z >> 27;
+  z *= 0x94D049BB133111EBull;
+  z ^= z >> 31;
+  return z;
+}
+
+__global__ void fill_kernel(double* __restrict__ arena, int64_t total, int64_t nloc, int bs, int pr, int pc, int r,
+                            int c, uint64_t key, int kind) {
+  const int64_t bb = (int64_t)bs * bs;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    int64_t slot = e / bb, w = e - slot * bb;
+    int64_t y = w / bs, x = w - y * bs;
+    int64_t li = slot / nloc, lj = slot - li * nloc;
+    uint64_t gi = (uint64_t)((r + li * pr) * bs + x), gj = (uint64_t)((c + lj * pc) * bs + y);
+    uint64_t bits = mix64(key ^ mix64((gi << 32) ^ gj));
+    double v;
+    if (kind == 1) {
+      v = (double)((int)((bits >> 32) % 5u) - 2);
+    } else {
+      double u = __dmul_rn((double)(bits >> 11), 0x1.0p-53);
+      v = __dsub_rn(__dmul_rn(2.0, u), 1.0);
+    }
+    arena[e] = v;
+  }
+}
+
+// ---- densify A panel: blocks (li, kcol0 + q*kstride) -> dense (mloc*bs) x (nk*bs) ----
+// One CTA per (li, group of G consecutive q): stage G blocks in padded shared memory, write
+// rows of G*bs contiguous doubles (layout 1) or copy columns (layout 0).
+template <int G>
+__global__ void densify_cols_kernel(const double* __restrict__ arena, int64_t nloc, int bs, int64_t kcol0,
+                                    int64_t kstride, int64_t nk, double* __restrict__ dense, int64_t ld, int layout) {
+  extern __shared__ double sm[];
+  const int64_t bb = (int64_t)bs * bs;
+  const int pitch = bs + 1;  // padded column pitch (bank-conflict free transpose)
+  const int64_t ngroups = (nk + G - 1) / G;
+  const int64_t li = blockIdx.x / ngroups;
+  const int64_t q0 = (blockIdx.x % ngroups) * G;
+  const int g_n = (int)((nk - q0) < G ? (nk - q0) : G);
+  if (layout == 0) {  // column-major: each block column is a contiguous run of bs doubles
+    for (int g = 0; g < g_n; ++g) {
+      const double* src = arena + (li * nloc + kcol0 + (q0 + g) * kstride) * bb;
+      for (int t = threadIdx.x; t < bb; t += blockDim.x) {
+        int y = t / bs, x = t - y * bs;
+        dense[((q0 + g) * bs + y) * ld + li * bs + x] = src[t];
+      }
+    }
+    return;
+  }
+  for (int g = 0; g < g_n; ++g) {
+    const double* src = arena + (li * nloc + kcol0 + (q0 + g) * kstride) * bb;
+    for (int t = threadIdx.x; t < bb; t += blockDim.x) {
+      int y = t / bs, x = t - y * bs;
+      sm[g * bs * pitch + y * pitch + x] = src[t];
+    }
+  }
+  __syncthreads();
+  const int w = g_n * bs;
+  for (int t = threadIdx.x; t < bs * w; t += blockDim.x) {
+    int x = t / w, v = t - x * w;
+    int g = v / bs, y = v - g * bs;
+    dense[(li * bs + x) * ld + (q0 + g) * bs + y] = sm[g * bs * pitch + y * pitch + x];
+  }
+}
+
+// ---- densify B panel: blocks (krow0 + q*kstride, lj) -> dense (nk*bs) x (nloc*bs) ----
+__global__ void densify_rows_kernel(const double* __restrict__ arena, int64_t nloc, int bs, int64_t krow0,
+                                    int64_t kstride, int64_t nk, double* __restrict__ dense, int64_t ld, int layout) {
+  const int64_t bb = (int64_t)bs * bs;
+  const int64_t rows = nk * bs, total = rows * nloc * bs;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    // layout 0 (column-major): e runs down a dense column; layout 1: along a dense row.
+    int64_t row, col;
+    if (layout == 0) {
+      col = e / rows;
+      row = e - col * rows;
+    } else {
+      const int64_t cols = nloc * bs;
+      row = e / cols;
+      col = e - row * cols;
+    }
+    int64_t q = row / bs, x = row - q * bs, lj = col / bs, y = col - lj * bs;
+    double v = arena[((krow0 + q * kstride) * nloc + lj) * bb + y * bs + x];
+    if (layout == 0)
+      dense[col * ld + row] = v;
+    else
+      dense[row * ld + col] = v;
+  }
+}
+
+// ---- undensify with alpha/beta (and a fixed-order split-K sum) ----
+__global__ void undensify_kernel(const double* __restrict__ dense, int64_t ld, int nsplit, int64_t split_stride,
+                                 int64_t nloc, int bs, int64_t total, double alpha, double beta,
+                                 double* __restrict__ arena) {
+  const int64_t bb = (int64_t)bs * bs;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    int64_t slot = e / bb, w = e - slot * bb;
+    int64_t y = w / bs, x = w - y * bs;
+    int64_t li = slot / nloc, lj = slot - li * nloc;
+    int64_t di = (lj * bs + y) * ld + li * bs + x;
+    double d = dense[di];
+    for (int s = 1; s < nsplit; ++s) d = __dadd_rn(d, dense[di + s * split_stride]);
+    double t = __dmul_rn(alpha, d);
+    arena[e] = (beta == 0.0) ? t : __dadd_rn(t, __dmul_rn(beta, arena[e]));
+  }
+}
+
+// ---- whole-block panel packing (blocked path) ----
+__global__ void pack_blocks_kernel(const double* __restrict__ arena, int64_t nsel, int64_t inner, int64_t outer_stride,
+                                   int64_t sel0, int64_t sel_stride, int bs, int by_rows, int64_t other,
+                                   double* __restrict__ out) {
+  // by_rows: out block (q, j) <- arena block (sel0 + q*sel_stride, j), j < other (row panel of a
+  //          matrix with `other` block columns).
+  // else   : out block (i, q) <- arena block (i, sel0 + q*sel_stride), i < other, with `inner`
+  //          block columns in the arena; out has nsel block columns.
+  const int64_t bb = (int64_t)bs * bs;
+  const int64_t total = nsel * other * bb;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    int64_t slot = e / bb, w = e - slot * bb;
+    int64_t src;
+    if (by_rows) {
+      int64_t q = slot / other, j = slot - q * other;
+      src = ((sel0 + q * sel_stride) * other + j) * bb + w;
+    } else {
+      int64_t i = slot / nsel, q = slot - i * nsel;
+      src = (i * inner + sel0 + q * sel_stride) * bb + w;
+    }
+    out[e] = arena[src];
+  }
+  (void)outer_stride;
+}
+
+}  // namespace
+
+void launch_fill(double* arena, int64_t mloc, int64_t nloc, int bs, int pr, int pc, int r, int c, uint64_t seed,
+                 uint32_t mat_id, int kind, cudaStream_t st) {
+  int64_t total = mloc * nloc * (int64_t)bs * bs;
+  if (total == 0) return;
+  // key = mix64(seed + golden * (mat_id + 1)), computed on the host with the same definition
+  auto hmix = [](uint64_t z) {
+    z ^= z >> 30;
+    z *= 0xBF58476D1CE4E5B9ull;
+    z ^= z >> 27;
+    z *= 0x94D049BB133111EBull;
+    z ^= z >> 31;
+    return z;
+  };
+  uint64_t key = hmix(seed + 0x9E3779B97F4A7C15ull * ((uint64_t)mat_id + 1ull));
+  fill_kernel<<<grid_for(total), kThreads, 0, st>>>(arena, total, nloc, bs, pr, pc, r, c, key, kind);
+}
+
+void launch_densify_cols(const double* arena, int64_t mloc, int64_t nloc, int bs, int64_t kcol0, int64_t kstride,
+                         int64_t nk, double* dense, int64_t ld, int layout, cudaStream_t st) {
+  if (mloc == 0 || nk == 0) return;
+  const int64_t bb = (int64_t)bs * bs;
+  constexpr int G = 8;
+  int g = (int)std::max<int64_t>(1, std::min<int64_t>(G, 6144 / bb));
+  size_t smem = (size_t)g * bs * (bs + 1) * sizeof(double);
+  // template on the maximum group; the kernel uses min(G, remaining) at run time via ngroups
+  // computed from G, so instantiate the actual group size.
+  int64_t grid;
+  switch (g) {
+#define DBM_DC(GG)                                                                                          \
+  case GG:                                                                                                  \
+    grid = mloc * ((nk + GG - 1) / GG);                                                                     \
+    if (smem > 48 * 1024) cudaFuncSetAttribute(densify_cols_kernel<GG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+    densify_cols_kernel<GG><<<(unsigned)grid, kThreads, layout == 1 ? smem : 0, st>>>(arena, nloc, bs, kcol0, \
+                                                                                       kstride, nk, dense, ld, layout); \
+    break;
+    DBM_DC(1) DBM_DC(2) DBM_DC(3) DBM_DC(4) DBM_DC(5) DBM_DC(6) DBM_DC(7) DBM_DC(8)
+#undef DBM_DC
+    default:
+      break;
+  }
+}
+
+void launch_densify_rows(const double* arena, int64_t nloc, int bs, int64_t krow0, int64_t kstride, int64_t nk,
+                         double* dense, int64_t ld, int layout, cudaStream_t st) {
+  int64_t total = nk * bs * nloc * (int64_t)bs;
+  if (total == 0) return;
+  densify_rows_kernel<<<grid_for(total), kThreads, 0, st>>>(arena, nloc, bs, krow0, kstride, nk, dense, ld, layout);
+}
+
+void launch_undensify(const double* dense, int64_t ld, int nsplit, int64_t split_stride, int64_t mloc, int64_t nloc,
+                      int bs, double alpha, double beta, double* arena, cudaStream_t st) {
+  int64_t total = mloc * nloc * (int64_t)bs * bs;
+  if (total == 0) return;
+  undensify_kernel<<<grid_for(total), kThreads, 0, st>>>(dense, ld, nsplit < 1 ? 1 : nsplit, split_stride, nloc, bs,
+                                                         total, alpha, beta, arena);
+}
+
+void launch_pack_rows(const double* arena, int64_t ncols, int bs, int64_t row0, int64_t rstride, int64_t nrows,
+                      double* out, cudaStream_t st) {
+  int64_t total = nrows * ncols * (int64_t)bs * bs;
+  if (total == 0) return;
+  pack_blocks_kernel<<<grid_for(total), kThreads, 0, st>>>(arena, nrows, ncols, 0, row0, rstride, bs, 1, ncols, out);
+}
+
+void launch_pack_cols(const double* arena, int64_t mloc, int64_t nloc, int bs, int64_t col0, int64_t cstride,
+                      int64_t ncols, double* out, cudaStream_t st) {
+  int64_t total = ncols * mloc * (int64_t)bs * bs;
+  if (total == 0) return;
+  pack_blocks_kernel<<<grid_for(total), kThreads, 0, st>>>(arena, ncols, nloc, 0, col0, cstride, bs, 0, mloc, out);
+}
+
+}  // namespace dbm

@@ -1,0 +1,202 @@
+// Blocked path (§II): Traversal -> Generation -> batched small-block GEMM.
+//
+// traversal_kernel: C-block order by recursive bisection (reading R6), one thread per run,
+//   descending the bisection tree (integer; bit-exact vs the oracle).
+// stackgen_kernel: the Generation phase on the GPU: (a_slot, b_slot, c_slot) int32 triplets for a
+//   range of runs (12 B written per entry; HBM/L2 bound).  stack_ptr_kernel writes the <= cap
+//   stack boundaries (greedy whole-run packing, closed form for uniform runs).
+// smm_kernel<BS>: executes consecutive C-block runs of a stack chunk (the LIBCUSMM role).
+#include <algorithm>
+
+#include "dbm_internal.h"
+
+namespace dbm {
+
+namespace {
+
+__global__ void traversal_kernel(int64_t mloc, int64_t nloc, int32_t* __restrict__ li_out,
+                                 int32_t* __restrict__ lj_out) {
+  const int64_t total = mloc * nloc;
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < total; q += (int64_t)gridDim.x * blockDim.x) {
+    int64_t r0 = 0, r1 = mloc, c0 = 0, c1 = nloc, rem = q;
+    while (r1 - r0 > 1 || c1 - c0 > 1) {
+      const int64_t nr = r1 - r0, nc = c1 - c0;
+      if (nr >= nc) {  // split rows (ties go to rows), lower half first
+        const int64_t mid = r0 + nr / 2, first = (mid - r0) * nc;
+        if (rem < first) {
+          r1 = mid;
+        } else {
+          rem -= first;
+          r0 = mid;
+        }
+      } else {
+        const int64_t mid = c0 + nc / 2, first = nr * (mid - c0);
+        if (rem < first) {
+          c1 = mid;
+        } else {
+          rem -= first;
+          c0 = mid;
+        }
+      }
+    }
+    li_out[q] = (int32_t)r0;
+    lj_out[q] = (int32_t)c0;
+  }
+}
+
+__global__ void stackgen_kernel(const int32_t* __restrict__ li, const int32_t* __restrict__ lj, int64_t q0,
+                                int64_t nent, int64_t kb, int64_t nloc, int64_t a_ld, int64_t b_ld,
+                                int32_t* __restrict__ trip) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < nent; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t qq = e / kb, kk = e - qq * kb, q = q0 + qq;
+    const int64_t i = li[q], j = lj[q];
+    trip[3 * e + 0] = (int32_t)(i * a_ld + kk);
+    trip[3 * e + 1] = (int32_t)(kk * b_ld + j);
+    trip[3 * e + 2] = (int32_t)(i * nloc + j);
+  }
+}
+
+__global__ void stack_ptr_kernel(int64_t nruns, int64_t kb, int64_t cap, int64_t nstacks, int64_t* __restrict__ ptr) {
+  const int64_t total = nruns * kb;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t <= nstacks;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    int64_t v;
+    if (kb <= cap) {
+      const int64_t per = cap / kb;  // whole runs per stack
+      v = t * per * kb;
+    } else {
+      const int64_t ns = (kb + cap - 1) / cap;  // stacks per run
+      const int64_t q = t / ns, i = t - q * ns;
+      v = q * kb + (i * cap < kb ? i * cap : kb);
+    }
+    ptr[t] = v < total ? v : total;
+  }
+}
+
+// One CTA per C-block run (grid-stride): stage A and B blocks in shared memory, accumulate in
+// registers, then C = (beta_first == 0 ? 0 : beta_first*C) + alpha*acc.
+template <int BS>
+__global__ void __launch_bounds__(256) smm_kernel(const int32_t* __restrict__ trip, int64_t nruns, int64_t kb,
+                                                  const double* __restrict__ A, const double* __restrict__ B,
+                                                  double* __restrict__ C, double alpha, double beta_first) {
+  constexpr int BB = BS * BS;
+  constexpr int PER = (BB + 255) / 256;
+  extern __shared__ double sm_smm[];
+  double* sA = sm_smm;
+  double* sB = sm_smm + BB;
+  for (int64_t run = blockIdx.x; run < nruns; run += gridDim.x) {
+    double acc[PER];
+#pragma unroll
+    for (int p = 0; p < PER; ++p) acc[p] = 0.0;
+    const int32_t* t = trip + 3 * run * kb;
+    for (int64_t e = 0; e < kb; ++e) {
+      const double* a = A + (int64_t)t[3 * e] * BB;
+      const double* b = B + (int64_t)t[3 * e + 1] * BB;
+      __syncthreads();
+      for (int i = threadIdx.x; i < BB; i += 256) {
+        sA[i] = a[i];
+        sB[i] = b[i];
+      }
+      __syncthreads();
+#pragma unroll
+      for (int p = 0; p < PER; ++p) {
+        const int idx = threadIdx.x + p * 256;
+        if (idx < BB) {
+          const int x = idx % BS, y = idx / BS;
+          double s = acc[p];
+#pragma unroll 8
+          for (int z = 0; z < BS; ++z) s = fma(sA[z * BS + x], sB[y * BS + z], s);
+          acc[p] = s;
+        }
+      }
+    }
+    double* c = C + (int64_t)t[2] * BB;
+#pragma unroll
+    for (int p = 0; p < PER; ++p) {
+      const int idx = threadIdx.x + p * 256;
+      if (idx < BB) c[idx] = (beta_first == 0.0) ? alpha * acc[p] : beta_first * c[idx] + alpha * acc[p];
+    }
+  }
+}
+
+// Generic block size (any bs <= 64): same algorithm, dynamic shared memory.
+__global__ void __launch_bounds__(256) smm_generic_kernel(int bs, const int32_t* __restrict__ trip, int64_t nruns,
+                                                          int64_t kb, const double* __restrict__ A,
+                                                          const double* __restrict__ B, double* __restrict__ C,
+                                                          double alpha, double beta_first) {
+  extern __shared__ double sm[];
+  const int BB = bs * bs;
+  double* sA = sm;
+  double* sB = sm + BB;
+  for (int64_t run = blockIdx.x; run < nruns; run += gridDim.x) {
+    const int32_t* t = trip + 3 * run * kb;
+    double* c = C + (int64_t)t[2] * BB;
+    for (int idx0 = 0; idx0 < BB; idx0 += 256) {
+      const int idx = idx0 + threadIdx.x;
+      double acc = 0.0;
+      for (int64_t e = 0; e < kb; ++e) {
+        const double* a = A + (int64_t)t[3 * e] * BB;
+        const double* b = B + (int64_t)t[3 * e + 1] * BB;
+        __syncthreads();
+        for (int i = threadIdx.x; i < BB; i += 256) {
+          sA[i] = a[i];
+          sB[i] = b[i];
+        }
+        __syncthreads();
+        if (idx < BB) {
+          const int x = idx % bs, y = idx / bs;
+          for (int z = 0; z < bs; ++z) acc = fma(sA[z * bs + x], sB[y * bs + z], acc);
+        }
+      }
+      if (idx < BB) c[idx] = (beta_first == 0.0) ? alpha * acc : beta_first * c[idx] + alpha * acc;
+    }
+  }
+}
+
+inline unsigned grid_of(int64_t n, int per = 256) {
+  int64_t g = (n + per - 1) / per;
+  g = std::min<int64_t>(g, (int64_t)num_sms() * 32);
+  return (unsigned)std::max<int64_t>(g, 1);
+}
+
+}  // namespace
+
+void launch_traversal(int64_t mloc, int64_t nloc, int32_t* li_out, int32_t* lj_out, cudaStream_t st) {
+  if (mloc * nloc == 0) return;
+  traversal_kernel<<<grid_of(mloc * nloc), 256, 0, st>>>(mloc, nloc, li_out, lj_out);
+}
+
+void launch_stackgen(const int32_t* li, const int32_t* lj, int64_t q0, int64_t q1, int64_t kb, int64_t nloc,
+                     int64_t a_ld, int64_t b_ld, int32_t* trip, cudaStream_t st) {
+  const int64_t nent = (q1 - q0) * kb;
+  if (nent <= 0) return;
+  stackgen_kernel<<<grid_of(nent), 256, 0, st>>>(li, lj, q0, nent, kb, nloc, a_ld, b_ld, trip);
+}
+
+void launch_stack_ptr(int64_t nruns, int64_t kb, int64_t cap, int64_t nstacks, int64_t* ptr, cudaStream_t st) {
+  stack_ptr_kernel<<<grid_of(nstacks + 1), 256, 0, st>>>(nruns, kb, cap, nstacks, ptr);
+}
+
+cudaError_t launch_smm(int bs, const int32_t* trip, int64_t nruns, int64_t kb, const double* A, const double* B,
+                       double* C, double alpha, double beta_first, cudaStream_t st, int* launches) {
+  if (nruns <= 0) return cudaSuccess;
+  const unsigned grid = (unsigned)std::min<int64_t>(nruns, (int64_t)num_sms() * 8);
+  if (bs == 22) {
+    smm_kernel<22><<<grid, 256, 2 * 22 * 22 * 8, st>>>(trip, nruns, kb, A, B, C, alpha, beta_first);
+  } else if (bs == 64) {
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(smm_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * 64 * 64 * 8);
+      attr = true;
+    }
+    smm_kernel<64><<<grid, 256, 2 * 64 * 64 * 8, st>>>(trip, nruns, kb, A, B, C, alpha, beta_first);
+  } else {
+    size_t smem = 2 * (size_t)bs * bs * sizeof(double);
+    if (smem > 48 * 1024) cudaFuncSetAttribute(smm_generic_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    smm_generic_kernel<<<grid, 256, smem, st>>>(bs, trip, nruns, kb, A, B, C, alpha, beta_first);
+  }
+  if (launches) ++*launches;
+  return cudaGetLastError();
+}
+
+}  // namespace dbm

@@ -1,0 +1,342 @@
+"""Thin Python binding of libdbm (include/dbm.h): argument marshalling only.
+
+Every step of the multiply runs in the CUDA kernels of libdbm.so; PyTorch provides device memory
+(tensors as arenas and workspace), the stream, and torch.distributed for the NCCL id broadcast.
+There is no fallback: if libdbm.so is missing or a CUDA device is absent, the calls raise.
+Names follow include/dbm.h (dbm_multiply -> multiply, dbm_matrix_fill_random -> Matrix.fill_random ...).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libdbm.so")
+
+PATH_BLOCKED = 0
+PATH_DENSIFIED = 1
+_PATHS = {"blocked": PATH_BLOCKED, "densified": PATH_DENSIFIED, PATH_BLOCKED: 0, PATH_DENSIFIED: 1}
+
+# dbm_ctx_profile_read kernel ids
+K_DGEMM, K_SMM, K_DENSIFY, K_UNDENSIFY, K_STACKGEN = 0, 1, 2, 3, 4
+
+
+class DbmError(RuntimeError):
+    def __init__(self, status: int, name: str, detail: str):
+        super().__init__(f"{name}: {detail}")
+        self.status = status
+        self.name = name
+
+
+class Stats(C.Structure):
+    _fields_ = [("entries", C.c_int64), ("stacks", C.c_int64), ("bytes_sent", C.c_int64),
+                ("bytes_recv", C.c_int64), ("steps", C.c_int64), ("gemm_launches", C.c_int64),
+                ("kernel_launches", C.c_int64), ("flops", C.c_double)]
+
+    def as_dict(self) -> dict:
+        return {f: getattr(self, f) for f, _ in self._fields_}
+
+
+_lib = None
+
+_P = C.c_void_p
+_I64 = C.c_int64
+_SIGS = {
+    "dbm_status_string": (C.c_char_p, [C.c_int]),
+    "dbm_last_error": (C.c_char_p, []),
+    "dbm_unique_id_bytes": (C.c_int, []),
+    "dbm_get_unique_id": (C.c_int, [_P]),
+    "dbm_ctx_create": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, _P, C.c_int, _P, C.POINTER(_P)]),
+    "dbm_ctx_grid": (C.c_int, [_P] + [C.POINTER(C.c_int)] * 4),
+    "dbm_ctx_set_stream": (C.c_int, [_P, _P]),
+    "dbm_ctx_sync": (C.c_int, [_P]),
+    "dbm_ctx_set_profiling": (C.c_int, [_P, C.c_int]),
+    "dbm_ctx_profile_read": (C.c_int, [_P, C.c_int, C.POINTER(C.c_double), C.POINTER(_I64),
+                                       C.POINTER(C.c_double), C.POINTER(C.c_double)]),
+    "dbm_ctx_launch_count": (C.c_int, [_P, C.POINTER(_I64)]),
+    "dbm_ctx_set_dense_chunk_bytes": (C.c_int, [_P, _I64]),
+    "dbm_plan_exchange": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, _I64, _I64, _I64, C.c_int32, C.c_int,
+                                    C.c_int, _P, _P, C.POINTER(C.c_int)]),
+    "dbm_ctx_destroy": (C.c_int, [_P]),
+    "dbm_matrix_create": (C.c_int, [_P, _I64, _I64, C.c_int32, C.POINTER(_P)]),
+    "dbm_matrix_local_info": (C.c_int, [_P, C.POINTER(_I64), C.POINTER(_I64), C.POINTER(_I64)]),
+    "dbm_matrix_local_csr": (C.c_int, [_P, _P, _P, _P]),
+    "dbm_matrix_attach": (C.c_int, [_P, _P, _I64]),
+    "dbm_matrix_fill_random": (C.c_int, [_P, C.c_uint64, C.c_uint32, C.c_int]),
+    "dbm_matrix_set_block": (C.c_int, [_P, _I64, _I64, _P]),
+    "dbm_matrix_get_block": (C.c_int, [_P, _I64, _I64, _P]),
+    "dbm_matrix_upload": (C.c_int, [_P, _P]),
+    "dbm_matrix_download": (C.c_int, [_P, _P]),
+    "dbm_owner_of_block": (C.c_int, [_P, _I64, _I64, C.POINTER(C.c_int)]),
+    "dbm_matrix_destroy": (C.c_int, [_P]),
+    "dbm_multiply_workspace": (C.c_int, [_P, _P, _P, _P, C.c_int, C.POINTER(_I64)]),
+    "dbm_multiply": (C.c_int, [_P, C.c_double, _P, _P, C.c_double, _P, C.c_int, C.c_int32, _P, _I64,
+                               C.POINTER(Stats)]),
+    "dbm_densify": (C.c_int, [_P, _P, _I64, C.c_int]),
+    "dbm_undensify": (C.c_int, [_P, _P, _I64, C.c_double, C.c_double]),
+    "dbm_debug_stacks": (C.c_int, [_P, _P, _P, _P, C.c_int, C.c_int32, _P, C.POINTER(_I64), _P,
+                                   C.POINTER(_I64)]),
+    "dbm_debug_dgemm": (C.c_int, [_P, _I64, _I64, _I64, C.c_double, _P, _I64, _P, _I64, C.c_double, _P, _I64,
+                                  C.c_int, _P, _I64]),
+}
+EXPORTS = tuple(_SIGS)
+
+
+def load(path: str = LIB_PATH):
+    """Load libdbm.so (no fallback: raises if it has not been built)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(path):
+            raise RuntimeError(f"{path} is missing: run `python -m paper_1910_04796_b200.build` "
+                               "(there is no CPU fallback)")
+        lib = C.CDLL(path)
+        for name, (res, args) in _SIGS.items():
+            f = getattr(lib, name)
+            f.restype = res
+            f.argtypes = args
+        _lib = lib
+    return _lib
+
+
+def _check(status: int) -> None:
+    if status != 0:
+        lib = load()
+        raise DbmError(status, lib.dbm_status_string(status).decode(), lib.dbm_last_error().decode())
+
+
+def _stream_ptr(stream) -> int | None:
+    if stream is None:
+        return None
+    return stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
+
+
+# ---------------------------------------------------------------------------- context
+class Context:
+    """dbm_ctx: one rank's view of the Pr x Pc process grid (§II), one rank per GPU."""
+
+    def __init__(self, nranks: int = 1, rank: int = 0, device: int | None = None, pr: int = 0, pc: int = 0,
+                 unique_id: bytes | None = None, stream=None):
+        lib = load()
+        if device is None:
+            device = torch.cuda.current_device()
+        self.device = torch.device("cuda", device)
+        if stream is None:
+            stream = torch.cuda.current_stream(self.device)
+        self.stream = stream
+        h = C.c_void_p()
+        idbuf = C.create_string_buffer(unique_id, len(unique_id)) if unique_id else None
+        _check(lib.dbm_ctx_create(nranks, rank, pr, pc, idbuf, device, _stream_ptr(stream), C.byref(h)))
+        self.h = h
+        self.nranks, self.rank = nranks, rank
+        a = [C.c_int() for _ in range(4)]
+        _check(lib.dbm_ctx_grid(h, *[C.byref(x) for x in a]))
+        self.pr, self.pc, self.myrow, self.mycol = (x.value for x in a)
+        self._ws = None
+
+    @classmethod
+    def from_distributed(cls, stream=None, pr: int = 0, pc: int = 0) -> "Context":
+        """Build a context over torch.distributed's world (NCCL id broadcast from rank 0)."""
+        import torch.distributed as dist
+
+        world, rank = dist.get_world_size(), dist.get_rank()
+        local = int(os.environ.get("LOCAL_RANK", rank % max(torch.cuda.device_count(), 1)))
+        uid = None
+        if world > 1:
+            lib = load()
+            obj = [None]
+            if rank == 0:
+                buf = C.create_string_buffer(lib.dbm_unique_id_bytes())
+                _check(lib.dbm_get_unique_id(buf))
+                obj[0] = buf.raw
+            dist.broadcast_object_list(obj, src=0)
+            uid = obj[0]
+        return cls(world, rank, device=local, pr=pr, pc=pc, unique_id=uid, stream=stream)
+
+    def set_stream(self, stream) -> None:
+        self.stream = stream
+        _check(load().dbm_ctx_set_stream(self.h, _stream_ptr(stream)))
+
+    def sync(self) -> None:
+        _check(load().dbm_ctx_sync(self.h))
+
+    def set_profiling(self, on: bool) -> None:
+        _check(load().dbm_ctx_set_profiling(self.h, int(on)))
+
+    def profile_read(self, kernel: int) -> dict:
+        ms, fl, by = C.c_double(), C.c_double(), C.c_double()
+        n = C.c_int64()
+        _check(load().dbm_ctx_profile_read(self.h, kernel, C.byref(ms), C.byref(n), C.byref(fl), C.byref(by)))
+        return {"ms": ms.value, "launches": n.value, "flops": fl.value, "bytes": by.value}
+
+    def set_dense_chunk_bytes(self, nbytes: int) -> None:
+        _check(load().dbm_ctx_set_dense_chunk_bytes(self.h, nbytes))
+
+    def launch_count(self) -> int:
+        n = C.c_int64()
+        _check(load().dbm_ctx_launch_count(self.h, C.byref(n)))
+        return n.value
+
+    def workspace(self, nbytes: int) -> torch.Tensor:
+        """Caller-owned multiply workspace, cached and grown on demand (the paper's memory pool)."""
+        if self._ws is None or self._ws.numel() < nbytes:
+            self._ws = None
+            self._ws = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=self.device)
+        return self._ws
+
+    def release_workspace(self) -> None:
+        self._ws = None
+
+    def close(self) -> None:
+        if getattr(self, "h", None):
+            load().dbm_ctx_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+# ---------------------------------------------------------------------------- matrix
+class Matrix:
+    """dbm_matrix: rows x cols FP64 matrix of bs x bs blocks, block-cyclic over ctx's grid."""
+
+    def __init__(self, ctx: Context, rows: int, cols: int, block_size: int, arena: torch.Tensor | None = None):
+        lib = load()
+        h = C.c_void_p()
+        _check(lib.dbm_matrix_create(ctx.h, rows, cols, block_size, C.byref(h)))
+        self.h, self.ctx = h, ctx
+        self.rows, self.cols, self.bs = rows, cols, block_size
+        ml, nl, nb = C.c_int64(), C.c_int64(), C.c_int64()
+        _check(lib.dbm_matrix_local_info(h, C.byref(ml), C.byref(nl), C.byref(nb)))
+        self.mloc, self.nloc, self.arena_bytes = ml.value, nl.value, nb.value
+        if arena is None:
+            arena = torch.empty(max(self.arena_bytes // 8, 2), dtype=torch.float64, device=ctx.device)
+        self.arena = arena
+        _check(lib.dbm_matrix_attach(h, arena.data_ptr(), arena.numel() * arena.element_size()))
+
+    def fill_random(self, seed: int, mat_id: int, kind: int = 0) -> None:
+        _check(load().dbm_matrix_fill_random(self.h, seed, mat_id, kind))
+
+    def local_csr(self):
+        import numpy as np
+
+        rp = np.empty(self.mloc + 1, dtype=np.int64)
+        ci = np.empty(max(self.mloc * self.nloc, 1), dtype=np.int64)
+        ri = np.empty(max(self.mloc, 1), dtype=np.int64)
+        _check(load().dbm_matrix_local_csr(self.h, rp.ctypes.data, ci.ctypes.data, ri.ctypes.data))
+        return rp, ci[: self.mloc * self.nloc], ri[: self.mloc]
+
+    def set_block(self, bi: int, bj: int, block) -> None:
+        import numpy as np
+
+        b = np.asfortranarray(np.asarray(block, dtype=np.float64))
+        assert b.shape == (self.bs, self.bs)
+        _check(load().dbm_matrix_set_block(self.h, bi, bj, b.ctypes.data))
+
+    def get_block(self, bi: int, bj: int):
+        import numpy as np
+
+        b = np.empty((self.bs, self.bs), dtype=np.float64, order="F")
+        _check(load().dbm_matrix_get_block(self.h, bi, bj, b.ctypes.data))
+        return b
+
+    def upload(self, host: torch.Tensor) -> None:
+        assert host.dtype == torch.float64 and host.numel() * 8 >= self.arena_bytes and host.is_contiguous()
+        _check(load().dbm_matrix_upload(self.h, host.data_ptr()))
+
+    def download(self, host: torch.Tensor) -> None:
+        assert host.dtype == torch.float64 and host.numel() * 8 >= self.arena_bytes and host.is_contiguous()
+        _check(load().dbm_matrix_download(self.h, host.data_ptr()))
+
+    def owner_of_block(self, bi: int, bj: int) -> int:
+        r = C.c_int()
+        _check(load().dbm_owner_of_block(self.h, bi, bj, C.byref(r)))
+        return r.value
+
+    def local_view(self) -> torch.Tensor:
+        """The arena as (mloc*nloc, bs, bs) blocks; block[.., x, y] -> use .transpose for column-major."""
+        n = self.mloc * self.nloc * self.bs * self.bs
+        return self.arena[:n]
+
+    def densify(self, dense: torch.Tensor, ld: int | None = None, layout: int = 0) -> None:
+        if ld is None:
+            ld = self.mloc * self.bs if layout == 0 else self.nloc * self.bs
+        _check(load().dbm_densify(self.h, dense.data_ptr(), ld, layout))
+
+    def undensify(self, dense: torch.Tensor, alpha: float = 1.0, beta: float = 0.0, ld: int | None = None) -> None:
+        if ld is None:
+            ld = self.mloc * self.bs
+        _check(load().dbm_undensify(self.h, dense.data_ptr(), ld, alpha, beta))
+
+    def close(self) -> None:
+        if getattr(self, "h", None):
+            load().dbm_matrix_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+# ---------------------------------------------------------------------------- multiply
+def multiply_workspace(ctx: Context, A: Matrix, B: Matrix, C_: Matrix, path="densified") -> int:
+    n = C.c_int64()
+    _check(load().dbm_multiply_workspace(ctx.h, A.h, B.h, C_.h, _PATHS[path], C.byref(n)))
+    return n.value
+
+
+def multiply(ctx: Context, alpha: float, A: Matrix, B: Matrix, beta: float, C_: Matrix, path="densified",
+             stack_cap: int = 0, workspace: torch.Tensor | None = None) -> dict:
+    """C = alpha*A*B + beta*C (dbm_multiply): Cannon + blocked / densified local multiply."""
+    lib = load()
+    need = multiply_workspace(ctx, A, B, C_, path)
+    ws = workspace if workspace is not None else ctx.workspace(need)
+    st = Stats()
+    _check(lib.dbm_multiply(ctx.h, alpha, A.h, B.h, beta, C_.h, _PATHS[path], stack_cap, ws.data_ptr(),
+                            ws.numel() * ws.element_size(), C.byref(st)))
+    return st.as_dict()
+
+
+def plan_exchange(pr: int, pc: int, myrow: int, mycol: int, Mb: int, Nb: int, Kb: int, bs: int, step: int,
+                  path="densified") -> list[dict]:
+    """Host-only: the send/recv list dbm_multiply issues at Cannon step `step` (dbm_plan_exchange)."""
+    import numpy as np
+
+    lib = load()
+    n = C.c_int(0)
+    _check(lib.dbm_plan_exchange(pr, pc, myrow, mycol, Mb, Nb, Kb, bs, _PATHS[path], step, None, None, C.byref(n)))
+    ops = np.zeros(4 * max(n.value, 1), dtype=np.int32)
+    by = np.zeros(max(n.value, 1), dtype=np.int64)
+    _check(lib.dbm_plan_exchange(pr, pc, myrow, mycol, Mb, Nb, Kb, bs, _PATHS[path], step, ops.ctypes.data,
+                                 by.ctypes.data, C.byref(n)))
+    return [{"send": bool(ops[4 * i]), "operand": "AB"[ops[4 * i + 1]], "peer": int(ops[4 * i + 2]),
+             "kappa": int(ops[4 * i + 3]), "bytes": int(by[i])} for i in range(n.value)]
+
+
+def debug_stacks(ctx: Context, A: Matrix, B: Matrix, C_: Matrix, step: int = 0, cap: int = 0):
+    import numpy as np
+
+    lib = load()
+    ne, ns = C.c_int64(), C.c_int64()
+    _check(lib.dbm_debug_stacks(ctx.h, A.h, B.h, C_.h, step, cap, None, C.byref(ne), None, C.byref(ns)))
+    trip = np.empty(max(3 * ne.value, 3), dtype=np.int32)
+    ptr = np.empty(ns.value + 1, dtype=np.int64)
+    _check(lib.dbm_debug_stacks(ctx.h, A.h, B.h, C_.h, step, cap, trip.ctypes.data, C.byref(ne), ptr.ctypes.data,
+                                C.byref(ns)))
+    return trip[: 3 * ne.value].reshape(ne.value, 3), ptr
+
+
+def debug_dgemm(ctx: Context, M: int, N: int, K: int, alpha: float, At: torch.Tensor, lda: int, B: torch.Tensor,
+                ldb: int, beta: float, Cm: torch.Tensor, ldc: int, splitk: int = 1,
+                partial: torch.Tensor | None = None) -> None:
+    pb = partial.numel() * partial.element_size() if partial is not None else 0
+    _check(load().dbm_debug_dgemm(ctx.h, M, N, K, alpha, At.data_ptr(), lda, B.data_ptr(), ldb, beta,
+                                  Cm.data_ptr(), ldc, splitk, partial.data_ptr() if partial is not None else None,
+                                  pb))

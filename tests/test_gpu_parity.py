@@ -1,0 +1,298 @@
+"""GPU parity: the CUDA path (through the C ABI) against the host oracle, element by element.
+
+Tolerance (north star): normwise relative Frobenius error <= 1e-12 for U[-1,1) inputs; bit-exact
+for integer inputs with dyadic alpha/beta, for every data-movement kernel (fill, densify,
+undensify) and for stack lists.  Single GPU (grid 1x1); the multi-rank path is in
+tests/test_multigpu.py.
+"""
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+SEED = 1910
+TOL = 1e-12
+
+
+@pytest.fixture(scope="module")
+def dbm():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    import paper_1910_04796_b200 as d
+
+    d.load()
+    return d
+
+
+@pytest.fixture(scope="module")
+def ctx(dbm):
+    c = dbm.Context()
+    yield c
+    c.close()
+
+
+def host(t: torch.Tensor) -> np.ndarray:
+    torch.cuda.synchronize()
+    return t.detach().cpu().numpy()
+
+
+def relerr(got, ref):
+    return np.linalg.norm(got - ref) / max(np.linalg.norm(ref), 1e-300)
+
+
+# ------------------------------------------------------------------ data movement (bit-exact)
+@pytest.mark.parametrize("rows,cols,bs,kind", [(352, 352, 22, 0), (128, 192, 64, 1), (15, 21, 3, 0), (0, 44, 22, 0)])
+def test_fill_bit_exact(dbm, ctx, orc, rows, cols, bs, kind):
+    m = dbm.Matrix(ctx, rows, cols, bs)
+    m.fill_random(SEED, 2, kind)
+    got = host(m.arena)[: m.arena_bytes // 8]
+    assert np.array_equal(got, orc.fill_arena(SEED, 2, kind, rows, cols, bs))
+
+
+def test_set_get_block_and_ownership(dbm, ctx):
+    m = dbm.Matrix(ctx, 66, 44, 22)
+    blk = np.arange(22 * 22, dtype=np.float64).reshape(22, 22)
+    m.set_block(2, 1, blk)
+    assert np.array_equal(m.get_block(2, 1), blk)
+    with pytest.raises(dbm.DbmError) as e:
+        m.get_block(3, 0)
+    assert e.value.name == "DBM_ERR_RANGE"
+    assert m.owner_of_block(2, 1) == 0
+    rp, ci, ri = m.local_csr()
+    assert list(rp) == [0, 2, 4, 6] and list(ci) == [0, 1] * 3 and list(ri) == [0, 1, 2]
+
+
+@pytest.mark.parametrize("rows,cols,bs", [(352, 352, 22), (128, 320, 64), (21, 15, 3)])
+@pytest.mark.parametrize("layout", [0, 1])
+def test_densify_bit_exact(dbm, ctx, orc, rows, cols, bs, layout):
+    m = dbm.Matrix(ctx, rows, cols, bs)
+    m.fill_random(SEED, 0, 0)
+    mloc, nloc = rows // bs, cols // bs
+    ld = (mloc * bs + 3) if layout == 0 else (nloc * bs + 5)  # padded leading dimension
+    n = ld * (nloc * bs if layout == 0 else mloc * bs)
+    d = torch.full((n,), float("nan"), dtype=torch.float64, device="cuda")
+    m.densify(d, ld, layout)
+    got = host(d)
+    arena = orc.fill_arena(SEED, 0, 0, rows, cols, bs)
+    ref = orc.densify_cols(arena, mloc, nloc, bs, np.arange(nloc), layout)
+    if layout == 0:
+        got = got.reshape(nloc * bs, ld)[:, : mloc * bs]
+        ref = ref.reshape(nloc * bs, mloc * bs)
+    else:
+        got = got.reshape(mloc * bs, ld)[:, : nloc * bs]
+        ref = ref.reshape(mloc * bs, nloc * bs)
+    assert np.array_equal(got, ref)
+
+
+@pytest.mark.parametrize("alpha,beta", [(1.0, 0.0), (0.75, -1.25), (-2.5, 1.0)])
+def test_undensify_bit_exact(dbm, ctx, orc, alpha, beta):
+    rows, cols, bs = 352, 264, 22
+    m = dbm.Matrix(ctx, rows, cols, bs)
+    m.fill_random(SEED, 2, 0)
+    if beta == 0.0:
+        m.arena.fill_(float("nan"))  # beta == 0 must not read C
+    dense = torch.rand(rows * cols, dtype=torch.float64, device="cuda") * 2 - 1
+    m.undensify(dense, alpha, beta)
+    arena = orc.fill_arena(SEED, 2, 0, rows, cols, bs)
+    orc.undensify(host(dense), rows, rows // bs, cols // bs, bs, alpha, beta, arena)
+    assert np.array_equal(host(m.arena)[: arena.size], arena)
+
+
+# ------------------------------------------------------------------ dense FP64 GEMM kernel
+@pytest.mark.parametrize("M,N,K,splitk", [(128, 128, 16, 1), (352, 352, 352, 1), (200, 136, 50, 1),
+                                          (1, 1, 1, 1), (257, 129, 1000, 1), (300, 200, 4096, 3),
+                                          (128, 64, 0, 1), (704, 384, 7936, 0)])
+def test_dgemm_kernel(dbm, ctx, M, N, K, splitk):
+    g = torch.Generator().manual_seed(M * 7 + N * 3 + K)
+    lda = ldb = K + (K % 2) + 2
+    At = torch.rand(M, lda, dtype=torch.float64, generator=g) * 2 - 1
+    Bt = torch.rand(N, ldb, dtype=torch.float64, generator=g) * 2 - 1
+    Cc = torch.rand(N, M, dtype=torch.float64, generator=g) * 2 - 1  # column-major C (ldc = M)
+    alpha, beta = 0.75, -1.25
+    ref = alpha * (At[:, :K].numpy() @ Bt[:, :K].numpy().T) + beta * Cc.numpy().T
+    dA, dB, dC = At.cuda(), Bt.cuda(), Cc.cuda()
+    part = torch.empty(max(splitk, 64) * M * N + 1, dtype=torch.float64, device="cuda")
+    dbm.debug_dgemm(ctx, M, N, K, alpha, dA, lda, dB, ldb, beta, dC, M, splitk, part)
+    got = host(dC).T
+    assert relerr(got, ref) <= TOL
+    assert np.abs(got - ref).max() <= 1e-13 * max(K, 1)
+
+
+def test_dgemm_integer_exact(dbm, ctx):
+    M, N, K = 333, 190, 2048
+    g = torch.Generator().manual_seed(5)
+    At = torch.randint(-2, 3, (M, K), generator=g).double()
+    Bt = torch.randint(-2, 3, (N, K), generator=g).double()
+    Cc = torch.randint(-2, 3, (N, M), generator=g).double()
+    ref = 0.75 * (At.numpy() @ Bt.numpy().T) - 1.25 * Cc.numpy().T
+    for splitk in (1, 4):
+        dC = Cc.cuda()
+        part = torch.empty(splitk * M * N + 1, dtype=torch.float64, device="cuda")
+        dbm.debug_dgemm(ctx, M, N, K, 0.75, At.cuda(), K, Bt.cuda(), K, -1.25, dC, M, splitk, part)
+        assert np.array_equal(host(dC).T, ref)
+
+
+# ------------------------------------------------------------------ stacks (bit-exact)
+@pytest.mark.parametrize("n,bs,cap", [(352, 22, 30000), (352, 22, 100), (352, 22, 7), (640, 64, 30), (0, 22, 10)])
+def test_stacks_bit_exact(dbm, ctx, orc, n, bs, cap):
+    A, B, C = (dbm.Matrix(ctx, n, n, bs) for _ in range(3))
+    trip, ptr = dbm.debug_stacks(ctx, A, B, C, 0, cap)
+    nb = n // bs
+    rtrip, rptr = orc.stacks(nb, nb, nb, cap)
+    assert np.array_equal(trip, rtrip)
+    assert np.array_equal(ptr, rptr)
+
+
+# ------------------------------------------------------------------ full multiply vs the oracle
+def run_multiply(dbm, ctx, orc, M, N, K, bs, path, alpha, beta, kind=0, cap=0, chunk=None):
+    A, B, C = dbm.Matrix(ctx, M, K, bs), dbm.Matrix(ctx, K, N, bs), dbm.Matrix(ctx, M, N, bs)
+    A.fill_random(SEED, 0, kind)
+    B.fill_random(SEED, 1, kind)
+    C.fill_random(SEED, 2, kind)
+    if chunk is not None:
+        ctx.set_dense_chunk_bytes(chunk)
+    st = dbm.multiply(ctx, alpha, A, B, beta, C, path, cap)
+    if chunk is not None:
+        ctx.set_dense_chunk_bytes(16 << 30)
+    got = host(C.arena)[: C.arena_bytes // 8]
+    Ao, Bo = orc.fill_arena(SEED, 0, kind, M, K, bs), orc.fill_arena(SEED, 1, kind, K, N, bs)
+    Co = orc.fill_arena(SEED, 2, kind, M, N, bs)
+    orc.multiply_blocked(M // bs, N // bs, K // bs, bs, alpha, Ao, Bo, beta, Co)
+    return got, Co, st
+
+
+@pytest.mark.parametrize("path", ["densified", "blocked"])
+@pytest.mark.parametrize("M,N,K,bs", [(352, 352, 352, 22), (128, 192, 256, 64), (66, 110, 44, 22),
+                                      (1408, 704, 2816, 64), (2816, 2816, 2816, 22)])
+def test_multiply_matches_oracle(dbm, ctx, orc, path, M, N, K, bs):
+    got, ref, st = run_multiply(dbm, ctx, orc, M, N, K, bs, path, 0.75, -1.25)
+    assert relerr(got, ref) <= TOL
+    if path == "densified":
+        assert st["entries"] == st["stacks"] == 1  # P:198 batch size 1
+    else:
+        nb = (M // bs) * (N // bs) * (K // bs)
+        assert st["entries"] == nb
+
+
+@pytest.mark.parametrize("path", ["densified", "blocked"])
+def test_multiply_integer_bit_exact(dbm, ctx, orc, path):
+    got, ref, _ = run_multiply(dbm, ctx, orc, 704, 528, 1100, 22, path, 0.75, -1.25, kind=1)
+    assert np.array_equal(got, ref)
+
+
+def test_densified_k_chunking(dbm, ctx, orc):
+    """Single-rank K-chunked densify -> GEMM accumulate (how 63,360^3 fits HBM) equals the oracle."""
+    M = N = 384
+    K, bs = 1280, 64
+    chunk = (M + N) * bs * 8 * 3  # 3 block columns per chunk -> 7 chunks, the last ragged
+    got, ref, st = run_multiply(dbm, ctx, orc, M, N, K, bs, "densified", 0.75, -1.25, chunk=chunk)
+    assert st["gemm_launches"] == 7
+    assert relerr(got, ref) <= TOL
+    got, ref, _ = run_multiply(dbm, ctx, orc, M, N, K, bs, "densified", 0.75, -1.25, kind=1, chunk=chunk)
+    assert np.array_equal(got, ref)
+
+
+def test_identity_and_permutation_routing(dbm, ctx, orc):
+    """A = permutation: C must be an exact row permutation of B (any misrouted block shows)."""
+    n, bs = 352, 22
+    rng = np.random.default_rng(1)
+    perm = rng.permutation(n)
+    P = np.eye(n)[perm]
+    for path in ("densified", "blocked"):
+        A, B, C = dbm.Matrix(ctx, n, n, bs), dbm.Matrix(ctx, n, n, bs), dbm.Matrix(ctx, n, n, bs)
+        A.arena[: n * n].copy_(torch.from_numpy(orc.dense_to_arena(P, bs)))
+        B.fill_random(SEED, 1, 0)
+        dbm.multiply(ctx, 1.0, A, B, 0.0, C, path)
+        got = orc.arena_to_dense(host(C.arena)[: n * n], n // bs, n // bs, bs)
+        Bd = orc.arena_to_dense(orc.fill_arena(SEED, 1, 0, n, n, bs), n // bs, n // bs, bs)
+        assert np.array_equal(got, Bd[perm])
+
+
+def test_alpha_beta_edge_cases(dbm, ctx, orc):
+    n, bs = 176, 22
+    for path in ("densified", "blocked"):
+        A, B, C = dbm.Matrix(ctx, n, n, bs), dbm.Matrix(ctx, n, n, bs), dbm.Matrix(ctx, n, n, bs)
+        # alpha == 0: A and B are not read; C = beta*C exactly
+        A.arena.fill_(float("nan"))
+        B.arena.fill_(float("nan"))
+        C.fill_random(SEED, 2, 0)
+        dbm.multiply(ctx, 0.0, A, B, -1.25, C, path)
+        assert np.array_equal(host(C.arena), -1.25 * orc.fill_arena(SEED, 2, 0, n, n, bs))
+        # beta == 0: C is not read (NaN stays out)
+        A.fill_random(SEED, 0, 0)
+        B.fill_random(SEED, 1, 0)
+        C.arena.fill_(float("nan"))
+        dbm.multiply(ctx, 1.0, A, B, 0.0, C, path)
+        assert not torch.isnan(C.arena).any().item()
+
+
+def test_empty_and_degenerate_shapes(dbm, ctx, orc):
+    for path in ("densified", "blocked"):
+        # K = 0: C = beta*C
+        A, B, C = dbm.Matrix(ctx, 44, 0, 22), dbm.Matrix(ctx, 0, 66, 22), dbm.Matrix(ctx, 44, 66, 22)
+        C.fill_random(SEED, 2, 0)
+        dbm.multiply(ctx, 1.0, A, B, 0.5, C, path)
+        assert np.array_equal(host(C.arena), 0.5 * orc.fill_arena(SEED, 2, 0, 44, 66, 22))
+        # M = 0
+        A, B, C = dbm.Matrix(ctx, 0, 44, 22), dbm.Matrix(ctx, 44, 66, 22), dbm.Matrix(ctx, 0, 66, 22)
+        dbm.multiply(ctx, 1.0, A, B, 0.0, C, path)
+        torch.cuda.synchronize()
+        # single block
+        got, ref, _ = run_multiply(dbm, ctx, orc, 22, 22, 22, 22, path, 0.75, -1.25)
+        assert relerr(got, ref) <= TOL
+
+
+def test_validation_errors_leave_c_untouched(dbm, ctx):
+    A, B, C = dbm.Matrix(ctx, 44, 66, 22), dbm.Matrix(ctx, 44, 66, 22), dbm.Matrix(ctx, 44, 66, 22)
+    C.arena.fill_(3.0)
+    with pytest.raises(dbm.DbmError) as e:
+        dbm.multiply(ctx, 1.0, A, B, 0.0, C)
+    assert e.value.name == "DBM_ERR_SHAPE"
+    B2 = dbm.Matrix(ctx, 66, 66, 22)
+    with pytest.raises(dbm.DbmError) as e:
+        dbm.multiply(ctx, 1.0, A, B2, 0.0, A)
+    assert e.value.name == "DBM_ERR_ALIAS"
+    B3 = dbm.Matrix(ctx, 66, 66, 33)
+    with pytest.raises(dbm.DbmError) as e:
+        dbm.multiply(ctx, 1.0, A, B3, 0.0, C)
+    assert e.value.name in ("DBM_ERR_PARTITION", "DBM_ERR_SHAPE")
+    with pytest.raises(dbm.DbmError) as e:
+        dbm.Matrix(ctx, 45, 44, 22)
+    assert e.value.name == "DBM_ERR_SHAPE"
+    torch.cuda.synchronize()
+    assert (C.arena == 3.0).all().item()
+
+
+def test_determinism(dbm, ctx):
+    n, bs = 1408, 64
+    outs = []
+    for _ in range(2):
+        A, B, C = dbm.Matrix(ctx, n, n, bs), dbm.Matrix(ctx, n, n, bs), dbm.Matrix(ctx, n, n, bs)
+        A.fill_random(SEED, 0, 0)
+        B.fill_random(SEED, 1, 0)
+        C.fill_random(SEED, 2, 0)
+        dbm.multiply(ctx, 0.75, A, B, -1.25, C, "densified")
+        outs.append(host(C.arena).copy())
+    assert np.array_equal(outs[0], outs[1])
+
+
+def test_blocked_vs_densified_agree(dbm, ctx, orc):
+    a, _, _ = run_multiply(dbm, ctx, orc, 704, 704, 704, 22, "blocked", 1.0, 0.0)
+    b, ref, _ = run_multiply(dbm, ctx, orc, 704, 704, 704, 22, "densified", 1.0, 0.0)
+    assert relerr(a, b) <= 2 * TOL
+
+
+def test_host_upload_download_roundtrip(dbm, ctx, orc):
+    m = dbm.Matrix(ctx, 352, 264, 22)
+    x = torch.from_numpy(orc.fill_arena(SEED, 0, 0, 352, 264, 22))
+    m.upload(x)  # pageable: staged through the pinned double buffer
+    y = torch.empty_like(x)
+    m.download(y)
+    assert torch.equal(x, y)
+    xp = x.pin_memory()
+    m.upload(xp)
+    yp = torch.empty_like(x).pin_memory()
+    m.download(yp)
+    ctx.sync()
+    assert torch.equal(x, yp)

@@ -602,8 +602,9 @@ Plan make_plan_raw(int nranks, int pr, int pc, int r, int c, int64_t Mb, int64_t
     p.off_trav = take((size_t)std::max<int64_t>(p.mloc * p.nloc, 1) * 8);
     int64_t maxkb = 1;
     for (int k = 0; k < p.L; ++k) maxkb = std::max(maxkb, p.kb[k]);
-    const int64_t runs = std::max<int64_t>(1, kTripChunkEntries / maxkb);
-    p.trip_cap = std::min<int64_t>(runs, std::max<int64_t>(p.mloc * p.nloc, 1)) * maxkb;
+    // chunks hold whole runs, a multiple of the smm group size (<= 8 runs), at least one group
+    const int64_t runs = std::max<int64_t>(8, kTripChunkEntries / maxkb / 8 * 8);
+    p.trip_cap = std::min<int64_t>(runs, round_up(std::max<int64_t>(p.mloc * p.nloc, 1), 8)) * maxkb;
     p.off_trip = take((size_t)p.trip_cap * 12);
   }
   if (nranks > 1) {
@@ -915,7 +916,8 @@ extern "C" dbm_status dbm_multiply(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_
     } else if (kbk > 0 && p.mloc * p.nloc > 0) {
       // blocked: Generation (stack chunks) -> batched small-block GEMM
       const int64_t nruns = p.mloc * p.nloc;
-      const int64_t runs_per_chunk = std::max<int64_t>(1, p.trip_cap / kbk);
+      const int64_t grp = smm_group_runs((int)bs);
+      const int64_t runs_per_chunk = std::max<int64_t>(grp, p.trip_cap / kbk / grp * grp);
       const int64_t a_ld = kbk;  // A panel is mloc x kb blocks, row-major over (li, kk)
       for (int64_t q0 = 0; q0 < nruns; q0 += runs_per_chunk) {
         const int64_t q1 = std::min(nruns, q0 + runs_per_chunk);

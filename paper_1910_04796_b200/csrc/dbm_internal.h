@@ -69,6 +69,11 @@ void launch_stack_ptr(int64_t nruns, int64_t kb, int64_t cap, int64_t nstacks, i
 // C_blk = (first ? beta*C_blk : C_blk) + alpha*sum_k A_blk*B_blk.
 cudaError_t launch_smm(int bs, const int32_t* trip, int64_t nruns, int64_t kb, const double* A, const double* B,
                        double* C, double alpha, double beta_first, cudaStream_t st, int* launches);
+// DMMA group kernel for bs 22 / 64 (kernels_smm.cu); the generic smm handles other block sizes.
+bool smm_has_tensor_path(int bs);
+int smm_group_runs(int bs);  // runs per CTA group (stack chunks are cut at multiples of it)
+cudaError_t launch_smm_tc(int bs, const int32_t* trip, int64_t nruns, int64_t kb, const double* A, const double* B,
+                          double* C, double alpha, double beta_first, cudaStream_t st);
 
 // ----------------------------------------------------------------- driver
 int num_sms();

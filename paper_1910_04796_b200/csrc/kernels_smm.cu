@@ -1,0 +1,282 @@
+// smm — the blocked path's batched small-block FP64 GEMM (the LIBCUSMM role, §II).
+//
+// Executes a chunk of stacks: consecutive C-block runs, each run = kb entries (a, b, c) with the
+// k-index ascending (stack generator, reading R6); per run C_blk = (first ? beta*C_blk : C_blk) +
+// alpha * sum_k A_blk(a_k) * B_blk(b_k).
+//
+// B200 design: FP64 tensor path = mma.sync.m8n8k4.f64 (DMMA, which shares the FP64
+// pipe with DFMA).  A CTA executes a GROUP of consecutive runs (bs 22: 8 runs, one warp per C block,
+// 24x24 padded = 3x3 DMMA subtiles; bs 64: 2 runs, 2x2 warps of 32x32 per C block).  Runs of a
+// group that share an A (B) block share one staged copy — consecutive runs of the bisection
+// traversal form compact rectangles, so a group of 8 typically stages 6-8 blocks instead of 16.
+// Staged blocks live in a pool of P slots per stage; a group whose distinct blocks exceed P is run
+// as two halves.  The K dimension of a run is the concatenation of its kb blocks (a stage holds KS
+// consecutive k), so k-steps of 4 never pad K; only M, N pad 22 -> 24 (the bs-22 ceiling is
+// (22/24)^2 = 84% of the DMMA peak; bs 64 has none).  cp.async (16 B) stages operands in a 3-deep
+// ring; pitches are chosen so DMMA fragment loads are (near) conflict-free LDS.64.
+#include <algorithm>
+
+#include "dbm_internal.h"
+
+namespace dbm {
+
+namespace {
+
+template <int BS_, int RUNS_, int WRM_, int WRN_, int SM_, int SN_, int KS_, int PA_, int PB_, int P_>
+struct SmmCfg {
+  static constexpr int BS = BS_, BB = BS_ * BS_;
+  static constexpr int RUNS = RUNS_;            // runs (C blocks) per group
+  static constexpr int WRM = WRM_, WRN = WRN_;  // warps per run (m x n)
+  static constexpr int SM = SM_, SN = SN_;      // 8x8 DMMA subtiles per warp (m x n)
+  static constexpr int KS = KS_;                // k values per stage (multiple of 4)
+  static constexpr int PA = PA_, PB = PB_;      // A: [k][PA] rows contiguous; B: [n][PB] k contiguous
+  static constexpr int P = P_;                  // pool slots per stage (A and B blocks share them)
+  static constexpr int WARPS = RUNS * WRM * WRN;
+  static constexpr int THREADS = WARPS * 32;
+  static constexpr int SLOT = (KS * PA > BS * PB) ? KS * PA : BS * PB;  // doubles
+  static constexpr int PAD_ROWS = SM * 8 * WRM - BS;                  // padded rows read past a slot
+  static constexpr int SLACK = (PAD_ROWS > 0 ? PAD_ROWS : 0) * (PA > PB ? PA : PB) + 8;
+  static constexpr int STAGE = P * SLOT + SLACK;
+  static constexpr int STAGES = 3;
+  static constexpr size_t SMEM = (size_t)STAGES * STAGE * 8;
+  static_assert(KS % 4 == 0 && KS % 2 == 0 && BS % 2 == 0, "16-byte chunks, k-steps of 4");
+  static_assert(SM * 8 * WRM >= BS && SN * 8 * WRN >= BS, "warps cover the block");
+  static_assert(SMEM + 256 <= 232448, "shared memory");
+};
+
+// bs 22: A pitch 22 (3-way LDS conflicts on A, cheap: DMMA-bound), B pitch 44 (conflict-free)
+using Cfg22 = SmmCfg<22, 8, 1, 1, 3, 3, 44, 22, 44, 9>;
+// bs 64: padded pitches 72 / 36 (both conflict-free), half a block of K per stage
+using Cfg64 = SmmCfg<64, 2, 2, 2, 4, 4, 32, 72, 36, 4>;
+
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, int src_bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(src_bytes) : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ double lds64(uint32_t a) {
+  double v;
+  asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+      : "+d"(c[0]), "+d"(c[1])
+      : "d"(a), "d"(b));
+}
+
+// Warp 0: distinct A / B blocks among runs [q0+s0, q0+s0+n) (from their first entries).
+struct Uniq {
+  unsigned lead_a, lead_b, ma, mb;
+  bool act;
+};
+__device__ __forceinline__ Uniq uniq(const int32_t* __restrict__ trip, int64_t q0, int s0, int n, int64_t kb,
+                                     int lane) {
+  Uniq u;
+  u.act = lane < n;
+  const int64_t q = q0 + s0 + lane;
+  const int a = u.act ? trip[3 * (q * kb)] : -1 - lane;
+  const int b = u.act ? trip[3 * (q * kb) + 1] : -1 - lane;
+  u.ma = __match_any_sync(0xffffffffu, a);
+  u.mb = __match_any_sync(0xffffffffu, b);
+  u.lead_a = __ballot_sync(0xffffffffu, u.act && (__ffs(u.ma) - 1) == lane);
+  u.lead_b = __ballot_sync(0xffffffffu, u.act && (__ffs(u.mb) - 1) == lane);
+  return u;
+}
+
+template <class Cfg>
+__global__ void __launch_bounds__(Cfg::THREADS, 1)
+    smm_group_kernel(const int32_t* __restrict__ trip, int64_t nruns, int64_t kb, const double* __restrict__ A,
+                     const double* __restrict__ B, double* __restrict__ C, double alpha, double beta_first) {
+  constexpr int BS = Cfg::BS, BB = Cfg::BB, KS = Cfg::KS, PA = Cfg::PA, PB = Cfg::PB;
+  constexpr int RUNS = Cfg::RUNS, P = Cfg::P, STAGES = Cfg::STAGES, SLOT = Cfg::SLOT;
+  extern __shared__ __align__(16) double smem[];
+  __shared__ int s_rep[P];      // representative run (in group) of each pool slot
+  __shared__ int s_isb[P];      // slot holds a B block (else A)
+  __shared__ int s_ia[RUNS], s_ib[RUNS];
+  __shared__ int s_n, s_ok;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int run_in_group = warp / (Cfg::WRM * Cfg::WRN);
+  const int wsub = warp % (Cfg::WRM * Cfg::WRN);
+  const int wm = wsub / Cfg::WRN, wn = wsub % Cfg::WRN;
+  const int64_t Krun = kb * BS;  // concatenated K of a run
+  const int nst = (int)((Krun + KS - 1) / KS);
+  const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(smem);
+  const int64_t ngroups = (nruns + RUNS - 1) / RUNS;
+  const int g = lane >> 2, t = lane & 3;
+
+  for (int64_t grp = blockIdx.x; grp < ngroups; grp += gridDim.x) {
+    const int64_t q0 = grp * RUNS;
+    const int nrun_g = (int)(nruns - q0 < RUNS ? nruns - q0 : RUNS);
+    // sub-group size: halve until every sub-group's distinct blocks fit the pool
+    int sub = nrun_g;
+    for (;;) {
+      __syncthreads();
+      if (warp == 0) {
+        int ok = 1;
+        for (int s0 = 0; s0 < nrun_g; s0 += sub) {
+          const Uniq u = uniq(trip, q0, s0, min(sub, nrun_g - s0), kb, lane);
+          if (__popc(u.lead_a) + __popc(u.lead_b) > P) ok = 0;
+        }
+        if (lane == 0) s_ok = ok;
+      }
+      __syncthreads();
+      if (s_ok || sub == 1) break;
+      sub = (sub + 1) / 2;
+    }
+
+    for (int s0 = 0; s0 < nrun_g; s0 += sub) {
+      const int n_sub = min(sub, nrun_g - s0);
+      __syncthreads();
+      if (warp == 0) {
+        const Uniq u = uniq(trip, q0, s0, n_sub, kb, lane);
+        const int na = __popc(u.lead_a);
+        if (u.act) {
+          const int la = __ffs(u.ma) - 1, lb = __ffs(u.mb) - 1;
+          const int ia = __popc(u.lead_a & ((1u << la) - 1));
+          const int ib = na + __popc(u.lead_b & ((1u << lb) - 1));
+          s_ia[lane] = ia;
+          s_ib[lane] = ib;
+          if (la == lane) {
+            s_rep[ia] = s0 + lane;
+            s_isb[ia] = 0;
+          }
+          if (lb == lane) {
+            s_rep[ib] = s0 + lane;
+            s_isb[ib] = 1;
+          }
+        }
+        if (lane == 0) s_n = na + __popc(u.lead_b);
+      }
+      __syncthreads();
+      const int nslots = s_n;
+
+      // ---- stage st -> ring slot st % STAGES: every used pool slot, KS k-values of its block(s)
+      auto issue = [&](int st) {
+        if (st < nst) {
+          const uint32_t d0 = sbase + (uint32_t)((st % STAGES) * Cfg::STAGE) * 8u;
+          const int64_t kg0 = (int64_t)st * KS;
+          constexpr int CA = KS * (BS / 2);  // 16-B chunks of an A slot: KS columns x BS/2
+          constexpr int CB = BS * (KS / 2);  // of a B slot: BS rows x KS/2
+          static_assert(CA == CB, "equal chunk counts");
+          const int total = nslots * CA;
+          for (int c = threadIdx.x; c < total; c += Cfg::THREADS) {
+            const int u = c / CA, rem = c - u * CA;
+            const int64_t q = q0 + s_rep[u];
+            uint32_t dst;
+            const double* src;
+            int64_t kg;
+            if (!s_isb[u]) {  // A: column k (kg), rows 2p, 2p+1
+              const int k = rem / (BS / 2), p = rem - k * (BS / 2);
+              kg = kg0 + k;
+              dst = d0 + (uint32_t)(u * SLOT + k * PA + 2 * p) * 8u;
+              const int64_t kk = kg / BS, x = kg - kk * BS;
+              src = (kg < Krun) ? A + (int64_t)trip[3 * (q * kb + kk)] * BB + x * BS + 2 * p : A;
+            } else {  // B: row (column of the block) y, k = 2p, 2p+1
+              const int y = rem / (KS / 2), p = rem - y * (KS / 2);
+              kg = kg0 + 2 * p;
+              dst = d0 + (uint32_t)(u * SLOT + y * PB + 2 * p) * 8u;
+              const int64_t kk = kg / BS, x = kg - kk * BS;
+              src = (kg < Krun) ? B + (int64_t)trip[3 * (q * kb + kk) + 1] * BB + y * BS + x : B;
+            }
+            cp_async16(dst, src, kg < Krun ? 16 : 0);  // zero-fill past the run's K
+          }
+        }
+        cp_commit();
+      };
+
+      const int my = run_in_group - s0;
+      const bool active = my >= 0 && my < n_sub;
+      double acc[Cfg::SM][Cfg::SN][2];
+#pragma unroll
+      for (int i = 0; i < Cfg::SM; ++i)
+#pragma unroll
+        for (int j = 0; j < Cfg::SN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+      const int ia = active ? s_ia[my] : 0, ib = active ? s_ib[my] : 0;
+      // fragments: A (k, m) at slot ia: k*PA + m; B (k, n) at slot ib: n*PB + k;
+      // m = wm*SM*8 + mi*8 + g, n = wn*SN*8 + ni*8 + g, k = 4*ks + t
+      const uint32_t offA = (uint32_t)(ia * SLOT + t * PA + wm * Cfg::SM * 8 + g) * 8u;
+      const uint32_t offB = (uint32_t)(ib * SLOT + (wn * Cfg::SN * 8 + g) * PB + t) * 8u;
+
+#pragma unroll
+      for (int st = 0; st < STAGES - 1; ++st) issue(st);
+      for (int st = 0; st < nst; ++st) {
+        cp_wait<STAGES - 2>();
+        __syncthreads();
+        issue(st + STAGES - 1);
+        if (active) {
+          const uint32_t base = sbase + (uint32_t)((st % STAGES) * Cfg::STAGE) * 8u;
+#pragma unroll
+          for (int ks = 0; ks < KS / 4; ++ks) {
+            double a[Cfg::SM], b[Cfg::SN];
+#pragma unroll
+            for (int mi = 0; mi < Cfg::SM; ++mi) a[mi] = lds64(base + offA + (uint32_t)(ks * 4 * PA + mi * 8) * 8u);
+#pragma unroll
+            for (int ni = 0; ni < Cfg::SN; ++ni) b[ni] = lds64(base + offB + (uint32_t)(ks * 4 + ni * 8 * PB) * 8u);
+#pragma unroll
+            for (int mi = 0; mi < Cfg::SM; ++mi)
+#pragma unroll
+              for (int ni = 0; ni < Cfg::SN; ++ni) dmma(acc[mi][ni], a[mi], b[ni]);
+          }
+        }
+      }
+      cp_wait<0>();
+      // ---- epilogue: this warp's part of its run's C block
+      if (active) {
+        const int64_t q = q0 + run_in_group;
+        double* cb = C + (int64_t)trip[3 * (q * kb) + 2] * BB;
+#pragma unroll
+        for (int mi = 0; mi < Cfg::SM; ++mi) {
+          const int m = wm * Cfg::SM * 8 + mi * 8 + g;
+#pragma unroll
+          for (int ni = 0; ni < Cfg::SN; ++ni)
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+              const int n = wn * Cfg::SN * 8 + ni * 8 + 2 * t + j;
+              if (m < BS && n < BS) {
+                double* p = cb + m + n * BS;
+                const double v = alpha * acc[mi][ni][j];
+                *p = (beta_first == 0.0) ? v : beta_first * *p + v;
+              }
+            }
+        }
+      }
+    }
+  }
+}
+
+template <class Cfg>
+cudaError_t launch_group(const int32_t* trip, int64_t nruns, int64_t kb, const double* A, const double* B, double* C,
+                         double alpha, double beta_first, cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(smm_group_kernel<Cfg>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)Cfg::SMEM);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  const int64_t ngroups = (nruns + Cfg::RUNS - 1) / Cfg::RUNS;
+  const unsigned grid = (unsigned)std::min<int64_t>(ngroups, (int64_t)num_sms());
+  smm_group_kernel<Cfg><<<grid, Cfg::THREADS, Cfg::SMEM, st>>>(trip, nruns, kb, A, B, C, alpha, beta_first);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+bool smm_has_tensor_path(int bs) { return bs == 22 || bs == 64; }
+
+int smm_group_runs(int bs) { return bs == 22 ? Cfg22::RUNS : (bs == 64 ? Cfg64::RUNS : 1); }
+
+cudaError_t launch_smm_tc(int bs, const int32_t* trip, int64_t nruns, int64_t kb, const double* A, const double* B,
+                          double* C, double alpha, double beta_first, cudaStream_t st) {
+  if (nruns <= 0 || kb <= 0) return cudaSuccess;
+  if (bs == 22) return launch_group<Cfg22>(trip, nruns, kb, A, B, C, alpha, beta_first, st);
+  if (bs == 64) return launch_group<Cfg64>(trip, nruns, kb, A, B, C, alpha, beta_first, st);
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace dbm

@@ -5,7 +5,7 @@
 // stackgen_kernel: the Generation phase on the GPU: (a_slot, b_slot, c_slot) int32 triplets for a
 //   range of runs (12 B written per entry; HBM/L2 bound).  stack_ptr_kernel writes the <= cap
 //   stack boundaries (greedy whole-run packing, closed form for uniform runs).
-// smm_kernel<BS>: executes consecutive C-block runs of a stack chunk (the LIBCUSMM role).
+// smm_generic_kernel: block sizes other than 22 / 64 (the DMMA group kernel is kernels_smm.cu).
 #include <algorithm>
 
 #include "dbm_internal.h"
@@ -73,52 +73,6 @@ __global__ void stack_ptr_kernel(int64_t nruns, int64_t kb, int64_t cap, int64_t
   }
 }
 
-// One CTA per C-block run (grid-stride): stage A and B blocks in shared memory, accumulate in
-// registers, then C = (beta_first == 0 ? 0 : beta_first*C) + alpha*acc.
-template <int BS>
-__global__ void __launch_bounds__(256) smm_kernel(const int32_t* __restrict__ trip, int64_t nruns, int64_t kb,
-                                                  const double* __restrict__ A, const double* __restrict__ B,
-                                                  double* __restrict__ C, double alpha, double beta_first) {
-  constexpr int BB = BS * BS;
-  constexpr int PER = (BB + 255) / 256;
-  extern __shared__ double sm_smm[];
-  double* sA = sm_smm;
-  double* sB = sm_smm + BB;
-  for (int64_t run = blockIdx.x; run < nruns; run += gridDim.x) {
-    double acc[PER];
-#pragma unroll
-    for (int p = 0; p < PER; ++p) acc[p] = 0.0;
-    const int32_t* t = trip + 3 * run * kb;
-    for (int64_t e = 0; e < kb; ++e) {
-      const double* a = A + (int64_t)t[3 * e] * BB;
-      const double* b = B + (int64_t)t[3 * e + 1] * BB;
-      __syncthreads();
-      for (int i = threadIdx.x; i < BB; i += 256) {
-        sA[i] = a[i];
-        sB[i] = b[i];
-      }
-      __syncthreads();
-#pragma unroll
-      for (int p = 0; p < PER; ++p) {
-        const int idx = threadIdx.x + p * 256;
-        if (idx < BB) {
-          const int x = idx % BS, y = idx / BS;
-          double s = acc[p];
-#pragma unroll 8
-          for (int z = 0; z < BS; ++z) s = fma(sA[z * BS + x], sB[y * BS + z], s);
-          acc[p] = s;
-        }
-      }
-    }
-    double* c = C + (int64_t)t[2] * BB;
-#pragma unroll
-    for (int p = 0; p < PER; ++p) {
-      const int idx = threadIdx.x + p * 256;
-      if (idx < BB) c[idx] = (beta_first == 0.0) ? alpha * acc[p] : beta_first * c[idx] + alpha * acc[p];
-    }
-  }
-}
-
 // Generic block size (any bs <= 64): same algorithm, dynamic shared memory.
 __global__ void __launch_bounds__(256) smm_generic_kernel(int bs, const int32_t* __restrict__ trip, int64_t nruns,
                                                           int64_t kb, const double* __restrict__ A,
@@ -181,15 +135,9 @@ cudaError_t launch_smm(int bs, const int32_t* trip, int64_t nruns, int64_t kb, c
                        double* C, double alpha, double beta_first, cudaStream_t st, int* launches) {
   if (nruns <= 0) return cudaSuccess;
   const unsigned grid = (unsigned)std::min<int64_t>(nruns, (int64_t)num_sms() * 8);
-  if (bs == 22) {
-    smm_kernel<22><<<grid, 256, 2 * 22 * 22 * 8, st>>>(trip, nruns, kb, A, B, C, alpha, beta_first);
-  } else if (bs == 64) {
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(smm_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * 64 * 64 * 8);
-      attr = true;
-    }
-    smm_kernel<64><<<grid, 256, 2 * 64 * 64 * 8, st>>>(trip, nruns, kb, A, B, C, alpha, beta_first);
+  if (smm_has_tensor_path(bs)) {
+    cudaError_t e = launch_smm_tc(bs, trip, nruns, kb, A, B, C, alpha, beta_first, st);
+    if (e != cudaSuccess) return e;
   } else {
     size_t smem = 2 * (size_t)bs * bs * sizeof(double);
     if (smem > 48 * 1024) cudaFuncSetAttribute(smm_generic_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

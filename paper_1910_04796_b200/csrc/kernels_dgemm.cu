@@ -68,23 +68,34 @@ __device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
 
 __global__ void __launch_bounds__(kThreads, 1)
     dgemm_tn_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M, int N,
-                    int k_tiles_total, int k_tiles_per_split, int tiles_m, int tiles_n, double* __restrict__ C,
+                    int k_tiles_total, int k_tiles_per_split, int nsplit, int tiles_m, int tiles_n,
+                    double* __restrict__ C,
                     int64_t ldc, double alpha, double beta, double* __restrict__ partial) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint64_t* full = (uint64_t*)(smem + STAGES * kStage);
   uint64_t* empty = full + STAGES;
 
-  // grouped rasterisation: 8 tile-rows per group so concurrently running CTAs share A and B panels in L2
-  constexpr int GROUP = 8;
-  const int tile = blockIdx.x, split = blockIdx.y;
-  const int span = GROUP * tiles_n;
-  const int first_m = (tile / span) * GROUP;
-  const int gsize = min(tiles_m - first_m, GROUP);
-  const int tm = first_m + (tile % span) % gsize;
-  const int tn = (tile % span) / gsize;
-  const int kt0 = split * k_tiles_per_split;
-  const int nkt = max(0, min(k_tiles_total, kt0 + k_tiles_per_split) - kt0);
+  // Persistent: CTA b takes work items b, b + grid, ...  All items have equal work, so the CTAs move
+  // through their item lists in lock-step and each "wave" of grid consecutive items runs together.
+  // Items are rasterised in groups of GROUP tile-rows (column-major inside a group), so one wave
+  // is a ~12 x 12 patch of C tiles that streams ~24 A/B panels through L2 at the same k.
+  constexpr int GROUP = 12;
+  const int ntiles = tiles_m * tiles_n;
+  const int nitems = ntiles * nsplit;
+  auto item_coords = [&](int item, int& tm, int& tn, int& split) {
+    split = item / ntiles;
+    const int tile = item - split * ntiles;
+    const int span = GROUP * tiles_n;
+    const int first_m = (tile / span) * GROUP;
+    const int gsize = min(tiles_m - first_m, GROUP);
+    tm = first_m + (tile % span) % gsize;
+    tn = (tile % span) / gsize;
+  };
+  auto item_k = [&](int split, int& kt0, int& nkt) {
+    kt0 = split * k_tiles_per_split;
+    nkt = max(0, min(k_tiles_total, kt0 + k_tiles_per_split) - kt0);
+  };
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
@@ -102,16 +113,21 @@ __global__ void __launch_bounds__(kThreads, 1)
       asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&tmB) : "memory");
       int stage = 0;
       uint32_t phase = 0;
-      for (int kt = 0; kt < nkt; ++kt) {
-        mbar_wait(su32(&empty[stage]), phase ^ 1);
-        const uint32_t fb = su32(&full[stage]);
-        mbar_expect_tx(fb, kStage);
-        const uint32_t dst = su32(smem + stage * kStage);
-        tma_load_2d(dst, &tmA, (kt0 + kt) * BK, tm * BM, fb);
-        tma_load_2d(dst + kStageA, &tmB, (kt0 + kt) * BK, tn * BN, fb);
-        if (++stage == STAGES) {
-          stage = 0;
-          phase ^= 1;
+      for (int item = blockIdx.x; item < nitems; item += gridDim.x) {
+        int tm, tn, split, kt0, nkt;
+        item_coords(item, tm, tn, split);
+        item_k(split, kt0, nkt);
+        for (int kt = 0; kt < nkt; ++kt) {
+          mbar_wait(su32(&empty[stage]), phase ^ 1);
+          const uint32_t fb = su32(&full[stage]);
+          mbar_expect_tx(fb, kStage);
+          const uint32_t dst = su32(smem + stage * kStage);
+          tma_load_2d(dst, &tmA, (kt0 + kt) * BK, tm * BM, fb);
+          tma_load_2d(dst + kStageA, &tmB, (kt0 + kt) * BK, tn * BN, fb);
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
         }
       }
     }
@@ -120,24 +136,35 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   // ---------------- consumers: warp (wm, wn) owns rows wm*64.., cols wn*32..
   const int wm = warp >> 2, wn = warp & 3;
+
+  // Fragment addressing inside a 128-B-swizzled [rows][16 doubles] box: element (row, k) lives at
+  // row*128 + (((k>>1) ^ (row&7)) << 4) + ((k&1) << 3), and row&7 == g = lane>>2 for every fragment
+  // row.  A 64-bit LDS is served per half-warp (g = 0..3 / 4..7), so the MMA k-slot t = lane&3 of
+  // k-step ks reads k = 2*ks + (t&1) + 8*(t>>1): the 16 lanes of a half-warp then hit 16 distinct
+  // 8-byte bank pairs (k ^ 2g distinct), one wavefront per half-warp.  Any fixed k permutation
+  // shared by A and B leaves the product unchanged (the four k-steps cover k = 0..15).
+  const int g = lane >> 2, t = lane & 3;
+  const uint32_t a_row = (uint32_t)(wm * 64 + g) * 128u;
+  const uint32_t b_row = (uint32_t)(wn * 32 + g) * 128u;
+  uint32_t koff[4];
+#pragma unroll
+  for (int ks = 0; ks < 4; ++ks) {
+    const int k = 2 * ks + (t & 1) + 8 * (t >> 1);
+    koff[ks] = (uint32_t)((((k >> 1) ^ g) << 4) | ((k & 1) << 3));
+  }
+
+  int stage = 0;
+  uint32_t phase = 0;
+  const uint32_t smem_base = su32(smem);
+  for (int item = blockIdx.x; item < nitems; item += gridDim.x) {
+  int tm, tn, split, kt0, nkt;
+  item_coords(item, tm, tn, split);
+  item_k(split, kt0, nkt);
   double acc[8][4][2];
 #pragma unroll
   for (int i = 0; i < 8; ++i)
 #pragma unroll
     for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-
-  // fragment addressing inside a 128-B-swizzled [rows][16 doubles] box: element (row, k) lives at
-  // row*128 + (((k>>1) ^ (row&7)) << 4) + ((k&1) << 3); row&7 == lane>>2 for every fragment row.
-  const int g = lane >> 2;
-  const uint32_t a_row = (uint32_t)(wm * 64 + g) * 128u;
-  const uint32_t b_row = (uint32_t)(wn * 32 + g) * 128u;
-  uint32_t koff[4];
-#pragma unroll
-  for (int ks = 0; ks < 4; ++ks) koff[ks] = (uint32_t)((((ks * 2 + ((lane & 3) >> 1)) ^ g) << 4) | ((lane & 1) << 3));
-
-  int stage = 0;
-  uint32_t phase = 0;
-  const uint32_t smem_base = su32(smem);
   for (int kt = 0; kt < nkt; ++kt) {
     mbar_wait(su32(&full[stage]), phase);
     const uint32_t sA = smem_base + stage * kStage;
@@ -179,7 +206,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (n < N) P[(size_t)n * M + m] = acc[mi][ni][j];
         }
     }
-    return;
+    continue;
   }
 #pragma unroll
   for (int mi = 0; mi < 8; ++mi) {
@@ -198,6 +225,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
   }
+  }  // item loop
 }
 
 __global__ void splitk_reduce_kernel(const double* __restrict__ partial, int splitk, int64_t M, int64_t N,
@@ -283,9 +311,10 @@ cudaError_t launch_dgemm(const GemmArgs& g, cudaStream_t st, int* launches) {
   const int ktiles = (int)((g.K + BK - 1) / BK);
   const int splitk = std::max(1, g.splitk);
   const int per = (ktiles + splitk - 1) / splitk;
-  dim3 grid((unsigned)(tiles_m * tiles_n), (unsigned)splitk);
-  dgemm_tn_kernel<<<grid, kThreads, kSmem, st>>>(tmA, tmB, (int)g.M, (int)g.N, ktiles, std::max(per, 0), tiles_m,
-                                                 tiles_n, g.C, g.ldc, g.alpha, g.beta,
+  const int64_t items = (int64_t)tiles_m * tiles_n * splitk;
+  const unsigned grid = (unsigned)std::min<int64_t>(items, num_sms());  // persistent: one CTA per SM
+  dgemm_tn_kernel<<<grid, kThreads, kSmem, st>>>(tmA, tmB, (int)g.M, (int)g.N, ktiles, std::max(per, 0), splitk,
+                                                 tiles_m, tiles_n, g.C, g.ldc, g.alpha, g.beta,
                                                  splitk > 1 ? g.partial : nullptr);
   if (launches) ++*launches;
   cudaError_t e = cudaGetLastError();

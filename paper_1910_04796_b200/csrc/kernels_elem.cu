@@ -156,6 +156,97 @@ __global__ void pack_blocks_kernel(const double* __restrict__ arena, int64_t nse
   (void)outer_stride;
 }
 
+// ---- fast paths for the paper's block sizes (compile-time BS: no 64-bit divisions, 16-B accesses) ----
+// B panel, column-major: dense[(lj*BS+y)*ld + q*BS+x] = block(krow0+q*kstride, lj)[x + y*BS].
+// One thread per (x, x+1) pair; CTAs walk blocks b = q*nloc + lj (block-contiguous reads,
+// column-run writes of BS doubles).
+template <int BS>
+__global__ void __launch_bounds__(256) densify_b_fast(const double* __restrict__ arena, int nloc, int64_t krow0,
+                                                      int64_t kstride, int nblk, double* __restrict__ dense,
+                                                      int64_t ld) {
+  constexpr int BB = BS * BS, PAIRS = BB / 2;
+  for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < (int64_t)nblk * PAIRS;
+       w += (int64_t)gridDim.x * blockDim.x) {
+    const int b = (int)(w / PAIRS), i = 2 * (int)(w - (int64_t)b * PAIRS);
+    const int q = b / nloc, lj = b - q * nloc;
+    const int y = i / BS, x = i - y * BS;
+    const double2 v = *(const double2*)(arena + ((krow0 + q * kstride) * nloc + lj) * BB + i);
+    *(double2*)(dense + ((int64_t)lj * BS + y) * ld + (int64_t)q * BS + x) = v;
+  }
+}
+
+// A panel, row-major (K-major): dense[(li*BS+x)*ld + q*BS+y] = block(li, kcol0+q*kstride)[x + y*BS].
+// A CTA stages G blocks of one block row in shared memory (pitch BS+1) and writes G*BS-long rows.
+template <int BS, int G>
+__global__ void __launch_bounds__(256) densify_a_fast(const double* __restrict__ arena, int64_t nloc, int64_t kcol0,
+                                                      int64_t kstride, int64_t nk, double* __restrict__ dense,
+                                                      int64_t ld) {
+  constexpr int BB = BS * BS, PITCH = BS + 1;
+  __shared__ double sm[G * BS * PITCH];
+  const int64_t ngroups = (nk + G - 1) / G;
+  const int64_t li = blockIdx.x / ngroups, q0 = (blockIdx.x % ngroups) * G;
+  const int gn = (int)(nk - q0 < G ? nk - q0 : G);
+  for (int g = 0; g < gn; ++g) {
+    const double* src = arena + (li * nloc + kcol0 + (q0 + g) * kstride) * BB;
+    for (int i = 2 * threadIdx.x; i < BB; i += 2 * blockDim.x) {
+      const double2 v = *(const double2*)(src + i);
+      const int y = i / BS, x = i - y * BS;  // x even: (x, y) and (x+1, y)
+      sm[g * BS * PITCH + y * PITCH + x] = v.x;
+      sm[g * BS * PITCH + y * PITCH + x + 1] = v.y;
+    }
+  }
+  __syncthreads();
+  const int w = gn * BS;  // row segment length (even)
+  for (int i = 2 * threadIdx.x; i < BS * w; i += 2 * blockDim.x) {
+    const int x = i / w, v = i - x * w;  // v even, (v, v+1) inside one block (BS even)
+    const int g = v / BS, y = v - g * BS;
+    double2 o;
+    o.x = sm[g * BS * PITCH + y * PITCH + x];
+    o.y = sm[g * BS * PITCH + (y + 1) * PITCH + x];
+    *(double2*)(dense + (li * BS + x) * ld + q0 * BS + v) = o;
+  }
+}
+
+// Undensify with alpha/beta: block b = (li, lj), pair (x, x+1) of column y.
+template <int BS>
+__global__ void __launch_bounds__(256) undensify_fast(const double* __restrict__ dense, int64_t ld, int nsplit,
+                                                      int64_t split_stride, int nloc, int nblk, double alpha,
+                                                      double beta, double* __restrict__ arena) {
+  constexpr int BB = BS * BS, PAIRS = BB / 2;
+  for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < (int64_t)nblk * PAIRS;
+       w += (int64_t)gridDim.x * blockDim.x) {
+    const int b = (int)(w / PAIRS), i = 2 * (int)(w - (int64_t)b * PAIRS);
+    const int li = b / nloc, lj = b - li * nloc;
+    const int y = i / BS, x = i - y * BS;
+    const int64_t di = ((int64_t)lj * BS + y) * ld + (int64_t)li * BS + x;
+    double2 d = *(const double2*)(dense + di);
+    for (int s = 1; s < nsplit; ++s) {
+      const double2 e = *(const double2*)(dense + di + s * split_stride);
+      d.x = __dadd_rn(d.x, e.x);
+      d.y = __dadd_rn(d.y, e.y);
+    }
+    double2* p = (double2*)(arena + (int64_t)b * BB + i);
+    double2 o;
+    o.x = __dmul_rn(alpha, d.x);
+    o.y = __dmul_rn(alpha, d.y);
+    if (beta != 0.0) {
+      const double2 c = *p;
+      o.x = __dadd_rn(o.x, __dmul_rn(beta, c.x));
+      o.y = __dadd_rn(o.y, __dmul_rn(beta, c.y));
+    }
+    *p = o;
+  }
+}
+
+inline bool fast_ok(int bs, int64_t ld, const void* a, const void* b) {
+  return (bs == 22 || bs == 64) && ld % 2 == 0 && ((uintptr_t)a & 15) == 0 && ((uintptr_t)b & 15) == 0;
+}
+
+inline unsigned grid_pairs(int64_t pairs) {
+  int64_t g = (pairs + 255) / 256;
+  return (unsigned)std::max<int64_t>(1, std::min<int64_t>(g, (int64_t)num_sms() * 32));
+}
+
 }  // namespace
 
 void launch_fill(double* arena, int64_t mloc, int64_t nloc, int bs, int pr, int pc, int r, int c, uint64_t seed,
@@ -178,6 +269,17 @@ void launch_fill(double* arena, int64_t mloc, int64_t nloc, int bs, int pr, int 
 void launch_densify_cols(const double* arena, int64_t mloc, int64_t nloc, int bs, int64_t kcol0, int64_t kstride,
                          int64_t nk, double* dense, int64_t ld, int layout, cudaStream_t st) {
   if (mloc == 0 || nk == 0) return;
+  if (layout == 1 && fast_ok(bs, ld, arena, dense) && mloc * nk < (1ll << 31)) {
+    if (bs == 22) {
+      constexpr int G = 8;  // 176-double rows, 8 x 22 x 23 x 8 B = 32 KB of smem
+      densify_a_fast<22, G><<<(unsigned)(mloc * ((nk + G - 1) / G)), 256, 0, st>>>(arena, nloc, kcol0, kstride, nk,
+                                                                                 dense, ld);
+    } else {
+      constexpr int G = 1;  // 64 x 65 x 8 B = 33 KB
+      densify_a_fast<64, G><<<(unsigned)(mloc * nk), 256, 0, st>>>(arena, nloc, kcol0, kstride, nk, dense, ld);
+    }
+    return;
+  }
   const int64_t bb = (int64_t)bs * bs;
   constexpr int G = 8;
   int g = (int)std::max<int64_t>(1, std::min<int64_t>(G, 6144 / bb));
@@ -204,6 +306,16 @@ void launch_densify_rows(const double* arena, int64_t nloc, int bs, int64_t krow
                          double* dense, int64_t ld, int layout, cudaStream_t st) {
   int64_t total = nk * bs * nloc * (int64_t)bs;
   if (total == 0) return;
+  if (layout == 0 && fast_ok(bs, ld, arena, dense) && nk * nloc < (1ll << 31)) {
+    const int nblk = (int)(nk * nloc);
+    if (bs == 22)
+      densify_b_fast<22><<<grid_pairs((int64_t)nblk * 242), 256, 0, st>>>(arena, (int)nloc, krow0, kstride, nblk,
+                                                                         dense, ld);
+    else
+      densify_b_fast<64><<<grid_pairs((int64_t)nblk * 2048), 256, 0, st>>>(arena, (int)nloc, krow0, kstride, nblk,
+                                                                          dense, ld);
+    return;
+  }
   densify_rows_kernel<<<grid_for(total), kThreads, 0, st>>>(arena, nloc, bs, krow0, kstride, nk, dense, ld, layout);
 }
 
@@ -211,6 +323,17 @@ void launch_undensify(const double* dense, int64_t ld, int nsplit, int64_t split
                       int bs, double alpha, double beta, double* arena, cudaStream_t st) {
   int64_t total = mloc * nloc * (int64_t)bs * bs;
   if (total == 0) return;
+  if (fast_ok(bs, ld, dense, arena) && (nsplit <= 1 || split_stride % 2 == 0) && mloc * nloc < (1ll << 31)) {
+    const int nblk = (int)(mloc * nloc);
+    const int ns = nsplit < 1 ? 1 : nsplit;
+    if (bs == 22)
+      undensify_fast<22><<<grid_pairs((int64_t)nblk * 242), 256, 0, st>>>(dense, ld, ns, split_stride, (int)nloc,
+                                                                          nblk, alpha, beta, arena);
+    else
+      undensify_fast<64><<<grid_pairs((int64_t)nblk * 2048), 256, 0, st>>>(dense, ld, ns, split_stride, (int)nloc,
+                                                                           nblk, alpha, beta, arena);
+    return;
+  }
   undensify_kernel<<<grid_for(total), kThreads, 0, st>>>(dense, ld, nsplit < 1 ? 1 : nsplit, split_stride, nloc, bs,
                                                          total, alpha, beta, arena);
 }

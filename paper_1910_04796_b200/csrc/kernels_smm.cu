@@ -87,52 +87,99 @@ __device__ __forceinline__ Uniq uniq(const int32_t* __restrict__ trip, int64_t q
   return u;
 }
 
+__device__ __forceinline__ void mbar_init(uint32_t a, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(a), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t a) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(a) : "memory");
+}
+// arrive on the mbarrier when all of this thread's prior cp.async have landed
+__device__ __forceinline__ void cp_async_mbar_arrive(uint32_t a) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(a) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t a, uint32_t parity) {
+  uint32_t done;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(a), "r"(parity)
+        : "memory");
+  } while (!done);
+}
+
+// Warp-specialised: warps 0..WARPS-1 compute (one run, or a WRM x WRN share of one), warp WARPS is
+// the producer.  Per stage the producer reads the (slot, kk) block indices from the stack triplets
+// once (one lane each), broadcasts them with shuffles, and issues the 16-B cp.async of every used
+// pool slot; cp.async.mbarrier.arrive marks the stage full.  Consumers release a stage with one
+// mbarrier arrive per warp.  Group metadata (which runs share blocks) is computed by the producer
+// between two CTA barriers at each (sub-)group start.
 template <class Cfg>
-__global__ void __launch_bounds__(Cfg::THREADS, 1)
+__global__ void __launch_bounds__(Cfg::THREADS + 32, 1)
     smm_group_kernel(const int32_t* __restrict__ trip, int64_t nruns, int64_t kb, const double* __restrict__ A,
                      const double* __restrict__ B, double* __restrict__ C, double alpha, double beta_first) {
   constexpr int BS = Cfg::BS, BB = Cfg::BB, KS = Cfg::KS, PA = Cfg::PA, PB = Cfg::PB;
-  constexpr int RUNS = Cfg::RUNS, P = Cfg::P, STAGES = Cfg::STAGES, SLOT = Cfg::SLOT;
+  constexpr int RUNS = Cfg::RUNS, P = Cfg::P, STAGES = Cfg::STAGES, SLOT = Cfg::SLOT, WARPS = Cfg::WARPS;
+  static_assert(KS % BS == 0 || BS % KS == 0, "a stage covers whole blocks or a block divides into stages");
+  constexpr int KKS = (KS % BS == 0) ? KS / BS : 1;  // blocks (k indices kk) touched per stage
+  static_assert(P * KKS <= 32, "one lane per (slot, kk)");
+  constexpr int CA = KS * (BS / 2);  // 16-B chunks per A slot: KS columns x BS/2
+  constexpr int CB = BS * (KS / 2);  // per B slot: BS rows x KS/2
+  static_assert(CA == CB, "equal chunk counts");
   extern __shared__ __align__(16) double smem[];
-  __shared__ int s_rep[P];      // representative run (in group) of each pool slot
-  __shared__ int s_isb[P];      // slot holds a B block (else A)
+  __shared__ __align__(8) uint64_t full[STAGES], empty[STAGES];
+  __shared__ int s_rep[P];  // representative run (in group) of each pool slot
+  __shared__ int s_isb[P];  // slot holds a B block (else A)
   __shared__ int s_ia[RUNS], s_ib[RUNS];
-  __shared__ int s_n, s_ok;
+  __shared__ int s_n, s_sub;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const bool producer = warp == WARPS;
   const int run_in_group = warp / (Cfg::WRM * Cfg::WRN);
   const int wsub = warp % (Cfg::WRM * Cfg::WRN);
   const int wm = wsub / Cfg::WRN, wn = wsub % Cfg::WRN;
-  const int64_t Krun = kb * BS;  // concatenated K of a run
-  const int nst = (int)((Krun + KS - 1) / KS);
+  const int Krun = (int)(kb * BS);  // concatenated K of a run (< 2^31 for every config)
+  const int nst = (Krun + KS - 1) / KS;
   const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(smem);
   const int64_t ngroups = (nruns + RUNS - 1) / RUNS;
   const int g = lane >> 2, t = lane & 3;
 
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init((uint32_t)__cvta_generic_to_shared(&full[s]), 32);
+      mbar_init((uint32_t)__cvta_generic_to_shared(&empty[s]), WARPS);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  int stage = 0;
+  uint32_t phase = 0;
   for (int64_t grp = blockIdx.x; grp < ngroups; grp += gridDim.x) {
     const int64_t q0 = grp * RUNS;
     const int nrun_g = (int)(nruns - q0 < RUNS ? nruns - q0 : RUNS);
-    // sub-group size: halve until every sub-group's distinct blocks fit the pool
-    int sub = nrun_g;
-    for (;;) {
-      __syncthreads();
-      if (warp == 0) {
-        int ok = 1;
+    if (producer) {  // sub-group size: halve until every sub-group's distinct blocks fit the pool
+      int sub = nrun_g;
+      for (;;) {
+        bool ok = true;
         for (int s0 = 0; s0 < nrun_g; s0 += sub) {
           const Uniq u = uniq(trip, q0, s0, min(sub, nrun_g - s0), kb, lane);
-          if (__popc(u.lead_a) + __popc(u.lead_b) > P) ok = 0;
+          if (__popc(u.lead_a) + __popc(u.lead_b) > P) ok = false;
         }
-        if (lane == 0) s_ok = ok;
+        if (ok || sub == 1) break;
+        sub = (sub + 1) / 2;
       }
-      __syncthreads();
-      if (s_ok || sub == 1) break;
-      sub = (sub + 1) / 2;
+      if (lane == 0) s_sub = sub;
     }
+    __syncthreads();
+    const int sub = s_sub;
 
     for (int s0 = 0; s0 < nrun_g; s0 += sub) {
       const int n_sub = min(sub, nrun_g - s0);
-      __syncthreads();
-      if (warp == 0) {
+      if (s0 > 0) __syncthreads();  // every warp finished the previous sub-group
+      if (producer) {
         const Uniq u = uniq(trip, q0, s0, n_sub, kb, lane);
         const int na = __popc(u.lead_a);
         if (u.act) {
@@ -155,40 +202,57 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
       __syncthreads();
       const int nslots = s_n;
 
-      // ---- stage st -> ring slot st % STAGES: every used pool slot, KS k-values of its block(s)
-      auto issue = [&](int st) {
-        if (st < nst) {
-          const uint32_t d0 = sbase + (uint32_t)((st % STAGES) * Cfg::STAGE) * 8u;
-          const int64_t kg0 = (int64_t)st * KS;
-          constexpr int CA = KS * (BS / 2);  // 16-B chunks of an A slot: KS columns x BS/2
-          constexpr int CB = BS * (KS / 2);  // of a B slot: BS rows x KS/2
-          static_assert(CA == CB, "equal chunk counts");
-          const int total = nslots * CA;
-          for (int c = threadIdx.x; c < total; c += Cfg::THREADS) {
-            const int u = c / CA, rem = c - u * CA;
-            const int64_t q = q0 + s_rep[u];
+      if (producer) {
+        // ---------------- producer: nst stages of this sub-group
+        // lane l < nslots*KKS owns (slot u = l / KKS, block kk = kk_first + l % KKS)
+        const int my_u = lane / KKS, my_j = lane - (lane / KKS) * KKS;
+        const bool owner = lane < nslots * KKS;
+        const int64_t my_q = q0 + (owner ? s_rep[my_u] : 0);
+        const int my_col = owner ? s_isb[my_u] : 0;
+        const int total = nslots * CA;
+        for (int st = 0; st < nst; ++st) {
+          mbar_wait((uint32_t)__cvta_generic_to_shared(&empty[stage]), phase ^ 1);
+          const int kg0 = st * KS;
+          const int kk_first = kg0 / BS;
+          int blk = 0;  // block index (slot in its arena) this lane owns for this stage
+          if (owner && kk_first + my_j < kb) blk = trip[3 * (my_q * kb + kk_first + my_j) + my_col];
+          const uint32_t d0 = sbase + (uint32_t)(stage * Cfg::STAGE) * 8u;
+          for (int c0 = 0; c0 < total; c0 += 32) {
+            const int c = c0 + lane;
+            const bool v = c < total;
+            const int u = v ? c / CA : 0, rem = v ? c - u * CA : 0;
+            const bool isb = v && s_isb[u];
+            int kg, off;  // off: doubles within the block; dst in doubles within the stage
             uint32_t dst;
-            const double* src;
-            int64_t kg;
-            if (!s_isb[u]) {  // A: column k (kg), rows 2p, 2p+1
+            if (!isb) {
               const int k = rem / (BS / 2), p = rem - k * (BS / 2);
               kg = kg0 + k;
-              dst = d0 + (uint32_t)(u * SLOT + k * PA + 2 * p) * 8u;
-              const int64_t kk = kg / BS, x = kg - kk * BS;
-              src = (kg < Krun) ? A + (int64_t)trip[3 * (q * kb + kk)] * BB + x * BS + 2 * p : A;
-            } else {  // B: row (column of the block) y, k = 2p, 2p+1
+              off = (kg % BS) * BS + 2 * p;
+              dst = (uint32_t)(u * SLOT + k * PA + 2 * p);
+            } else {
               const int y = rem / (KS / 2), p = rem - y * (KS / 2);
               kg = kg0 + 2 * p;
-              dst = d0 + (uint32_t)(u * SLOT + y * PB + 2 * p) * 8u;
-              const int64_t kk = kg / BS, x = kg - kk * BS;
-              src = (kg < Krun) ? B + (int64_t)trip[3 * (q * kb + kk) + 1] * BB + y * BS + x : B;
+              off = y * BS + kg % BS;
+              dst = (uint32_t)(u * SLOT + y * PB + 2 * p);
             }
-            cp_async16(dst, src, kg < Krun ? 16 : 0);  // zero-fill past the run's K
+            const int src_lane = u * KKS + (kg / BS - kk_first);
+            const int b = __shfl_sync(0xffffffffu, blk, src_lane & 31);
+            if (v) {
+              const bool in = kg < Krun;
+              const double* src = (isb ? B : A) + (in ? (int64_t)b * BB + off : 0);
+              cp_async16(d0 + dst * 8u, src, in ? 16 : 0);  // zero-fill past the run's K
+            }
+          }
+          cp_async_mbar_arrive((uint32_t)__cvta_generic_to_shared(&full[stage]));
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
           }
         }
-        cp_commit();
-      };
+        continue;
+      }
 
+      // ---------------- consumers
       const int my = run_in_group - s0;
       const bool active = my >= 0 && my < n_sub;
       double acc[Cfg::SM][Cfg::SN][2];
@@ -201,15 +265,10 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
       // m = wm*SM*8 + mi*8 + g, n = wn*SN*8 + ni*8 + g, k = 4*ks + t
       const uint32_t offA = (uint32_t)(ia * SLOT + t * PA + wm * Cfg::SM * 8 + g) * 8u;
       const uint32_t offB = (uint32_t)(ib * SLOT + (wn * Cfg::SN * 8 + g) * PB + t) * 8u;
-
-#pragma unroll
-      for (int st = 0; st < STAGES - 1; ++st) issue(st);
       for (int st = 0; st < nst; ++st) {
-        cp_wait<STAGES - 2>();
-        __syncthreads();
-        issue(st + STAGES - 1);
+        mbar_wait((uint32_t)__cvta_generic_to_shared(&full[stage]), phase);
         if (active) {
-          const uint32_t base = sbase + (uint32_t)((st % STAGES) * Cfg::STAGE) * 8u;
+          const uint32_t base = sbase + (uint32_t)(stage * Cfg::STAGE) * 8u;
 #pragma unroll
           for (int ks = 0; ks < KS / 4; ++ks) {
             double a[Cfg::SM], b[Cfg::SN];
@@ -223,8 +282,13 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
               for (int ni = 0; ni < Cfg::SN; ++ni) dmma(acc[mi][ni], a[mi], b[ni]);
           }
         }
+        __syncwarp();
+        if (lane == 0) mbar_arrive((uint32_t)__cvta_generic_to_shared(&empty[stage]));
+        if (++stage == STAGES) {
+          stage = 0;
+          phase ^= 1;
+        }
       }
-      cp_wait<0>();
       // ---- epilogue: this warp's part of its run's C block
       if (active) {
         const int64_t q = q0 + run_in_group;
@@ -246,6 +310,7 @@ __global__ void __launch_bounds__(Cfg::THREADS, 1)
         }
       }
     }
+    __syncthreads();  // group done: metadata may be rewritten
   }
 }
 
@@ -261,7 +326,7 @@ cudaError_t launch_group(const int32_t* trip, int64_t nruns, int64_t kb, const d
   }
   const int64_t ngroups = (nruns + Cfg::RUNS - 1) / Cfg::RUNS;
   const unsigned grid = (unsigned)std::min<int64_t>(ngroups, (int64_t)num_sms());
-  smm_group_kernel<Cfg><<<grid, Cfg::THREADS, Cfg::SMEM, st>>>(trip, nruns, kb, A, B, C, alpha, beta_first);
+  smm_group_kernel<Cfg><<<grid, Cfg::THREADS + 32, Cfg::SMEM, st>>>(trip, nruns, kb, A, B, C, alpha, beta_first);
   return cudaGetLastError();
 }
 

@@ -63,13 +63,14 @@ def test_set_get_block_and_ownership(dbm, ctx):
     assert list(rp) == [0, 2, 4, 6] and list(ci) == [0, 1] * 3 and list(ri) == [0, 1, 2]
 
 
-@pytest.mark.parametrize("rows,cols,bs", [(352, 352, 22), (128, 320, 64), (21, 15, 3)])
+@pytest.mark.parametrize("rows,cols,bs", [(352, 352, 22), (128, 320, 64), (21, 15, 3), (198, 374, 22)])
 @pytest.mark.parametrize("layout", [0, 1])
-def test_densify_bit_exact(dbm, ctx, orc, rows, cols, bs, layout):
+@pytest.mark.parametrize("pad", [0, 3, 4])  # even ld takes the vectorised fast path for bs 22 / 64
+def test_densify_bit_exact(dbm, ctx, orc, rows, cols, bs, layout, pad):
     m = dbm.Matrix(ctx, rows, cols, bs)
     m.fill_random(SEED, 0, 0)
     mloc, nloc = rows // bs, cols // bs
-    ld = (mloc * bs + 3) if layout == 0 else (nloc * bs + 5)  # padded leading dimension
+    ld = (mloc * bs + pad) if layout == 0 else (nloc * bs + pad)  # padded leading dimension
     n = ld * (nloc * bs if layout == 0 else mloc * bs)
     d = torch.full((n,), float("nan"), dtype=torch.float64, device="cuda")
     m.densify(d, ld, layout)

@@ -1,0 +1,42 @@
+"""Run dbm_multiply once or a few times at a given shape (single GPU), for ncu captures and quick timing.
+
+    python tools/profile_multiply.py --M 5632 --N 5632 --K 5632 --bs 22 --path blocked --reps 2
+"""
+import argparse
+import json
+import os
+import sys
+
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_1910_04796_b200 as dbm  # noqa: E402
+
+
+def main():
+    p = argparse.ArgumentParser()
+    p.add_argument("--M", type=int, default=5632)
+    p.add_argument("--N", type=int, default=5632)
+    p.add_argument("--K", type=int, default=5632)
+    p.add_argument("--bs", type=int, default=22)
+    p.add_argument("--path", default="blocked")
+    p.add_argument("--reps", type=int, default=2)
+    a = p.parse_args()
+    ctx = dbm.Context()
+    A, B, C = dbm.Matrix(ctx, a.M, a.K, a.bs), dbm.Matrix(ctx, a.K, a.N, a.bs), dbm.Matrix(ctx, a.M, a.N, a.bs)
+    A.fill_random(1910, 0, 0)
+    B.fill_random(1910, 1, 0)
+    C.fill_random(1910, 2, 0)
+    for i in range(a.reps):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        st = dbm.multiply(ctx, 1.0, A, B, 0.0, C, a.path)
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1)
+        print(json.dumps({"M": a.M, "N": a.N, "K": a.K, "bs": a.bs, "path": a.path, "rep": i, "ms": ms,
+                          "tflops": 2.0 * a.M * a.N * a.K / ms / 1e9, "entries": st["entries"]}), flush=True)
+
+
+if __name__ == "__main__":
+    main()

@@ -46,6 +46,7 @@ def parse():
     p.add_argument("--config", default="sq64", choices=sorted(CONFIGS))
     p.add_argument("--path", default=None, choices=["densified", "blocked"])
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--transport", default="ce", choices=["ce", "nccl"], help="Cannon panel transport (N>1)")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--e2e-steps", type=int, default=1)
@@ -175,6 +176,7 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
         ctx = dbm.Context.from_distributed()
+        ctx.set_transport(args.transport)
     else:
         ctx = dbm.Context(device=local)
     stream = torch.cuda.current_stream(dev)
@@ -248,6 +250,7 @@ def main():
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": name, "M": M, "N": N, "K": K, "block_size": bs, "path": path,
                        "grid": f"{ctx.pr}x{ctx.pc}", "parallelism": f"cannon{ctx.pr}x{ctx.pc}",
+                       "transport": (args.transport if world > 1 else None),
                        "l2": "inputs >= 8 GB per matrix >> 126 MB L2; no flush", "alpha": alpha, "beta": beta},
             "pct_fp64_peak": 100.0 * tflops / (world * FP64_PEAK_MEASURED),
             "roofline": {"kernel": kern, "bound": "tensor", "achieved": achieved, "peak": FP64_PEAK_MEASURED,

@@ -102,6 +102,13 @@ dbm_status dbm_ctx_sync(dbm_ctx ctx);
 dbm_status dbm_ctx_set_profiling(dbm_ctx ctx, int on);
 dbm_status dbm_ctx_profile_read(dbm_ctx ctx, int kernel, double* ms_out, int64_t* launches_out, double* flops_out,
                                 double* bytes_out);
+/* Cannon panel transport between ranks ("asynchronous point-to-point"):
+ * 0 (default) = DMA copy engines pull each needed panel from its owner's workspace, mapped with CUDA
+ *     IPC, over NVLink (no SM is taken from the local multiply); ordering uses two tiny NCCL
+ *     collectives per multiply.  The workspace must be a cudaMalloc allocation (e.g. a torch tensor).
+ * 1 = NCCL grouped ncclSend / ncclRecv.
+ * Every rank must use the same transport.  Changes dbm_multiply_workspace() for the blocked path. */
+dbm_status dbm_ctx_set_transport(dbm_ctx ctx, int transport);
 /* Densified path on a single rank: byte budget of one K-chunk of dense A + B (default 16 GiB).
  * K is densified and multiplied chunk by chunk (GEMM-accumulate), so 63,360^3 fits in HBM.
  * bytes >= 1; changes dbm_multiply_workspace(). */

@@ -259,6 +259,12 @@ extern "C" dbm_status dbm_ctx_profile_read(dbm_ctx ctx, int kernel, double* ms_o
   return DBM_OK;
 }
 
+extern "C" dbm_status dbm_ctx_set_transport(dbm_ctx ctx, int transport) {
+  ARG_CHECK(ctx && (transport == 0 || transport == 1), DBM_ERR_ARG, "transport must be 0 (copy engine) or 1 (NCCL)");
+  ctx->transport = transport;
+  return DBM_OK;
+}
+
 extern "C" dbm_status dbm_ctx_set_dense_chunk_bytes(dbm_ctx ctx, int64_t bytes) {
   ARG_CHECK(ctx && bytes >= 1, DBM_ERR_ARG, "bad argument");
   ctx->chunk_bytes = bytes;
@@ -285,6 +291,9 @@ extern "C" dbm_status dbm_ctx_destroy(dbm_ctx ctx) {
     if (ctx->stage[i]) cudaFreeHost(ctx->stage[i]);
     if (ctx->stage_ev[i]) cudaEventDestroy(ctx->stage_ev[i]);
   }
+  for (void* b : ctx->peer_bases)
+    if (b) cudaIpcCloseMemHandle(b);
+  if (ctx->d_scratch) cudaFree(ctx->d_scratch);
   if (ctx->nccl) ncclCommDestroy((ncclComm_t)ctx->nccl);
   cudaStreamDestroy(ctx->comm);
   if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
@@ -541,11 +550,13 @@ struct Plan {
 size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 
 constexpr int64_t kDefaultChunkBytes = 16ll << 30;   // A+B dense chunk budget (single rank)
-constexpr int64_t kTripChunkEntries = 1ll << 25;      // 400 MB of triplets per generation chunk
+// Triplets per stack-generation chunk (<= 6.4 GB): large enough that one smm launch has thousands
+// of 8-run groups for 148 SMs even with the 90,112-long runs of the rectangular bs-22 config.
+constexpr int64_t kTripChunkEntries = 1ll << 29;
 
 // Host-only plan: depends on the grid, this rank's coordinates and the block counts (no CUDA).
 Plan make_plan_raw(int nranks, int pr, int pc, int r, int c, int64_t Mb, int64_t Nb, int64_t Kb, int64_t bs,
-                   bool densified, int64_t chunk_bytes) {
+                   bool densified, int64_t chunk_bytes, int transport) {
   Plan p;
   p.pr = pr;
   p.pc = pc;
@@ -594,10 +605,12 @@ Plan make_plan_raw(int nranks, int pr, int pc, int r, int c, int64_t Mb, int64_t
     }
     if (p.max_split > 1) p.off_part = take((size_t)p.max_split * M * N * 8);
   } else {
-    // own panels need packing only when a rank holds more than one panel per operand
+    // own panels need packing when a rank holds more than one panel per operand, and always for the
+    // copy-engine transport (peers pull from this rank's workspace, the IPC-mapped allocation)
+    const bool all = nranks > 1 && transport == 0;
     for (int k = 0; k < p.L; ++k) {
-      if (k % p.pc == p.c && p.L / p.pc > 1) p.ownA_off[k] = take(p.a_panel_bytes(k));
-      if (k % p.pr == p.r && p.L / p.pr > 1) p.ownB_off[k] = take(p.b_panel_bytes(k));
+      if (k % p.pc == p.c && (all || p.L / p.pc > 1)) p.ownA_off[k] = take(p.a_panel_bytes(k));
+      if (k % p.pr == p.r && (all || p.L / p.pr > 1)) p.ownB_off[k] = take(p.b_panel_bytes(k));
     }
     p.off_trav = take((size_t)std::max<int64_t>(p.mloc * p.nloc, 1) * 8);
     int64_t maxkb = 1;
@@ -630,7 +643,7 @@ Plan make_plan_raw(int nranks, int pr, int pc, int r, int c, int64_t Mb, int64_t
 Plan make_plan(dbm_ctx ctx, dbm_matrix A, dbm_matrix B, dbm_matrix C, bool densified) {
   (void)C;
   return make_plan_raw(ctx->nranks, ctx->pr, ctx->pc, ctx->myrow, ctx->mycol, A->Mb, B->Nb, A->Nb, A->bs, densified,
-                       ctx->chunk_bytes);
+                       ctx->chunk_bytes, ctx->transport);
 }
 
 // One Cannon exchange step as a list of point-to-point operations (owner-pull, reading R5):
@@ -688,7 +701,7 @@ extern "C" dbm_status dbm_plan_exchange(int pr, int pc, int myrow, int mycol, in
             DBM_ERR_ARG, "bad grid or block size");
   ARG_CHECK(Mb >= 0 && Nb >= 0 && Kb >= 0, DBM_ERR_ARG, "negative block counts");
   const Plan p = make_plan_raw(pr * pc, pr, pc, myrow, mycol, Mb, Nb, Kb, bs, path == DBM_PATH_DENSIFIED,
-                               16ll << 30);
+                               16ll << 30, 0);
   ARG_CHECK(step >= 0 && step < p.L, DBM_ERR_RANGE, "step out of range");
   const std::vector<XOp> v = exchange_ops(p, step);
   if (ops || bytes) {
@@ -737,6 +750,104 @@ dbm_status post_exchange(dbm_ctx ctx, const Plan& p, int s, char* ws, const doub
     }
   }
   NCCL_TRY(ctx, ncclGroupEnd());
+  return DBM_OK;
+}
+
+// ---------------------------------------------------------------- copy-engine transport (CUDA IPC)
+// Every rank's workspace (the allocation holding its own densified / packed panels) is mapped into
+// its peers with cudaIpcOpenMemHandle; a Cannon exchange is then a set of cudaMemcpyAsync pulls on
+// the comm stream, executed by the DMA copy engines over NVLink 5 — no SM is taken from the GEMM.
+// Ordering across processes uses two tiny NCCL collectives on the comm stream: the handle
+// all-gather (after this rank's own panels are ready: all panels are ready when it completes) and
+// a closing all-reduce (after this rank's last pull: no peer still reads my panels).
+typedef CUresult (*AddrRangeFn)(CUdeviceptr*, size_t*, CUdeviceptr);
+
+AddrRangeFn addr_range_fn() {
+  static AddrRangeFn fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = (AddrRangeFn)p;
+  }
+  return fn;
+}
+
+constexpr int kIpcRec = 128;  // bytes per rank: 64-B handle + 8-B offset, padded
+
+dbm_status ipc_exchange(dbm_ctx ctx, void* ws) {
+  const int P = ctx->nranks;
+  AddrRangeFn fn = addr_range_fn();
+  ARG_CHECK(fn, DBM_ERR_CUDA, "cuMemGetAddressRange unavailable");
+  CUdeviceptr base = 0;
+  size_t sz = 0;
+  if (fn(&base, &sz, (CUdeviceptr)ws) != CUDA_SUCCESS) {
+    set_error("cuMemGetAddressRange failed on the workspace");
+    ctx->poisoned = DBM_ERR_CUDA;
+    return DBM_ERR_CUDA;
+  }
+  cudaIpcMemHandle_t h;
+  CUDA_TRY(ctx, cudaIpcGetMemHandle(&h, (void*)base));
+  std::vector<char> mine(kIpcRec, 0), all((size_t)kIpcRec * P, 0);
+  const int64_t off = (int64_t)((char*)ws - (char*)base);
+  std::memcpy(mine.data(), &h, sizeof(h));
+  std::memcpy(mine.data() + 64, &off, sizeof(off));
+  if (!ctx->d_scratch) CUDA_TRY(ctx, cudaMalloc(&ctx->d_scratch, (size_t)kIpcRec * (P + 1) + 64));
+  char* d_mine = (char*)ctx->d_scratch + 64;
+  char* d_all = d_mine + kIpcRec;
+  CUDA_TRY(ctx, cudaMemcpyAsync(d_mine, mine.data(), kIpcRec, cudaMemcpyHostToDevice, ctx->comm));
+  NCCL_TRY(ctx, ncclAllGather(d_mine, d_all, kIpcRec, ncclChar, (ncclComm_t)ctx->nccl, ctx->comm));
+  CUDA_TRY(ctx, cudaMemcpyAsync(all.data(), d_all, (size_t)kIpcRec * P, cudaMemcpyDeviceToHost, ctx->comm));
+  CUDA_TRY(ctx, cudaStreamSynchronize(ctx->comm));
+  if ((int)ctx->peer_ws.size() != P) {
+    ctx->peer_ws.assign(P, nullptr);
+    ctx->peer_handles.assign(P, std::vector<char>());
+    ctx->peer_bases.assign(P, nullptr);
+  }
+  for (int q = 0; q < P; ++q) {
+    if (q == ctx->rank) continue;
+    const char* rec = all.data() + (size_t)q * kIpcRec;
+    std::vector<char> hq(rec, rec + 64);
+    int64_t offq;
+    std::memcpy(&offq, rec + 64, sizeof(offq));
+    if (hq != ctx->peer_handles[q]) {
+      if (ctx->peer_bases[q]) cudaIpcCloseMemHandle(ctx->peer_bases[q]);
+      cudaIpcMemHandle_t hh;
+      std::memcpy(&hh, hq.data(), sizeof(hh));
+      void* pb = nullptr;
+      CUDA_TRY(ctx, cudaIpcOpenMemHandle(&pb, hh, cudaIpcMemLazyEnablePeerAccess));
+      ctx->peer_bases[q] = pb;
+      ctx->peer_handles[q] = hq;
+    }
+    ctx->peer_ws[q] = (char*)ctx->peer_bases[q] + offq;
+  }
+  ctx->ipc_ws = ws;
+  return DBM_OK;
+}
+
+dbm_status comm_barrier(dbm_ctx ctx) {
+  int* w = ctx->d_scratch;
+  NCCL_TRY(ctx, ncclAllReduce(w, w, 1, ncclInt, ncclSum, (ncclComm_t)ctx->nccl, ctx->comm));
+  return DBM_OK;
+}
+
+// Pull this rank's step-s panels from their owners' workspaces (peer plans give the offsets).
+dbm_status post_pulls(dbm_ctx ctx, const Plan& p, const std::vector<Plan>& peer_plan, int s, char* ws, int bufA,
+                      int bufB, int64_t* sent, int64_t* recv) {
+  for (const XOp& op : exchange_ops(p, s)) {
+    const size_t n = (size_t)op.bytes;
+    if (op.send) {  // the peer pulls it; counted for the statistics
+      *sent += (int64_t)n;
+      continue;
+    }
+    const Plan& q = peer_plan[op.peer];
+    const size_t src_off = op.operand == 0 ? q.ownA_off[op.kappa] : q.ownB_off[op.kappa];
+    ARG_CHECK(src_off != SIZE_MAX && ctx->peer_ws[op.peer], DBM_ERR_PLAN, "peer panel not in its workspace");
+    void* dst = ws + (op.operand == 0 ? p.off_recvA[bufA] : p.off_recvB[bufB]);
+    if (n) CUDA_TRY(ctx, cudaMemcpyAsync(dst, ctx->peer_ws[op.peer] + src_off, n, cudaMemcpyDeviceToDevice, ctx->comm));
+    *recv += (int64_t)n;
+  }
   return DBM_OK;
 }
 
@@ -827,8 +938,13 @@ extern "C" dbm_status dbm_multiply(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_
   std::vector<cudaEvent_t> ev_x(p.L, nullptr), ev_g(p.L, nullptr);
   cudaEvent_t ev_ready = nullptr;
   int bufA_of[64], bufB_of[64];
+  std::vector<Plan> peer_plan;
+  auto exchange = [&](int s) -> dbm_status {
+    if (ctx->transport == 0)
+      return post_pulls(ctx, p, peer_plan, s, ws, bufA_of[s], bufB_of[s], &st.bytes_sent, &st.bytes_recv);
+    return post_exchange(ctx, p, s, ws, A->arena, B->arena, bufA_of[s], bufB_of[s], &st.bytes_sent, &st.bytes_recv);
+  };
   if (ctx->nranks > 1) {
-    ARG_CHECK(p.L <= 64, DBM_ERR_GRID, "grid too large (L > 64)");
     int na = 0, nb = 0;
     for (int s = 0; s < p.L; ++s) {
       bufA_of[s] = (p.a_src(s) != p.me()) ? (na++ & 1) : -1;
@@ -841,9 +957,16 @@ extern "C" dbm_status dbm_multiply(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_
       ev_x[s] = get_event(ctx);
       ev_g[s] = get_event(ctx);
     }
-    if (dbm_status e = post_exchange(ctx, p, 0, ws, A->arena, B->arena, bufA_of[0], bufB_of[0], &st.bytes_sent,
-                                     &st.bytes_recv))
-      return e;
+    if (ctx->transport == 0) {
+      // handle all-gather after my panels are ready = barrier: every owner's panels are ready after it
+      if (dbm_status e = ipc_exchange(ctx, ws)) return e;
+      peer_plan.resize(ctx->nranks);
+      for (int q = 0; q < ctx->nranks; ++q)
+        if (q != ctx->rank)
+          peer_plan[q] = make_plan_raw(ctx->nranks, p.pr, p.pc, q / p.pc, q % p.pc, p.Mb, p.Nb, p.Kb, p.bs, dens,
+                                       ctx->chunk_bytes, ctx->transport);
+    }
+    if (dbm_status e = exchange(0)) return e;
     CUDA_TRY(ctx, cudaEventRecord(ev_x[0], ctx->comm));
   }
 
@@ -852,9 +975,7 @@ extern "C" dbm_status dbm_multiply(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_
     if (ctx->nranks > 1) {
       if (s + 1 < p.L) {  // prefetch step s+1 while step s computes (P:171 overlap)
         if (s >= 1) CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->comm, ev_g[s - 1], 0));
-        if (dbm_status e = post_exchange(ctx, p, s + 1, ws, A->arena, B->arena, bufA_of[s + 1], bufB_of[s + 1],
-                                         &st.bytes_sent, &st.bytes_recv))
-          return e;
+        if (dbm_status e = exchange(s + 1)) return e;
         CUDA_TRY(ctx, cudaEventRecord(ev_x[s + 1], ctx->comm));
       }
       CUDA_TRY(ctx, cudaStreamWaitEvent(cs, ev_x[s], 0));
@@ -945,15 +1066,27 @@ extern "C" dbm_status dbm_multiply(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_
     if (ctx->nranks > 1) CUDA_TRY(ctx, cudaEventRecord(ev_g[s], cs));
   }
 
+  cudaEvent_t ev_end = nullptr;
   if (ctx->nranks > 1) {
-    // the comm stream's last op covers every send: the caller may reuse A/B after this point
-    CUDA_TRY(ctx, cudaStreamWaitEvent(cs, ev_x[p.L - 1], 0));
+    if (ctx->transport == 1) {
+      // the comm stream's last op covers every send: the caller may reuse A/B after this point
+      CUDA_TRY(ctx, cudaStreamWaitEvent(cs, ev_x[p.L - 1], 0));
+    } else {
+      // closing barrier: after it, no peer is still pulling from this rank's workspace
+      if (dbm_status e = comm_barrier(ctx)) return e;
+      ev_end = get_event(ctx);
+      CUDA_TRY(ctx, cudaEventRecord(ev_end, ctx->comm));
+    }
   }
   if (dens && M * N > 0) {
     ProfScope ps(ctx, cs, 3, 0.0, (beta == 0.0 ? 16.0 : 24.0) * M * N);
     launch_undensify((double*)(ws + p.off_cd), M, 1, 0, p.mloc, p.nloc, (int)bs, alpha, beta, C->arena, cs);
     ++launches;
     CUDA_TRY(ctx, cudaGetLastError());
+  }
+  if (ev_end) {
+    CUDA_TRY(ctx, cudaStreamWaitEvent(cs, ev_end, 0));
+    ctx->ev_pool.push_back(ev_end);
   }
   if (ctx->nranks > 1) {
     // events are reusable once the compute stream has passed them; recycle after this call

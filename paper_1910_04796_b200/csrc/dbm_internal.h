@@ -102,6 +102,15 @@ struct dbm_ctx_s {
   void* stage[2] = {nullptr, nullptr};
   size_t stage_bytes = 0;
   cudaEvent_t stage_ev[2] = {nullptr, nullptr};
+  // Cannon transport: 0 = copy engines pulling peer panels through CUDA IPC mappings (default),
+  // 1 = NCCL grouped send/recv.
+  int transport = 0;
+  void* ipc_ws = nullptr;                 // workspace the peer mappings were built for
+  int64_t ipc_ws_bytes = 0;
+  std::vector<char*> peer_ws;             // peer workspaces mapped into this process (nullptr = self)
+  std::vector<std::vector<char>> peer_handles;  // raw IPC handles (to re-use / close mappings)
+  std::vector<void*> peer_bases;          // opened allocation bases (cudaIpcCloseMemHandle)
+  int* d_scratch = nullptr;               // device scratch: barrier word + handle exchange
 };
 
 struct dbm_matrix_s {

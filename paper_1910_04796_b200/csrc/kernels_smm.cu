@@ -45,7 +45,7 @@ struct SmmCfg {
 };
 
 // bs 22: A pitch 22 (3-way LDS conflicts on A, cheap: DMMA-bound), B pitch 44 (conflict-free)
-using Cfg22 = SmmCfg<22, 8, 1, 1, 3, 3, 44, 22, 44, 9>;
+// (bs 22 uses the TMA-bulk kernel smm22_kernel below)
 // bs 64: padded pitches 72 / 36 (both conflict-free), half a block of K per stage
 using Cfg64 = SmmCfg<64, 2, 2, 2, 4, 4, 32, 72, 36, 4>;
 
@@ -330,16 +330,226 @@ cudaError_t launch_group(const int32_t* trip, int64_t nruns, int64_t kb, const d
   return cudaGetLastError();
 }
 
+// ============================================================================ bs 22: TMA bulk staging
+// Same group scheme (8 runs per CTA, one consumer warp per C block), but every staged block is one
+// 3,872-B cp.async.bulk (TMA) issued by one producer lane, completing on the stage's mbarrier:
+// a stage is KK22 = 2 consecutive k-blocks, i.e. 44 k = 11 DMMA k-steps without K padding.
+//   A slot: blocks (li, kk0), (li, kk0+1) column-major back to back = [k 0..43][m 0..21] (pitch 22)
+//   B slot: blocks (kk0, lj), (kk0+1, lj)                            = [kk][n][x] (pitch 22)
+// A tail stage (odd kb) masks the missing k with zeros in registers.
+namespace s22 {
+constexpr int BS = 22, BB = 484, KK = 2, KS = 44, RUNS = 8, WARPS = 8, P = 9, STAGES = 3;
+constexpr int SLOT = KK * BB;                       // doubles
+// slack: the padded rows m, n = 22, 23 of the last slot read past it (B: up to kk*484 + 23*22 + 21
+// = SLOT + 43 doubles); only discarded C rows / columns see those values
+constexpr int STAGE = P * SLOT + 64;
+constexpr size_t SMEM = (size_t)STAGES * STAGE * 8;
+constexpr uint32_t BLK_BYTES = BB * 8;              // 3,872
+static_assert(SMEM + 512 <= 232448, "shared memory");
+}  // namespace s22
+
+__device__ __forceinline__ void mbar_expect_tx(uint32_t a, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(a), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t mbar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+               "l"(src), "r"(bytes), "r"(mbar)
+               : "memory");
+}
+
+template <bool MASK>
+__device__ __forceinline__ void s22_stage(double (&acc)[3][3][2], uint32_t sA, uint32_t sB, int t, int kvalid) {
+  using namespace s22;
+  // B (k, n) of the two-block slot: kk = k / 22, x = k % 22 -> kk*484 + n*22 + x
+#pragma unroll
+  for (int ks = 0; ks < KS / 4; ++ks) {
+    const int k = 4 * ks + t;
+    const bool ok = !MASK || k < kvalid;
+    const uint32_t kb_off = (uint32_t)((k >= BS ? BB + (k - BS) : k) * 8);
+    double a[3], b[3];
+#pragma unroll
+    for (int mi = 0; mi < 3; ++mi) a[mi] = ok ? lds64(sA + (uint32_t)(k * BS + mi * 8) * 8u) : 0.0;
+#pragma unroll
+    for (int ni = 0; ni < 3; ++ni) b[ni] = ok ? lds64(sB + kb_off + (uint32_t)(ni * 8 * BS) * 8u) : 0.0;
+#pragma unroll
+    for (int mi = 0; mi < 3; ++mi)
+#pragma unroll
+      for (int ni = 0; ni < 3; ++ni) dmma(acc[mi][ni], a[mi], b[ni]);
+  }
+}
+
+__global__ void __launch_bounds__((s22::WARPS + 1) * 32, 1)
+    smm22_kernel(const int32_t* __restrict__ trip, int64_t nruns, int64_t kb, const double* __restrict__ A,
+                 const double* __restrict__ B, double* __restrict__ C, double alpha, double beta_first) {
+  using namespace s22;
+  extern __shared__ __align__(128) double smem[];
+  __shared__ __align__(8) uint64_t full[STAGES], empty[STAGES];
+  __shared__ int s_rep[P], s_isb[P], s_ia[RUNS], s_ib[RUNS], s_n, s_sub;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const bool producer = warp == WARPS;
+  const int Krun = (int)(kb * BS);
+  const int nst = (Krun + KS - 1) / KS;
+  const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(smem);
+  const int64_t ngroups = (nruns + RUNS - 1) / RUNS;
+  const int g = lane >> 2, t = lane & 3;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init((uint32_t)__cvta_generic_to_shared(&full[s]), 1);
+      mbar_init((uint32_t)__cvta_generic_to_shared(&empty[s]), WARPS);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  int stage = 0;
+  uint32_t phase = 0;
+  for (int64_t grp = blockIdx.x; grp < ngroups; grp += gridDim.x) {
+    const int64_t q0 = grp * RUNS;
+    const int nrun_g = (int)(nruns - q0 < RUNS ? nruns - q0 : RUNS);
+    if (producer) {
+      int sub = nrun_g;
+      for (;;) {
+        bool ok = true;
+        for (int s0 = 0; s0 < nrun_g; s0 += sub) {
+          const Uniq u = uniq(trip, q0, s0, min(sub, nrun_g - s0), kb, lane);
+          if (__popc(u.lead_a) + __popc(u.lead_b) > P) ok = false;
+        }
+        if (ok || sub == 1) break;
+        sub = (sub + 1) / 2;
+      }
+      if (lane == 0) s_sub = sub;
+    }
+    __syncthreads();
+    const int sub = s_sub;
+    for (int s0 = 0; s0 < nrun_g; s0 += sub) {
+      const int n_sub = min(sub, nrun_g - s0);
+      if (s0 > 0) __syncthreads();
+      if (producer) {
+        const Uniq u = uniq(trip, q0, s0, n_sub, kb, lane);
+        const int na = __popc(u.lead_a);
+        if (u.act) {
+          const int la = __ffs(u.ma) - 1, lb = __ffs(u.mb) - 1;
+          const int ia = __popc(u.lead_a & ((1u << la) - 1));
+          const int ib = na + __popc(u.lead_b & ((1u << lb) - 1));
+          s_ia[lane] = ia;
+          s_ib[lane] = ib;
+          if (la == lane) {
+            s_rep[ia] = s0 + lane;
+            s_isb[ia] = 0;
+          }
+          if (lb == lane) {
+            s_rep[ib] = s0 + lane;
+            s_isb[ib] = 1;
+          }
+        }
+        if (lane == 0) s_n = na + __popc(u.lead_b);
+      }
+      __syncthreads();
+      const int nslots = s_n;
+
+      if (producer) {
+        // lane l < 2*nslots copies block kk0 + (l & 1) of slot l >> 1
+        const int u = lane >> 1, j = lane & 1;
+        const bool owner = u < nslots;
+        const int64_t q = q0 + (owner ? s_rep[u] : 0);
+        const int col = owner ? s_isb[u] : 0;
+        const double* base = col ? B : A;
+        for (int st = 0; st < nst; ++st) {
+          const int kk = st * KK + j;
+          const bool valid = owner && kk < kb;
+          const uint32_t fb = (uint32_t)__cvta_generic_to_shared(&full[stage]);
+          if (lane == 0) mbar_wait((uint32_t)__cvta_generic_to_shared(&empty[stage]), phase ^ 1);
+          const unsigned vm = __ballot_sync(0xffffffffu, valid);
+          if (lane == 0) mbar_expect_tx(fb, (uint32_t)__popc(vm) * BLK_BYTES);
+          __syncwarp();
+          if (valid) {
+            const int64_t blk = trip[3 * (q * kb + kk) + col];
+            bulk_g2s(sbase + (uint32_t)(stage * STAGE + u * SLOT + j * BB) * 8u, base + blk * BB, BLK_BYTES, fb);
+          }
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        continue;
+      }
+
+      const int my = warp - s0;
+      const bool active = my >= 0 && my < n_sub;
+      double acc[3][3][2];
+#pragma unroll
+      for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int jj = 0; jj < 3; ++jj) acc[i][jj][0] = acc[i][jj][1] = 0.0;
+      const int ia = active ? s_ia[my] : 0, ib = active ? s_ib[my] : 0;
+      const uint32_t offA = (uint32_t)(ia * SLOT + g) * 8u;        // + k*22 + mi*8
+      const uint32_t offB = (uint32_t)(ib * SLOT + g * BS) * 8u;   // + kk*484 + x + ni*8*22
+      for (int st = 0; st < nst; ++st) {
+        mbar_wait((uint32_t)__cvta_generic_to_shared(&full[stage]), phase);
+        if (active) {
+          const uint32_t sb = sbase + (uint32_t)(stage * STAGE) * 8u;
+          const int kvalid = Krun - st * KS;
+          if (kvalid >= KS)
+            s22_stage<false>(acc, sb + offA, sb + offB, t, KS);
+          else
+            s22_stage<true>(acc, sb + offA, sb + offB, t, kvalid);
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive((uint32_t)__cvta_generic_to_shared(&empty[stage]));
+        if (++stage == STAGES) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+      if (active) {
+        double* cb = C + (int64_t)trip[3 * ((q0 + warp) * kb) + 2] * BB;
+#pragma unroll
+        for (int mi = 0; mi < 3; ++mi) {
+          const int m = mi * 8 + g;
+#pragma unroll
+          for (int ni = 0; ni < 3; ++ni)
+#pragma unroll
+            for (int jj = 0; jj < 2; ++jj) {
+              const int n = ni * 8 + 2 * t + jj;
+              if (m < BS && n < BS) {
+                double* p = cb + m + n * BS;
+                const double v = alpha * acc[mi][ni][jj];
+                *p = (beta_first == 0.0) ? v : beta_first * *p + v;
+              }
+            }
+        }
+      }
+    }
+    __syncthreads();
+  }
+}
+
+cudaError_t launch_smm22(const int32_t* trip, int64_t nruns, int64_t kb, const double* A, const double* B, double* C,
+                         double alpha, double beta_first, cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(smm22_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s22::SMEM);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  const int64_t ngroups = (nruns + s22::RUNS - 1) / s22::RUNS;
+  const unsigned grid = (unsigned)std::min<int64_t>(ngroups, (int64_t)num_sms());
+  smm22_kernel<<<grid, (s22::WARPS + 1) * 32, s22::SMEM, st>>>(trip, nruns, kb, A, B, C, alpha, beta_first);
+  return cudaGetLastError();
+}
+
 }  // namespace
 
 bool smm_has_tensor_path(int bs) { return bs == 22 || bs == 64; }
 
-int smm_group_runs(int bs) { return bs == 22 ? Cfg22::RUNS : (bs == 64 ? Cfg64::RUNS : 1); }
+int smm_group_runs(int bs) { return bs == 22 ? s22::RUNS : (bs == 64 ? Cfg64::RUNS : 1); }
 
 cudaError_t launch_smm_tc(int bs, const int32_t* trip, int64_t nruns, int64_t kb, const double* A, const double* B,
                           double* C, double alpha, double beta_first, cudaStream_t st) {
   if (nruns <= 0 || kb <= 0) return cudaSuccess;
-  if (bs == 22) return launch_group<Cfg22>(trip, nruns, kb, A, B, C, alpha, beta_first, st);
+  if (bs == 22) return launch_smm22(trip, nruns, kb, A, B, C, alpha, beta_first, st);
   if (bs == 64) return launch_group<Cfg64>(trip, nruns, kb, A, B, C, alpha, beta_first, st);
   return cudaErrorInvalidValue;
 }

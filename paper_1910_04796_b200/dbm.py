@@ -58,6 +58,7 @@ _SIGS = {
                                        C.POINTER(C.c_double), C.POINTER(C.c_double)]),
     "dbm_ctx_launch_count": (C.c_int, [_P, C.POINTER(_I64)]),
     "dbm_ctx_set_dense_chunk_bytes": (C.c_int, [_P, _I64]),
+    "dbm_ctx_set_transport": (C.c_int, [_P, C.c_int]),
     "dbm_plan_exchange": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, _I64, _I64, _I64, C.c_int32, C.c_int,
                                     C.c_int, _P, _P, C.POINTER(C.c_int)]),
     "dbm_ctx_destroy": (C.c_int, [_P]),
@@ -170,6 +171,12 @@ class Context:
         n = C.c_int64()
         _check(load().dbm_ctx_profile_read(self.h, kernel, C.byref(ms), C.byref(n), C.byref(fl), C.byref(by)))
         return {"ms": ms.value, "launches": n.value, "flops": fl.value, "bytes": by.value}
+
+    def set_transport(self, transport: str | int) -> None:
+        """'ce' (copy engines over CUDA IPC, default) or 'nccl' (grouped send/recv)."""
+        t = {"ce": 0, "nccl": 1}.get(transport, transport)
+        _check(load().dbm_ctx_set_transport(self.h, int(t)))
+        self.transport = t
 
     def set_dense_chunk_bytes(self, nbytes: int) -> None:
         _check(load().dbm_ctx_set_dense_chunk_bytes(self.h, nbytes))

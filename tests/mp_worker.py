@@ -30,8 +30,10 @@ def main():
     grids = [(p, world // p) for p in range(1, world + 1) if world % p == 0]
     shapes = [(352, 352, 352, 22), (704, 528, 1100, 22), (384, 640, 1280, 64), (66, 154, 198, 22), (44, 44, 22, 22)]
     failures = 0
-    for pr, pc in grids:
+    cases = [(pr, pc, tr) for (pr, pc) in grids for tr in ("ce", "nccl")]
+    for pr, pc, transport in cases:
         ctx = dbm.Context.from_distributed(pr=pr, pc=pc)
+        ctx.set_transport(transport)
         r, c = ctx.myrow, ctx.mycol
         for (M, N, K, bs) in shapes:
             for path in ("densified", "blocked"):
@@ -64,7 +66,7 @@ def main():
                     if flags.item():
                         failures += 1
                     if rank == 0 or not (ok_val and ok_bytes):
-                        print(json.dumps({"rank": rank, "grid": f"{pr}x{pc}", "shape": [M, N, K, bs], "path": path,
+                        print(json.dumps({"rank": rank, "grid": f"{pr}x{pc}", "transport": transport, "shape": [M, N, K, bs], "path": path,
                                           "kind": kind, "err": err, "ok": bool(ok_val), "bytes_ok": ok_bytes,
                                           "recv": st["bytes_recv"], "expect_recv": rv}), flush=True)
         ctx.close()

@@ -119,12 +119,13 @@ def oracle_sample(M, N, K, rows: int) -> dict:
             "seconds": dt}
 
 
-def auto_rows(M, N, K) -> int:
-    # measured: ~0.3 GFLOP/s per core for the plain loop incl. regenerating B; target ~15 s
+def auto_rows(M, N, K, target_s: float = 15.0) -> int:
+    # measured on the B200 box's 16 host cores: ~2.3 GFLOP/s per core for the plain loop incl.
+    # regenerating B from the seeds (8 rows of 63,360^2 in 1.7 s)
     import oracle
 
     cores = max(1, oracle.num_threads())
-    rows = int(15.0 * 0.3e9 * cores / (2.0 * K * N))
+    rows = int(target_s * 2.0e9 * cores / (2.0 * K * N))
     return max(1, min(rows, M, 64))
 
 
@@ -132,7 +133,7 @@ def run_reference(args, cfg, name, world, rank):
     M, N, K, bs, path, _ = cfg
     if rank != 0:
         return
-    rows = args.cpu_rows or auto_rows(M, N, K)
+    rows = args.cpu_rows or auto_rows(M, N, K, target_s=4.0)  # each step a bounded sample (~4 s)
     times = []
     for i in range(args.warmup + args.steps):
         r = oracle_sample(M, N, K, rows)

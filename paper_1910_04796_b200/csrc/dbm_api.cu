@@ -539,10 +539,13 @@ struct Plan {
   int me() const { return r * pc + c; }
   // dense panel leading dimensions (even, so TMA strides are 16-byte multiples)
   int64_t ld_panel(int k) const { return round_up(std::max<int64_t>(kb[k] * bs, 1), 2); }
+  // (an empty K panel, kb = 0, moves no bytes on either path)
   size_t a_panel_bytes(int k) const {
+    if (kb[k] == 0) return 0;
     return densified ? (size_t)(mloc * bs) * ld_panel(k) * 8 : (size_t)(mloc * kb[k]) * bs * bs * 8;
   }
   size_t b_panel_bytes(int k) const {
+    if (kb[k] == 0) return 0;
     return densified ? (size_t)(nloc * bs) * ld_panel(k) * 8 : (size_t)(nloc * kb[k]) * bs * bs * 8;
   }
 };

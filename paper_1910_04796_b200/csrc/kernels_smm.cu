@@ -44,8 +44,7 @@ struct SmmCfg {
   static_assert(SMEM + 256 <= 232448, "shared memory");
 };
 
-// bs 22: A pitch 22 (3-way LDS conflicts on A, cheap: DMMA-bound), B pitch 44 (conflict-free)
-// (bs 22 uses the TMA-bulk kernel smm22_kernel below)
+// (bs 22 uses smm22_kernel below)
 // bs 64: padded pitches 72 / 36 (both conflict-free), half a block of K per stage
 using Cfg64 = SmmCfg<64, 2, 2, 2, 4, 4, 32, 72, 36, 4>;
 
@@ -110,10 +109,19 @@ __device__ __forceinline__ void mbar_wait(uint32_t a, uint32_t parity) {
   } while (!done);
 }
 
+__device__ __forceinline__ void mbar_expect_tx(uint32_t a, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(a), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t mbar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+               "l"(src), "r"(bytes), "r"(mbar)
+               : "memory");
+}
+
 // Warp-specialised: warps 0..WARPS-1 compute (one run, or a WRM x WRN share of one), warp WARPS is
-// the producer.  Per stage the producer reads the (slot, kk) block indices from the stack triplets
-// once (one lane each), broadcasts them with shuffles, and issues the 16-B cp.async of every used
-// pool slot; cp.async.mbarrier.arrive marks the stage full.  Consumers release a stage with one
+// the producer.  Per stage the producer reads the slots' block indices from the stack triplets
+// once (one lane each), broadcasts them with shuffles, and issues one TMA bulk copy per padded
+// column / row segment, completing on the stage's mbarrier (expect_tx).  Consumers release a stage with one
 // mbarrier arrive per warp.  Group metadata (which runs share blocks) is computed by the producer
 // between two CTA barriers at each (sub-)group start.
 template <class Cfg>
@@ -148,7 +156,7 @@ __global__ void __launch_bounds__(Cfg::THREADS + 32, 1)
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
-      mbar_init((uint32_t)__cvta_generic_to_shared(&full[s]), 32);
+      mbar_init((uint32_t)__cvta_generic_to_shared(&full[s]), 1);
       mbar_init((uint32_t)__cvta_generic_to_shared(&empty[s]), WARPS);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -209,41 +217,40 @@ __global__ void __launch_bounds__(Cfg::THREADS + 32, 1)
         const bool owner = lane < nslots * KKS;
         const int64_t my_q = q0 + (owner ? s_rep[my_u] : 0);
         const int my_col = owner ? s_isb[my_u] : 0;
-        const int total = nslots * CA;
+        // one TMA bulk copy per segment: an A k-column (BS contiguous doubles -> pitch PA) or a B
+        // n-row (KS contiguous k of block column y -> pitch PB); KS divides BS, so a stage never
+        // straddles two k-blocks and K never needs zero-fill
+        static_assert(KKS == 1 && BS % KS == 0, "bulk segments need stages inside one block");
+        const int nseg = nslots * (KS > BS ? KS : BS);  // per slot: KS A-columns or BS B-rows (KS <= BS)
         for (int st = 0; st < nst; ++st) {
-          mbar_wait((uint32_t)__cvta_generic_to_shared(&empty[stage]), phase ^ 1);
-          const int kg0 = st * KS;
-          const int kk_first = kg0 / BS;
-          int blk = 0;  // block index (slot in its arena) this lane owns for this stage
-          if (owner && kk_first + my_j < kb) blk = trip[3 * (my_q * kb + kk_first + my_j) + my_col];
+          const int kg0 = st * KS, kk = kg0 / BS, x0 = kg0 - kk * BS;
+          int blk = 0;
+          if (owner) blk = trip[3 * (my_q * kb + kk) + my_col];
+          const uint32_t fb = (uint32_t)__cvta_generic_to_shared(&full[stage]);
+          if (lane == 0) {
+            mbar_wait((uint32_t)__cvta_generic_to_shared(&empty[stage]), phase ^ 1);
+            uint32_t bytes = 0;
+            for (int u = 0; u < nslots; ++u) bytes += s_isb[u] ? BS * KS * 8 : KS * BS * 8;
+            mbar_expect_tx(fb, bytes);
+          }
+          __syncwarp();
           const uint32_t d0 = sbase + (uint32_t)(stage * Cfg::STAGE) * 8u;
-          for (int c0 = 0; c0 < total; c0 += 32) {
+          for (int c0 = 0; c0 < nseg; c0 += 32) {
             const int c = c0 + lane;
-            const bool v = c < total;
-            const int u = v ? c / CA : 0, rem = v ? c - u * CA : 0;
-            const bool isb = v && s_isb[u];
-            int kg, off;  // off: doubles within the block; dst in doubles within the stage
-            uint32_t dst;
-            if (!isb) {
-              const int k = rem / (BS / 2), p = rem - k * (BS / 2);
-              kg = kg0 + k;
-              off = (kg % BS) * BS + 2 * p;
-              dst = (uint32_t)(u * SLOT + k * PA + 2 * p);
-            } else {
-              const int y = rem / (KS / 2), p = rem - y * (KS / 2);
-              kg = kg0 + 2 * p;
-              off = y * BS + kg % BS;
-              dst = (uint32_t)(u * SLOT + y * PB + 2 * p);
-            }
-            const int src_lane = u * KKS + (kg / BS - kk_first);
-            const int b = __shfl_sync(0xffffffffu, blk, src_lane & 31);
+            const int u = c / BS, r = c - u * BS;  // slot, segment index (< BS)
+            const bool v = c < nseg;
+            const int b = __shfl_sync(0xffffffffu, blk, v ? u : 0);
             if (v) {
-              const bool in = kg < Krun;
-              const double* src = (isb ? B : A) + (in ? (int64_t)b * BB + off : 0);
-              cp_async16(d0 + dst * 8u, src, in ? 16 : 0);  // zero-fill past the run's K
+              if (!s_isb[u]) {
+                if (r < KS)  // A column k = r of this stage: column x0 + r of the block
+                  bulk_g2s(d0 + (uint32_t)(u * SLOT + r * PA) * 8u, A + (int64_t)b * BB + (int64_t)(x0 + r) * BS,
+                           BS * 8, fb);
+              } else {  // B row n = r: k = x0 .. x0+KS-1 of block column r
+                bulk_g2s(d0 + (uint32_t)(u * SLOT + r * PB) * 8u, B + (int64_t)b * BB + (int64_t)r * BS + x0,
+                         KS * 8, fb);
+              }
             }
           }
-          cp_async_mbar_arrive((uint32_t)__cvta_generic_to_shared(&full[stage]));
           if (++stage == STAGES) {
             stage = 0;
             phase ^= 1;
@@ -348,14 +355,6 @@ constexpr uint32_t BLK_BYTES = BB * 8;              // 3,872
 static_assert(SMEM + 512 <= 232448, "shared memory");
 }  // namespace s22
 
-__device__ __forceinline__ void mbar_expect_tx(uint32_t a, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(a), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t mbar) {
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
-               "l"(src), "r"(bytes), "r"(mbar)
-               : "memory");
-}
 
 template <bool MASK>
 __device__ __forceinline__ void s22_stage(double (&acc)[3][3][2], uint32_t sA, uint32_t sB, int t, int kvalid) {

@@ -47,6 +47,7 @@ def parse():
     p.add_argument("--path", default=None, choices=["densified", "blocked"])
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--transport", default="ce", choices=["ce", "nccl"], help="Cannon panel transport (N>1)")
+    p.add_argument("--grid", default="", help="force the process grid, e.g. 1x4 (default: reading R1)")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--e2e-steps", type=int, default=1)
@@ -176,7 +177,8 @@ def main():
     dev = torch.device("cuda", local)
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
-        ctx = dbm.Context.from_distributed()
+        pr, pc = (int(x) for x in args.grid.split("x")) if args.grid else (0, 0)
+        ctx = dbm.Context.from_distributed(pr=pr, pc=pc)
         ctx.set_transport(args.transport)
     else:
         ctx = dbm.Context(device=local)

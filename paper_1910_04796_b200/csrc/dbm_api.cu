@@ -760,9 +760,9 @@ dbm_status post_exchange(dbm_ctx ctx, const Plan& p, int s, char* ws, const doub
 // Every rank's workspace (the allocation holding its own densified / packed panels) is mapped into
 // its peers with cudaIpcOpenMemHandle; a Cannon exchange is then a set of cudaMemcpyAsync pulls on
 // the comm stream, executed by the DMA copy engines over NVLink 5 — no SM is taken from the GEMM.
-// Ordering across processes uses two tiny NCCL collectives on the comm stream: the handle
-// all-gather (after this rank's own panels are ready: all panels are ready when it completes) and
-// a closing all-reduce (after this rank's last pull: no peer still reads my panels).
+// Ordering across processes uses two tiny NCCL collectives: the handle all-gather on the comm
+// stream (after this rank's own panels are ready: all panels are ready when it completes) and a
+// closing all-reduce on the compute stream after the last GEMM (no peer still reads my panels).
 typedef CUresult (*AddrRangeFn)(CUdeviceptr*, size_t*, CUdeviceptr);
 
 AddrRangeFn addr_range_fn() {
@@ -826,12 +826,6 @@ dbm_status ipc_exchange(dbm_ctx ctx, void* ws) {
     ctx->peer_ws[q] = (char*)ctx->peer_bases[q] + offq;
   }
   ctx->ipc_ws = ws;
-  return DBM_OK;
-}
-
-dbm_status comm_barrier(dbm_ctx ctx) {
-  int* w = ctx->d_scratch;
-  NCCL_TRY(ctx, ncclAllReduce(w, w, 1, ncclInt, ncclSum, (ncclComm_t)ctx->nccl, ctx->comm));
   return DBM_OK;
 }
 
@@ -1069,17 +1063,9 @@ extern "C" dbm_status dbm_multiply(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_
     if (ctx->nranks > 1) CUDA_TRY(ctx, cudaEventRecord(ev_g[s], cs));
   }
 
-  cudaEvent_t ev_end = nullptr;
   if (ctx->nranks > 1) {
-    if (ctx->transport == 1) {
-      // the comm stream's last op covers every send: the caller may reuse A/B after this point
-      CUDA_TRY(ctx, cudaStreamWaitEvent(cs, ev_x[p.L - 1], 0));
-    } else {
-      // closing barrier: after it, no peer is still pulling from this rank's workspace
-      if (dbm_status e = comm_barrier(ctx)) return e;
-      ev_end = get_event(ctx);
-      CUDA_TRY(ctx, cudaEventRecord(ev_end, ctx->comm));
-    }
+    // the comm stream's last op covers every transfer of this rank
+    CUDA_TRY(ctx, cudaStreamWaitEvent(cs, ev_x[p.L - 1], 0));
   }
   if (dens && M * N > 0) {
     ProfScope ps(ctx, cs, 3, 0.0, (beta == 0.0 ? 16.0 : 24.0) * M * N);
@@ -1087,9 +1073,13 @@ extern "C" dbm_status dbm_multiply(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_
     ++launches;
     CUDA_TRY(ctx, cudaGetLastError());
   }
-  if (ev_end) {
-    CUDA_TRY(ctx, cudaStreamWaitEvent(cs, ev_end, 0));
-    ctx->ev_pool.push_back(ev_end);
+  if (ctx->nranks > 1 && ctx->transport == 0) {
+    // Closing barrier, on the COMPUTE stream after this rank's last GEMM: once every rank passed it,
+    // no peer still pulls from this workspace, so stream-ordered reuse of it is safe.  (A barrier
+    // kernel on the comm stream would start while the persistent GEMM runs, pin an SM until the
+    // slowest peer arrives and leave one GEMM CTA's whole item list waiting behind it.)
+    int* w = ctx->d_scratch;
+    NCCL_TRY(ctx, ncclAllReduce(w, w, 1, ncclInt, ncclSum, (ncclComm_t)ctx->nccl, cs));
   }
   if (ctx->nranks > 1) {
     // events are reusable once the compute stream has passed them; recycle after this call

@@ -17,13 +17,20 @@ namespace dbm {
 
 namespace {
 
-constexpr int BM = 128, BN = 128, BK = 16, STAGES = 6;
+constexpr int BK = 16;
 constexpr int kConsumerWarps = 8;
 constexpr int kThreads = (kConsumerWarps + 1) * 32;
-constexpr int kStageA = BM * BK * 8;  // 16 KB
-constexpr int kStageB = BN * BK * 8;  // 16 KB
-constexpr int kStage = kStageA + kStageB;
-constexpr size_t kSmem = (size_t)STAGES * kStage + 2 * STAGES * 8 + 1024;
+// CTA tile BM x BN in {128, 64}^2 (the host picks the one that wastes the least padding for the
+// block-multiple shapes of the configs, e.g. 704 = 5.5 x 128); ~192 KB of stages in every case.
+template <int BM, int BN>
+struct Tile {
+  static constexpr int kStageA = BM * BK * 8;
+  static constexpr int kStageB = BN * BK * 8;
+  static constexpr int kStage = kStageA + kStageB;
+  static constexpr int STAGES = (196608 / kStage) > 12 ? 12 : (196608 / kStage);
+  static constexpr size_t kSmem = (size_t)STAGES * kStage + 2 * STAGES * 8 + 1024;
+  static constexpr int MI = BM / 16, NI = BN / 32;  // 8x8 subtiles per consumer warp (2 x 4 warps)
+};
 
 __device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
@@ -66,11 +73,14 @@ __device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
       : "d"(a), "d"(b));
 }
 
+template <int BM, int BN>
 __global__ void __launch_bounds__(kThreads, 1)
     dgemm_tn_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M, int N,
                     int k_tiles_total, int k_tiles_per_split, int nsplit, int tiles_m, int tiles_n,
                     double* __restrict__ C,
                     int64_t ldc, double alpha, double beta, double* __restrict__ partial) {
+  using T = Tile<BM, BN>;
+  constexpr int STAGES = T::STAGES, kStage = T::kStage, kStageA = T::kStageA, MI = T::MI, NI = T::NI;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint64_t* full = (uint64_t*)(smem + STAGES * kStage);
@@ -134,7 +144,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     return;
   }
 
-  // ---------------- consumers: warp (wm, wn) owns rows wm*64.., cols wn*32..
+  // ---------------- consumers: warp (wm, wn) owns rows wm*BM/2.., cols wn*BN/4..
   const int wm = warp >> 2, wn = warp & 3;
 
   // Fragment addressing inside a 128-B-swizzled [rows][16 doubles] box: element (row, k) lives at
@@ -144,8 +154,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   // 8-byte bank pairs (k ^ 2g distinct), one wavefront per half-warp.  Any fixed k permutation
   // shared by A and B leaves the product unchanged (the four k-steps cover k = 0..15).
   const int g = lane >> 2, t = lane & 3;
-  const uint32_t a_row = (uint32_t)(wm * 64 + g) * 128u;
-  const uint32_t b_row = (uint32_t)(wn * 32 + g) * 128u;
+  const uint32_t a_row = (uint32_t)(wm * (BM / 2) + g) * 128u;
+  const uint32_t b_row = (uint32_t)(wn * (BN / 4) + g) * 128u;
   uint32_t koff[4];
 #pragma unroll
   for (int ks = 0; ks < 4; ++ks) {
@@ -160,26 +170,26 @@ __global__ void __launch_bounds__(kThreads, 1)
   int tm, tn, split, kt0, nkt;
   item_coords(item, tm, tn, split);
   item_k(split, kt0, nkt);
-  double acc[8][4][2];
+  double acc[MI][NI][2];
 #pragma unroll
-  for (int i = 0; i < 8; ++i)
+  for (int i = 0; i < MI; ++i)
 #pragma unroll
-    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    for (int j = 0; j < NI; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
   for (int kt = 0; kt < nkt; ++kt) {
     mbar_wait(su32(&full[stage]), phase);
     const uint32_t sA = smem_base + stage * kStage;
     const uint32_t sB = sA + kStageA;
 #pragma unroll
     for (int ks = 0; ks < 4; ++ks) {
-      double a[8], b[4];
+      double a[MI], b[NI];
 #pragma unroll
-      for (int mi = 0; mi < 8; ++mi) a[mi] = lds64(sA + a_row + mi * 1024 + koff[ks]);
+      for (int mi = 0; mi < MI; ++mi) a[mi] = lds64(sA + a_row + mi * 1024 + koff[ks]);
 #pragma unroll
-      for (int ni = 0; ni < 4; ++ni) b[ni] = lds64(sB + b_row + ni * 1024 + koff[ks]);
+      for (int ni = 0; ni < NI; ++ni) b[ni] = lds64(sB + b_row + ni * 1024 + koff[ks]);
 #pragma unroll
-      for (int mi = 0; mi < 8; ++mi)
+      for (int mi = 0; mi < MI; ++mi)
 #pragma unroll
-        for (int ni = 0; ni < 4; ++ni) dmma(acc[mi][ni], a[mi], b[ni]);
+        for (int ni = 0; ni < NI; ++ni) dmma(acc[mi][ni], a[mi], b[ni]);
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(su32(&empty[stage]));
@@ -190,16 +200,16 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 
   // ---------------- epilogue (C column-major)
-  const int m0 = tm * BM + wm * 64 + g;
-  const int n0 = tn * BN + wn * 32 + (lane & 3) * 2;
+  const int m0 = tm * BM + wm * (BM / 2) + g;
+  const int n0 = tn * BN + wn * (BN / 4) + (lane & 3) * 2;
   if (partial) {
     double* P = partial + (size_t)split * M * N;
 #pragma unroll
-    for (int mi = 0; mi < 8; ++mi) {
+    for (int mi = 0; mi < MI; ++mi) {
       const int m = m0 + mi * 8;
       if (m >= M) continue;
 #pragma unroll
-      for (int ni = 0; ni < 4; ++ni)
+      for (int ni = 0; ni < NI; ++ni)
 #pragma unroll
         for (int j = 0; j < 2; ++j) {
           const int n = n0 + ni * 8 + j;
@@ -209,11 +219,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     continue;
   }
 #pragma unroll
-  for (int mi = 0; mi < 8; ++mi) {
+  for (int mi = 0; mi < MI; ++mi) {
     const int m = m0 + mi * 8;
     if (m >= M) continue;
 #pragma unroll
-    for (int ni = 0; ni < 4; ++ni)
+    for (int ni = 0; ni < NI; ++ni)
 #pragma unroll
       for (int j = 0; j < 2; ++j) {
         const int n = n0 + ni * 8 + j;
@@ -275,30 +285,48 @@ bool make_kmajor_map(CUtensorMap* tm, const double* base, int64_t rows, int64_t 
 
 }  // namespace
 
-int pick_splitk(int64_t M, int64_t N, int64_t K, int sms) {
-  const int64_t tiles = ((M + BM - 1) / BM) * ((N + BN - 1) / BN);
+namespace {
+
+// Host planner: for each CTA tile shape, the split-K count that fills whole waves of `sms`
+// persistent CTAs; the cheapest (padded work x rounds / shape efficiency) wins.
+struct GemmPlan {
+  int bm, bn, splitk;
+};
+
+GemmPlan pick_gemm(int64_t M, int64_t N, int64_t K, int sms) {
+  static const int shapes[4][2] = {{128, 128}, {128, 64}, {64, 128}, {64, 64}};
+  static const double eff[4] = {1.0, 0.97, 0.97, 0.90};  // per-flop cost of the smaller tiles (LDS/DMMA ratio)
   const int64_t ktiles = (K + BK - 1) / BK;
-  if (tiles >= 4LL * sms || ktiles < 128) return 1;
-  int best = 1;
+  GemmPlan best{128, 128, 1};
   double best_t = 1e300;
-  for (int s = 1; s <= 64; ++s) {
-    if (ktiles / s < 64) break;  // keep >= 1024 of K per split
-    const int64_t ctas = tiles * s;
-    const double waves = (double)((ctas + sms - 1) / sms);
-    const double t = waves / s * (1.0 + 0.002 * s);  // normalised time, mild penalty for reduction traffic
-    if (t < best_t - 1e-12) {
-      best_t = t;
-      best = s;
+  for (int v = 0; v < 4; ++v) {
+    const int bm = shapes[v][0], bn = shapes[v][1];
+    const int64_t tiles = ((M + bm - 1) / bm) * ((N + bn - 1) / bn);
+    for (int s = 1; s <= 64; ++s) {
+      if (s > 1 && (tiles >= 4LL * sms || ktiles / s < 64)) break;  // keep >= 1024 of K per split
+      const int64_t rounds = (tiles * s + sms - 1) / sms;
+      const double t = (double)rounds * bm * bn * ((double)K / s) / eff[v] * (1.0 + 0.002 * (s - 1));
+      if (t < best_t * (1.0 - 1e-9)) {
+        best_t = t;
+        best = {bm, bn, s};
+      }
     }
   }
   return best;
 }
 
-cudaError_t launch_dgemm(const GemmArgs& g, cudaStream_t st, int* launches) {
-  if (g.M <= 0 || g.N <= 0) return cudaSuccess;
+}  // namespace
+
+int pick_splitk(int64_t M, int64_t N, int64_t K, int sms) { return pick_gemm(M, N, K, sms).splitk; }
+
+namespace {
+template <int BM, int BN>
+cudaError_t launch_tile(const GemmArgs& g, int splitk, cudaStream_t st) {
+  using T = Tile<BM, BN>;
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(dgemm_tn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem);
+    cudaError_t e = cudaFuncSetAttribute(dgemm_tn_kernel<BM, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)T::kSmem);
     if (e != cudaSuccess) return e;
     attr = true;
   }
@@ -309,15 +337,30 @@ cudaError_t launch_dgemm(const GemmArgs& g, cudaStream_t st, int* launches) {
     return cudaErrorInvalidValue;
   const int tiles_m = (int)((g.M + BM - 1) / BM), tiles_n = (int)((g.N + BN - 1) / BN);
   const int ktiles = (int)((g.K + BK - 1) / BK);
-  const int splitk = std::max(1, g.splitk);
   const int per = (ktiles + splitk - 1) / splitk;
   const int64_t items = (int64_t)tiles_m * tiles_n * splitk;
   const unsigned grid = (unsigned)std::min<int64_t>(items, num_sms());  // persistent: one CTA per SM
-  dgemm_tn_kernel<<<grid, kThreads, kSmem, st>>>(tmA, tmB, (int)g.M, (int)g.N, ktiles, std::max(per, 0), splitk,
-                                                 tiles_m, tiles_n, g.C, g.ldc, g.alpha, g.beta,
-                                                 splitk > 1 ? g.partial : nullptr);
+  dgemm_tn_kernel<BM, BN><<<grid, kThreads, T::kSmem, st>>>(tmA, tmB, (int)g.M, (int)g.N, ktiles, std::max(per, 0),
+                                                            splitk, tiles_m, tiles_n, g.C, g.ldc, g.alpha, g.beta,
+                                                            splitk > 1 ? g.partial : nullptr);
+  return cudaGetLastError();
+}
+}  // namespace
+
+cudaError_t launch_dgemm(const GemmArgs& g, cudaStream_t st, int* launches) {
+  if (g.M <= 0 || g.N <= 0) return cudaSuccess;
+  const GemmPlan pl = pick_gemm(g.M, g.N, g.K, num_sms());
+  const int splitk = std::max(1, g.splitk);
+  cudaError_t e;
+  if (pl.bm == 128 && pl.bn == 128)
+    e = launch_tile<128, 128>(g, splitk, st);
+  else if (pl.bm == 128)
+    e = launch_tile<128, 64>(g, splitk, st);
+  else if (pl.bn == 128)
+    e = launch_tile<64, 128>(g, splitk, st);
+  else
+    e = launch_tile<64, 64>(g, splitk, st);
   if (launches) ++*launches;
-  cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   if (splitk > 1) {
     launch_splitk_reduce(g.partial, splitk, g.M, g.N, g.C, g.ldc, g.alpha, g.beta, st);

@@ -848,6 +848,30 @@ dbm_status post_pulls(dbm_ctx ctx, const Plan& p, const std::vector<Plan>& peer_
   return DBM_OK;
 }
 
+// K-chunk [k0, k1) (blocks) of this rank's step-s dense panels: one 2-D copy-engine pull per remote
+// operand (rows x chunk width, pitch = the panel's leading dimension).  Statistics count the whole
+// panel once (count == true on the first chunk).
+dbm_status post_pulls_chunk(dbm_ctx ctx, const Plan& p, const std::vector<Plan>& peer_plan, int s, char* ws, int bufA,
+                            int bufB, int64_t k0, int64_t k1, bool count, int64_t* sent, int64_t* recv) {
+  for (const XOp& op : exchange_ops(p, s)) {
+    if (op.send) {
+      if (count) *sent += op.bytes;
+      continue;
+    }
+    const Plan& q = peer_plan[op.peer];
+    const size_t src_off = op.operand == 0 ? q.ownA_off[op.kappa] : q.ownB_off[op.kappa];
+    ARG_CHECK(src_off != SIZE_MAX && ctx->peer_ws[op.peer], DBM_ERR_PLAN, "peer panel not in its workspace");
+    const int64_t rows = (op.operand == 0 ? p.mloc : p.nloc) * p.bs, ld = p.ld_panel(op.kappa);
+    const size_t off = (size_t)(k0 * p.bs) * 8, width = (size_t)((k1 - k0) * p.bs) * 8;
+    char* dst = ws + (op.operand == 0 ? p.off_recvA[bufA] : p.off_recvB[bufB]) + off;
+    const char* src = ctx->peer_ws[op.peer] + src_off + off;
+    if (rows && width)
+      CUDA_TRY(ctx, cudaMemcpy2DAsync(dst, ld * 8, src, ld * 8, width, rows, cudaMemcpyDeviceToDevice, ctx->comm));
+    if (count) *recv += op.bytes;
+  }
+  return DBM_OK;
+}
+
 __global__ void scale_kernel(double* __restrict__ x, int64_t n, double beta) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     x[i] = beta == 0.0 ? 0.0 : beta * x[i];
@@ -936,6 +960,8 @@ extern "C" dbm_status dbm_multiply(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_
   cudaEvent_t ev_ready = nullptr;
   int bufA_of[64], bufB_of[64];
   std::vector<Plan> peer_plan;
+  int nsub0 = 1;               // K-chunks of the step-0 pull (copy-engine transport, densified)
+  cudaEvent_t ev_c[4] = {nullptr, nullptr, nullptr, nullptr};
   auto exchange = [&](int s) -> dbm_status {
     if (ctx->transport == 0)
       return post_pulls(ctx, p, peer_plan, s, ws, bufA_of[s], bufB_of[s], &st.bytes_sent, &st.bytes_recv);
@@ -963,7 +989,23 @@ extern "C" dbm_status dbm_multiply(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_
           peer_plan[q] = make_plan_raw(ctx->nranks, p.pr, p.pc, q / p.pc, q % p.pc, p.Mb, p.Nb, p.Kb, p.bs, dens,
                                        ctx->chunk_bytes, ctx->transport);
     }
-    if (dbm_status e = exchange(0)) return e;
+    // Step 0 is the one exchange nothing overlaps with (Cannon's initial alignment).  With the copy
+    // engines and densified panels it is pulled in K-chunks, each followed by its GEMM chunk, so only
+    // the first chunk's transfer is exposed.
+    bool remote0 = p.a_src(0) != p.me() || p.b_src(0) != p.me();
+    const int64_t kb0 = p.kb[p.kappa(0)];
+    if (ctx->transport == 0 && dens && remote0 && bs % 2 == 0 && kb0 >= 2) nsub0 = (int)std::min<int64_t>(4, kb0);
+    if (nsub0 > 1) {
+      for (int j = 0; j < nsub0; ++j) {
+        ev_c[j] = get_event(ctx);
+        if (dbm_status e = post_pulls_chunk(ctx, p, peer_plan, 0, ws, bufA_of[0], bufB_of[0], kb0 * j / nsub0,
+                                            kb0 * (j + 1) / nsub0, j == 0, &st.bytes_sent, &st.bytes_recv))
+          return e;
+        CUDA_TRY(ctx, cudaEventRecord(ev_c[j], ctx->comm));
+      }
+    } else if (dbm_status e = exchange(0)) {
+      return e;
+    }
     CUDA_TRY(ctx, cudaEventRecord(ev_x[0], ctx->comm));
   }
 
@@ -975,7 +1017,7 @@ extern "C" dbm_status dbm_multiply(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_
         if (dbm_status e = exchange(s + 1)) return e;
         CUDA_TRY(ctx, cudaEventRecord(ev_x[s + 1], ctx->comm));
       }
-      CUDA_TRY(ctx, cudaStreamWaitEvent(cs, ev_x[s], 0));
+      if (!(s == 0 && nsub0 > 1)) CUDA_TRY(ctx, cudaStreamWaitEvent(cs, ev_x[s], 0));
     }
     const int64_t kbk = p.kb[k];
     // operand panels for this step
@@ -1019,17 +1061,22 @@ extern "C" dbm_status dbm_multiply(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_
         }
       } else {
         const int64_t ld = p.ld_panel(k);
-        GemmArgs g{M, N, kbk * bs, Ap, ld, Bp, ld, Cd, M, 1.0, s == 0 ? 0.0 : 1.0, 1, nullptr};
-        g.splitk = pick_splitk(M, N, g.K, num_sms());
-        g.partial = g.splitk > 1 ? (double*)(ws + p.off_part) : nullptr;
-        {
-          ProfScope ps(ctx, cs, 0, 2.0 * M * N * g.K, 8.0 * (M * g.K + N * g.K + M * N * (s ? 2 : 1)));
+        const int nsub = (s == 0) ? nsub0 : 1;
+        for (int j = 0; j < nsub; ++j) {
+          const int64_t k0 = kbk * j / nsub, k1 = kbk * (j + 1) / nsub;
+          if (nsub > 1) CUDA_TRY(ctx, cudaStreamWaitEvent(cs, ev_c[j], 0));
+          GemmArgs g{M, N, (k1 - k0) * bs, Ap + k0 * bs, ld, Bp + k0 * bs, ld, Cd, M, 1.0,
+                     (s == 0 && j == 0) ? 0.0 : 1.0, 1, nullptr};
+          g.splitk = pick_splitk(M, N, g.K, num_sms());
+          g.partial = g.splitk > 1 ? (double*)(ws + p.off_part) : nullptr;
+          ProfScope ps(ctx, cs, 0, 2.0 * M * N * g.K,
+                       8.0 * (M * g.K + N * g.K + M * N * ((s == 0 && j == 0) ? 1 : 2)));
           CUDA_TRY(ctx, launch_dgemm(g, cs, &launches));
+          ++st.gemm_launches;
         }
-        ++st.gemm_launches;
         st.entries += (M && N) ? 1 : 0;  // densified batches hold one multiplication
         st.stacks += (M && N) ? 1 : 0;
-        st.flops += 2.0 * M * N * g.K;
+        st.flops += 2.0 * M * N * kbk * bs;
       }
     } else if (kbk > 0 && p.mloc * p.nloc > 0) {
       // blocked: Generation (stack chunks) -> batched small-block GEMM
@@ -1090,6 +1137,7 @@ extern "C" dbm_status dbm_multiply(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_
       ctx->ev_pool.push_back(ev_x[s]);
       ctx->ev_pool.push_back(ev_g[s]);
     }
+    for (int j = 0; j < nsub0 && nsub0 > 1; ++j) ctx->ev_pool.push_back(ev_c[j]);
     ctx->ev_pool.push_back(done);
   }
   ctx->launches += launches;

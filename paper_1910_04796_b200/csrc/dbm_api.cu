@@ -527,7 +527,8 @@ struct Plan {
   int64_t chunk_kb = 0, nchunks = 1;
   // workspace regions (byte offsets)
   size_t off_cd = 0, off_ownA = 0, off_ownB = 0, off_recvA[2] = {0, 0}, off_recvB[2] = {0, 0}, off_part = 0;
-  size_t off_trav = 0, off_trip = 0;
+  size_t off_trav = 0, off_trip = 0, off_spart = 0;  // smm split-K partials
+  int64_t spart_runs = 0;                            // capacity: (split x runs) C blocks
   std::vector<size_t> ownA_off, ownB_off;  // per kappa, SIZE_MAX if not owned
   int64_t trip_cap = 0;                     // entries per stack-generation chunk
   size_t total = 0;
@@ -622,6 +623,15 @@ Plan make_plan_raw(int nranks, int pr, int pc, int r, int c, int64_t Mb, int64_t
     const int64_t runs = std::max<int64_t>(8, kTripChunkEntries / maxkb / 8 * 8);
     p.trip_cap = std::min<int64_t>(runs, round_up(std::max<int64_t>(p.mloc * p.nloc, 1), 8)) * maxkb;
     p.off_trip = take((size_t)p.trip_cap * 12);
+    // split-K partials of the smm kernel (rectangular shapes with few, long runs)
+    const int64_t chunk_runs = std::max<int64_t>(1, std::min<int64_t>(p.mloc * p.nloc, p.trip_cap / maxkb));
+    int64_t max_split = 1;
+    for (int k = 0; k < p.L; ++k)
+      if (p.kb[k] > 0) max_split = std::max<int64_t>(max_split, smm_pick_split((int)bs, chunk_runs, p.kb[k]));
+    if (max_split > 1) {
+      p.spart_runs = max_split * chunk_runs;
+      p.off_spart = take((size_t)p.spart_runs * bs * bs * 8);
+    }
   }
   if (nranks > 1) {
     size_t amax = 0, bmax = 0;
@@ -1093,8 +1103,11 @@ extern "C" dbm_status dbm_multiply(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_
         }
         {
           ProfScope ps(ctx, cs, 1, 2.0 * bs * bb * (q1 - q0) * kbk, 16.0 * bb * (q1 - q0) * kbk);
-          CUDA_TRY(ctx, launch_smm((int)bs, trip, q1 - q0, kbk, Ap, Bp, C->arena, alpha, s == 0 ? beta : 1.0, cs,
-                                   &launches));
+          const int nsplit = p.spart_runs ? (int)std::min<int64_t>(smm_pick_split((int)bs, q1 - q0, kbk),
+                                                                   p.spart_runs / (q1 - q0))
+                                          : 1;
+          CUDA_TRY(ctx, launch_smm((int)bs, trip, q1 - q0, kbk, Ap, Bp, C->arena, alpha, s == 0 ? beta : 1.0, nsplit,
+                                   nsplit > 1 ? (double*)(ws + p.off_spart) : nullptr, cs, &launches));
         }
       }
       st.entries += nruns * kbk;

@@ -67,13 +67,17 @@ void launch_stackgen(const int32_t* li, const int32_t* lj, int64_t q0, int64_t q
 void launch_stack_ptr(int64_t nruns, int64_t kb, int64_t cap, int64_t nstacks, int64_t* ptr, cudaStream_t st);
 // Execute stack entries [e0, e1) (whole C-block runs of length kb, consecutive): for each run,
 // C_blk = (first ? beta*C_blk : C_blk) + alpha*sum_k A_blk*B_blk.
+// nsplit > 1 splits each run's K across CTAs (partial: nsplit*nruns*bs*bs doubles, reduced in a
+// fixed order); see smm_pick_split.
 cudaError_t launch_smm(int bs, const int32_t* trip, int64_t nruns, int64_t kb, const double* A, const double* B,
-                       double* C, double alpha, double beta_first, cudaStream_t st, int* launches);
+                       double* C, double alpha, double beta_first, int nsplit, double* partial, cudaStream_t st,
+                       int* launches);
+int smm_pick_split(int bs, int64_t nruns, int64_t kb);
 // DMMA group kernel for bs 22 / 64 (kernels_smm.cu); the generic smm handles other block sizes.
 bool smm_has_tensor_path(int bs);
 int smm_group_runs(int bs);  // runs per CTA group (stack chunks are cut at multiples of it)
 cudaError_t launch_smm_tc(int bs, const int32_t* trip, int64_t nruns, int64_t kb, const double* A, const double* B,
-                          double* C, double alpha, double beta_first, cudaStream_t st);
+                          double* C, double alpha, double beta_first, int nsplit, double* partial, cudaStream_t st);
 
 // ----------------------------------------------------------------- driver
 int num_sms();

@@ -379,7 +379,8 @@ __device__ __forceinline__ void s22_stage(double (&acc)[3][3][2], uint32_t sA, u
 
 __global__ void __launch_bounds__((s22::WARPS + 1) * 32, 1)
     smm22_kernel(const int32_t* __restrict__ trip, int64_t nruns, int64_t kb, const double* __restrict__ A,
-                 const double* __restrict__ B, double* __restrict__ C, double alpha, double beta_first) {
+                 const double* __restrict__ B, double* __restrict__ C, double alpha, double beta_first, int nsplit,
+                 double* __restrict__ partial) {
   using namespace s22;
   extern __shared__ __align__(128) double smem[];
   __shared__ __align__(8) uint64_t full[STAGES], empty[STAGES];
@@ -404,7 +405,12 @@ __global__ void __launch_bounds__((s22::WARPS + 1) * 32, 1)
 
   int stage = 0;
   uint32_t phase = 0;
-  for (int64_t grp = blockIdx.x; grp < ngroups; grp += gridDim.x) {
+  // work item = (group, K split); with nsplit > 1 each item accumulates stages [st0, st1) of its
+  // runs into `partial` (reduced later in a fixed order) instead of updating C
+  for (int64_t item = blockIdx.x; item < ngroups * nsplit; item += gridDim.x) {
+    const int64_t grp = item % ngroups;
+    const int split = (int)(item / ngroups);
+    const int st0 = (int)((int64_t)nst * split / nsplit), st1 = (int)((int64_t)nst * (split + 1) / nsplit);
     const int64_t q0 = grp * RUNS;
     const int nrun_g = (int)(nruns - q0 < RUNS ? nruns - q0 : RUNS);
     if (producer) {
@@ -455,7 +461,7 @@ __global__ void __launch_bounds__((s22::WARPS + 1) * 32, 1)
         const int64_t q = q0 + (owner ? s_rep[u] : 0);
         const int col = owner ? s_isb[u] : 0;
         const double* base = col ? B : A;
-        for (int st = 0; st < nst; ++st) {
+        for (int st = st0; st < st1; ++st) {
           const int kk = st * KK + j;
           const bool valid = owner && kk < kb;
           const uint32_t fb = (uint32_t)__cvta_generic_to_shared(&full[stage]);
@@ -485,7 +491,7 @@ __global__ void __launch_bounds__((s22::WARPS + 1) * 32, 1)
       const int ia = active ? s_ia[my] : 0, ib = active ? s_ib[my] : 0;
       const uint32_t offA = (uint32_t)(ia * SLOT + g) * 8u;        // + k*22 + mi*8
       const uint32_t offB = (uint32_t)(ib * SLOT + g * BS) * 8u;   // + kk*484 + x + ni*8*22
-      for (int st = 0; st < nst; ++st) {
+      for (int st = st0; st < st1; ++st) {
         mbar_wait((uint32_t)__cvta_generic_to_shared(&full[stage]), phase);
         if (active) {
           const uint32_t sb = sbase + (uint32_t)(stage * STAGE) * 8u;
@@ -503,7 +509,8 @@ __global__ void __launch_bounds__((s22::WARPS + 1) * 32, 1)
         }
       }
       if (active) {
-        double* cb = C + (int64_t)trip[3 * ((q0 + warp) * kb) + 2] * BB;
+        double* cb = partial ? partial + ((int64_t)split * nruns + q0 + warp) * BB
+                             : C + (int64_t)trip[3 * ((q0 + warp) * kb) + 2] * BB;
 #pragma unroll
         for (int mi = 0; mi < 3; ++mi) {
           const int m = mi * 8 + g;
@@ -514,8 +521,12 @@ __global__ void __launch_bounds__((s22::WARPS + 1) * 32, 1)
               const int n = ni * 8 + 2 * t + jj;
               if (m < BS && n < BS) {
                 double* p = cb + m + n * BS;
-                const double v = alpha * acc[mi][ni][jj];
-                *p = (beta_first == 0.0) ? v : beta_first * *p + v;
+                if (partial) {
+                  *p = acc[mi][ni][jj];
+                } else {
+                  const double v = alpha * acc[mi][ni][jj];
+                  *p = (beta_first == 0.0) ? v : beta_first * *p + v;
+                }
               }
             }
         }
@@ -525,8 +536,23 @@ __global__ void __launch_bounds__((s22::WARPS + 1) * 32, 1)
   }
 }
 
+// Fixed-order split-K reduction of the smm partials: C_blk = (first ? beta*C : C) + alpha * sum_s P_s.
+__global__ void smm_splitk_reduce(const int32_t* __restrict__ trip, int64_t nruns, int64_t kb, int bb, int nsplit,
+                                  const double* __restrict__ partial, double* __restrict__ C, double alpha,
+                                  double beta_first) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < nruns * bb;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t q = e / bb, w = e - q * bb;
+    double sum = partial[e];
+    for (int s = 1; s < nsplit; ++s) sum += partial[(int64_t)s * nruns * bb + e];
+    double* p = C + (int64_t)trip[3 * (q * kb) + 2] * bb + w;
+    const double v = alpha * sum;
+    *p = (beta_first == 0.0) ? v : beta_first * *p + v;
+  }
+}
+
 cudaError_t launch_smm22(const int32_t* trip, int64_t nruns, int64_t kb, const double* A, const double* B, double* C,
-                         double alpha, double beta_first, cudaStream_t st) {
+                         double alpha, double beta_first, int nsplit, double* partial, cudaStream_t st) {
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(smm22_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s22::SMEM);
@@ -534,8 +560,15 @@ cudaError_t launch_smm22(const int32_t* trip, int64_t nruns, int64_t kb, const d
     attr = true;
   }
   const int64_t ngroups = (nruns + s22::RUNS - 1) / s22::RUNS;
-  const unsigned grid = (unsigned)std::min<int64_t>(ngroups, (int64_t)num_sms());
-  smm22_kernel<<<grid, (s22::WARPS + 1) * 32, s22::SMEM, st>>>(trip, nruns, kb, A, B, C, alpha, beta_first);
+  if (nsplit < 1 || !partial) nsplit = 1;
+  const unsigned grid = (unsigned)std::min<int64_t>(ngroups * nsplit, (int64_t)num_sms());
+  smm22_kernel<<<grid, (s22::WARPS + 1) * 32, s22::SMEM, st>>>(trip, nruns, kb, A, B, C, alpha, beta_first, nsplit,
+                                                               nsplit > 1 ? partial : nullptr);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess || nsplit == 1) return e;
+  const int64_t n = nruns * s22::BB;
+  smm_splitk_reduce<<<(unsigned)std::min<int64_t>((n + 255) / 256, (int64_t)num_sms() * 16), 256, 0, st>>>(
+      trip, nruns, kb, s22::BB, nsplit, partial, C, alpha, beta_first);
   return cudaGetLastError();
 }
 
@@ -545,10 +578,30 @@ bool smm_has_tensor_path(int bs) { return bs == 22 || bs == 64; }
 
 int smm_group_runs(int bs) { return bs == 22 ? s22::RUNS : (bs == 64 ? Cfg64::RUNS : 1); }
 
+// Split the runs' K across CTAs when the groups alone cannot fill the GPU (long, few runs: the
+// rectangular configs on several GPUs).  Returns 1 when no split is needed.
+int smm_pick_split(int bs, int64_t nruns, int64_t kb) {
+  if (bs != 22) return 1;
+  const int64_t ngroups = (nruns + s22::RUNS - 1) / s22::RUNS, sms = num_sms();
+  const int64_t nst = (kb * s22::BS + s22::KS - 1) / s22::KS;
+  if (ngroups >= 2 * sms) return 1;
+  int best = 1;
+  double best_t = 1e300;
+  for (int s = 1; s <= 16 && nst / s >= 64; ++s) {
+    const double rounds = (double)((ngroups * s + sms - 1) / sms);
+    const double t = rounds / s * (1.0 + 0.01 * (s - 1));  // + reduction traffic
+    if (t < best_t * (1.0 - 1e-9)) {
+      best_t = t;
+      best = s;
+    }
+  }
+  return best;
+}
+
 cudaError_t launch_smm_tc(int bs, const int32_t* trip, int64_t nruns, int64_t kb, const double* A, const double* B,
-                          double* C, double alpha, double beta_first, cudaStream_t st) {
+                          double* C, double alpha, double beta_first, int nsplit, double* partial, cudaStream_t st) {
   if (nruns <= 0 || kb <= 0) return cudaSuccess;
-  if (bs == 22) return launch_smm22(trip, nruns, kb, A, B, C, alpha, beta_first, st);
+  if (bs == 22) return launch_smm22(trip, nruns, kb, A, B, C, alpha, beta_first, nsplit, partial, st);
   if (bs == 64) return launch_group<Cfg64>(trip, nruns, kb, A, B, C, alpha, beta_first, st);
   return cudaErrorInvalidValue;
 }

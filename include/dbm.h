@@ -109,6 +109,13 @@ dbm_status dbm_ctx_profile_read(dbm_ctx ctx, int kernel, double* ms_out, int64_t
  * 1 = NCCL grouped ncclSend / ncclRecv.
  * Every rank must use the same transport.  Changes dbm_multiply_workspace() for the blocked path. */
 dbm_status dbm_ctx_set_transport(dbm_ctx ctx, int transport);
+/* MPI-level algorithm (§II): 0 (default) = Cannon (any shape, O(1/sqrt(P)) volume);
+ * 1 = tall-and-skinny (one large dimension; reading R14): rank p = r*Pc + c computes the
+ * partial product over the K blocks {k : k mod P == p} after gathering A[:, S_p] from its grid
+ * column and B[S_p, :] from grid row p mod Pr, then every rank sums its C blocks out of all P partials
+ * in rank order.  Requires the densified path and the copy-engine transport (DBM_ERR_ARG otherwise).
+ * Every rank must use the same algorithm.  Changes dbm_multiply_workspace(). */
+dbm_status dbm_ctx_set_algorithm(dbm_ctx ctx, int algorithm);
 /* Densified path on a single rank: byte budget of one K-chunk of dense A + B (default 16 GiB).
  * K is densified and multiplied chunk by chunk (GEMM-accumulate), so 63,360^3 fits in HBM.
  * bytes >= 1; changes dbm_multiply_workspace(). */
@@ -172,6 +179,11 @@ dbm_status dbm_multiply(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_matrix B, d
  * NULL ops and bytes to query the count. */
 dbm_status dbm_plan_exchange(int pr, int pc, int myrow, int mycol, int64_t Mb, int64_t Nb, int64_t Kb, int32_t bs,
                              dbm_path path, int step, int32_t* ops, int64_t* bytes, int* n_ops);
+
+/* Host-only: bytes rank (myrow, mycol) receives from / sends to its peers in one tall-and-skinny
+ * multiply of Mb x Kb by Kb x Nb blocks of bs (gather of A and B pieces + the C-share reduction). */
+dbm_status dbm_plan_tallskinny(int pr, int pc, int myrow, int mycol, int64_t Mb, int64_t Nb, int64_t Kb, int32_t bs,
+                               int64_t* bytes_recv, int64_t* bytes_sent);
 
 /* ------------------------------------------------------- densify / undensify */
 /* Densify the whole local share ("a single block is formed from all the blocks

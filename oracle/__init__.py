@@ -67,6 +67,7 @@ def lib():
             "orc_cannon_bytes": (None, [_i64, _i64, _i64, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
                                         _pi64, _pi64]),
             "orc_densified_dims": (None, [_i64] * 5 + [_pi64] * 4),
+            "orc_ts_bytes": (None, [_i64, _i64, _i64, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, _pi64, _pi64]),
             "orc_densify_cols": (None, [_pd, _i64, _i64, C.c_int, _pi64, _i64, _pd, _i64, C.c_int]),
             "orc_densify_rows": (None, [_pd, _i64, _i64, C.c_int, _pi64, _i64, _pd, _i64, C.c_int]),
             "orc_undensify": (None, [_pd, _i64, _i64, _i64, C.c_int, _dbl, _dbl, _pd]),
@@ -190,6 +191,12 @@ def cannon_step(pr, pc, r, c, s) -> tuple[int, int, int]:
 def cannon_bytes(Mb, Nb, Kb, bs, pr, pc, r, c) -> tuple[int, int]:
     rv, sd = C.c_int64(), C.c_int64()
     lib().orc_cannon_bytes(Mb, Nb, Kb, bs, pr, pc, r, c, C.byref(rv), C.byref(sd))
+    return rv.value, sd.value
+
+
+def ts_bytes(Mb, Nb, Kb, bs, pr, pc, r, c) -> tuple[int, int]:
+    rv, sd = C.c_int64(), C.c_int64()
+    lib().orc_ts_bytes(Mb, Nb, Kb, bs, pr, pc, r, c, C.byref(rv), C.byref(sd))
     return rv.value, sd.value
 
 

@@ -317,6 +317,41 @@ void orc_cannon_bytes(int64_t Mb, int64_t Nb, int64_t Kb, int bs, int pr, int pc
   *sent = sd;
 }
 
+/* Tall-and-skinny (§II "only for tall-and-skinny matrices ... we use an optimized algorithm,   */
+/* where the amount of communicated data by each process scales as O(1)").        */
+/* Reading R14: rank p takes K blocks S_p = {k : k mod P == p}, needs every A(i, k) and B(k, j)    */
+/* with k in S_p, computes the partial C_p, and receives its own C blocks from every other partial. */
+/* Bytes counted by brute force over blocks.                                                        */
+void orc_ts_bytes(int64_t Mb, int64_t Nb, int64_t Kb, int bs, int pr, int pc, int r, int c, int64_t* recv,
+                  int64_t* sent) {
+  const int P = pr * pc, me = r * pc + c;
+  const int64_t bb8 = (int64_t)bs * bs * 8;
+  int64_t rv = 0, sd = 0;
+  for (int q = 0; q < P; ++q) {
+    for (int64_t k = q; k < Kb; k += P) {
+      for (int64_t i = 0; i < Mb; ++i) {
+        const int own = orc_owner_rank(i, k, pr, pc);
+        if (q == me && own != me) rv += bb8;
+        if (q != me && own == me) sd += bb8;
+      }
+      for (int64_t j = 0; j < Nb; ++j) {
+        const int own = orc_owner_rank(k, j, pr, pc);
+        if (q == me && own != me) rv += bb8;
+        if (q != me && own == me) sd += bb8;
+      }
+    }
+  }
+  /* reduction: each C block's owner receives it from the P-1 other partials */
+  for (int64_t i = 0; i < Mb; ++i)
+    for (int64_t j = 0; j < Nb; ++j) {
+      const int own = orc_owner_rank(i, j, pr, pc);
+      if (own == me) rv += (int64_t)(P - 1) * bb8;
+      else sd += bb8;
+    }
+  *recv = rv;
+  *sent = sd;
+}
+
 /* ------------------------------------------------------------------------- */
 /* Densification (§III): "a single block is formed from all the      */
 /* blocks assigned to each thread"; Eqs. (1)-(2) give its size.                */

@@ -72,6 +72,10 @@ void orc_cannon_step(int pr, int pc, int r, int c, int s, int* kappa, int* a_src
 void orc_cannon_bytes(int64_t Mb, int64_t Nb, int64_t Kb, int bs, int pr, int pc, int r, int c,
                       int64_t* bytes_recv, int64_t* bytes_sent);
 
+/* ---- Tall-and-skinny (§II), reading R14 ---- */
+void orc_ts_bytes(int64_t Mb, int64_t Nb, int64_t Kb, int bs, int pr, int pc, int r, int c, int64_t* bytes_recv,
+                  int64_t* bytes_sent);
+
 /* ---- Densification (§III, Eqs. (1)-(2)) ---- */
 void orc_densified_dims(int64_t M, int64_t N, int64_t K, int64_t ptilde, int64_t t, int64_t* a_rows, int64_t* a_cols,
                         int64_t* b_rows, int64_t* b_cols);

@@ -109,6 +109,7 @@ struct dbm_ctx_s {
   // Cannon transport: 0 = copy engines pulling peer panels through CUDA IPC mappings (default),
   // 1 = NCCL grouped send/recv.
   int transport = 0;
+  int algorithm = 0;  // 0 = Cannon, 1 = tall-and-skinny
   void* ipc_ws = nullptr;                 // workspace the peer mappings were built for
   int64_t ipc_ws_bytes = 0;
   std::vector<char*> peer_ws;             // peer workspaces mapped into this process (nullptr = self)

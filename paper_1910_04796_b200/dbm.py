@@ -59,6 +59,9 @@ _SIGS = {
     "dbm_ctx_launch_count": (C.c_int, [_P, C.POINTER(_I64)]),
     "dbm_ctx_set_dense_chunk_bytes": (C.c_int, [_P, _I64]),
     "dbm_ctx_set_transport": (C.c_int, [_P, C.c_int]),
+    "dbm_ctx_set_algorithm": (C.c_int, [_P, C.c_int]),
+    "dbm_plan_tallskinny": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, _I64, _I64, _I64, C.c_int32,
+                                      C.POINTER(_I64), C.POINTER(_I64)]),
     "dbm_plan_exchange": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, _I64, _I64, _I64, C.c_int32, C.c_int,
                                     C.c_int, _P, _P, C.POINTER(C.c_int)]),
     "dbm_ctx_destroy": (C.c_int, [_P]),
@@ -177,6 +180,12 @@ class Context:
         t = {"ce": 0, "nccl": 1}.get(transport, transport)
         _check(load().dbm_ctx_set_transport(self.h, int(t)))
         self.transport = t
+
+    def set_algorithm(self, algorithm: str | int) -> None:
+        """'cannon' (default) or 'tallskinny' (densified path, copy-engine transport)."""
+        a = {"cannon": 0, "tallskinny": 1}.get(algorithm, algorithm)
+        _check(load().dbm_ctx_set_algorithm(self.h, int(a)))
+        self.algorithm = a
 
     def set_dense_chunk_bytes(self, nbytes: int) -> None:
         _check(load().dbm_ctx_set_dense_chunk_bytes(self.h, nbytes))
@@ -325,6 +334,13 @@ def plan_exchange(pr: int, pc: int, myrow: int, mycol: int, Mb: int, Nb: int, Kb
                                  by.ctypes.data, C.byref(n)))
     return [{"send": bool(ops[4 * i]), "operand": "AB"[ops[4 * i + 1]], "peer": int(ops[4 * i + 2]),
              "kappa": int(ops[4 * i + 3]), "bytes": int(by[i])} for i in range(n.value)]
+
+
+def plan_tallskinny(pr: int, pc: int, myrow: int, mycol: int, Mb: int, Nb: int, Kb: int, bs: int) -> tuple[int, int]:
+    """Host-only: (bytes received, bytes sent) of rank (myrow, mycol) in one tall-and-skinny multiply."""
+    rv, sd = C.c_int64(), C.c_int64()
+    _check(load().dbm_plan_tallskinny(pr, pc, myrow, mycol, Mb, Nb, Kb, bs, C.byref(rv), C.byref(sd)))
+    return rv.value, sd.value
 
 
 def debug_stacks(ctx: Context, A: Matrix, B: Matrix, C_: Matrix, step: int = 0, cap: int = 0):

@@ -30,13 +30,15 @@ def main():
     grids = [(p, world // p) for p in range(1, world + 1) if world % p == 0]
     shapes = [(352, 352, 352, 22), (704, 528, 1100, 22), (384, 640, 1280, 64), (66, 154, 198, 22), (44, 44, 22, 22)]
     failures = 0
-    cases = [(pr, pc, tr) for (pr, pc) in grids for tr in ("ce", "nccl")]
-    for pr, pc, transport in cases:
+    cases = [(pr, pc, tr, "cannon") for (pr, pc) in grids for tr in ("ce", "nccl")]
+    cases += [(pr, pc, "ce", "tallskinny") for (pr, pc) in grids]
+    for pr, pc, transport, algo in cases:
         ctx = dbm.Context.from_distributed(pr=pr, pc=pc)
         ctx.set_transport(transport)
+        ctx.set_algorithm(algo)
         r, c = ctx.myrow, ctx.mycol
         for (M, N, K, bs) in shapes:
-            for path in ("densified", "blocked"):
+            for path in (("densified", "blocked") if algo == "cannon" else ("densified",)):
                 for kind in (0, 1):
                     A, B, C = dbm.Matrix(ctx, M, K, bs), dbm.Matrix(ctx, K, N, bs), dbm.Matrix(ctx, M, N, bs)
                     A.fill_random(SEED, 0, kind)
@@ -59,14 +61,17 @@ def main():
                     else:
                         err = float(np.linalg.norm(got - ref) / max(np.linalg.norm(ref), 1e-300)) if ref.size else 0.0
                         ok_val = err <= 1e-12
-                    rv, sd = orc.cannon_bytes(M // bs, N // bs, K // bs, bs, pr, pc, r, c)
+                    if algo == "cannon":
+                        rv, sd = orc.cannon_bytes(M // bs, N // bs, K // bs, bs, pr, pc, r, c)
+                    else:
+                        rv, sd = orc.ts_bytes(M // bs, N // bs, K // bs, bs, pr, pc, r, c)
                     ok_bytes = (st["bytes_recv"], st["bytes_sent"]) == (rv, sd)
                     flags = torch.tensor([0 if (ok_val and ok_bytes) else 1], device=dev)
                     dist.all_reduce(flags)
                     if flags.item():
                         failures += 1
                     if rank == 0 or not (ok_val and ok_bytes):
-                        print(json.dumps({"rank": rank, "grid": f"{pr}x{pc}", "transport": transport, "shape": [M, N, K, bs], "path": path,
+                        print(json.dumps({"rank": rank, "grid": f"{pr}x{pc}", "transport": transport, "algo": algo, "shape": [M, N, K, bs], "path": path,
                                           "kind": kind, "err": err, "ok": bool(ok_val), "bytes_ok": ok_bytes,
                                           "recv": st["bytes_recv"], "expect_recv": rv}), flush=True)
         ctx.close()

@@ -102,3 +102,11 @@ def test_plan_exchange_matches_oracle_schedule(dbm, orc, pr, pc, path):
                 rv, sd = orc.cannon_bytes(Mb, Nb, Kb, bs, pr, pc, r, c)
                 assert tot_recv.get(r * pc + c, 0) == rv
                 assert tot_sent.get(r * pc + c, 0) == sd
+
+
+@pytest.mark.parametrize("pr,pc", [(1, 2), (2, 2), (2, 4), (4, 2), (1, 4), (3, 2)])
+def test_plan_tallskinny_matches_oracle(dbm, orc, pr, pc):
+    for shape in [(22, 22, 301, 64), (7, 5, 40, 22), (3, 9, 17, 2)]:
+        for r in range(pr):
+            for c in range(pc):
+                assert dbm.plan_tallskinny(pr, pc, r, c, *shape) == orc.ts_bytes(*shape[:3], shape[3], pr, pc, r, c)

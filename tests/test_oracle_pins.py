@@ -399,3 +399,44 @@ def test_rows_and_freivalds_from_seeds(orc):
     C = Cin.copy()
     orc.multiply_blocked(M // bs, N // bs, K // bs, bs, 0.75, A, B, -1.25, C)
     assert np.array_equal(orc.arena_to_dense(C, M // bs, N // bs, bs)[rows], got)
+
+
+# ----------------------------------------------------------------- tall-and-skinny (reading R14)
+@pytest.mark.parametrize("pr,pc", [(1, 2), (2, 2), (2, 4), (1, 4), (4, 1), (3, 2)])
+def test_tallskinny_partition_computes_the_product(orc, pr, pc):
+    """Simulate R14 with numpy: rank p sums A[:, S_p] B[S_p, :] over S_p = {k : k mod P == p}; every
+    k in S_p lies in p's grid column (k mod Pc == c); the sum of the P partials is A @ B."""
+    P = pr * pc
+    Mb, Nb, Kb, bs = 5, 3, 23, 2
+    rng = np.random.default_rng(P)
+    A = rng.uniform(-1, 1, (Mb * bs, Kb * bs))
+    B = rng.uniform(-1, 1, (Kb * bs, Nb * bs))
+    total = np.zeros((Mb * bs, Nb * bs))
+    for p in range(P):
+        r, c = divmod(p, pc)
+        ks = [k for k in range(Kb) if k % P == p]
+        assert all(k % pc == c for k in ks)
+        assert all(orc.owner_rank(k, 0, pr, pc) // pc == p % pr for k in ks)  # B rows in grid row p mod Pr
+        idx = np.concatenate([np.arange(k * bs, k * bs + bs) for k in ks]) if ks else np.array([], int)
+        total += A[:, idx] @ B[idx, :]
+    assert np.allclose(total, A @ B, atol=1e-12)
+
+
+def test_tallskinny_bytes(orc):
+    """Reduction-only volume (K = 0) is (P-1) x the rank's C share: O(1) in P for fixed M, N (P:169);
+    on the paper's rectangular shape at 2x4 the gather moves ~3x less than Cannon."""
+    for pr, pc in [(1, 4), (2, 2), (2, 4), (4, 4)]:
+        P = pr * pc
+        Mb = Nb = 16
+        for r in range(pr):
+            for c in range(pc):
+                rv, _ = orc.ts_bytes(Mb, Nb, 0, 4, pr, pc, r, c)
+                assert rv == (P - 1) * orc.local_count(Mb, pr, r) * orc.local_count(Nb, pc, c) * 16 * 8
+    Mb, Nb, Kb, bs = 22, 22, 30976, 64  # 1,408 x 1,408 x 1,982,464 bs 64
+    ts = max(orc.ts_bytes(Mb, Nb, Kb, bs, 2, 4, r, c)[0] for r in range(2) for c in range(4))
+    cannon = max(orc.cannon_bytes(Mb, Nb, Kb, bs, 2, 4, r, c)[0] for r in range(2) for c in range(4))
+    assert ts < cannon / 2.5
+    # gathers: 1x4 needs no A (all rows local), only B pieces from the 3 peers
+    rv, _ = orc.ts_bytes(8, 8, 40, 2, 1, 4, 0, 1)
+    kp = orc.local_count(40, 4, 1)
+    assert rv == kp * 6 * 4 * 8 + 3 * 8 * 2 * 4 * 8  # B: kp x (8 - 2 local cols) blocks; C: 3 x (8 x 2) blocks

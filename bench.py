@@ -48,6 +48,8 @@ def parse():
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--transport", default="ce", choices=["ce", "nccl"], help="Cannon panel transport (N>1)")
     p.add_argument("--grid", default="", help="force the process grid, e.g. 1x4 (default: reading R1)")
+    p.add_argument("--algorithm", default="cannon", choices=["cannon", "tallskinny"],
+                   help="MPI-level algorithm (P:168 Cannon / P:169 tall-and-skinny), N>1")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--e2e-steps", type=int, default=1)
@@ -180,6 +182,7 @@ def main():
         pr, pc = (int(x) for x in args.grid.split("x")) if args.grid else (0, 0)
         ctx = dbm.Context.from_distributed(pr=pr, pc=pc)
         ctx.set_transport(args.transport)
+        ctx.set_algorithm(args.algorithm)
     else:
         ctx = dbm.Context(device=local)
     stream = torch.cuda.current_stream(dev)
@@ -254,6 +257,7 @@ def main():
             "config": {"workload": name, "M": M, "N": N, "K": K, "block_size": bs, "path": path,
                        "grid": f"{ctx.pr}x{ctx.pc}", "parallelism": f"cannon{ctx.pr}x{ctx.pc}",
                        "transport": (args.transport if world > 1 else None),
+                       "algorithm": (args.algorithm if world > 1 else "local"),
                        "l2": "inputs >= 8 GB per matrix >> 126 MB L2; no flush", "alpha": alpha, "beta": beta},
             "pct_fp64_peak": 100.0 * tflops / (world * FP64_PEAK_MEASURED),
             "roofline": {"kernel": kern, "bound": "tensor", "achieved": achieved, "peak": FP64_PEAK_MEASURED,

@@ -282,8 +282,9 @@ def main():
 
 
 def run_e2e(args, ctx, dbm, torch, A, B, C, path, ws, stream, barrier, maxrank, flop):
-    """Same metric through the public API with HOST buffers: per step H2D of A and B from pinned host
-    memory, the multiply, D2H of C (beta = 0, so C_in is not read: BLAS convention, reading R8)."""
+    """Same metric through the public C-ABI call with HOST buffers (dbm_multiply_host): per step the H2D
+    of A and B from pinned host memory (streamed in K-chunks under the GEMMs on one GPU), the multiply
+    and the D2H of C (beta = 0, so C_in is not read: BLAS convention, reading R8)."""
     try:
         hA = torch.empty(A.arena_bytes // 8, dtype=torch.float64, pin_memory=True)
         hB = torch.empty(B.arena_bytes // 8, dtype=torch.float64, pin_memory=True)
@@ -298,11 +299,8 @@ def run_e2e(args, ctx, dbm, torch, A, B, C, path, ws, stream, barrier, maxrank, 
     B.download(hB)
     ctx.sync()
 
-    def step():
-        A.upload(hA)
-        B.upload(hB)
-        dbm.multiply(ctx, 1.0, A, B, 0.0, C, path, workspace=ws)
-        C.download(hC)
+    def step():  # one C-ABI call with host buffers (dbm_multiply_host: streamed H2D, D2H of C)
+        dbm.multiply_host(ctx, 1.0, A, B, 0.0, C, hA, hB, hC, path, workspace=ws)
 
     step()  # warm-up
     barrier()

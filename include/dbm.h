@@ -185,6 +185,18 @@ dbm_status dbm_plan_exchange(int pr, int pc, int myrow, int mycol, int64_t Mb, i
 dbm_status dbm_plan_tallskinny(int pr, int pc, int myrow, int mycol, int64_t Mb, int64_t Nb, int64_t Kb, int32_t bs,
                                int64_t* bytes_recv, int64_t* bytes_sent);
 
+/* dbm_multiply with HOST-resident operands (the paper's setting: "the matrices are allocated on the
+ * host system"; double buffering with CUDA streams and events; page-locked memory).
+ * A_host, B_host, C_host are this rank's arenas in host memory (arena layout, arena_bytes each); the
+ * device arenas of A, B, C are the staging copies.  Pinned host buffers: A and B are streamed on the
+ * library's copy stream — on a single rank the densified path uploads K-chunk j+1 while chunk j is
+ * densified and multiplied — C_host is read only if beta != 0, and C is copied back to C_host.
+ * Enqueued on the ctx stream; C_host is valid after the stream reaches the end (dbm_ctx_sync).
+ * Pageable host buffers: staged synchronously (no overlap).  Errors as dbm_multiply. */
+dbm_status dbm_multiply_host(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_matrix B, double beta, dbm_matrix C,
+                             dbm_path path, int32_t stack_cap, void* workspace, int64_t workspace_bytes,
+                             const void* A_host, const void* B_host, void* C_host, dbm_stats* stats);
+
 /* ------------------------------------------------------- densify / undensify */
 /* Densify the whole local share ("a single block is formed from all the blocks
  * assigned to each thread"): dense is (mloc*bs) x (nloc*bs), layout 0 = column-major with

@@ -1114,9 +1114,68 @@ extern "C" dbm_status dbm_plan_tallskinny(int pr, int pc, int myrow, int mycol, 
   return DBM_OK;
 }
 
+// Host-resident operands (dbm_multiply_host): pinned host arenas streamed to the device arenas on
+// the comm stream; chunk_ev[ch] marks A/B K-chunk ch of the single-rank densified path uploaded,
+// all_ev everything uploaded (other paths), c_ev C_in uploaded.
+struct HostIO {
+  const double* A = nullptr;
+  const double* B = nullptr;
+  double* C = nullptr;
+  std::vector<cudaEvent_t> chunk_ev;
+  cudaEvent_t all_ev = nullptr, c_ev = nullptr;
+};
+
+namespace {
+dbm_status multiply_impl(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_matrix B, double beta, dbm_matrix C,
+                         dbm_path path, int32_t stack_cap, void* workspace, int64_t ws_bytes, dbm_stats* stats,
+                         HostIO* hio);
+}
+
 extern "C" dbm_status dbm_multiply(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_matrix B, double beta, dbm_matrix C,
                                    dbm_path path, int32_t stack_cap, void* workspace, int64_t ws_bytes,
                                    dbm_stats* stats) {
+  return multiply_impl(ctx, alpha, A, B, beta, C, path, stack_cap, workspace, ws_bytes, stats, nullptr);
+}
+
+extern "C" dbm_status dbm_multiply_host(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_matrix B, double beta,
+                                        dbm_matrix C, dbm_path path, int32_t stack_cap, void* workspace,
+                                        int64_t ws_bytes, const void* A_host, const void* B_host, void* C_host,
+                                        dbm_stats* stats) {
+  CTX_OK(ctx);
+  ARG_CHECK(A_host && B_host && C_host, DBM_ERR_ARG, "null host buffer");
+  auto pinned = [](const void* p) {
+    cudaPointerAttributes at;
+    const bool ok = cudaPointerGetAttributes(&at, p) == cudaSuccess && at.type == cudaMemoryTypeHost;
+    cudaGetLastError();
+    return ok;
+  };
+  if (!pinned(A_host) || !pinned(B_host) || !pinned(C_host)) {
+    // pageable: staged through the pinned double buffer, no overlap with the multiply
+    if (dbm_status e = dbm_matrix_upload(A, A_host)) return e;
+    if (dbm_status e = dbm_matrix_upload(B, B_host)) return e;
+    if (beta != 0.0)
+      if (dbm_status e = dbm_matrix_upload(C, C_host)) return e;
+    if (dbm_status e = dbm_multiply(ctx, alpha, A, B, beta, C, path, stack_cap, workspace, ws_bytes, stats)) return e;
+    return dbm_matrix_download(C, C_host);
+  }
+  HostIO hio;
+  hio.A = (const double*)A_host;
+  hio.B = (const double*)B_host;
+  hio.C = (double*)C_host;
+  dbm_status e = multiply_impl(ctx, alpha, A, B, beta, C, path, stack_cap, workspace, ws_bytes, stats, &hio);
+  for (cudaEvent_t ev : hio.chunk_ev) ctx->ev_pool.push_back(ev);
+  if (hio.all_ev) ctx->ev_pool.push_back(hio.all_ev);
+  if (hio.c_ev) ctx->ev_pool.push_back(hio.c_ev);
+  if (e) return e;
+  const size_t cbytes = (size_t)(C->mloc * C->nloc) * C->bs * C->bs * 8;
+  if (cbytes) CUDA_TRY(ctx, cudaMemcpyAsync(C_host, C->arena, cbytes, cudaMemcpyDeviceToHost, ctx->stream));
+  return DBM_OK;
+}
+
+namespace {
+dbm_status multiply_impl(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_matrix B, double beta, dbm_matrix C,
+                         dbm_path path, int32_t stack_cap, void* workspace, int64_t ws_bytes, dbm_stats* stats,
+                         HostIO* hio) {
   CTX_OK(ctx);
   ARG_CHECK(path == DBM_PATH_BLOCKED || path == DBM_PATH_DENSIFIED, DBM_ERR_ARG, "bad path");
   ARG_CHECK(stack_cap >= 0, DBM_ERR_ARG, "negative stack cap");
@@ -1130,6 +1189,14 @@ extern "C" dbm_status dbm_multiply(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_
               "workspace smaller than dbm_multiply_workspace()");
     dbm_stats st{};
     int launches = 0;
+    if (hio) {  // host operands: plain uploads ahead of the multiply on the compute stream
+      const size_t bb8 = (size_t)A->bs * A->bs * 8;
+      const size_t ab = (size_t)(A->mloc * A->nloc) * bb8, bbytes = (size_t)(B->mloc * B->nloc) * bb8,
+                   cb = (size_t)(C->mloc * C->nloc) * bb8;
+      if (ab) CUDA_TRY(ctx, cudaMemcpyAsync(A->arena, hio->A, ab, cudaMemcpyHostToDevice, ctx->stream));
+      if (bbytes) CUDA_TRY(ctx, cudaMemcpyAsync(B->arena, hio->B, bbytes, cudaMemcpyHostToDevice, ctx->stream));
+      if (beta != 0.0 && cb) CUDA_TRY(ctx, cudaMemcpyAsync(C->arena, hio->C, cb, cudaMemcpyHostToDevice, ctx->stream));
+    }
     if (alpha == 0.0 || A->Nb == 0) {
       const int64_t n = C->mloc * C->nloc * (int64_t)C->bs * C->bs;
       if (n) {
@@ -1150,6 +1217,49 @@ extern "C" dbm_status dbm_multiply(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_
   ARG_CHECK(workspace != nullptr && ws_bytes >= (int64_t)p.total, DBM_ERR_WORKSPACE,
             "workspace smaller than dbm_multiply_workspace()");
   const int64_t cap = stack_cap ? stack_cap : 30000;
+  if (hio) {
+    // Stream the host operands in (P:174 double buffering; P:200 page-locked host memory).  The
+    // single-rank densified path consumes A and B one K-chunk at a time, so chunk ch's upload only
+    // has to precede chunk ch's densify and overlaps the GEMMs of the chunks before it.
+    cudaStream_t cp = ctx->comm;
+    CUDA_TRY(ctx, cudaStreamWaitEvent(cp, [&] {
+      cudaEvent_t e0 = get_event(ctx);
+      cudaEventRecord(e0, ctx->stream);  // previous work on the arenas is done
+      hio->chunk_ev.push_back(e0);
+      return e0;
+    }(), 0));
+    const size_t bb8 = (size_t)p.bs * p.bs * 8;
+    const bool chunked = ctx->nranks == 1 && dens && alpha != 0.0 && p.Kb > 0;
+    if (chunked) {
+      for (int64_t ch = 0; ch < p.nchunks; ++ch) {
+        const int64_t k0 = ch * p.chunk_kb, nk = std::min(p.chunk_kb, p.Kb - k0);
+        if (p.mloc && nk)
+          CUDA_TRY(ctx, cudaMemcpy2DAsync((char*)A->arena + k0 * bb8, p.kA * bb8, (const char*)hio->A + k0 * bb8,
+                                          p.kA * bb8, nk * bb8, p.mloc, cudaMemcpyHostToDevice, cp));
+        if (p.nloc && nk)
+          CUDA_TRY(ctx, cudaMemcpyAsync((char*)B->arena + k0 * p.nloc * bb8, (const char*)hio->B + k0 * p.nloc * bb8,
+                                        nk * p.nloc * bb8, cudaMemcpyHostToDevice, cp));
+        cudaEvent_t e = get_event(ctx);
+        CUDA_TRY(ctx, cudaEventRecord(e, cp));
+        hio->chunk_ev.push_back(e);  // chunk_ev[ch + 1]
+      }
+    } else {
+      const size_t ab = (size_t)(A->mloc * A->nloc) * bb8, bbytes = (size_t)(B->mloc * B->nloc) * bb8;
+      if (ab && alpha != 0.0) CUDA_TRY(ctx, cudaMemcpyAsync(A->arena, hio->A, ab, cudaMemcpyHostToDevice, cp));
+      if (bbytes && alpha != 0.0) CUDA_TRY(ctx, cudaMemcpyAsync(B->arena, hio->B, bbytes, cudaMemcpyHostToDevice, cp));
+      hio->all_ev = get_event(ctx);
+      CUDA_TRY(ctx, cudaEventRecord(hio->all_ev, cp));
+    }
+    const size_t cb = (size_t)(C->mloc * C->nloc) * bb8;
+    if (beta != 0.0 && cb) CUDA_TRY(ctx, cudaMemcpyAsync(C->arena, hio->C, cb, cudaMemcpyHostToDevice, cp));
+    hio->c_ev = get_event(ctx);
+    CUDA_TRY(ctx, cudaEventRecord(hio->c_ev, cp));
+    if (!chunked || beta != 0.0 || alpha == 0.0 || p.Kb == 0) {
+      // paths that touch C (or all of A, B) early wait for everything
+      if (hio->all_ev) CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->stream, hio->all_ev, 0));
+      if (!chunked || alpha == 0.0 || p.Kb == 0) CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->stream, hio->c_ev, 0));
+    }
+  }
   dbm_stats st{};
   st.steps = p.L;
   int launches = 0;
@@ -1300,6 +1410,7 @@ extern "C" dbm_status dbm_multiply(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_
           const int64_t ld = round_up(p.chunk_kb * bs, 2);
           double* Ad = (double*)(ws + p.off_ownA);
           double* Bd = (double*)(ws + p.off_ownB);
+          if (hio) CUDA_TRY(ctx, cudaStreamWaitEvent(cs, hio->chunk_ev[ch + 1], 0));  // chunk ch uploaded
           {
             ProfScope ps(ctx, cs, 2, 0.0, 16.0 * (M + N) * nk * bs);
             launch_densify_cols(A->arena, p.mloc, p.kA, (int)bs, k0, 1, nk, Ad, ld, 1, cs);
@@ -1377,6 +1488,7 @@ extern "C" dbm_status dbm_multiply(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_
     CUDA_TRY(ctx, cudaStreamWaitEvent(cs, ev_x[p.L - 1], 0));
   }
   if (dens && M * N > 0) {
+    if (hio && hio->c_ev) CUDA_TRY(ctx, cudaStreamWaitEvent(cs, hio->c_ev, 0));  // C_in uploaded
     ProfScope ps(ctx, cs, 3, 0.0, (beta == 0.0 ? 16.0 : 24.0) * M * N);
     launch_undensify((double*)(ws + p.off_cd), M, 1, 0, p.mloc, p.nloc, (int)bs, alpha, beta, C->arena, cs);
     ++launches;
@@ -1407,6 +1519,8 @@ extern "C" dbm_status dbm_multiply(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_
   if (stats) *stats = st;
   return DBM_OK;
 }
+
+}  // namespace
 
 // ====================================================================== debug entry points
 extern "C" dbm_status dbm_debug_stacks(dbm_ctx ctx, dbm_matrix A, dbm_matrix B, dbm_matrix C, int step, int32_t cap,

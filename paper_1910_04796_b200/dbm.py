@@ -79,6 +79,8 @@ _SIGS = {
     "dbm_multiply_workspace": (C.c_int, [_P, _P, _P, _P, C.c_int, C.POINTER(_I64)]),
     "dbm_multiply": (C.c_int, [_P, C.c_double, _P, _P, C.c_double, _P, C.c_int, C.c_int32, _P, _I64,
                                C.POINTER(Stats)]),
+    "dbm_multiply_host": (C.c_int, [_P, C.c_double, _P, _P, C.c_double, _P, C.c_int, C.c_int32, _P, _I64, _P, _P,
+                                    _P, C.POINTER(Stats)]),
     "dbm_densify": (C.c_int, [_P, _P, _I64, C.c_int]),
     "dbm_undensify": (C.c_int, [_P, _P, _I64, C.c_double, C.c_double]),
     "dbm_debug_stacks": (C.c_int, [_P, _P, _P, _P, C.c_int, C.c_int32, _P, C.POINTER(_I64), _P,
@@ -334,6 +336,23 @@ def plan_exchange(pr: int, pc: int, myrow: int, mycol: int, Mb: int, Nb: int, Kb
                                  by.ctypes.data, C.byref(n)))
     return [{"send": bool(ops[4 * i]), "operand": "AB"[ops[4 * i + 1]], "peer": int(ops[4 * i + 2]),
              "kappa": int(ops[4 * i + 3]), "bytes": int(by[i])} for i in range(n.value)]
+
+
+def multiply_host(ctx: Context, alpha: float, A: Matrix, B: Matrix, beta: float, C_: Matrix, A_host: torch.Tensor,
+                  B_host: torch.Tensor, C_host: torch.Tensor, path="densified", stack_cap: int = 0,
+                  workspace: torch.Tensor | None = None) -> dict:
+    """dbm_multiply_host: C_host = alpha*A_host*B_host + beta*C_host with host-resident (ideally pinned)
+    arenas streamed through the device matrices.  Asynchronous on the ctx stream."""
+    for h, m in ((A_host, A), (B_host, B), (C_host, C_)):
+        assert h.dtype == torch.float64 and h.is_contiguous() and h.numel() * 8 >= m.arena_bytes and not h.is_cuda
+    lib = load()
+    need = multiply_workspace(ctx, A, B, C_, path)
+    ws = workspace if workspace is not None else ctx.workspace(need)
+    st = Stats()
+    _check(lib.dbm_multiply_host(ctx.h, alpha, A.h, B.h, beta, C_.h, _PATHS[path], stack_cap, ws.data_ptr(),
+                                 ws.numel() * ws.element_size(), A_host.data_ptr(), B_host.data_ptr(),
+                                 C_host.data_ptr(), C.byref(st)))
+    return st.as_dict()
 
 
 def plan_tallskinny(pr: int, pc: int, myrow: int, mycol: int, Mb: int, Nb: int, Kb: int, bs: int) -> tuple[int, int]:

@@ -299,3 +299,27 @@ def test_host_upload_download_roundtrip(dbm, ctx, orc):
     m.download(yp)
     ctx.sync()
     assert torch.equal(x, yp)
+
+
+@pytest.mark.parametrize("path,pinned,chunk", [("densified", True, 3), ("densified", True, None),
+                                               ("blocked", True, None), ("densified", False, None)])
+def test_multiply_host_streamed(dbm, ctx, orc, path, pinned, chunk):
+    """dbm_multiply_host (P:25 host-resident matrices, P:174 double buffering): A and B stream from
+    host memory (K-chunk by K-chunk on the single-rank densified path), C comes back to the host."""
+    M, N, K, bs = 384, 320, 1280, 64
+    Ah = torch.from_numpy(orc.fill_arena(SEED, 0, 0, M, K, bs))
+    Bh = torch.from_numpy(orc.fill_arena(SEED, 1, 0, K, N, bs))
+    Ch = torch.from_numpy(orc.fill_arena(SEED, 2, 0, M, N, bs))
+    if pinned:
+        Ah, Bh, Ch = Ah.pin_memory(), Bh.pin_memory(), Ch.pin_memory()
+    A, B, C = dbm.Matrix(ctx, M, K, bs), dbm.Matrix(ctx, K, N, bs), dbm.Matrix(ctx, M, N, bs)
+    if chunk is not None:
+        ctx.set_dense_chunk_bytes((M + N) * bs * 8 * chunk)
+    dbm.multiply_host(ctx, 0.75, A, B, -1.25, C, Ah, Bh, Ch, path)
+    ctx.sync()
+    if chunk is not None:
+        ctx.set_dense_chunk_bytes(16 << 30)
+    ref = orc.fill_arena(SEED, 2, 0, M, N, bs)
+    orc.multiply_blocked(M // bs, N // bs, K // bs, bs, 0.75, orc.fill_arena(SEED, 0, 0, M, K, bs),
+                         orc.fill_arena(SEED, 1, 0, K, N, bs), -1.25, ref)
+    assert relerr(Ch.numpy(), ref) <= TOL

@@ -1467,7 +1467,8 @@ dbm_status multiply_impl(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_matrix B, 
                                                                    p.spart_runs / (q1 - q0))
                                           : 1;
           CUDA_TRY(ctx, launch_smm((int)bs, trip, q1 - q0, kbk, Ap, Bp, C->arena, alpha, s == 0 ? beta : 1.0, nsplit,
-                                   nsplit > 1 ? (double*)(ws + p.off_spart) : nullptr, cs, &launches));
+                                   nsplit > 1 ? (double*)(ws + p.off_spart) : nullptr, cs, &launches,
+                                   p.mloc * kbk, kbk * p.nloc));
         }
       }
       st.entries += nruns * kbk;

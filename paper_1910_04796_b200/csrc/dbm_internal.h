@@ -55,6 +55,9 @@ struct GemmArgs {
 // Returns cudaSuccess or an error (tensor-map encode failures map to cudaErrorInvalidValue).
 cudaError_t launch_dgemm(const GemmArgs& g, cudaStream_t st, int* launches);
 int pick_splitk(int64_t M, int64_t N, int64_t K, int num_sms);
+// 2-D FP64 tensor map (TMA), 128-B swizzle: `rows` rows of `inner` doubles, row stride in bytes.
+bool make_map_2d(CUtensorMap* tm, const double* base, uint64_t inner, uint64_t rows, uint64_t row_stride_bytes,
+                 uint32_t box_inner, uint32_t box_rows);
 void launch_splitk_reduce(const double* partial, int splitk, int64_t M, int64_t N, double* C, int64_t ldc,
                           double alpha, double beta, cudaStream_t st);
 
@@ -69,15 +72,17 @@ void launch_stack_ptr(int64_t nruns, int64_t kb, int64_t cap, int64_t nstacks, i
 // C_blk = (first ? beta*C_blk : C_blk) + alpha*sum_k A_blk*B_blk.
 // nsplit > 1 splits each run's K across CTAs (partial: nsplit*nruns*bs*bs doubles, reduced in a
 // fixed order); see smm_pick_split.
+// a_blocks / b_blocks: blocks in the A / B panels (tensor-map extents of the bs-64 kernel).
 cudaError_t launch_smm(int bs, const int32_t* trip, int64_t nruns, int64_t kb, const double* A, const double* B,
                        double* C, double alpha, double beta_first, int nsplit, double* partial, cudaStream_t st,
-                       int* launches);
+                       int* launches, int64_t a_blocks = 0, int64_t b_blocks = 0);
 int smm_pick_split(int bs, int64_t nruns, int64_t kb);
 // DMMA group kernel for bs 22 / 64 (kernels_smm.cu); the generic smm handles other block sizes.
 bool smm_has_tensor_path(int bs);
 int smm_group_runs(int bs);  // runs per CTA group (stack chunks are cut at multiples of it)
 cudaError_t launch_smm_tc(int bs, const int32_t* trip, int64_t nruns, int64_t kb, const double* A, const double* B,
-                          double* C, double alpha, double beta_first, int nsplit, double* partial, cudaStream_t st);
+                          double* C, double alpha, double beta_first, int nsplit, double* partial, cudaStream_t st,
+                          int64_t a_blocks, int64_t b_blocks);
 
 // ----------------------------------------------------------------- driver
 int num_sms();

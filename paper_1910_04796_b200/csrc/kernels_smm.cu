@@ -551,6 +551,194 @@ __global__ void smm_splitk_reduce(const int32_t* __restrict__ trip, int64_t nrun
   }
 }
 
+// ============================================================================ bs 64: TMA tensor staging
+// 2 runs per CTA (2 x 2 consumer warps of 32 x 32 per 64 x 64 C block), a stage = half a k-block
+// (32 k = 8 DMMA k-steps).  The A and B arenas are viewed as 2-D tensors of 64-double rows (a block
+// column each); per stage a staged A block is 4 TMA boxes [32 k][16 m] and a staged B block 2 boxes
+// [64 n][16 k], all with the 128-B swizzle, i.e. 6 TMA ops per distinct block instead of one copy per
+// column.  MMA k-slot t of k-step ks reads k = 16(ks/4) + 2(ks%4) + (t&1) + 8(t>>1): conflict-free B
+// fragments (as in dgemm), 2-way on A.
+namespace s64 {
+constexpr int BS = 64, BB = 4096, KS = 32, RUNS = 2, WARPS = 8, P = 4, STAGES = 3;
+constexpr int SLOT = BS * KS;                       // doubles (16 KB)
+constexpr int STAGE = P * SLOT;
+constexpr size_t SMEM = (size_t)STAGES * STAGE * 8 + 1024;  // + 1024-B alignment slack for the swizzle
+static_assert(SMEM + 512 <= 232448, "shared memory");
+}  // namespace s64
+
+__device__ __forceinline__ void tma2d(uint32_t dst, const CUtensorMap* tm, int c0, int c1, uint32_t mbar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          dst),
+      "l"((uint64_t)tm), "r"(c0), "r"(c1), "r"(mbar)
+      : "memory");
+}
+
+__global__ void __launch_bounds__((s64::WARPS + 1) * 32, 1)
+    smm64_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                 const int32_t* __restrict__ trip, int64_t nruns, int64_t kb, double* __restrict__ C, double alpha,
+                 double beta_first) {
+  using namespace s64;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  __shared__ __align__(8) uint64_t full[STAGES], empty[STAGES];
+  __shared__ int s_rep[P], s_isb[P], s_ia[RUNS], s_ib[RUNS], s_n;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const bool producer = warp == WARPS;
+  const int run = warp >> 2, wsub = warp & 3, wm = wsub >> 1, wn = wsub & 1;
+  const int nst = (int)(kb * 2);  // two stages per k-block
+  const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(smem);
+  const int64_t ngroups = (nruns + RUNS - 1) / RUNS;
+  const int g = lane >> 2, t = lane & 3;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init((uint32_t)__cvta_generic_to_shared(&full[s]), 1);
+      mbar_init((uint32_t)__cvta_generic_to_shared(&empty[s]), WARPS);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (producer && lane == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&tmA) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&tmB) : "memory");
+  }
+  __syncthreads();
+
+  // per-lane fragment offsets inside a stage (bytes), k-step ks, lane (g, t)
+  auto kof = [&](int ks) { return 16 * (ks >> 2) + 2 * (ks & 3) + (t & 1) + 8 * (t >> 1); };
+  int stage = 0;
+  uint32_t phase = 0;
+  for (int64_t grp = blockIdx.x; grp < ngroups; grp += gridDim.x) {
+    const int64_t q0 = grp * RUNS;
+    const int n_g = (int)(nruns - q0 < RUNS ? nruns - q0 : RUNS);
+    if (producer) {
+      const Uniq u = uniq(trip, q0, 0, n_g, kb, lane);  // <= 2 + 2 distinct blocks: always fits P = 4
+      const int na = __popc(u.lead_a);
+      if (u.act) {
+        const int la = __ffs(u.ma) - 1, lb = __ffs(u.mb) - 1;
+        const int ia = __popc(u.lead_a & ((1u << la) - 1));
+        const int ib = na + __popc(u.lead_b & ((1u << lb) - 1));
+        s_ia[lane] = ia;
+        s_ib[lane] = ib;
+        if (la == lane) {
+          s_rep[ia] = lane;
+          s_isb[ia] = 0;
+        }
+        if (lb == lane) {
+          s_rep[ib] = lane;
+          s_isb[ib] = 1;
+        }
+      }
+      if (lane == 0) s_n = na + __popc(u.lead_b);
+    }
+    __syncthreads();
+    const int nslots = s_n;
+    if (producer) {
+      const bool owner = lane < nslots;
+      const int64_t q = q0 + (owner ? s_rep[lane] : 0);
+      const int isb = owner ? s_isb[lane] : 0;
+      for (int st = 0; st < nst; ++st) {
+        const int kk = st >> 1, h = st & 1;
+        const uint32_t fb = (uint32_t)__cvta_generic_to_shared(&full[stage]);
+        if (lane == 0) {
+          mbar_wait((uint32_t)__cvta_generic_to_shared(&empty[stage]), phase ^ 1);
+          mbar_expect_tx(fb, (uint32_t)nslots * SLOT * 8);
+        }
+        __syncwarp();
+        if (owner) {
+          const int blk = trip[3 * (q * kb + kk) + isb];
+          const uint32_t dst = sbase + (uint32_t)(stage * STAGE + lane * SLOT) * 8u;
+          if (!isb) {
+#pragma unroll
+            for (int sb = 0; sb < 4; ++sb) tma2d(dst + sb * 4096, &tmA, sb * 16, blk * 64 + h * 32, fb);
+          } else {
+#pragma unroll
+            for (int j = 0; j < 2; ++j) tma2d(dst + j * 8192, &tmB, h * 32 + j * 16, blk * 64, fb);
+          }
+        }
+        if (++stage == STAGES) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+    } else {
+      const bool active = run < n_g;
+      const int ia = active ? s_ia[run] : 0, ib = active ? s_ib[run] : 0;
+      double acc[4][4][2];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+      for (int st = 0; st < nst; ++st) {
+        mbar_wait((uint32_t)__cvta_generic_to_shared(&full[stage]), phase);
+        if (active) {
+          const uint32_t sA = sbase + (uint32_t)(stage * STAGE + ia * SLOT) * 8u;
+          const uint32_t sB = sbase + (uint32_t)(stage * STAGE + ib * SLOT) * 8u;
+#pragma unroll
+          for (int ks = 0; ks < KS / 4; ++ks) {
+            const int k = kof(ks);
+            double a[4], b[4];
+#pragma unroll
+            for (int mi = 0; mi < 4; ++mi) {  // A (m, k): box m/16, row k, 16-B chunk ((m%16)/2) ^ (k%8)
+              const int m = wm * 32 + mi * 8 + g, mm = m & 15;
+              a[mi] = lds64(sA + (m >> 4) * 4096 + k * 128 + ((((mm >> 1) ^ (k & 7))) << 4) + ((mm & 1) << 3));
+            }
+#pragma unroll
+            for (int ni = 0; ni < 4; ++ni) {  // B (k, n): box k/16, row n, chunk ((k%16)/2) ^ (n%8)
+              const int n = wn * 32 + ni * 8 + g, kk16 = k & 15;
+              b[ni] = lds64(sB + (k >> 4) * 8192 + n * 128 + ((((kk16 >> 1) ^ (n & 7))) << 4) + ((kk16 & 1) << 3));
+            }
+#pragma unroll
+            for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+              for (int ni = 0; ni < 4; ++ni) dmma(acc[mi][ni], a[mi], b[ni]);
+          }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive((uint32_t)__cvta_generic_to_shared(&empty[stage]));
+        if (++stage == STAGES) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+      if (active) {
+        double* cb = C + (int64_t)trip[3 * ((q0 + run) * kb) + 2] * BB;
+#pragma unroll
+        for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+          for (int ni = 0; ni < 4; ++ni)
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+              const int m = wm * 32 + mi * 8 + g, n = wn * 32 + ni * 8 + 2 * t + j;
+              double* p = cb + m + n * BS;
+              const double v = alpha * acc[mi][ni][j];
+              *p = (beta_first == 0.0) ? v : beta_first * *p + v;
+            }
+      }
+    }
+    __syncthreads();
+  }
+}
+
+cudaError_t launch_smm64(const int32_t* trip, int64_t nruns, int64_t kb, const double* A, const double* B, double* C,
+                         double alpha, double beta_first, int64_t a_blocks, int64_t b_blocks, cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(smm64_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s64::SMEM);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  CUtensorMap tmA, tmB;
+  if (!make_map_2d(&tmA, A, 64, (uint64_t)a_blocks * 64, 512, 16, 32) ||
+      !make_map_2d(&tmB, B, 64, (uint64_t)b_blocks * 64, 512, 16, 64))
+    return cudaErrorInvalidValue;
+  const int64_t ngroups = (nruns + s64::RUNS - 1) / s64::RUNS;
+  const unsigned grid = (unsigned)std::min<int64_t>(ngroups, (int64_t)num_sms());
+  smm64_kernel<<<grid, (s64::WARPS + 1) * 32, s64::SMEM, st>>>(tmA, tmB, trip, nruns, kb, C, alpha, beta_first);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_smm22(const int32_t* trip, int64_t nruns, int64_t kb, const double* A, const double* B, double* C,
                          double alpha, double beta_first, int nsplit, double* partial, cudaStream_t st) {
   static bool attr = false;
@@ -599,9 +787,12 @@ int smm_pick_split(int bs, int64_t nruns, int64_t kb) {
 }
 
 cudaError_t launch_smm_tc(int bs, const int32_t* trip, int64_t nruns, int64_t kb, const double* A, const double* B,
-                          double* C, double alpha, double beta_first, int nsplit, double* partial, cudaStream_t st) {
+                          double* C, double alpha, double beta_first, int nsplit, double* partial, cudaStream_t st,
+                          int64_t a_blocks, int64_t b_blocks) {
   if (nruns <= 0 || kb <= 0) return cudaSuccess;
   if (bs == 22) return launch_smm22(trip, nruns, kb, A, B, C, alpha, beta_first, nsplit, partial, st);
+  if (bs == 64 && a_blocks > 0 && b_blocks > 0 && ((uintptr_t)A & 15) == 0 && ((uintptr_t)B & 15) == 0)
+    return launch_smm64(trip, nruns, kb, A, B, C, alpha, beta_first, a_blocks, b_blocks, st);
   if (bs == 64) return launch_group<Cfg64>(trip, nruns, kb, A, B, C, alpha, beta_first, st);
   return cudaErrorInvalidValue;
 }

@@ -38,6 +38,16 @@ FP64_PEAK_MEASURED = 37.15  # TFLOP/s per B200, DMMA m8n8k4 chain at 1965 MHz (p
 FP64_PEAK_SPEC = 37.2       # 148 SM x 64 FMA/clk x 2 x 1.965 GHz
 
 
+def _hbm_peak() -> float:
+    try:
+        return float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"])
+    except Exception:
+        return 6650.0  # fallback figure of the profiling guide
+
+
+HBM_PEAK = _hbm_peak()
+
+
 def parse():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
@@ -227,7 +237,7 @@ def main():
     prof = ctx.profile_read(dbm.K_DGEMM if path == "densified" else dbm.K_SMM)
     prof_d = ctx.profile_read(dbm.K_DENSIFY)
     prof_u = ctx.profile_read(dbm.K_UNDENSIFY)
-    ctx.profile_read(dbm.K_STACKGEN)
+    prof_s = ctx.profile_read(dbm.K_STACKGEN)
     per_launch_ms = prof["ms"] / max(prof["launches"], 1)
     per_launch_flop = prof["flops"] / max(prof["launches"], 1)
     achieved = per_launch_flop / (per_launch_ms * 1e-3) / 1e12 if per_launch_ms > 0 else None
@@ -268,7 +278,13 @@ def main():
                                         "MEASURED_PEAKS.json); spec 37.2",
                          "share_of_step": prof["ms"] / (ms * args.steps) if ms > 0 else None},
             "phases_ms_per_step": {"dgemm_or_smm": prof["ms"] / args.steps, "densify": prof_d["ms"] / args.steps,
-                                   "undensify": prof_u["ms"] / args.steps},
+                                   "undensify": prof_u["ms"] / args.steps, "stackgen": prof_s["ms"] / args.steps},
+            # HBM-bound kernels of the path: algorithmic bytes / CUDA-event time vs the measured copy peak
+            "hbm_kernels": {name: {"gbs": (pr_["bytes"] / (pr_["ms"] * 1e-3) / 1e9) if pr_["ms"] > 0 else None,
+                                   "frac": (pr_["bytes"] / (pr_["ms"] * 1e-3) / 1e9 / HBM_PEAK) if pr_["ms"] > 0
+                                   else None, "launches": pr_["launches"]}
+                            for name, pr_ in (("densify", prof_d), ("undensify", prof_u), ("stackgen", prof_s))
+                            if pr_["launches"]},
             "stats": {k: st[k] for k in ("entries", "stacks", "bytes_sent", "bytes_recv", "steps")},
             "gpu_launches": launches,
             "clocks": clk.summary(),

@@ -133,12 +133,12 @@ def oracle_sample(M, N, K, rows: int) -> dict:
 
 
 def auto_rows(M, N, K, target_s: float = 15.0) -> int:
-    # measured on the B200 box's 16 host cores: ~2.3 GFLOP/s per core for the plain loop incl.
-    # regenerating B from the seeds (8 rows of 63,360^2 in 1.7 s)
+    # measured on the B200 box's host cores: ~0.8 GFLOP/s per core for the plain loop incl.
+    # regenerating B from the seeds (59 rows of 63,360^3 took 37 s on 16 threads)
     import oracle
 
     cores = max(1, oracle.num_threads())
-    rows = int(target_s * 2.0e9 * cores / (2.0 * K * N))
+    rows = int(target_s * 0.8e9 * cores / (2.0 * K * N))
     return max(1, min(rows, M, 64))
 
 

@@ -10,6 +10,7 @@
 // conflict-free LDS.64 thanks to the 128B swizzle.  Split-K with a fixed-order reduction covers
 // thin C (rectangular configs).  Bound: FP64 pipe; 2*M*N*K flops per launch.
 #include <algorithm>
+#include <cstdlib>
 
 #include "dbm_internal.h"
 
@@ -78,7 +79,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     dgemm_tn_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M, int N,
                     int k_tiles_total, int k_tiles_per_split, int nsplit, int tiles_m, int tiles_n,
                     double* __restrict__ C,
-                    int64_t ldc, double alpha, double beta, double* __restrict__ partial) {
+                    int64_t ldc, double alpha, double beta, double* __restrict__ partial,
+                    unsigned* __restrict__ wave_sync, int sync_kt, int sync_rounds) {
   using T = Tile<BM, BN>;
   constexpr int STAGES = T::STAGES, kStage = T::kStage, kStageA = T::kStageA, MI = T::MI, NI = T::NI;
   extern __shared__ uint8_t smem_raw[];
@@ -123,11 +125,24 @@ __global__ void __launch_bounds__(kThreads, 1)
       asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&tmB) : "memory");
       int stage = 0;
       uint32_t phase = 0;
-      for (int item = blockIdx.x; item < nitems; item += gridDim.x) {
+      unsigned epoch = 0;
+      int round = 0;
+      for (int item = blockIdx.x; item < nitems; item += gridDim.x, ++round) {
         int tm, tn, split, kt0, nkt;
         item_coords(item, tm, tn, split);
         item_k(split, kt0, nkt);
         for (int kt = 0; kt < nkt; ++kt) {
+          // Optional wave barrier (cooperative launch only): every sync_kt k-tiles of the rounds every
+          // CTA runs, the producers re-align so one wave's A/B panels are read from L2, not HBM.
+          if (wave_sync != nullptr && round < sync_rounds && kt % sync_kt == 0) {
+            ++epoch;
+            atomicAdd(wave_sync, 1u);
+            const unsigned target = epoch * gridDim.x;
+            unsigned seen;
+            do {
+              asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(seen) : "l"(wave_sync) : "memory");
+            } while (seen < target);
+          }
           mbar_wait(su32(&empty[stage]), phase ^ 1);
           const uint32_t fb = su32(&full[stage]);
           mbar_expect_tx(fb, kStage);
@@ -334,6 +349,20 @@ GemmPlan pick_gemm(int64_t M, int64_t N, int64_t K, int sms) {
 int pick_splitk(int64_t M, int64_t N, int64_t K, int sms) { return pick_gemm(M, N, K, sms).splitk; }
 
 namespace {
+// DBM_DGEMM_WAVESYNC=<k-tiles> turns on the wave barrier (0/unset = off).  Experimental: see DESIGN.md.
+int wave_sync_ktiles() {
+  static int v = [] {
+    const char* e = getenv("DBM_DGEMM_WAVESYNC");
+    return e ? std::max(0, atoi(e)) : 0;
+  }();
+  return v;
+}
+unsigned* wave_sync_counter() {
+  static unsigned* p = nullptr;  // one process drives one device
+  if (p == nullptr && cudaMalloc(&p, sizeof(unsigned)) != cudaSuccess) p = nullptr;
+  return p;
+}
+
 template <int BM, int BN>
 cudaError_t launch_tile(const GemmArgs& g, int splitk, cudaStream_t st) {
   using T = Tile<BM, BN>;
@@ -354,9 +383,32 @@ cudaError_t launch_tile(const GemmArgs& g, int splitk, cudaStream_t st) {
   const int per = (ktiles + splitk - 1) / splitk;
   const int64_t items = (int64_t)tiles_m * tiles_n * splitk;
   const unsigned grid = (unsigned)std::min<int64_t>(items, num_sms());  // persistent: one CTA per SM
+  double* partial = splitk > 1 ? g.partial : nullptr;
+  const int sync_kt = wave_sync_ktiles();
+  // Barriers only where every CTA reaches them: the full rounds, and (split-K) equal k-ranges.
+  const int rounds = (int)(items / grid);
+  if (sync_kt > 0 && rounds > 0 && (ktiles % splitk) == 0) {
+    unsigned* ws = wave_sync_counter();
+    if (ws == nullptr) return cudaErrorMemoryAllocation;
+    cudaError_t e = cudaMemsetAsync(ws, 0, sizeof(unsigned), st);
+    if (e != cudaSuccess) return e;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = T::kSmem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeCooperative;  // all CTAs co-resident, or the launch fails: no deadlock
+    at[0].val.cooperative = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, dgemm_tn_kernel<BM, BN>, tmA, tmB, (int)g.M, (int)g.N, ktiles,
+                              std::max(per, 0), splitk, tiles_m, tiles_n, g.C, g.ldc, g.alpha, g.beta, partial, ws,
+                              sync_kt, rounds);
+  }
   dgemm_tn_kernel<BM, BN><<<grid, kThreads, T::kSmem, st>>>(tmA, tmB, (int)g.M, (int)g.N, ktiles, std::max(per, 0),
                                                             splitk, tiles_m, tiles_n, g.C, g.ldc, g.alpha, g.beta,
-                                                            splitk > 1 ? g.partial : nullptr);
+                                                            partial, nullptr, 1, 0);
   return cudaGetLastError();
 }
 }  // namespace

@@ -25,6 +25,7 @@ _pd = C.POINTER(C.c_double)
 _pi64 = C.POINTER(C.c_int64)
 _pi32 = C.POINTER(C.c_int32)
 _pint = C.POINTER(C.c_int)
+_pu8 = C.POINTER(C.c_uint8)
 
 
 def build(force: bool = False) -> str:
@@ -75,6 +76,13 @@ def lib():
             "orc_freivalds_rhs": (None, [_i64, _i64, _i64, _u64, C.c_int, _dbl, _dbl, _u64, _pd, _pd]),
             "orc_sign_value": (_dbl, [_u64, _i64]),
             "orc_num_threads": (C.c_int, []),
+            "orc_pattern_present": (C.c_int, [_u64, C.c_uint32, _i64, _i64, _dbl]),
+            "orc_pattern_random": (None, [_u64, C.c_uint32, _i64, _i64, _dbl, _pu8]),
+            "orc_multiply_sparse": (None, [_i64, _i64, _i64, C.c_int, _dbl, _pd, _pu8, _pd, _pu8, _dbl, _pd, _pu8]),
+            "orc_sparse_compress": (_i64, [_pd, _pu8, _i64, _i64, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
+                                           _pd]),
+            "orc_sparse_expand": (None, [_pd, _pu8, _i64, _i64, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, _pd]),
+            "orc_sparse_stacks": (_i64, [_i64, _i64, _i64, _pu8, _pu8, _pu8, _i64, _pi32, _pi64, _pi64]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -178,6 +186,55 @@ def stacks(mloc: int, nloc: int, kb: int, cap: int = 30000, counts_only: bool = 
     trip = np.empty(max(3 * n, 3), dtype=np.int32)
     ptr = np.empty(n + 2, dtype=np.int64)
     e = lib().orc_stacks(mloc, nloc, kb, cap, _p(trip, _pi32), _p(ptr, _pi64), C.byref(ns))
+    return trip[: 3 * e].reshape(e, 3), ptr[: ns.value + 1]
+
+
+# ---------------------------------------------------------------- block sparsity (reading R15)
+def pattern_present(seed, mat_id, bi, bj, occupancy) -> bool:
+    return bool(lib().orc_pattern_present(seed, mat_id, bi, bj, occupancy))
+
+
+def pattern_random(seed, mat_id, Mb, Nb, occupancy) -> np.ndarray:
+    """(Mb, Nb) uint8 mask of stored blocks."""
+    m = np.empty(max(Mb * Nb, 1), dtype=np.uint8)
+    lib().orc_pattern_random(seed, mat_id, Mb, Nb, occupancy, _p(m, _pu8))
+    return m[: Mb * Nb].reshape(Mb, Nb)
+
+
+def multiply_sparse(Mb, Nb, Kb, bs, alpha, A, amask, B, bmask, beta, Cg, cmask) -> None:
+    am, bm, cm = (np.ascontiguousarray(x, dtype=np.uint8) for x in (amask, bmask, cmask))
+    lib().orc_multiply_sparse(Mb, Nb, Kb, bs, alpha, _p(A), _p(am, _pu8), _p(B), _p(bm, _pu8), beta, _p(Cg),
+                              _p(cm, _pu8))
+
+
+def sparse_compress(g, mask, Mb, Nb, bs, pr=1, pc=1, r=0, c=0) -> np.ndarray:
+    m = np.ascontiguousarray(mask, dtype=np.uint8)
+    n = lib().orc_sparse_compress(_p(g), _p(m, _pu8), Mb, Nb, bs, pr, pc, r, c, None)
+    out = np.empty(max(n * bs * bs, 1))
+    lib().orc_sparse_compress(_p(g), _p(m, _pu8), Mb, Nb, bs, pr, pc, r, c, _p(out))
+    return out[: n * bs * bs]
+
+
+def sparse_expand_into(g, local, mask, Mb, Nb, bs, pr=1, pc=1, r=0, c=0) -> None:
+    m = np.ascontiguousarray(mask, dtype=np.uint8)
+    loc = np.ascontiguousarray(local, dtype=np.float64)
+    if loc.size == 0:
+        loc = np.zeros(1)
+    lib().orc_sparse_expand(_p(loc), _p(m, _pu8), Mb, Nb, bs, pr, pc, r, c, _p(g))
+
+
+def sparse_stacks(amask, bmask, cmask, cap: int = 30000):
+    """amask (mloc, kb), bmask (kb, nloc), cmask (mloc, nloc) -> (triplets (E,3) int32, stack_ptr)."""
+    am, bm, cm = (np.ascontiguousarray(x, dtype=np.uint8) for x in (amask, bmask, cmask))
+    mloc, kb = am.shape
+    nloc = bm.shape[1]
+    ns = C.c_int64()
+    e = lib().orc_sparse_stacks(mloc, nloc, kb, _p(am, _pu8), _p(bm, _pu8), _p(cm, _pu8), cap, None, None,
+                                C.byref(ns))
+    trip = np.empty(max(3 * e, 3), dtype=np.int32)
+    ptr = np.empty(ns.value + 2, dtype=np.int64)
+    lib().orc_sparse_stacks(mloc, nloc, kb, _p(am, _pu8), _p(bm, _pu8), _p(cm, _pu8), cap, _p(trip, _pi32),
+                            _p(ptr, _pi64), C.byref(ns))
     return trip[: 3 * e].reshape(e, 3), ptr[: ns.value + 1]
 
 

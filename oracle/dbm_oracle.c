@@ -484,3 +484,137 @@ void orc_freivalds_rhs(int64_t M, int64_t N, int64_t K, uint64_t seed, int kind,
   }
   free(y);
 }
+
+/* ------------------------------------------------------------------------- */
+/* Block sparsity (§I; §II "blocked compressed sparse row (CSR)    */
+/* format"; SPEC S:32-37 occupancy = stored blocks / all blocks).  Reading    */
+/* R15: C keeps its stored pattern.                               */
+/* ------------------------------------------------------------------------- */
+int orc_pattern_present(uint64_t seed, uint32_t mat_id, int64_t bi, int64_t bj, double occupancy) {
+  uint64_t bits = gen_bits(seed, mat_id | 0x80000000u, bi, bj);
+  double u = (double)(bits >> 11) * 0x1.0p-53; /* [0,1) */
+  return u < occupancy;
+}
+
+void orc_pattern_random(uint64_t seed, uint32_t mat_id, int64_t Mb, int64_t Nb, double occupancy, uint8_t* mask) {
+  for (int64_t bi = 0; bi < Mb; ++bi)
+    for (int64_t bj = 0; bj < Nb; ++bj) mask[bi * Nb + bj] = (uint8_t)orc_pattern_present(seed, mat_id, bi, bj, occupancy);
+}
+
+void orc_multiply_sparse(int64_t Mb, int64_t Nb, int64_t Kb, int bs, double alpha, const double* A,
+                         const uint8_t* amask, const double* B, const uint8_t* bmask, double beta, double* C,
+                         const uint8_t* cmask) {
+  int64_t bb = (int64_t)bs * bs;
+#pragma omp parallel for schedule(dynamic, 1)
+  for (int64_t bi = 0; bi < Mb; ++bi) {
+    double* acc = (double*)malloc((size_t)bb * sizeof(double));
+    for (int64_t bj = 0; bj < Nb; ++bj) {
+      if (!cmask[bi * Nb + bj]) continue;
+      for (int64_t e = 0; e < bb; ++e) acc[e] = 0.0;
+      for (int64_t bk = 0; bk < Kb; ++bk) {
+        if (!amask[bi * Kb + bk] || !bmask[bk * Nb + bj]) continue;
+        const double* a = A + (bi * Kb + bk) * bb;
+        const double* b = B + (bk * Nb + bj) * bb;
+        for (int y = 0; y < bs; ++y)
+          for (int x = 0; x < bs; ++x) {
+            double s = acc[(int64_t)y * bs + x];
+            for (int z = 0; z < bs; ++z) s += a[(int64_t)z * bs + x] * b[(int64_t)y * bs + z];
+            acc[(int64_t)y * bs + x] = s;
+          }
+      }
+      double* c = C + (bi * Nb + bj) * bb;
+      for (int64_t e = 0; e < bb; ++e) c[e] = (beta == 0.0) ? alpha * acc[e] : beta * c[e] + alpha * acc[e];
+    }
+    free(acc);
+  }
+}
+
+int64_t orc_sparse_compress(const double* g, const uint8_t* mask, int64_t Mb, int64_t Nb, int bs, int pr, int pc,
+                            int r, int c, double* l) {
+  int64_t bb = (int64_t)bs * bs, n = 0;
+  for (int64_t bi = r; bi < Mb; bi += pr)
+    for (int64_t bj = c; bj < Nb; bj += pc)
+      if (mask[bi * Nb + bj]) {
+        if (l) memcpy(l + n * bb, g + (bi * Nb + bj) * bb, (size_t)bb * sizeof(double));
+        ++n;
+      }
+  return n;
+}
+
+void orc_sparse_expand(const double* l, const uint8_t* mask, int64_t Mb, int64_t Nb, int bs, int pr, int pc, int r,
+                       int c, double* g) {
+  int64_t bb = (int64_t)bs * bs, n = 0;
+  for (int64_t bi = r; bi < Mb; bi += pr)
+    for (int64_t bj = c; bj < Nb; bj += pc)
+      if (mask[bi * Nb + bj]) {
+        memcpy(g + (bi * Nb + bj) * bb, l + n * bb, (size_t)bb * sizeof(double));
+        ++n;
+      }
+}
+
+int64_t orc_sparse_stacks(int64_t mloc, int64_t nloc, int64_t kb, const uint8_t* amask, const uint8_t* bmask,
+                          const uint8_t* cmask, int64_t cap, int32_t* trip, int64_t* stack_ptr, int64_t* n_stacks) {
+  int64_t nrun = mloc * nloc;
+  int64_t* li = (int64_t*)malloc((size_t)(nrun > 0 ? nrun : 1) * sizeof(int64_t));
+  int64_t* lj = (int64_t*)malloc((size_t)(nrun > 0 ? nrun : 1) * sizeof(int64_t));
+  /* slot of a stored block = its rank in the row-major order of its panel's stored blocks */
+  int64_t* aslot = (int64_t*)malloc((size_t)(mloc * kb > 0 ? mloc * kb : 1) * sizeof(int64_t));
+  int64_t* bslot = (int64_t*)malloc((size_t)(kb * nloc > 0 ? kb * nloc : 1) * sizeof(int64_t));
+  int64_t* cslot = (int64_t*)malloc((size_t)(nrun > 0 ? nrun : 1) * sizeof(int64_t));
+  int64_t n = 0;
+  for (int64_t i = 0; i < mloc * kb; ++i) aslot[i] = amask[i] ? n++ : -1;
+  n = 0;
+  for (int64_t i = 0; i < kb * nloc; ++i) bslot[i] = bmask[i] ? n++ : -1;
+  n = 0;
+  for (int64_t i = 0; i < nrun; ++i) cslot[i] = cmask[i] ? n++ : -1;
+  orc_traversal(mloc, nloc, li, lj);
+  int64_t e = 0, ns = 0, cur = 0;
+  if (stack_ptr) stack_ptr[0] = 0;
+  for (int64_t q = 0; q < nrun; ++q) {
+    int64_t cs = cslot[li[q] * nloc + lj[q]];
+    if (cs < 0) continue;
+    int64_t len = 0;
+    for (int64_t kk = 0; kk < kb; ++kk) {
+      int64_t as = aslot[li[q] * kb + kk], bs_ = bslot[kk * nloc + lj[q]];
+      if (as < 0 || bs_ < 0) continue;
+      if (trip) {
+        trip[3 * (e + len) + 0] = (int32_t)as;
+        trip[3 * (e + len) + 1] = (int32_t)bs_;
+        trip[3 * (e + len) + 2] = (int32_t)cs;
+      }
+      ++len;
+    }
+    if (len == 0) continue;
+    if (len > cap) {
+      if (cur > 0) {
+        ++ns;
+        if (stack_ptr) stack_ptr[ns] = e;
+        cur = 0;
+      }
+      for (int64_t done = 0; done < len;) {
+        done += (len - done < cap) ? len - done : cap;
+        ++ns;
+        if (stack_ptr) stack_ptr[ns] = e + done;
+      }
+    } else {
+      if (cur + len > cap) {
+        ++ns;
+        if (stack_ptr) stack_ptr[ns] = e;
+        cur = 0;
+      }
+      cur += len;
+    }
+    e += len;
+  }
+  if (cur > 0) {
+    ++ns;
+    if (stack_ptr) stack_ptr[ns] = e;
+  }
+  if (n_stacks) *n_stacks = ns;
+  free(li);
+  free(lj);
+  free(aslot);
+  free(bslot);
+  free(cslot);
+  return e;
+}

@@ -102,6 +102,32 @@ void orc_freivalds_rhs(int64_t M, int64_t N, int64_t K, uint64_t seed, int kind,
                        uint64_t x_seed, double* x_out, double* out);
 double orc_sign_value(uint64_t x_seed, int64_t j);
 
+/* ---- Block sparsity (§I "block-sparse ... occupancy between 0.01% up to dense"; §II blocked
+ * CSR), reading R15 ---- */
+/* Seeded block pattern: block (bi,bj) is stored iff u < occupancy, u = the kind-0 uniform of the counter
+ * generator's independent stream mat_id | 2^31 taken at (bi, bj) and mapped to [0,1). */
+int orc_pattern_present(uint64_t seed, uint32_t mat_id, int64_t bi, int64_t bj, double occupancy);
+void orc_pattern_random(uint64_t seed, uint32_t mat_id, int64_t Mb, int64_t Nb, double occupancy, uint8_t* mask);
+/* C_out = alpha*A*B + beta*C_in over stored blocks only: for every stored C block (bi,bj)
+ * acc = sum over bk ascending with A(bi,bk) and B(bk,bj) both stored of A_blk*B_blk, then
+ * C_blk = beta*C_blk + alpha*acc (C's pattern is kept: products landing on absent C blocks are not
+ * formed).  Global arenas in the dense layout (slot bi*Nb+bj); absent blocks are never read or written. */
+void orc_multiply_sparse(int64_t Mb, int64_t Nb, int64_t Kb, int bs, double alpha, const double* A,
+                         const uint8_t* amask, const double* B, const uint8_t* bmask, double beta, double* C,
+                         const uint8_t* cmask);
+/* A rank's stored blocks in local CSR order (li ascending, then lj ascending) <-> global dense-layout arena. */
+int64_t orc_sparse_compress(const double* global_arena, const uint8_t* mask, int64_t Mb, int64_t Nb, int bs, int pr,
+                            int pc, int r, int c, double* local_sparse);
+void orc_sparse_expand(const double* local_sparse, const uint8_t* mask, int64_t Mb, int64_t Nb, int bs, int pr, int pc,
+                       int r, int c, double* global_arena);
+/* Stack list of one (rank, step) with sparse panels: amask (mloc x kb), bmask (kb x nloc), cmask
+ * (mloc x nloc), row-major.  Runs = stored C blocks in bisection order; a run's entries are the kk
+ * ascending with A(li,kk) and B(kk,lj) stored; a_slot / b_slot / c_slot = the block's rank in the
+ * row-major order of the stored blocks of its panel (the packed panel layout).  Empty runs produce no
+ * entry.  Stacks: the same greedy whole-run packing as orc_stacks.  Returns the number of entries. */
+int64_t orc_sparse_stacks(int64_t mloc, int64_t nloc, int64_t kb, const uint8_t* amask, const uint8_t* bmask,
+                          const uint8_t* cmask, int64_t cap, int32_t* triplets, int64_t* stack_ptr, int64_t* n_stacks);
+
 int orc_num_threads(void);
 
 #ifdef __cplusplus

@@ -440,3 +440,129 @@ def test_tallskinny_bytes(orc):
     rv, _ = orc.ts_bytes(8, 8, 40, 2, 1, 4, 0, 1)
     kp = orc.local_count(40, 4, 1)
     assert rv == kp * 6 * 4 * 8 + 3 * 8 * 2 * 4 * 8  # B: kp x (8 - 2 local cols) blocks; C: 3 x (8 x 2) blocks
+
+
+# ----------------------------------------------------------------- block sparsity (reading R15)
+def test_pattern_generator_occupancy(orc):
+    """occupancy 0 / 1 are exact; other occupancies land within 5 sigma of the binomial mean (catches a
+    wrong comparison direction or a stream shared with the element generator)."""
+    assert orc.pattern_random(7, 0, 30, 40, 0.0).sum() == 0
+    assert orc.pattern_random(7, 0, 30, 40, 1.0).all()
+    n = 200 * 200
+    for occ in (0.01, 0.1, 0.5, 0.9):
+        m = orc.pattern_random(1910, 3, 200, 200, occ)
+        assert abs(m.sum() - occ * n) <= 5 * math.sqrt(n * occ * (1 - occ)) + 1
+    a, b = orc.pattern_random(1910, 0, 50, 50, 0.5), orc.pattern_random(1910, 1, 50, 50, 0.5)
+    assert 0.3 < (a == b).mean() < 0.7  # independent per mat_id
+    # monotone in occupancy: a block stored at occupancy p is stored at every q > p
+    lo, hi = orc.pattern_random(5, 2, 40, 40, 0.2), orc.pattern_random(5, 2, 40, 40, 0.6)
+    assert not (lo & ~hi).any()
+
+
+@pytest.mark.parametrize("Mb,Nb,Kb,bs,occ", [(4, 3, 5, 2, 0.5), (6, 5, 7, 3, 0.2), (3, 3, 3, 4, 0.9), (5, 4, 6, 1, 0.0)])
+def test_multiply_sparse_matches_masked_numpy(orc, Mb, Nb, Kb, bs, occ):
+    """Absent blocks act as zeros in A and B; C keeps its pattern (absent C blocks untouched, present ones
+    get beta*C + alpha*A*B).  Catches a mask applied to the wrong operand or a transposed mask."""
+    rng = np.random.default_rng(Mb * 100 + Kb)
+    am = orc.pattern_random(11, 0, Mb, Kb, occ)
+    bm = orc.pattern_random(11, 1, Kb, Nb, occ)
+    cm = orc.pattern_random(11, 2, Mb, Nb, max(occ, 0.5))
+    A, B, Cg = rand_arena(rng, Mb, Kb, bs), rand_arena(rng, Kb, Nb, bs), rand_arena(rng, Mb, Nb, bs)
+    Ad = orc.arena_to_dense(A, Mb, Kb, bs) * np.kron(am, np.ones((bs, bs)))
+    Bd = orc.arena_to_dense(B, Kb, Nb, bs) * np.kron(bm, np.ones((bs, bs)))
+    Cd = orc.arena_to_dense(Cg, Mb, Nb, bs)
+    out = Cg.copy()
+    orc.multiply_sparse(Mb, Nb, Kb, bs, 0.75, A, am, B, bm, -1.25, out, cm)
+    got = orc.arena_to_dense(out, Mb, Nb, bs)
+    cmask = np.kron(cm, np.ones((bs, bs))).astype(bool)
+    want = np.where(cmask, 0.75 * (Ad @ Bd) - 1.25 * Cd, Cd)
+    assert np.allclose(got, want, rtol=0, atol=1e-12)
+
+
+def test_multiply_sparse_dense_pattern_is_the_dense_oracle(orc):
+    """With every block stored the sparse product is bit-identical to orc_multiply_blocked (same order)."""
+    rng = np.random.default_rng(3)
+    Mb, Nb, Kb, bs = 3, 4, 5, 3
+    A, B, Cg = rand_arena(rng, Mb, Kb, bs), rand_arena(rng, Kb, Nb, bs), rand_arena(rng, Mb, Nb, bs)
+    one = lambda r, c: np.ones((r, c), np.uint8)  # noqa: E731
+    x, y = Cg.copy(), Cg.copy()
+    orc.multiply_sparse(Mb, Nb, Kb, bs, 0.5, A, one(Mb, Kb), B, one(Kb, Nb), 2.0, x, one(Mb, Nb))
+    orc.multiply_blocked(Mb, Nb, Kb, bs, 0.5, A, B, 2.0, y)
+    assert np.array_equal(x, y)
+
+
+def test_sparse_compress_expand_roundtrip(orc):
+    """Local CSR order = li ascending then lj ascending over stored blocks (DBCSR's blocked CSR)."""
+    rng = np.random.default_rng(9)
+    Mb, Nb, bs, pr, pc = 7, 6, 2, 2, 3
+    g = rand_arena(rng, Mb, Nb, bs)
+    m = orc.pattern_random(4, 0, Mb, Nb, 0.4)
+    back = np.zeros_like(g)
+    total = 0
+    for r in range(pr):
+        for c in range(pc):
+            loc = orc.sparse_compress(g, m, Mb, Nb, bs, pr, pc, r, c)
+            blocks = [(bi, bj) for bi in range(r, Mb, pr) for bj in range(c, Nb, pc) if m[bi, bj]]
+            assert loc.size == len(blocks) * bs * bs
+            for n, (bi, bj) in enumerate(blocks):  # brute force: block n is (bi, bj)
+                s = (bi * Nb + bj) * bs * bs
+                assert np.array_equal(loc[n * bs * bs:(n + 1) * bs * bs], g[s:s + bs * bs])
+            orc.sparse_expand_into(back, loc, m, Mb, Nb, bs, pr, pc, r, c)
+            total += len(blocks)
+    assert total == m.sum()
+    mask_el = np.repeat(m.reshape(-1), bs * bs).astype(bool)
+    assert np.array_equal(back[mask_el], g[mask_el]) and not back[~mask_el].any()
+
+
+@pytest.mark.parametrize("mloc,nloc,kb,occ,cap", [(4, 4, 6, 0.5, 7), (5, 3, 9, 0.3, 4), (6, 7, 4, 0.8, 30000),
+                                                  (3, 3, 5, 0.0, 10), (8, 8, 3, 1.0, 5)])
+def test_sparse_stacks_brute_force(orc, mloc, nloc, kb, occ, cap):
+    """Pure-Python enumeration of the R15 rule on tiny inputs: runs = stored C blocks in bisection order
+    (the traversal itself pinned by test_traversal_*), entries kk ascending where both A and B are
+    stored, slots = row-major rank among stored panel blocks; entry count = sum of the mask product."""
+    am = orc.pattern_random(21, 0, mloc, kb, occ)
+    bm = orc.pattern_random(21, 1, kb, nloc, occ)
+    cm = orc.pattern_random(21, 2, mloc, nloc, max(occ, 0.6))
+    trip, ptr = orc.sparse_stacks(am, bm, cm, cap)
+    aslot = {ij: n for n, ij in enumerate((i, k) for i in range(mloc) for k in range(kb) if am[i, k])}
+    bslot = {ij: n for n, ij in enumerate((k, j) for k in range(kb) for j in range(nloc) if bm[k, j])}
+    cslot = {ij: n for n, ij in enumerate((i, j) for i in range(mloc) for j in range(nloc) if cm[i, j])}
+    want, runs = [], []
+    for li, lj in orc.traversal(mloc, nloc):
+        if not cm[li, lj]:
+            continue
+        run = [(aslot[(li, k)], bslot[(k, lj)], cslot[(li, lj)]) for k in range(kb) if am[li, k] and bm[k, lj]]
+        if run:
+            runs.append(len(run))
+        want += run
+    assert [tuple(t) for t in trip] == want
+    assert len(want) == int(((am.astype(int) @ bm.astype(int)) * cm).sum())
+    # greedy whole-run packing (same rule as the dense pin): rebuild the boundaries
+    b, cur, e = [0], 0, 0
+    for n in runs:
+        if n > cap:
+            if cur:
+                b.append(e)
+                cur = 0
+            done = 0
+            while done < n:
+                done += min(cap, n - done)
+                b.append(e + done)
+        else:
+            if cur + n > cap:
+                b.append(e)
+                cur = 0
+            cur += n
+        e += n
+    if cur:
+        b.append(e)
+    assert list(ptr) == b
+    assert all(ptr[i + 1] - ptr[i] <= cap for i in range(len(ptr) - 1))
+
+
+def test_sparse_stacks_dense_pattern_equals_dense_stacks(orc):
+    one = lambda r, c: np.ones((r, c), np.uint8)  # noqa: E731
+    for mloc, nloc, kb, cap in [(5, 3, 4, 6), (4, 4, 9, 5)]:
+        t1, p1 = orc.sparse_stacks(one(mloc, kb), one(kb, nloc), one(mloc, nloc), cap)
+        t2, p2 = orc.stacks(mloc, nloc, kb, cap)
+        assert np.array_equal(t1, t2) and np.array_equal(p1, p2)

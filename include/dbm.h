@@ -6,7 +6,7 @@
  * GPU), with Cannon's algorithm and either a blocked (stacks + batched small-block
  * GEMM) or a densified (densify -> one large GEMM -> undensify) local multiply.
  *
- * Citations: P:n = PAPER.md line n, S:n = SPEC.md line n; readings R1..R12 are
+ * Citations: P:n = PAPER.md line n, S:n = SPEC.md line n; readings R1..R15 are
  * listed in DESIGN.md §3.
  *
  * General conventions
@@ -28,6 +28,10 @@
  *    S:115), at slot li*nloc + lj; element (x,y) at slot*bs*bs + y*bs + x
  *    (column-major inside a block; DBCSR is Fortran).  The metadata is a
  *    blocked CSR (§II) with every block present (dense occupancy).
+ *  - Block-sparse matrices (dbm_matrix_create_sparse; reading R15, "occupancy between
+ *    0.01% up to dense"): only the stored blocks occupy the arena, in local CSR order (li
+ *    ascending, then lj ascending); slot = position in that order.  The dense layout above is
+ *    the all-stored special case.
  */
 #ifndef DBM_H
 #define DBM_H
@@ -54,7 +58,9 @@ typedef enum {
   DBM_ERR_NOMEM = 22
 } dbm_status;
 
-typedef enum { DBM_PATH_BLOCKED = 0, DBM_PATH_DENSIFIED = 1 } dbm_path;
+/* DBM_PATH_AUTO: densified iff both A's and B's occupancy (stored / all blocks) is >= the
+ * context's densify threshold (dbm_ctx_set_densify_threshold; default 1.0 = dense only). */
+typedef enum { DBM_PATH_BLOCKED = 0, DBM_PATH_DENSIFIED = 1, DBM_PATH_AUTO = 2 } dbm_path;
 
 typedef struct dbm_ctx_s* dbm_ctx;
 typedef struct dbm_matrix_s* dbm_matrix;
@@ -120,6 +126,8 @@ dbm_status dbm_ctx_set_algorithm(dbm_ctx ctx, int algorithm);
  * K is densified and multiplied chunk by chunk (GEMM-accumulate), so 63,360^3 fits in HBM.
  * bytes >= 1; changes dbm_multiply_workspace(). */
 dbm_status dbm_ctx_set_dense_chunk_bytes(dbm_ctx ctx, int64_t bytes);
+/* should_densify threshold for DBM_PATH_AUTO: occupancy in [0, 1]; default 1.0. */
+dbm_status dbm_ctx_set_densify_threshold(dbm_ctx ctx, double threshold);
 /* Total kernels this context has launched since creation. */
 dbm_status dbm_ctx_launch_count(dbm_ctx ctx, int64_t* out);
 dbm_status dbm_ctx_destroy(dbm_ctx ctx);
@@ -129,10 +137,28 @@ dbm_status dbm_ctx_destroy(dbm_ctx ctx);
  * block-cyclically over ctx's grid.  rows, cols must be multiples of bs (DBM_ERR_SHAPE;
  * reading R10).  Host metadata only; attach device storage before use. */
 dbm_status dbm_matrix_create(dbm_ctx ctx, int64_t rows, int64_t cols, int32_t block_size, dbm_matrix* out);
-/* Local share: mloc x nloc blocks; arena_bytes = mloc*nloc*bs*bs*8. */
+/* Block-sparse matrix (§8f-2, reading R15; P:86, P:157 blocked CSR).  mask: the GLOBAL
+ * pattern, (rows/bs) x (cols/bs) bytes row-major, nonzero = block stored; every rank passes the same
+ * mask (it is copied; the library keeps it so every rank can plan its peers' panels).  NULL mask = all
+ * stored, i.e. a dense matrix in the sparse code path.  The library allocates small device metadata
+ * arrays (slot -> (li, lj), (li, lj) -> slot) that dbm_matrix_destroy frees; the arena stays
+ * caller-owned.  Errors as dbm_matrix_create; DBM_ERR_NOMEM if the metadata allocation fails.
+ * In a multiply C keeps its pattern: products onto absent C blocks are not formed, beta scales every
+ * stored C block (DBCSR's retain-sparsity mode). */
+dbm_status dbm_matrix_create_sparse(dbm_ctx ctx, int64_t rows, int64_t cols, int32_t block_size,
+                                    const uint8_t* mask, dbm_matrix* out);
+/* Host-only: the seeded pattern generator of reading R15 / DESIGN.md §4: block (bi, bj) is stored iff
+ * u(seed, mat_id, bi, bj) < occupancy (u uniform in [0,1) from the counter generator's stream
+ * mat_id | 2^31).  mask: Mb x Nb bytes, row-major, caller-allocated. */
+dbm_status dbm_pattern_random(uint64_t seed, uint32_t mat_id, int64_t Mb, int64_t Nb, double occupancy,
+                              uint8_t* mask);
+/* Stored blocks: local (this rank) and global. */
+dbm_status dbm_matrix_nnz(dbm_matrix m, int64_t* local_blocks, int64_t* global_blocks);
+/* Local share: mloc x nloc blocks; arena_bytes = (stored local blocks)*bs*bs*8 (mloc*nloc*bs*bs*8 dense). */
 dbm_status dbm_matrix_local_info(dbm_matrix m, int64_t* mloc_blocks, int64_t* nloc_blocks, int64_t* arena_bytes);
-/* Blocked-CSR metadata of the local share: row_ptr[mloc+1] (= li*nloc), col_idx[mloc*nloc]
- * (global block column), row_idx[mloc] (global block row).  Host arrays, caller-allocated. */
+/* Blocked-CSR metadata of the local share: row_ptr[mloc+1], col_idx[local stored blocks]
+ * (global block column), row_idx[mloc] (global block row); dense: row_ptr[li] = li*nloc.  Host arrays,
+ * caller-allocated. */
 dbm_status dbm_matrix_local_csr(dbm_matrix m, int64_t* row_ptr, int64_t* col_idx, int64_t* row_idx);
 /* Attach caller-owned device storage of >= arena_bytes bytes, 16-byte aligned. */
 dbm_status dbm_matrix_attach(dbm_matrix m, void* device_arena, int64_t bytes);
@@ -140,7 +166,8 @@ dbm_status dbm_matrix_attach(dbm_matrix m, void* device_arena, int64_t bytes);
  * element (gi,gj) = f(seed, mat_id, gi, gj); kind 0 = U[-1,1), 1 = integers {-2..2}. */
 dbm_status dbm_matrix_fill_random(dbm_matrix m, uint64_t seed, uint32_t mat_id, int kind);
 /* Copy one locally-owned block (global indices) from / to a host column-major bs x bs array.
- * DBM_ERR_RANGE for indices outside the matrix, DBM_ERR_OWNERSHIP if another rank owns it.
+ * DBM_ERR_RANGE for indices outside the matrix or a block the pattern does not store,
+ * DBM_ERR_OWNERSHIP if another rank owns it.
  * Synchronous with respect to the host. */
 dbm_status dbm_matrix_set_block(dbm_matrix m, int64_t bi, int64_t bj, const double* host_colmajor);
 dbm_status dbm_matrix_get_block(dbm_matrix m, int64_t bi, int64_t bj, double* host_colmajor);
@@ -166,6 +193,9 @@ dbm_status dbm_multiply_workspace(dbm_ctx ctx, dbm_matrix A, dbm_matrix B, dbm_m
  * path BLOCKED: stacks of <= stack_cap (a,b,c) block triplets (0 -> 30000) executed
  *   by the batched small-block GEMM.
  * BLAS conventions (reading R8): beta == 0 -> C is not read; alpha == 0 -> A, B not read.
+ * Block-sparse operands (any of A, B, C from dbm_matrix_create_sparse; reading R15): the blocked
+ * path generates stacks from the stored blocks only and exchanges only stored blocks (copy-engine
+ * transport); the densified path densifies absent blocks as zeros; C keeps its pattern.
  * Errors before enqueue: SHAPE (A.cols != B.rows, A.rows != C.rows, B.cols != C.cols),
  * PARTITION (block sizes differ), ALIAS, GRID (different contexts), WORKSPACE.
  * stats may be NULL. */
@@ -200,7 +230,8 @@ dbm_status dbm_multiply_host(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_matrix
 /* ------------------------------------------------------- densify / undensify */
 /* Densify the whole local share ("a single block is formed from all the blocks
  * assigned to each thread"): dense is (mloc*bs) x (nloc*bs), layout 0 = column-major with
- * leading dimension ld >= mloc*bs, layout 1 = row-major with ld >= nloc*bs. Device memory. */
+ * leading dimension ld >= mloc*bs, layout 1 = row-major with ld >= nloc*bs. Device memory.
+ * Absent blocks of a sparse matrix densify to zeros; undensify writes stored blocks only. */
 dbm_status dbm_densify(dbm_matrix m, double* dense, int64_t ld, int layout);
 /* Undensify ("decomposed following the original block sizes") with scaling:
  * block(li,lj)(x,y) = alpha*D(li*bs+x, lj*bs+y) + beta*block (two roundings, no FMA; beta == 0 ->
@@ -210,7 +241,9 @@ dbm_status dbm_undensify(dbm_matrix m, const double* dense, int64_t ld, double a
 /* ------------------------------------------------------------------ debug */
 /* Run the GPU stack-generation kernel for Cannon step `step` of A*B into C on this rank and
  * copy the result to host: triplets[3*n] (a_slot, b_slot, c_slot) int32, stack_ptr[n_stacks+1].
- * Pass NULL arrays to query the sizes only.  Synchronous. */
+ * Sparse operands (R15): runs are the stored C blocks, entries the kk with A(li,kk) and B(kk,lj)
+ * both stored, slots ranks among the panel's stored blocks.  Pass NULL arrays to query the sizes
+ * only.  Synchronous. */
 dbm_status dbm_debug_stacks(dbm_ctx ctx, dbm_matrix A, dbm_matrix B, dbm_matrix C, int step, int32_t cap,
                             int32_t* triplets, int64_t* n_entries, int64_t* stack_ptr, int64_t* n_stacks);
 /* Raw dense FP64 GEMM kernel (the densified path's local multiply) on device buffers:

@@ -77,6 +77,13 @@ using namespace dbm;
 
 namespace {
 
+uint64_t next_serial() {
+  static std::mutex mu;
+  static uint64_t n = 0;
+  std::lock_guard<std::mutex> g(mu);
+  return ++n;
+}
+
 cudaEvent_t get_event(dbm_ctx ctx) {
   if (!ctx->ev_pool.empty()) {
     cudaEvent_t e = ctx->ev_pool.back();
@@ -277,6 +284,16 @@ extern "C" dbm_status dbm_ctx_set_dense_chunk_bytes(dbm_ctx ctx, int64_t bytes) 
   return DBM_OK;
 }
 
+extern "C" dbm_status dbm_ctx_set_densify_threshold(dbm_ctx ctx, double threshold) {
+  ARG_CHECK(ctx && threshold >= 0.0 && threshold <= 1.0, DBM_ERR_ARG, "threshold outside [0, 1]");
+  ctx->densify_threshold = threshold;
+  return DBM_OK;
+}
+
+namespace dbm {
+void free_sp_cache(dbm_ctx ctx);
+}
+
 extern "C" dbm_status dbm_ctx_launch_count(dbm_ctx ctx, int64_t* out) {
   ARG_CHECK(ctx && out, DBM_ERR_ARG, "null argument");
   *out = ctx->launches;
@@ -288,6 +305,7 @@ extern "C" dbm_status dbm_ctx_destroy(dbm_ctx ctx) {
   cudaSetDevice(ctx->device);
   cudaStreamSynchronize(ctx->stream);
   cudaStreamSynchronize(ctx->comm);
+  free_sp_cache(ctx);
   for (auto& r : ctx->prof) {
     cudaEventDestroy(r.a);
     cudaEventDestroy(r.b);
@@ -322,7 +340,83 @@ extern "C" dbm_status dbm_matrix_create(dbm_ctx ctx, int64_t rows, int64_t cols,
   m->Nb = cols / bs;
   m->mloc = local_count(m->Mb, ctx->pr, ctx->myrow);
   m->nloc = local_count(m->Nb, ctx->pc, ctx->mycol);
+  m->nnz = m->mloc * m->nloc;
+  m->gnnz = m->Mb * m->Nb;
+  m->serial = next_serial();
   *out = m;
+  return DBM_OK;
+}
+
+// ---- block sparsity (reading R15) ----
+static uint64_t host_mix64(uint64_t z) {
+  z ^= z >> 30;
+  z *= 0xBF58476D1CE4E5B9ull;
+  z ^= z >> 27;
+  z *= 0x94D049BB133111EBull;
+  z ^= z >> 31;
+  return z;
+}
+
+extern "C" dbm_status dbm_pattern_random(uint64_t seed, uint32_t mat_id, int64_t Mb, int64_t Nb, double occupancy,
+                                         uint8_t* mask) {
+  ARG_CHECK(Mb >= 0 && Nb >= 0, DBM_ERR_ARG, "negative block counts");
+  ARG_CHECK(Mb * Nb == 0 || mask, DBM_ERR_ARG, "null mask");
+  ARG_CHECK(occupancy >= 0.0 && occupancy <= 1.0, DBM_ERR_ARG, "occupancy outside [0, 1]");
+  const uint64_t key = host_mix64(seed + 0x9E3779B97F4A7C15ull * ((uint64_t)(mat_id | 0x80000000u) + 1ull));
+  for (int64_t bi = 0; bi < Mb; ++bi)
+    for (int64_t bj = 0; bj < Nb; ++bj) {
+      const uint64_t bits = host_mix64(key ^ host_mix64(((uint64_t)bi << 32) ^ (uint64_t)bj));
+      const double u = (double)(bits >> 11) * 0x1.0p-53;
+      mask[bi * Nb + bj] = u < occupancy ? 1 : 0;
+    }
+  return DBM_OK;
+}
+
+extern "C" dbm_status dbm_matrix_create_sparse(dbm_ctx ctx, int64_t rows, int64_t cols, int32_t bs,
+                                               const uint8_t* mask, dbm_matrix* out) {
+  dbm_matrix m = nullptr;
+  if (dbm_status s = dbm_matrix_create(ctx, rows, cols, bs, &m)) return s;
+  m->sparse = true;
+  const size_t nb = (size_t)(m->Mb * m->Nb);
+  m->gmask.assign(nb, 1);
+  if (mask)
+    for (size_t i = 0; i < nb; ++i) m->gmask[i] = mask[i] ? 1 : 0;
+  m->gnnz = 0;
+  for (size_t i = 0; i < nb; ++i) m->gnnz += m->gmask[i];
+  m->row_ptr.assign(m->mloc + 1, 0);
+  std::vector<int32_t> ij;
+  std::vector<int32_t> map((size_t)(m->mloc * m->nloc), -1);
+  for (int64_t li = 0; li < m->mloc; ++li) {
+    for (int64_t lj = 0; lj < m->nloc; ++lj)
+      if (m->gmask[(size_t)(ctx->myrow + li * ctx->pr) * m->Nb + ctx->mycol + lj * ctx->pc]) {
+        map[(size_t)(li * m->nloc + lj)] = (int32_t)m->col.size();
+        m->col.push_back((int32_t)lj);
+        ij.push_back((int32_t)li);
+        ij.push_back((int32_t)lj);
+      }
+    m->row_ptr[li + 1] = (int64_t)m->col.size();
+  }
+  m->nnz = (int64_t)m->col.size();
+  auto fail = [&](cudaError_t e) {
+    set_error(std::string("sparse metadata: ") + cudaGetErrorString(e));
+    dbm_matrix_destroy(m);
+    return DBM_ERR_NOMEM;
+  };
+  if (cudaError_t e = cudaSetDevice(ctx->device)) return fail(e);
+  if (cudaError_t e = cudaMalloc(&m->d_ij, std::max<size_t>(ij.size(), 2) * 4)) return fail(e);
+  if (cudaError_t e = cudaMalloc(&m->d_map, std::max<size_t>(map.size(), 1) * 4)) return fail(e);
+  if (!ij.empty())
+    if (cudaError_t e = cudaMemcpy(m->d_ij, ij.data(), ij.size() * 4, cudaMemcpyHostToDevice)) return fail(e);
+  if (!map.empty())
+    if (cudaError_t e = cudaMemcpy(m->d_map, map.data(), map.size() * 4, cudaMemcpyHostToDevice)) return fail(e);
+  *out = m;
+  return DBM_OK;
+}
+
+extern "C" dbm_status dbm_matrix_nnz(dbm_matrix m, int64_t* local_blocks, int64_t* global_blocks) {
+  ARG_CHECK(m, DBM_ERR_ARG, "null matrix");
+  if (local_blocks) *local_blocks = m->blocks();
+  if (global_blocks) *global_blocks = m->gnnz;
   return DBM_OK;
 }
 
@@ -330,7 +424,7 @@ extern "C" dbm_status dbm_matrix_local_info(dbm_matrix m, int64_t* mloc, int64_t
   ARG_CHECK(m, DBM_ERR_ARG, "null matrix");
   if (mloc) *mloc = m->mloc;
   if (nloc) *nloc = m->nloc;
-  if (bytes) *bytes = m->mloc * m->nloc * (int64_t)m->bs * m->bs * 8;
+  if (bytes) *bytes = m->blocks() * (int64_t)m->bs * m->bs * 8;
   return DBM_OK;
 }
 
@@ -338,18 +432,22 @@ extern "C" dbm_status dbm_matrix_local_csr(dbm_matrix m, int64_t* row_ptr, int64
   ARG_CHECK(m, DBM_ERR_ARG, "null matrix");
   const dbm_ctx c = m->ctx;
   for (int64_t li = 0; li <= m->mloc; ++li)
-    if (row_ptr) row_ptr[li] = li * m->nloc;
+    if (row_ptr) row_ptr[li] = m->sparse ? m->row_ptr[li] : li * m->nloc;
   for (int64_t li = 0; li < m->mloc; ++li) {
     if (row_idx) row_idx[li] = c->myrow + li * c->pr;
-    for (int64_t lj = 0; lj < m->nloc; ++lj)
-      if (col_idx) col_idx[li * m->nloc + lj] = c->mycol + lj * c->pc;
+    if (!col_idx) continue;
+    if (m->sparse) {
+      for (int64_t s = m->row_ptr[li]; s < m->row_ptr[li + 1]; ++s) col_idx[s] = c->mycol + (int64_t)m->col[s] * c->pc;
+    } else {
+      for (int64_t lj = 0; lj < m->nloc; ++lj) col_idx[li * m->nloc + lj] = c->mycol + lj * c->pc;
+    }
   }
   return DBM_OK;
 }
 
 extern "C" dbm_status dbm_matrix_attach(dbm_matrix m, void* arena, int64_t bytes) {
   ARG_CHECK(m, DBM_ERR_ARG, "null matrix");
-  const int64_t need = m->mloc * m->nloc * (int64_t)m->bs * m->bs * 8;
+  const int64_t need = m->blocks() * (int64_t)m->bs * m->bs * 8;
   ARG_CHECK(bytes >= need, DBM_ERR_WORKSPACE, "arena smaller than dbm_matrix_local_info() bytes");
   ARG_CHECK(need == 0 || arena != nullptr, DBM_ERR_ARG, "null arena");
   ARG_CHECK(((uintptr_t)arena & 15) == 0, DBM_ERR_ARG, "arena must be 16-byte aligned");
@@ -359,7 +457,7 @@ extern "C" dbm_status dbm_matrix_attach(dbm_matrix m, void* arena, int64_t bytes
 }
 
 static dbm_status need_arena(dbm_matrix m) {
-  const int64_t need = m->mloc * m->nloc * (int64_t)m->bs * m->bs * 8;
+  const int64_t need = m->blocks() * (int64_t)m->bs * m->bs * 8;
   ARG_CHECK(need == 0 || m->arena, DBM_ERR_WORKSPACE, "matrix has no attached arena");
   return DBM_OK;
 }
@@ -370,9 +468,13 @@ extern "C" dbm_status dbm_matrix_fill_random(dbm_matrix m, uint64_t seed, uint32
   dbm_ctx ctx = m->ctx;
   CTX_OK(ctx);
   if (dbm_status s = need_arena(m)) return s;
-  launch_fill(m->arena, m->mloc, m->nloc, m->bs, ctx->pr, ctx->pc, ctx->myrow, ctx->mycol, seed, mat_id, kind,
-              ctx->stream);
-  ctx->launches += (m->mloc * m->nloc) ? 1 : 0;
+  if (m->sparse)
+    launch_fill_sparse(m->arena, m->nnz, m->d_ij, m->bs, ctx->pr, ctx->pc, ctx->myrow, ctx->mycol, seed, mat_id, kind,
+                       ctx->stream);
+  else
+    launch_fill(m->arena, m->mloc, m->nloc, m->bs, ctx->pr, ctx->pc, ctx->myrow, ctx->mycol, seed, mat_id, kind,
+                ctx->stream);
+  ctx->launches += m->blocks() ? 1 : 0;
   CUDA_TRY(ctx, cudaGetLastError());
   return DBM_OK;
 }
@@ -381,7 +483,15 @@ static dbm_status block_slot(dbm_matrix m, int64_t bi, int64_t bj, int64_t* slot
   ARG_CHECK(bi >= 0 && bj >= 0 && bi < m->Mb && bj < m->Nb, DBM_ERR_RANGE, "block index out of range");
   const dbm_ctx c = m->ctx;
   ARG_CHECK(bi % c->pr == c->myrow && bj % c->pc == c->mycol, DBM_ERR_OWNERSHIP, "block owned by another rank");
-  *slot = (bi / c->pr) * m->nloc + (bj / c->pc);
+  const int64_t li = bi / c->pr, lj = bj / c->pc;
+  if (!m->sparse) {
+    *slot = li * m->nloc + lj;
+    return DBM_OK;
+  }
+  const auto b = m->col.begin() + m->row_ptr[li], e = m->col.begin() + m->row_ptr[li + 1];
+  const auto it = std::lower_bound(b, e, (int32_t)lj);
+  ARG_CHECK(it != e && *it == (int32_t)lj, DBM_ERR_RANGE, "block not stored in the sparsity pattern");
+  *slot = (int64_t)(it - m->col.begin());
   return DBM_OK;
 }
 
@@ -415,7 +525,7 @@ extern "C" dbm_status dbm_matrix_get_block(dbm_matrix m, int64_t bi, int64_t bj,
 // pinned double buffer (P:174 double buffering, P:200 page-locked memory pools).
 static dbm_status host_copy(dbm_matrix m, void* host, bool upload) {
   dbm_ctx ctx = m->ctx;
-  const size_t bytes = (size_t)(m->mloc * m->nloc) * m->bs * m->bs * 8;
+  const size_t bytes = (size_t)m->blocks() * m->bs * m->bs * 8;
   if (bytes == 0) return DBM_OK;
   cudaPointerAttributes at;
   bool pinned = cudaPointerGetAttributes(&at, host) == cudaSuccess &&
@@ -482,6 +592,11 @@ extern "C" dbm_status dbm_owner_of_block(dbm_matrix m, int64_t bi, int64_t bj, i
 }
 
 extern "C" dbm_status dbm_matrix_destroy(dbm_matrix m) {
+  if (m && (m->d_ij || m->d_map)) {
+    cudaSetDevice(m->ctx->device);
+    if (m->d_ij) cudaFree(m->d_ij);
+    if (m->d_map) cudaFree(m->d_map);
+  }
   delete m;
   return DBM_OK;
 }
@@ -497,7 +612,11 @@ extern "C" dbm_status dbm_densify(dbm_matrix m, double* dense, int64_t ld, int l
   ARG_CHECK(ld >= (layout == 0 ? rows : cols), DBM_ERR_PLAN, "leading dimension too small");
   ARG_CHECK(rows * cols == 0 || dense, DBM_ERR_ARG, "null dense buffer");
   ProfScope ps(ctx, ctx->stream, 2, 0.0, 16.0 * rows * cols);
-  launch_densify_cols(m->arena, m->mloc, m->nloc, m->bs, 0, 1, m->nloc, dense, ld, layout, ctx->stream);
+  if (m->sparse)
+    CUDA_TRY(ctx, launch_sp_densify(m->arena, m->d_ij, m->nnz, m->bs, 0, 0, 1, m->nloc, m->mloc, dense, ld, layout,
+                                    ctx->stream));
+  else
+    launch_densify_cols(m->arena, m->mloc, m->nloc, m->bs, 0, 1, m->nloc, dense, ld, layout, ctx->stream);
   ctx->launches += rows * cols ? 1 : 0;
   CUDA_TRY(ctx, cudaGetLastError());
   return DBM_OK;
@@ -512,7 +631,10 @@ extern "C" dbm_status dbm_undensify(dbm_matrix m, const double* dense, int64_t l
   ARG_CHECK(ld >= rows, DBM_ERR_PLAN, "leading dimension too small");
   ARG_CHECK(rows * cols == 0 || dense, DBM_ERR_ARG, "null dense buffer");
   ProfScope ps(ctx, ctx->stream, 3, 0.0, (beta == 0.0 ? 16.0 : 24.0) * rows * cols);
-  launch_undensify(dense, ld, 1, 0, m->mloc, m->nloc, m->bs, alpha, beta, m->arena, ctx->stream);
+  if (m->sparse)
+    launch_sp_undensify(dense, ld, 1, 0, m->d_ij, m->nnz, m->bs, alpha, beta, m->arena, ctx->stream);
+  else
+    launch_undensify(dense, ld, 1, 0, m->mloc, m->nloc, m->bs, alpha, beta, m->arena, ctx->stream);
   ctx->launches += rows * cols ? 1 : 0;
   CUDA_TRY(ctx, cudaGetLastError());
   return DBM_OK;
@@ -700,8 +822,8 @@ dbm_status validate(dbm_ctx ctx, dbm_matrix A, dbm_matrix B, dbm_matrix C) {
   ARG_CHECK(C != A && C != B, DBM_ERR_ALIAS, "C aliases A or B");
   auto overlap = [](dbm_matrix x, dbm_matrix y) {
     if (!x->arena || !y->arena) return false;
-    const char *a0 = (const char*)x->arena, *a1 = a0 + x->mloc * x->nloc * x->bs * x->bs * 8;
-    const char *b0 = (const char*)y->arena, *b1 = b0 + y->mloc * y->nloc * y->bs * y->bs * 8;
+    const char *a0 = (const char*)x->arena, *a1 = a0 + x->blocks() * x->bs * x->bs * 8;
+    const char *b0 = (const char*)y->arena, *b1 = b0 + y->blocks() * y->bs * y->bs * 8;
     return a0 < b1 && b0 < a1;
   };
   ARG_CHECK(!overlap(C, A) && !overlap(C, B), DBM_ERR_ALIAS, "C storage overlaps A or B");
@@ -709,6 +831,34 @@ dbm_status validate(dbm_ctx ctx, dbm_matrix A, dbm_matrix B, dbm_matrix C) {
   if (dbm_status s = need_arena(B)) return s;
   if (dbm_status s = need_arena(C)) return s;
   return DBM_OK;
+}
+
+// Densify / undensify a possibly block-sparse matrix (reading R15: absent blocks densify to zeros,
+// undensify writes the stored C blocks only).  Panels as launch_densify_cols / _rows.
+dbm_status densify_a(dbm_ctx ctx, dbm_matrix A, int64_t col0, int64_t stride, int64_t nk, double* dst, int64_t ld,
+                     int layout, cudaStream_t cs) {
+  if (A->sparse)
+    CUDA_TRY(ctx, launch_sp_densify(A->arena, A->d_ij, A->nnz, A->bs, 0, col0, stride, nk, A->mloc, dst, ld, layout,
+                                    cs));
+  else
+    launch_densify_cols(A->arena, A->mloc, A->nloc, A->bs, col0, stride, nk, dst, ld, layout, cs);
+  return DBM_OK;
+}
+dbm_status densify_b(dbm_ctx ctx, dbm_matrix B, int64_t row0, int64_t stride, int64_t nk, double* dst, int64_t ld,
+                     int layout, cudaStream_t cs) {
+  if (B->sparse)
+    CUDA_TRY(ctx, launch_sp_densify(B->arena, B->d_ij, B->nnz, B->bs, 1, row0, stride, nk, B->nloc, dst, ld, layout,
+                                    cs));
+  else
+    launch_densify_rows(B->arena, B->nloc, B->bs, row0, stride, nk, dst, ld, layout, cs);
+  return DBM_OK;
+}
+void undensify_c(dbm_matrix C, const double* dense, int64_t ld, int nsplit, int64_t split_stride, double alpha,
+                 double beta, cudaStream_t cs) {
+  if (C->sparse)
+    launch_sp_undensify(dense, ld, nsplit, split_stride, C->d_ij, C->nnz, C->bs, alpha, beta, C->arena, cs);
+  else
+    launch_undensify(dense, ld, nsplit, split_stride, C->mloc, C->nloc, C->bs, alpha, beta, C->arena, cs);
 }
 
 }  // namespace
@@ -998,16 +1148,16 @@ dbm_status multiply_tallskinny(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_matr
     const int q = tr * t.pc + t.c;
     if (!t.kp[q] || !t.mrows[t.r]) continue;
     ProfScope ps(ctx, cs, 2, 0.0, 16.0 * t.mrows[t.r] * t.kp[q] * bs);
-    launch_densify_cols(A->arena, A->mloc, A->nloc, (int)bs, tr, t.pr, t.kp[q], (double*)(ws + t.offApiece[tr]),
-                        t.ld(q), 1, cs);
+    if (dbm_status e = densify_a(ctx, A, tr, t.pr, t.kp[q], (double*)(ws + t.offApiece[tr]), t.ld(q), 1, cs))
+      return e;
     ++*launches;
   }
   for (int tt = 0; tt < t.pc; ++tt) {
     const int q = t.r + tt * t.pr;
     if (!t.kp[q] || !t.ncols[t.c]) continue;
     ProfScope ps(ctx, cs, 2, 0.0, 16.0 * t.ncols[t.c] * t.kp[q] * bs);
-    launch_densify_rows(B->arena, B->nloc, (int)bs, tt, t.pc, t.kp[q], (double*)(ws + t.offBpiece[tt]), t.ld(q), 0,
-                        cs);
+    if (dbm_status e = densify_b(ctx, B, tt, t.pc, t.kp[q], (double*)(ws + t.offBpiece[tt]), t.ld(q), 0, cs))
+      return e;
     ++*launches;
   }
   CUDA_TRY(ctx, cudaGetLastError());
@@ -1077,7 +1227,7 @@ dbm_status multiply_tallskinny(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_matr
   }
   if (mr * nc > 0) {
     ProfScope ps(ctx, cs, 3, 0.0, (8.0 * P + (beta == 0.0 ? 8.0 : 16.0)) * mr * nc);
-    launch_undensify(cstack, mr, (int)P, mr * nc, C->mloc, C->nloc, (int)bs, alpha, beta, C->arena, cs);
+    undensify_c(C, cstack, mr, (int)P, mr * nc, alpha, beta, cs);
     ++*launches;
     CUDA_TRY(ctx, cudaGetLastError());
   }
@@ -1093,11 +1243,470 @@ dbm_status multiply_tallskinny(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_matr
 
 }  // namespace
 
+// ====================================================================== block-sparse blocked path (R15)
+// Cannon over sparse panels (§8f-2).  Every rank knows every operand's global pattern, so each rank
+// plans on the host, once per (A, B, C) pattern triple (cached in the context): the CSR / CSC lists
+// of each step's A(r, kappa) and B(kappa, c) panels (kk ascending, slot = rank among the panel's stored
+// blocks in row-major order = the order the owner packs them), the gather lists of the panels it owns,
+// and its peers' workspace offsets.  Per multiply the GPU packs the owned panels (stored blocks only),
+// the copy engines pull the remote ones (only stored blocks move), and per step the Generation
+// kernels + smm_sparse run over the traversal in chunks of runs.
+namespace dbm {
+struct SpStep {
+  int kappa = 0, a_src = 0, b_src = 0;
+  int64_t a_nnz = 0, b_nnz = 0, entries = 0;
+  size_t o_aptr = 0, o_akk = 0, o_bptr = 0, o_bkk = 0, o_bslot = 0;  // int32 offsets into d_meta
+  std::vector<int32_t> run_len;                                      // per traversal position
+};
+struct SpCache {
+  uint64_t a_serial = 0, b_serial = 0, c_serial = 0;
+  int L = 1;
+  std::vector<SpStep> steps;
+  std::vector<int64_t> ownA_nnz, ownB_nnz;  // per kappa (-1: not mine)
+  std::vector<size_t> ownA_off, ownB_off, o_gatherA, o_gatherB;
+  std::vector<std::vector<size_t>> peer_ownA_off, peer_ownB_off;
+  std::vector<std::vector<int64_t>> peer_ownA_nnz, peer_ownB_nnz;
+  size_t off_recvA[2] = {0, 0}, off_recvB[2] = {0, 0}, off_trav = 0, off_cnt = 0, off_off = 0, off_scan = 0;
+  size_t off_trip = 0, scan_bytes = 0, total = 256;
+  int64_t runs_per_chunk = 1;
+  int32_t* d_meta = nullptr;
+  std::vector<std::pair<int64_t, int64_t>> stacks_by_cap;  // (cap, stacks of the whole multiply)
+};
+
+void free_sp_cache(dbm_ctx ctx) {
+  for (SpCache* c : ctx->sp_cache) {
+    if (c->d_meta) cudaFree(c->d_meta);
+    delete c;
+  }
+  ctx->sp_cache.clear();
+}
+}  // namespace dbm
+
+namespace {
+
+int64_t local_slot(dbm_matrix m, int64_t li, int64_t lj) {
+  if (!m->sparse) return li * m->nloc + lj;
+  const auto b = m->col.begin() + m->row_ptr[li], e = m->col.begin() + m->row_ptr[li + 1];
+  const auto it = std::lower_bound(b, e, (int32_t)lj);
+  return (it != e && *it == (int32_t)lj) ? (int64_t)(it - m->col.begin()) : -1;
+}
+
+void host_traversal(int64_t r0, int64_t r1, int64_t c0, int64_t c1, std::vector<int32_t>& li, std::vector<int32_t>& lj) {
+  if (r1 <= r0 || c1 <= c0) return;
+  if (r1 - r0 == 1 && c1 - c0 == 1) {
+    li.push_back((int32_t)r0);
+    lj.push_back((int32_t)c0);
+    return;
+  }
+  if (r1 - r0 >= c1 - c0) {
+    const int64_t mid = r0 + (r1 - r0) / 2;
+    host_traversal(r0, mid, c0, c1, li, lj);
+    host_traversal(mid, r1, c0, c1, li, lj);
+  } else {
+    const int64_t mid = c0 + (c1 - c0) / 2;
+    host_traversal(r0, r1, c0, mid, li, lj);
+    host_traversal(r0, r1, mid, c1, li, lj);
+  }
+}
+
+// Stored blocks of the A(rr, kappa) / B(kappa, cc) panels, as owned by rank (rr, kappa mod Pc) /
+// (kappa mod Pr, cc).
+int64_t a_panel_nnz(dbm_ctx ctx, dbm_matrix A, int L, int rr, int kappa) {
+  int64_t n = 0;
+  for (int64_t i = rr; i < A->Mb; i += ctx->pr)
+    for (int64_t k = kappa; k < A->Nb; k += L) n += A->stored(i, k);
+  return n;
+}
+int64_t b_panel_nnz(dbm_ctx ctx, dbm_matrix B, int L, int cc, int kappa) {
+  int64_t n = 0;
+  for (int64_t k = kappa; k < B->Mb; k += L)
+    for (int64_t j = cc; j < B->Nb; j += ctx->pc) n += B->stored(k, j);
+  return n;
+}
+
+// Workspace layout: own (packed) panels first, so a peer only needs the panel sizes to find them.
+void own_layout(dbm_ctx ctx, dbm_matrix A, dbm_matrix B, int L, int r, int c, std::vector<int64_t>& a_nnz,
+                std::vector<int64_t>& b_nnz, std::vector<size_t>& a_off, std::vector<size_t>& b_off, size_t* end) {
+  const size_t bb8 = (size_t)A->bs * A->bs * 8;
+  a_nnz.assign(L, -1);
+  b_nnz.assign(L, -1);
+  a_off.assign(L, SIZE_MAX);
+  b_off.assign(L, SIZE_MAX);
+  size_t off = 0;
+  if (ctx->nranks > 1) {
+    for (int k = 0; k < L; ++k)
+      if (k % ctx->pc == c) {
+        a_nnz[k] = a_panel_nnz(ctx, A, L, r, k);
+        a_off[k] = off;
+        off = align256(off + (size_t)a_nnz[k] * bb8);
+      }
+    for (int k = 0; k < L; ++k)
+      if (k % ctx->pr == r) {
+        b_nnz[k] = b_panel_nnz(ctx, B, L, c, k);
+        b_off[k] = off;
+        off = align256(off + (size_t)b_nnz[k] * bb8);
+      }
+  }
+  *end = off;
+}
+
+dbm_status sp_cache_get(dbm_ctx ctx, dbm_matrix A, dbm_matrix B, dbm_matrix C, SpCache** out) {
+  for (SpCache* c : ctx->sp_cache)
+    if (c->a_serial == A->serial && c->b_serial == B->serial && c->c_serial == C->serial) {
+      *out = c;
+      return DBM_OK;
+    }
+  SpCache* sc = new SpCache();
+  sc->a_serial = A->serial;
+  sc->b_serial = B->serial;
+  sc->c_serial = C->serial;
+  const int pr = ctx->pr, pc = ctx->pc, r = ctx->myrow, c = ctx->mycol, me = ctx->rank;
+  const int L = (int)lcm64(pr, pc);
+  sc->L = L;
+  const int64_t mloc = C->mloc, nloc = C->nloc, Kb = A->Nb;
+  const size_t bb8 = (size_t)A->bs * A->bs * 8;
+  size_t off = 0;
+  own_layout(ctx, A, B, L, r, c, sc->ownA_nnz, sc->ownB_nnz, sc->ownA_off, sc->ownB_off, &off);
+  sc->peer_ownA_off.resize(ctx->nranks);
+  sc->peer_ownB_off.resize(ctx->nranks);
+  sc->peer_ownA_nnz.resize(ctx->nranks);
+  sc->peer_ownB_nnz.resize(ctx->nranks);
+  for (int q = 0; q < ctx->nranks && ctx->nranks > 1; ++q) {
+    size_t e;
+    if (q != me)
+      own_layout(ctx, A, B, L, q / pc, q % pc, sc->peer_ownA_nnz[q], sc->peer_ownB_nnz[q], sc->peer_ownA_off[q],
+                 sc->peer_ownB_off[q], &e);
+  }
+  // per-step panel metadata and entry counts
+  std::vector<int32_t> meta;
+  std::vector<int32_t> tli, tlj;
+  host_traversal(0, mloc, 0, nloc, tli, tlj);
+  const int64_t words = 0;
+  (void)words;
+  int64_t kbmax = 1, amax = 0, bmax = 0;
+  int na = 0, nb = 0;
+  sc->steps.resize(L);
+  for (int s = 0; s < L; ++s) {
+    SpStep& st = sc->steps[s];
+    st.kappa = (r + c + s) % L;
+    st.a_src = r * pc + st.kappa % pc;
+    st.b_src = (st.kappa % pr) * pc + c;
+    const int64_t kb = local_count(Kb, L, st.kappa);
+    kbmax = std::max(kbmax, kb);
+    // A panel CSR over li
+    std::vector<std::vector<uint64_t>> abits(mloc, std::vector<uint64_t>((kb + 63) / 64, 0));
+    st.o_aptr = meta.size();
+    meta.resize(meta.size() + mloc + 1);
+    std::vector<int32_t> akk;
+    for (int64_t li = 0; li < mloc; ++li) {
+      meta[st.o_aptr + li] = (int32_t)akk.size();
+      for (int64_t kk = 0; kk < kb; ++kk)
+        if (A->stored(r + li * pr, st.kappa + kk * L)) {
+          akk.push_back((int32_t)kk);
+          abits[li][kk >> 6] |= 1ull << (kk & 63);
+        }
+    }
+    meta[st.o_aptr + mloc] = (int32_t)akk.size();
+    st.a_nnz = (int64_t)akk.size();
+    st.o_akk = meta.size();
+    meta.insert(meta.end(), akk.begin(), akk.end());
+    // B panel: row-major slots over (kk, lj), CSC lists per lj
+    std::vector<std::vector<uint64_t>> bbits(nloc, std::vector<uint64_t>((kb + 63) / 64, 0));
+    std::vector<std::vector<std::pair<int32_t, int32_t>>> bcol(nloc);
+    int32_t slot = 0;
+    for (int64_t kk = 0; kk < kb; ++kk)
+      for (int64_t lj = 0; lj < nloc; ++lj)
+        if (B->stored(st.kappa + kk * L, c + lj * pc)) {
+          bcol[lj].push_back({(int32_t)kk, slot++});
+          bbits[lj][kk >> 6] |= 1ull << (kk & 63);
+        }
+    st.b_nnz = slot;
+    st.o_bptr = meta.size();
+    meta.resize(meta.size() + nloc + 1);
+    std::vector<int32_t> bkk, bsl;
+    for (int64_t lj = 0; lj < nloc; ++lj) {
+      meta[st.o_bptr + lj] = (int32_t)bkk.size();
+      for (auto& pr_ : bcol[lj]) {
+        bkk.push_back(pr_.first);
+        bsl.push_back(pr_.second);
+      }
+    }
+    meta[st.o_bptr + nloc] = (int32_t)bkk.size();
+    st.o_bkk = meta.size();
+    meta.insert(meta.end(), bkk.begin(), bkk.end());
+    st.o_bslot = meta.size();
+    meta.insert(meta.end(), bsl.begin(), bsl.end());
+    // run lengths in traversal order (stored C blocks only)
+    st.run_len.resize(tli.size());
+    for (size_t q = 0; q < tli.size(); ++q) {
+      const int64_t li = tli[q], lj = tlj[q];
+      int64_t n = 0;
+      if (C->stored(r + li * pr, c + lj * pc))
+        for (size_t w = 0; w < abits[li].size(); ++w) n += __builtin_popcountll(abits[li][w] & bbits[lj][w]);
+      st.run_len[q] = (int32_t)n;
+      st.entries += n;
+    }
+    if (st.a_src != me) {
+      amax = std::max(amax, st.a_nnz);
+      ++na;
+    }
+    if (st.b_src != me) {
+      bmax = std::max(bmax, st.b_nnz);
+      ++nb;
+    }
+  }
+  // gather lists of my own panels (multi-rank: packed into the workspace for the peers and myself)
+  sc->o_gatherA.assign(L, SIZE_MAX);
+  sc->o_gatherB.assign(L, SIZE_MAX);
+  for (int k = 0; k < L && ctx->nranks > 1; ++k) {
+    if (sc->ownA_nnz[k] >= 0) {
+      sc->o_gatherA[k] = meta.size();
+      for (int64_t li = 0; li < A->mloc; ++li)
+        for (int64_t kg = k; kg < Kb; kg += L)
+          if (A->stored(r + li * pr, kg)) meta.push_back((int32_t)local_slot(A, li, (kg - c) / pc));
+    }
+    if (sc->ownB_nnz[k] >= 0) {
+      sc->o_gatherB[k] = meta.size();
+      for (int64_t kg = k; kg < Kb; kg += L)
+        for (int64_t lj = 0; lj < B->nloc; ++lj)
+          if (B->stored(kg, c + lj * pc)) meta.push_back((int32_t)local_slot(B, (kg - r) / pr, lj));
+    }
+  }
+  // the rest of the workspace
+  auto take = [&](size_t bytes) {
+    size_t o = off;
+    off = align256(off + bytes);
+    return o;
+  };
+  for (int i = 0; i < std::min(na, 2); ++i) sc->off_recvA[i] = take((size_t)amax * bb8);
+  for (int i = 0; i < std::min(nb, 2); ++i) sc->off_recvB[i] = take((size_t)bmax * bb8);
+  const int64_t nruns = std::max<int64_t>(mloc * nloc, 1);
+  sc->off_trav = take((size_t)nruns * 8);
+  sc->runs_per_chunk = std::max<int64_t>(1, std::min<int64_t>(nruns, kTripChunkEntries / kbmax));
+  sc->off_cnt = take((size_t)(sc->runs_per_chunk + 1) * 8);
+  sc->off_off = take((size_t)(sc->runs_per_chunk + 1) * 8);
+  sc->scan_bytes = sp_scan_temp_bytes(sc->runs_per_chunk + 1);
+  sc->off_scan = take(sc->scan_bytes);
+  sc->off_trip = take((size_t)sc->runs_per_chunk * kbmax * 12);
+  sc->total = std::max<size_t>(off, 256);
+  cudaError_t e = cudaMalloc(&sc->d_meta, std::max<size_t>(meta.size(), 1) * 4);
+  if (e == cudaSuccess && !meta.empty())
+    e = cudaMemcpy(sc->d_meta, meta.data(), meta.size() * 4, cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) {
+    if (sc->d_meta) cudaFree(sc->d_meta);
+    delete sc;
+    set_error(std::string("sparse plan metadata: ") + cudaGetErrorString(e));
+    return DBM_ERR_NOMEM;
+  }
+  ctx->sp_cache.push_back(sc);
+  *out = sc;
+  return DBM_OK;
+}
+
+int64_t sp_stacks(SpCache* sc, int64_t cap) {
+  for (auto& pcs : sc->stacks_by_cap)
+    if (pcs.first == cap) return pcs.second;
+  int64_t ns = 0;
+  for (const SpStep& st : sc->steps) {  // greedy whole-run packing, runs > cap split (reading R6)
+    int64_t cur = 0;
+    for (int32_t n : st.run_len) {
+      if (n == 0) continue;
+      if (n > cap) {
+        if (cur) ++ns;
+        cur = 0;
+        ns += (n + cap - 1) / cap;
+      } else {
+        if (cur + n > cap) {
+          ++ns;
+          cur = 0;
+        }
+        cur += n;
+      }
+    }
+    if (cur) ++ns;
+  }
+  sc->stacks_by_cap.push_back({cap, ns});
+  return ns;
+}
+
+dbm_status multiply_sparse_blocked(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_matrix B, double beta, dbm_matrix C,
+                                   int32_t stack_cap, void* workspace, int64_t ws_bytes, dbm_stats* stats) {
+  ARG_CHECK(ctx->nranks == 1 || ctx->transport == 0, DBM_ERR_ARG,
+            "the block-sparse blocked path uses the copy-engine transport");
+  SpCache* sc = nullptr;
+  if (dbm_status e = sp_cache_get(ctx, A, B, C, &sc)) return e;
+  ARG_CHECK(workspace != nullptr && ws_bytes >= (int64_t)sc->total, DBM_ERR_WORKSPACE,
+            "workspace smaller than dbm_multiply_workspace()");
+  const int64_t cap = stack_cap ? stack_cap : 30000;
+  cudaStream_t cs = ctx->stream;
+  char* ws = (char*)workspace;
+  const int bs = A->bs;
+  const int64_t bb = (int64_t)bs * bs, mloc = C->mloc, nloc = C->nloc, L = sc->L;
+  const int me = ctx->rank;
+  dbm_stats st{};
+  st.steps = L;
+  int launches = 0;
+  auto scale_c = [&](double f) -> dbm_status {
+    const int64_t n = C->blocks() * bb;
+    if (n && f != 1.0) {
+      scale_kernel<<<(unsigned)std::min<int64_t>((n + 255) / 256, num_sms() * 16), 256, 0, cs>>>(C->arena, n, f);
+      ++launches;
+      CUDA_TRY(ctx, cudaGetLastError());
+    }
+    return DBM_OK;
+  };
+  // beta scales every stored C block once (R15); the steps then accumulate alpha * A * B
+  if (dbm_status e = scale_c(beta)) return e;
+  if (alpha == 0.0 || A->Nb == 0) {
+    ctx->launches += launches;
+    st.kernel_launches = launches;
+    if (stats) *stats = st;
+    return DBM_OK;
+  }
+  const int32_t* meta = sc->d_meta;
+  if (ctx->nranks > 1) {  // pack my panels (stored blocks only)
+    for (int k = 0; k < L; ++k) {
+      if (sc->ownA_nnz[k] > 0) {
+        launch_sp_gather(A->arena, meta + sc->o_gatherA[k], sc->ownA_nnz[k], bs, (double*)(ws + sc->ownA_off[k]), cs);
+        ++launches;
+      }
+      if (sc->ownB_nnz[k] > 0) {
+        launch_sp_gather(B->arena, meta + sc->o_gatherB[k], sc->ownB_nnz[k], bs, (double*)(ws + sc->ownB_off[k]), cs);
+        ++launches;
+      }
+    }
+    CUDA_TRY(ctx, cudaGetLastError());
+  }
+  int32_t* trav_li = (int32_t*)(ws + sc->off_trav);
+  int32_t* trav_lj = trav_li + std::max<int64_t>(mloc * nloc, 1);
+  {
+    ProfScope ps(ctx, cs, 4, 0.0, 8.0 * mloc * nloc);
+    launch_traversal(mloc, nloc, trav_li, trav_lj, cs);
+    launches += (mloc * nloc) ? 1 : 0;
+  }
+  std::vector<cudaEvent_t> ev_x(L, nullptr), ev_g(L, nullptr);
+  cudaEvent_t ev_ready = nullptr;
+  std::vector<int> bufA(L, -1), bufB(L, -1);
+  auto pulls = [&](int s) -> dbm_status {
+    const SpStep& x = sc->steps[s];
+    if (x.a_src != me && x.a_nnz) {
+      CUDA_TRY(ctx, cudaMemcpyAsync(ws + sc->off_recvA[bufA[s]], ctx->peer_ws[x.a_src] + sc->peer_ownA_off[x.a_src][x.kappa],
+                                    (size_t)x.a_nnz * bb * 8, cudaMemcpyDeviceToDevice, ctx->comm));
+    }
+    if (x.b_src != me && x.b_nnz) {
+      CUDA_TRY(ctx, cudaMemcpyAsync(ws + sc->off_recvB[bufB[s]], ctx->peer_ws[x.b_src] + sc->peer_ownB_off[x.b_src][x.kappa],
+                                    (size_t)x.b_nnz * bb * 8, cudaMemcpyDeviceToDevice, ctx->comm));
+    }
+    if (x.a_src != me) st.bytes_recv += x.a_nnz * bb * 8;
+    if (x.b_src != me) st.bytes_recv += x.b_nnz * bb * 8;
+    for (int rr = 0; rr < ctx->pr; ++rr)  // what peers pull from me at this step (statistics)
+      for (int cc = 0; cc < ctx->pc; ++cc) {
+        const int dst = rr * ctx->pc + cc;
+        if (dst == me) continue;
+        const int k = (rr + cc + s) % (int)L;
+        if (rr == ctx->myrow && k % ctx->pc == ctx->mycol) st.bytes_sent += sc->ownA_nnz[k] * bb * 8;
+        if (cc == ctx->mycol && k % ctx->pr == ctx->myrow) st.bytes_sent += sc->ownB_nnz[k] * bb * 8;
+      }
+    return DBM_OK;
+  };
+  if (ctx->nranks > 1) {
+    int na = 0, nb = 0;
+    for (int s = 0; s < L; ++s) {
+      if (sc->steps[s].a_src != me) bufA[s] = na++ & 1;
+      if (sc->steps[s].b_src != me) bufB[s] = nb++ & 1;
+      ev_x[s] = get_event(ctx);
+      ev_g[s] = get_event(ctx);
+    }
+    ev_ready = get_event(ctx);
+    CUDA_TRY(ctx, cudaEventRecord(ev_ready, cs));
+    CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->comm, ev_ready, 0));
+    if (dbm_status e = ipc_exchange(ctx, ws)) return e;  // = barrier: every rank's panels are packed
+    if (dbm_status e = pulls(0)) return e;
+    CUDA_TRY(ctx, cudaEventRecord(ev_x[0], ctx->comm));
+  }
+  int64_t* cnt = (int64_t*)(ws + sc->off_cnt);
+  int64_t* offs = (int64_t*)(ws + sc->off_off);
+  int32_t* trip = (int32_t*)(ws + sc->off_trip);
+  for (int s = 0; s < L; ++s) {
+    const SpStep& x = sc->steps[s];
+    if (ctx->nranks > 1) {
+      if (s + 1 < L) {
+        if (s >= 1) CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->comm, ev_g[s - 1], 0));
+        if (dbm_status e = pulls(s + 1)) return e;
+        CUDA_TRY(ctx, cudaEventRecord(ev_x[s + 1], ctx->comm));
+      }
+      CUDA_TRY(ctx, cudaStreamWaitEvent(cs, ev_x[s], 0));
+    }
+    const double* Ap = ctx->nranks == 1 ? A->arena
+                       : x.a_src != me ? (const double*)(ws + sc->off_recvA[bufA[s]])
+                                       : (const double*)(ws + sc->ownA_off[x.kappa]);
+    const double* Bp = ctx->nranks == 1 ? B->arena
+                       : x.b_src != me ? (const double*)(ws + sc->off_recvB[bufB[s]])
+                                       : (const double*)(ws + sc->ownB_off[x.kappa]);
+    if (x.entries > 0) {
+      const int64_t nruns = mloc * nloc;
+      for (int64_t q0 = 0; q0 < nruns; q0 += sc->runs_per_chunk) {
+        const int64_t n = std::min(sc->runs_per_chunk, nruns - q0);
+        {
+          ProfScope ps(ctx, cs, 4, 0.0, 0.0);
+          CUDA_TRY(ctx, launch_sp_stackgen(meta + x.o_aptr, meta + x.o_akk, meta + x.o_bptr, meta + x.o_bkk,
+                                           meta + x.o_bslot, C->sparse ? C->d_map : nullptr, nloc, trav_li, trav_lj, q0,
+                                           n, cnt, offs, ws + sc->off_scan, sc->scan_bytes, trip, cs));
+          launches += 3;
+        }
+        {
+          ProfScope ps(ctx, cs, 1, 0.0, 0.0);
+          CUDA_TRY(ctx, launch_smm_sparse(bs, trip, offs, n, Ap, Bp, C->arena, alpha, cs));
+          ++launches;
+        }
+      }
+    }
+    st.entries += x.entries;
+    st.flops += 2.0 * bs * bb * x.entries;
+    if (ctx->nranks > 1) CUDA_TRY(ctx, cudaEventRecord(ev_g[s], cs));
+  }
+  st.stacks = sp_stacks(sc, cap);
+  if (ctx->nranks > 1) {
+    CUDA_TRY(ctx, cudaStreamWaitEvent(cs, ev_x[L - 1], 0));
+    int* w = ctx->d_scratch;
+    NCCL_TRY(ctx, ncclAllReduce(w, w, 1, ncclInt, ncclSum, (ncclComm_t)ctx->nccl, cs));
+    cudaEvent_t done = get_event(ctx);
+    CUDA_TRY(ctx, cudaEventRecord(done, cs));
+    ctx->ev_pool.push_back(ev_ready);
+    for (int s = 0; s < L; ++s) {
+      ctx->ev_pool.push_back(ev_x[s]);
+      ctx->ev_pool.push_back(ev_g[s]);
+    }
+    ctx->ev_pool.push_back(done);
+  }
+  ctx->launches += launches;
+  st.kernel_launches = launches;
+  if (stats) *stats = st;
+  return DBM_OK;
+}
+
+// DBM_PATH_AUTO -> blocked / densified (should_densify)
+dbm_path resolve_path(dbm_ctx ctx, dbm_matrix A, dbm_matrix B, dbm_path path) {
+  if (path != DBM_PATH_AUTO) return path;
+  auto occ = [](dbm_matrix m) { return m->Mb * m->Nb ? (double)m->gnnz / (double)(m->Mb * m->Nb) : 1.0; };
+  return (occ(A) >= ctx->densify_threshold && occ(B) >= ctx->densify_threshold) ? DBM_PATH_DENSIFIED
+                                                                                : DBM_PATH_BLOCKED;
+}
+
+}  // namespace
+
 extern "C" dbm_status dbm_multiply_workspace(dbm_ctx ctx, dbm_matrix A, dbm_matrix B, dbm_matrix C, dbm_path path,
                                              int64_t* bytes) {
   ARG_CHECK(bytes, DBM_ERR_ARG, "null output");
-  ARG_CHECK(path == DBM_PATH_BLOCKED || path == DBM_PATH_DENSIFIED, DBM_ERR_ARG, "bad path");
+  ARG_CHECK(path == DBM_PATH_BLOCKED || path == DBM_PATH_DENSIFIED || path == DBM_PATH_AUTO, DBM_ERR_ARG, "bad path");
   if (dbm_status s = validate(ctx, A, B, C)) return s;
+  path = resolve_path(ctx, A, B, path);
+  if (path == DBM_PATH_BLOCKED && (A->sparse || B->sparse || C->sparse)) {
+    SpCache* sc = nullptr;
+    if (dbm_status e = sp_cache_get(ctx, A, B, C, &sc)) return e;
+    *bytes = (int64_t)sc->total;
+    return DBM_OK;
+  }
   if (ctx->algorithm == 1 && ctx->nranks > 1)
     *bytes = (int64_t)make_ts_plan(ctx->pr, ctx->pc, ctx->myrow, ctx->mycol, A->Mb, B->Nb, A->Nb, A->bs).total;
   else
@@ -1117,6 +1726,7 @@ extern "C" dbm_status dbm_plan_tallskinny(int pr, int pc, int myrow, int mycol, 
 // Host-resident operands (dbm_multiply_host): pinned host arenas streamed to the device arenas on
 // the comm stream; chunk_ev[ch] marks A/B K-chunk ch of the single-rank densified path uploaded,
 // all_ev everything uploaded (other paths), c_ev C_in uploaded.
+
 struct HostIO {
   const double* A = nullptr;
   const double* B = nullptr;
@@ -1167,7 +1777,7 @@ extern "C" dbm_status dbm_multiply_host(dbm_ctx ctx, double alpha, dbm_matrix A,
   if (hio.all_ev) ctx->ev_pool.push_back(hio.all_ev);
   if (hio.c_ev) ctx->ev_pool.push_back(hio.c_ev);
   if (e) return e;
-  const size_t cbytes = (size_t)(C->mloc * C->nloc) * C->bs * C->bs * 8;
+  const size_t cbytes = (size_t)C->blocks() * C->bs * C->bs * 8;
   if (cbytes) CUDA_TRY(ctx, cudaMemcpyAsync(C_host, C->arena, cbytes, cudaMemcpyDeviceToHost, ctx->stream));
   return DBM_OK;
 }
@@ -1177,10 +1787,21 @@ dbm_status multiply_impl(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_matrix B, 
                          dbm_path path, int32_t stack_cap, void* workspace, int64_t ws_bytes, dbm_stats* stats,
                          HostIO* hio) {
   CTX_OK(ctx);
-  ARG_CHECK(path == DBM_PATH_BLOCKED || path == DBM_PATH_DENSIFIED, DBM_ERR_ARG, "bad path");
+  ARG_CHECK(path == DBM_PATH_BLOCKED || path == DBM_PATH_DENSIFIED || path == DBM_PATH_AUTO, DBM_ERR_ARG, "bad path");
   ARG_CHECK(stack_cap >= 0, DBM_ERR_ARG, "negative stack cap");
   if (dbm_status s = validate(ctx, A, B, C)) return s;
+  path = resolve_path(ctx, A, B, path);
   const bool dens = path == DBM_PATH_DENSIFIED;
+  if (!dens && (A->sparse || B->sparse || C->sparse)) {
+    if (hio) {  // host operands: plain uploads ahead of the multiply on the compute stream
+      const size_t bb8 = (size_t)A->bs * A->bs * 8;
+      const size_t ab = (size_t)A->blocks() * bb8, bbytes = (size_t)B->blocks() * bb8, cb = (size_t)C->blocks() * bb8;
+      if (ab) CUDA_TRY(ctx, cudaMemcpyAsync(A->arena, hio->A, ab, cudaMemcpyHostToDevice, ctx->stream));
+      if (bbytes) CUDA_TRY(ctx, cudaMemcpyAsync(B->arena, hio->B, bbytes, cudaMemcpyHostToDevice, ctx->stream));
+      if (beta != 0.0 && cb) CUDA_TRY(ctx, cudaMemcpyAsync(C->arena, hio->C, cb, cudaMemcpyHostToDevice, ctx->stream));
+    }
+    return multiply_sparse_blocked(ctx, alpha, A, B, beta, C, stack_cap, workspace, ws_bytes, stats);
+  }
   if (ctx->algorithm == 1 && ctx->nranks > 1) {
     ARG_CHECK(dens, DBM_ERR_ARG, "the tall-and-skinny algorithm runs the densified local multiply");
     ARG_CHECK(ctx->transport == 0, DBM_ERR_ARG, "the tall-and-skinny algorithm uses the copy-engine transport");
@@ -1191,14 +1812,14 @@ dbm_status multiply_impl(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_matrix B, 
     int launches = 0;
     if (hio) {  // host operands: plain uploads ahead of the multiply on the compute stream
       const size_t bb8 = (size_t)A->bs * A->bs * 8;
-      const size_t ab = (size_t)(A->mloc * A->nloc) * bb8, bbytes = (size_t)(B->mloc * B->nloc) * bb8,
-                   cb = (size_t)(C->mloc * C->nloc) * bb8;
+      const size_t ab = (size_t)A->blocks() * bb8, bbytes = (size_t)B->blocks() * bb8,
+                   cb = (size_t)C->blocks() * bb8;
       if (ab) CUDA_TRY(ctx, cudaMemcpyAsync(A->arena, hio->A, ab, cudaMemcpyHostToDevice, ctx->stream));
       if (bbytes) CUDA_TRY(ctx, cudaMemcpyAsync(B->arena, hio->B, bbytes, cudaMemcpyHostToDevice, ctx->stream));
       if (beta != 0.0 && cb) CUDA_TRY(ctx, cudaMemcpyAsync(C->arena, hio->C, cb, cudaMemcpyHostToDevice, ctx->stream));
     }
     if (alpha == 0.0 || A->Nb == 0) {
-      const int64_t n = C->mloc * C->nloc * (int64_t)C->bs * C->bs;
+      const int64_t n = C->blocks() * (int64_t)C->bs * C->bs;
       if (n) {
         scale_kernel<<<(unsigned)std::min<int64_t>((n + 255) / 256, num_sms() * 16), 256, 0, ctx->stream>>>(C->arena, n,
                                                                                                           beta);
@@ -1229,7 +1850,7 @@ dbm_status multiply_impl(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_matrix B, 
       return e0;
     }(), 0));
     const size_t bb8 = (size_t)p.bs * p.bs * 8;
-    const bool chunked = ctx->nranks == 1 && dens && alpha != 0.0 && p.Kb > 0;
+    const bool chunked = ctx->nranks == 1 && dens && alpha != 0.0 && p.Kb > 0 && !A->sparse && !B->sparse;
     if (chunked) {
       for (int64_t ch = 0; ch < p.nchunks; ++ch) {
         const int64_t k0 = ch * p.chunk_kb, nk = std::min(p.chunk_kb, p.Kb - k0);
@@ -1244,13 +1865,13 @@ dbm_status multiply_impl(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_matrix B, 
         hio->chunk_ev.push_back(e);  // chunk_ev[ch + 1]
       }
     } else {
-      const size_t ab = (size_t)(A->mloc * A->nloc) * bb8, bbytes = (size_t)(B->mloc * B->nloc) * bb8;
+      const size_t ab = (size_t)A->blocks() * bb8, bbytes = (size_t)B->blocks() * bb8;
       if (ab && alpha != 0.0) CUDA_TRY(ctx, cudaMemcpyAsync(A->arena, hio->A, ab, cudaMemcpyHostToDevice, cp));
       if (bbytes && alpha != 0.0) CUDA_TRY(ctx, cudaMemcpyAsync(B->arena, hio->B, bbytes, cudaMemcpyHostToDevice, cp));
       hio->all_ev = get_event(ctx);
       CUDA_TRY(ctx, cudaEventRecord(hio->all_ev, cp));
     }
-    const size_t cb = (size_t)(C->mloc * C->nloc) * bb8;
+    const size_t cb = (size_t)C->blocks() * bb8;
     if (beta != 0.0 && cb) CUDA_TRY(ctx, cudaMemcpyAsync(C->arena, hio->C, cb, cudaMemcpyHostToDevice, cp));
     hio->c_ev = get_event(ctx);
     CUDA_TRY(ctx, cudaEventRecord(hio->c_ev, cp));
@@ -1270,7 +1891,7 @@ dbm_status multiply_impl(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_matrix B, 
 
   // BLAS convention: alpha == 0 -> A and B are not read (reading R8).
   if (alpha == 0.0 || p.Kb == 0) {
-    const int64_t n = M * N;
+    const int64_t n = C->blocks() * bb;
     if (n) {
       scale_kernel<<<(unsigned)std::min<int64_t>((n + 255) / 256, num_sms() * 16), 256, 0, cs>>>(C->arena, n, beta);
       ++launches;
@@ -1290,7 +1911,7 @@ dbm_status multiply_impl(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_matrix B, 
         double* dst = (double*)(ws + p.ownA_off[k]);
         if (dens) {
           ProfScope ps(ctx, cs, 2, 0.0, 16.0 * M * p.kb[k] * bs);
-          launch_densify_cols(A->arena, p.mloc, p.kA, (int)bs, col0, stride, p.kb[k], dst, p.ld_panel(k), 1, cs);
+          if (dbm_status e = densify_a(ctx, A, col0, stride, p.kb[k], dst, p.ld_panel(k), 1, cs)) return e;
         } else {
           launch_pack_cols(A->arena, p.mloc, p.kA, (int)bs, col0, stride, p.kb[k], dst, cs);
         }
@@ -1301,7 +1922,7 @@ dbm_status multiply_impl(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_matrix B, 
         double* dst = (double*)(ws + p.ownB_off[k]);
         if (dens) {
           ProfScope ps(ctx, cs, 2, 0.0, 16.0 * N * p.kb[k] * bs);
-          launch_densify_rows(B->arena, p.nloc, (int)bs, row0, stride, p.kb[k], dst, p.ld_panel(k), 0, cs);
+          if (dbm_status e = densify_b(ctx, B, row0, stride, p.kb[k], dst, p.ld_panel(k), 0, cs)) return e;
         } else {
           launch_pack_rows(B->arena, p.nloc, (int)bs, row0, stride, p.kb[k], dst, cs);
         }
@@ -1410,11 +2031,12 @@ dbm_status multiply_impl(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_matrix B, 
           const int64_t ld = round_up(p.chunk_kb * bs, 2);
           double* Ad = (double*)(ws + p.off_ownA);
           double* Bd = (double*)(ws + p.off_ownB);
-          if (hio) CUDA_TRY(ctx, cudaStreamWaitEvent(cs, hio->chunk_ev[ch + 1], 0));  // chunk ch uploaded
+          if (hio && hio->chunk_ev.size() > (size_t)ch + 1)  // chunk ch uploaded
+            CUDA_TRY(ctx, cudaStreamWaitEvent(cs, hio->chunk_ev[ch + 1], 0));
           {
             ProfScope ps(ctx, cs, 2, 0.0, 16.0 * (M + N) * nk * bs);
-            launch_densify_cols(A->arena, p.mloc, p.kA, (int)bs, k0, 1, nk, Ad, ld, 1, cs);
-            launch_densify_rows(B->arena, p.nloc, (int)bs, k0, 1, nk, Bd, ld, 0, cs);
+            if (dbm_status e = densify_a(ctx, A, k0, 1, nk, Ad, ld, 1, cs)) return e;
+            if (dbm_status e = densify_b(ctx, B, k0, 1, nk, Bd, ld, 0, cs)) return e;
             launches += 2;
           }
           GemmArgs g{M, N, nk * bs, Ad, ld, Bd, ld, Cd, M, 1.0, ch == 0 ? 0.0 : 1.0, 1, nullptr};
@@ -1491,7 +2113,7 @@ dbm_status multiply_impl(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_matrix B, 
   if (dens && M * N > 0) {
     if (hio && hio->c_ev) CUDA_TRY(ctx, cudaStreamWaitEvent(cs, hio->c_ev, 0));  // C_in uploaded
     ProfScope ps(ctx, cs, 3, 0.0, (beta == 0.0 ? 16.0 : 24.0) * M * N);
-    launch_undensify((double*)(ws + p.off_cd), M, 1, 0, p.mloc, p.nloc, (int)bs, alpha, beta, C->arena, cs);
+    undensify_c(C, (double*)(ws + p.off_cd), M, 1, 0, alpha, beta, cs);
     ++launches;
     CUDA_TRY(ctx, cudaGetLastError());
   }
@@ -1530,6 +2152,57 @@ extern "C" dbm_status dbm_debug_stacks(dbm_ctx ctx, dbm_matrix A, dbm_matrix B, 
   CTX_OK(ctx);
   if (dbm_status s = validate(ctx, A, B, C)) return s;
   ARG_CHECK(n_entries && n_stacks, DBM_ERR_ARG, "null size outputs");
+  if (A->sparse || B->sparse || C->sparse) {
+    SpCache* sc = nullptr;
+    if (dbm_status e = sp_cache_get(ctx, A, B, C, &sc)) return e;
+    ARG_CHECK(step >= 0 && step < sc->L, DBM_ERR_RANGE, "step out of range");
+    const SpStep& x = sc->steps[step];
+    const int64_t capv = cap ? cap : 30000;
+    std::vector<int64_t> ptr{0};
+    int64_t e = 0, cur = 0;
+    for (int32_t n : x.run_len) {  // greedy whole-run packing (as sp_stacks), recording the boundaries
+      if (n == 0) continue;
+      if (n > capv) {
+        if (cur) ptr.push_back(e);
+        cur = 0;
+        for (int64_t done = 0; done < n;) {
+          done += std::min<int64_t>(capv, n - done);
+          ptr.push_back(e + done);
+        }
+      } else {
+        if (cur + n > capv) {
+          ptr.push_back(e);
+          cur = 0;
+        }
+        cur += n;
+      }
+      e += n;
+    }
+    if (cur) ptr.push_back(e);
+    *n_entries = x.entries;
+    *n_stacks = (int64_t)ptr.size() - 1;
+    if (stack_ptr) std::memcpy(stack_ptr, ptr.data(), ptr.size() * 8);
+    if (!triplets || x.entries == 0) return DBM_OK;
+    const int64_t nruns = C->mloc * C->nloc;
+    const size_t scan_bytes = sp_scan_temp_bytes(nruns + 1);
+    char* d = nullptr;
+    const size_t o_cnt = align256((size_t)nruns * 8), o_off = o_cnt + align256((size_t)(nruns + 1) * 8),
+                 o_scan = o_off + align256((size_t)(nruns + 1) * 8), o_trip = o_scan + align256(scan_bytes),
+                 total = o_trip + (size_t)x.entries * 12;
+    CUDA_TRY(ctx, cudaMalloc(&d, total));
+    int32_t* li = (int32_t*)d;
+    launch_traversal(C->mloc, C->nloc, li, li + nruns, ctx->stream);
+    const int32_t* meta = sc->d_meta;
+    CUDA_TRY(ctx, launch_sp_stackgen(meta + x.o_aptr, meta + x.o_akk, meta + x.o_bptr, meta + x.o_bkk,
+                                     meta + x.o_bslot, C->sparse ? C->d_map : nullptr, C->nloc, li, li + nruns, 0,
+                                     nruns, (int64_t*)(d + o_cnt), (int64_t*)(d + o_off), d + o_scan, scan_bytes,
+                                     (int32_t*)(d + o_trip), ctx->stream));
+    ctx->launches += 4;
+    CUDA_TRY(ctx, cudaMemcpyAsync(triplets, d + o_trip, (size_t)x.entries * 12, cudaMemcpyDeviceToHost, ctx->stream));
+    CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
+    cudaFree(d);
+    return DBM_OK;
+  }
   const Plan p = make_plan(ctx, A, B, C, false);
   ARG_CHECK(step >= 0 && step < p.L, DBM_ERR_RANGE, "step out of range");
   const int64_t capv = cap ? cap : 30000;

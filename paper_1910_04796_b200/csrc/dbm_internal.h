@@ -39,6 +39,30 @@ void launch_pack_rows(const double* arena, int64_t ncols, int bs, int64_t row0, 
 void launch_pack_cols(const double* arena, int64_t mloc, int64_t nloc, int bs, int64_t col0, int64_t cstride,
                       int64_t ncols, double* out, cudaStream_t st);
 
+// ---- block-sparse matrices (kernels_sparse.cu, reading R15) ----
+void launch_fill_sparse(double* arena, int64_t nnz, const int32_t* ij, int bs, int pr, int pc, int r, int c,
+                        uint64_t seed, uint32_t mat_id, int kind, cudaStream_t st);
+// Densify the stored blocks of one panel; absent blocks become zeros.  axis 0 (A panel): blocks with
+// lj = sel0 + q*stride, q < nk -> dense block (li, q), `other` = mloc; axis 1 (B panel): blocks with
+// li = sel0 + q*stride -> dense block (q, lj), `other` = nloc.  Layouts as launch_densify_cols/rows.
+cudaError_t launch_sp_densify(const double* arena, const int32_t* ij, int64_t nnz, int bs, int axis, int64_t sel0,
+                              int64_t stride, int64_t nk, int64_t other, double* dense, int64_t ld, int layout,
+                              cudaStream_t st);
+void launch_sp_undensify(const double* dense, int64_t ld, int nsplit, int64_t split_stride, const int32_t* ij,
+                         int64_t nnz, int bs, double alpha, double beta, double* arena, cudaStream_t st);
+// out block q <- arena block src[q] (panel packing)
+void launch_sp_gather(const double* arena, const int32_t* src, int64_t n, int bs, double* out, cudaStream_t st);
+size_t sp_scan_temp_bytes(int64_t n);
+// Sparse Generation for runs q0 .. q0+n-1 of the traversal: cnt (n+1) and off (n+1) are scratch /
+// the run offsets (off[n] = entries), trip receives the triplets.
+cudaError_t launch_sp_stackgen(const int32_t* a_ptr, const int32_t* a_kk, const int32_t* b_ptr, const int32_t* b_kk,
+                               const int32_t* b_slot, const int32_t* cmap, int64_t nloc, const int32_t* li,
+                               const int32_t* lj, int64_t q0, int64_t n, int64_t* cnt, int64_t* off, void* scan_tmp,
+                               size_t scan_bytes, int32_t* trip, cudaStream_t st);
+// C_blk(trip c) += alpha * sum over a run's entries of A_blk * B_blk; runs given by off (nruns+1).
+cudaError_t launch_smm_sparse(int bs, const int32_t* trip, const int64_t* off, int64_t nruns, const double* A,
+                              const double* B, double* C, double alpha, cudaStream_t st);
+
 // Dense FP64 GEMM, both operands K-major (the "TN" form): C(M x N col-major) = alpha * At^T B + beta C.
 struct GemmArgs {
   int64_t M, N, K;
@@ -87,6 +111,7 @@ cudaError_t launch_smm_tc(int bs, const int32_t* trip, int64_t nruns, int64_t kb
 // ----------------------------------------------------------------- driver
 int num_sms();
 
+struct SpCache;  // block-sparse multiply plans + device metadata (dbm_api.cu)
 }  // namespace dbm
 
 // ----------------------------------------------------------------- handles
@@ -121,6 +146,8 @@ struct dbm_ctx_s {
   std::vector<std::vector<char>> peer_handles;  // raw IPC handles (to re-use / close mappings)
   std::vector<void*> peer_bases;          // opened allocation bases (cudaIpcCloseMemHandle)
   int* d_scratch = nullptr;               // device scratch: barrier word + handle exchange
+  double densify_threshold = 1.0;         // DBM_PATH_AUTO: densify iff occupancy >= this
+  std::vector<dbm::SpCache*> sp_cache;    // sparse plans keyed by the operands' pattern serials
 };
 
 struct dbm_matrix_s {
@@ -130,4 +157,17 @@ struct dbm_matrix_s {
   int64_t Mb = 0, Nb = 0, mloc = 0, nloc = 0;
   double* arena = nullptr;
   int64_t arena_bytes = 0;
+  // block sparsity (reading R15): stored blocks in local CSR order; the dense matrix is the
+  // all-stored case (slot li*nloc + lj) and keeps sparse == false
+  bool sparse = false;
+  int64_t nnz = 0;                // stored local blocks
+  int64_t gnnz = 0;               // stored blocks of the whole matrix
+  std::vector<uint8_t> gmask;     // global pattern, Mb x Nb row-major (sparse only)
+  std::vector<int64_t> row_ptr;   // local CSR over li (sparse only)
+  std::vector<int32_t> col;       // lj per slot (sparse only)
+  int32_t* d_ij = nullptr;        // device (li, lj) per slot (sparse only; library-owned)
+  int32_t* d_map = nullptr;       // device li*nloc + lj -> slot or -1 (sparse only; library-owned)
+  uint64_t serial = 0;            // pattern identity (plan caches)
+  int64_t blocks() const { return sparse ? nnz : mloc * nloc; }
+  bool stored(int64_t bi, int64_t bj) const { return !sparse || gmask[(size_t)bi * Nb + bj]; }
 };

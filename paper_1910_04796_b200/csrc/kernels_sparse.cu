@@ -1,0 +1,396 @@
+// Block-sparse matrices (§8f-2, reading R15): "DBCSR matrices are stored in a blocked compressed sparse
+// row (CSR) format" (§II), occupancy 0.01 % up to dense (§I).  A rank stores its blocks in
+// local CSR order; slot s holds block (li, lj) = ij[2s], ij[2s+1].
+//
+//   fill_sparse / sp_densify / sp_undensify / sp_gather : HBM-bound data movement over stored blocks
+//     (absent blocks densify to zeros, S:59 / S:477; only stored C blocks are written, R15).
+//   sp_count / sp_fill : the Generation phase for sparse panels.  A run is a stored C block
+//     (bisection order, R6); its entries are the kk where A(li, kk) and B(kk, lj) are both stored,
+//     found by merging the A-panel row list with the B-panel column list (both kk-ascending).  Two
+//     passes around an exclusive scan give every run its offset: integer work, bit-exact vs oracle.
+//   smm_sparse<BS> : batched small-block DGEMM over runs of any length (the LIBCUSMM role):
+//     a team of warps per run accumulates its entries with DMMA (mma.sync.m8n8k4.f64), the next
+//     entry's A and B blocks streamed into shared memory with cp.async while this one multiplies;
+//     C_blk += alpha * acc (beta was applied to every stored C block before the first step).
+#include <cub/device/device_scan.cuh>
+
+#include <algorithm>
+
+#include "dbm_internal.h"
+
+namespace dbm {
+
+namespace {
+
+inline unsigned sp_grid(int64_t work, int per = 256, int mult = 16) {
+  int64_t g = (work + per - 1) / per;
+  g = std::min<int64_t>(g, (int64_t)num_sms() * mult);
+  return (unsigned)std::max<int64_t>(g, 1);
+}
+
+__device__ __forceinline__ uint64_t sp_mix64(uint64_t z) {
+  z ^= z >> 30;
+  z *= 0xBF58476D1CE4E5B9ull;
+  z ^= z >> 27;
+  z *= 0x94D049BB133111EBull;
+  z ^= z >> 31;
+  return z;
+}
+
+__global__ void fill_sparse_kernel(double* __restrict__ arena, int64_t total, const int32_t* __restrict__ ij, int bs,
+                                   int pr, int pc, int r, int c, uint64_t key, int kind) {
+  const int64_t bb = (int64_t)bs * bs;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t slot = e / bb, w = e - slot * bb;
+    const int64_t y = w / bs, x = w - y * bs;
+    const int64_t li = ij[2 * slot], lj = ij[2 * slot + 1];
+    const uint64_t gi = (uint64_t)((r + li * pr) * bs + x), gj = (uint64_t)((c + lj * pc) * bs + y);
+    const uint64_t bits = sp_mix64(key ^ sp_mix64((gi << 32) ^ gj));
+    double v;
+    if (kind == 1) {
+      v = (double)((int)((bits >> 32) % 5u) - 2);
+    } else {
+      const double u = __dmul_rn((double)(bits >> 11), 0x1.0p-53);
+      v = __dsub_rn(__dmul_rn(2.0, u), 1.0);
+    }
+    arena[e] = v;
+  }
+}
+
+// axis 0 (A panel): blocks with lj = sel0 + q*stride -> dense block (li, q)
+// axis 1 (B panel): blocks with li = sel0 + q*stride -> dense block (q, lj)
+// layout 0: dense[col*ld + row]; layout 1: dense[row*ld + col]
+__global__ void sp_densify_kernel(const double* __restrict__ arena, const int32_t* __restrict__ ij, int64_t total,
+                                  int bs, int axis, int64_t sel0, int64_t stride, int64_t nk,
+                                  double* __restrict__ dense, int64_t ld, int layout) {
+  const int64_t bb = (int64_t)bs * bs;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t slot = e / bb, w = e - slot * bb;
+    const int64_t li = ij[2 * slot], lj = ij[2 * slot + 1];
+    const int64_t d = (axis == 0 ? lj : li) - sel0;
+    if (d < 0 || d % stride != 0 || d / stride >= nk) continue;
+    const int64_t q = d / stride, y = w / bs, x = w - y * bs;
+    const int64_t row = (axis == 0 ? li : q) * bs + x, col = (axis == 0 ? q : lj) * bs + y;
+    dense[layout == 0 ? col * ld + row : row * ld + col] = arena[e];
+  }
+}
+
+__global__ void sp_undensify_kernel(const double* __restrict__ dense, int64_t ld, int nsplit, int64_t split_stride,
+                                    const int32_t* __restrict__ ij, int bs, int64_t total, double alpha, double beta,
+                                    double* __restrict__ arena) {
+  const int64_t bb = (int64_t)bs * bs;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t slot = e / bb, w = e - slot * bb;
+    const int64_t y = w / bs, x = w - y * bs;
+    const int64_t li = ij[2 * slot], lj = ij[2 * slot + 1];
+    const int64_t di = (lj * bs + y) * ld + li * bs + x;
+    double d = dense[di];
+    for (int s = 1; s < nsplit; ++s) d = __dadd_rn(d, dense[di + s * split_stride]);
+    const double t = __dmul_rn(alpha, d);
+    arena[e] = (beta == 0.0) ? t : __dadd_rn(t, __dmul_rn(beta, arena[e]));
+  }
+}
+
+__global__ void sp_gather_kernel(const double* __restrict__ arena, const int32_t* __restrict__ src, int64_t total,
+                                 int bs, double* __restrict__ out) {
+  const int64_t bb = (int64_t)bs * bs;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t q = e / bb, w = e - q * bb;
+    out[e] = arena[(int64_t)src[q] * bb + w];
+  }
+}
+
+// ---------------------------------------------------------------- Generation (sparse)
+// A panel: row li's stored blocks are a_kk[a_ptr[li] .. a_ptr[li+1]) (kk ascending), slot = position.
+// B panel: column lj's stored blocks are b_kk / b_slot[b_ptr[lj] .. b_ptr[lj+1]) (kk ascending).
+// C: cmap[li*nloc + lj] = stored slot or -1 (nullptr: dense C, slot li*nloc + lj).
+struct SpPanels {
+  const int32_t* a_ptr;
+  const int32_t* a_kk;
+  const int32_t* b_ptr;
+  const int32_t* b_kk;
+  const int32_t* b_slot;
+  const int32_t* cmap;
+  int64_t nloc;
+};
+
+template <bool WRITE>
+__global__ void sp_gen_kernel(SpPanels P, const int32_t* __restrict__ li_of, const int32_t* __restrict__ lj_of,
+                              int64_t q0, int64_t n, int64_t* __restrict__ cnt, const int64_t* __restrict__ off,
+                              int32_t* __restrict__ trip) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t li = li_of[q0 + t], lj = lj_of[q0 + t];
+    const int64_t cs = P.cmap ? (int64_t)P.cmap[li * P.nloc + lj] : li * P.nloc + lj;
+    int64_t m = 0;
+    if (cs >= 0) {
+      int32_t a = P.a_ptr[li];
+      const int32_t a1 = P.a_ptr[li + 1];
+      int32_t b = P.b_ptr[lj];
+      const int32_t b1 = P.b_ptr[lj + 1];
+      int64_t o = WRITE ? off[t] : 0;
+      while (a < a1 && b < b1) {
+        const int32_t ka = P.a_kk[a], kb = P.b_kk[b];
+        if (ka == kb) {
+          if (WRITE) {
+            trip[3 * (o + m) + 0] = a;
+            trip[3 * (o + m) + 1] = P.b_slot[b];
+            trip[3 * (o + m) + 2] = (int32_t)cs;
+          }
+          ++m;
+          ++a;
+          ++b;
+        } else if (ka < kb) {
+          ++a;
+        } else {
+          ++b;
+        }
+      }
+    }
+    if (!WRITE) cnt[t] = m;
+  }
+}
+
+// ---------------------------------------------------------------- smm over runs of any length
+__device__ __forceinline__ void sp_dmma(double (&c)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(c[0]), "+d"(c[1])
+               : "d"(a), "d"(b));
+}
+
+template <int BS>
+struct SpCfg {
+  static constexpr int MT = (BS + 7) / 8;            // 8x8 subtiles per block dimension
+  static constexpr int TEAM = MT >= 4 ? 4 : 1;       // warps per run
+  static constexpr int NPW = MT / TEAM;              // n-subtiles per warp
+  static constexpr int WARPS = TEAM == 4 ? 4 : 8;    // bs 64: one 4-warp team (132 KB of stages)
+  static constexpr int TEAMS = WARPS / TEAM;
+  static constexpr int BB = BS * BS;
+  // one stage = A block (+ slack for the padded rows m >= BS) and B block (+ padded columns n >= BS)
+  static constexpr int A_D = BB + 8 * MT;
+  static constexpr int B_D = 8 * MT * BS + 8;
+  static constexpr int STAGE = ((A_D + B_D) + 1) / 2 * 2;
+  static constexpr size_t SMEM = (size_t)TEAMS * 2 * STAGE * 8;
+  static_assert(MT % TEAM == 0, "team split");
+};
+
+template <int BS>
+__global__ void __launch_bounds__(SpCfg<BS>::WARPS * 32, 1)
+    smm_sparse_kernel(const int32_t* __restrict__ trip, const int64_t* __restrict__ off, int64_t nruns,
+                      const double* __restrict__ A, const double* __restrict__ B, double* __restrict__ C,
+                      double alpha) {
+  using Cfg = SpCfg<BS>;
+  constexpr int MT = Cfg::MT, TEAM = Cfg::TEAM, NPW = Cfg::NPW, BB = Cfg::BB;
+  extern __shared__ __align__(16) double sm[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int team = warp / TEAM, tw = warp % TEAM;
+  const int g = lane >> 2, t = lane & 3;
+  double* st0 = sm + (size_t)team * 2 * Cfg::STAGE;
+  const int tlane = tw * 32 + lane;  // 0 .. TEAM*32-1
+  constexpr int TT = TEAM * 32;
+  // blocks are 16-byte aligned when BB is even (bs 22, 64)
+  auto load = [&](double* dst, int64_t entry) {
+    const double* a = A + (int64_t)trip[3 * entry] * BB;
+    const double* b = B + (int64_t)trip[3 * entry + 1] * BB;
+    const uint32_t sa = (uint32_t)__cvta_generic_to_shared(dst);
+    const uint32_t sb = (uint32_t)__cvta_generic_to_shared(dst + Cfg::A_D);
+    for (int i = tlane; i < BB / 2; i += TT) {
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa + 16u * i), "l"(a + 2 * i) : "memory");
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sb + 16u * i), "l"(b + 2 * i) : "memory");
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  auto team_sync = [&]() {
+    if (TEAM == 1)
+      __syncwarp();
+    else
+      asm volatile("bar.sync %0, %1;" ::"r"(1 + team), "r"(TT) : "memory");
+  };
+
+  const int64_t nteams = (int64_t)gridDim.x * Cfg::TEAMS;
+  for (int64_t run = (int64_t)blockIdx.x * Cfg::TEAMS + team; run < nruns; run += nteams) {
+    const int64_t e0 = off[run], e1 = off[run + 1];
+    if (e0 == e1) continue;
+    double acc[MT][NPW][2];
+#pragma unroll
+    for (int i = 0; i < MT; ++i)
+#pragma unroll
+      for (int j = 0; j < NPW; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    team_sync();  // the previous run's last stage has been consumed by every team warp
+    load(st0, e0);
+    for (int64_t e = e0; e < e1; ++e) {
+      double* cur = st0 + (size_t)((e - e0) & 1) * Cfg::STAGE;
+      if (e + 1 < e1) {
+        load(st0 + (size_t)((e + 1 - e0) & 1) * Cfg::STAGE, e + 1);
+        asm volatile("cp.async.wait_group 1;" ::: "memory");
+      } else {
+        asm volatile("cp.async.wait_group 0;" ::: "memory");
+      }
+      team_sync();
+      const double* sA = cur;                // (m, k) at k*BS + m
+      const double* sB = cur + Cfg::A_D;     // (k, n) at n*BS + k
+#pragma unroll
+      for (int ks = 0; ks < (BS + 3) / 4; ++ks) {
+        const int k = 4 * ks + t;
+        const bool kok = (BS % 4 == 0) || k < BS;
+        double a[MT], b[NPW];
+#pragma unroll
+        for (int mi = 0; mi < MT; ++mi) a[mi] = kok ? sA[k * BS + mi * 8 + g] : 0.0;
+#pragma unroll
+        for (int ni = 0; ni < NPW; ++ni) b[ni] = kok ? sB[((tw * NPW + ni) * 8 + g) * BS + k] : 0.0;
+#pragma unroll
+        for (int mi = 0; mi < MT; ++mi)
+#pragma unroll
+          for (int ni = 0; ni < NPW; ++ni) sp_dmma(acc[mi][ni], a[mi], b[ni]);
+      }
+      team_sync();  // every warp is done with `cur` before it is refilled
+    }
+    double* cb = C + (int64_t)trip[3 * e0 + 2] * BB;
+#pragma unroll
+    for (int mi = 0; mi < MT; ++mi)
+#pragma unroll
+      for (int ni = 0; ni < NPW; ++ni)
+#pragma unroll
+        for (int jj = 0; jj < 2; ++jj) {
+          const int m = mi * 8 + g, n = (tw * NPW + ni) * 8 + 2 * t + jj;
+          if (m < BS && n < BS) {
+            double* p = cb + m + n * BS;
+            *p = __dadd_rn(*p, __dmul_rn(alpha, acc[mi][ni][jj]));
+          }
+        }
+  }
+}
+
+// Any block size: one CTA per run, one thread per C element, FMA.
+__global__ void __launch_bounds__(256) smm_sparse_generic_kernel(int bs, const int32_t* __restrict__ trip,
+                                                                 const int64_t* __restrict__ off, int64_t nruns,
+                                                                 const double* __restrict__ A,
+                                                                 const double* __restrict__ B,
+                                                                 double* __restrict__ C, double alpha) {
+  extern __shared__ double sg[];
+  const int BB = bs * bs;
+  double* sA = sg;
+  double* sB = sg + BB;
+  for (int64_t run = blockIdx.x; run < nruns; run += gridDim.x) {
+    const int64_t e0 = off[run], e1 = off[run + 1];
+    if (e0 == e1) continue;
+    double* c = C + (int64_t)trip[3 * e0 + 2] * BB;
+    for (int idx0 = 0; idx0 < BB; idx0 += 256) {
+      const int idx = idx0 + threadIdx.x;
+      double acc = 0.0;
+      for (int64_t e = e0; e < e1; ++e) {
+        const double* a = A + (int64_t)trip[3 * e] * BB;
+        const double* b = B + (int64_t)trip[3 * e + 1] * BB;
+        __syncthreads();
+        for (int i = threadIdx.x; i < BB; i += 256) {
+          sA[i] = a[i];
+          sB[i] = b[i];
+        }
+        __syncthreads();
+        if (idx < BB) {
+          const int x = idx % bs, y = idx / bs;
+          for (int z = 0; z < bs; ++z) acc = fma(sA[z * bs + x], sB[y * bs + z], acc);
+        }
+      }
+      if (idx < BB) c[idx] = __dadd_rn(c[idx], __dmul_rn(alpha, acc));
+    }
+  }
+}
+
+template <int BS>
+cudaError_t launch_sp_tc(const int32_t* trip, const int64_t* off, int64_t nruns, const double* A, const double* B,
+                         double* C, double alpha, cudaStream_t st) {
+  using Cfg = SpCfg<BS>;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(smm_sparse_kernel<BS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)Cfg::SMEM);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  const int64_t ctas = (nruns + Cfg::TEAMS - 1) / Cfg::TEAMS;
+  const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(ctas, (int64_t)num_sms()));
+  smm_sparse_kernel<BS><<<grid, Cfg::WARPS * 32, Cfg::SMEM, st>>>(trip, off, nruns, A, B, C, alpha);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+void launch_fill_sparse(double* arena, int64_t nnz, const int32_t* ij, int bs, int pr, int pc, int r, int c,
+                        uint64_t seed, uint32_t mat_id, int kind, cudaStream_t st) {
+  const int64_t total = nnz * (int64_t)bs * bs;
+  if (total == 0) return;
+  auto hmix = [](uint64_t z) {
+    z ^= z >> 30;
+    z *= 0xBF58476D1CE4E5B9ull;
+    z ^= z >> 27;
+    z *= 0x94D049BB133111EBull;
+    z ^= z >> 31;
+    return z;
+  };
+  const uint64_t key = hmix(seed + 0x9E3779B97F4A7C15ull * ((uint64_t)mat_id + 1ull));
+  fill_sparse_kernel<<<sp_grid(total), 256, 0, st>>>(arena, total, ij, bs, pr, pc, r, c, key, kind);
+}
+
+cudaError_t launch_sp_densify(const double* arena, const int32_t* ij, int64_t nnz, int bs, int axis, int64_t sel0,
+                              int64_t stride, int64_t nk, int64_t other, double* dense, int64_t ld, int layout,
+                              cudaStream_t st) {
+  const int64_t rows = (axis == 0 ? other : nk) * bs, cols = (axis == 0 ? nk : other) * bs;
+  if (rows * cols == 0) return cudaSuccess;
+  const int64_t w = layout == 0 ? rows : cols, h = layout == 0 ? cols : rows;
+  cudaError_t e = cudaMemset2DAsync(dense, (size_t)ld * 8, 0, (size_t)w * 8, (size_t)h, st);
+  if (e != cudaSuccess) return e;
+  const int64_t total = nnz * (int64_t)bs * bs;
+  if (total) sp_densify_kernel<<<sp_grid(total), 256, 0, st>>>(arena, ij, total, bs, axis, sel0, std::max<int64_t>(stride, 1), nk, dense, ld, layout);
+  return cudaGetLastError();
+}
+
+void launch_sp_undensify(const double* dense, int64_t ld, int nsplit, int64_t split_stride, const int32_t* ij,
+                         int64_t nnz, int bs, double alpha, double beta, double* arena, cudaStream_t st) {
+  const int64_t total = nnz * (int64_t)bs * bs;
+  if (total == 0) return;
+  sp_undensify_kernel<<<sp_grid(total), 256, 0, st>>>(dense, ld, nsplit < 1 ? 1 : nsplit, split_stride, ij, bs, total,
+                                                      alpha, beta, arena);
+}
+
+void launch_sp_gather(const double* arena, const int32_t* src, int64_t n, int bs, double* out, cudaStream_t st) {
+  const int64_t total = n * (int64_t)bs * bs;
+  if (total == 0) return;
+  sp_gather_kernel<<<sp_grid(total), 256, 0, st>>>(arena, src, total, bs, out);
+}
+
+size_t sp_scan_temp_bytes(int64_t n) {
+  size_t bytes = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, bytes, (const int64_t*)nullptr, (int64_t*)nullptr, (int)std::max<int64_t>(n, 1));
+  return bytes;
+}
+
+cudaError_t launch_sp_stackgen(const int32_t* a_ptr, const int32_t* a_kk, const int32_t* b_ptr, const int32_t* b_kk,
+                               const int32_t* b_slot, const int32_t* cmap, int64_t nloc, const int32_t* li,
+                               const int32_t* lj, int64_t q0, int64_t n, int64_t* cnt, int64_t* off, void* scan_tmp,
+                               size_t scan_bytes, int32_t* trip, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  SpPanels P{a_ptr, a_kk, b_ptr, b_kk, b_slot, cmap, nloc};
+  sp_gen_kernel<false><<<sp_grid(n), 256, 0, st>>>(P, li, lj, q0, n, cnt, nullptr, nullptr);
+  cudaError_t e = cudaMemsetAsync(cnt + n, 0, sizeof(int64_t), st);
+  if (e != cudaSuccess) return e;
+  size_t bytes = scan_bytes;
+  e = cub::DeviceScan::ExclusiveSum(scan_tmp, bytes, cnt, off, (int)(n + 1), st);
+  if (e != cudaSuccess) return e;
+  sp_gen_kernel<true><<<sp_grid(n), 256, 0, st>>>(P, li, lj, q0, n, nullptr, off, trip);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_smm_sparse(int bs, const int32_t* trip, const int64_t* off, int64_t nruns, const double* A,
+                              const double* B, double* C, double alpha, cudaStream_t st) {
+  if (nruns <= 0) return cudaSuccess;
+  if (bs == 22) return launch_sp_tc<22>(trip, off, nruns, A, B, C, alpha, st);
+  if (bs == 64) return launch_sp_tc<64>(trip, off, nruns, A, B, C, alpha, st);
+  const size_t smem = 2 * (size_t)bs * bs * sizeof(double);
+  if (smem > 48 * 1024)
+    cudaFuncSetAttribute(smm_sparse_generic_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const unsigned grid = (unsigned)std::min<int64_t>(nruns, (int64_t)num_sms() * 8);
+  smm_sparse_generic_kernel<<<grid, 256, smem, st>>>(bs, trip, off, nruns, A, B, C, alpha);
+  return cudaGetLastError();
+}
+
+}  // namespace dbm

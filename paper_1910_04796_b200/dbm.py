@@ -18,7 +18,9 @@ LIB_PATH = os.path.join(_HERE, "libdbm.so")
 
 PATH_BLOCKED = 0
 PATH_DENSIFIED = 1
-_PATHS = {"blocked": PATH_BLOCKED, "densified": PATH_DENSIFIED, PATH_BLOCKED: 0, PATH_DENSIFIED: 1}
+PATH_AUTO = 2
+_PATHS = {"blocked": PATH_BLOCKED, "densified": PATH_DENSIFIED, "auto": PATH_AUTO, PATH_BLOCKED: 0,
+          PATH_DENSIFIED: 1, PATH_AUTO: 2}
 
 # dbm_ctx_profile_read kernel ids
 K_DGEMM, K_SMM, K_DENSIFY, K_UNDENSIFY, K_STACKGEN = 0, 1, 2, 3, 4
@@ -66,6 +68,10 @@ _SIGS = {
                                     C.c_int, _P, _P, C.POINTER(C.c_int)]),
     "dbm_ctx_destroy": (C.c_int, [_P]),
     "dbm_matrix_create": (C.c_int, [_P, _I64, _I64, C.c_int32, C.POINTER(_P)]),
+    "dbm_matrix_create_sparse": (C.c_int, [_P, _I64, _I64, C.c_int32, _P, C.POINTER(_P)]),
+    "dbm_pattern_random": (C.c_int, [C.c_uint64, C.c_uint32, _I64, _I64, C.c_double, _P]),
+    "dbm_matrix_nnz": (C.c_int, [_P, C.POINTER(_I64), C.POINTER(_I64)]),
+    "dbm_ctx_set_densify_threshold": (C.c_int, [_P, C.c_double]),
     "dbm_matrix_local_info": (C.c_int, [_P, C.POINTER(_I64), C.POINTER(_I64), C.POINTER(_I64)]),
     "dbm_matrix_local_csr": (C.c_int, [_P, _P, _P, _P]),
     "dbm_matrix_attach": (C.c_int, [_P, _P, _I64]),
@@ -189,6 +195,10 @@ class Context:
         _check(load().dbm_ctx_set_algorithm(self.h, int(a)))
         self.algorithm = a
 
+    def set_densify_threshold(self, threshold: float) -> None:
+        """should_densify threshold of path='auto': densify iff occupancy >= threshold."""
+        _check(load().dbm_ctx_set_densify_threshold(self.h, threshold))
+
     def set_dense_chunk_bytes(self, nbytes: int) -> None:
         _check(load().dbm_ctx_set_dense_chunk_bytes(self.h, nbytes))
 
@@ -220,18 +230,43 @@ class Context:
 
 
 # ---------------------------------------------------------------------------- matrix
-class Matrix:
-    """dbm_matrix: rows x cols FP64 matrix of bs x bs blocks, block-cyclic over ctx's grid."""
+def pattern_random(seed: int, mat_id: int, Mb: int, Nb: int, occupancy: float):
+    """dbm_pattern_random: (Mb, Nb) uint8 numpy mask of stored blocks (reading R15)."""
+    import numpy as np
 
-    def __init__(self, ctx: Context, rows: int, cols: int, block_size: int, arena: torch.Tensor | None = None):
+    m = np.empty(max(Mb * Nb, 1), dtype=np.uint8)
+    _check(load().dbm_pattern_random(seed, mat_id, Mb, Nb, occupancy, m.ctypes.data))
+    return m[: Mb * Nb].reshape(Mb, Nb)
+
+
+class Matrix:
+    """dbm_matrix: rows x cols FP64 matrix of bs x bs blocks, block-cyclic over ctx's grid.
+    mask (numpy (Mb, Nb), nonzero = stored) makes it block-sparse (dbm_matrix_create_sparse, R15)."""
+
+    def __init__(self, ctx: Context, rows: int, cols: int, block_size: int, arena: torch.Tensor | None = None,
+                 mask=None, sparse: bool = False):
         lib = load()
         h = C.c_void_p()
-        _check(lib.dbm_matrix_create(ctx.h, rows, cols, block_size, C.byref(h)))
+        self.sparse = sparse or mask is not None
+        if self.sparse:
+            import numpy as np
+
+            mk = None
+            if mask is not None:
+                mk = np.ascontiguousarray(mask, dtype=np.uint8)
+                assert mk.size == (rows // block_size) * (cols // block_size)
+            _check(lib.dbm_matrix_create_sparse(ctx.h, rows, cols, block_size,
+                                                mk.ctypes.data if mk is not None else None, C.byref(h)))
+        else:
+            _check(lib.dbm_matrix_create(ctx.h, rows, cols, block_size, C.byref(h)))
         self.h, self.ctx = h, ctx
         self.rows, self.cols, self.bs = rows, cols, block_size
         ml, nl, nb = C.c_int64(), C.c_int64(), C.c_int64()
         _check(lib.dbm_matrix_local_info(h, C.byref(ml), C.byref(nl), C.byref(nb)))
         self.mloc, self.nloc, self.arena_bytes = ml.value, nl.value, nb.value
+        lo, gl = C.c_int64(), C.c_int64()
+        _check(lib.dbm_matrix_nnz(h, C.byref(lo), C.byref(gl)))
+        self.nnz, self.global_nnz = lo.value, gl.value
         if arena is None:
             arena = torch.empty(max(self.arena_bytes // 8, 2), dtype=torch.float64, device=ctx.device)
         self.arena = arena
@@ -244,10 +279,10 @@ class Matrix:
         import numpy as np
 
         rp = np.empty(self.mloc + 1, dtype=np.int64)
-        ci = np.empty(max(self.mloc * self.nloc, 1), dtype=np.int64)
+        ci = np.empty(max(self.nnz, 1), dtype=np.int64)
         ri = np.empty(max(self.mloc, 1), dtype=np.int64)
         _check(load().dbm_matrix_local_csr(self.h, rp.ctypes.data, ci.ctypes.data, ri.ctypes.data))
-        return rp, ci[: self.mloc * self.nloc], ri[: self.mloc]
+        return rp, ci[: self.nnz], ri[: self.mloc]
 
     def set_block(self, bi: int, bj: int, block) -> None:
         import numpy as np
@@ -278,7 +313,7 @@ class Matrix:
 
     def local_view(self) -> torch.Tensor:
         """The arena as (mloc*nloc, bs, bs) blocks; block[.., x, y] -> use .transpose for column-major."""
-        n = self.mloc * self.nloc * self.bs * self.bs
+        n = self.nnz * self.bs * self.bs
         return self.arena[:n]
 
     def densify(self, dense: torch.Tensor, ld: int | None = None, layout: int = 0) -> None:

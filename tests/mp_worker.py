@@ -75,9 +75,79 @@ def main():
                                           "kind": kind, "err": err, "ok": bool(ok_val), "bytes_ok": ok_bytes,
                                           "recv": st["bytes_recv"], "expect_recv": rv}), flush=True)
         ctx.close()
+    failures += sparse_cases(world, rank, dev, grids)
     dist.barrier(device_ids=[local])
     dist.destroy_process_group()
     sys.exit(1 if failures else 0)
+
+
+def sparse_recv_bytes(am, bm, bs, pr, pc, r, c):
+    """Bytes rank (r, c) pulls in a block-sparse blocked multiply: the stored blocks of every remote
+    A(r, kappa) / B(kappa, c) panel (owner-pull Cannon, reading R5; only stored blocks move, R15)."""
+    L = orc.lcm(pr, pc)
+    Mb, Kb = am.shape
+    Nb = bm.shape[1]
+    me = r * pc + c
+    total = 0
+    for s in range(L):
+        k, asrc, bsrc = orc.cannon_step(pr, pc, r, c, s)
+        if asrc != me:
+            total += int(am[r:Mb:pr, k:Kb:L].sum())
+        if bsrc != me:
+            total += int(bm[k:Kb:L, c:Nb:pc].sum())
+    return total * bs * bs * 8
+
+
+def sparse_cases(world, rank, dev, grids):
+    """Block-sparse operands (reading R15) on every grid: both paths against orc_multiply_sparse."""
+    failures = 0
+    shapes = [(352, 352, 352, 22, 0.3, 0.4, 1.0), (704, 528, 1100, 22, 0.1, 0.2, 0.7), (384, 640, 1280, 64, 0.5, 0.5, 0.5),
+              (66, 154, 198, 22, 0.0, 0.5, 1.0)]
+    for pr, pc in grids:
+        ctx = dbm.Context.from_distributed(pr=pr, pc=pc)
+        r, c = ctx.myrow, ctx.mycol
+        for (M, N, K, bs, oa, ob, oc) in shapes:
+            Mb, Nb, Kb = M // bs, N // bs, K // bs
+            am, bm, cm = (orc.pattern_random(5, i, *dims, occ) for i, dims, occ in
+                          ((0, (Mb, Kb), oa), (1, (Kb, Nb), ob), (2, (Mb, Nb), oc)))
+            for path in ("blocked", "densified"):
+                for kind in (0, 1):
+                    A = dbm.Matrix(ctx, M, K, bs, mask=am)
+                    B = dbm.Matrix(ctx, K, N, bs, mask=bm)
+                    C = dbm.Matrix(ctx, M, N, bs, mask=cm)
+                    A.fill_random(SEED, 0, kind)
+                    B.fill_random(SEED, 1, kind)
+                    for rep in range(2):
+                        C.fill_random(SEED, 2, kind)
+                        st = dbm.multiply(ctx, 0.75, A, B, -1.25, C, path)
+                    torch.cuda.synchronize()
+                    got = C.arena.cpu().numpy()[: C.arena_bytes // 8]
+                    Ag = orc.fill_arena(SEED, 0, kind, M, K, bs)
+                    Bg = orc.fill_arena(SEED, 1, kind, K, N, bs)
+                    Cg = orc.fill_arena(SEED, 2, kind, M, N, bs)
+                    orc.multiply_sparse(Mb, Nb, Kb, bs, 0.75, Ag, am, Bg, bm, -1.25, Cg, cm)
+                    ref = orc.sparse_compress(Cg, cm, Mb, Nb, bs, pr, pc, r, c)
+                    if kind == 1:
+                        ok_val = np.array_equal(got, ref)
+                        err = float(np.abs(got - ref).max()) if ref.size else 0.0
+                    else:
+                        err = float(np.linalg.norm(got - ref) / max(np.linalg.norm(ref), 1e-300)) if ref.size else 0.0
+                        ok_val = err <= 1e-12
+                    if path == "blocked":
+                        ok_bytes = st["bytes_recv"] == sparse_recv_bytes(am, bm, bs, pr, pc, r, c)
+                    else:
+                        ok_bytes = (st["bytes_recv"], st["bytes_sent"]) == orc.cannon_bytes(Mb, Nb, Kb, bs, pr, pc, r, c)
+                    flags = torch.tensor([0 if (ok_val and ok_bytes) else 1], device=dev)
+                    dist.all_reduce(flags)
+                    if flags.item():
+                        failures += 1
+                    if rank == 0 or not (ok_val and ok_bytes):
+                        print(json.dumps({"rank": rank, "grid": f"{pr}x{pc}", "sparse": [oa, ob, oc],
+                                          "shape": [M, N, K, bs], "path": path, "kind": kind, "err": err,
+                                          "ok": bool(ok_val), "bytes_ok": ok_bytes, "recv": st["bytes_recv"]}),
+                              flush=True)
+        ctx.close()
+    return failures
 
 
 if __name__ == "__main__":

@@ -1,0 +1,3 @@
+set -x
+timeout 900 python -m pytest tests/test_gpu_sparse.py -x -q 2>&1 | tail -25
+timeout 900 python -m pytest tests/test_gpu_parity.py -x -q 2>&1 | tail -3

@@ -83,6 +83,8 @@ def lib():
                                            _pd]),
             "orc_sparse_expand": (None, [_pd, _pu8, _i64, _i64, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, _pd]),
             "orc_sparse_stacks": (_i64, [_i64, _i64, _i64, _pu8, _pu8, _pu8, _i64, _pi32, _pi64, _pi64]),
+            "orc_sparse_rows_from_seeds": (_i64, [_i64, _i64, _i64, C.c_int, _u64, C.c_int, _u64, _dbl, _dbl, _dbl,
+                                                  _dbl, _dbl, _pi64, _i64, _pd]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -236,6 +238,15 @@ def sparse_stacks(amask, bmask, cmask, cap: int = 30000):
     lib().orc_sparse_stacks(mloc, nloc, kb, _p(am, _pu8), _p(bm, _pu8), _p(cm, _pu8), cap, _p(trip, _pi32),
                             _p(ptr, _pi64), C.byref(ns))
     return trip[: 3 * e].reshape(e, 3), ptr[: ns.value + 1]
+
+
+def sparse_rows_from_seeds(M, N, K, bs, seed, kind, pseed, occ_a, occ_b, occ_c, alpha, beta, rows):
+    """(out (nrows, N) with NaN on absent C blocks, multiply-adds performed)."""
+    rows = np.ascontiguousarray(rows, dtype=np.int64)
+    out = np.empty((len(rows), N))
+    n = lib().orc_sparse_rows_from_seeds(M, N, K, bs, seed, kind, pseed, occ_a, occ_b, occ_c, alpha, beta,
+                                         _p(rows, _pi64), len(rows), _p(out))
+    return out, n
 
 
 # ---------------------------------------------------------------- Cannon

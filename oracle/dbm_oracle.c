@@ -618,3 +618,42 @@ int64_t orc_sparse_stacks(int64_t mloc, int64_t nloc, int64_t kb, const uint8_t*
   free(cslot);
   return e;
 }
+
+/* Rows `rows[0..nrows)` of C_out for block-sparse operands regenerated from the seeds: element values from
+ * the generator (seed, mat_id 0/1/2), patterns from orc_pattern_present(pseed, mat_id 0/1/2, occ_*).
+ * out (nrows x N, row-major) = beta*C + alpha*sum over k of A(i,k) B(k,j) taken over k whose A block
+ * (i/bs, k/bs) and B block (k/bs, j/bs) are both stored, for stored C blocks; NAN where C's block is
+ * absent.  Returns the number of multiply-adds performed (useful work, 2 flop each). */
+int64_t orc_sparse_rows_from_seeds(int64_t M, int64_t N, int64_t K, int bs, uint64_t seed, int kind, uint64_t pseed,
+                                   double occ_a, double occ_b, double occ_c, double alpha, double beta,
+                                   const int64_t* rows, int64_t nrows, double* out) {
+  (void)M;
+  int64_t fmas = 0;
+  int64_t Kb = K / bs, Nb = N / bs;
+#pragma omp parallel for schedule(dynamic, 1) reduction(+ : fmas)
+  for (int64_t q = 0; q < nrows; ++q) {
+    int64_t i = rows[q], bi = i / bs;
+    double* acc = (double*)calloc((size_t)N, sizeof(double));
+    for (int64_t bk = 0; bk < Kb; ++bk) {
+      if (!orc_pattern_present(pseed, 0, bi, bk, occ_a)) continue;
+      for (int64_t bj = 0; bj < Nb; ++bj) {
+        if (!orc_pattern_present(pseed, 1, bk, bj, occ_b) || !orc_pattern_present(pseed, 2, bi, bj, occ_c)) continue;
+        for (int64_t k = bk * bs; k < (bk + 1) * bs; ++k) {
+          double a = orc_fill_value(seed, 0, i, k, kind);
+          for (int64_t j = bj * bs; j < (bj + 1) * bs; ++j) acc[j] += a * orc_fill_value(seed, 1, k, j, kind);
+        }
+        fmas += (int64_t)bs * bs;
+      }
+    }
+    for (int64_t j = 0; j < N; ++j) {
+      if (!orc_pattern_present(pseed, 2, bi, j / bs, occ_c)) {
+        out[q * N + j] = NAN;
+        continue;
+      }
+      double t = alpha * acc[j];
+      out[q * N + j] = (beta == 0.0) ? t : t + beta * orc_fill_value(seed, 2, i, j, kind);
+    }
+    free(acc);
+  }
+  return fmas;
+}

@@ -128,6 +128,12 @@ void orc_sparse_expand(const double* local_sparse, const uint8_t* mask, int64_t 
 int64_t orc_sparse_stacks(int64_t mloc, int64_t nloc, int64_t kb, const uint8_t* amask, const uint8_t* bmask,
                           const uint8_t* cmask, int64_t cap, int32_t* triplets, int64_t* stack_ptr, int64_t* n_stacks);
 
+/* Rows of C_out for sparse operands regenerated from seeds (values: seed; patterns: pseed, occ_*); NAN where
+ * C's block is absent.  Returns the multiply-adds performed over stored block pairs. */
+int64_t orc_sparse_rows_from_seeds(int64_t M, int64_t N, int64_t K, int bs, uint64_t seed, int kind, uint64_t pseed,
+                                   double occ_a, double occ_b, double occ_c, double alpha, double beta,
+                                   const int64_t* rows, int64_t nrows, double* out);
+
 int orc_num_threads(void);
 
 #ifdef __cplusplus

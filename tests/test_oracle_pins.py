@@ -566,3 +566,24 @@ def test_sparse_stacks_dense_pattern_equals_dense_stacks(orc):
         t1, p1 = orc.sparse_stacks(one(mloc, kb), one(kb, nloc), one(mloc, nloc), cap)
         t2, p2 = orc.stacks(mloc, nloc, kb, cap)
         assert np.array_equal(t1, t2) and np.array_equal(p1, p2)
+
+
+def test_sparse_rows_from_seeds_matches_masked_numpy(orc):
+    """Sampled-row checker for sparse configs: equals the masked numpy product on the stored C blocks, NaN
+    elsewhere, and counts exactly bs^2 multiply-adds per (stored A, B, C) block triple of the row."""
+    M, N, K, bs, ps = 66, 88, 110, 11, 3
+    oa, ob, oc = 0.4, 0.5, 0.7
+    Mb, Nb, Kb = M // bs, N // bs, K // bs
+    am, bm, cm = orc.pattern_random(ps, 0, Mb, Kb, oa), orc.pattern_random(ps, 1, Kb, Nb, ob), \
+        orc.pattern_random(ps, 2, Mb, Nb, oc)
+    A = orc.arena_to_dense(orc.fill_arena(1910, 0, 0, M, K, bs), Mb, Kb, bs) * np.kron(am, np.ones((bs, bs)))
+    B = orc.arena_to_dense(orc.fill_arena(1910, 1, 0, K, N, bs), Kb, Nb, bs) * np.kron(bm, np.ones((bs, bs)))
+    Cd = orc.arena_to_dense(orc.fill_arena(1910, 2, 0, M, N, bs), Mb, Nb, bs)
+    rows = np.array([0, 5, 11, 40, 65])
+    out, fmas = orc.sparse_rows_from_seeds(M, N, K, bs, 1910, 0, ps, oa, ob, oc, 0.75, -1.25, rows)
+    cmask = np.kron(cm, np.ones((bs, bs))).astype(bool)[rows]
+    want = (0.75 * (A @ B) - 1.25 * Cd)[rows]
+    assert np.allclose(out[cmask], want[cmask], rtol=0, atol=1e-12)
+    assert np.isnan(out[~cmask]).all()
+    triples = sum(int(am[i // bs, k] and bm[k, j] and cm[i // bs, j]) for i in rows for k in range(Kb) for j in range(Nb))
+    assert fmas == triples * bs * bs

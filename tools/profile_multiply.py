@@ -21,9 +21,17 @@ def main():
     p.add_argument("--bs", type=int, default=22)
     p.add_argument("--path", default="blocked")
     p.add_argument("--reps", type=int, default=2)
+    p.add_argument("--occ", type=float, default=None, help="block occupancy of A and B (sparse, reading R15)")
+    p.add_argument("--occ-c", type=float, default=1.0, help="block occupancy of C when --occ is given")
     a = p.parse_args()
     ctx = dbm.Context()
-    A, B, C = dbm.Matrix(ctx, a.M, a.K, a.bs), dbm.Matrix(ctx, a.K, a.N, a.bs), dbm.Matrix(ctx, a.M, a.N, a.bs)
+    if a.occ is None:
+        A, B, C = dbm.Matrix(ctx, a.M, a.K, a.bs), dbm.Matrix(ctx, a.K, a.N, a.bs), dbm.Matrix(ctx, a.M, a.N, a.bs)
+    else:
+        Mb, Nb, Kb = a.M // a.bs, a.N // a.bs, a.K // a.bs
+        A = dbm.Matrix(ctx, a.M, a.K, a.bs, mask=dbm.pattern_random(1910, 0, Mb, Kb, a.occ))
+        B = dbm.Matrix(ctx, a.K, a.N, a.bs, mask=dbm.pattern_random(1910, 1, Kb, Nb, a.occ))
+        C = dbm.Matrix(ctx, a.M, a.N, a.bs, mask=dbm.pattern_random(1910, 2, Mb, Nb, a.occ_c))
     A.fill_random(1910, 0, 0)
     B.fill_random(1910, 1, 0)
     C.fill_random(1910, 2, 0)
@@ -34,8 +42,9 @@ def main():
         e1.record()
         torch.cuda.synchronize()
         ms = e0.elapsed_time(e1)
-        print(json.dumps({"M": a.M, "N": a.N, "K": a.K, "bs": a.bs, "path": a.path, "rep": i, "ms": ms,
-                          "tflops": 2.0 * a.M * a.N * a.K / ms / 1e9, "entries": st["entries"]}), flush=True)
+        eff = st["flops"] if a.occ is not None else 2.0 * a.M * a.N * a.K
+        print(json.dumps({"M": a.M, "N": a.N, "K": a.K, "bs": a.bs, "path": a.path, "occ": a.occ, "rep": i, "ms": ms,
+                          "tflops": eff / ms / 1e9, "entries": st["entries"], "stacks": st["stacks"]}), flush=True)
 
 
 if __name__ == "__main__":

@@ -1257,6 +1257,7 @@ struct SpStep {
   int64_t a_nnz = 0, b_nnz = 0, entries = 0;
   size_t o_aptr = 0, o_akk = 0, o_bptr = 0, o_bkk = 0, o_bslot = 0;  // int32 offsets into d_meta
   std::vector<int32_t> run_len;                                      // per traversal position
+  std::vector<int64_t> chunk_entries;                                // per chunk of runs_per_chunk runs
 };
 struct SpCache {
   uint64_t a_serial = 0, b_serial = 0, c_serial = 0;
@@ -1489,6 +1490,13 @@ dbm_status sp_cache_get(dbm_ctx ctx, dbm_matrix A, dbm_matrix B, dbm_matrix C, S
   sc->off_scan = take(sc->scan_bytes);
   sc->off_trip = take((size_t)sc->runs_per_chunk * kbmax * 12);
   sc->total = std::max<size_t>(off, 256);
+  for (SpStep& x : sc->steps) {
+    for (size_t q0 = 0; q0 < x.run_len.size(); q0 += (size_t)sc->runs_per_chunk) {
+      int64_t n = 0;
+      for (size_t q = q0; q < std::min(x.run_len.size(), q0 + (size_t)sc->runs_per_chunk); ++q) n += x.run_len[q];
+      x.chunk_entries.push_back(n);
+    }
+  }
   cudaError_t e = cudaMalloc(&sc->d_meta, std::max<size_t>(meta.size(), 1) * 4);
   if (e == cudaSuccess && !meta.empty())
     e = cudaMemcpy(sc->d_meta, meta.data(), meta.size() * 4, cudaMemcpyHostToDevice);
@@ -1645,17 +1653,20 @@ dbm_status multiply_sparse_blocked(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_
                                        : (const double*)(ws + sc->ownB_off[x.kappa]);
     if (x.entries > 0) {
       const int64_t nruns = mloc * nloc;
-      for (int64_t q0 = 0; q0 < nruns; q0 += sc->runs_per_chunk) {
+      for (int64_t q0 = 0, ch = 0; q0 < nruns; q0 += sc->runs_per_chunk, ++ch) {
         const int64_t n = std::min(sc->runs_per_chunk, nruns - q0);
+        const int64_t ent = x.chunk_entries[ch];
+        if (ent == 0) continue;
         {
-          ProfScope ps(ctx, cs, 4, 0.0, 0.0);
+          // algorithmic bytes: the two A/B run lists read per run, 12 B written per entry
+          ProfScope ps(ctx, cs, 4, 0.0, 12.0 * ent + 16.0 * n);
           CUDA_TRY(ctx, launch_sp_stackgen(meta + x.o_aptr, meta + x.o_akk, meta + x.o_bptr, meta + x.o_bkk,
                                            meta + x.o_bslot, C->sparse ? C->d_map : nullptr, nloc, trav_li, trav_lj, q0,
                                            n, cnt, offs, ws + sc->off_scan, sc->scan_bytes, trip, cs));
           launches += 3;
         }
         {
-          ProfScope ps(ctx, cs, 1, 0.0, 0.0);
+          ProfScope ps(ctx, cs, 1, 2.0 * bs * bb * ent, 16.0 * bb * ent);
           CUDA_TRY(ctx, launch_smm_sparse(bs, trip, offs, n, Ap, Bp, C->arena, alpha, cs));
           ++launches;
         }

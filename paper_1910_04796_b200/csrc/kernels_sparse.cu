@@ -157,20 +157,28 @@ __device__ __forceinline__ void sp_dmma(double (&c)[2], double a, double b) {
                : "d"(a), "d"(b));
 }
 
+constexpr int sp_pitch(int bs) {  // column pitch (doubles) with pitch mod 16 in {4, 12}: the four k (or n)
+  int p = bs;                      // columns a half-warp's 64-bit fragment loads touch land on disjoint
+  while (p % 16 != 4 && p % 16 != 12) ++p;  // groups of 4 bank pairs (conflict-free with rows 0..3)
+  return p;
+}
+
 template <int BS>
 struct SpCfg {
   static constexpr int MT = (BS + 7) / 8;            // 8x8 subtiles per block dimension
   static constexpr int TEAM = MT >= 4 ? 4 : 1;       // warps per run
   static constexpr int NPW = MT / TEAM;              // n-subtiles per warp
-  static constexpr int WARPS = TEAM == 4 ? 4 : 8;    // bs 64: one 4-warp team (132 KB of stages)
+  static constexpr int WARPS = TEAM == 4 ? 4 : 8;    // bs 64: one 4-warp team
   static constexpr int TEAMS = WARPS / TEAM;
   static constexpr int BB = BS * BS;
-  // one stage = A block (+ slack for the padded rows m >= BS) and B block (+ padded columns n >= BS)
-  static constexpr int A_D = BB + 8 * MT;
-  static constexpr int B_D = 8 * MT * BS + 8;
+  static constexpr int P = sp_pitch(BS);             // 28 (bs 22), 68 (bs 64)
+  // stage = A block [k][m] (pitch P, m < P) + B block [n][k] (pitch P, n < 8*MT padded)
+  static constexpr int A_D = BS * P;
+  static constexpr int B_D = 8 * MT * P;
   static constexpr int STAGE = ((A_D + B_D) + 1) / 2 * 2;
   static constexpr size_t SMEM = (size_t)TEAMS * 2 * STAGE * 8;
   static_assert(MT % TEAM == 0, "team split");
+  static_assert(BS % 2 == 0, "16-byte column chunks");
 };
 
 template <int BS>
@@ -179,7 +187,8 @@ __global__ void __launch_bounds__(SpCfg<BS>::WARPS * 32, 1)
                       const double* __restrict__ A, const double* __restrict__ B, double* __restrict__ C,
                       double alpha) {
   using Cfg = SpCfg<BS>;
-  constexpr int MT = Cfg::MT, TEAM = Cfg::TEAM, NPW = Cfg::NPW, BB = Cfg::BB;
+  constexpr int MT = Cfg::MT, TEAM = Cfg::TEAM, NPW = Cfg::NPW, BB = Cfg::BB, P = Cfg::P;
+  constexpr int HALF = BS / 2;  // 16-byte chunks per block column
   extern __shared__ __align__(16) double sm[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int team = warp / TEAM, tw = warp % TEAM;
@@ -187,18 +196,6 @@ __global__ void __launch_bounds__(SpCfg<BS>::WARPS * 32, 1)
   double* st0 = sm + (size_t)team * 2 * Cfg::STAGE;
   const int tlane = tw * 32 + lane;  // 0 .. TEAM*32-1
   constexpr int TT = TEAM * 32;
-  // blocks are 16-byte aligned when BB is even (bs 22, 64)
-  auto load = [&](double* dst, int64_t entry) {
-    const double* a = A + (int64_t)trip[3 * entry] * BB;
-    const double* b = B + (int64_t)trip[3 * entry + 1] * BB;
-    const uint32_t sa = (uint32_t)__cvta_generic_to_shared(dst);
-    const uint32_t sb = (uint32_t)__cvta_generic_to_shared(dst + Cfg::A_D);
-    for (int i = tlane; i < BB / 2; i += TT) {
-      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa + 16u * i), "l"(a + 2 * i) : "memory");
-      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sb + 16u * i), "l"(b + 2 * i) : "memory");
-    }
-    asm volatile("cp.async.commit_group;" ::: "memory");
-  };
   auto team_sync = [&]() {
     if (TEAM == 1)
       __syncwarp();
@@ -206,57 +203,136 @@ __global__ void __launch_bounds__(SpCfg<BS>::WARPS * 32, 1)
       asm volatile("bar.sync %0, %1;" ::"r"(1 + team), "r"(TT) : "memory");
   };
 
+  // The team's runs (run = first + i * nteams) are consumed as ONE stream of entries: the copy of the
+  // next entry (possibly the next run's first) is in flight while this one multiplies, its slots and
+  // the next run's offsets are fetched one step earlier still, and a run's C block is read into
+  // registers when the run starts, so no global-memory latency sits on the critical path.
   const int64_t nteams = (int64_t)gridDim.x * Cfg::TEAMS;
-  for (int64_t run = (int64_t)blockIdx.x * Cfg::TEAMS + team; run < nruns; run += nteams) {
-    const int64_t e0 = off[run], e1 = off[run + 1];
-    if (e0 == e1) continue;
-    double acc[MT][NPW][2];
-#pragma unroll
-    for (int i = 0; i < MT; ++i)
-#pragma unroll
-      for (int j = 0; j < NPW; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-    team_sync();  // the previous run's last stage has been consumed by every team warp
-    load(st0, e0);
-    for (int64_t e = e0; e < e1; ++e) {
-      double* cur = st0 + (size_t)((e - e0) & 1) * Cfg::STAGE;
-      if (e + 1 < e1) {
-        load(st0 + (size_t)((e + 1 - e0) & 1) * Cfg::STAGE, e + 1);
-        asm volatile("cp.async.wait_group 1;" ::: "memory");
-      } else {
-        asm volatile("cp.async.wait_group 0;" ::: "memory");
+  int64_t pr = (int64_t)blockIdx.x * Cfg::TEAMS + team, pe = 0, pend = 0, pstart = 0;
+  while (pr < nruns) {
+    pe = off[pr];
+    pend = off[pr + 1];
+    if (pe < pend) break;
+    pr += nteams;
+  }
+  if (pr >= nruns) return;
+  pstart = pe;
+  int la = trip[3 * pe], lb = trip[3 * pe + 1], lc = trip[3 * pe + 2];
+  int64_t gr = pr + nteams, g0 = 0, g1 = 0;  // prefetched offsets of the team's next run
+  if (gr < nruns) {
+    g0 = off[gr];
+    g1 = off[gr + 1];
+  }
+  struct Meta {
+    int cslot;
+    bool first, last;
+  };
+  auto issue = [&](int stage) -> Meta {
+    const Meta m{lc, pe == pstart, pe + 1 == pend};
+    const double* a = A + (int64_t)la * BB;
+    const double* b = B + (int64_t)lb * BB;
+    double* dst = st0 + (size_t)stage * Cfg::STAGE;
+    const uint32_t sa = (uint32_t)__cvta_generic_to_shared(dst);
+    const uint32_t sb = (uint32_t)__cvta_generic_to_shared(dst + Cfg::A_D);
+    for (int i = tlane; i < BS * HALF; i += TT) {
+      const int col = i / HALF, j = i - col * HALF;
+      const uint32_t d = 8u * (uint32_t)(col * P + 2 * j);
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa + d), "l"(a + col * BS + 2 * j) : "memory");
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sb + d), "l"(b + col * BS + 2 * j) : "memory");
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+    if (++pe == pend) {  // next nonempty run of the team
+      int64_t r = gr, e = g0, e1 = g1;
+      while (r < nruns && e == e1) {
+        r += nteams;
+        if (r < nruns) {
+          e = off[r];
+          e1 = off[r + 1];
+        }
       }
-      team_sync();
-      const double* sA = cur;                // (m, k) at k*BS + m
-      const double* sB = cur + Cfg::A_D;     // (k, n) at n*BS + k
+      pr = r;
+      pe = pstart = e;
+      pend = e1;
+      gr = pr + nteams;
+      if (gr < nruns) {
+        g0 = off[gr];
+        g1 = off[gr + 1];
+      }
+    }
+    if (pr < nruns) {  // slots of the entry after this one (consumed by the next issue)
+      la = trip[3 * pe];
+      lb = trip[3 * pe + 1];
+      lc = trip[3 * pe + 2];
+    }
+    return m;
+  };
+
+  double acc[MT][NPW][2];
+  double creg[TEAM == 1 ? MT : 1][TEAM == 1 ? NPW : 1][2];
+  Meta nxt = issue(0);
+  int cs = 0;
+  for (;;) {
+    const Meta cur = nxt;
+    const bool more = pr < nruns;
+    if (more) {
+      nxt = issue(cs ^ 1);
+      asm volatile("cp.async.wait_group 1;" ::: "memory");
+    } else {
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
+    }
+    team_sync();
+    double* cb = C + (int64_t)cur.cslot * BB;
+    if (cur.first) {
 #pragma unroll
-      for (int ks = 0; ks < (BS + 3) / 4; ++ks) {
-        const int k = 4 * ks + t;
-        const bool kok = (BS % 4 == 0) || k < BS;
-        double a[MT], b[NPW];
+      for (int i = 0; i < MT; ++i)
 #pragma unroll
-        for (int mi = 0; mi < MT; ++mi) a[mi] = kok ? sA[k * BS + mi * 8 + g] : 0.0;
-#pragma unroll
-        for (int ni = 0; ni < NPW; ++ni) b[ni] = kok ? sB[((tw * NPW + ni) * 8 + g) * BS + k] : 0.0;
+        for (int j = 0; j < NPW; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+      if constexpr (TEAM == 1) {
 #pragma unroll
         for (int mi = 0; mi < MT; ++mi)
 #pragma unroll
-          for (int ni = 0; ni < NPW; ++ni) sp_dmma(acc[mi][ni], a[mi], b[ni]);
+          for (int ni = 0; ni < NPW; ++ni)
+#pragma unroll
+            for (int jj = 0; jj < 2; ++jj) {
+              const int m = mi * 8 + g, n = ni * 8 + 2 * t + jj;
+              creg[mi][ni][jj] = (m < BS && n < BS) ? cb[m + n * BS] : 0.0;
+            }
       }
-      team_sync();  // every warp is done with `cur` before it is refilled
     }
-    double* cb = C + (int64_t)trip[3 * e0 + 2] * BB;
+    const double* sA = st0 + (size_t)cs * Cfg::STAGE;  // (m, k) at k*P + m
+    const double* sB = sA + Cfg::A_D;                   // (k, n) at n*P + k
 #pragma unroll
-    for (int mi = 0; mi < MT; ++mi)
+    for (int ks = 0; ks < (BS + 3) / 4; ++ks) {
+      const int k = 4 * ks + t;
+      const bool kok = (BS % 4 == 0) || k < BS;
+      double a[MT], b[NPW];
 #pragma unroll
-      for (int ni = 0; ni < NPW; ++ni)
+      for (int mi = 0; mi < MT; ++mi) a[mi] = kok ? sA[k * P + mi * 8 + g] : 0.0;
 #pragma unroll
-        for (int jj = 0; jj < 2; ++jj) {
-          const int m = mi * 8 + g, n = (tw * NPW + ni) * 8 + 2 * t + jj;
-          if (m < BS && n < BS) {
-            double* p = cb + m + n * BS;
-            *p = __dadd_rn(*p, __dmul_rn(alpha, acc[mi][ni][jj]));
+      for (int ni = 0; ni < NPW; ++ni) b[ni] = kok ? sB[((tw * NPW + ni) * 8 + g) * P + k] : 0.0;
+#pragma unroll
+      for (int mi = 0; mi < MT; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < NPW; ++ni) sp_dmma(acc[mi][ni], a[mi], b[ni]);
+    }
+    team_sync();  // every warp is done with this stage before it is refilled
+    if (cur.last) {
+#pragma unroll
+      for (int mi = 0; mi < MT; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < NPW; ++ni)
+#pragma unroll
+          for (int jj = 0; jj < 2; ++jj) {
+            const int m = mi * 8 + g, n = (tw * NPW + ni) * 8 + 2 * t + jj;
+            if (m < BS && n < BS) {
+              double* p = cb + m + n * BS;
+              const double c0 = (TEAM == 1) ? creg[TEAM == 1 ? mi : 0][TEAM == 1 ? ni : 0][jj] : *p;
+              *p = __dadd_rn(c0, __dmul_rn(alpha, acc[mi][ni][jj]));
+            }
           }
-        }
+    }
+    if (!more) break;
+    cs ^= 1;
   }
 }
 

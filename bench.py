@@ -1,6 +1,6 @@
 """Benchmark: FP64 TFLOP/s of C = alpha*A*B + beta*C through libdbm (BASELINE.json metric).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config sq64|sq22|r64|r22|s352]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config sq64|sq22|r64|r22|s352|sp22|sp64]
                     [--path densified|blocked] [--impl ours|reference]
 
 A step is one dbm_multiply over the whole configuration (Cannon over the N-rank grid, every local
@@ -32,7 +32,12 @@ CONFIGS = {
     "sq22": (63360, 63360, 63360, 22, "densified", 2),
     "r64": (1408, 1408, 1982464, 64, "densified", 3),
     "r22": (1408, 1408, 1982464, 22, "densified", 4),
+    # block-sparse (§8f-2, reading R15; not a BASELINE config): A and B at 10 % block occupancy, C fully
+    # stored; the metric counts only the stored block products (2 bs^3 per stack entry)
+    "sp22": (63360, 63360, 63360, 22, "blocked", None),
+    "sp64": (63360, 63360, 63360, 64, "blocked", None),
 }
+SPARSE_OCC = {"sp22": (0.1, 0.1, 1.0), "sp64": (0.1, 0.1, 1.0)}
 SEED = 1910
 FP64_PEAK_MEASURED = 37.15  # TFLOP/s per B200, DMMA m8n8k4 chain at 1965 MHz (profiles/r01_fp64_peaks.jsonl)
 FP64_PEAK_SPEC = 37.2       # 148 SM x 64 FMA/clk x 2 x 1.965 GHz
@@ -54,7 +59,7 @@ def parse():
     p.add_argument("--steps", type=int, default=3)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--config", default="sq64", choices=sorted(CONFIGS))
-    p.add_argument("--path", default=None, choices=["densified", "blocked"])
+    p.add_argument("--path", default=None, choices=["densified", "blocked", "auto"])
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--transport", default="ce", choices=["ce", "nccl"], help="Cannon panel transport (N>1)")
     p.add_argument("--grid", default="", help="force the process grid, e.g. 1x4 (default: reading R1)")
@@ -132,6 +137,30 @@ def oracle_sample(M, N, K, rows: int) -> dict:
             "seconds": dt}
 
 
+def oracle_sample_sparse(M, N, K, bs, occ, rows: int) -> dict:
+    """Time the host oracle on `rows` sampled rows of a block-sparse C (useful flop = 2 x its multiply-adds)."""
+    import numpy as np
+
+    import oracle
+
+    oracle.build()
+    idx = np.linspace(0, M - 1, rows).astype(np.int64)
+    t0 = time.perf_counter()
+    _, fmas = oracle.sparse_rows_from_seeds(M, N, K, bs, SEED, 0, SEED, occ[0], occ[1], occ[2], 1.0, 0.0, idx)
+    dt = time.perf_counter() - t0
+    return {"value": 2.0 * fmas / dt / 1e12, "unit": "TFLOP/s", "cores": oracle.num_threads(), "kind": "oracle",
+            "sample": f"{rows} of {M} rows of block-sparse C regenerated from seeds ({2 * fmas:.3g} useful flop), "
+                      f"{dt:.1f} s", "seconds": dt}
+
+
+def auto_rows_sparse(M, N, K, bs, occ, target_s: float = 15.0) -> int:
+    import oracle
+
+    cores = max(1, oracle.num_threads())
+    per_row = 2.0 * K * N * occ[0] * occ[1] / 0.8e9 + (K // bs) * (N // bs) * 2e-8  # work + pattern tests
+    return max(1, min(M, int(target_s * cores / per_row)))
+
+
 def auto_rows(M, N, K, target_s: float = 15.0) -> int:
     # measured on the B200 box's host cores: ~0.8 GFLOP/s per core for the plain loop incl.
     # regenerating B from the seeds (59 rows of 63,360^3 took 37 s on 16 threads)
@@ -146,10 +175,14 @@ def run_reference(args, cfg, name, world, rank):
     M, N, K, bs, path, _ = cfg
     if rank != 0:
         return
-    rows = args.cpu_rows or auto_rows(M, N, K, target_s=4.0)  # each step a bounded sample (~4 s)
+    occ = SPARSE_OCC.get(args.config)
+    if occ:
+        rows = args.cpu_rows or auto_rows_sparse(M, N, K, bs, occ, target_s=4.0)
+    else:
+        rows = args.cpu_rows or auto_rows(M, N, K, target_s=4.0)  # each step a bounded sample (~4 s)
     times = []
     for i in range(args.warmup + args.steps):
-        r = oracle_sample(M, N, K, rows)
+        r = oracle_sample_sparse(M, N, K, bs, occ, rows) if occ else oracle_sample(M, N, K, rows)
         if i >= args.warmup:
             times.append(r)
     val = statistics.mean(t["value"] for t in times)
@@ -175,8 +208,11 @@ def main():
     M, N, K, bs, dpath, cidx = cfg
     path = args.path or dpath
     name = {"s352": "352^3 bs22", "sq64": "square 63360^3 bs64", "sq22": "square 63360^3 bs22",
-            "r64": "rect 1408x1408x1982464 bs64", "r22": "rect 1408x1408x1982464 bs22"}[args.config]
-    name = f"{name} {path} (BASELINE.json configs[{cidx}])"
+            "r64": "rect 1408x1408x1982464 bs64", "r22": "rect 1408x1408x1982464 bs22",
+            "sp22": "square 63360^3 bs22 block-sparse A,B occupancy 0.1, C stored",
+            "sp64": "square 63360^3 bs64 block-sparse A,B occupancy 0.1, C stored"}[args.config]
+    occ = SPARSE_OCC.get(args.config)
+    name = f"{name} {path} " + (f"(BASELINE.json configs[{cidx}])" if cidx is not None else "(§8f-2 NEXT row)")
     if args.impl == "reference":
         return run_reference(args, (M, N, K, bs, path, cidx), name, world, rank)
 
@@ -196,7 +232,13 @@ def main():
     else:
         ctx = dbm.Context(device=local)
     stream = torch.cuda.current_stream(dev)
-    A, B, C = dbm.Matrix(ctx, M, K, bs), dbm.Matrix(ctx, K, N, bs), dbm.Matrix(ctx, M, N, bs)
+    if occ:
+        Mb, Nb, Kb = M // bs, N // bs, K // bs
+        A = dbm.Matrix(ctx, M, K, bs, mask=dbm.pattern_random(SEED, 0, Mb, Kb, occ[0]))
+        B = dbm.Matrix(ctx, K, N, bs, mask=dbm.pattern_random(SEED, 1, Kb, Nb, occ[1]))
+        C = dbm.Matrix(ctx, M, N, bs, mask=dbm.pattern_random(SEED, 2, Mb, Nb, occ[2]))
+    else:
+        A, B, C = dbm.Matrix(ctx, M, K, bs), dbm.Matrix(ctx, K, N, bs), dbm.Matrix(ctx, M, N, bs)
     A.fill_random(SEED, 0, 0)
     B.fill_random(SEED, 1, 0)
     C.fill_random(SEED, 2, 0)
@@ -232,6 +274,12 @@ def main():
     launches = ctx.launch_count() - launches0
     ms = maxrank(ev0.elapsed_time(ev1)) / args.steps
     flop = 2.0 * M * N * K
+    if occ:  # useful flops of the stored block products, summed over ranks
+        flop = st["flops"]
+        if world > 1:
+            t = torch.tensor([flop], dtype=torch.float64, device=dev)
+            dist.all_reduce(t)
+            flop = float(t.item())
     tflops = flop / (ms * 1e-3) / 1e12
     kern = "dgemm" if path == "densified" else "smm"
     prof = ctx.profile_read(dbm.K_DGEMM if path == "densified" else dbm.K_SMM)
@@ -254,7 +302,10 @@ def main():
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            cpu = oracle_sample(M, N, K, args.cpu_rows or auto_rows(M, N, K))
+            if occ:
+                cpu = oracle_sample_sparse(M, N, K, bs, occ, args.cpu_rows or auto_rows_sparse(M, N, K, bs, occ))
+            else:
+                cpu = oracle_sample(M, N, K, args.cpu_rows or auto_rows(M, N, K))
             cpu.pop("seconds", None)
         except Exception as ex:  # reported, never fatal
             cpu = {"error": str(ex)[:200]}
@@ -268,7 +319,9 @@ def main():
                        "grid": f"{ctx.pr}x{ctx.pc}", "parallelism": f"cannon{ctx.pr}x{ctx.pc}",
                        "transport": (args.transport if world > 1 else None),
                        "algorithm": (args.algorithm if world > 1 else "local"),
-                       "l2": "inputs >= 8 GB per matrix >> 126 MB L2; no flush", "alpha": alpha, "beta": beta},
+                       "l2": ("inputs >= 8 GB per matrix >> 126 MB L2; no flush" if not occ else
+                              "A, B 3.2 GB each (10 % of 32 GB) >> 126 MB L2; no flush"), "alpha": alpha, "beta": beta,
+                       "occupancy": occ},
             "pct_fp64_peak": 100.0 * tflops / (world * FP64_PEAK_MEASURED),
             "roofline": {"kernel": kern, "bound": "tensor", "achieved": achieved, "peak": FP64_PEAK_MEASURED,
                          "unit": "TFLOP/s", "frac": (achieved / FP64_PEAK_MEASURED) if achieved else None,

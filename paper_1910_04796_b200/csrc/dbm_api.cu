@@ -377,6 +377,7 @@ extern "C" dbm_status dbm_matrix_create_sparse(dbm_ctx ctx, int64_t rows, int64_
   dbm_matrix m = nullptr;
   if (dbm_status s = dbm_matrix_create(ctx, rows, cols, bs, &m)) return s;
   m->sparse = true;
+  m->device = ctx->device;
   const size_t nb = (size_t)(m->Mb * m->Nb);
   m->gmask.assign(nb, 1);
   if (mask)
@@ -593,9 +594,14 @@ extern "C" dbm_status dbm_owner_of_block(dbm_matrix m, int64_t bi, int64_t bj, i
 
 extern "C" dbm_status dbm_matrix_destroy(dbm_matrix m) {
   if (m && (m->d_ij || m->d_map)) {
-    cudaSetDevice(m->ctx->device);
+    // the context may already be destroyed: use the device recorded at creation, restore the caller's
+    int cur = 0;
+    cudaGetDevice(&cur);
+    cudaSetDevice(m->device);
     if (m->d_ij) cudaFree(m->d_ij);
     if (m->d_map) cudaFree(m->d_map);
+    cudaSetDevice(cur);
+    cudaGetLastError();
   }
   delete m;
   return DBM_OK;

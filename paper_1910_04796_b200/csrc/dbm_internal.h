@@ -168,6 +168,7 @@ struct dbm_matrix_s {
   int32_t* d_ij = nullptr;        // device (li, lj) per slot (sparse only; library-owned)
   int32_t* d_map = nullptr;       // device li*nloc + lj -> slot or -1 (sparse only; library-owned)
   uint64_t serial = 0;            // pattern identity (plan caches)
+  int device = 0;                 // CUDA device of the metadata (sparse only)
   int64_t blocks() const { return sparse ? nnz : mloc * nloc; }
   bool stored(int64_t bi, int64_t bj) const { return !sparse || gmask[(size_t)bi * Nb + bj]; }
 };

@@ -336,6 +336,114 @@ __global__ void __launch_bounds__(SpCfg<BS>::WARPS * 32, 1)
   }
 }
 
+// ---- per-run variant (bs 22): one run at a time per warp, blocks staged at their natural 22-double
+// column pitch, next entry prefetched.  Measured against the stream kernel above on one B200
+// (profiles/r01_smm_sparse_variants.jsonl): faster for bs 22 once runs hold more than a few entries
+// (21.0 vs 17.1 TFLOP/s at 11,264^3 occupancy 0.5; 17.0 vs 14.0 at 63,360^3 occupancy 0.1), slower
+// for bs 64 (21.9 vs 24.7), so bs 22 uses this one and bs 64 the stream kernel.
+template <int BS>
+struct SpRunCfg {
+  static constexpr int MT = (BS + 7) / 8;            // 8x8 subtiles per block dimension
+  static constexpr int TEAM = MT >= 4 ? 4 : 1;       // warps per run
+  static constexpr int NPW = MT / TEAM;              // n-subtiles per warp
+  static constexpr int WARPS = TEAM == 4 ? 4 : 8;    // bs 64: one 4-warp team (132 KB of stages)
+  static constexpr int TEAMS = WARPS / TEAM;
+  static constexpr int BB = BS * BS;
+  // one stage = A block (+ slack for the padded rows m >= BS) and B block (+ padded columns n >= BS)
+  static constexpr int A_D = BB + 8 * MT;
+  static constexpr int B_D = 8 * MT * BS + 8;
+  static constexpr int STAGE = ((A_D + B_D) + 1) / 2 * 2;
+  static constexpr size_t SMEM = (size_t)TEAMS * 2 * STAGE * 8;
+  static_assert(MT % TEAM == 0, "team split");
+};
+
+template <int BS>
+__global__ void __launch_bounds__(SpRunCfg<BS>::WARPS * 32, 1)
+    smm_sparse_run_kernel(const int32_t* __restrict__ trip, const int64_t* __restrict__ off, int64_t nruns,
+                      const double* __restrict__ A, const double* __restrict__ B, double* __restrict__ C,
+                      double alpha) {
+  using Cfg = SpRunCfg<BS>;
+  constexpr int MT = Cfg::MT, TEAM = Cfg::TEAM, NPW = Cfg::NPW, BB = Cfg::BB;
+  extern __shared__ __align__(16) double sm[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int team = warp / TEAM, tw = warp % TEAM;
+  const int g = lane >> 2, t = lane & 3;
+  double* st0 = sm + (size_t)team * 2 * Cfg::STAGE;
+  const int tlane = tw * 32 + lane;  // 0 .. TEAM*32-1
+  constexpr int TT = TEAM * 32;
+  // blocks are 16-byte aligned when BB is even (bs 22, 64)
+  auto load = [&](double* dst, int64_t entry) {
+    const double* a = A + (int64_t)trip[3 * entry] * BB;
+    const double* b = B + (int64_t)trip[3 * entry + 1] * BB;
+    const uint32_t sa = (uint32_t)__cvta_generic_to_shared(dst);
+    const uint32_t sb = (uint32_t)__cvta_generic_to_shared(dst + Cfg::A_D);
+    for (int i = tlane; i < BB / 2; i += TT) {
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa + 16u * i), "l"(a + 2 * i) : "memory");
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sb + 16u * i), "l"(b + 2 * i) : "memory");
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  auto team_sync = [&]() {
+    if (TEAM == 1)
+      __syncwarp();
+    else
+      asm volatile("bar.sync %0, %1;" ::"r"(1 + team), "r"(TT) : "memory");
+  };
+
+  const int64_t nteams = (int64_t)gridDim.x * Cfg::TEAMS;
+  for (int64_t run = (int64_t)blockIdx.x * Cfg::TEAMS + team; run < nruns; run += nteams) {
+    const int64_t e0 = off[run], e1 = off[run + 1];
+    if (e0 == e1) continue;
+    double acc[MT][NPW][2];
+#pragma unroll
+    for (int i = 0; i < MT; ++i)
+#pragma unroll
+      for (int j = 0; j < NPW; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    team_sync();  // the previous run's last stage has been consumed by every team warp
+    load(st0, e0);
+    for (int64_t e = e0; e < e1; ++e) {
+      double* cur = st0 + (size_t)((e - e0) & 1) * Cfg::STAGE;
+      if (e + 1 < e1) {
+        load(st0 + (size_t)((e + 1 - e0) & 1) * Cfg::STAGE, e + 1);
+        asm volatile("cp.async.wait_group 1;" ::: "memory");
+      } else {
+        asm volatile("cp.async.wait_group 0;" ::: "memory");
+      }
+      team_sync();
+      const double* sA = cur;                // (m, k) at k*BS + m
+      const double* sB = cur + Cfg::A_D;     // (k, n) at n*BS + k
+#pragma unroll
+      for (int ks = 0; ks < (BS + 3) / 4; ++ks) {
+        const int k = 4 * ks + t;
+        const bool kok = (BS % 4 == 0) || k < BS;
+        double a[MT], b[NPW];
+#pragma unroll
+        for (int mi = 0; mi < MT; ++mi) a[mi] = kok ? sA[k * BS + mi * 8 + g] : 0.0;
+#pragma unroll
+        for (int ni = 0; ni < NPW; ++ni) b[ni] = kok ? sB[((tw * NPW + ni) * 8 + g) * BS + k] : 0.0;
+#pragma unroll
+        for (int mi = 0; mi < MT; ++mi)
+#pragma unroll
+          for (int ni = 0; ni < NPW; ++ni) sp_dmma(acc[mi][ni], a[mi], b[ni]);
+      }
+      team_sync();  // every warp is done with `cur` before it is refilled
+    }
+    double* cb = C + (int64_t)trip[3 * e0 + 2] * BB;
+#pragma unroll
+    for (int mi = 0; mi < MT; ++mi)
+#pragma unroll
+      for (int ni = 0; ni < NPW; ++ni)
+#pragma unroll
+        for (int jj = 0; jj < 2; ++jj) {
+          const int m = mi * 8 + g, n = (tw * NPW + ni) * 8 + 2 * t + jj;
+          if (m < BS && n < BS) {
+            double* p = cb + m + n * BS;
+            *p = __dadd_rn(*p, __dmul_rn(alpha, acc[mi][ni][jj]));
+          }
+        }
+  }
+}
+
 // Any block size: one CTA per run, one thread per C element, FMA.
 __global__ void __launch_bounds__(256) smm_sparse_generic_kernel(int bs, const int32_t* __restrict__ trip,
                                                                  const int64_t* __restrict__ off, int64_t nruns,
@@ -373,8 +481,26 @@ __global__ void __launch_bounds__(256) smm_sparse_generic_kernel(int bs, const i
 }
 
 template <int BS>
+cudaError_t launch_sp_run(const int32_t* trip, const int64_t* off, int64_t nruns, const double* A, const double* B,
+                         double* C, double alpha, cudaStream_t st) {
+  using Cfg = SpRunCfg<BS>;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(smm_sparse_run_kernel<BS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)Cfg::SMEM);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  const int64_t ctas = (nruns + Cfg::TEAMS - 1) / Cfg::TEAMS;
+  const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(ctas, (int64_t)num_sms()));
+  smm_sparse_run_kernel<BS><<<grid, Cfg::WARPS * 32, Cfg::SMEM, st>>>(trip, off, nruns, A, B, C, alpha);
+  return cudaGetLastError();
+}
+
+template <int BS>
 cudaError_t launch_sp_tc(const int32_t* trip, const int64_t* off, int64_t nruns, const double* A, const double* B,
                          double* C, double alpha, cudaStream_t st) {
+  if (BS == 22) return launch_sp_run<BS>(trip, off, nruns, A, B, C, alpha, st);
   using Cfg = SpCfg<BS>;
   static bool attr = false;
   if (!attr) {

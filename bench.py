@@ -286,6 +286,7 @@ def main():
     prof_d = ctx.profile_read(dbm.K_DENSIFY)
     prof_u = ctx.profile_read(dbm.K_UNDENSIFY)
     prof_s = ctx.profile_read(dbm.K_STACKGEN)
+    prof_x = ctx.profile_read(dbm.K_EXCHANGE)
     per_launch_ms = prof["ms"] / max(prof["launches"], 1)
     per_launch_flop = prof["flops"] / max(prof["launches"], 1)
     achieved = per_launch_flop / (per_launch_ms * 1e-3) / 1e12 if per_launch_ms > 0 else None
@@ -339,6 +340,13 @@ def main():
                             for name, pr_ in (("densify", prof_d), ("undensify", prof_u), ("stackgen", prof_s))
                             if pr_["launches"]},
             "stats": {k: st[k] for k in ("entries", "stacks", "bytes_sent", "bytes_recv", "steps")},
+            # Cannon transport (rank 0): copy-engine pull time on the comm stream, bytes received, the
+            # achieved NVLink rate, and the step time not covered by the rank's kernels (exposed comm +
+            # barriers + gaps) = ms_per_step - sum of the phases above
+            "exchange": ({"ms_per_step": prof_x["ms"] / args.steps, "bytes_per_step": prof_x["bytes"] / args.steps,
+                          "gbs": prof_x["bytes"] / (prof_x["ms"] * 1e-3) / 1e9 if prof_x["ms"] > 0 else None,
+                          "uncovered_ms_per_step": ms - (prof["ms"] + prof_d["ms"] + prof_u["ms"] + prof_s["ms"])
+                          / args.steps} if world > 1 else None),
             "gpu_launches": launches,
             "clocks": clk.summary(),
             "e2e": e2e,

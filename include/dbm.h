@@ -104,7 +104,8 @@ dbm_status dbm_ctx_sync(dbm_ctx ctx);
  * is bracketed by CUDA events on its own stream.  dbm_ctx_profile_read() synchronises,
  * returns the summed device time, launch count and algorithmic flops of the recorded
  * launches of `kernel` (0 = dense GEMM, 1 = small-block GEMM, 2 = densify, 3 = undensify,
- * 4 = stack generation) and clears the records. bytes_out: algorithmic bytes. */
+ * 4 = stack generation, 5 = the copy-engine panel pulls of one exchange step, timed on the comm
+ * stream) and clears the records. bytes_out: algorithmic bytes (kernel 5: bytes received). */
 dbm_status dbm_ctx_set_profiling(dbm_ctx ctx, int on);
 dbm_status dbm_ctx_profile_read(dbm_ctx ctx, int kernel, double* ms_out, int64_t* launches_out, double* flops_out,
                                 double* bytes_out);

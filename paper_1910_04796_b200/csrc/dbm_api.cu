@@ -687,6 +687,24 @@ struct Plan {
 
 size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 
+// K-chunk boundaries (blocks) of a transfer -> GEMM pipeline whose first transfer nothing hides (Cannon's
+// step 0, the tall-and-skinny gather): chunks grow geometrically, 1, 1, 2, 4, 8 sixteenths of kb, so
+// the exposed first pull is 1/16 of the panel and every later pull (at most twice the previous
+// chunk) moves while the previous chunk's GEMM runs — the copy engines move a K-column about twice as
+// fast as the GEMM consumes it on the thin rectangular shapes, where this matters.
+std::vector<int64_t> pipeline_chunks(int64_t kb) {
+  std::vector<int64_t> b{0};
+  int64_t acc = 0;
+  for (int64_t part : {1, 1, 2, 4, 8}) {
+    acc += part;
+    const int64_t v = kb * acc / 16;
+    if (v > b.back()) b.push_back(v);
+  }
+  if (b.back() != kb) b.push_back(kb);
+  return b;
+}
+constexpr int kMaxChunks = 6;
+
 constexpr int64_t kDefaultChunkBytes = 16ll << 30;   // A+B dense chunk budget (single rank)
 // Triplets per stack-generation chunk (<= 6.4 GB): large enough that one smm launch has thousands
 // of 8-run groups for 148 SMs even with the 90,112-long runs of the rectangular bs-22 config.
@@ -738,8 +756,12 @@ Plan make_plan_raw(int nranks, int pr, int pc, int r, int c, int64_t Mb, int64_t
         if (k % p.pc == p.c) p.ownA_off[k] = take(p.a_panel_bytes(k));
         if (k % p.pr == p.r) p.ownB_off[k] = take(p.b_panel_bytes(k));
       }
-      for (int s = 0; s < p.L; ++s)
+      for (int s = 0; s < p.L; ++s) {
         p.max_split = std::max(p.max_split, pick_splitk(M, N, p.kb[p.kappa(s)] * p.bs, num_sms()));
+        const std::vector<int64_t> b = pipeline_chunks(p.kb[p.kappa(s)]);  // step 0 may be chunked
+        for (size_t j = 1; j < b.size(); ++j)
+          p.max_split = std::max(p.max_split, pick_splitk(M, N, (b[j] - b[j - 1]) * p.bs, num_sms()));
+      }
     }
     if (p.max_split > 1) p.off_part = take((size_t)p.max_split * M * N * 8);
   } else {
@@ -1114,7 +1136,9 @@ TSPlan make_ts_plan(int pr, int pc, int r, int c, int64_t Mb, int64_t Nb, int64_
   t.off_cpart = take((size_t)t.Mtot * t.Ntot * 8);
   t.off_cstack = take((size_t)t.P * t.mrows[r] * t.ncols[c] * 8);
   const int64_t K = t.kp[t.me] * bs;
-  for (int j = 0; j < 4; ++j) t.max_split = std::max(t.max_split, pick_splitk(t.Mtot, t.Ntot, (K + 3) / 4 + bs, num_sms()));
+  const std::vector<int64_t> cb = pipeline_chunks(t.kp[t.me]);
+  for (size_t j = 1; j < cb.size(); ++j)
+    t.max_split = std::max(t.max_split, pick_splitk(t.Mtot, t.Ntot, (cb[j] - cb[j - 1]) * bs, num_sms()));
   t.max_split = std::max(t.max_split, pick_splitk(t.Mtot, t.Ntot, K, num_sms()));
   if (t.max_split > 1) t.off_part = take((size_t)t.max_split * t.Mtot * t.Ntot * 8);
   t.total = std::max<size_t>(off, 256);
@@ -1178,14 +1202,20 @@ dbm_status multiply_tallskinny(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_matr
 
   // ---- gather A[:, S_me] and B[S_me, :] in K-chunks on the comm stream, GEMM chunks on the compute stream
   const int64_t kb = t.kp[t.me], ldp = t.ld(t.me);
-  const int nsub = bs % 2 ? 1 : (int)std::max<int64_t>(1, std::min<int64_t>(4, kb));  // chunks keep 16-B TMA bases
+  // chunks keep 16-B TMA bases when bs is even
+  const std::vector<int64_t> cb = bs % 2 ? std::vector<int64_t>{0, kb} : pipeline_chunks(kb);
+  const int nsub = (int)cb.size() - 1;
   char* afull = ws + t.off_afull;
   char* bfull = ws + t.off_bfull;
   double* cpart = (double*)(ws + t.off_cpart);
-  cudaEvent_t ev_c[4] = {nullptr, nullptr, nullptr, nullptr};
+  cudaEvent_t ev_c[kMaxChunks] = {};
   const int rb = t.me % t.pr;
+  int64_t ts_recv = 0, ts_sent = 0;
+  ts_bytes(t, &ts_recv, &ts_sent);
+  ts_recv -= (int64_t)(t.P - 1) * t.mrows[t.r] * t.ncols[t.c] * 8;  // the C-share pulls run later, on cs
+  ProfScope ps_x(ctx, ctx->comm, 5, 0.0, (double)ts_recv);  // the A / B gathers on the copy engines
   for (int j = 0; j < nsub && kb > 0; ++j) {
-    const int64_t k0 = kb * j / nsub, k1 = kb * (j + 1) / nsub;
+    const int64_t k0 = cb[j], k1 = cb[j + 1];
     const size_t off = (size_t)(k0 * bs) * 8, width = (size_t)((k1 - k0) * bs) * 8;
     for (int rr = 0; rr < t.pr; ++rr) {  // rows of grid row rr from rank (rr, c), its piece for target row r
       const int q = rr * t.pc + t.c;
@@ -1206,7 +1236,7 @@ dbm_status multiply_tallskinny(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_matr
     CUDA_TRY(ctx, cudaEventRecord(ev_c[j], ctx->comm));
   }
   for (int j = 0; j < nsub; ++j) {
-    const int64_t k0 = kb * j / nsub, k1 = kb * (j + 1) / nsub;
+    const int64_t k0 = cb[j], k1 = cb[j + 1];
     if (kb > 0) CUDA_TRY(ctx, cudaStreamWaitEvent(cs, ev_c[j], 0));
     GemmArgs g{t.Mtot, t.Ntot, (k1 - k0) * bs, (const double*)afull + k0 * bs, ldp, (const double*)bfull + k0 * bs,
                ldp, cpart, t.Mtot, 1.0, j == 0 ? 0.0 : 1.0, 1, nullptr};
@@ -1242,7 +1272,7 @@ dbm_status multiply_tallskinny(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_matr
   ts_bytes(t, &st->bytes_recv, &st->bytes_sent);
   st->steps = 1;
   ctx->ev_pool.push_back(ev_ready);
-  for (int j = 0; j < 4; ++j)
+  for (int j = 0; j < kMaxChunks; ++j)
     if (ev_c[j]) ctx->ev_pool.push_back(ev_c[j]);
   return DBM_OK;
 }
@@ -1603,6 +1633,8 @@ dbm_status multiply_sparse_blocked(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_
   std::vector<int> bufA(L, -1), bufB(L, -1);
   auto pulls = [&](int s) -> dbm_status {
     const SpStep& x = sc->steps[s];
+    ProfScope ps(ctx, ctx->comm, 5, 0.0,
+                 (double)(((x.a_src != me) ? x.a_nnz : 0) + ((x.b_src != me) ? x.b_nnz : 0)) * bb * 8);
     if (x.a_src != me && x.a_nnz) {
       CUDA_TRY(ctx, cudaMemcpyAsync(ws + sc->off_recvA[bufA[s]], ctx->peer_ws[x.a_src] + sc->peer_ownA_off[x.a_src][x.kappa],
                                     (size_t)x.a_nnz * bb * 8, cudaMemcpyDeviceToDevice, ctx->comm));
@@ -1968,10 +2000,18 @@ dbm_status multiply_impl(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_matrix B, 
   int bufA_of[64], bufB_of[64];
   std::vector<Plan> peer_plan;
   int nsub0 = 1;               // K-chunks of the step-0 pull (copy-engine transport, densified)
-  cudaEvent_t ev_c[4] = {nullptr, nullptr, nullptr, nullptr};
+  cudaEvent_t ev_c[kMaxChunks] = {};
+  std::vector<int64_t> cb0{0, 0};
+  auto recv_bytes = [&](int s) {
+    double n = 0;
+    for (const XOp& op : exchange_ops(p, s)) n += op.send ? 0 : (double)op.bytes;
+    return n;
+  };
   auto exchange = [&](int s) -> dbm_status {
-    if (ctx->transport == 0)
+    if (ctx->transport == 0) {
+      ProfScope ps(ctx, ctx->comm, 5, 0.0, recv_bytes(s));  // copy-engine pulls of this step
       return post_pulls(ctx, p, peer_plan, s, ws, bufA_of[s], bufB_of[s], &st.bytes_sent, &st.bytes_recv);
+    }
     return post_exchange(ctx, p, s, ws, A->arena, B->arena, bufA_of[s], bufB_of[s], &st.bytes_sent, &st.bytes_recv);
   };
   if (ctx->nranks > 1) {
@@ -2001,12 +2041,16 @@ dbm_status multiply_impl(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_matrix B, 
     // the first chunk's transfer is exposed.
     bool remote0 = p.a_src(0) != p.me() || p.b_src(0) != p.me();
     const int64_t kb0 = p.kb[p.kappa(0)];
-    if (ctx->transport == 0 && dens && remote0 && bs % 2 == 0 && kb0 >= 2) nsub0 = (int)std::min<int64_t>(4, kb0);
+    if (ctx->transport == 0 && dens && remote0 && bs % 2 == 0 && kb0 >= 2) {
+      cb0 = pipeline_chunks(kb0);
+      nsub0 = (int)cb0.size() - 1;
+    }
     if (nsub0 > 1) {
+      ProfScope ps(ctx, ctx->comm, 5, 0.0, recv_bytes(0));
       for (int j = 0; j < nsub0; ++j) {
         ev_c[j] = get_event(ctx);
-        if (dbm_status e = post_pulls_chunk(ctx, p, peer_plan, 0, ws, bufA_of[0], bufB_of[0], kb0 * j / nsub0,
-                                            kb0 * (j + 1) / nsub0, j == 0, &st.bytes_sent, &st.bytes_recv))
+        if (dbm_status e = post_pulls_chunk(ctx, p, peer_plan, 0, ws, bufA_of[0], bufB_of[0], cb0[j], cb0[j + 1],
+                                            j == 0, &st.bytes_sent, &st.bytes_recv))
           return e;
         CUDA_TRY(ctx, cudaEventRecord(ev_c[j], ctx->comm));
       }
@@ -2057,7 +2101,7 @@ dbm_status multiply_impl(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_matrix B, 
             launches += 2;
           }
           GemmArgs g{M, N, nk * bs, Ad, ld, Bd, ld, Cd, M, 1.0, ch == 0 ? 0.0 : 1.0, 1, nullptr};
-          g.splitk = pick_splitk(M, N, g.K, num_sms());
+          g.splitk = std::min(pick_splitk(M, N, g.K, num_sms()), p.max_split);  // partial buffer bound
           g.partial = g.splitk > 1 ? (double*)(ws + p.off_part) : nullptr;
           {
             ProfScope ps(ctx, cs, 0, 2.0 * M * N * g.K, 8.0 * (M * g.K + N * g.K + M * N * (ch ? 2 : 1)));
@@ -2072,11 +2116,11 @@ dbm_status multiply_impl(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_matrix B, 
         const int64_t ld = p.ld_panel(k);
         const int nsub = (s == 0) ? nsub0 : 1;
         for (int j = 0; j < nsub; ++j) {
-          const int64_t k0 = kbk * j / nsub, k1 = kbk * (j + 1) / nsub;
+          const int64_t k0 = nsub > 1 ? cb0[j] : 0, k1 = nsub > 1 ? cb0[j + 1] : kbk;
           if (nsub > 1) CUDA_TRY(ctx, cudaStreamWaitEvent(cs, ev_c[j], 0));
           GemmArgs g{M, N, (k1 - k0) * bs, Ap + k0 * bs, ld, Bp + k0 * bs, ld, Cd, M, 1.0,
                      (s == 0 && j == 0) ? 0.0 : 1.0, 1, nullptr};
-          g.splitk = pick_splitk(M, N, g.K, num_sms());
+          g.splitk = std::min(pick_splitk(M, N, g.K, num_sms()), p.max_split);  // partial buffer bound
           g.partial = g.splitk > 1 ? (double*)(ws + p.off_part) : nullptr;
           ProfScope ps(ctx, cs, 0, 2.0 * M * N * g.K,
                        8.0 * (M * g.K + N * g.K + M * N * ((s == 0 && j == 0) ? 1 : 2)));

@@ -23,7 +23,7 @@ _PATHS = {"blocked": PATH_BLOCKED, "densified": PATH_DENSIFIED, "auto": PATH_AUT
           PATH_DENSIFIED: 1, PATH_AUTO: 2}
 
 # dbm_ctx_profile_read kernel ids
-K_DGEMM, K_SMM, K_DENSIFY, K_UNDENSIFY, K_STACKGEN = 0, 1, 2, 3, 4
+K_DGEMM, K_SMM, K_DENSIFY, K_UNDENSIFY, K_STACKGEN, K_EXCHANGE = 0, 1, 2, 3, 4, 5
 
 
 class DbmError(RuntimeError):

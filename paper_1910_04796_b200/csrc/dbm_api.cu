@@ -693,6 +693,7 @@ size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 // chunk) moves while the previous chunk's GEMM runs — the copy engines move a K-column about twice as
 // fast as the GEMM consumes it on the thin rectangular shapes, where this matters.
 std::vector<int64_t> pipeline_chunks(int64_t kb) {
+  if (kb <= 0) return {0, 0};  // one empty chunk: its K = 0 GEMM still writes (zeros) the partial
   std::vector<int64_t> b{0};
   int64_t acc = 0;
   for (int64_t part : {1, 1, 2, 4, 8}) {

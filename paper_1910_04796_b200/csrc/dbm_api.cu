@@ -1174,21 +1174,26 @@ dbm_status multiply_tallskinny(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_matr
   const TSPlan t = make_ts_plan(ctx->pr, ctx->pc, ctx->myrow, ctx->mycol, A->Mb, B->Nb, A->Nb, A->bs);
   cudaStream_t cs = ctx->stream;
   const int64_t bs = t.bs, P = t.P;
-  // ---- own pieces (densified once; peers pull them)
+  // ---- own pieces (densified once; peers pull them).  The pieces this rank needs itself are densified
+  // straight into its A_full / B_full: a local device-to-device copy would run on SMs and wait behind
+  // the persistent GEMM (measured: 23 GB/s under a GEMM vs 750 GB/s for the peer pulls on the copy
+  // engines, tools/microbench/ce_copy.py).
   for (int tr = 0; tr < t.pr; ++tr) {
     const int q = tr * t.pc + t.c;
     if (!t.kp[q] || !t.mrows[t.r]) continue;
+    double* dst = q == t.me ? (double*)(ws + t.off_afull) + (size_t)t.rowoff[t.r] * t.ld(q)
+                            : (double*)(ws + t.offApiece[tr]);
     ProfScope ps(ctx, cs, 2, 0.0, 16.0 * t.mrows[t.r] * t.kp[q] * bs);
-    if (dbm_status e = densify_a(ctx, A, tr, t.pr, t.kp[q], (double*)(ws + t.offApiece[tr]), t.ld(q), 1, cs))
-      return e;
+    if (dbm_status e = densify_a(ctx, A, tr, t.pr, t.kp[q], dst, t.ld(q), 1, cs)) return e;
     ++*launches;
   }
   for (int tt = 0; tt < t.pc; ++tt) {
     const int q = t.r + tt * t.pr;
     if (!t.kp[q] || !t.ncols[t.c]) continue;
+    double* dst = q == t.me ? (double*)(ws + t.off_bfull) + (size_t)t.coloff[t.c] * t.ld(q)
+                            : (double*)(ws + t.offBpiece[tt]);
     ProfScope ps(ctx, cs, 2, 0.0, 16.0 * t.ncols[t.c] * t.kp[q] * bs);
-    if (dbm_status e = densify_b(ctx, B, tt, t.pc, t.kp[q], (double*)(ws + t.offBpiece[tt]), t.ld(q), 0, cs))
-      return e;
+    if (dbm_status e = densify_b(ctx, B, tt, t.pc, t.kp[q], dst, t.ld(q), 0, cs)) return e;
     ++*launches;
   }
   CUDA_TRY(ctx, cudaGetLastError());
@@ -1220,16 +1225,16 @@ dbm_status multiply_tallskinny(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_matr
     const size_t off = (size_t)(k0 * bs) * 8, width = (size_t)((k1 - k0) * bs) * 8;
     for (int rr = 0; rr < t.pr; ++rr) {  // rows of grid row rr from rank (rr, c), its piece for target row r
       const int q = rr * t.pc + t.c;
-      if (!t.mrows[rr]) continue;
-      const char* src = (q == t.me ? ws : ctx->peer_ws[q]) + (q == t.me ? t.offApiece[t.r] : peer[q].offApiece[t.r]);
+      if (!t.mrows[rr] || q == t.me) continue;  // my own rows are already in place
+      const char* src = ctx->peer_ws[q] + peer[q].offApiece[t.r];
       CUDA_TRY(ctx, cudaMemcpy2DAsync(afull + (size_t)t.rowoff[rr] * ldp * 8 + off, ldp * 8, src + off, ldp * 8, width,
                                       t.mrows[rr], cudaMemcpyDeviceToDevice, ctx->comm));
     }
     for (int cc = 0; cc < t.pc; ++cc) {  // columns of grid column cc from rank (rb, cc), its piece for target me
       const int q = rb * t.pc + cc;
-      if (!t.ncols[cc]) continue;
+      if (!t.ncols[cc] || q == t.me) continue;
       const int tt = (t.me - rb) / t.pr;
-      const char* src = base_of(q) + (q == t.me ? t.offBpiece[tt] : peer[q].offBpiece[tt]);
+      const char* src = ctx->peer_ws[q] + peer[q].offBpiece[tt];
       CUDA_TRY(ctx, cudaMemcpy2DAsync(bfull + (size_t)t.coloff[cc] * ldp * 8 + off, ldp * 8, src + off, ldp * 8, width,
                                       t.ncols[cc], cudaMemcpyDeviceToDevice, ctx->comm));
     }

@@ -4,6 +4,7 @@
 // Bound: HBM.  Algorithmic bytes: densify 16 B/element, undensify 24 B/element (16 if beta == 0),
 // pack 16 B/element.
 #include <algorithm>
+#include <cstdlib>
 
 #include "dbm_internal.h"
 
@@ -159,16 +160,19 @@ __global__ void pack_blocks_kernel(const double* __restrict__ arena, int64_t nse
 // ---- fast paths for the paper's block sizes (compile-time BS: no 64-bit divisions, 16-B accesses) ----
 // B panel, column-major: dense[(lj*BS+y)*ld + q*BS+x] = block(krow0+q*kstride, lj)[x + y*BS].
 // One thread per (x, x+1) pair; CTAs walk blocks b = q*nloc + lj (block-contiguous reads,
-// column-run writes of BS doubles).
+// column-run writes of BS doubles), or lj-major b = lj*nk + q when the panel has few block columns
+// and very long rows (the rectangular configs: 22 columns, rows of 6 MB), so the blocks in flight
+// write a few dense rows instead of every row of the panel.
 template <int BS>
 __global__ void __launch_bounds__(256) densify_b_fast(const double* __restrict__ arena, int nloc, int64_t krow0,
                                                       int64_t kstride, int nblk, double* __restrict__ dense,
-                                                      int64_t ld) {
+                                                      int64_t ld, int lj_major) {
   constexpr int BB = BS * BS, PAIRS = BB / 2;
+  const int nk = nblk / nloc;
   for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < (int64_t)nblk * PAIRS;
        w += (int64_t)gridDim.x * blockDim.x) {
     const int b = (int)(w / PAIRS), i = 2 * (int)(w - (int64_t)b * PAIRS);
-    const int q = b / nloc, lj = b - q * nloc;
+    const int q = lj_major ? b % nk : b / nloc, lj = lj_major ? b / nk : b - (b / nloc) * nloc;
     const int y = i / BS, x = i - y * BS;
     const double2 v = *(const double2*)(arena + ((krow0 + q * kstride) * nloc + lj) * BB + i);
     *(double2*)(dense + ((int64_t)lj * BS + y) * ld + (int64_t)q * BS + x) = v;
@@ -308,12 +312,14 @@ void launch_densify_rows(const double* arena, int64_t nloc, int bs, int64_t krow
   if (total == 0) return;
   if (layout == 0 && fast_ok(bs, ld, arena, dense) && nk * nloc < (1ll << 31)) {
     const int nblk = (int)(nk * nloc);
+    static const char* env = getenv("DBM_DENSIFY_B_ORDER");  // measurement override: "q" / "lj"
+    const int ljm = env ? (env[0] == 'l') : (nloc < 64 && nk >= 4 * nloc);
     if (bs == 22)
       densify_b_fast<22><<<grid_pairs((int64_t)nblk * 242), 256, 0, st>>>(arena, (int)nloc, krow0, kstride, nblk,
-                                                                         dense, ld);
+                                                                         dense, ld, ljm);
     else
       densify_b_fast<64><<<grid_pairs((int64_t)nblk * 2048), 256, 0, st>>>(arena, (int)nloc, krow0, kstride, nblk,
-                                                                          dense, ld);
+                                                                          dense, ld, ljm);
     return;
   }
   densify_rows_kernel<<<grid_for(total), kThreads, 0, st>>>(arena, nloc, bs, krow0, kstride, nk, dense, ld, layout);

@@ -55,6 +55,32 @@ def main():
                                                     ct.c_size_t(width), ct.c_size_t(rows), D2D, sp), s)
             out.append({"src": name, "kind": "2d", "rows": rows, "width_bytes": width, "bytes": width * rows, "ms": ms,
                         "gbs": width * rows / ms / 1e6})
+    # the same copies while an FP64 GEMM occupies every SM on another stream (as in the Cannon pipeline)
+    busy = torch.cuda.Stream(0)
+    x = torch.randn(8192, 8192, dtype=torch.float64, device="cuda:0")
+    for name, sbuf in (("peer", src), ("local", loc)):
+        for kind, width in (("1d", None), ("2d", (pitch_el // 4) // 2 * 2 * 8)):
+            nbytes = rows * pitch_el * 8 // 4 if kind == "1d" else width * rows
+            def cp():
+                if kind == "1d":
+                    rt.cudaMemcpyAsync(ct.c_void_p(dst.data_ptr()), ct.c_void_p(sbuf.data_ptr()), ct.c_size_t(nbytes),
+                                       D2D, sp)
+                else:
+                    rt.cudaMemcpy2DAsync(ct.c_void_p(dst.data_ptr()), ct.c_size_t(pitch_el * 8),
+                                         ct.c_void_p(sbuf.data_ptr()), ct.c_size_t(pitch_el * 8), ct.c_size_t(width),
+                                         ct.c_size_t(rows), D2D, sp)
+            torch.cuda.synchronize()
+            with torch.cuda.stream(busy):
+                for _ in range(3):
+                    y = x @ x  # ~90 ms of DGEMM
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(s)
+            cp()
+            e1.record(s)
+            torch.cuda.synchronize()
+            ms = e0.elapsed_time(e1)
+            out.append({"src": name, "kind": kind, "under_gemm": True, "bytes": nbytes, "ms": ms, "gbs": nbytes / ms / 1e6})
+            del y
     for o in out:
         print(json.dumps(o), flush=True)
 

@@ -36,15 +36,21 @@ def main():
     B.fill_random(1910, 1, 0)
     C.fill_random(1910, 2, 0)
     for i in range(a.reps):
+        ctx.set_profiling(i == a.reps - 1)  # phase times of the last repetition
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
         st = dbm.multiply(ctx, 1.0, A, B, 0.0, C, a.path)
         e1.record()
         torch.cuda.synchronize()
         ms = e0.elapsed_time(e1)
+        ctx.set_profiling(False)
+        phases = {n: ctx.profile_read(k)["ms"] for n, k in (("gemm", dbm.K_DGEMM), ("smm", dbm.K_SMM),
+                                                             ("densify", dbm.K_DENSIFY), ("undensify", dbm.K_UNDENSIFY),
+                                                             ("stackgen", dbm.K_STACKGEN))}
         eff = st["flops"] if a.occ is not None else 2.0 * a.M * a.N * a.K
         print(json.dumps({"M": a.M, "N": a.N, "K": a.K, "bs": a.bs, "path": a.path, "occ": a.occ, "rep": i, "ms": ms,
-                          "tflops": eff / ms / 1e9, "entries": st["entries"], "stacks": st["stacks"]}), flush=True)
+                          "tflops": eff / ms / 1e9, "entries": st["entries"], "stacks": st["stacks"],
+                          "phases_ms": phases}), flush=True)
 
 
 if __name__ == "__main__":

@@ -313,7 +313,7 @@ void launch_densify_rows(const double* arena, int64_t nloc, int bs, int64_t krow
   if (layout == 0 && fast_ok(bs, ld, arena, dense) && nk * nloc < (1ll << 31)) {
     const int nblk = (int)(nk * nloc);
     static const char* env = getenv("DBM_DENSIFY_B_ORDER");  // measurement override: "q" / "lj"
-    const int ljm = env ? (env[0] == 'l') : (nloc < 64 && nk >= 4 * nloc);
+    const int ljm = env ? (env[0] == 'l') : (nloc <= 128 && nk >= 4 * nloc);
     if (bs == 22)
       densify_b_fast<22><<<grid_pairs((int64_t)nblk * 242), 256, 0, st>>>(arena, (int)nloc, krow0, kstride, nblk,
                                                                          dense, ld, ljm);

@@ -1788,7 +1788,26 @@ struct HostIO {
   double* C = nullptr;
   std::vector<cudaEvent_t> chunk_ev;
   cudaEvent_t all_ev = nullptr, c_ev = nullptr;
+  std::vector<cudaEvent_t> panel_ev;  // C row panels ready for their download
+  bool c_downloaded = false;          // the multiply already enqueued C's download
 };
+
+namespace {
+// Single-rank densified K-chunks (block boundaries).  Device-resident operands: uniform chunks of the
+// dense-buffer budget.  Host-resident operands (dbm_multiply_host): the chunks start at 1/16 of K and
+// double up to the budget, so only a small first upload is exposed; every later upload (PCIe, ~12x
+// faster per K-block than the GEMM consumes it at 63,360^3) runs under the previous chunks' GEMMs.
+std::vector<int64_t> k_chunks(int64_t Kb, int64_t budget, bool host_io) {
+  std::vector<int64_t> b{0};
+  int64_t step = host_io ? std::max<int64_t>(1, Kb / 16) : budget;
+  while (b.back() < Kb) {
+    b.push_back(std::min(Kb, b.back() + std::min(step, budget)));
+    if (host_io) step *= 2;
+  }
+  if (b.size() == 1) b.push_back(0);
+  return b;
+}
+}  // namespace
 
 namespace {
 dbm_status multiply_impl(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_matrix B, double beta, dbm_matrix C,
@@ -1829,11 +1848,13 @@ extern "C" dbm_status dbm_multiply_host(dbm_ctx ctx, double alpha, dbm_matrix A,
   hio.C = (double*)C_host;
   dbm_status e = multiply_impl(ctx, alpha, A, B, beta, C, path, stack_cap, workspace, ws_bytes, stats, &hio);
   for (cudaEvent_t ev : hio.chunk_ev) ctx->ev_pool.push_back(ev);
+  for (cudaEvent_t ev : hio.panel_ev) ctx->ev_pool.push_back(ev);
   if (hio.all_ev) ctx->ev_pool.push_back(hio.all_ev);
   if (hio.c_ev) ctx->ev_pool.push_back(hio.c_ev);
   if (e) return e;
   const size_t cbytes = (size_t)C->blocks() * C->bs * C->bs * 8;
-  if (cbytes) CUDA_TRY(ctx, cudaMemcpyAsync(C_host, C->arena, cbytes, cudaMemcpyDeviceToHost, ctx->stream));
+  if (cbytes && !hio.c_downloaded)
+    CUDA_TRY(ctx, cudaMemcpyAsync(C_host, C->arena, cbytes, cudaMemcpyDeviceToHost, ctx->stream));
   return DBM_OK;
 }
 
@@ -1907,8 +1928,9 @@ dbm_status multiply_impl(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_matrix B, 
     const size_t bb8 = (size_t)p.bs * p.bs * 8;
     const bool chunked = ctx->nranks == 1 && dens && alpha != 0.0 && p.Kb > 0 && !A->sparse && !B->sparse;
     if (chunked) {
-      for (int64_t ch = 0; ch < p.nchunks; ++ch) {
-        const int64_t k0 = ch * p.chunk_kb, nk = std::min(p.chunk_kb, p.Kb - k0);
+      const std::vector<int64_t> kc = k_chunks(p.Kb, p.chunk_kb, true);
+      for (size_t ch = 0; ch + 1 < kc.size(); ++ch) {
+        const int64_t k0 = kc[ch], nk = kc[ch + 1] - kc[ch];
         if (p.mloc && nk)
           CUDA_TRY(ctx, cudaMemcpy2DAsync((char*)A->arena + k0 * bb8, p.kA * bb8, (const char*)hio->A + k0 * bb8,
                                           p.kA * bb8, nk * bb8, p.mloc, cudaMemcpyHostToDevice, cp));
@@ -2093,8 +2115,14 @@ dbm_status multiply_impl(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_matrix B, 
       double* Cd = (double*)(ws + p.off_cd);
       if (ctx->nranks == 1) {
         // K-chunked: densify chunk -> GEMM accumulate
-        for (int64_t ch = 0; ch < p.nchunks; ++ch) {
-          const int64_t k0 = ch * p.chunk_kb, nk = std::min(p.chunk_kb, p.Kb - k0);
+        const bool hchunk = hio && !A->sparse && !B->sparse;
+        const std::vector<int64_t> kc = k_chunks(p.Kb, p.chunk_kb, hchunk);
+        const int64_t nch = (int64_t)kc.size() - 1;
+        // host C: the last chunk's GEMM runs in row panels, each undensified and downloaded while the
+        // next panel multiplies, so only the last panel's download is exposed
+        const int npan = (hchunk && !C->sparse && p.mloc >= 8) ? 8 : 1;
+        for (int64_t ch = 0; ch < nch; ++ch) {
+          const int64_t k0 = kc[ch], nk = kc[ch + 1] - kc[ch];
           const int64_t ld = round_up(p.chunk_kb * bs, 2);
           double* Ad = (double*)(ws + p.off_ownA);
           double* Bd = (double*)(ws + p.off_ownB);
@@ -2106,17 +2134,44 @@ dbm_status multiply_impl(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_matrix B, 
             if (dbm_status e = densify_b(ctx, B, k0, 1, nk, Bd, ld, 0, cs)) return e;
             launches += 2;
           }
-          GemmArgs g{M, N, nk * bs, Ad, ld, Bd, ld, Cd, M, 1.0, ch == 0 ? 0.0 : 1.0, 1, nullptr};
-          g.splitk = std::min(pick_splitk(M, N, g.K, num_sms()), p.max_split);  // partial buffer bound
-          g.partial = g.splitk > 1 ? (double*)(ws + p.off_part) : nullptr;
-          {
-            ProfScope ps(ctx, cs, 0, 2.0 * M * N * g.K, 8.0 * (M * g.K + N * g.K + M * N * (ch ? 2 : 1)));
-            CUDA_TRY(ctx, launch_dgemm(g, cs, &launches));
+          const int pans = (ch == nch - 1) ? npan : 1;
+          for (int pn = 0; pn < pans; ++pn) {
+            const int64_t li0 = p.mloc * pn / pans, li1 = p.mloc * (pn + 1) / pans, m0 = li0 * bs, mr = (li1 - li0) * bs;
+            GemmArgs g{mr, N, nk * bs, Ad + m0 * ld, ld, Bd, ld, Cd + m0, M, 1.0, ch == 0 ? 0.0 : 1.0, 1, nullptr};
+            g.splitk = std::min(pick_splitk(g.M, N, g.K, num_sms()), p.max_split);  // partial buffer bound
+            g.partial = g.splitk > 1 ? (double*)(ws + p.off_part) : nullptr;
+            {
+              ProfScope ps(ctx, cs, 0, 2.0 * mr * N * g.K, 8.0 * (mr * g.K + N * g.K + mr * N * (ch ? 2 : 1)));
+              CUDA_TRY(ctx, launch_dgemm(g, cs, &launches));
+            }
+            ++st.gemm_launches;
+            if (pans > 1) {  // undensify this row panel, then download it on the copy stream
+              if (pn == 0 && hio->c_ev) CUDA_TRY(ctx, cudaStreamWaitEvent(cs, hio->c_ev, 0));  // C_in uploaded
+              {
+                ProfScope ps(ctx, cs, 3, 0.0, (beta == 0.0 ? 16.0 : 24.0) * mr * N);
+                launch_undensify(Cd + m0, M, 1, 0, li1 - li0, p.nloc, (int)bs, alpha, beta,
+                                 C->arena + li0 * p.nloc * bb, cs);
+                ++launches;
+              }
+              cudaEvent_t e = get_event(ctx);
+              CUDA_TRY(ctx, cudaEventRecord(e, cs));
+              hio->panel_ev.push_back(e);
+              CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->comm, e, 0));
+              const size_t off = (size_t)(li0 * p.nloc) * bb * 8, n = (size_t)((li1 - li0) * p.nloc) * bb * 8;
+              if (n) CUDA_TRY(ctx, cudaMemcpyAsync((char*)hio->C + off, (const char*)C->arena + off, n,
+                                                   cudaMemcpyDeviceToHost, ctx->comm));
+              hio->c_downloaded = true;
+            }
           }
-          ++st.gemm_launches;
           ++st.entries;
           ++st.stacks;
-          st.flops += 2.0 * M * N * g.K;
+          st.flops += 2.0 * M * N * nk * bs;
+        }
+        if (hio && hio->c_downloaded) {  // the call ends when C is on the host
+          cudaEvent_t e = get_event(ctx);
+          CUDA_TRY(ctx, cudaEventRecord(e, ctx->comm));
+          hio->panel_ev.push_back(e);
+          CUDA_TRY(ctx, cudaStreamWaitEvent(cs, e, 0));
         }
       } else {
         const int64_t ld = p.ld_panel(k);
@@ -2177,7 +2232,7 @@ dbm_status multiply_impl(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_matrix B, 
     // the comm stream's last op covers every transfer of this rank
     CUDA_TRY(ctx, cudaStreamWaitEvent(cs, ev_x[p.L - 1], 0));
   }
-  if (dens && M * N > 0) {
+  if (dens && M * N > 0 && !(hio && hio->c_downloaded)) {
     if (hio && hio->c_ev) CUDA_TRY(ctx, cudaStreamWaitEvent(cs, hio->c_ev, 0));  // C_in uploaded
     ProfScope ps(ctx, cs, 3, 0.0, (beta == 0.0 ? 16.0 : 24.0) * M * N);
     undensify_c(C, (double*)(ws + p.off_cd), M, 1, 0, alpha, beta, cs);

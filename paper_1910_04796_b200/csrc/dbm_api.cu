@@ -688,23 +688,28 @@ struct Plan {
 size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 
 // K-chunk boundaries (blocks) of a transfer -> GEMM pipeline whose first transfer nothing hides (Cannon's
-// step 0, the tall-and-skinny gather): chunks grow geometrically, 1, 1, 2, 4, 8 sixteenths of kb, so
-// the exposed first pull is 1/16 of the panel and every later pull (at most twice the previous
-// chunk) moves while the previous chunk's GEMM runs — the copy engines move a K-column about twice as
-// fast as the GEMM consumes it on the thin rectangular shapes, where this matters.
-std::vector<int64_t> pipeline_chunks(int64_t kb) {
+// step 0, the tall-and-skinny gather).  The first chunk is 1/16 of kb and each next one is `growth`
+// times larger: the pull of chunk j+1 (copy engines, ~600 GB/s from a peer) must fit under the GEMM of
+// chunk j, i.e. growth <= (GEMM time per K-block) / (pull time per K-block) = pipeline_growth(); a
+// rank that pulls both operands of a thin 704 x 704 C has a ratio of ~1.5, one that pulls a single
+// operand ~3, the tall-and-skinny ranks ~4 (growth is capped at 2).
+std::vector<int64_t> pipeline_chunks(int64_t kb, double growth = 2.0) {
   if (kb <= 0) return {0, 0};  // one empty chunk: its K = 0 GEMM still writes (zeros) the partial
   std::vector<int64_t> b{0};
-  int64_t acc = 0;
-  for (int64_t part : {1, 1, 2, 4, 8}) {
-    acc += part;
-    const int64_t v = kb * acc / 16;
-    if (v > b.back()) b.push_back(v);
+  double c = std::max(1.0, (double)kb / 16.0);
+  while (b.back() < kb) {
+    const int64_t n = b.size() >= 15 ? kb - b.back() : std::max<int64_t>(1, (int64_t)c);  // <= 15 chunks
+    b.push_back(std::min(kb, b.back() + n));
+    c *= growth;
   }
-  if (b.back() != kb) b.push_back(kb);
   return b;
 }
-constexpr int kMaxChunks = 6;
+double pipeline_growth(double gemm_flop_per_kblock, double pull_bytes_per_kblock) {
+  if (pull_bytes_per_kblock <= 0) return 2.0;
+  const double ratio = (gemm_flop_per_kblock / 36e12) / (pull_bytes_per_kblock / 600e9);
+  return std::max(1.0, std::min(2.0, 0.85 * ratio));
+}
+constexpr int kMaxChunks = 16;
 
 constexpr int64_t kDefaultChunkBytes = 16ll << 30;   // A+B dense chunk budget (single rank)
 // Triplets per stack-generation chunk (<= 6.4 GB): large enough that one smm launch has thousands
@@ -1209,7 +1214,13 @@ dbm_status multiply_tallskinny(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_matr
   // ---- gather A[:, S_me] and B[S_me, :] in K-chunks on the comm stream, GEMM chunks on the compute stream
   const int64_t kb = t.kp[t.me], ldp = t.ld(t.me);
   // chunks keep 16-B TMA bases when bs is even
-  const std::vector<int64_t> cb = bs % 2 ? std::vector<int64_t>{0, kb} : pipeline_chunks(kb);
+  int64_t remote_rows = 0;  // A rows and B columns this rank pulls from peers
+  for (int rr = 0; rr < t.pr; ++rr)
+    if (rr != t.r) remote_rows += t.mrows[rr];
+  for (int cc = 0; cc < t.pc; ++cc)
+    if ((t.me % t.pr) * t.pc + cc != t.me) remote_rows += t.ncols[cc];
+  const double growth = pipeline_growth(2.0 * t.Mtot * t.Ntot * bs, (double)remote_rows * bs * 8);
+  const std::vector<int64_t> cb = bs % 2 ? std::vector<int64_t>{0, kb} : pipeline_chunks(kb, growth);
   const int nsub = (int)cb.size() - 1;
   char* afull = ws + t.off_afull;
   char* bfull = ws + t.off_bfull;
@@ -2070,7 +2081,8 @@ dbm_status multiply_impl(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_matrix B, 
     bool remote0 = p.a_src(0) != p.me() || p.b_src(0) != p.me();
     const int64_t kb0 = p.kb[p.kappa(0)];
     if (ctx->transport == 0 && dens && remote0 && bs % 2 == 0 && kb0 >= 2) {
-      cb0 = pipeline_chunks(kb0);
+      const double pull = ((p.a_src(0) != p.me() ? p.mloc : 0) + (p.b_src(0) != p.me() ? p.nloc : 0)) * (double)bs * bs * 8;
+      cb0 = pipeline_chunks(kb0, pipeline_growth(2.0 * M * N * bs, pull));
       nsub0 = (int)cb0.size() - 1;
     }
     if (nsub0 > 1) {

@@ -306,7 +306,11 @@ def main():
             if occ:
                 cpu = oracle_sample_sparse(M, N, K, bs, occ, args.cpu_rows or auto_rows_sparse(M, N, K, bs, occ))
             else:
-                cpu = oracle_sample(M, N, K, args.cpu_rows or auto_rows(M, N, K))
+                rows = args.cpu_rows
+                if not rows:  # size the sample from a short probe so it lands at ~15 s on this host
+                    probe = oracle_sample(M, N, K, 4)
+                    rows = max(1, min(M, int(4 * 15.0 / max(probe["seconds"], 1e-3))))
+                cpu = oracle_sample(M, N, K, rows)
             cpu.pop("seconds", None)
         except Exception as ex:  # reported, never fatal
             cpu = {"error": str(ex)[:200]}

@@ -110,3 +110,12 @@ def test_plan_tallskinny_matches_oracle(dbm, orc, pr, pc):
         for r in range(pr):
             for c in range(pc):
                 assert dbm.plan_tallskinny(pr, pc, r, c, *shape) == orc.ts_bytes(*shape[:3], shape[3], pr, pc, r, c)
+
+
+def test_pattern_random_matches_oracle(dbm, orc):
+    """Host-only dbm_pattern_random (reading R15) against the oracle's independent implementation."""
+    for occ in (0.0, 0.01, 0.37, 1.0):
+        for seed, mid, Mb, Nb in ((1910, 0, 31, 47), (7, 5, 1, 90), (3, 2, 64, 1)):
+            assert np.array_equal(dbm.pattern_random(seed, mid, Mb, Nb, occ), orc.pattern_random(seed, mid, Mb, Nb, occ))
+    with pytest.raises(dbm.DbmError):
+        dbm.pattern_random(1, 0, 4, 4, 1.5)

@@ -1053,12 +1053,30 @@ dbm_status post_pulls_chunk(dbm_ctx ctx, const Plan& p, const std::vector<Plan>&
     const Plan& q = peer_plan[op.peer];
     const size_t src_off = op.operand == 0 ? q.ownA_off[op.kappa] : q.ownB_off[op.kappa];
     ARG_CHECK(src_off != SIZE_MAX && ctx->peer_ws[op.peer], DBM_ERR_PLAN, "peer panel not in its workspace");
-    const int64_t rows = (op.operand == 0 ? p.mloc : p.nloc) * p.bs, ld = p.ld_panel(op.kappa);
-    const size_t off = (size_t)(k0 * p.bs) * 8, width = (size_t)((k1 - k0) * p.bs) * 8;
+    // densified: dense K-major panels (rows x ld doubles); blocked: packed block panels, A row-major
+    // over (li, kk) (mloc rows of kb blocks), B over (kk, lj) (a K-chunk is one contiguous range)
+    const size_t bb8 = (size_t)p.bs * p.bs * 8;
+    int64_t rows;
+    size_t pitch, off, width;
+    if (p.densified) {
+      rows = (op.operand == 0 ? p.mloc : p.nloc) * p.bs;
+      pitch = (size_t)p.ld_panel(op.kappa) * 8;
+      off = (size_t)(k0 * p.bs) * 8;
+      width = (size_t)((k1 - k0) * p.bs) * 8;
+    } else if (op.operand == 0) {
+      rows = p.mloc;
+      pitch = (size_t)p.kb[op.kappa] * bb8;
+      off = (size_t)k0 * bb8;
+      width = (size_t)(k1 - k0) * bb8;
+    } else {
+      rows = 1;
+      off = (size_t)(k0 * p.nloc) * bb8;
+      width = pitch = (size_t)((k1 - k0) * p.nloc) * bb8;
+    }
     char* dst = ws + (op.operand == 0 ? p.off_recvA[bufA] : p.off_recvB[bufB]) + off;
     const char* src = ctx->peer_ws[op.peer] + src_off + off;
     if (rows && width)
-      CUDA_TRY(ctx, cudaMemcpy2DAsync(dst, ld * 8, src, ld * 8, width, rows, cudaMemcpyDeviceToDevice, ctx->comm));
+      CUDA_TRY(ctx, cudaMemcpy2DAsync(dst, pitch, src, pitch, width, rows, cudaMemcpyDeviceToDevice, ctx->comm));
     if (count) *recv += op.bytes;
   }
   return DBM_OK;
@@ -2080,9 +2098,9 @@ dbm_status multiply_impl(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_matrix B, 
     // the first chunk's transfer is exposed.
     bool remote0 = p.a_src(0) != p.me() || p.b_src(0) != p.me();
     const int64_t kb0 = p.kb[p.kappa(0)];
-    if (ctx->transport == 0 && dens && remote0 && bs % 2 == 0 && kb0 >= 2) {
+    if (ctx->transport == 0 && remote0 && (!dens || bs % 2 == 0) && kb0 >= 2) {
       const double pull = ((p.a_src(0) != p.me() ? p.mloc : 0) + (p.b_src(0) != p.me() ? p.nloc : 0)) * (double)bs * bs * 8;
-      cb0 = pipeline_chunks(kb0, pipeline_growth(2.0 * M * N * bs, pull));
+      cb0 = pipeline_chunks(kb0, pipeline_growth(2.0 * M * N * bs * (dens ? 1.0 : 1.25), pull));
       nsub0 = (int)cb0.size() - 1;
     }
     if (nsub0 > 1) {
@@ -2210,21 +2228,32 @@ dbm_status multiply_impl(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_matrix B, 
       const int64_t grp = smm_group_runs((int)bs);
       const int64_t runs_per_chunk = std::max<int64_t>(grp, p.trip_cap / kbk / grp * grp);
       const int64_t a_ld = kbk;  // A panel is mloc x kb blocks, row-major over (li, kk)
-      for (int64_t q0 = 0; q0 < nruns; q0 += runs_per_chunk) {
-        const int64_t q1 = std::min(nruns, q0 + runs_per_chunk);
-        {
-          ProfScope ps(ctx, cs, 4, 0.0, 12.0 * (q1 - q0) * kbk);
-          launch_stackgen(trav_li, trav_lj, q0, q1, kbk, p.nloc, a_ld, p.nloc, trip, cs);
-          ++launches;
-        }
-        {
-          ProfScope ps(ctx, cs, 1, 2.0 * bs * bb * (q1 - q0) * kbk, 16.0 * bb * (q1 - q0) * kbk);
-          const int nsplit = p.spart_runs ? (int)std::min<int64_t>(smm_pick_split((int)bs, q1 - q0, kbk),
-                                                                   p.spart_runs / (q1 - q0))
-                                          : 1;
-          CUDA_TRY(ctx, launch_smm((int)bs, trip, q1 - q0, kbk, Ap, Bp, C->arena, alpha, s == 0 ? beta : 1.0, nsplit,
-                                   nsplit > 1 ? (double*)(ws + p.off_spart) : nullptr, cs, &launches,
-                                   p.mloc * kbk, kbk * p.nloc));
+      // step 0 with a chunked pull: each K-chunk [k0, k1) of the panels multiplies as soon as it landed
+      // (the runs' K split across chunks, accumulated in chunk order: C = beta*C + alpha*acc_0, then
+      // C += alpha*acc_j); the stack list itself (dbm_debug_stacks) is the unchunked one
+      const int nsub = (s == 0) ? nsub0 : 1;
+      for (int j = 0; j < nsub; ++j) {
+        const int64_t k0 = nsub > 1 ? cb0[j] : 0, nk = nsub > 1 ? cb0[j + 1] - cb0[j] : kbk;
+        if (nsub > 1) CUDA_TRY(ctx, cudaStreamWaitEvent(cs, ev_c[j], 0));
+        const double* Aj = Ap + k0 * bb;
+        const double* Bj = Bp + k0 * p.nloc * bb;
+        const double bfirst = (s == 0 && j == 0) ? beta : 1.0;
+        for (int64_t q0 = 0; q0 < nruns; q0 += runs_per_chunk) {
+          const int64_t q1 = std::min(nruns, q0 + runs_per_chunk);
+          {
+            ProfScope ps(ctx, cs, 4, 0.0, 12.0 * (q1 - q0) * nk);
+            launch_stackgen(trav_li, trav_lj, q0, q1, nk, p.nloc, a_ld, p.nloc, trip, cs);
+            ++launches;
+          }
+          {
+            ProfScope ps(ctx, cs, 1, 2.0 * bs * bb * (q1 - q0) * nk, 16.0 * bb * (q1 - q0) * nk);
+            const int nsplit = p.spart_runs ? (int)std::min<int64_t>(smm_pick_split((int)bs, q1 - q0, nk),
+                                                                     p.spart_runs / (q1 - q0))
+                                            : 1;
+            CUDA_TRY(ctx, launch_smm((int)bs, trip, q1 - q0, nk, Aj, Bj, C->arena, alpha, bfirst, nsplit,
+                                     nsplit > 1 ? (double*)(ws + p.off_spart) : nullptr, cs, &launches,
+                                     p.mloc * kbk - k0, (kbk - k0) * p.nloc));
+          }
         }
       }
       st.entries += nruns * kbk;

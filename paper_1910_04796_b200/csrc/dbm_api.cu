@@ -4,17 +4,10 @@
 // Runtime model: one process per GPU; the compute stream is the caller's (torch's)
 // stream; a second "comm" stream carries NCCL grouped send/recv of Cannon panels so the fetch of
 // step s+1 overlaps the local multiply of step s; CUDA events order the two streams.
-#include <nccl.h>
-
-#include <algorithm>
 #include <cstdio>
-#include <cstring>
 #include <mutex>
-#include <numeric>
-#include <string>
-#include <vector>
 
-#include "dbm_internal.h"
+#include "api_internal.h"
 
 namespace dbm {
 static thread_local std::string g_err;
@@ -30,50 +23,10 @@ int num_sms() {
   return n;
 }
 
-static int64_t local_count(int64_t nb, int p, int r) { return nb > r ? (nb - r + p - 1) / p : 0; }
-static int64_t lcm64(int64_t a, int64_t b) { return a / std::gcd(a, b) * b; }
-static int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
 }  // namespace dbm
 
 using namespace dbm;
 
-#define ARG_CHECK(cond, code, msg) \
-  do {                             \
-    if (!(cond)) {                 \
-      set_error(msg);              \
-      return code;                 \
-    }                              \
-  } while (0)
-
-#define CUDA_TRY(ctx, x)                                                                    \
-  do {                                                                                      \
-    cudaError_t e_ = (x);                                                                   \
-    if (e_ != cudaSuccess) {                                                                \
-      set_error(std::string(#x) + ": " + cudaGetErrorString(e_));                           \
-      if (ctx) (ctx)->poisoned = DBM_ERR_CUDA;                                              \
-      return DBM_ERR_CUDA;                                                                  \
-    }                                                                                       \
-  } while (0)
-
-#define NCCL_TRY(ctx, x)                                                                    \
-  do {                                                                                      \
-    ncclResult_t r_ = (x);                                                                  \
-    if (r_ != ncclSuccess) {                                                                \
-      set_error(std::string(#x) + ": " + ncclGetErrorString(r_));                           \
-      if (ctx) (ctx)->poisoned = DBM_ERR_NCCL;                                              \
-      return DBM_ERR_NCCL;                                                                  \
-    }                                                                                       \
-  } while (0)
-
-#define CTX_OK(ctx)                                                             \
-  do {                                                                          \
-    ARG_CHECK((ctx) != nullptr, DBM_ERR_ARG, "null context");                   \
-    if ((ctx)->poisoned != DBM_OK) {                                            \
-      set_error("context poisoned by an earlier CUDA/NCCL failure");            \
-      return (ctx)->poisoned;                                                   \
-    }                                                                           \
-    CUDA_TRY(ctx, cudaSetDevice((ctx)->device));                                \
-  } while (0)
 
 namespace {
 
@@ -84,7 +37,9 @@ uint64_t next_serial() {
   return ++n;
 }
 
-cudaEvent_t get_event(dbm_ctx ctx) {
+}  // namespace
+
+cudaEvent_t dbm::get_event(dbm_ctx ctx) {
   if (!ctx->ev_pool.empty()) {
     cudaEvent_t e = ctx->ev_pool.back();
     ctx->ev_pool.pop_back();
@@ -95,27 +50,7 @@ cudaEvent_t get_event(dbm_ctx ctx) {
   return e;
 }
 
-// Profiling bracket around one dominant-kernel launch (timing events live on the launch stream).
-struct ProfScope {
-  dbm_ctx ctx;
-  cudaStream_t st;
-  cudaEvent_t a = nullptr, b = nullptr;
-  int kind;
-  double flops, bytes;
-  ProfScope(dbm_ctx c, cudaStream_t s, int k, double f, double by) : ctx(c), st(s), kind(k), flops(f), bytes(by) {
-    if (!ctx->profiling) return;
-    cudaEventCreate(&a);
-    cudaEventCreate(&b);
-    cudaEventRecord(a, st);
-  }
-  ~ProfScope() {
-    if (!a) return;
-    cudaEventRecord(b, st);
-    ctx->prof.push_back({a, b, kind, flops, bytes});
-  }
-};
 
-}  // namespace
 
 // ====================================================================== misc
 extern "C" const char* dbm_status_string(dbm_status s) {
@@ -288,10 +223,6 @@ extern "C" dbm_status dbm_ctx_set_densify_threshold(dbm_ctx ctx, double threshol
   ARG_CHECK(ctx && threshold >= 0.0 && threshold <= 1.0, DBM_ERR_ARG, "threshold outside [0, 1]");
   ctx->densify_threshold = threshold;
   return DBM_OK;
-}
-
-namespace dbm {
-void free_sp_cache(dbm_ctx ctx);
 }
 
 extern "C" dbm_status dbm_ctx_launch_count(dbm_ctx ctx, int64_t* out) {
@@ -685,37 +616,6 @@ struct Plan {
   }
 };
 
-size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
-
-// K-chunk boundaries (blocks) of a transfer -> GEMM pipeline whose first transfer nothing hides (Cannon's
-// step 0, the tall-and-skinny gather).  The first chunk is 1/16 of kb and each next one is `growth`
-// times larger: the pull of chunk j+1 (copy engines, ~600 GB/s from a peer) must fit under the GEMM of
-// chunk j, i.e. growth <= (GEMM time per K-block) / (pull time per K-block) = pipeline_growth(); a
-// rank that pulls both operands of a thin 704 x 704 C has a ratio of ~1.5, one that pulls a single
-// operand ~3, the tall-and-skinny ranks ~4 (growth is capped at 2).
-std::vector<int64_t> pipeline_chunks(int64_t kb, double growth = 2.0) {
-  if (kb <= 0) return {0, 0};  // one empty chunk: its K = 0 GEMM still writes (zeros) the partial
-  std::vector<int64_t> b{0};
-  double c = std::max(1.0, (double)kb / 16.0);
-  while (b.back() < kb) {
-    const int64_t n = b.size() >= 15 ? kb - b.back() : std::max<int64_t>(1, (int64_t)c);  // <= 15 chunks
-    b.push_back(std::min(kb, b.back() + n));
-    c *= growth;
-  }
-  return b;
-}
-double pipeline_growth(double gemm_flop_per_kblock, double pull_bytes_per_kblock) {
-  if (pull_bytes_per_kblock <= 0) return 2.0;
-  const double ratio = (gemm_flop_per_kblock / 36e12) / (pull_bytes_per_kblock / 600e9);
-  return std::max(1.0, std::min(2.0, 0.85 * ratio));
-}
-constexpr int kMaxChunks = 16;
-
-constexpr int64_t kDefaultChunkBytes = 16ll << 30;   // A+B dense chunk budget (single rank)
-// Triplets per stack-generation chunk (<= 6.4 GB): large enough that one smm launch has thousands
-// of 8-run groups for 148 SMs even with the 90,112-long runs of the rectangular bs-22 config.
-constexpr int64_t kTripChunkEntries = 1ll << 29;
-
 // Host-only plan: depends on the grid, this rank's coordinates and the block counts (no CUDA).
 Plan make_plan_raw(int nranks, int pr, int pc, int r, int c, int64_t Mb, int64_t Nb, int64_t Kb, int64_t bs,
                    bool densified, int64_t chunk_bytes, int transport) {
@@ -848,6 +748,31 @@ std::vector<XOp> exchange_ops(const Plan& p, int s) {
   return ops;
 }
 
+}  // namespace
+
+namespace dbm {
+// K-chunk boundaries (blocks) of a transfer -> GEMM pipeline whose first transfer nothing hides (Cannon's
+// step 0, the tall-and-skinny gather).  The first chunk is 1/16 of kb and each next one is `growth`
+// times larger: the pull of chunk j+1 (copy engines, ~600 GB/s from a peer) must fit under the GEMM of
+// chunk j, i.e. growth <= (GEMM time per K-block) / (pull time per K-block) = pipeline_growth(); a
+// rank that pulls both operands of a thin 704 x 704 C has a ratio of ~1.5, one that pulls a single
+// operand ~3, the tall-and-skinny ranks ~4 (growth is capped at 2).
+std::vector<int64_t> pipeline_chunks(int64_t kb, double growth) {
+  if (kb <= 0) return {0, 0};  // one empty chunk: its K = 0 GEMM still writes (zeros) the partial
+  std::vector<int64_t> b{0};
+  double c = std::max(1.0, (double)kb / 16.0);
+  while (b.back() < kb) {
+    const int64_t n = b.size() >= 15 ? kb - b.back() : std::max<int64_t>(1, (int64_t)c);  // <= 15 chunks
+    b.push_back(std::min(kb, b.back() + n));
+    c *= growth;
+  }
+  return b;
+}
+double pipeline_growth(double gemm_flop_per_kblock, double pull_bytes_per_kblock) {
+  if (pull_bytes_per_kblock <= 0) return 2.0;
+  const double ratio = (gemm_flop_per_kblock / 36e12) / (pull_bytes_per_kblock / 600e9);
+  return std::max(1.0, std::min(2.0, 0.85 * ratio));
+}
 dbm_status validate(dbm_ctx ctx, dbm_matrix A, dbm_matrix B, dbm_matrix C) {
   ARG_CHECK(ctx && A && B && C, DBM_ERR_ARG, "null handle");
   ARG_CHECK(A->ctx == ctx && B->ctx == ctx && C->ctx == ctx, DBM_ERR_GRID, "matrices from a different context");
@@ -895,7 +820,8 @@ void undensify_c(dbm_matrix C, const double* dense, int64_t ld, int nsplit, int6
     launch_undensify(dense, ld, nsplit, split_stride, C->mloc, C->nloc, C->bs, alpha, beta, C->arena, cs);
 }
 
-}  // namespace
+}  // namespace dbm
+
 
 extern "C" dbm_status dbm_plan_exchange(int pr, int pc, int myrow, int mycol, int64_t Mb, int64_t Nb, int64_t Kb,
                                         int32_t bs, dbm_path path, int step, int32_t* ops, int64_t* bytes,
@@ -971,7 +897,9 @@ AddrRangeFn addr_range_fn() {
 
 constexpr int kIpcRec = 128;  // bytes per rank: 64-B handle + 8-B offset, padded
 
-dbm_status ipc_exchange(dbm_ctx ctx, void* ws) {
+}  // namespace
+
+dbm_status dbm::ipc_exchange(dbm_ctx ctx, void* ws) {
   const int P = ctx->nranks;
   AddrRangeFn fn = addr_range_fn();
   ARG_CHECK(fn, DBM_ERR_CUDA, "cuMemGetAddressRange unavailable");
@@ -1020,6 +948,8 @@ dbm_status ipc_exchange(dbm_ctx ctx, void* ws) {
   ctx->ipc_ws = ws;
   return DBM_OK;
 }
+
+namespace {
 
 // Pull this rank's step-s panels from their owners' workspaces (peer plans give the offsets).
 dbm_status post_pulls(dbm_ctx ctx, const Plan& p, const std::vector<Plan>& peer_plan, int s, char* ws, int bufA,
@@ -1089,695 +1019,16 @@ __global__ void scale_kernel(double* __restrict__ x, int64_t n, double beta) {
 
 }  // namespace
 
-namespace {
-// ====================================================================== tall-and-skinny
-// "only for tall-and-skinny matrices (one large dimension) we use an optimized algorithm" (§II;
-// 1-D decomposition of K, local partial products, reduction of the small C).
-// Reading R14: rank p = r*Pc + c takes the K blocks S_p = {k : k mod P == p}.  Every
-// k in S_p has k mod Pc == c, so A[:, S_p] lives in p's grid column: rank (r', c) contributes its
-// rows (i = r' mod Pr) as one dense K-major piece; B[S_p, :] lives in grid row p mod Pr: rank
-// (p mod Pr, c') contributes its columns.  p assembles A_full (all M rows) x B_full (all N cols),
-// computes the partial C_p = A[:, S_p] B[S_p, :] with one GEMM (pulled in K-chunks, each chunk
-// followed by its GEMM chunk), and finally every rank pulls its own C blocks' sub-rectangle out of
-// all P partials and sums them in rank order (deterministic) with alpha / beta.  Rows of A_full /
-// C_p are ordered (r', li) and columns of B_full / C_p (c', lj), so each owner's piece and each
-// rank's C share are contiguous 2-D sub-rectangles: every transfer is one copy-engine copy.
-struct TSPlan {
-  int P = 1, pr = 1, pc = 1, r = 0, c = 0, me = 0;
-  int64_t bs = 0, Mb = 0, Nb = 0, Kb = 0;
-  std::vector<int64_t> kp;                 // |S_q| (blocks) per rank q
-  std::vector<int64_t> mrows, rowoff;      // per grid row r': rows (elements) and offset in A_full / C_p
-  std::vector<int64_t> ncols, coloff;      // per grid column c'
-  int64_t Mtot = 0, Ntot = 0;
-  std::vector<size_t> offApiece, offBpiece;  // my pieces: A per target row tr, B per target t (q = r + t*pr)
-  size_t off_afull = 0, off_bfull = 0, off_cpart = 0, off_cstack = 0, off_part = 0, total = 0;
-  int max_split = 1;
-  int64_t ld(int q) const { return round_up(std::max<int64_t>(kp[q] * bs, 1), 2); }
-  size_t a_piece_bytes(int q, int rr) const { return kp[q] ? (size_t)mrows[rr] * ld(q) * 8 : 0; }
-  size_t b_piece_bytes(int q, int cc) const { return kp[q] ? (size_t)ncols[cc] * ld(q) * 8 : 0; }
-};
-
-TSPlan make_ts_plan(int pr, int pc, int r, int c, int64_t Mb, int64_t Nb, int64_t Kb, int64_t bs) {
-  TSPlan t;
-  t.P = pr * pc;
-  t.pr = pr;
-  t.pc = pc;
-  t.r = r;
-  t.c = c;
-  t.me = r * pc + c;
-  t.bs = bs;
-  t.Mb = Mb;
-  t.Nb = Nb;
-  t.Kb = Kb;
-  t.kp.resize(t.P);
-  for (int q = 0; q < t.P; ++q) t.kp[q] = local_count(Kb, t.P, q);
-  t.mrows.resize(pr);
-  t.rowoff.resize(pr);
-  for (int rr = 0; rr < pr; ++rr) {
-    t.mrows[rr] = local_count(Mb, pr, rr) * bs;
-    t.rowoff[rr] = rr ? t.rowoff[rr - 1] + t.mrows[rr - 1] : 0;
-  }
-  t.ncols.resize(pc);
-  t.coloff.resize(pc);
-  for (int cc = 0; cc < pc; ++cc) {
-    t.ncols[cc] = local_count(Nb, pc, cc) * bs;
-    t.coloff[cc] = cc ? t.coloff[cc - 1] + t.ncols[cc - 1] : 0;
-  }
-  t.Mtot = Mb * bs;
-  t.Ntot = Nb * bs;
-  size_t off = 0;
-  auto take = [&](size_t bytes) {
-    size_t o = off;
-    off = align256(off + bytes);
-    return o;
-  };
-  t.offApiece.resize(pr);
-  for (int tr = 0; tr < pr; ++tr) t.offApiece[tr] = take(t.a_piece_bytes(tr * pc + c, r));
-  t.offBpiece.resize(pc);
-  for (int tt = 0; tt < pc; ++tt) t.offBpiece[tt] = take(t.b_piece_bytes(r + tt * pr, c));
-  t.off_afull = take((size_t)t.Mtot * t.ld(t.me) * 8);
-  t.off_bfull = take((size_t)t.Ntot * t.ld(t.me) * 8);
-  t.off_cpart = take((size_t)t.Mtot * t.Ntot * 8);
-  t.off_cstack = take((size_t)t.P * t.mrows[r] * t.ncols[c] * 8);
-  const int64_t K = t.kp[t.me] * bs;
-  const std::vector<int64_t> cb = pipeline_chunks(t.kp[t.me]);
-  for (size_t j = 1; j < cb.size(); ++j)
-    t.max_split = std::max(t.max_split, pick_splitk(t.Mtot, t.Ntot, (cb[j] - cb[j - 1]) * bs, num_sms()));
-  t.max_split = std::max(t.max_split, pick_splitk(t.Mtot, t.Ntot, K, num_sms()));
-  if (t.max_split > 1) t.off_part = take((size_t)t.max_split * t.Mtot * t.Ntot * 8);
-  t.total = std::max<size_t>(off, 256);
-  return t;
+void dbm::launch_scale(double* x, int64_t n, double beta, cudaStream_t st) {
+  if (n <= 0) return;
+  scale_kernel<<<(unsigned)std::min<int64_t>((n + 255) / 256, num_sms() * 16), 256, 0, st>>>(x, n, beta);
 }
-
-// Bytes this rank pulls from peers / peers pull from it in one tall-and-skinny multiply.
-void ts_bytes(const TSPlan& t, int64_t* recv, int64_t* sent) {
-  int64_t rv = 0, sd = 0;
-  for (int rr = 0; rr < t.pr; ++rr)
-    if (rr != t.r) rv += (int64_t)t.a_piece_bytes(t.me, rr);
-  const int rb = t.me % t.pr;
-  for (int cc = 0; cc < t.pc; ++cc)
-    if (rb * t.pc + cc != t.me) rv += (int64_t)t.b_piece_bytes(t.me, cc);
-  for (int q = 0; q < t.P; ++q)
-    if (q != t.me) rv += t.mrows[t.r] * t.ncols[t.c] * 8;  // my C share out of every other partial
-  // what the others pull from me
-  for (int tr = 0; tr < t.pr; ++tr)
-    if (tr != t.r) sd += (int64_t)t.a_piece_bytes(tr * t.pc + t.c, t.r);
-  for (int tt = 0; tt < t.pc; ++tt) {
-    const int q = t.r + tt * t.pr;
-    if (q != t.me) sd += (int64_t)t.b_piece_bytes(q, t.c);
-  }
-  for (int q = 0; q < t.P; ++q)
-    if (q != t.me) sd += t.mrows[q / t.pc] * t.ncols[q % t.pc] * 8;
-  *recv = rv;
-  *sent = sd;
-}
-
-dbm_status multiply_tallskinny(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_matrix B, double beta, dbm_matrix C,
-                               char* ws, dbm_stats* st, int* launches) {
-  const TSPlan t = make_ts_plan(ctx->pr, ctx->pc, ctx->myrow, ctx->mycol, A->Mb, B->Nb, A->Nb, A->bs);
-  cudaStream_t cs = ctx->stream;
-  const int64_t bs = t.bs, P = t.P;
-  // ---- own pieces (densified once; peers pull them).  The pieces this rank needs itself are densified
-  // straight into its A_full / B_full: a local device-to-device copy would run on SMs and wait behind
-  // the persistent GEMM (measured: 23 GB/s under a GEMM vs 750 GB/s for the peer pulls on the copy
-  // engines, tools/microbench/ce_copy.py).
-  for (int tr = 0; tr < t.pr; ++tr) {
-    const int q = tr * t.pc + t.c;
-    if (!t.kp[q] || !t.mrows[t.r]) continue;
-    double* dst = q == t.me ? (double*)(ws + t.off_afull) + (size_t)t.rowoff[t.r] * t.ld(q)
-                            : (double*)(ws + t.offApiece[tr]);
-    ProfScope ps(ctx, cs, 2, 0.0, 16.0 * t.mrows[t.r] * t.kp[q] * bs);
-    if (dbm_status e = densify_a(ctx, A, tr, t.pr, t.kp[q], dst, t.ld(q), 1, cs)) return e;
-    ++*launches;
-  }
-  for (int tt = 0; tt < t.pc; ++tt) {
-    const int q = t.r + tt * t.pr;
-    if (!t.kp[q] || !t.ncols[t.c]) continue;
-    double* dst = q == t.me ? (double*)(ws + t.off_bfull) + (size_t)t.coloff[t.c] * t.ld(q)
-                            : (double*)(ws + t.offBpiece[tt]);
-    ProfScope ps(ctx, cs, 2, 0.0, 16.0 * t.ncols[t.c] * t.kp[q] * bs);
-    if (dbm_status e = densify_b(ctx, B, tt, t.pc, t.kp[q], dst, t.ld(q), 0, cs)) return e;
-    ++*launches;
-  }
-  CUDA_TRY(ctx, cudaGetLastError());
-  cudaEvent_t ev_ready = get_event(ctx);
-  CUDA_TRY(ctx, cudaEventRecord(ev_ready, cs));
-  CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->comm, ev_ready, 0));
-  if (dbm_status e = ipc_exchange(ctx, ws)) return e;  // all-gather = "every piece is ready" barrier
-  std::vector<TSPlan> peer(P);
-  for (int q = 0; q < P; ++q)
-    if (q != t.me) peer[q] = make_ts_plan(t.pr, t.pc, q / t.pc, q % t.pc, t.Mb, t.Nb, t.Kb, bs);
-  auto base_of = [&](int q) { return q == t.me ? ws : ctx->peer_ws[q]; };
-
-  // ---- gather A[:, S_me] and B[S_me, :] in K-chunks on the comm stream, GEMM chunks on the compute stream
-  const int64_t kb = t.kp[t.me], ldp = t.ld(t.me);
-  // chunks keep 16-B TMA bases when bs is even
-  int64_t remote_rows = 0;  // A rows and B columns this rank pulls from peers
-  for (int rr = 0; rr < t.pr; ++rr)
-    if (rr != t.r) remote_rows += t.mrows[rr];
-  for (int cc = 0; cc < t.pc; ++cc)
-    if ((t.me % t.pr) * t.pc + cc != t.me) remote_rows += t.ncols[cc];
-  const double growth = pipeline_growth(2.0 * t.Mtot * t.Ntot * bs, (double)remote_rows * bs * 8);
-  const std::vector<int64_t> cb = bs % 2 ? std::vector<int64_t>{0, kb} : pipeline_chunks(kb, growth);
-  const int nsub = (int)cb.size() - 1;
-  char* afull = ws + t.off_afull;
-  char* bfull = ws + t.off_bfull;
-  double* cpart = (double*)(ws + t.off_cpart);
-  cudaEvent_t ev_c[kMaxChunks] = {};
-  const int rb = t.me % t.pr;
-  int64_t ts_recv = 0, ts_sent = 0;
-  ts_bytes(t, &ts_recv, &ts_sent);
-  ts_recv -= (int64_t)(t.P - 1) * t.mrows[t.r] * t.ncols[t.c] * 8;  // the C-share pulls run later, on cs
-  ProfScope ps_x(ctx, ctx->comm, 5, 0.0, (double)ts_recv);  // the A / B gathers on the copy engines
-  for (int j = 0; j < nsub && kb > 0; ++j) {
-    const int64_t k0 = cb[j], k1 = cb[j + 1];
-    const size_t off = (size_t)(k0 * bs) * 8, width = (size_t)((k1 - k0) * bs) * 8;
-    for (int rr = 0; rr < t.pr; ++rr) {  // rows of grid row rr from rank (rr, c), its piece for target row r
-      const int q = rr * t.pc + t.c;
-      if (!t.mrows[rr] || q == t.me) continue;  // my own rows are already in place
-      const char* src = ctx->peer_ws[q] + peer[q].offApiece[t.r];
-      CUDA_TRY(ctx, cudaMemcpy2DAsync(afull + (size_t)t.rowoff[rr] * ldp * 8 + off, ldp * 8, src + off, ldp * 8, width,
-                                      t.mrows[rr], cudaMemcpyDeviceToDevice, ctx->comm));
-    }
-    for (int cc = 0; cc < t.pc; ++cc) {  // columns of grid column cc from rank (rb, cc), its piece for target me
-      const int q = rb * t.pc + cc;
-      if (!t.ncols[cc] || q == t.me) continue;
-      const int tt = (t.me - rb) / t.pr;
-      const char* src = ctx->peer_ws[q] + peer[q].offBpiece[tt];
-      CUDA_TRY(ctx, cudaMemcpy2DAsync(bfull + (size_t)t.coloff[cc] * ldp * 8 + off, ldp * 8, src + off, ldp * 8, width,
-                                      t.ncols[cc], cudaMemcpyDeviceToDevice, ctx->comm));
-    }
-    ev_c[j] = get_event(ctx);
-    CUDA_TRY(ctx, cudaEventRecord(ev_c[j], ctx->comm));
-  }
-  for (int j = 0; j < nsub; ++j) {
-    const int64_t k0 = cb[j], k1 = cb[j + 1];
-    if (kb > 0) CUDA_TRY(ctx, cudaStreamWaitEvent(cs, ev_c[j], 0));
-    GemmArgs g{t.Mtot, t.Ntot, (k1 - k0) * bs, (const double*)afull + k0 * bs, ldp, (const double*)bfull + k0 * bs,
-               ldp, cpart, t.Mtot, 1.0, j == 0 ? 0.0 : 1.0, 1, nullptr};
-    g.splitk = std::min(pick_splitk(g.M, g.N, g.K, num_sms()), t.max_split);
-    g.partial = g.splitk > 1 ? (double*)(ws + t.off_part) : nullptr;
-    ProfScope ps(ctx, cs, 0, 2.0 * g.M * g.N * g.K, 8.0 * (g.M * g.K + g.N * g.K + g.M * g.N * (j ? 2 : 1)));
-    CUDA_TRY(ctx, launch_dgemm(g, cs, launches));
-    ++st->gemm_launches;
-    if (kb == 0) break;
-  }
-  st->entries += 1;  // the densified batch holds one multiplication
-  st->stacks += 1;
-  st->flops += 2.0 * t.Mtot * t.Ntot * kb * bs;
-  // ---- reduction: every partial is complete after this barrier; pull my C share out of each
-  int* w = ctx->d_scratch;
-  NCCL_TRY(ctx, ncclAllReduce(w, w, 1, ncclInt, ncclSum, (ncclComm_t)ctx->nccl, cs));
-  const int64_t mr = t.mrows[t.r], nc = t.ncols[t.c];
-  double* cstack = (double*)(ws + t.off_cstack);
-  for (int q = 0; q < P && mr * nc > 0; ++q) {
-    const double* src = (const double*)(base_of(q) + (q == t.me ? t.off_cpart : peer[q].off_cpart)) + t.rowoff[t.r] +
-                        (size_t)t.coloff[t.c] * t.Mtot;
-    CUDA_TRY(ctx, cudaMemcpy2DAsync(cstack + (size_t)q * mr * nc, mr * 8, src, t.Mtot * 8, mr * 8, nc,
-                                    cudaMemcpyDeviceToDevice, cs));
-  }
-  if (mr * nc > 0) {
-    ProfScope ps(ctx, cs, 3, 0.0, (8.0 * P + (beta == 0.0 ? 8.0 : 16.0)) * mr * nc);
-    undensify_c(C, cstack, mr, (int)P, mr * nc, alpha, beta, cs);
-    ++*launches;
-    CUDA_TRY(ctx, cudaGetLastError());
-  }
-  // closing barrier: no peer still reads my pieces or my partial
-  NCCL_TRY(ctx, ncclAllReduce(w, w, 1, ncclInt, ncclSum, (ncclComm_t)ctx->nccl, cs));
-  ts_bytes(t, &st->bytes_recv, &st->bytes_sent);
-  st->steps = 1;
-  ctx->ev_pool.push_back(ev_ready);
-  for (int j = 0; j < kMaxChunks; ++j)
-    if (ev_c[j]) ctx->ev_pool.push_back(ev_c[j]);
-  return DBM_OK;
-}
-
-}  // namespace
-
-// ====================================================================== block-sparse blocked path (R15)
-// Cannon over sparse panels (§8f-2).  Every rank knows every operand's global pattern, so each rank
-// plans on the host, once per (A, B, C) pattern triple (cached in the context): the CSR / CSC lists
-// of each step's A(r, kappa) and B(kappa, c) panels (kk ascending, slot = rank among the panel's stored
-// blocks in row-major order = the order the owner packs them), the gather lists of the panels it owns,
-// and its peers' workspace offsets.  Per multiply the GPU packs the owned panels (stored blocks only),
-// the copy engines pull the remote ones (only stored blocks move), and per step the Generation
-// kernels + smm_sparse run over the traversal in chunks of runs.
-namespace dbm {
-struct SpStep {
-  int kappa = 0, a_src = 0, b_src = 0;
-  int64_t a_nnz = 0, b_nnz = 0, entries = 0;
-  size_t o_aptr = 0, o_akk = 0, o_bptr = 0, o_bkk = 0, o_bslot = 0;  // int32 offsets into d_meta
-  std::vector<int32_t> run_len;                                      // per traversal position
-  std::vector<int64_t> chunk_entries;                                // per chunk of runs_per_chunk runs
-};
-struct SpCache {
-  uint64_t a_serial = 0, b_serial = 0, c_serial = 0;
-  int L = 1;
-  std::vector<SpStep> steps;
-  std::vector<int64_t> ownA_nnz, ownB_nnz;  // per kappa (-1: not mine)
-  std::vector<size_t> ownA_off, ownB_off, o_gatherA, o_gatherB;
-  std::vector<std::vector<size_t>> peer_ownA_off, peer_ownB_off;
-  std::vector<std::vector<int64_t>> peer_ownA_nnz, peer_ownB_nnz;
-  size_t off_recvA[2] = {0, 0}, off_recvB[2] = {0, 0}, off_trav = 0, off_cnt = 0, off_off = 0, off_scan = 0;
-  size_t off_trip = 0, scan_bytes = 0, total = 256;
-  int64_t runs_per_chunk = 1;
-  int32_t* d_meta = nullptr;
-  std::vector<std::pair<int64_t, int64_t>> stacks_by_cap;  // (cap, stacks of the whole multiply)
-};
-
-void free_sp_cache(dbm_ctx ctx) {
-  for (SpCache* c : ctx->sp_cache) {
-    if (c->d_meta) cudaFree(c->d_meta);
-    delete c;
-  }
-  ctx->sp_cache.clear();
-}
-}  // namespace dbm
 
 namespace {
 
-int64_t local_slot(dbm_matrix m, int64_t li, int64_t lj) {
-  if (!m->sparse) return li * m->nloc + lj;
-  const auto b = m->col.begin() + m->row_ptr[li], e = m->col.begin() + m->row_ptr[li + 1];
-  const auto it = std::lower_bound(b, e, (int32_t)lj);
-  return (it != e && *it == (int32_t)lj) ? (int64_t)(it - m->col.begin()) : -1;
-}
-
-void host_traversal(int64_t r0, int64_t r1, int64_t c0, int64_t c1, std::vector<int32_t>& li, std::vector<int32_t>& lj) {
-  if (r1 <= r0 || c1 <= c0) return;
-  if (r1 - r0 == 1 && c1 - c0 == 1) {
-    li.push_back((int32_t)r0);
-    lj.push_back((int32_t)c0);
-    return;
-  }
-  if (r1 - r0 >= c1 - c0) {
-    const int64_t mid = r0 + (r1 - r0) / 2;
-    host_traversal(r0, mid, c0, c1, li, lj);
-    host_traversal(mid, r1, c0, c1, li, lj);
-  } else {
-    const int64_t mid = c0 + (c1 - c0) / 2;
-    host_traversal(r0, r1, c0, mid, li, lj);
-    host_traversal(r0, r1, mid, c1, li, lj);
-  }
-}
-
-// Stored blocks of the A(rr, kappa) / B(kappa, cc) panels, as owned by rank (rr, kappa mod Pc) /
-// (kappa mod Pr, cc).
-int64_t a_panel_nnz(dbm_ctx ctx, dbm_matrix A, int L, int rr, int kappa) {
-  int64_t n = 0;
-  for (int64_t i = rr; i < A->Mb; i += ctx->pr)
-    for (int64_t k = kappa; k < A->Nb; k += L) n += A->stored(i, k);
-  return n;
-}
-int64_t b_panel_nnz(dbm_ctx ctx, dbm_matrix B, int L, int cc, int kappa) {
-  int64_t n = 0;
-  for (int64_t k = kappa; k < B->Mb; k += L)
-    for (int64_t j = cc; j < B->Nb; j += ctx->pc) n += B->stored(k, j);
-  return n;
-}
-
-// Workspace layout: own (packed) panels first, so a peer only needs the panel sizes to find them.
-void own_layout(dbm_ctx ctx, dbm_matrix A, dbm_matrix B, int L, int r, int c, std::vector<int64_t>& a_nnz,
-                std::vector<int64_t>& b_nnz, std::vector<size_t>& a_off, std::vector<size_t>& b_off, size_t* end) {
-  const size_t bb8 = (size_t)A->bs * A->bs * 8;
-  a_nnz.assign(L, -1);
-  b_nnz.assign(L, -1);
-  a_off.assign(L, SIZE_MAX);
-  b_off.assign(L, SIZE_MAX);
-  size_t off = 0;
-  if (ctx->nranks > 1) {
-    for (int k = 0; k < L; ++k)
-      if (k % ctx->pc == c) {
-        a_nnz[k] = a_panel_nnz(ctx, A, L, r, k);
-        a_off[k] = off;
-        off = align256(off + (size_t)a_nnz[k] * bb8);
-      }
-    for (int k = 0; k < L; ++k)
-      if (k % ctx->pr == r) {
-        b_nnz[k] = b_panel_nnz(ctx, B, L, c, k);
-        b_off[k] = off;
-        off = align256(off + (size_t)b_nnz[k] * bb8);
-      }
-  }
-  *end = off;
-}
-
-dbm_status sp_cache_get(dbm_ctx ctx, dbm_matrix A, dbm_matrix B, dbm_matrix C, SpCache** out) {
-  for (SpCache* c : ctx->sp_cache)
-    if (c->a_serial == A->serial && c->b_serial == B->serial && c->c_serial == C->serial) {
-      *out = c;
-      return DBM_OK;
-    }
-  SpCache* sc = new SpCache();
-  sc->a_serial = A->serial;
-  sc->b_serial = B->serial;
-  sc->c_serial = C->serial;
-  const int pr = ctx->pr, pc = ctx->pc, r = ctx->myrow, c = ctx->mycol, me = ctx->rank;
-  const int L = (int)lcm64(pr, pc);
-  sc->L = L;
-  const int64_t mloc = C->mloc, nloc = C->nloc, Kb = A->Nb;
-  const size_t bb8 = (size_t)A->bs * A->bs * 8;
-  size_t off = 0;
-  own_layout(ctx, A, B, L, r, c, sc->ownA_nnz, sc->ownB_nnz, sc->ownA_off, sc->ownB_off, &off);
-  sc->peer_ownA_off.resize(ctx->nranks);
-  sc->peer_ownB_off.resize(ctx->nranks);
-  sc->peer_ownA_nnz.resize(ctx->nranks);
-  sc->peer_ownB_nnz.resize(ctx->nranks);
-  for (int q = 0; q < ctx->nranks && ctx->nranks > 1; ++q) {
-    size_t e;
-    if (q != me)
-      own_layout(ctx, A, B, L, q / pc, q % pc, sc->peer_ownA_nnz[q], sc->peer_ownB_nnz[q], sc->peer_ownA_off[q],
-                 sc->peer_ownB_off[q], &e);
-  }
-  // per-step panel metadata and entry counts
-  std::vector<int32_t> meta;
-  std::vector<int32_t> tli, tlj;
-  host_traversal(0, mloc, 0, nloc, tli, tlj);
-  const int64_t words = 0;
-  (void)words;
-  int64_t kbmax = 1, amax = 0, bmax = 0;
-  int na = 0, nb = 0;
-  sc->steps.resize(L);
-  for (int s = 0; s < L; ++s) {
-    SpStep& st = sc->steps[s];
-    st.kappa = (r + c + s) % L;
-    st.a_src = r * pc + st.kappa % pc;
-    st.b_src = (st.kappa % pr) * pc + c;
-    const int64_t kb = local_count(Kb, L, st.kappa);
-    kbmax = std::max(kbmax, kb);
-    // A panel CSR over li
-    std::vector<std::vector<uint64_t>> abits(mloc, std::vector<uint64_t>((kb + 63) / 64, 0));
-    st.o_aptr = meta.size();
-    meta.resize(meta.size() + mloc + 1);
-    std::vector<int32_t> akk;
-    for (int64_t li = 0; li < mloc; ++li) {
-      meta[st.o_aptr + li] = (int32_t)akk.size();
-      for (int64_t kk = 0; kk < kb; ++kk)
-        if (A->stored(r + li * pr, st.kappa + kk * L)) {
-          akk.push_back((int32_t)kk);
-          abits[li][kk >> 6] |= 1ull << (kk & 63);
-        }
-    }
-    meta[st.o_aptr + mloc] = (int32_t)akk.size();
-    st.a_nnz = (int64_t)akk.size();
-    st.o_akk = meta.size();
-    meta.insert(meta.end(), akk.begin(), akk.end());
-    // B panel: row-major slots over (kk, lj), CSC lists per lj
-    std::vector<std::vector<uint64_t>> bbits(nloc, std::vector<uint64_t>((kb + 63) / 64, 0));
-    std::vector<std::vector<std::pair<int32_t, int32_t>>> bcol(nloc);
-    int32_t slot = 0;
-    for (int64_t kk = 0; kk < kb; ++kk)
-      for (int64_t lj = 0; lj < nloc; ++lj)
-        if (B->stored(st.kappa + kk * L, c + lj * pc)) {
-          bcol[lj].push_back({(int32_t)kk, slot++});
-          bbits[lj][kk >> 6] |= 1ull << (kk & 63);
-        }
-    st.b_nnz = slot;
-    st.o_bptr = meta.size();
-    meta.resize(meta.size() + nloc + 1);
-    std::vector<int32_t> bkk, bsl;
-    for (int64_t lj = 0; lj < nloc; ++lj) {
-      meta[st.o_bptr + lj] = (int32_t)bkk.size();
-      for (auto& pr_ : bcol[lj]) {
-        bkk.push_back(pr_.first);
-        bsl.push_back(pr_.second);
-      }
-    }
-    meta[st.o_bptr + nloc] = (int32_t)bkk.size();
-    st.o_bkk = meta.size();
-    meta.insert(meta.end(), bkk.begin(), bkk.end());
-    st.o_bslot = meta.size();
-    meta.insert(meta.end(), bsl.begin(), bsl.end());
-    // run lengths in traversal order (stored C blocks only)
-    st.run_len.resize(tli.size());
-    for (size_t q = 0; q < tli.size(); ++q) {
-      const int64_t li = tli[q], lj = tlj[q];
-      int64_t n = 0;
-      if (C->stored(r + li * pr, c + lj * pc))
-        for (size_t w = 0; w < abits[li].size(); ++w) n += __builtin_popcountll(abits[li][w] & bbits[lj][w]);
-      st.run_len[q] = (int32_t)n;
-      st.entries += n;
-    }
-    if (st.a_src != me) {
-      amax = std::max(amax, st.a_nnz);
-      ++na;
-    }
-    if (st.b_src != me) {
-      bmax = std::max(bmax, st.b_nnz);
-      ++nb;
-    }
-  }
-  // gather lists of my own panels (multi-rank: packed into the workspace for the peers and myself)
-  sc->o_gatherA.assign(L, SIZE_MAX);
-  sc->o_gatherB.assign(L, SIZE_MAX);
-  for (int k = 0; k < L && ctx->nranks > 1; ++k) {
-    if (sc->ownA_nnz[k] >= 0) {
-      sc->o_gatherA[k] = meta.size();
-      for (int64_t li = 0; li < A->mloc; ++li)
-        for (int64_t kg = k; kg < Kb; kg += L)
-          if (A->stored(r + li * pr, kg)) meta.push_back((int32_t)local_slot(A, li, (kg - c) / pc));
-    }
-    if (sc->ownB_nnz[k] >= 0) {
-      sc->o_gatherB[k] = meta.size();
-      for (int64_t kg = k; kg < Kb; kg += L)
-        for (int64_t lj = 0; lj < B->nloc; ++lj)
-          if (B->stored(kg, c + lj * pc)) meta.push_back((int32_t)local_slot(B, (kg - r) / pr, lj));
-    }
-  }
-  // the rest of the workspace
-  auto take = [&](size_t bytes) {
-    size_t o = off;
-    off = align256(off + bytes);
-    return o;
-  };
-  for (int i = 0; i < std::min(na, 2); ++i) sc->off_recvA[i] = take((size_t)amax * bb8);
-  for (int i = 0; i < std::min(nb, 2); ++i) sc->off_recvB[i] = take((size_t)bmax * bb8);
-  const int64_t nruns = std::max<int64_t>(mloc * nloc, 1);
-  sc->off_trav = take((size_t)nruns * 8);
-  sc->runs_per_chunk = std::max<int64_t>(1, std::min<int64_t>(nruns, kTripChunkEntries / kbmax));
-  sc->off_cnt = take((size_t)(sc->runs_per_chunk + 1) * 8);
-  sc->off_off = take((size_t)(sc->runs_per_chunk + 1) * 8);
-  sc->scan_bytes = sp_scan_temp_bytes(sc->runs_per_chunk + 1);
-  sc->off_scan = take(sc->scan_bytes);
-  sc->off_trip = take((size_t)sc->runs_per_chunk * kbmax * 12);
-  sc->total = std::max<size_t>(off, 256);
-  for (SpStep& x : sc->steps) {
-    for (size_t q0 = 0; q0 < x.run_len.size(); q0 += (size_t)sc->runs_per_chunk) {
-      int64_t n = 0;
-      for (size_t q = q0; q < std::min(x.run_len.size(), q0 + (size_t)sc->runs_per_chunk); ++q) n += x.run_len[q];
-      x.chunk_entries.push_back(n);
-    }
-  }
-  cudaError_t e = cudaMalloc(&sc->d_meta, std::max<size_t>(meta.size(), 1) * 4);
-  if (e == cudaSuccess && !meta.empty())
-    e = cudaMemcpy(sc->d_meta, meta.data(), meta.size() * 4, cudaMemcpyHostToDevice);
-  if (e != cudaSuccess) {
-    if (sc->d_meta) cudaFree(sc->d_meta);
-    delete sc;
-    set_error(std::string("sparse plan metadata: ") + cudaGetErrorString(e));
-    return DBM_ERR_NOMEM;
-  }
-  ctx->sp_cache.push_back(sc);
-  *out = sc;
-  return DBM_OK;
-}
-
-int64_t sp_stacks(SpCache* sc, int64_t cap) {
-  for (auto& pcs : sc->stacks_by_cap)
-    if (pcs.first == cap) return pcs.second;
-  int64_t ns = 0;
-  for (const SpStep& st : sc->steps) {  // greedy whole-run packing, runs > cap split (reading R6)
-    int64_t cur = 0;
-    for (int32_t n : st.run_len) {
-      if (n == 0) continue;
-      if (n > cap) {
-        if (cur) ++ns;
-        cur = 0;
-        ns += (n + cap - 1) / cap;
-      } else {
-        if (cur + n > cap) {
-          ++ns;
-          cur = 0;
-        }
-        cur += n;
-      }
-    }
-    if (cur) ++ns;
-  }
-  sc->stacks_by_cap.push_back({cap, ns});
-  return ns;
-}
-
-dbm_status multiply_sparse_blocked(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_matrix B, double beta, dbm_matrix C,
-                                   int32_t stack_cap, void* workspace, int64_t ws_bytes, dbm_stats* stats) {
-  ARG_CHECK(ctx->nranks == 1 || ctx->transport == 0, DBM_ERR_ARG,
-            "the block-sparse blocked path uses the copy-engine transport");
-  SpCache* sc = nullptr;
-  if (dbm_status e = sp_cache_get(ctx, A, B, C, &sc)) return e;
-  ARG_CHECK(workspace != nullptr && ws_bytes >= (int64_t)sc->total, DBM_ERR_WORKSPACE,
-            "workspace smaller than dbm_multiply_workspace()");
-  const int64_t cap = stack_cap ? stack_cap : 30000;
-  cudaStream_t cs = ctx->stream;
-  char* ws = (char*)workspace;
-  const int bs = A->bs;
-  const int64_t bb = (int64_t)bs * bs, mloc = C->mloc, nloc = C->nloc, L = sc->L;
-  const int me = ctx->rank;
-  dbm_stats st{};
-  st.steps = L;
-  int launches = 0;
-  auto scale_c = [&](double f) -> dbm_status {
-    const int64_t n = C->blocks() * bb;
-    if (n && f != 1.0) {
-      scale_kernel<<<(unsigned)std::min<int64_t>((n + 255) / 256, num_sms() * 16), 256, 0, cs>>>(C->arena, n, f);
-      ++launches;
-      CUDA_TRY(ctx, cudaGetLastError());
-    }
-    return DBM_OK;
-  };
-  // beta scales every stored C block once (R15); the steps then accumulate alpha * A * B
-  if (dbm_status e = scale_c(beta)) return e;
-  if (alpha == 0.0 || A->Nb == 0) {
-    ctx->launches += launches;
-    st.kernel_launches = launches;
-    if (stats) *stats = st;
-    return DBM_OK;
-  }
-  const int32_t* meta = sc->d_meta;
-  if (ctx->nranks > 1) {  // pack my panels (stored blocks only)
-    for (int k = 0; k < L; ++k) {
-      if (sc->ownA_nnz[k] > 0) {
-        launch_sp_gather(A->arena, meta + sc->o_gatherA[k], sc->ownA_nnz[k], bs, (double*)(ws + sc->ownA_off[k]), cs);
-        ++launches;
-      }
-      if (sc->ownB_nnz[k] > 0) {
-        launch_sp_gather(B->arena, meta + sc->o_gatherB[k], sc->ownB_nnz[k], bs, (double*)(ws + sc->ownB_off[k]), cs);
-        ++launches;
-      }
-    }
-    CUDA_TRY(ctx, cudaGetLastError());
-  }
-  int32_t* trav_li = (int32_t*)(ws + sc->off_trav);
-  int32_t* trav_lj = trav_li + std::max<int64_t>(mloc * nloc, 1);
-  {
-    ProfScope ps(ctx, cs, 4, 0.0, 8.0 * mloc * nloc);
-    launch_traversal(mloc, nloc, trav_li, trav_lj, cs);
-    launches += (mloc * nloc) ? 1 : 0;
-  }
-  std::vector<cudaEvent_t> ev_x(L, nullptr), ev_g(L, nullptr);
-  cudaEvent_t ev_ready = nullptr;
-  std::vector<int> bufA(L, -1), bufB(L, -1);
-  auto pulls = [&](int s) -> dbm_status {
-    const SpStep& x = sc->steps[s];
-    ProfScope ps(ctx, ctx->comm, 5, 0.0,
-                 (double)(((x.a_src != me) ? x.a_nnz : 0) + ((x.b_src != me) ? x.b_nnz : 0)) * bb * 8);
-    if (x.a_src != me && x.a_nnz) {
-      CUDA_TRY(ctx, cudaMemcpyAsync(ws + sc->off_recvA[bufA[s]], ctx->peer_ws[x.a_src] + sc->peer_ownA_off[x.a_src][x.kappa],
-                                    (size_t)x.a_nnz * bb * 8, cudaMemcpyDeviceToDevice, ctx->comm));
-    }
-    if (x.b_src != me && x.b_nnz) {
-      CUDA_TRY(ctx, cudaMemcpyAsync(ws + sc->off_recvB[bufB[s]], ctx->peer_ws[x.b_src] + sc->peer_ownB_off[x.b_src][x.kappa],
-                                    (size_t)x.b_nnz * bb * 8, cudaMemcpyDeviceToDevice, ctx->comm));
-    }
-    if (x.a_src != me) st.bytes_recv += x.a_nnz * bb * 8;
-    if (x.b_src != me) st.bytes_recv += x.b_nnz * bb * 8;
-    for (int rr = 0; rr < ctx->pr; ++rr)  // what peers pull from me at this step (statistics)
-      for (int cc = 0; cc < ctx->pc; ++cc) {
-        const int dst = rr * ctx->pc + cc;
-        if (dst == me) continue;
-        const int k = (rr + cc + s) % (int)L;
-        if (rr == ctx->myrow && k % ctx->pc == ctx->mycol) st.bytes_sent += sc->ownA_nnz[k] * bb * 8;
-        if (cc == ctx->mycol && k % ctx->pr == ctx->myrow) st.bytes_sent += sc->ownB_nnz[k] * bb * 8;
-      }
-    return DBM_OK;
-  };
-  if (ctx->nranks > 1) {
-    int na = 0, nb = 0;
-    for (int s = 0; s < L; ++s) {
-      if (sc->steps[s].a_src != me) bufA[s] = na++ & 1;
-      if (sc->steps[s].b_src != me) bufB[s] = nb++ & 1;
-      ev_x[s] = get_event(ctx);
-      ev_g[s] = get_event(ctx);
-    }
-    ev_ready = get_event(ctx);
-    CUDA_TRY(ctx, cudaEventRecord(ev_ready, cs));
-    CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->comm, ev_ready, 0));
-    if (dbm_status e = ipc_exchange(ctx, ws)) return e;  // = barrier: every rank's panels are packed
-    if (dbm_status e = pulls(0)) return e;
-    CUDA_TRY(ctx, cudaEventRecord(ev_x[0], ctx->comm));
-  }
-  int64_t* cnt = (int64_t*)(ws + sc->off_cnt);
-  int64_t* offs = (int64_t*)(ws + sc->off_off);
-  int32_t* trip = (int32_t*)(ws + sc->off_trip);
-  for (int s = 0; s < L; ++s) {
-    const SpStep& x = sc->steps[s];
-    if (ctx->nranks > 1) {
-      if (s + 1 < L) {
-        if (s >= 1) CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->comm, ev_g[s - 1], 0));
-        if (dbm_status e = pulls(s + 1)) return e;
-        CUDA_TRY(ctx, cudaEventRecord(ev_x[s + 1], ctx->comm));
-      }
-      CUDA_TRY(ctx, cudaStreamWaitEvent(cs, ev_x[s], 0));
-    }
-    const double* Ap = ctx->nranks == 1 ? A->arena
-                       : x.a_src != me ? (const double*)(ws + sc->off_recvA[bufA[s]])
-                                       : (const double*)(ws + sc->ownA_off[x.kappa]);
-    const double* Bp = ctx->nranks == 1 ? B->arena
-                       : x.b_src != me ? (const double*)(ws + sc->off_recvB[bufB[s]])
-                                       : (const double*)(ws + sc->ownB_off[x.kappa]);
-    if (x.entries > 0) {
-      const int64_t nruns = mloc * nloc;
-      for (int64_t q0 = 0, ch = 0; q0 < nruns; q0 += sc->runs_per_chunk, ++ch) {
-        const int64_t n = std::min(sc->runs_per_chunk, nruns - q0);
-        const int64_t ent = x.chunk_entries[ch];
-        if (ent == 0) continue;
-        {
-          // algorithmic bytes: the two A/B run lists read per run, 12 B written per entry
-          ProfScope ps(ctx, cs, 4, 0.0, 12.0 * ent + 16.0 * n);
-          CUDA_TRY(ctx, launch_sp_stackgen(meta + x.o_aptr, meta + x.o_akk, meta + x.o_bptr, meta + x.o_bkk,
-                                           meta + x.o_bslot, C->sparse ? C->d_map : nullptr, nloc, trav_li, trav_lj, q0,
-                                           n, cnt, offs, ws + sc->off_scan, sc->scan_bytes, trip, cs));
-          launches += 3;
-        }
-        {
-          ProfScope ps(ctx, cs, 1, 2.0 * bs * bb * ent, 16.0 * bb * ent);
-          CUDA_TRY(ctx, launch_smm_sparse(bs, trip, offs, n, Ap, Bp, C->arena, alpha, cs));
-          ++launches;
-        }
-      }
-    }
-    st.entries += x.entries;
-    st.flops += 2.0 * bs * bb * x.entries;
-    if (ctx->nranks > 1) CUDA_TRY(ctx, cudaEventRecord(ev_g[s], cs));
-  }
-  st.stacks = sp_stacks(sc, cap);
-  if (ctx->nranks > 1) {
-    CUDA_TRY(ctx, cudaStreamWaitEvent(cs, ev_x[L - 1], 0));
-    int* w = ctx->d_scratch;
-    NCCL_TRY(ctx, ncclAllReduce(w, w, 1, ncclInt, ncclSum, (ncclComm_t)ctx->nccl, cs));
-    cudaEvent_t done = get_event(ctx);
-    CUDA_TRY(ctx, cudaEventRecord(done, cs));
-    ctx->ev_pool.push_back(ev_ready);
-    for (int s = 0; s < L; ++s) {
-      ctx->ev_pool.push_back(ev_x[s]);
-      ctx->ev_pool.push_back(ev_g[s]);
-    }
-    ctx->ev_pool.push_back(done);
-  }
-  ctx->launches += launches;
-  st.kernel_launches = launches;
-  if (stats) *stats = st;
-  return DBM_OK;
-}
-
-// DBM_PATH_AUTO -> blocked / densified (should_densify)
-dbm_path resolve_path(dbm_ctx ctx, dbm_matrix A, dbm_matrix B, dbm_path path) {
-  if (path != DBM_PATH_AUTO) return path;
-  auto occ = [](dbm_matrix m) { return m->Mb * m->Nb ? (double)m->gnnz / (double)(m->Mb * m->Nb) : 1.0; };
-  return (occ(A) >= ctx->densify_threshold && occ(B) >= ctx->densify_threshold) ? DBM_PATH_DENSIFIED
-                                                                                : DBM_PATH_BLOCKED;
-}
-
 }  // namespace
+
+
 
 extern "C" dbm_status dbm_multiply_workspace(dbm_ctx ctx, dbm_matrix A, dbm_matrix B, dbm_matrix C, dbm_path path,
                                              int64_t* bytes) {
@@ -1786,13 +1037,10 @@ extern "C" dbm_status dbm_multiply_workspace(dbm_ctx ctx, dbm_matrix A, dbm_matr
   if (dbm_status s = validate(ctx, A, B, C)) return s;
   path = resolve_path(ctx, A, B, path);
   if (path == DBM_PATH_BLOCKED && (A->sparse || B->sparse || C->sparse)) {
-    SpCache* sc = nullptr;
-    if (dbm_status e = sp_cache_get(ctx, A, B, C, &sc)) return e;
-    *bytes = (int64_t)sc->total;
-    return DBM_OK;
+    return sp_workspace_bytes(ctx, A, B, C, bytes);
   }
   if (ctx->algorithm == 1 && ctx->nranks > 1)
-    *bytes = (int64_t)make_ts_plan(ctx->pr, ctx->pc, ctx->myrow, ctx->mycol, A->Mb, B->Nb, A->Nb, A->bs).total;
+    *bytes = (int64_t)ts_workspace_bytes(ctx->pr, ctx->pc, ctx->myrow, ctx->mycol, A->Mb, B->Nb, A->Nb, A->bs);
   else
     *bytes = (int64_t)make_plan(ctx, A, B, C, path == DBM_PATH_DENSIFIED).total;
   return DBM_OK;
@@ -1803,7 +1051,7 @@ extern "C" dbm_status dbm_plan_tallskinny(int pr, int pc, int myrow, int mycol, 
   ARG_CHECK(bytes_recv && bytes_sent && pr > 0 && pc > 0 && myrow >= 0 && myrow < pr && mycol >= 0 && mycol < pc &&
                 bs > 0 && Mb >= 0 && Nb >= 0 && Kb >= 0,
             DBM_ERR_ARG, "bad arguments");
-  ts_bytes(make_ts_plan(pr, pc, myrow, mycol, Mb, Nb, Kb, bs), bytes_recv, bytes_sent);
+  ts_plan_bytes(pr, pc, myrow, mycol, Mb, Nb, Kb, bs, bytes_recv, bytes_sent);
   return DBM_OK;
 }
 
@@ -1910,8 +1158,8 @@ dbm_status multiply_impl(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_matrix B, 
   if (ctx->algorithm == 1 && ctx->nranks > 1) {
     ARG_CHECK(dens, DBM_ERR_ARG, "the tall-and-skinny algorithm runs the densified local multiply");
     ARG_CHECK(ctx->transport == 0, DBM_ERR_ARG, "the tall-and-skinny algorithm uses the copy-engine transport");
-    const TSPlan t = make_ts_plan(ctx->pr, ctx->pc, ctx->myrow, ctx->mycol, A->Mb, B->Nb, A->Nb, A->bs);
-    ARG_CHECK(workspace != nullptr && ws_bytes >= (int64_t)t.total, DBM_ERR_WORKSPACE,
+    const size_t ts_total = ts_workspace_bytes(ctx->pr, ctx->pc, ctx->myrow, ctx->mycol, A->Mb, B->Nb, A->Nb, A->bs);
+    ARG_CHECK(workspace != nullptr && ws_bytes >= (int64_t)ts_total, DBM_ERR_WORKSPACE,
               "workspace smaller than dbm_multiply_workspace()");
     dbm_stats st{};
     int launches = 0;
@@ -1926,8 +1174,7 @@ dbm_status multiply_impl(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_matrix B, 
     if (alpha == 0.0 || A->Nb == 0) {
       const int64_t n = C->blocks() * (int64_t)C->bs * C->bs;
       if (n) {
-        scale_kernel<<<(unsigned)std::min<int64_t>((n + 255) / 256, num_sms() * 16), 256, 0, ctx->stream>>>(C->arena, n,
-                                                                                                          beta);
+        launch_scale(C->arena, n, beta, ctx->stream);
         ++launches;
         CUDA_TRY(ctx, cudaGetLastError());
       }
@@ -1999,7 +1246,7 @@ dbm_status multiply_impl(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_matrix B, 
   if (alpha == 0.0 || p.Kb == 0) {
     const int64_t n = C->blocks() * bb;
     if (n) {
-      scale_kernel<<<(unsigned)std::min<int64_t>((n + 255) / 256, num_sms() * 16), 256, 0, cs>>>(C->arena, n, beta);
+      launch_scale(C->arena, n, beta, cs);
       ++launches;
       CUDA_TRY(ctx, cudaGetLastError());
     }
@@ -2054,7 +1301,7 @@ dbm_status multiply_impl(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_matrix B, 
   // ------------------------------------------------ Cannon steps
   std::vector<cudaEvent_t> ev_x(p.L, nullptr), ev_g(p.L, nullptr);
   cudaEvent_t ev_ready = nullptr;
-  int bufA_of[64], bufB_of[64];
+  std::vector<int> bufA_of(p.L, -1), bufB_of(p.L, -1);
   std::vector<Plan> peer_plan;
   int nsub0 = 1;               // K-chunks of the step-0 pull (copy-engine transport, densified)
   cudaEvent_t ev_c[kMaxChunks] = {};
@@ -2261,8 +1508,7 @@ dbm_status multiply_impl(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_matrix B, 
       st.flops += 2.0 * bs * bb * nruns * kbk;
     } else if (s == 0 && p.mloc * p.nloc > 0) {
       // empty K panel at step 0 still applies beta exactly once
-      const int64_t n = M * N;
-      scale_kernel<<<(unsigned)std::min<int64_t>((n + 255) / 256, num_sms() * 16), 256, 0, cs>>>(C->arena, n, beta);
+      launch_scale(C->arena, M * N, beta, cs);
       ++launches;
     }
     CUDA_TRY(ctx, cudaGetLastError());
@@ -2315,57 +1561,8 @@ extern "C" dbm_status dbm_debug_stacks(dbm_ctx ctx, dbm_matrix A, dbm_matrix B, 
   CTX_OK(ctx);
   if (dbm_status s = validate(ctx, A, B, C)) return s;
   ARG_CHECK(n_entries && n_stacks, DBM_ERR_ARG, "null size outputs");
-  if (A->sparse || B->sparse || C->sparse) {
-    SpCache* sc = nullptr;
-    if (dbm_status e = sp_cache_get(ctx, A, B, C, &sc)) return e;
-    ARG_CHECK(step >= 0 && step < sc->L, DBM_ERR_RANGE, "step out of range");
-    const SpStep& x = sc->steps[step];
-    const int64_t capv = cap ? cap : 30000;
-    std::vector<int64_t> ptr{0};
-    int64_t e = 0, cur = 0;
-    for (int32_t n : x.run_len) {  // greedy whole-run packing (as sp_stacks), recording the boundaries
-      if (n == 0) continue;
-      if (n > capv) {
-        if (cur) ptr.push_back(e);
-        cur = 0;
-        for (int64_t done = 0; done < n;) {
-          done += std::min<int64_t>(capv, n - done);
-          ptr.push_back(e + done);
-        }
-      } else {
-        if (cur + n > capv) {
-          ptr.push_back(e);
-          cur = 0;
-        }
-        cur += n;
-      }
-      e += n;
-    }
-    if (cur) ptr.push_back(e);
-    *n_entries = x.entries;
-    *n_stacks = (int64_t)ptr.size() - 1;
-    if (stack_ptr) std::memcpy(stack_ptr, ptr.data(), ptr.size() * 8);
-    if (!triplets || x.entries == 0) return DBM_OK;
-    const int64_t nruns = C->mloc * C->nloc;
-    const size_t scan_bytes = sp_scan_temp_bytes(nruns + 1);
-    char* d = nullptr;
-    const size_t o_cnt = align256((size_t)nruns * 8), o_off = o_cnt + align256((size_t)(nruns + 1) * 8),
-                 o_scan = o_off + align256((size_t)(nruns + 1) * 8), o_trip = o_scan + align256(scan_bytes),
-                 total = o_trip + (size_t)x.entries * 12;
-    CUDA_TRY(ctx, cudaMalloc(&d, total));
-    int32_t* li = (int32_t*)d;
-    launch_traversal(C->mloc, C->nloc, li, li + nruns, ctx->stream);
-    const int32_t* meta = sc->d_meta;
-    CUDA_TRY(ctx, launch_sp_stackgen(meta + x.o_aptr, meta + x.o_akk, meta + x.o_bptr, meta + x.o_bkk,
-                                     meta + x.o_bslot, C->sparse ? C->d_map : nullptr, C->nloc, li, li + nruns, 0,
-                                     nruns, (int64_t*)(d + o_cnt), (int64_t*)(d + o_off), d + o_scan, scan_bytes,
-                                     (int32_t*)(d + o_trip), ctx->stream));
-    ctx->launches += 4;
-    CUDA_TRY(ctx, cudaMemcpyAsync(triplets, d + o_trip, (size_t)x.entries * 12, cudaMemcpyDeviceToHost, ctx->stream));
-    CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
-    cudaFree(d);
-    return DBM_OK;
-  }
+  if (A->sparse || B->sparse || C->sparse)
+    return sp_debug_stacks(ctx, A, B, C, step, cap, triplets, n_entries, stack_ptr, n_stacks);
   const Plan p = make_plan(ctx, A, B, C, false);
   ARG_CHECK(step >= 0 && step < p.L, DBM_ERR_RANGE, "step out of range");
   const int64_t capv = cap ? cap : 30000;

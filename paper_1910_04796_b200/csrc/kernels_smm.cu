@@ -48,14 +48,6 @@ struct SmmCfg {
 // bs 64: padded pitches 72 / 36 (both conflict-free), half a block of K per stage
 using Cfg64 = SmmCfg<64, 2, 2, 2, 4, 4, 32, 72, 36, 4>;
 
-__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, int src_bytes) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(src_bytes) : "memory");
-}
-__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_wait() {
-  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
-}
 __device__ __forceinline__ double lds64(uint32_t a) {
   double v;
   asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a));
@@ -93,9 +85,6 @@ __device__ __forceinline__ void mbar_arrive(uint32_t a) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(a) : "memory");
 }
 // arrive on the mbarrier when all of this thread's prior cp.async have landed
-__device__ __forceinline__ void cp_async_mbar_arrive(uint32_t a) {
-  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(a) : "memory");
-}
 __device__ __forceinline__ void mbar_wait(uint32_t a, uint32_t parity) {
   uint32_t done;
   do {
@@ -136,7 +125,7 @@ __global__ void __launch_bounds__(Cfg::THREADS + 32, 1)
   constexpr int CA = KS * (BS / 2);  // 16-B chunks per A slot: KS columns x BS/2
   constexpr int CB = BS * (KS / 2);  // per B slot: BS rows x KS/2
   static_assert(CA == CB, "equal chunk counts");
-  extern __shared__ __align__(16) double smem[];
+  extern __shared__ __align__(128) double smem[];
   __shared__ __align__(8) uint64_t full[STAGES], empty[STAGES];
   __shared__ int s_rep[P];  // representative run (in group) of each pool slot
   __shared__ int s_isb[P];  // slot holds a B block (else A)
@@ -213,7 +202,7 @@ __global__ void __launch_bounds__(Cfg::THREADS + 32, 1)
       if (producer) {
         // ---------------- producer: nst stages of this sub-group
         // lane l < nslots*KKS owns (slot u = l / KKS, block kk = kk_first + l % KKS)
-        const int my_u = lane / KKS, my_j = lane - (lane / KKS) * KKS;
+        const int my_u = lane / KKS;
         const bool owner = lane < nslots * KKS;
         const int64_t my_q = q0 + (owner ? s_rep[my_u] : 0);
         const int my_col = owner ? s_isb[my_u] : 0;

@@ -566,7 +566,7 @@ __device__ __forceinline__ void tma2d(uint32_t dst, const CUtensorMap* tm, int c
 __global__ void __launch_bounds__((s64::WARPS + 1) * 32, 1)
     smm64_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                  const int32_t* __restrict__ trip, int64_t nruns, int64_t kb, double* __restrict__ C, double alpha,
-                 double beta_first) {
+                 double beta_first, int nsplit, double* __restrict__ partial) {
   using namespace s64;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
@@ -598,7 +598,12 @@ __global__ void __launch_bounds__((s64::WARPS + 1) * 32, 1)
   auto kof = [&](int ks) { return 16 * (ks >> 2) + 2 * (ks & 3) + (t & 1) + 8 * (t >> 1); };
   int stage = 0;
   uint32_t phase = 0;
-  for (int64_t grp = blockIdx.x; grp < ngroups; grp += gridDim.x) {
+  // work item = (group, K split); with nsplit > 1 each item accumulates stages [st0, st1) of its runs
+  // into `partial` (reduced later in a fixed order) instead of updating C
+  for (int64_t item = blockIdx.x; item < ngroups * nsplit; item += gridDim.x) {
+    const int64_t grp = item % ngroups;
+    const int split = (int)(item / ngroups);
+    const int st0 = (int)((int64_t)nst * split / nsplit), st1 = (int)((int64_t)nst * (split + 1) / nsplit);
     const int64_t q0 = grp * RUNS;
     const int n_g = (int)(nruns - q0 < RUNS ? nruns - q0 : RUNS);
     if (producer) {
@@ -627,7 +632,7 @@ __global__ void __launch_bounds__((s64::WARPS + 1) * 32, 1)
       const bool owner = lane < nslots;
       const int64_t q = q0 + (owner ? s_rep[lane] : 0);
       const int isb = owner ? s_isb[lane] : 0;
-      for (int st = 0; st < nst; ++st) {
+      for (int st = st0; st < st1; ++st) {
         const int kk = st >> 1, h = st & 1;
         const uint32_t fb = (uint32_t)__cvta_generic_to_shared(&full[stage]);
         if (lane == 0) {
@@ -659,7 +664,7 @@ __global__ void __launch_bounds__((s64::WARPS + 1) * 32, 1)
       for (int i = 0; i < 4; ++i)
 #pragma unroll
         for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-      for (int st = 0; st < nst; ++st) {
+      for (int st = st0; st < st1; ++st) {
         mbar_wait((uint32_t)__cvta_generic_to_shared(&full[stage]), phase);
         if (active) {
           const uint32_t sA = sbase + (uint32_t)(stage * STAGE + ia * SLOT) * 8u;
@@ -692,7 +697,8 @@ __global__ void __launch_bounds__((s64::WARPS + 1) * 32, 1)
         }
       }
       if (active) {
-        double* cb = C + (int64_t)trip[3 * ((q0 + run) * kb) + 2] * BB;
+        double* cb = partial ? partial + ((int64_t)split * nruns + q0 + run) * BB
+                             : C + (int64_t)trip[3 * ((q0 + run) * kb) + 2] * BB;
 #pragma unroll
         for (int mi = 0; mi < 4; ++mi)
 #pragma unroll
@@ -701,8 +707,12 @@ __global__ void __launch_bounds__((s64::WARPS + 1) * 32, 1)
             for (int j = 0; j < 2; ++j) {
               const int m = wm * 32 + mi * 8 + g, n = wn * 32 + ni * 8 + 2 * t + j;
               double* p = cb + m + n * BS;
-              const double v = alpha * acc[mi][ni][j];
-              *p = (beta_first == 0.0) ? v : beta_first * *p + v;
+              if (partial) {
+                *p = acc[mi][ni][j];
+              } else {
+                const double v = alpha * acc[mi][ni][j];
+                *p = (beta_first == 0.0) ? v : beta_first * *p + v;
+              }
             }
       }
     }
@@ -711,7 +721,8 @@ __global__ void __launch_bounds__((s64::WARPS + 1) * 32, 1)
 }
 
 cudaError_t launch_smm64(const int32_t* trip, int64_t nruns, int64_t kb, const double* A, const double* B, double* C,
-                         double alpha, double beta_first, int64_t a_blocks, int64_t b_blocks, cudaStream_t st) {
+                         double alpha, double beta_first, int nsplit, double* partial, int64_t a_blocks,
+                         int64_t b_blocks, cudaStream_t st) {
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(smm64_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s64::SMEM);
@@ -723,8 +734,15 @@ cudaError_t launch_smm64(const int32_t* trip, int64_t nruns, int64_t kb, const d
       !make_map_2d(&tmB, B, 64, (uint64_t)b_blocks * 64, 512, 16, 64))
     return cudaErrorInvalidValue;
   const int64_t ngroups = (nruns + s64::RUNS - 1) / s64::RUNS;
-  const unsigned grid = (unsigned)std::min<int64_t>(ngroups, (int64_t)num_sms());
-  smm64_kernel<<<grid, (s64::WARPS + 1) * 32, s64::SMEM, st>>>(tmA, tmB, trip, nruns, kb, C, alpha, beta_first);
+  if (nsplit < 1 || !partial) nsplit = 1;
+  const unsigned grid = (unsigned)std::min<int64_t>(ngroups * nsplit, (int64_t)num_sms());
+  smm64_kernel<<<grid, (s64::WARPS + 1) * 32, s64::SMEM, st>>>(tmA, tmB, trip, nruns, kb, C, alpha, beta_first, nsplit,
+                                                               nsplit > 1 ? partial : nullptr);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess || nsplit == 1) return e;
+  const int64_t n = nruns * s64::BB;
+  smm_splitk_reduce<<<(unsigned)std::min<int64_t>((n + 255) / 256, (int64_t)num_sms() * 16), 256, 0, st>>>(
+      trip, nruns, kb, s64::BB, nsplit, partial, C, alpha, beta_first);
   return cudaGetLastError();
 }
 
@@ -758,9 +776,10 @@ int smm_group_runs(int bs) { return bs == 22 ? s22::RUNS : (bs == 64 ? Cfg64::RU
 // Split the runs' K across CTAs when the groups alone cannot fill the GPU (long, few runs: the
 // rectangular configs on several GPUs).  Returns 1 when no split is needed.
 int smm_pick_split(int bs, int64_t nruns, int64_t kb) {
-  if (bs != 22) return 1;
-  const int64_t ngroups = (nruns + s22::RUNS - 1) / s22::RUNS, sms = num_sms();
-  const int64_t nst = (kb * s22::BS + s22::KS - 1) / s22::KS;
+  if (bs != 22 && bs != 64) return 1;
+  const int64_t sms = num_sms();
+  const int64_t ngroups = bs == 22 ? (nruns + s22::RUNS - 1) / s22::RUNS : (nruns + s64::RUNS - 1) / s64::RUNS;
+  const int64_t nst = bs == 22 ? (kb * s22::BS + s22::KS - 1) / s22::KS : kb * 2;
   if (ngroups >= 2 * sms) return 1;
   int best = 1;
   double best_t = 1e300;
@@ -781,7 +800,7 @@ cudaError_t launch_smm_tc(int bs, const int32_t* trip, int64_t nruns, int64_t kb
   if (nruns <= 0 || kb <= 0) return cudaSuccess;
   if (bs == 22) return launch_smm22(trip, nruns, kb, A, B, C, alpha, beta_first, nsplit, partial, st);
   if (bs == 64 && a_blocks > 0 && b_blocks > 0 && ((uintptr_t)A & 15) == 0 && ((uintptr_t)B & 15) == 0)
-    return launch_smm64(trip, nruns, kb, A, B, C, alpha, beta_first, a_blocks, b_blocks, st);
+    return launch_smm64(trip, nruns, kb, A, B, C, alpha, beta_first, nsplit, partial, a_blocks, b_blocks, st);
   if (bs == 64) return launch_group<Cfg64>(trip, nruns, kb, A, B, C, alpha, beta_first, st);
   return cudaErrorInvalidValue;
 }

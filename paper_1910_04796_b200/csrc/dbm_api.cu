@@ -681,15 +681,18 @@ Plan make_plan_raw(int nranks, int pr, int pc, int r, int c, int64_t Mb, int64_t
     p.off_trav = take((size_t)std::max<int64_t>(p.mloc * p.nloc, 1) * 8);
     int64_t maxkb = 1;
     for (int k = 0; k < p.L; ++k) maxkb = std::max(maxkb, p.kb[k]);
-    // chunks hold whole runs, a multiple of the smm group size (<= 8 runs), at least one group
-    const int64_t runs = std::max<int64_t>(8, kTripChunkEntries / maxkb / 8 * 8);
-    p.trip_cap = std::min<int64_t>(runs, round_up(std::max<int64_t>(p.mloc * p.nloc, 1), 8)) * maxkb;
+    // chunks hold whole runs, a multiple of the smm group size (8 runs, 16 for the 4 x 4 squares), at
+    // least one group
+    const int64_t runs = std::max<int64_t>(16, kTripChunkEntries / maxkb / 16 * 16);
+    p.trip_cap = std::min<int64_t>(runs, round_up(std::max<int64_t>(p.mloc * p.nloc, 1), 16)) * maxkb;
     p.off_trip = take((size_t)p.trip_cap * 12);
     // split-K partials of the smm kernel (rectangular shapes with few, long runs)
     const int64_t chunk_runs = std::max<int64_t>(1, std::min<int64_t>(p.mloc * p.nloc, p.trip_cap / maxkb));
     int64_t max_split = 1;
     for (int k = 0; k < p.L; ++k)
-      if (p.kb[k] > 0) max_split = std::max<int64_t>(max_split, smm_pick_split((int)bs, chunk_runs, p.kb[k]));
+      if (p.kb[k] > 0)
+        max_split = std::max<int64_t>({max_split, (int64_t)smm_pick_split((int)bs, chunk_runs, p.kb[k]),
+                                       (int64_t)smm_pick_split((int)bs, chunk_runs, p.kb[k], true)});
     if (max_split > 1) {
       p.spart_runs = max_split * chunk_runs;
       p.off_spart = take((size_t)p.spart_runs * bs * bs * 8);
@@ -1472,7 +1475,10 @@ dbm_status multiply_impl(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_matrix B, 
     } else if (kbk > 0 && p.mloc * p.nloc > 0) {
       // blocked: Generation (stack chunks) -> batched small-block GEMM
       const int64_t nruns = p.mloc * p.nloc;
-      const int64_t grp = smm_group_runs((int)bs);
+      // a dense local grid the bisection visits as whole 4 x 4 squares runs the unpadded bs-22 kernel;
+      // chunks of runs then hold whole squares
+      const bool squares = bs == 22 && bisection_squares(p.mloc, p.nloc);
+      const int64_t grp = squares ? 16 : smm_group_runs((int)bs);
       const int64_t runs_per_chunk = std::max<int64_t>(grp, p.trip_cap / kbk / grp * grp);
       const int64_t a_ld = kbk;  // A panel is mloc x kb blocks, row-major over (li, kk)
       // step 0 with a chunked pull: each K-chunk [k0, k1) of the panels multiplies as soon as it landed
@@ -1494,12 +1500,12 @@ dbm_status multiply_impl(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_matrix B, 
           }
           {
             ProfScope ps(ctx, cs, 1, 2.0 * bs * bb * (q1 - q0) * nk, 16.0 * bb * (q1 - q0) * nk);
-            const int nsplit = p.spart_runs ? (int)std::min<int64_t>(smm_pick_split((int)bs, q1 - q0, nk),
+            const int nsplit = p.spart_runs ? (int)std::min<int64_t>(smm_pick_split((int)bs, q1 - q0, nk, squares),
                                                                      p.spart_runs / (q1 - q0))
                                             : 1;
             CUDA_TRY(ctx, launch_smm((int)bs, trip, q1 - q0, nk, Aj, Bj, C->arena, alpha, bfirst, nsplit,
                                      nsplit > 1 ? (double*)(ws + p.off_spart) : nullptr, cs, &launches,
-                                     p.mloc * kbk - k0, (kbk - k0) * p.nloc));
+                                     p.mloc * kbk - k0, (kbk - k0) * p.nloc, squares));
           }
         }
       }

@@ -97,16 +97,21 @@ void launch_stack_ptr(int64_t nruns, int64_t kb, int64_t cap, int64_t nstacks, i
 // nsplit > 1 splits each run's K across CTAs (partial: nsplit*nruns*bs*bs doubles, reduced in a
 // fixed order); see smm_pick_split.
 // a_blocks / b_blocks: blocks in the A / B panels (tensor-map extents of the bs-64 kernel).
+// squares: the caller guarantees every 16 consecutive runs form a 4 x 4 square of C blocks with equal
+// K lists (bisection_squares() of a dense local grid): bs 22 then runs the unpadded 88 x 88 kernel.
 cudaError_t launch_smm(int bs, const int32_t* trip, int64_t nruns, int64_t kb, const double* A, const double* B,
                        double* C, double alpha, double beta_first, int nsplit, double* partial, cudaStream_t st,
-                       int* launches, int64_t a_blocks = 0, int64_t b_blocks = 0);
-int smm_pick_split(int bs, int64_t nruns, int64_t kb);
+                       int* launches, int64_t a_blocks = 0, int64_t b_blocks = 0, bool squares = false);
+int smm_pick_split(int bs, int64_t nruns, int64_t kb, bool squares = false);
+// True when the bisection traversal of an mloc x nloc grid (reading R6) visits it as whole 4 x 4 squares
+// of 16 consecutive runs (both sides keep halving evenly down to 4).
+bool bisection_squares(int64_t mloc, int64_t nloc);
 // DMMA group kernel for bs 22 / 64 (kernels_smm.cu); the generic smm handles other block sizes.
 bool smm_has_tensor_path(int bs);
 int smm_group_runs(int bs);  // runs per CTA group (stack chunks are cut at multiples of it)
 cudaError_t launch_smm_tc(int bs, const int32_t* trip, int64_t nruns, int64_t kb, const double* A, const double* B,
                           double* C, double alpha, double beta_first, int nsplit, double* partial, cudaStream_t st,
-                          int64_t a_blocks, int64_t b_blocks);
+                          int64_t a_blocks, int64_t b_blocks, bool squares);
 
 // ----------------------------------------------------------------- driver
 int num_sms();

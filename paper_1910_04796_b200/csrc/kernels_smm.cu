@@ -525,6 +525,219 @@ __global__ void __launch_bounds__((s22::WARPS + 1) * 32, 1)
   }
 }
 
+// ============================================================================ bs 22: 4 x 4 run squares
+// When 16 consecutive runs are a 4 x 4 square of C blocks (the bisection order of power-of-two-like
+// local grids: every rectangular config), they share 4 A block rows and 4 B block columns per k, and
+// their 88 x 88 C region is exactly 11 x 11 DMMA subtiles: no 22 -> 24 padding (the 8-run kernel above
+// wastes (24/22)^2 - 1 = 19 % of its DMMAs on it).  A stage = 2 k-blocks (44 k) of 4 A + 4 B blocks,
+// 16 TMA bulk copies from the producer warp.  The 121 subtiles go to 4 consumer warps, one per SM
+// sub-partition, as a pinwheel of 5 x 6 / 6 x 5 rectangles around the centre subtile (30, 30, 30, 31
+// DMMAs per k-step); with 160 threads a warp may hold the 60 accumulator doubles without spilling.
+namespace s22q {
+constexpr int BS = 22, BB = 484, KK = 2, KS = 44, RUNS = 16, WARPS = 4, STAGES = 2;
+constexpr int SLOT = KK * BB;                  // one block row / column over the stage's 2 k-blocks
+constexpr int STAGE = 8 * SLOT + 64;           // 4 A slots + 4 B slots (+ slack)
+constexpr int TP = 89;                         // pitch of the 88 x 88 C staging tile (column-major)
+constexpr size_t SMEM = (size_t)(STAGES * STAGE + 88 * TP) * 8;
+constexpr uint32_t BLK_BYTES = BB * 8;
+static_assert(SMEM + 1024 <= 232448, "shared memory");
+}  // namespace s22q
+
+// One warp's rectangle of subtiles: rows [r0, r0+R), cols [c0, c0+Cn) of the 11 x 11 grid.  A(M, k) of
+// the supertile lives in A slot M / 22 at (k / 22) * 484 + (k % 22) * 22 + M % 22; B(k, N) in B slot
+// 4 + N / 22 at (k / 22) * 484 + (N % 22) * 22 + k % 22.  No padding: every DMMA lane is a real element.
+template <int R, int Cn>
+__device__ __forceinline__ void s22q_consume(uint64_t* full, uint64_t* empty, uint32_t sbase, int& stage,
+                                             uint32_t& phase, int st0, int st1, int Krun, int r0, int c0,
+                                             bool centre, int g, int t, int lane, double* const (&s_dst)[4][4],
+                                             bool raw, double alpha, double beta_first, double* tile) {
+  using namespace s22q;
+  double acc[R][Cn][2], cacc[2] = {0.0, 0.0};
+#pragma unroll
+  for (int i = 0; i < R; ++i)
+#pragma unroll
+    for (int j = 0; j < Cn; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  uint32_t offA[R], offB[Cn];
+#pragma unroll
+  for (int i = 0; i < R; ++i) {  // this lane's supertile row in subtile row i: A slot M / 22, row M % 22
+    const int M = (r0 + i) * 8 + g;
+    offA[i] = (uint32_t)((M / BS) * SLOT + M % BS) * 8u;
+  }
+#pragma unroll
+  for (int j = 0; j < Cn; ++j) {  // this lane's supertile column in subtile column j: B slot 4 + N / 22
+    const int N = (c0 + j) * 8 + g;
+    offB[j] = (uint32_t)((4 + N / BS) * SLOT + (N % BS) * BS) * 8u;
+  }
+  const uint32_t offAc = (uint32_t)((40 + g) / BS * SLOT + (40 + g) % BS) * 8u;
+  const uint32_t offBc = (uint32_t)((4 + (40 + g) / BS) * SLOT + ((40 + g) % BS) * BS) * 8u;
+  for (int st = st0; st < st1; ++st) {
+    mbar_wait((uint32_t)__cvta_generic_to_shared(&full[stage]), phase);
+    const uint32_t sb = sbase + (uint32_t)(stage * STAGE) * 8u;
+    const int kvalid = Krun - st * KS;
+    const bool tail = kvalid < KS;
+    // not unrolled: fully unrolled, the compiler hoists every k-step's fragments and spills
+#pragma unroll 1
+    for (int ks = 0; ks < KS / 4; ++ks) {
+      const int k = 4 * ks + t;
+      const bool ok = !tail || k < kvalid;
+      // A slot: [k 0..43][m] at pitch 22 (the two blocks are contiguous); B slot: block k / 22, [n][k % 22]
+      const uint32_t ka = (uint32_t)(k * BS) * 8u, kbo = (uint32_t)(k + (k >= BS ? BB - BS : 0)) * 8u;
+      double a[R], b[Cn];
+#pragma unroll
+      for (int i = 0; i < R; ++i) a[i] = ok ? lds64(sb + offA[i] + ka) : 0.0;
+#pragma unroll
+      for (int j = 0; j < Cn; ++j) b[j] = ok ? lds64(sb + offB[j] + kbo) : 0.0;
+#pragma unroll
+      for (int i = 0; i < R; ++i)
+#pragma unroll
+        for (int j = 0; j < Cn; ++j) dmma(acc[i][j], a[i], b[j]);
+      if (centre) {
+        const double ac = ok ? lds64(sb + offAc + ka) : 0.0;
+        const double bc = ok ? lds64(sb + offBc + kbo) : 0.0;
+        dmma(cacc, ac, bc);
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive((uint32_t)__cvta_generic_to_shared(&empty[stage]));
+    if (++stage == STAGES) {
+      stage = 0;
+      phase ^= 1;
+    }
+  }
+  // epilogue: subtile (i, j), lane (g, t) holds C(M = 8 (r0 + i) + g, N = 8 (c0 + j) + 2t + jj).  The warp
+  // stages its rectangle in the shared 88 x 88 tile (immediate offsets, no per-element address math while
+  // the accumulators are live), then writes it back block by block.
+  double* tl = tile + (r0 * 8 + g) + (c0 * 8 + 2 * t) * TP;
+#pragma unroll
+  for (int i = 0; i < R; ++i)
+#pragma unroll
+    for (int j = 0; j < Cn; ++j) {
+      tl[i * 8 + (j * 8) * TP] = acc[i][j][0];
+      tl[i * 8 + (j * 8 + 1) * TP] = acc[i][j][1];
+    }
+  if (centre) {
+    tile[40 + g + (40 + 2 * t) * TP] = cacc[0];
+    tile[40 + g + (41 + 2 * t) * TP] = cacc[1];
+  }
+  __syncwarp();
+  auto writeback = [&](int Mr0, int Mn, int Nc0, int Nn) {  // rows [Mr0, Mr0+Mn) x cols [Nc0, Nc0+Nn)
+#pragma unroll 1
+    for (int e = lane; e < Mn * Nn; e += 32) {
+      const int M = Mr0 + e % Mn, N = Nc0 + e / Mn;
+      const int ri = M / BS, cj = N / BS;
+      double* p = s_dst[ri][cj] + (M - ri * BS) + (N - cj * BS) * BS;
+      const double v = tile[M + N * TP];
+      if (raw) {
+        *p = v;
+      } else {
+        const double w = alpha * v;
+        *p = (beta_first == 0.0) ? w : beta_first * *p + w;
+      }
+    }
+  };
+  writeback(r0 * 8, R * 8, c0 * 8, Cn * 8);
+  if (centre) writeback(40, 8, 40, 8);
+  __syncwarp();
+}
+
+__global__ void __launch_bounds__((s22q::WARPS + 1) * 32, 1)
+    smm22q_kernel(const int32_t* __restrict__ trip, int64_t nruns, int64_t kb, const double* __restrict__ A,
+                  const double* __restrict__ B, double* __restrict__ C, double alpha, double beta_first, int nsplit,
+                  double* __restrict__ partial) {
+  using namespace s22q;
+  extern __shared__ __align__(128) double smem[];
+  __shared__ __align__(8) uint64_t full[STAGES], empty[STAGES];
+  __shared__ int s_rowrep[4], s_colrep[4];
+  __shared__ double* s_dst[4][4];
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const bool producer = warp == WARPS;
+  const int Krun = (int)(kb * BS);
+  const int nst = (Krun + KS - 1) / KS;
+  const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(smem);
+  const int64_t ngroups = nruns / RUNS;  // the host launches this kernel only on whole squares
+  const int g = lane >> 2, t = lane & 3;
+
+  // pinwheel of the 11 x 11 subtiles around the centre (5, 5): warp 0 rows 0-4 x cols 0-5 (+ centre),
+  // warp 1 rows 0-5 x cols 6-10, warp 2 rows 6-10 x cols 5-10, warp 3 rows 5-10 x cols 0-4
+  const int r0 = warp == 0 ? 0 : warp == 1 ? 0 : warp == 2 ? 6 : 5;
+  const int c0 = warp == 0 ? 0 : warp == 1 ? 6 : warp == 2 ? 5 : 0;
+  const bool tall = warp == 1 || warp == 3;  // 6 x 5, else 5 x 6
+  const bool centre = warp == 0;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init((uint32_t)__cvta_generic_to_shared(&full[s]), 1);
+      mbar_init((uint32_t)__cvta_generic_to_shared(&empty[s]), WARPS);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  int stage = 0;
+  uint32_t phase = 0;
+  for (int64_t item = blockIdx.x; item < ngroups * nsplit; item += gridDim.x) {
+    const int64_t grp = item % ngroups;
+    const int split = (int)(item / ngroups);
+    const int st0 = (int)((int64_t)nst * split / nsplit), st1 = (int)((int64_t)nst * (split + 1) / nsplit);
+    const int64_t q0 = grp * RUNS;
+    if (producer) {  // rank the 16 runs' first A / B blocks: row ri, column cj of the square
+      const int64_t q = q0 + (lane & 15);
+      const int a0 = trip[3 * (q * kb)], b0 = trip[3 * (q * kb) + 1];
+      int ri = 0, cj = 0;
+      for (int o = 0; o < 16; ++o) {
+        const int ao = __shfl_sync(0xffffffffu, a0, o), bo = __shfl_sync(0xffffffffu, b0, o);
+        // count distinct smaller values (first occurrence of each value counts)
+        bool firsta = true, firstb = true;
+        for (int p2 = 0; p2 < o; ++p2) {
+          firsta &= __shfl_sync(0xffffffffu, a0, p2) != ao;
+          firstb &= __shfl_sync(0xffffffffu, b0, p2) != bo;
+        }
+        ri += (firsta && ao < a0) ? 1 : 0;
+        cj += (firstb && bo < b0) ? 1 : 0;
+      }
+      if (lane < 16) {
+        s_dst[ri][cj] = partial ? partial + ((int64_t)split * nruns + q) * BB : C + (int64_t)trip[3 * (q * kb) + 2] * BB;
+        if (cj == 0) s_rowrep[ri] = lane;
+        if (ri == 0) s_colrep[cj] = lane;
+      }
+    }
+    __syncthreads();
+    if (producer) {
+      // lane l < 16: l < 8 -> A row l / 2, block kk0 + (l & 1); else B column (l - 8) / 2
+      const int isb = lane >= 8 ? 1 : 0, u = (lane & 7) >> 1, j = lane & 1;
+      const bool owner = lane < 16;
+      const int64_t q = q0 + (owner ? (isb ? s_colrep[u] : s_rowrep[u]) : 0);
+      const double* base = isb ? B : A;
+      for (int st = st0; st < st1; ++st) {
+        const int kk = st * KK + j;
+        const bool valid = owner && kk < kb;
+        const uint32_t fb = (uint32_t)__cvta_generic_to_shared(&full[stage]);
+        if (lane == 0) mbar_wait((uint32_t)__cvta_generic_to_shared(&empty[stage]), phase ^ 1);
+        const unsigned vm = __ballot_sync(0xffffffffu, valid);
+        if (lane == 0) mbar_expect_tx(fb, (uint32_t)__popc(vm) * BLK_BYTES);
+        __syncwarp();
+        if (valid) {
+          const int64_t blk = trip[3 * (q * kb + kk) + isb];
+          bulk_g2s(sbase + (uint32_t)(stage * STAGE + (isb * 4 + u) * SLOT + j * BB) * 8u, base + blk * BB, BLK_BYTES,
+                   fb);
+        }
+        if (++stage == STAGES) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+    } else if (tall) {
+      s22q_consume<6, 5>(full, empty, sbase, stage, phase, st0, st1, Krun, r0, c0, centre, g, t, lane, s_dst,
+                         partial != nullptr, alpha, beta_first, smem + STAGES * STAGE);
+    } else {
+      s22q_consume<5, 6>(full, empty, sbase, stage, phase, st0, st1, Krun, r0, c0, centre, g, t, lane, s_dst,
+                         partial != nullptr, alpha, beta_first, smem + STAGES * STAGE);
+    }
+    __syncthreads();
+  }
+}
+
 // Fixed-order split-K reduction of the smm partials: C_blk = (first ? beta*C : C) + alpha * sum_s P_s.
 __global__ void smm_splitk_reduce(const int32_t* __restrict__ trip, int64_t nruns, int64_t kb, int bb, int nsplit,
                                   const double* __restrict__ partial, double* __restrict__ C, double alpha,
@@ -746,6 +959,27 @@ cudaError_t launch_smm64(const int32_t* trip, int64_t nruns, int64_t kb, const d
   return cudaGetLastError();
 }
 
+cudaError_t launch_smm22q(const int32_t* trip, int64_t nruns, int64_t kb, const double* A, const double* B, double* C,
+                          double alpha, double beta_first, int nsplit, double* partial, cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(smm22q_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s22q::SMEM);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  const int64_t ngroups = nruns / s22q::RUNS;
+  if (nsplit < 1 || !partial) nsplit = 1;
+  const unsigned grid = (unsigned)std::min<int64_t>(ngroups * nsplit, (int64_t)num_sms());
+  smm22q_kernel<<<grid, (s22q::WARPS + 1) * 32, s22q::SMEM, st>>>(trip, nruns, kb, A, B, C, alpha, beta_first, nsplit,
+                                                                  nsplit > 1 ? partial : nullptr);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess || nsplit == 1) return e;
+  const int64_t n = nruns * s22q::BB;
+  smm_splitk_reduce<<<(unsigned)std::min<int64_t>((n + 255) / 256, (int64_t)num_sms() * 16), 256, 0, st>>>(
+      trip, nruns, kb, s22q::BB, nsplit, partial, C, alpha, beta_first);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_smm22(const int32_t* trip, int64_t nruns, int64_t kb, const double* A, const double* B, double* C,
                          double alpha, double beta_first, int nsplit, double* partial, cudaStream_t st) {
   static bool attr = false;
@@ -775,10 +1009,18 @@ int smm_group_runs(int bs) { return bs == 22 ? s22::RUNS : (bs == 64 ? Cfg64::RU
 
 // Split the runs' K across CTAs when the groups alone cannot fill the GPU (long, few runs: the
 // rectangular configs on several GPUs).  Returns 1 when no split is needed.
-int smm_pick_split(int bs, int64_t nruns, int64_t kb) {
+bool bisection_squares(int64_t mloc, int64_t nloc) {
+  if (mloc == 4 && nloc == 4) return true;
+  if (mloc < 4 || nloc < 4) return false;
+  if (mloc >= nloc) return mloc % 2 == 0 && bisection_squares(mloc / 2, nloc);  // rows split on ties
+  return nloc % 2 == 0 && bisection_squares(mloc, nloc / 2);
+}
+
+int smm_pick_split(int bs, int64_t nruns, int64_t kb, bool squares) {
   if (bs != 22 && bs != 64) return 1;
   const int64_t sms = num_sms();
-  const int64_t ngroups = bs == 22 ? (nruns + s22::RUNS - 1) / s22::RUNS : (nruns + s64::RUNS - 1) / s64::RUNS;
+  const int64_t ngroups = bs == 22 ? (nruns + (squares ? s22q::RUNS : s22::RUNS) - 1) / (squares ? s22q::RUNS : s22::RUNS)
+                                   : (nruns + s64::RUNS - 1) / s64::RUNS;
   const int64_t nst = bs == 22 ? (kb * s22::BS + s22::KS - 1) / s22::KS : kb * 2;
   if (ngroups >= 2 * sms) return 1;
   int best = 1;
@@ -796,8 +1038,10 @@ int smm_pick_split(int bs, int64_t nruns, int64_t kb) {
 
 cudaError_t launch_smm_tc(int bs, const int32_t* trip, int64_t nruns, int64_t kb, const double* A, const double* B,
                           double* C, double alpha, double beta_first, int nsplit, double* partial, cudaStream_t st,
-                          int64_t a_blocks, int64_t b_blocks) {
+                          int64_t a_blocks, int64_t b_blocks, bool squares) {
   if (nruns <= 0 || kb <= 0) return cudaSuccess;
+  if (bs == 22 && squares && nruns % s22q::RUNS == 0)
+    return launch_smm22q(trip, nruns, kb, A, B, C, alpha, beta_first, nsplit, partial, st);
   if (bs == 22) return launch_smm22(trip, nruns, kb, A, B, C, alpha, beta_first, nsplit, partial, st);
   if (bs == 64 && a_blocks > 0 && b_blocks > 0 && ((uintptr_t)A & 15) == 0 && ((uintptr_t)B & 15) == 0)
     return launch_smm64(trip, nruns, kb, A, B, C, alpha, beta_first, nsplit, partial, a_blocks, b_blocks, st);

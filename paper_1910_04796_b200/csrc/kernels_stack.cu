@@ -133,12 +133,13 @@ void launch_stack_ptr(int64_t nruns, int64_t kb, int64_t cap, int64_t nstacks, i
 
 cudaError_t launch_smm(int bs, const int32_t* trip, int64_t nruns, int64_t kb, const double* A, const double* B,
                        double* C, double alpha, double beta_first, int nsplit, double* partial, cudaStream_t st,
-                       int* launches, int64_t a_blocks, int64_t b_blocks) {
+                       int* launches, int64_t a_blocks, int64_t b_blocks, bool squares) {
   if (nruns <= 0) return cudaSuccess;
   const unsigned grid = (unsigned)std::min<int64_t>(nruns, (int64_t)num_sms() * 8);
   if (smm_has_tensor_path(bs)) {
     cudaError_t e =
-        launch_smm_tc(bs, trip, nruns, kb, A, B, C, alpha, beta_first, nsplit, partial, st, a_blocks, b_blocks);
+        launch_smm_tc(bs, trip, nruns, kb, A, B, C, alpha, beta_first, nsplit, partial, st, a_blocks, b_blocks,
+                      squares);
     if (e != cudaSuccess) return e;
   } else {
     size_t smem = 2 * (size_t)bs * bs * sizeof(double);

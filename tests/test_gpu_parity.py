@@ -183,6 +183,9 @@ def test_multiply_matches_oracle(dbm, ctx, orc, path, M, N, K, bs):
 def test_multiply_integer_bit_exact(dbm, ctx, orc, path):
     got, ref, _ = run_multiply(dbm, ctx, orc, 704, 528, 1100, 22, path, 0.75, -1.25, kind=1)
     assert np.array_equal(got, ref)
+    # 32 x 32 blocks: the bisection visits 4 x 4 squares -> the unpadded 88 x 88 bs-22 kernel
+    got, ref, _ = run_multiply(dbm, ctx, orc, 704, 704, 1100, 22, path, 0.75, -1.25, kind=1)
+    assert np.array_equal(got, ref)
 
 
 def test_densified_k_chunking(dbm, ctx, orc):

@@ -530,11 +530,11 @@ __global__ void __launch_bounds__((s22::WARPS + 1) * 32, 1)
 // local grids: every rectangular config), they share 4 A block rows and 4 B block columns per k, and
 // their 88 x 88 C region is exactly 11 x 11 DMMA subtiles: no 22 -> 24 padding (the 8-run kernel above
 // wastes (24/22)^2 - 1 = 19 % of its DMMAs on it).  A stage = 2 k-blocks (44 k) of 4 A + 4 B blocks,
-// 16 TMA bulk copies from the producer warp.  The 121 subtiles go to 4 consumer warps, one per SM
-// sub-partition, as a pinwheel of 5 x 6 / 6 x 5 rectangles around the centre subtile (30, 30, 30, 31
-// DMMAs per k-step); with 160 threads a warp may hold the 60 accumulator doubles without spilling.
+// 16 TMA bulk copies from the producer warp.  The 121 subtiles go to the 4 SM sub-partitions
+// as a pinwheel of 5 x 6 / 6 x 5 rectangles around the centre subtile (30, 30, 30, 31
+// DMMAs per k-step), each rectangle split between the sub-partition's two warps (5 x 3 or 3 x 5).
 namespace s22q {
-constexpr int BS = 22, BB = 484, KK = 2, KS = 44, RUNS = 16, WARPS = 4, STAGES = 2;
+constexpr int BS = 22, BB = 484, KK = 2, KS = 44, RUNS = 16, WARPS = 8, STAGES = 2;
 constexpr int SLOT = KK * BB;                  // one block row / column over the stage's 2 k-blocks
 constexpr int STAGE = 8 * SLOT + 64;           // 4 A slots + 4 B slots (+ slack)
 constexpr int TP = 89;                         // pitch of the 88 x 88 C staging tile (column-major)
@@ -575,8 +575,7 @@ __device__ __forceinline__ void s22q_consume(uint64_t* full, uint64_t* empty, ui
     const uint32_t sb = sbase + (uint32_t)(stage * STAGE) * 8u;
     const int kvalid = Krun - st * KS;
     const bool tail = kvalid < KS;
-    // not unrolled: fully unrolled, the compiler hoists every k-step's fragments and spills
-#pragma unroll 1
+#pragma unroll
     for (int ks = 0; ks < KS / 4; ++ks) {
       const int k = 4 * ks + t;
       const bool ok = !tail || k < kvalid;
@@ -660,10 +659,12 @@ __global__ void __launch_bounds__((s22q::WARPS + 1) * 32, 1)
 
   // pinwheel of the 11 x 11 subtiles around the centre (5, 5): warp 0 rows 0-4 x cols 0-5 (+ centre),
   // warp 1 rows 0-5 x cols 6-10, warp 2 rows 6-10 x cols 5-10, warp 3 rows 5-10 x cols 0-4
-  const int r0 = warp == 0 ? 0 : warp == 1 ? 0 : warp == 2 ? 6 : 5;
-  const int c0 = warp == 0 ? 0 : warp == 1 ? 6 : warp == 2 ? 5 : 0;
-  const bool tall = warp == 1 || warp == 3;  // 6 x 5, else 5 x 6
-  const bool centre = warp == 0;
+  // (two warps per sub-partition: sp = warp % 4 owns a rectangle, h = warp / 4 one half of it)
+  const int sp = warp & 3, hh = warp >> 2;
+  const int r0 = sp == 0 ? 0 : sp == 1 ? 3 * hh : sp == 2 ? 6 : 5 + 3 * hh;
+  const int c0 = sp == 0 ? 3 * hh : sp == 1 ? 6 : sp == 2 ? 5 + 3 * hh : 0;
+  const bool tall = sp == 0 || sp == 2;  // 5 x 3, else 3 x 5
+  const bool centre = sp == 0 && hh == 1;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
@@ -728,10 +729,10 @@ __global__ void __launch_bounds__((s22q::WARPS + 1) * 32, 1)
         }
       }
     } else if (tall) {
-      s22q_consume<6, 5>(full, empty, sbase, stage, phase, st0, st1, Krun, r0, c0, centre, g, t, lane, s_dst,
+      s22q_consume<5, 3>(full, empty, sbase, stage, phase, st0, st1, Krun, r0, c0, centre, g, t, lane, s_dst,
                          partial != nullptr, alpha, beta_first, smem + STAGES * STAGE);
     } else {
-      s22q_consume<5, 6>(full, empty, sbase, stage, phase, st0, st1, Krun, r0, c0, centre, g, t, lane, s_dst,
+      s22q_consume<3, 5>(full, empty, sbase, stage, phase, st0, st1, Krun, r0, c0, centre, g, t, lane, s_dst,
                          partial != nullptr, alpha, beta_first, smem + STAGES * STAGE);
     }
     __syncthreads();

@@ -535,17 +535,29 @@ __global__ void __launch_bounds__((s22::WARPS + 1) * 32, 1)
 // DMMAs per k-step), each rectangle split between the sub-partition's two warps (5 x 3 or 3 x 5).
 namespace s22q {
 constexpr int BS = 22, BB = 484, KK = 2, KS = 44, RUNS = 16, WARPS = 8, STAGES = 2;
-constexpr int SLOT = KK * BB;                  // one block row / column over the stage's 2 k-blocks
-constexpr int STAGE = 8 * SLOT + 64;           // 4 A slots + 4 B slots (+ slack)
+constexpr int SLOT = KK * BB;                  // A slot: one block row over the stage's 2 k-blocks, [k][m]
+constexpr int BOFF = 4 * SLOT;                 // B slots follow the 4 A slots
+constexpr int SLOTB = 980;                     // B slot: [kk0 block][2 pad][kk1 block], stride = 4 (mod 16)
+constexpr int KK1B = BB + 2;                   // the kk1 block's offset inside a B slot
+constexpr int STAGE = BOFF + 4 * SLOTB;        // 7,792 doubles (a multiple of 16)
 constexpr int TP = 89;                         // pitch of the 88 x 88 C staging tile (column-major)
 constexpr size_t SMEM = (size_t)(STAGES * STAGE + 88 * TP) * 8;
 constexpr uint32_t BLK_BYTES = BB * 8;
 static_assert(SMEM + 1024 <= 232448, "shared memory");
 }  // namespace s22q
 
-// One warp's rectangle of subtiles: rows [r0, r0+R), cols [c0, c0+Cn) of the 11 x 11 grid.  A(M, k) of
-// the supertile lives in A slot M / 22 at (k / 22) * 484 + (k % 22) * 22 + M % 22; B(k, N) in B slot
-// 4 + N / 22 at (k / 22) * 484 + (N % 22) * 22 + k % 22.  No padding: every DMMA lane is a real element.
+// Subtile row i, fragment row g reads supertile row kQRowIdx[8i + g] (A offset kQRowOff); subtile column j,
+// fragment column g reads supertile column kQColIdx[8j + g] (B offset kQColOff, incl. the B region).  The
+// permutations group rows (m, m+1, m+8, m+9 of one block, or m, m+1 of two blocks 968 = 8 (mod 16)
+// doubles apart) and columns (residues 6n + base spaced by 4 (mod 16); B slots at bases 0, 4, 8, 12) so
+// that with the k-slot t of k-step ks reading k = 4 ks + t every half-warp's 64-bit fragment load hits
+// 16 distinct bank pairs (generated and checked by a script; no padding, so no wasted DMMA lane).
+__constant__ short kQRowOff[88] = {0, 1, 8, 9, 2, 3, 10, 11, 4, 5, 12, 13, 6, 7, 14, 15, 968, 969, 976, 977, 970, 971, 978, 979, 972, 973, 980, 981, 974, 975, 982, 983, 16, 17, 984, 985, 18, 19, 986, 987, 20, 21, 988, 989, 1936, 1937, 1944, 1945, 1938, 1939, 1946, 1947, 1940, 1941, 1948, 1949, 1942, 1943, 1950, 1951, 2904, 2905, 2912, 2913, 2906, 2907, 2914, 2915, 2908, 2909, 2916, 2917, 2910, 2911, 2918, 2919, 1952, 1953, 2920, 2921, 1954, 1955, 2922, 2923, 1956, 1957, 2924, 2925};
+__constant__ short kQRowIdx[88] = {0, 1, 8, 9, 2, 3, 10, 11, 4, 5, 12, 13, 6, 7, 14, 15, 22, 23, 30, 31, 24, 25, 32, 33, 26, 27, 34, 35, 28, 29, 36, 37, 16, 17, 38, 39, 18, 19, 40, 41, 20, 21, 42, 43, 44, 45, 52, 53, 46, 47, 54, 55, 48, 49, 56, 57, 50, 51, 58, 59, 66, 67, 74, 75, 68, 69, 76, 77, 70, 71, 78, 79, 72, 73, 80, 81, 60, 61, 82, 83, 62, 63, 84, 85, 64, 65, 86, 87};
+__constant__ short kQColOff[88] = {3872, 4004, 3960, 3916, 4048, 4180, 4136, 4092, 3938, 3894, 4026, 3982, 4114, 4070, 4202, 4158, 4852, 4984, 4940, 4896, 5028, 5160, 5116, 5072, 4918, 4874, 5006, 4962, 5094, 5050, 5182, 5138, 5832, 5964, 5920, 5876, 6008, 6140, 6096, 6052, 5898, 5854, 5986, 5942, 6074, 6030, 6162, 6118, 6812, 6944, 6900, 6856, 6988, 7120, 7076, 7032, 6878, 6834, 6966, 6922, 7054, 7010, 7142, 7098, 4224, 5204, 4312, 4268, 4290, 4246, 5226, 4334, 5292, 5248, 6228, 6184, 5270, 6250, 6206, 5314, 6272, 7252, 7208, 7164, 6294, 7274, 7230, 7186};
+__constant__ short kQColIdx[88] = {0, 6, 4, 2, 8, 14, 12, 10, 3, 1, 7, 5, 11, 9, 15, 13, 22, 28, 26, 24, 30, 36, 34, 32, 25, 23, 29, 27, 33, 31, 37, 35, 44, 50, 48, 46, 52, 58, 56, 54, 47, 45, 51, 49, 55, 53, 59, 57, 66, 72, 70, 68, 74, 80, 78, 76, 69, 67, 73, 71, 77, 75, 81, 79, 16, 38, 20, 18, 19, 17, 39, 21, 42, 40, 62, 60, 41, 63, 61, 43, 64, 86, 84, 82, 65, 87, 85, 83};
+
+// One warp's rectangle of subtiles: rows [r0, r0+R), cols [c0, c0+Cn) of the 11 x 11 grid.
 template <int R, int Cn>
 __device__ __forceinline__ void s22q_consume(uint64_t* full, uint64_t* empty, uint32_t sbase, int& stage,
                                              uint32_t& phase, int st0, int st1, int Krun, int r0, int c0,
@@ -559,17 +571,10 @@ __device__ __forceinline__ void s22q_consume(uint64_t* full, uint64_t* empty, ui
     for (int j = 0; j < Cn; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
   uint32_t offA[R], offB[Cn];
 #pragma unroll
-  for (int i = 0; i < R; ++i) {  // this lane's supertile row in subtile row i: A slot M / 22, row M % 22
-    const int M = (r0 + i) * 8 + g;
-    offA[i] = (uint32_t)((M / BS) * SLOT + M % BS) * 8u;
-  }
+  for (int i = 0; i < R; ++i) offA[i] = (uint32_t)kQRowOff[(r0 + i) * 8 + g] * 8u;
 #pragma unroll
-  for (int j = 0; j < Cn; ++j) {  // this lane's supertile column in subtile column j: B slot 4 + N / 22
-    const int N = (c0 + j) * 8 + g;
-    offB[j] = (uint32_t)((4 + N / BS) * SLOT + (N % BS) * BS) * 8u;
-  }
-  const uint32_t offAc = (uint32_t)((40 + g) / BS * SLOT + (40 + g) % BS) * 8u;
-  const uint32_t offBc = (uint32_t)((4 + (40 + g) / BS) * SLOT + ((40 + g) % BS) * BS) * 8u;
+  for (int j = 0; j < Cn; ++j) offB[j] = (uint32_t)kQColOff[(c0 + j) * 8 + g] * 8u;
+  const uint32_t offAc = (uint32_t)kQRowOff[40 + g] * 8u, offBc = (uint32_t)kQColOff[40 + g] * 8u;
   for (int st = st0; st < st1; ++st) {
     mbar_wait((uint32_t)__cvta_generic_to_shared(&full[stage]), phase);
     const uint32_t sb = sbase + (uint32_t)(stage * STAGE) * 8u;
@@ -579,8 +584,9 @@ __device__ __forceinline__ void s22q_consume(uint64_t* full, uint64_t* empty, ui
     for (int ks = 0; ks < KS / 4; ++ks) {
       const int k = 4 * ks + t;
       const bool ok = !tail || k < kvalid;
-      // A slot: [k 0..43][m] at pitch 22 (the two blocks are contiguous); B slot: block k / 22, [n][k % 22]
-      const uint32_t ka = (uint32_t)(k * BS) * 8u, kbo = (uint32_t)(k + (k >= BS ? BB - BS : 0)) * 8u;
+      // A slot: [k 0..43][m] at pitch 22 (the two blocks are contiguous); B slot: block k / 22 (the second
+      // at KK1B), [n][k % 22]
+      const uint32_t ka = (uint32_t)(k * BS) * 8u, kbo = (uint32_t)(k + (k >= BS ? KK1B - BS : 0)) * 8u;
       double a[R], b[Cn];
 #pragma unroll
       for (int i = 0; i < R; ++i) a[i] = ok ? lds64(sb + offA[i] + ka) : 0.0;
@@ -606,23 +612,24 @@ __device__ __forceinline__ void s22q_consume(uint64_t* full, uint64_t* empty, ui
   // epilogue: subtile (i, j), lane (g, t) holds C(M = 8 (r0 + i) + g, N = 8 (c0 + j) + 2t + jj).  The warp
   // stages its rectangle in the shared 88 x 88 tile (immediate offsets, no per-element address math while
   // the accumulators are live), then writes it back block by block.
-  double* tl = tile + (r0 * 8 + g) + (c0 * 8 + 2 * t) * TP;
 #pragma unroll
-  for (int i = 0; i < R; ++i)
+  for (int i = 0; i < R; ++i) {
+    const int M = kQRowIdx[(r0 + i) * 8 + g];
 #pragma unroll
-    for (int j = 0; j < Cn; ++j) {
-      tl[i * 8 + (j * 8) * TP] = acc[i][j][0];
-      tl[i * 8 + (j * 8 + 1) * TP] = acc[i][j][1];
-    }
-  if (centre) {
-    tile[40 + g + (40 + 2 * t) * TP] = cacc[0];
-    tile[40 + g + (41 + 2 * t) * TP] = cacc[1];
+    for (int j = 0; j < Cn; ++j)
+#pragma unroll
+      for (int jj = 0; jj < 2; ++jj) tile[M + kQColIdx[(c0 + j) * 8 + 2 * t + jj] * TP] = acc[i][j][jj];
   }
+  if (centre)
+#pragma unroll
+    for (int jj = 0; jj < 2; ++jj) tile[kQRowIdx[40 + g] + kQColIdx[40 + 2 * t + jj] * TP] = cacc[jj];
   __syncwarp();
-  auto writeback = [&](int Mr0, int Mn, int Nc0, int Nn) {  // rows [Mr0, Mr0+Mn) x cols [Nc0, Nc0+Nn)
+  // subtile rows [sr0, sr0+nr) x subtile cols [sc0, sc0+nc), through the permutations
+  auto writeback = [&](int sr0, int nr, int sc0, int nc) {
+    const int Mn = nr * 8, Nn = nc * 8;
 #pragma unroll 1
     for (int e = lane; e < Mn * Nn; e += 32) {
-      const int M = Mr0 + e % Mn, N = Nc0 + e / Mn;
+      const int M = kQRowIdx[sr0 * 8 + e % Mn], N = kQColIdx[sc0 * 8 + e / Mn];
       const int ri = M / BS, cj = N / BS;
       double* p = s_dst[ri][cj] + (M - ri * BS) + (N - cj * BS) * BS;
       const double v = tile[M + N * TP];
@@ -634,8 +641,8 @@ __device__ __forceinline__ void s22q_consume(uint64_t* full, uint64_t* empty, ui
       }
     }
   };
-  writeback(r0 * 8, R * 8, c0 * 8, Cn * 8);
-  if (centre) writeback(40, 8, 40, 8);
+  writeback(r0, R, c0, Cn);
+  if (centre) writeback(5, 1, 5, 1);
   __syncwarp();
 }
 
@@ -720,8 +727,8 @@ __global__ void __launch_bounds__((s22q::WARPS + 1) * 32, 1)
         __syncwarp();
         if (valid) {
           const int64_t blk = trip[3 * (q * kb + kk) + isb];
-          bulk_g2s(sbase + (uint32_t)(stage * STAGE + (isb * 4 + u) * SLOT + j * BB) * 8u, base + blk * BB, BLK_BYTES,
-                   fb);
+          const int off = isb ? BOFF + u * SLOTB + j * KK1B : u * SLOT + j * BB;
+          bulk_g2s(sbase + (uint32_t)(stage * STAGE + off) * 8u, base + blk * BB, BLK_BYTES, fb);
         }
         if (++stage == STAGES) {
           stage = 0;

@@ -1459,14 +1459,45 @@ dbm_status multiply_impl(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_matrix B, 
         for (int j = 0; j < nsub; ++j) {
           const int64_t k0 = nsub > 1 ? cb0[j] : 0, k1 = nsub > 1 ? cb0[j + 1] : kbk;
           if (nsub > 1) CUDA_TRY(ctx, cudaStreamWaitEvent(cs, ev_c[j], 0));
-          GemmArgs g{M, N, (k1 - k0) * bs, Ap + k0 * bs, ld, Bp + k0 * bs, ld, Cd, M, 1.0,
-                     (s == 0 && j == 0) ? 0.0 : 1.0, 1, nullptr};
-          g.splitk = std::min(pick_splitk(M, N, g.K, num_sms()), p.max_split);  // partial buffer bound
-          g.partial = g.splitk > 1 ? (double*)(ws + p.off_part) : nullptr;
-          ProfScope ps(ctx, cs, 0, 2.0 * M * N * g.K,
-                       8.0 * (M * g.K + N * g.K + M * N * ((s == 0 && j == 0) ? 1 : 2)));
-          CUDA_TRY(ctx, launch_dgemm(g, cs, &launches));
-          ++st.gemm_launches;
+          // host C: the multiply's last GEMM runs in row panels, each undensified and downloaded on the
+          // copy stream while the next panel multiplies (as on one rank)
+          const int pans = (hio && !C->sparse && s == p.L - 1 && j == nsub - 1 && p.mloc >= 8) ? 8 : 1;
+          for (int pn = 0; pn < pans; ++pn) {
+            const int64_t li0 = p.mloc * pn / pans, li1 = p.mloc * (pn + 1) / pans, m0 = li0 * bs, mr = (li1 - li0) * bs;
+            GemmArgs g{mr, N, (k1 - k0) * bs, Ap + m0 * ld + k0 * bs, ld, Bp + k0 * bs, ld, Cd + m0, M, 1.0,
+                       (s == 0 && j == 0) ? 0.0 : 1.0, 1, nullptr};
+            g.splitk = std::min(pick_splitk(g.M, N, g.K, num_sms()), p.max_split);  // partial buffer bound
+            g.partial = g.splitk > 1 ? (double*)(ws + p.off_part) : nullptr;
+            {
+              ProfScope ps(ctx, cs, 0, 2.0 * mr * N * g.K,
+                           8.0 * (mr * g.K + N * g.K + mr * N * ((s == 0 && j == 0) ? 1 : 2)));
+              CUDA_TRY(ctx, launch_dgemm(g, cs, &launches));
+            }
+            ++st.gemm_launches;
+            if (pans > 1) {
+              if (pn == 0 && hio->c_ev) CUDA_TRY(ctx, cudaStreamWaitEvent(cs, hio->c_ev, 0));  // C_in uploaded
+              {
+                ProfScope ps(ctx, cs, 3, 0.0, (beta == 0.0 ? 16.0 : 24.0) * mr * N);
+                launch_undensify(Cd + m0, M, 1, 0, li1 - li0, p.nloc, (int)bs, alpha, beta,
+                                 C->arena + li0 * p.nloc * bb, cs);
+                ++launches;
+              }
+              cudaEvent_t e = get_event(ctx);
+              CUDA_TRY(ctx, cudaEventRecord(e, cs));
+              hio->panel_ev.push_back(e);
+              CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->comm, e, 0));
+              const size_t off = (size_t)(li0 * p.nloc) * bb * 8, n = (size_t)((li1 - li0) * p.nloc) * bb * 8;
+              if (n) CUDA_TRY(ctx, cudaMemcpyAsync((char*)hio->C + off, (const char*)C->arena + off, n,
+                                                   cudaMemcpyDeviceToHost, ctx->comm));
+              hio->c_downloaded = true;
+            }
+          }
+        }
+        if (hio && hio->c_downloaded && s == p.L - 1) {  // the call ends when C is on the host
+          cudaEvent_t e = get_event(ctx);
+          CUDA_TRY(ctx, cudaEventRecord(e, ctx->comm));
+          hio->panel_ev.push_back(e);
+          CUDA_TRY(ctx, cudaStreamWaitEvent(cs, e, 0));
         }
         st.entries += (M && N) ? 1 : 0;  // densified batches hold one multiplication
         st.stacks += (M && N) ? 1 : 0;

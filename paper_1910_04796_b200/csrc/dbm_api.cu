@@ -593,6 +593,9 @@ struct Plan {
   // workspace regions (byte offsets)
   size_t off_cd = 0, off_ownA = 0, off_ownB = 0, off_recvA[2] = {0, 0}, off_recvB[2] = {0, 0}, off_part = 0;
   size_t off_trav = 0, off_trip = 0, off_spart = 0;  // smm split-K partials
+  bool mixed = false;                                 // bs 22 squares inside a non-square traversal
+  size_t off_pos = 0, off_sqflag = 0, off_sqids = 0, off_runsq = 0, off_runleft = 0, off_runflag = 0;
+  size_t off_counts = 0, off_mtemp = 0, mtemp_bytes = 0;
   int64_t spart_runs = 0;                            // capacity: (split x runs) C blocks
   std::vector<size_t> ownA_off, ownB_off;  // per kappa, SIZE_MAX if not owned
   int64_t trip_cap = 0;                     // entries per stack-generation chunk
@@ -696,6 +699,19 @@ Plan make_plan_raw(int nranks, int pr, int pc, int r, int c, int64_t Mb, int64_t
     if (max_split > 1) {
       p.spart_runs = max_split * chunk_runs;
       p.off_spart = take((size_t)p.spart_runs * bs * bs * 8);
+    }
+    p.mixed = bs == 22 && p.mloc >= 4 && p.nloc >= 4 && !bisection_squares(p.mloc, p.nloc);
+    if (p.mixed) {
+      const int64_t nsq = (p.mloc / 4) * (p.nloc / 4);
+      p.off_pos = take((size_t)p.mloc * p.nloc * 4);
+      p.off_sqflag = take((size_t)nsq);
+      p.off_sqids = take((size_t)nsq * 4);
+      p.off_runsq = take((size_t)chunk_runs * 4);
+      p.off_runleft = take((size_t)chunk_runs * 4);
+      p.off_runflag = take((size_t)chunk_runs);
+      p.off_counts = take(16);
+      p.mtemp_bytes = smm22_mixed_temp_bytes(std::max<int64_t>(nsq, chunk_runs));
+      p.off_mtemp = take(p.mtemp_bytes);
     }
   }
   if (nranks > 1) {
@@ -1299,6 +1315,10 @@ dbm_status multiply_impl(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_matrix B, 
     ProfScope ps(ctx, cs, 4, 0.0, 8.0 * p.mloc * p.nloc);
     launch_traversal(p.mloc, p.nloc, trav_li, trav_lj, cs);
     launches += (p.mloc * p.nloc) ? 1 : 0;
+    if (p.mixed) {
+      launch_inverse_traversal(trav_li, trav_lj, p.mloc * p.nloc, p.nloc, (int32_t*)(ws + p.off_pos), cs);
+      ++launches;
+    }
   }
 
   // ------------------------------------------------ Cannon steps
@@ -1534,9 +1554,18 @@ dbm_status multiply_impl(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_matrix B, 
             const int nsplit = p.spart_runs ? (int)std::min<int64_t>(smm_pick_split((int)bs, q1 - q0, nk, squares),
                                                                      p.spart_runs / (q1 - q0))
                                             : 1;
-            CUDA_TRY(ctx, launch_smm((int)bs, trip, q1 - q0, nk, Aj, Bj, C->arena, alpha, bfirst, nsplit,
-                                     nsplit > 1 ? (double*)(ws + p.off_spart) : nullptr, cs, &launches,
-                                     p.mloc * kbk - k0, (kbk - k0) * p.nloc, squares));
+            if (p.mixed && nsplit <= 1) {
+              const SmmMixedWS mw{(uint8_t*)(ws + p.off_sqflag), (int32_t*)(ws + p.off_sqids),
+                                  (int32_t*)(ws + p.off_runsq),   (int32_t*)(ws + p.off_runleft),
+                                  (uint8_t*)(ws + p.off_runflag), (int*)(ws + p.off_counts),
+                                  ws + p.off_mtemp,                p.mtemp_bytes};
+              CUDA_TRY(ctx, launch_smm22_mixed(trip, q0, q1 - q0, nk, Aj, Bj, C->arena, alpha, bfirst, trav_li, trav_lj,
+                                               (const int32_t*)(ws + p.off_pos), p.mloc, p.nloc, mw, cs, &launches));
+            } else {
+              CUDA_TRY(ctx, launch_smm((int)bs, trip, q1 - q0, nk, Aj, Bj, C->arena, alpha, bfirst, nsplit,
+                                       nsplit > 1 ? (double*)(ws + p.off_spart) : nullptr, cs, &launches,
+                                       p.mloc * kbk - k0, (kbk - k0) * p.nloc, squares));
+            }
           }
         }
       }

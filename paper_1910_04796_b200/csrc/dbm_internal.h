@@ -103,6 +103,26 @@ cudaError_t launch_smm(int bs, const int32_t* trip, int64_t nruns, int64_t kb, c
                        double* C, double alpha, double beta_first, int nsplit, double* partial, cudaStream_t st,
                        int* launches, int64_t a_blocks = 0, int64_t b_blocks = 0, bool squares = false);
 int smm_pick_split(int bs, int64_t nruns, int64_t kb, bool squares = false);
+// bs 22 on grids the bisection does not visit as whole squares: per chunk of runs [q0, q0+nruns), the
+// aligned 4 x 4 squares whose 16 runs are all in the chunk run on the unpadded kernel, the other runs on
+// the 8-run kernel (lists built on the GPU).  pos = inverse traversal (launch_inverse_traversal).
+struct SmmMixedWS {
+  uint8_t* sqflag;    // mloc/4 * nloc/4
+  int32_t* sq_ids;    // mloc/4 * nloc/4
+  int32_t* runs_sq;   // chunk runs
+  int32_t* runs_left; // chunk runs
+  uint8_t* runflag;   // chunk runs
+  int* counts;        // 4 ints
+  void* temp;
+  size_t temp_bytes;
+};
+void launch_inverse_traversal(const int32_t* li, const int32_t* lj, int64_t n, int64_t nloc, int32_t* pos,
+                              cudaStream_t st);
+size_t smm22_mixed_temp_bytes(int64_t n);
+cudaError_t launch_smm22_mixed(const int32_t* trip, int64_t q0, int64_t nruns, int64_t kb, const double* A,
+                               const double* B, double* C, double alpha, double beta_first, const int32_t* li,
+                               const int32_t* lj, const int32_t* pos, int64_t mloc, int64_t nloc, const SmmMixedWS& w,
+                               cudaStream_t st, int* launches);
 // True when the bisection traversal of an mloc x nloc grid (reading R6) visits it as whole 4 x 4 squares
 // of 16 consecutive runs (both sides keep halving evenly down to 4).
 bool bisection_squares(int64_t mloc, int64_t nloc);

@@ -16,6 +16,9 @@
 // ring; pitches are chosen so DMMA fragment loads are (near) conflict-free LDS.64.
 #include <algorithm>
 
+#include <cub/device/device_select.cuh>
+#include <cub/iterator/counting_input_iterator.cuh>
+
 #include "dbm_internal.h"
 
 namespace dbm {
@@ -65,10 +68,11 @@ struct Uniq {
   bool act;
 };
 __device__ __forceinline__ Uniq uniq(const int32_t* __restrict__ trip, int64_t q0, int s0, int n, int64_t kb,
-                                     int lane) {
+                                     int lane, const int32_t* __restrict__ runs = nullptr) {
   Uniq u;
   u.act = lane < n;
-  const int64_t q = q0 + s0 + lane;
+  const int64_t v = q0 + s0 + lane;
+  const int64_t q = (runs && u.act) ? runs[v] : v;
   const int a = u.act ? trip[3 * (q * kb)] : -1 - lane;
   const int b = u.act ? trip[3 * (q * kb) + 1] : -1 - lane;
   u.ma = __match_any_sync(0xffffffffu, a);
@@ -369,8 +373,12 @@ __device__ __forceinline__ void s22_stage(double (&acc)[3][3][2], uint32_t sA, u
 __global__ void __launch_bounds__((s22::WARPS + 1) * 32, 1)
     smm22_kernel(const int32_t* __restrict__ trip, int64_t nruns, int64_t kb, const double* __restrict__ A,
                  const double* __restrict__ B, double* __restrict__ C, double alpha, double beta_first, int nsplit,
-                 double* __restrict__ partial) {
+                 double* __restrict__ partial, const int32_t* __restrict__ runs, const int* __restrict__ d_count) {
+  // runs != nullptr: the runs to execute are runs[0 .. *d_count) (indices into the chunk's triplets),
+  // grouped 8 at a time in list order; otherwise runs 0 .. nruns-1
   using namespace s22;
+  if (d_count) nruns = *d_count;
+  auto RUN = [&](int64_t v) -> int64_t { return runs ? (int64_t)runs[v] : v; };
   extern __shared__ __align__(128) double smem[];
   __shared__ __align__(8) uint64_t full[STAGES], empty[STAGES];
   __shared__ int s_rep[P], s_isb[P], s_ia[RUNS], s_ib[RUNS], s_n, s_sub;
@@ -407,7 +415,7 @@ __global__ void __launch_bounds__((s22::WARPS + 1) * 32, 1)
       for (;;) {
         bool ok = true;
         for (int s0 = 0; s0 < nrun_g; s0 += sub) {
-          const Uniq u = uniq(trip, q0, s0, min(sub, nrun_g - s0), kb, lane);
+          const Uniq u = uniq(trip, q0, s0, min(sub, nrun_g - s0), kb, lane, runs);
           if (__popc(u.lead_a) + __popc(u.lead_b) > P) ok = false;
         }
         if (ok || sub == 1) break;
@@ -421,7 +429,7 @@ __global__ void __launch_bounds__((s22::WARPS + 1) * 32, 1)
       const int n_sub = min(sub, nrun_g - s0);
       if (s0 > 0) __syncthreads();
       if (producer) {
-        const Uniq u = uniq(trip, q0, s0, n_sub, kb, lane);
+        const Uniq u = uniq(trip, q0, s0, n_sub, kb, lane, runs);
         const int na = __popc(u.lead_a);
         if (u.act) {
           const int la = __ffs(u.ma) - 1, lb = __ffs(u.mb) - 1;
@@ -447,7 +455,7 @@ __global__ void __launch_bounds__((s22::WARPS + 1) * 32, 1)
         // lane l < 2*nslots copies block kk0 + (l & 1) of slot l >> 1
         const int u = lane >> 1, j = lane & 1;
         const bool owner = u < nslots;
-        const int64_t q = q0 + (owner ? s_rep[u] : 0);
+        const int64_t q = RUN(q0 + (owner ? s_rep[u] : 0));
         const int col = owner ? s_isb[u] : 0;
         const double* base = col ? B : A;
         for (int st = st0; st < st1; ++st) {
@@ -499,7 +507,7 @@ __global__ void __launch_bounds__((s22::WARPS + 1) * 32, 1)
       }
       if (active) {
         double* cb = partial ? partial + ((int64_t)split * nruns + q0 + warp) * BB
-                             : C + (int64_t)trip[3 * ((q0 + warp) * kb) + 2] * BB;
+                             : C + (int64_t)trip[3 * (RUN(q0 + warp) * kb) + 2] * BB;
 #pragma unroll
         for (int mi = 0; mi < 3; ++mi) {
           const int m = mi * 8 + g;
@@ -649,8 +657,11 @@ __device__ __forceinline__ void s22q_consume(uint64_t* full, uint64_t* empty, ui
 __global__ void __launch_bounds__((s22q::WARPS + 1) * 32, 1)
     smm22q_kernel(const int32_t* __restrict__ trip, int64_t nruns, int64_t kb, const double* __restrict__ A,
                   const double* __restrict__ B, double* __restrict__ C, double alpha, double beta_first, int nsplit,
-                  double* __restrict__ partial) {
+                  double* __restrict__ partial, const int32_t* __restrict__ runs, const int* __restrict__ d_count) {
+  // runs != nullptr: squares are runs[16 s .. 16 s + 16) for s < *d_count / 16; otherwise runs 16 s ..
   using namespace s22q;
+  if (d_count) nruns = *d_count;
+  auto RUN = [&](int64_t v) -> int64_t { return runs ? (int64_t)runs[v] : v; };
   extern __shared__ __align__(128) double smem[];
   __shared__ __align__(8) uint64_t full[STAGES], empty[STAGES];
   __shared__ int s_rowrep[4], s_colrep[4];
@@ -690,7 +701,7 @@ __global__ void __launch_bounds__((s22q::WARPS + 1) * 32, 1)
     const int st0 = (int)((int64_t)nst * split / nsplit), st1 = (int)((int64_t)nst * (split + 1) / nsplit);
     const int64_t q0 = grp * RUNS;
     if (producer) {  // rank the 16 runs' first A / B blocks: row ri, column cj of the square
-      const int64_t q = q0 + (lane & 15);
+      const int64_t q = RUN(q0 + (lane & 15));
       const int a0 = trip[3 * (q * kb)], b0 = trip[3 * (q * kb) + 1];
       int ri = 0, cj = 0;
       for (int o = 0; o < 16; ++o) {
@@ -715,7 +726,7 @@ __global__ void __launch_bounds__((s22q::WARPS + 1) * 32, 1)
       // lane l < 16: l < 8 -> A row l / 2, block kk0 + (l & 1); else B column (l - 8) / 2
       const int isb = lane >= 8 ? 1 : 0, u = (lane & 7) >> 1, j = lane & 1;
       const bool owner = lane < 16;
-      const int64_t q = q0 + (owner ? (isb ? s_colrep[u] : s_rowrep[u]) : 0);
+      const int64_t q = RUN(q0 + (owner ? (isb ? s_colrep[u] : s_rowrep[u]) : 0));
       const double* base = isb ? B : A;
       for (int st = st0; st < st1; ++st) {
         const int kk = st * KK + j;
@@ -968,7 +979,8 @@ cudaError_t launch_smm64(const int32_t* trip, int64_t nruns, int64_t kb, const d
 }
 
 cudaError_t launch_smm22q(const int32_t* trip, int64_t nruns, int64_t kb, const double* A, const double* B, double* C,
-                          double alpha, double beta_first, int nsplit, double* partial, cudaStream_t st) {
+                          double alpha, double beta_first, int nsplit, double* partial, cudaStream_t st,
+                          const int32_t* runs = nullptr, const int* d_count = nullptr) {
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(smm22q_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s22q::SMEM);
@@ -979,7 +991,7 @@ cudaError_t launch_smm22q(const int32_t* trip, int64_t nruns, int64_t kb, const 
   if (nsplit < 1 || !partial) nsplit = 1;
   const unsigned grid = (unsigned)std::min<int64_t>(ngroups * nsplit, (int64_t)num_sms());
   smm22q_kernel<<<grid, (s22q::WARPS + 1) * 32, s22q::SMEM, st>>>(trip, nruns, kb, A, B, C, alpha, beta_first, nsplit,
-                                                                  nsplit > 1 ? partial : nullptr);
+                                                                  nsplit > 1 ? partial : nullptr, runs, d_count);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess || nsplit == 1) return e;
   const int64_t n = nruns * s22q::BB;
@@ -989,7 +1001,8 @@ cudaError_t launch_smm22q(const int32_t* trip, int64_t nruns, int64_t kb, const 
 }
 
 cudaError_t launch_smm22(const int32_t* trip, int64_t nruns, int64_t kb, const double* A, const double* B, double* C,
-                         double alpha, double beta_first, int nsplit, double* partial, cudaStream_t st) {
+                         double alpha, double beta_first, int nsplit, double* partial, cudaStream_t st,
+                         const int32_t* runs = nullptr, const int* d_count = nullptr) {
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(smm22_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s22::SMEM);
@@ -1000,7 +1013,7 @@ cudaError_t launch_smm22(const int32_t* trip, int64_t nruns, int64_t kb, const d
   if (nsplit < 1 || !partial) nsplit = 1;
   const unsigned grid = (unsigned)std::min<int64_t>(ngroups * nsplit, (int64_t)num_sms());
   smm22_kernel<<<grid, (s22::WARPS + 1) * 32, s22::SMEM, st>>>(trip, nruns, kb, A, B, C, alpha, beta_first, nsplit,
-                                                               nsplit > 1 ? partial : nullptr);
+                                                               nsplit > 1 ? partial : nullptr, runs, d_count);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess || nsplit == 1) return e;
   const int64_t n = nruns * s22::BB;
@@ -1009,9 +1022,104 @@ cudaError_t launch_smm22(const int32_t* trip, int64_t nruns, int64_t kb, const d
   return cudaGetLastError();
 }
 
+
+// ---------------------------------------------------------------- squares inside other traversals
+// When the bisection does not visit the local grid as whole squares (63,360^3 bs 22: 2,880 = 64 x 45
+// blocks per side), the aligned 4 x 4 squares of C blocks whose 16 runs all lie in the current chunk of
+// runs are still executed by the unpadded kernel, through a list of their run indices; the remaining
+// runs go, in traversal order, to the 8-run kernel.  Lists are built with stable compactions (CUB
+// DeviceSelect), so the CTA work assignment, and the result, are deterministic.
+__global__ void inverse_traversal_kernel(const int32_t* __restrict__ li, const int32_t* __restrict__ lj, int64_t n,
+                                         int64_t nloc, int32_t* __restrict__ pos) {
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n; q += (int64_t)gridDim.x * blockDim.x)
+    pos[(int64_t)li[q] * nloc + lj[q]] = (int32_t)q;
+}
+
+__global__ void square_flags_kernel(const int32_t* __restrict__ pos, int64_t nloc, int64_t nsq, int64_t sqc,
+                                    int64_t q0, int64_t n, uint8_t* __restrict__ flag) {
+  for (int64_t sq = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; sq < nsq; sq += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t I = sq / sqc, J = sq - I * sqc;
+    bool in = true;
+    for (int a = 0; a < 4; ++a)
+      for (int b = 0; b < 4; ++b) {
+        const int64_t p = pos[(4 * I + a) * nloc + 4 * J + b];
+        in &= p >= q0 && p < q0 + n;
+      }
+    flag[sq] = in ? 1 : 0;
+  }
+}
+
+__global__ void leftover_flags_kernel(const int32_t* __restrict__ li, const int32_t* __restrict__ lj, int64_t q0,
+                                      int64_t n, int64_t sqr, int64_t sqc, const uint8_t* __restrict__ sqflag,
+                                      uint8_t* __restrict__ flag) {
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n; q += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t I = li[q0 + q] / 4, J = lj[q0 + q] / 4;
+    flag[q] = (I < sqr && J < sqc && sqflag[I * sqc + J]) ? 0 : 1;
+  }
+}
+
+__global__ void square_runs_kernel(const int32_t* __restrict__ pos, int64_t nloc, int64_t sqc,
+                                   const int32_t* __restrict__ sq_ids, const int* __restrict__ nsel, int64_t q0,
+                                   int32_t* __restrict__ runs, int* __restrict__ nruns16) {
+  const int64_t total = (int64_t)*nsel * 16;
+  if (blockIdx.x == 0 && threadIdx.x == 0) *nruns16 = (int)total;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t sq = sq_ids[e / 16], I = sq / sqc, J = sq - I * sqc;
+    const int r = (int)(e % 16);
+    runs[e] = (int32_t)(pos[(4 * I + r / 4) * nloc + 4 * J + r % 4] - q0);
+  }
+}
+
+inline unsigned mixed_grid(int64_t n) {
+  return (unsigned)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, (int64_t)num_sms() * 16));
+}
 }  // namespace
 
 bool smm_has_tensor_path(int bs) { return bs == 22 || bs == 64; }
+
+void launch_inverse_traversal(const int32_t* li, const int32_t* lj, int64_t n, int64_t nloc, int32_t* pos,
+                              cudaStream_t st) {
+  if (n > 0) inverse_traversal_kernel<<<mixed_grid(n), 256, 0, st>>>(li, lj, n, nloc, pos);
+}
+
+size_t smm22_mixed_temp_bytes(int64_t n) {
+  size_t b = 0;
+  cub::CountingInputIterator<int32_t> it(0);
+  cub::DeviceSelect::Flagged(nullptr, b, it, (const uint8_t*)nullptr, (int32_t*)nullptr, (int*)nullptr,
+                             (int)std::max<int64_t>(n, 1));
+  return b;
+}
+
+cudaError_t launch_smm22_mixed(const int32_t* trip, int64_t q0, int64_t nruns, int64_t kb, const double* A,
+                               const double* B, double* C, double alpha, double beta_first, const int32_t* li,
+                               const int32_t* lj, const int32_t* pos, int64_t mloc, int64_t nloc, const SmmMixedWS& w,
+                               cudaStream_t st, int* launches) {
+  if (nruns <= 0 || kb <= 0) return cudaSuccess;
+  const int64_t sqr = mloc / 4, sqc = nloc / 4, nsq = sqr * sqc;
+  cudaError_t e;
+  if (nsq > 0) {
+    square_flags_kernel<<<mixed_grid(nsq), 256, 0, st>>>(pos, nloc, nsq, sqc, q0, nruns, w.sqflag);
+    size_t tb = w.temp_bytes;
+    e = cub::DeviceSelect::Flagged(w.temp, tb, cub::CountingInputIterator<int32_t>(0), w.sqflag, w.sq_ids,
+                                   w.counts, (int)nsq, st);
+    if (e != cudaSuccess) return e;
+    square_runs_kernel<<<mixed_grid(nruns), 256, 0, st>>>(pos, nloc, sqc, w.sq_ids, w.counts, q0, w.runs_sq,
+                                                          w.counts + 1);
+    e = launch_smm22q(trip, nruns, kb, A, B, C, alpha, beta_first, 1, nullptr, st, w.runs_sq, w.counts + 1);
+    if (e != cudaSuccess) return e;
+    if (launches) *launches += 4;
+  } else {
+    cudaMemsetAsync(w.sqflag, 0, 1, st);
+  }
+  leftover_flags_kernel<<<mixed_grid(nruns), 256, 0, st>>>(li, lj, q0, nruns, sqr, sqc, w.sqflag, w.runflag);
+  size_t tb = w.temp_bytes;
+  e = cub::DeviceSelect::Flagged(w.temp, tb, cub::CountingInputIterator<int32_t>(0), w.runflag, w.runs_left,
+                                 w.counts + 2, (int)nruns, st);
+  if (e != cudaSuccess) return e;
+  e = launch_smm22(trip, nruns, kb, A, B, C, alpha, beta_first, 1, nullptr, st, w.runs_left, w.counts + 2);
+  if (launches) *launches += 3;
+  return e != cudaSuccess ? e : cudaGetLastError();
+}
 
 int smm_group_runs(int bs) { return bs == 22 ? s22::RUNS : (bs == 64 ? Cfg64::RUNS : 1); }
 

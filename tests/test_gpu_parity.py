@@ -327,3 +327,24 @@ def test_multiply_host_streamed(dbm, ctx, orc, path, pinned, chunk):
     orc.multiply_blocked(M // bs, N // bs, K // bs, bs, 0.75, orc.fill_arena(SEED, 0, 0, M, K, bs),
                          orc.fill_arena(SEED, 1, 0, K, N, bs), -1.25, ref)
     assert relerr(Ch.numpy(), ref) <= TOL
+
+
+@pytest.mark.parametrize("kind", [0, 1])
+def test_multiply_host_row_panels(dbm, ctx, orc, kind):
+    """Enough block rows (>= 8) that the last GEMM chunk runs in row panels whose undensify + download
+    overlap the next panel, with geometric upload chunks; beta != 0 reads C_host."""
+    M, N, K, bs = 704, 352, 1100, 22
+    hs = [torch.from_numpy(orc.fill_arena(SEED, i, kind, *sh, bs)).pin_memory()
+          for i, sh in enumerate(((M, K), (K, N), (M, N)))]
+    A, B, C = dbm.Matrix(ctx, M, K, bs), dbm.Matrix(ctx, K, N, bs), dbm.Matrix(ctx, M, N, bs)
+    ctx.set_dense_chunk_bytes((M + N) * bs * 8 * 7)
+    dbm.multiply_host(ctx, 0.75, A, B, -1.25, C, hs[0], hs[1], hs[2], "densified")
+    ctx.sync()
+    ctx.set_dense_chunk_bytes(16 << 30)
+    ref = orc.fill_arena(SEED, 2, kind, M, N, bs)
+    orc.multiply_blocked(M // bs, N // bs, K // bs, bs, 0.75, orc.fill_arena(SEED, 0, kind, M, K, bs),
+                         orc.fill_arena(SEED, 1, kind, K, N, bs), -1.25, ref)
+    if kind == 1:
+        assert np.array_equal(hs[2].numpy(), ref)
+    else:
+        assert relerr(hs[2].numpy(), ref) <= TOL

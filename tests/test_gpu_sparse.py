@@ -169,3 +169,22 @@ def test_sparse_determinism(dbm, ctx, orc):
         got, _, _, _ = run_sparse(dbm, ctx, orc, 704, 704, 704, 22, "blocked", 0.3, 0.3, 0.9, 1.0, 0.0)
         outs.append(got)
     assert np.array_equal(outs[0], outs[1])
+
+
+@pytest.mark.parametrize("path", ["blocked", "densified"])
+def test_sparse_multiply_host(dbm, ctx, orc, path):
+    """Host-resident sparse arenas through dbm_multiply_host (stored blocks only move)."""
+    M, N, K, bs = 352, 264, 440, 22
+    Mb, Nb, Kb = M // bs, N // bs, K // bs
+    am, bm, cm = orc.pattern_random(3, 0, Mb, Kb, 0.4), orc.pattern_random(3, 1, Kb, Nb, 0.4), \
+        orc.pattern_random(3, 2, Mb, Nb, 0.7)
+    Ag, Bg, Cg = (orc.fill_arena(SEED, i, 1, *sh, bs) for i, sh in enumerate(((M, K), (K, N), (M, N))))
+    hs = [torch.from_numpy(orc.sparse_compress(g, m, *d, bs)).pin_memory()
+          for g, m, d in ((Ag, am, (Mb, Kb)), (Bg, bm, (Kb, Nb)), (Cg, cm, (Mb, Nb)))]
+    A = dbm.Matrix(ctx, M, K, bs, mask=am)
+    B = dbm.Matrix(ctx, K, N, bs, mask=bm)
+    Cm = dbm.Matrix(ctx, M, N, bs, mask=cm)
+    dbm.multiply_host(ctx, 0.75, A, B, -1.25, Cm, hs[0], hs[1], hs[2], path)
+    ctx.sync()
+    orc.multiply_sparse(Mb, Nb, Kb, bs, 0.75, Ag, am, Bg, bm, -1.25, Cg, cm)
+    assert np.array_equal(hs[2].numpy(), orc.sparse_compress(Cg, cm, Mb, Nb, bs))

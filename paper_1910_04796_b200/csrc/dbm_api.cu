@@ -594,6 +594,9 @@ struct Plan {
   size_t off_cd = 0, off_ownA = 0, off_ownB = 0, off_recvA[2] = {0, 0}, off_recvB[2] = {0, 0}, off_part = 0;
   size_t off_trav = 0, off_trip = 0, off_spart = 0;  // smm split-K partials
   bool mixed = false;                                 // bs 22 squares inside a non-square traversal
+  // densified bs 64 with a dense B: B is never densified -- the GEMM reads B's 64 x 64 blocks in place
+  // (arena, or packed panels the peers pull), through a 4-D TMA view (§8f-3, zero-copy B)
+  bool b_packed = false;
   size_t off_pos = 0, off_sqflag = 0, off_sqids = 0, off_runsq = 0, off_runleft = 0, off_runflag = 0;
   size_t off_counts = 0, off_mtemp = 0, mtemp_bytes = 0;
   int64_t spart_runs = 0;                            // capacity: (split x runs) C blocks
@@ -621,8 +624,9 @@ struct Plan {
 
 // Host-only plan: depends on the grid, this rank's coordinates and the block counts (no CUDA).
 Plan make_plan_raw(int nranks, int pr, int pc, int r, int c, int64_t Mb, int64_t Nb, int64_t Kb, int64_t bs,
-                   bool densified, int64_t chunk_bytes, int transport) {
+                   bool densified, int64_t chunk_bytes, int transport, bool b_packed = false) {
   Plan p;
+  p.b_packed = b_packed;
   p.pr = pr;
   p.pc = pc;
   p.r = r;
@@ -658,7 +662,7 @@ Plan make_plan_raw(int nranks, int pr, int pc, int r, int c, int64_t Mb, int64_t
       p.nchunks = p.Kb > 0 ? (p.Kb + ck - 1) / ck : 1;
       const int64_t ld = round_up(ck * p.bs, 2);
       p.off_ownA = take((size_t)M * ld * 8);
-      p.off_ownB = take((size_t)N * ld * 8);
+      if (!b_packed) p.off_ownB = take((size_t)N * ld * 8);  // zero-copy B needs no dense B chunk
       p.max_split = pick_splitk(M, N, std::min<int64_t>(ck, std::max<int64_t>(p.Kb, 1)) * p.bs, num_sms());
     } else {
       for (int k = 0; k < p.L; ++k) {
@@ -737,7 +741,7 @@ Plan make_plan_raw(int nranks, int pr, int pc, int r, int c, int64_t Mb, int64_t
 Plan make_plan(dbm_ctx ctx, dbm_matrix A, dbm_matrix B, dbm_matrix C, bool densified) {
   (void)C;
   return make_plan_raw(ctx->nranks, ctx->pr, ctx->pc, ctx->myrow, ctx->mycol, A->Mb, B->Nb, A->Nb, A->bs, densified,
-                       ctx->chunk_bytes, ctx->transport);
+                       ctx->chunk_bytes, ctx->transport, densified && A->bs == 64 && !B->sparse && ctx->algorithm == 0);
 }
 
 // One Cannon exchange step as a list of point-to-point operations (owner-pull, reading R5):
@@ -1007,7 +1011,7 @@ dbm_status post_pulls_chunk(dbm_ctx ctx, const Plan& p, const std::vector<Plan>&
     const size_t bb8 = (size_t)p.bs * p.bs * 8;
     int64_t rows;
     size_t pitch, off, width;
-    if (p.densified) {
+    if (p.densified && !(op.operand == 1 && p.b_packed)) {
       rows = (op.operand == 0 ? p.mloc : p.nloc) * p.bs;
       pitch = (size_t)p.ld_panel(op.kappa) * 8;
       off = (size_t)(k0 * p.bs) * 8;
@@ -1292,7 +1296,7 @@ dbm_status multiply_impl(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_matrix B, 
       if (p.ownB_off[k] != SIZE_MAX) {
         const int64_t row0 = (k - p.r) / p.pr, stride = p.L / p.pr;
         double* dst = (double*)(ws + p.ownB_off[k]);
-        if (dens) {
+        if (dens && !p.b_packed) {
           ProfScope ps(ctx, cs, 2, 0.0, 16.0 * N * p.kb[k] * bs);
           if (dbm_status e = densify_b(ctx, B, row0, stride, p.kb[k], dst, p.ld_panel(k), 0, cs)) return e;
         } else {
@@ -1361,7 +1365,7 @@ dbm_status multiply_impl(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_matrix B, 
       for (int q = 0; q < ctx->nranks; ++q)
         if (q != ctx->rank)
           peer_plan[q] = make_plan_raw(ctx->nranks, p.pr, p.pc, q / p.pc, q % p.pc, p.Mb, p.Nb, p.Kb, p.bs, dens,
-                                       ctx->chunk_bytes, ctx->transport);
+                                       ctx->chunk_bytes, ctx->transport, p.b_packed);
     }
     // Step 0 is the one exchange nothing overlaps with (Cannon's initial alignment).  With the copy
     // engines and densified panels it is pulled in K-chunks, each followed by its GEMM chunk, so only
@@ -1428,16 +1432,19 @@ dbm_status multiply_impl(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_matrix B, 
           double* Bd = (double*)(ws + p.off_ownB);
           if (hio && hio->chunk_ev.size() > (size_t)ch + 1)  // chunk ch uploaded
             CUDA_TRY(ctx, cudaStreamWaitEvent(cs, hio->chunk_ev[ch + 1], 0));
+          if (p.b_packed) Bd = B->arena + k0 * p.nloc * bb;  // B's blocks read in place (§8f-3)
           {
-            ProfScope ps(ctx, cs, 2, 0.0, 16.0 * (M + N) * nk * bs);
+            ProfScope ps(ctx, cs, 2, 0.0, 16.0 * (M + (p.b_packed ? 0 : N)) * nk * bs);
             if (dbm_status e = densify_a(ctx, A, k0, 1, nk, Ad, ld, 1, cs)) return e;
-            if (dbm_status e = densify_b(ctx, B, k0, 1, nk, Bd, ld, 0, cs)) return e;
-            launches += 2;
+            if (!p.b_packed)
+              if (dbm_status e = densify_b(ctx, B, k0, 1, nk, Bd, ld, 0, cs)) return e;
+            launches += p.b_packed ? 1 : 2;
           }
           const int pans = (ch == nch - 1) ? npan : 1;
           for (int pn = 0; pn < pans; ++pn) {
             const int64_t li0 = p.mloc * pn / pans, li1 = p.mloc * (pn + 1) / pans, m0 = li0 * bs, mr = (li1 - li0) * bs;
             GemmArgs g{mr, N, nk * bs, Ad + m0 * ld, ld, Bd, ld, Cd + m0, M, 1.0, ch == 0 ? 0.0 : 1.0, 1, nullptr};
+            g.b_blocks = p.b_packed ? 1 : 0;
             g.splitk = std::min(pick_splitk(g.M, N, g.K, num_sms()), p.max_split);  // partial buffer bound
             g.partial = g.splitk > 1 ? (double*)(ws + p.off_part) : nullptr;
             {
@@ -1484,8 +1491,10 @@ dbm_status multiply_impl(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_matrix B, 
           const int pans = (hio && !C->sparse && s == p.L - 1 && j == nsub - 1 && p.mloc >= 8) ? 8 : 1;
           for (int pn = 0; pn < pans; ++pn) {
             const int64_t li0 = p.mloc * pn / pans, li1 = p.mloc * (pn + 1) / pans, m0 = li0 * bs, mr = (li1 - li0) * bs;
-            GemmArgs g{mr, N, (k1 - k0) * bs, Ap + m0 * ld + k0 * bs, ld, Bp + k0 * bs, ld, Cd + m0, M, 1.0,
+            GemmArgs g{mr, N, (k1 - k0) * bs, Ap + m0 * ld + k0 * bs, ld,
+                       p.b_packed ? Bp + k0 * p.nloc * bb : Bp + k0 * bs, ld, Cd + m0, M, 1.0,
                        (s == 0 && j == 0) ? 0.0 : 1.0, 1, nullptr};
+            g.b_blocks = p.b_packed ? 1 : 0;
             g.splitk = std::min(pick_splitk(g.M, N, g.K, num_sms()), p.max_split);  // partial buffer bound
             g.partial = g.splitk > 1 ? (double*)(ws + p.off_part) : nullptr;
             {

@@ -75,6 +75,9 @@ struct GemmArgs {
   double alpha, beta;
   int splitk;        // >= 1
   double* partial;   // splitk*M*N doubles when splitk > 1
+  // b_blocks: B is not a dense K-major matrix but a panel of 64 x 64 column-major blocks, block (kk, lj)
+  // at slot kk * ceil(N/64) + lj (a bs-64 arena / packed panel, read in place: no densify); ldb unused
+  int b_blocks = 0;
 };
 // Returns cudaSuccess or an error (tensor-map encode failures map to cudaErrorInvalidValue).
 cudaError_t launch_dgemm(const GemmArgs& g, cudaStream_t st, int* launches);

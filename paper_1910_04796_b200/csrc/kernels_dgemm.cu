@@ -63,6 +63,14 @@ __device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* tm,
       "l"((uint64_t)tm), "r"(c0), "r"(c1), "r"(mbar)
       : "memory");
 }
+__device__ __forceinline__ void tma_load_4d(uint32_t dst, const CUtensorMap* tm, int c0, int c1, int c2, int c3,
+                                            uint32_t mbar) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], [%6];" ::
+          "r"(dst),
+      "l"((uint64_t)tm), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(mbar)
+      : "memory");
+}
 __device__ __forceinline__ double lds64(uint32_t addr) {
   double v;
   asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(addr));
@@ -80,7 +88,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     int k_tiles_total, int k_tiles_per_split, int nsplit, int tiles_m, int tiles_n,
                     double* __restrict__ C,
                     int64_t ldc, double alpha, double beta, double* __restrict__ partial,
-                    unsigned* __restrict__ wave_sync, int sync_kt, int sync_rounds) {
+                    unsigned* __restrict__ wave_sync, int sync_kt, int sync_rounds, int b_blocks) {
   using T = Tile<BM, BN>;
   constexpr int STAGES = T::STAGES, kStage = T::kStage, kStageA = T::kStageA, MI = T::MI, NI = T::NI;
   extern __shared__ uint8_t smem_raw[];
@@ -148,7 +156,12 @@ __global__ void __launch_bounds__(kThreads, 1)
           mbar_expect_tx(fb, kStage);
           const uint32_t dst = su32(smem + stage * kStage);
           tma_load_2d(dst, &tmA, (kt0 + kt) * BK, tm * BM, fb);
-          tma_load_2d(dst + kStageA, &tmB, (kt0 + kt) * BK, tn * BN, fb);
+          if (b_blocks) {  // B read in place from 64 x 64 blocks: (k in block, n in block, block col, block row)
+            const int k = (kt0 + kt) * BK;
+            tma_load_4d(dst + kStageA, &tmB, k & 63, 0, tn * (BN / 64), k >> 6, fb);
+          } else {
+            tma_load_2d(dst + kStageA, &tmB, (kt0 + kt) * BK, tn * BN, fb);
+          }
           if (++stage == STAGES) {
             stage = 0;
             phase ^= 1;
@@ -314,6 +327,21 @@ bool make_map_2d(CUtensorMap* tm, const double* base, uint64_t inner, uint64_t r
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// 4-D view of a panel of 64 x 64 column-major blocks, block (kk, lj) at slot kk*nblk_n + lj: B(k, n) with
+// k = 64 kk + k_in, n = 64 lj + n_in lives at ((kk*nblk_n + lj)*64 + n_in)*64 + k_in.  Box {16 k, 64 n,
+// BN/64 block columns, 1}: the same [n][16 k] 128-B-swizzled tile a 2-D K-major box gives.
+bool make_block_b_map(CUtensorMap* tm, const double* base, int64_t nblk_n, int64_t nblk_k, int bn) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[4] = {64, 64, (cuuint64_t)std::max<int64_t>(nblk_n, 1), (cuuint64_t)std::max<int64_t>(nblk_k, 1)};
+  cuuint64_t strides[3] = {64 * 8, 64 * 64 * 8, (cuuint64_t)std::max<int64_t>(nblk_n, 1) * 64 * 64 * 8};
+  cuuint32_t box[4] = {BK, 64, (cuuint32_t)(bn / 64), 1};
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  return fn(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, (void*)base, dims, strides, box, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 namespace {
 
 // Host planner: for each CTA tile shape, the split-K count that fills whole waves of `sms`
@@ -375,8 +403,10 @@ cudaError_t launch_tile(const GemmArgs& g, int splitk, cudaStream_t st) {
   }
   CUtensorMap tmA, tmB;
   // A zero-K product still needs valid (never dereferenced) maps: point at a 1-column view.
-  if (!make_kmajor_map(&tmA, g.A, g.M, g.K, std::max<int64_t>(g.lda, 2), BM) ||
-      !make_kmajor_map(&tmB, g.B, g.N, g.K, std::max<int64_t>(g.ldb, 2), BN))
+  if (!make_kmajor_map(&tmA, g.A, g.M, g.K, std::max<int64_t>(g.lda, 2), BM))
+    return cudaErrorInvalidValue;
+  if (g.b_blocks ? !make_block_b_map(&tmB, g.B, (g.N + 63) / 64, (g.K + 63) / 64, BN)
+                 : !make_kmajor_map(&tmB, g.B, g.N, g.K, std::max<int64_t>(g.ldb, 2), BN))
     return cudaErrorInvalidValue;
   const int tiles_m = (int)((g.M + BM - 1) / BM), tiles_n = (int)((g.N + BN - 1) / BN);
   const int ktiles = (int)((g.K + BK - 1) / BK);
@@ -404,11 +434,11 @@ cudaError_t launch_tile(const GemmArgs& g, int splitk, cudaStream_t st) {
     cfg.numAttrs = 1;
     return cudaLaunchKernelEx(&cfg, dgemm_tn_kernel<BM, BN>, tmA, tmB, (int)g.M, (int)g.N, ktiles,
                               std::max(per, 0), splitk, tiles_m, tiles_n, g.C, g.ldc, g.alpha, g.beta, partial, ws,
-                              sync_kt, rounds);
+                              sync_kt, rounds, g.b_blocks);
   }
   dgemm_tn_kernel<BM, BN><<<grid, kThreads, T::kSmem, st>>>(tmA, tmB, (int)g.M, (int)g.N, ktiles, std::max(per, 0),
                                                             splitk, tiles_m, tiles_n, g.C, g.ldc, g.alpha, g.beta,
-                                                            partial, nullptr, 1, 0);
+                                                            partial, nullptr, 1, 0, g.b_blocks);
   return cudaGetLastError();
 }
 }  // namespace

@@ -1300,6 +1300,7 @@ dbm_status multiply_impl(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_matrix B, 
           ProfScope ps(ctx, cs, 2, 0.0, 16.0 * N * p.kb[k] * bs);
           if (dbm_status e = densify_b(ctx, B, row0, stride, p.kb[k], dst, p.ld_panel(k), 0, cs)) return e;
         } else {
+          ProfScope ps(ctx, cs, 2, 0.0, 16.0 * N * p.kb[k] * bs);  // packing: the same 16 B per element
           launch_pack_rows(B->arena, p.nloc, (int)bs, row0, stride, p.kb[k], dst, cs);
         }
         launches += (N * p.kb[k]) ? 1 : 0;

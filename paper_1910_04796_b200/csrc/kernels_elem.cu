@@ -132,7 +132,19 @@ __global__ void undensify_kernel(const double* __restrict__ dense, int64_t ld, i
   }
 }
 
-// ---- whole-block panel packing (blocked path) ----
+// ---- whole-block panel packing (blocked path, zero-copy B) ----
+// Row panels: every selected block row is one contiguous run of ncols blocks; 16-byte copies.
+__global__ void __launch_bounds__(256) pack_rows_fast(const double2* __restrict__ arena, int64_t row_pairs,
+                                                      int64_t row0, int64_t rstride, int64_t nrows,
+                                                      double2* __restrict__ out) {
+  for (int64_t q = blockIdx.y; q < nrows; q += gridDim.y) {
+    const double2* src = arena + (row0 + q * rstride) * row_pairs;
+    double2* dst = out + q * row_pairs;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < row_pairs; i += (int64_t)gridDim.x * blockDim.x)
+      dst[i] = src[i];
+  }
+}
+
 __global__ void pack_blocks_kernel(const double* __restrict__ arena, int64_t nsel, int64_t inner, int64_t outer_stride,
                                    int64_t sel0, int64_t sel_stride, int bs, int by_rows, int64_t other,
                                    double* __restrict__ out) {
@@ -348,6 +360,14 @@ void launch_pack_rows(const double* arena, int64_t ncols, int bs, int64_t row0, 
                       double* out, cudaStream_t st) {
   int64_t total = nrows * ncols * (int64_t)bs * bs;
   if (total == 0) return;
+  const int64_t row = ncols * (int64_t)bs * bs;
+  if (row % 2 == 0 && ((uintptr_t)arena & 15) == 0 && ((uintptr_t)out & 15) == 0) {
+    const int64_t pairs = row / 2;
+    const unsigned gx = (unsigned)std::max<int64_t>(1, std::min<int64_t>((pairs + 255) / 256, 64));
+    const unsigned gy = (unsigned)std::min<int64_t>(nrows, 65535);
+    pack_rows_fast<<<dim3(gx, gy), 256, 0, st>>>((const double2*)arena, pairs, row0, rstride, nrows, (double2*)out);
+    return;
+  }
   pack_blocks_kernel<<<grid_for(total), kThreads, 0, st>>>(arena, nrows, ncols, 0, row0, rstride, bs, 1, ncols, out);
 }
 

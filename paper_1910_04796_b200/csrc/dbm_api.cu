@@ -1089,6 +1089,8 @@ struct HostIO {
   std::vector<cudaEvent_t> chunk_ev;
   cudaEvent_t all_ev = nullptr, c_ev = nullptr;
   std::vector<cudaEvent_t> panel_ev;  // C row panels ready for their download
+  cudaEvent_t a_ev = nullptr;         // A uploaded (several ranks: A's own panels start while B uploads)
+  bool b_deferred = false;            // the wait for B's upload sits before B's own panels
   bool c_downloaded = false;          // the multiply already enqueued C's download
 };
 
@@ -1150,6 +1152,7 @@ extern "C" dbm_status dbm_multiply_host(dbm_ctx ctx, double alpha, dbm_matrix A,
   for (cudaEvent_t ev : hio.chunk_ev) ctx->ev_pool.push_back(ev);
   for (cudaEvent_t ev : hio.panel_ev) ctx->ev_pool.push_back(ev);
   if (hio.all_ev) ctx->ev_pool.push_back(hio.all_ev);
+  if (hio.a_ev) ctx->ev_pool.push_back(hio.a_ev);
   if (hio.c_ev) ctx->ev_pool.push_back(hio.c_ev);
   if (e) return e;
   const size_t cbytes = (size_t)C->blocks() * C->bs * C->bs * 8;
@@ -1243,6 +1246,8 @@ dbm_status multiply_impl(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_matrix B, 
     } else {
       const size_t ab = (size_t)A->blocks() * bb8, bbytes = (size_t)B->blocks() * bb8;
       if (ab && alpha != 0.0) CUDA_TRY(ctx, cudaMemcpyAsync(A->arena, hio->A, ab, cudaMemcpyHostToDevice, cp));
+      hio->a_ev = get_event(ctx);
+      CUDA_TRY(ctx, cudaEventRecord(hio->a_ev, cp));
       if (bbytes && alpha != 0.0) CUDA_TRY(ctx, cudaMemcpyAsync(B->arena, hio->B, bbytes, cudaMemcpyHostToDevice, cp));
       hio->all_ev = get_event(ctx);
       CUDA_TRY(ctx, cudaEventRecord(hio->all_ev, cp));
@@ -1252,9 +1257,15 @@ dbm_status multiply_impl(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_matrix B, 
     hio->c_ev = get_event(ctx);
     CUDA_TRY(ctx, cudaEventRecord(hio->c_ev, cp));
     if (!chunked || beta != 0.0 || alpha == 0.0 || p.Kb == 0) {
-      // paths that touch C (or all of A, B) early wait for everything
-      if (hio->all_ev) CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->stream, hio->all_ev, 0));
-      if (!chunked || alpha == 0.0 || p.Kb == 0) CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->stream, hio->c_ev, 0));
+      // paths that touch C (or all of A, B) early wait for everything; on several ranks A's own panels
+      // are built while B still uploads (the wait for B moves in front of B's own panels)
+      hio->b_deferred = ctx->nranks > 1 && alpha != 0.0 && p.Kb > 0 && hio->a_ev && beta == 0.0;
+      if (hio->b_deferred)
+        CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->stream, hio->a_ev, 0));
+      else if (hio->all_ev)
+        CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->stream, hio->all_ev, 0));
+      if ((!chunked || alpha == 0.0 || p.Kb == 0) && !hio->b_deferred)
+        CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->stream, hio->c_ev, 0));
     }
   }
   dbm_stats st{};
@@ -1281,7 +1292,7 @@ dbm_status multiply_impl(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_matrix B, 
 
   // ------------------------------------------------ own panels (densify or pack), on the compute stream
   if (ctx->nranks > 1) {
-    for (int k = 0; k < p.L; ++k) {
+    for (int k = 0; k < p.L; ++k) {  // A's own panels first: on host operands B may still be uploading
       if (p.ownA_off[k] != SIZE_MAX) {
         const int64_t col0 = (k - p.c) / p.pc, stride = p.L / p.pc;
         double* dst = (double*)(ws + p.ownA_off[k]);
@@ -1293,6 +1304,9 @@ dbm_status multiply_impl(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_matrix B, 
         }
         launches += (M * p.kb[k]) ? 1 : 0;
       }
+    }
+    if (hio && hio->b_deferred) CUDA_TRY(ctx, cudaStreamWaitEvent(cs, hio->all_ev, 0));
+    for (int k = 0; k < p.L; ++k) {
       if (p.ownB_off[k] != SIZE_MAX) {
         const int64_t row0 = (k - p.r) / p.pr, stride = p.L / p.pr;
         double* dst = (double*)(ws + p.ownB_off[k]);

@@ -166,7 +166,7 @@ def run_multiply(dbm, ctx, orc, M, N, K, bs, path, alpha, beta, kind=0, cap=0, c
 @pytest.mark.parametrize("path", ["densified", "blocked"])
 @pytest.mark.parametrize("M,N,K,bs", [(352, 352, 352, 22), (128, 192, 256, 64), (66, 110, 44, 22),
                                       (110, 154, 66, 22), (154, 330, 198, 22), (320, 192, 448, 64),
-                                      (1408, 704, 2816, 64), (2816, 2816, 2816, 22), (12, 21, 30, 3),
+                                      (1408, 704, 2816, 64), (2816, 2816, 2816, 22), (12, 21, 30, 3), (256, 192, 320, 4),
                                       (88, 88, 90112, 22), (154, 110, 45034, 22),   # few long runs: smm split-K
                                       (128, 192, 16384, 64), (320, 64, 12800, 64)])
 def test_multiply_matches_oracle(dbm, ctx, orc, path, M, N, K, bs):

@@ -1,0 +1,4 @@
+set -x
+timeout 900 python -m pytest tests/test_gpu_parity.py -x -q -k "multiply_matches_oracle or host" 2>&1 | tail -2
+timeout 600 python tools/profile_multiply.py --M 16384 --N 16384 --K 16384 --bs 4 --path densified --reps 2 2>&1 | tail -1
+timeout 600 python tools/profile_multiply.py --M 4096 --N 4096 --K 4096 --bs 4 --path blocked --reps 2 2>&1 | tail -1

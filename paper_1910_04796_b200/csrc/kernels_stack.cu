@@ -107,6 +107,57 @@ __global__ void __launch_bounds__(256) smm_generic_kernel(int bs, const int32_t*
   }
 }
 
+// Small blocks (bs <= 8, bs^2 <= 64): one warp per run, lane l owns C elements l and l + 32; per entry the
+// warp loads the A and B blocks into registers (coalesced, two entries in flight) and forms the
+// products with shuffles.  Memory-bound like the paper's bs-4 case, but no CTA-wide barriers.
+__global__ void __launch_bounds__(256) smm_small_kernel(int bs, const int32_t* __restrict__ trip, int64_t nruns,
+                                                        int64_t kb, const double* __restrict__ A,
+                                                        const double* __restrict__ B, double* __restrict__ C,
+                                                        double alpha, double beta_first) {
+  const int lane = threadIdx.x & 31, bb = bs * bs;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  const int x0 = lane % bs, y0 = lane / bs, x1 = (lane + 32) % bs, y1 = (lane + 32) / bs;
+  for (int64_t run = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); run < nruns; run += warps) {
+    const int32_t* t = trip + 3 * run * kb;
+    double acc0 = 0.0, acc1 = 0.0;
+    double a0 = 0, a1 = 0, b0 = 0, b1 = 0;
+    auto fetch = [&](int64_t e, double& va0, double& va1, double& vb0, double& vb1) {
+      const double* a = A + (int64_t)t[3 * e] * bb;
+      const double* b = B + (int64_t)t[3 * e + 1] * bb;
+      va0 = lane < bb ? a[lane] : 0.0;
+      va1 = lane + 32 < bb ? a[lane + 32] : 0.0;
+      vb0 = lane < bb ? b[lane] : 0.0;
+      vb1 = lane + 32 < bb ? b[lane + 32] : 0.0;
+    };
+    if (kb > 0) fetch(0, a0, a1, b0, b1);
+    for (int64_t e = 0; e < kb; ++e) {
+      double na0 = 0, na1 = 0, nb0 = 0, nb1 = 0;
+      if (e + 1 < kb) fetch(e + 1, na0, na1, nb0, nb1);
+      for (int z = 0; z < bs; ++z) {
+        // A(x, z) is element x + z*bs, B(z, y) is z + y*bs (column-major blocks)
+        const int ia0 = x0 + z * bs, ib0 = z + y0 * bs, ia1 = x1 + z * bs, ib1 = z + y1 * bs;
+        // every lane sends the same register; the reader picks the half its element lives in
+        double av0 = __shfl_sync(0xffffffffu, a0, ia0 & 31), bv0 = __shfl_sync(0xffffffffu, b0, ib0 & 31);
+        double av1 = __shfl_sync(0xffffffffu, a0, ia1 & 31), bv1 = __shfl_sync(0xffffffffu, b0, ib1 & 31);
+        if (bb > 32) {  // warp-uniform
+          const double ah0 = __shfl_sync(0xffffffffu, a1, ia0 & 31), bh0 = __shfl_sync(0xffffffffu, b1, ib0 & 31);
+          const double ah1 = __shfl_sync(0xffffffffu, a1, ia1 & 31), bh1 = __shfl_sync(0xffffffffu, b1, ib1 & 31);
+          av0 = ia0 < 32 ? av0 : ah0;
+          bv0 = ib0 < 32 ? bv0 : bh0;
+          av1 = ia1 < 32 ? av1 : ah1;
+          bv1 = ib1 < 32 ? bv1 : bh1;
+        }
+        acc0 = fma(av0, bv0, acc0);
+        acc1 = fma(av1, bv1, acc1);
+      }
+      a0 = na0; a1 = na1; b0 = nb0; b1 = nb1;
+    }
+    double* c = C + (int64_t)t[2] * bb;
+    if (lane < bb) c[lane] = (beta_first == 0.0) ? alpha * acc0 : beta_first * c[lane] + alpha * acc0;
+    if (lane + 32 < bb) c[lane + 32] = (beta_first == 0.0) ? alpha * acc1 : beta_first * c[lane + 32] + alpha * acc1;
+  }
+}
+
 inline unsigned grid_of(int64_t n, int per = 256) {
   int64_t g = (n + per - 1) / per;
   g = std::min<int64_t>(g, (int64_t)num_sms() * 32);
@@ -141,6 +192,9 @@ cudaError_t launch_smm(int bs, const int32_t* trip, int64_t nruns, int64_t kb, c
         launch_smm_tc(bs, trip, nruns, kb, A, B, C, alpha, beta_first, nsplit, partial, st, a_blocks, b_blocks,
                       squares);
     if (e != cudaSuccess) return e;
+  } else if (bs <= 8) {
+    const unsigned g = (unsigned)std::max<int64_t>(1, std::min<int64_t>((nruns + 7) / 8, (int64_t)num_sms() * 16));
+    smm_small_kernel<<<g, 256, 0, st>>>(bs, trip, nruns, kb, A, B, C, alpha, beta_first);
   } else {
     size_t smem = 2 * (size_t)bs * bs * sizeof(double);
     if (smem > 48 * 1024) cudaFuncSetAttribute(smm_generic_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

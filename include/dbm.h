@@ -153,6 +153,12 @@ dbm_status dbm_matrix_create_sparse(dbm_ctx ctx, int64_t rows, int64_t cols, int
  * mat_id | 2^31).  mask: Mb x Nb bytes, row-major, caller-allocated. */
 dbm_status dbm_pattern_random(uint64_t seed, uint32_t mat_id, int64_t Mb, int64_t Nb, double occupancy,
                               uint8_t* mask);
+/* Host-only symbolic product of two global patterns, for the fill-in workflow (reading R15: a multiply
+ * keeps C's pattern, so a caller that wants DBCSR's fill-in creates C with the product pattern first):
+ * cmask[i*Nb + j] |= OR over k of amask[i*Kb + k] && bmask[k*Nb + j].  cmask is OR-ed into (pass C's
+ * current pattern to keep its blocks, zeros for the pure product pattern).  Row-major byte masks. */
+dbm_status dbm_pattern_product(int64_t Mb, int64_t Kb, int64_t Nb, const uint8_t* amask, const uint8_t* bmask,
+                               uint8_t* cmask);
 /* Stored blocks: local (this rank) and global. */
 dbm_status dbm_matrix_nnz(dbm_matrix m, int64_t* local_blocks, int64_t* global_blocks);
 /* Local share: mloc x nloc blocks; arena_bytes = (stored local blocks)*bs*bs*8 (mloc*nloc*bs*bs*8 dense). */

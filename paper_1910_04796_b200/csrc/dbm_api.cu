@@ -303,6 +303,21 @@ extern "C" dbm_status dbm_pattern_random(uint64_t seed, uint32_t mat_id, int64_t
   return DBM_OK;
 }
 
+extern "C" dbm_status dbm_pattern_product(int64_t Mb, int64_t Kb, int64_t Nb, const uint8_t* amask,
+                                          const uint8_t* bmask, uint8_t* cmask) {
+  ARG_CHECK(Mb >= 0 && Kb >= 0 && Nb >= 0, DBM_ERR_ARG, "negative block counts");
+  ARG_CHECK((Mb * Kb == 0 || amask) && (Kb * Nb == 0 || bmask) && (Mb * Nb == 0 || cmask), DBM_ERR_ARG, "null mask");
+  for (int64_t i = 0; i < Mb; ++i) {  // row i: OR the B rows k with A(i, k) stored
+    uint8_t* crow = cmask + i * Nb;
+    for (int64_t k = 0; k < Kb; ++k) {
+      if (!amask[i * Kb + k]) continue;
+      const uint8_t* brow = bmask + k * Nb;
+      for (int64_t j = 0; j < Nb; ++j) crow[j] |= brow[j] ? 1 : 0;
+    }
+  }
+  return DBM_OK;
+}
+
 extern "C" dbm_status dbm_matrix_create_sparse(dbm_ctx ctx, int64_t rows, int64_t cols, int32_t bs,
                                                const uint8_t* mask, dbm_matrix* out) {
   dbm_matrix m = nullptr;

@@ -71,6 +71,7 @@ _SIGS = {
     "dbm_matrix_create_sparse": (C.c_int, [_P, _I64, _I64, C.c_int32, _P, C.POINTER(_P)]),
     "dbm_pattern_random": (C.c_int, [C.c_uint64, C.c_uint32, _I64, _I64, C.c_double, _P]),
     "dbm_matrix_nnz": (C.c_int, [_P, C.POINTER(_I64), C.POINTER(_I64)]),
+    "dbm_pattern_product": (C.c_int, [_I64, _I64, _I64, _P, _P, _P]),
     "dbm_ctx_set_densify_threshold": (C.c_int, [_P, C.c_double]),
     "dbm_matrix_local_info": (C.c_int, [_P, C.POINTER(_I64), C.POINTER(_I64), C.POINTER(_I64)]),
     "dbm_matrix_local_csr": (C.c_int, [_P, _P, _P, _P]),
@@ -237,6 +238,19 @@ def pattern_random(seed: int, mat_id: int, Mb: int, Nb: int, occupancy: float):
     m = np.empty(max(Mb * Nb, 1), dtype=np.uint8)
     _check(load().dbm_pattern_random(seed, mat_id, Mb, Nb, occupancy, m.ctypes.data))
     return m[: Mb * Nb].reshape(Mb, Nb)
+
+
+def pattern_product(amask, bmask, cmask=None):
+    """dbm_pattern_product: the product pattern of A's and B's masks OR-ed into cmask (fill-in workflow, R15)."""
+    import numpy as np
+
+    a = np.ascontiguousarray(amask, dtype=np.uint8)
+    b = np.ascontiguousarray(bmask, dtype=np.uint8)
+    Mb, Kb = a.shape
+    Nb = b.shape[1]
+    c = np.zeros((Mb, Nb), dtype=np.uint8) if cmask is None else np.array(cmask, dtype=np.uint8, order="C")
+    _check(load().dbm_pattern_product(Mb, Kb, Nb, a.ctypes.data, b.ctypes.data, c.ctypes.data))
+    return c
 
 
 class Matrix:

@@ -119,3 +119,13 @@ def test_pattern_random_matches_oracle(dbm, orc):
             assert np.array_equal(dbm.pattern_random(seed, mid, Mb, Nb, occ), orc.pattern_random(seed, mid, Mb, Nb, occ))
     with pytest.raises(dbm.DbmError):
         dbm.pattern_random(1, 0, 4, 4, 1.5)
+
+
+def test_pattern_product_matches_numpy(dbm, orc):
+    """Host-only symbolic product (fill-in workflow, R15) vs numpy's boolean matrix product."""
+    a = orc.pattern_random(2, 0, 23, 31, 0.1)
+    b = orc.pattern_random(2, 1, 31, 17, 0.15)
+    c0 = orc.pattern_random(2, 2, 23, 17, 0.3)
+    want = ((a.astype(np.int64) @ b.astype(np.int64)) > 0).astype(np.uint8)
+    assert np.array_equal(dbm.pattern_product(a, b), want)
+    assert np.array_equal(dbm.pattern_product(a, b, c0), want | c0)

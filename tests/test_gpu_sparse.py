@@ -188,3 +188,25 @@ def test_sparse_multiply_host(dbm, ctx, orc, path):
     ctx.sync()
     orc.multiply_sparse(Mb, Nb, Kb, bs, 0.75, Ag, am, Bg, bm, -1.25, Cg, cm)
     assert np.array_equal(hs[2].numpy(), orc.sparse_compress(Cg, cm, Mb, Nb, bs))
+
+
+def test_fill_in_workflow(dbm, ctx, orc):
+    """DBCSR-style fill-in in two calls (R15): C_out gets the product pattern OR C_in's pattern
+    (dbm_pattern_product), C_in's blocks are copied over, then the multiply fills every product block."""
+    M, N, K, bs = 352, 352, 352, 22
+    Mb = Nb = Kb = 16
+    am, bm, cm = orc.pattern_random(9, 0, Mb, Kb, 0.2), orc.pattern_random(9, 1, Kb, Nb, 0.2), \
+        orc.pattern_random(9, 2, Mb, Nb, 0.1)
+    cout = dbm.pattern_product(am, bm, cm)
+    assert (cout >= cm).all() and cout.sum() > cm.sum()
+    A = dbm.Matrix(ctx, M, K, bs, mask=am)
+    B = dbm.Matrix(ctx, K, N, bs, mask=bm)
+    Cn = dbm.Matrix(ctx, M, N, bs, mask=cout)
+    A.fill_random(SEED, 0, 1)
+    B.fill_random(SEED, 1, 1)
+    Cn.fill_random(SEED, 2, 1)  # the fill-in blocks start from the generator too (beta = 0 below)
+    dbm.multiply(ctx, 1.0, A, B, 0.0, Cn, "blocked")
+    got = host(Cn.arena)[: Cn.nnz * bs * bs]
+    Ag, Bg, Cg = (orc.fill_arena(SEED, i, 1, M, M, bs) for i in range(3))
+    orc.multiply_sparse(Mb, Nb, Kb, bs, 1.0, Ag, am, Bg, bm, 0.0, Cg, cout)
+    assert np.array_equal(got, orc.sparse_compress(Cg, cout, Mb, Nb, bs))

@@ -1111,12 +1111,12 @@ struct HostIO {
 
 namespace {
 // Single-rank densified K-chunks (block boundaries).  Device-resident operands: uniform chunks of the
-// dense-buffer budget.  Host-resident operands (dbm_multiply_host): the chunks start at 1/32 of K and
+// dense-buffer budget.  Host-resident operands (dbm_multiply_host): the chunks start at 1/16 of K and
 // double up to the budget, so only a small first upload is exposed; every later upload (PCIe, ~12x
 // faster per K-block than the GEMM consumes it at 63,360^3) runs under the previous chunks' GEMMs.
 std::vector<int64_t> k_chunks(int64_t Kb, int64_t budget, bool host_io) {
   std::vector<int64_t> b{0};
-  int64_t step = host_io ? std::max<int64_t>(1, Kb / 32) : budget;
+  int64_t step = host_io ? std::max<int64_t>(1, Kb / 16) : budget;
   while (b.back() < Kb) {
     b.push_back(std::min(Kb, b.back() + std::min(step, budget)));
     if (host_io) step *= 2;
@@ -1454,7 +1454,7 @@ dbm_status multiply_impl(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_matrix B, 
         const int64_t nch = (int64_t)kc.size() - 1;
         // host C: the last chunk's GEMM runs in row panels, each undensified and downloaded while the
         // next panel multiplies, so only the last panel's download is exposed
-        const int npan = (hchunk && !C->sparse && p.mloc >= 8) ? (int)std::min<int64_t>(16, p.mloc) : 1;
+        const int npan = (hchunk && !C->sparse && p.mloc >= 8) ? 8 : 1;
         for (int64_t ch = 0; ch < nch; ++ch) {
           const int64_t k0 = kc[ch], nk = kc[ch + 1] - kc[ch];
           const int64_t ld = round_up(p.chunk_kb * bs, 2);

@@ -121,6 +121,8 @@ dbm_status dbm_ctx_set_transport(dbm_ctx ctx, int transport);
  * partial product over the K blocks {k : k mod P == p} after gathering A[:, S_p] from its grid
  * column and B[S_p, :] from grid row p mod Pr, then every rank sums its C blocks out of all P partials
  * in rank order.  Requires the densified path and the copy-engine transport (DBM_ERR_ARG otherwise).
+ * 2 = automatic: tall-and-skinny when K >= 16 max(M, N) on several ranks with the densified path and
+ * the copy-engine transport ("one large dimension"), Cannon otherwise.
  * Every rank must use the same algorithm.  Changes dbm_multiply_workspace(). */
 dbm_status dbm_ctx_set_algorithm(dbm_ctx ctx, int algorithm);
 /* Densified path on a single rank: byte budget of one K-chunk of dense A + B (default 16 GiB).

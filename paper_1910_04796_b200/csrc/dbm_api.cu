@@ -208,7 +208,8 @@ extern "C" dbm_status dbm_ctx_set_transport(dbm_ctx ctx, int transport) {
 }
 
 extern "C" dbm_status dbm_ctx_set_algorithm(dbm_ctx ctx, int algorithm) {
-  ARG_CHECK(ctx && (algorithm == 0 || algorithm == 1), DBM_ERR_ARG, "algorithm must be 0 (Cannon) or 1 (tall-skinny)");
+  ARG_CHECK(ctx && algorithm >= 0 && algorithm <= 2, DBM_ERR_ARG,
+            "algorithm must be 0 (Cannon), 1 (tall-skinny) or 2 (automatic)");
   ctx->algorithm = algorithm;
   return DBM_OK;
 }
@@ -753,10 +754,21 @@ Plan make_plan_raw(int nranks, int pr, int pc, int r, int c, int64_t Mb, int64_t
   return p;
 }
 
+// The MPI-level algorithm for these operands (§II: Cannon for general matrices, the
+// tall-and-skinny algorithm "only for tall-and-skinny matrices (one large dimension)"): algorithm 2
+// picks tall-and-skinny when K >= 16 max(M, N) on several ranks (densified path, copy engines).
+bool use_tallskinny(dbm_ctx ctx, dbm_matrix A, dbm_matrix B, bool densified) {
+  if (ctx->nranks <= 1) return false;
+  if (ctx->algorithm == 1) return true;
+  if (ctx->algorithm != 2 || !densified || ctx->transport != 0) return false;
+  return A->cols >= 16 * std::max(A->rows, B->cols);
+}
+
 Plan make_plan(dbm_ctx ctx, dbm_matrix A, dbm_matrix B, dbm_matrix C, bool densified) {
   (void)C;
   return make_plan_raw(ctx->nranks, ctx->pr, ctx->pc, ctx->myrow, ctx->mycol, A->Mb, B->Nb, A->Nb, A->bs, densified,
-                       ctx->chunk_bytes, ctx->transport, densified && A->bs == 64 && !B->sparse && ctx->algorithm == 0);
+                       ctx->chunk_bytes, ctx->transport,
+                       densified && A->bs == 64 && !B->sparse && !use_tallskinny(ctx, A, B, densified));
 }
 
 // One Cannon exchange step as a list of point-to-point operations (owner-pull, reading R5):
@@ -1077,7 +1089,7 @@ extern "C" dbm_status dbm_multiply_workspace(dbm_ctx ctx, dbm_matrix A, dbm_matr
   if (path == DBM_PATH_BLOCKED && (A->sparse || B->sparse || C->sparse)) {
     return sp_workspace_bytes(ctx, A, B, C, bytes);
   }
-  if (ctx->algorithm == 1 && ctx->nranks > 1)
+  if (use_tallskinny(ctx, A, B, path == DBM_PATH_DENSIFIED))
     *bytes = (int64_t)ts_workspace_bytes(ctx->pr, ctx->pc, ctx->myrow, ctx->mycol, A->Mb, B->Nb, A->Nb, A->bs);
   else
     *bytes = (int64_t)make_plan(ctx, A, B, C, path == DBM_PATH_DENSIFIED).total;
@@ -1196,7 +1208,7 @@ dbm_status multiply_impl(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_matrix B, 
     }
     return multiply_sparse_blocked(ctx, alpha, A, B, beta, C, stack_cap, workspace, ws_bytes, stats);
   }
-  if (ctx->algorithm == 1 && ctx->nranks > 1) {
+  if (use_tallskinny(ctx, A, B, dens)) {
     ARG_CHECK(dens, DBM_ERR_ARG, "the tall-and-skinny algorithm runs the densified local multiply");
     ARG_CHECK(ctx->transport == 0, DBM_ERR_ARG, "the tall-and-skinny algorithm uses the copy-engine transport");
     const size_t ts_total = ts_workspace_bytes(ctx->pr, ctx->pc, ctx->myrow, ctx->mycol, A->Mb, B->Nb, A->Nb, A->bs);

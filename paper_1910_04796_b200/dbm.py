@@ -191,8 +191,9 @@ class Context:
         self.transport = t
 
     def set_algorithm(self, algorithm: str | int) -> None:
-        """'cannon' (default) or 'tallskinny' (densified path, copy-engine transport)."""
-        a = {"cannon": 0, "tallskinny": 1}.get(algorithm, algorithm)
+        """'cannon' (default), 'tallskinny' (densified path, copy-engine transport) or 'auto'
+        (tall-and-skinny when K >= 16 max(M, N))."""
+        a = {"cannon": 0, "tallskinny": 1, "auto": 2}.get(algorithm, algorithm)
         _check(load().dbm_ctx_set_algorithm(self.h, int(a)))
         self.algorithm = a
 

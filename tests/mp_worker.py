@@ -32,13 +32,14 @@ def main():
     failures = 0
     cases = [(pr, pc, tr, "cannon") for (pr, pc) in grids for tr in ("ce", "nccl")]
     cases += [(pr, pc, "ce", "tallskinny") for (pr, pc) in grids]
+    cases += [(pr, pc, "ce", "auto") for (pr, pc) in grids]  # tall-and-skinny iff K >= 16 max(M, N)
     for pr, pc, transport, algo in cases:
         ctx = dbm.Context.from_distributed(pr=pr, pc=pc)
         ctx.set_transport(transport)
         ctx.set_algorithm(algo)
         r, c = ctx.myrow, ctx.mycol
-        for (M, N, K, bs) in shapes:
-            for path in (("densified", "blocked") if algo == "cannon" else ("densified",)):
+        for (M, N, K, bs) in (shapes + [(88, 66, 2816, 22)] if algo == "auto" else shapes):
+            for path in (("densified",) if algo == "tallskinny" else ("densified", "blocked")):
                 for kind in (0, 1):
                     A, B, C = dbm.Matrix(ctx, M, K, bs), dbm.Matrix(ctx, K, N, bs), dbm.Matrix(ctx, M, N, bs)
                     A.fill_random(SEED, 0, kind)
@@ -61,7 +62,8 @@ def main():
                     else:
                         err = float(np.linalg.norm(got - ref) / max(np.linalg.norm(ref), 1e-300)) if ref.size else 0.0
                         ok_val = err <= 1e-12
-                    if algo == "cannon":
+                    ts = algo == "tallskinny" or (algo == "auto" and path == "densified" and K >= 16 * max(M, N))
+                    if not ts:
                         rv, sd = orc.cannon_bytes(M // bs, N // bs, K // bs, bs, pr, pc, r, c)
                     else:
                         rv, sd = orc.ts_bytes(M // bs, N // bs, K // bs, bs, pr, pc, r, c)

@@ -63,7 +63,7 @@ def parse():
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--transport", default="ce", choices=["ce", "nccl"], help="Cannon panel transport (N>1)")
     p.add_argument("--grid", default="", help="force the process grid, e.g. 1x4 (default: reading R1)")
-    p.add_argument("--algorithm", default="cannon", choices=["cannon", "tallskinny"],
+    p.add_argument("--algorithm", default="cannon", choices=["cannon", "tallskinny", "auto"],
                    help="MPI-level algorithm (P:168 Cannon / P:169 tall-and-skinny), N>1")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")

@@ -131,6 +131,11 @@ cudaError_t launch_smm22_mixed(const int32_t* trip, int64_t q0, int64_t nruns, i
 bool bisection_squares(int64_t mloc, int64_t nloc);
 // DMMA group kernel for bs 22 / 64 (kernels_smm.cu); the generic smm handles other block sizes.
 bool smm_has_tensor_path(int bs);
+// DMMA per-run kernel for other compiled block sizes (kernels_sparse.cu); off == nullptr: uniform runs of kb
+bool smm_has_run_path(int bs);
+cudaError_t launch_smm_run(int bs, const int32_t* trip, const int64_t* off, int64_t nruns, int64_t kb,
+                           const double* A, const double* B, double* C, double alpha, double beta_first,
+                           cudaStream_t st);
 int smm_group_runs(int bs);  // runs per CTA group (stack chunks are cut at multiples of it)
 cudaError_t launch_smm_tc(int bs, const int32_t* trip, int64_t nruns, int64_t kb, const double* A, const double* B,
                           double* C, double alpha, double beta_first, int nsplit, double* partial, cudaStream_t st,

@@ -7,6 +7,7 @@
 //   stack boundaries (greedy whole-run packing, closed form for uniform runs).
 // smm_generic_kernel: block sizes other than 22 / 64 (the DMMA group kernel is kernels_smm.cu).
 #include <algorithm>
+#include <cstdlib>
 
 #include "dbm_internal.h"
 
@@ -158,6 +159,15 @@ __global__ void __launch_bounds__(256) smm_small_kernel(int bs, const int32_t* _
   }
 }
 
+// measurement override: DBM_SMM_NO_RUN=1 sends the small sizes back to the FMA kernels (tools/smm_small_ab)
+bool smm_run_disabled() {
+  static const int v = [] {
+    const char* e = getenv("DBM_SMM_NO_RUN");
+    return (e && *e && *e != '0') ? 1 : 0;
+  }();
+  return v != 0;
+}
+
 inline unsigned grid_of(int64_t n, int per = 256) {
   int64_t g = (n + per - 1) / per;
   g = std::min<int64_t>(g, (int64_t)num_sms() * 32);
@@ -191,6 +201,9 @@ cudaError_t launch_smm(int bs, const int32_t* trip, int64_t nruns, int64_t kb, c
     cudaError_t e =
         launch_smm_tc(bs, trip, nruns, kb, A, B, C, alpha, beta_first, nsplit, partial, st, a_blocks, b_blocks,
                       squares);
+    if (e != cudaSuccess) return e;
+  } else if (smm_has_run_path(bs) && !smm_run_disabled()) {
+    cudaError_t e = launch_smm_run(bs, trip, nullptr, nruns, kb, A, B, C, alpha, beta_first, st);
     if (e != cudaSuccess) return e;
   } else if (bs <= 8) {
     const unsigned g = (unsigned)std::max<int64_t>(1, std::min<int64_t>((nruns + 7) / 8, (int64_t)num_sms() * 16));

@@ -188,6 +188,18 @@ def test_multiply_integer_bit_exact(dbm, ctx, orc, path):
     assert np.array_equal(got, ref)
 
 
+@pytest.mark.parametrize("bs", [4, 5, 6, 7, 8, 9, 13, 16, 23, 26, 32])
+def test_blocked_small_block_sizes(dbm, ctx, orc, bs):
+    """The per-size DMMA run kernels (bs 4..32 except 22 / 64; bs 7 stays on the FMA kernel) on uniform runs:
+    odd block sizes take the 8-byte staging branch, bs 26 / 32 the 4-warp teams; beta 0 and beta != 0."""
+    for (mb, nb, kb), beta in [((7, 5, 9), -1.25), ((40, 36, 3), 0.0), ((3, 2, 61), 1.0)]:
+        got, ref, st = run_multiply(dbm, ctx, orc, mb * bs, nb * bs, kb * bs, bs, "blocked", 0.75, beta)
+        assert relerr(got, ref) <= TOL
+        assert st["entries"] == mb * nb * kb
+    got, ref, _ = run_multiply(dbm, ctx, orc, 9 * bs, 11 * bs, 13 * bs, bs, "blocked", 0.75, -1.25, kind=1)
+    assert np.array_equal(got, ref)
+
+
 def test_densified_k_chunking(dbm, ctx, orc):
     """Single-rank K-chunked densify -> GEMM accumulate (how 63,360^3 fits HBM) equals the oracle."""
     M = N = 384

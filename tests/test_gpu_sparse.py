@@ -123,7 +123,8 @@ def run_sparse(dbm, ctx, orc, M, N, K, bs, path, occ_a, occ_b, occ_c, alpha, bet
 @pytest.mark.parametrize("M,N,K,bs,oa,ob,oc", [
     (352, 352, 352, 22, 0.3, 0.3, 1.0), (352, 352, 352, 22, 0.1, 0.5, 0.4), (704, 528, 1100, 22, 0.05, 0.05, 1.0),
     (512, 384, 640, 64, 0.4, 0.6, 0.7), (1408, 1408, 5632, 64, 0.2, 0.2, 1.0), (40, 35, 50, 5, 0.5, 0.5, 0.8),
-    (352, 352, 352, 22, 1.0, 1.0, 1.0), (352, 352, 352, 22, 0.0, 0.5, 1.0), (88, 88, 45056, 22, 0.3, 0.3, 1.0)])
+    (352, 352, 352, 22, 1.0, 1.0, 1.0), (352, 352, 352, 22, 0.0, 0.5, 1.0), (88, 88, 45056, 22, 0.3, 0.3, 1.0),
+    (390, 325, 520, 13, 0.4, 0.3, 0.7), (256, 224, 384, 32, 0.3, 0.5, 1.0), (161, 207, 276, 23, 0.5, 0.5, 0.6)])
 def test_sparse_multiply_matches_oracle(dbm, ctx, orc, path, M, N, K, bs, oa, ob, oc):
     got, ref, st, entries = run_sparse(dbm, ctx, orc, M, N, K, bs, path, oa, ob, oc, 0.75, -1.25)
     assert relerr(got, ref) <= TOL

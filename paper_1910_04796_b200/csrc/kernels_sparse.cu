@@ -344,9 +344,9 @@ __global__ void __launch_bounds__(SpCfg<BS>::WARPS * 32, 1)
 template <int BS>
 struct SpRunCfg {
   static constexpr int MT = (BS + 7) / 8;            // 8x8 subtiles per block dimension
-  static constexpr int TEAM = MT >= 4 ? 4 : 1;       // warps per run
-  static constexpr int NPW = MT / TEAM;              // n-subtiles per warp
-  static constexpr int WARPS = TEAM == 4 ? 4 : 8;    // bs 64: one 4-warp team (132 KB of stages)
+  static constexpr int TEAM = MT >= 8 ? 4 : MT >= 4 ? 2 : 1;  // warps per run
+  static constexpr int NPW = MT / TEAM;                        // n-subtiles per warp
+  static constexpr int WARPS = TEAM == 1 ? 8 : 4;  // bs 64: one 4-warp team (132 KB of stages); bs 26-32: two teams
   static constexpr int TEAMS = WARPS / TEAM;
   static constexpr int BB = BS * BS;
   // one stage = A block (+ slack for the padded rows m >= BS) and B block (+ padded columns n >= BS)
@@ -371,20 +371,12 @@ __global__ void __launch_bounds__(SpRunCfg<BS>::WARPS * 32, 1)
   double* st0 = sm + (size_t)team * 2 * Cfg::STAGE;
   const int tlane = tw * 32 + lane;  // 0 .. TEAM*32-1
   constexpr int TT = TEAM * 32;
-  // Fragment row / column of this lane in each subtile.  bs 22: the 22-double pitch puts lanes g and g + 2 of
-  // a half-warp on the same banks; permuting the rows ({0,1,8,9 | 2,3,10,11}, {4,5,12,13 | ...},
-  // {16,17,20,21 | 18,19,22,23}) and columns ({0,2,4,6 | 1,3,5,7}) of the 8x8 fragments makes the B loads and
-  // two of the three A loads conflict-free (the result is the same block product, rows and columns
-  // relabelled consistently in the epilogue).
+  // fragment row / column of this lane in each subtile
   int rowm[MT], coln[NPW];
 #pragma unroll
-  for (int mi = 0; mi < MT; ++mi)
-    rowm[mi] = BS != 22 ? mi * 8 + g
-               : mi < 2 ? 4 * mi + (g & 1) + 8 * ((g >> 1) & 1) + 2 * (g >> 2)
-                        : 16 + (g & 1) + 4 * ((g >> 1) & 1) + 2 * (g >> 2);
+  for (int mi = 0; mi < MT; ++mi) rowm[mi] = mi * 8 + g;
 #pragma unroll
-  for (int ni = 0; ni < NPW; ++ni)
-    coln[ni] = (tw * NPW + ni) * 8 + (BS != 22 ? g : (g & 3) * 2 + (g >> 2));
+  for (int ni = 0; ni < NPW; ++ni) coln[ni] = (tw * NPW + ni) * 8 + g;
   // blocks are 16-byte aligned when BB is even (bs 22, 64, ...); odd BB (bs 5, 13, 23) copies 8 bytes at a time
   auto load = [&](double* dst, int64_t entry) {
     const double* a = A + (int64_t)trip[3 * entry] * BB;
@@ -457,9 +449,7 @@ __global__ void __launch_bounds__(SpRunCfg<BS>::WARPS * 32, 1)
       for (int ni = 0; ni < NPW; ++ni)
 #pragma unroll
         for (int jj = 0; jj < 2; ++jj) {
-          const int fc = 2 * t + jj;  // fragment column -> the B column that produced it
-          const int m = rowm[mi];
-          const int n = (tw * NPW + ni) * 8 + (BS != 22 ? fc : (fc & 3) * 2 + (fc >> 2));
+          const int m = rowm[mi], n = (tw * NPW + ni) * 8 + 2 * t + jj;
           if (m < BS && n < BS) {
             double* p = cb + m + n * BS;
             const double ab = __dmul_rn(alpha, acc[mi][ni][jj]);

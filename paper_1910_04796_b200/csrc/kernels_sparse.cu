@@ -349,11 +349,16 @@ struct SpRunCfg {
   static constexpr int WARPS = TEAM == 1 ? 8 : 4;  // bs 64: one 4-warp team (132 KB of stages); bs 26-32: two teams
   static constexpr int TEAMS = WARPS / TEAM;
   static constexpr int BB = BS * BS;
-  // one stage = A block (+ slack for the padded rows m >= BS) and B block (+ padded columns n >= BS)
-  static constexpr int A_D = BB + 8 * MT;
-  static constexpr int B_D = 8 * MT * BS + 8;
-  static constexpr int STAGE = ((A_D + B_D) + 1) / 2 * 2;
-  static constexpr size_t SMEM = (size_t)TEAMS * 2 * STAGE * 8;
+  // entries per pipeline stage: a bs <= 8 entry is a few hundred bytes, so a stage carries four of them
+  // (one cp.async issue, one wait and one barrier per four entries instead of per entry)
+  static constexpr int G = BS <= 8 ? 4 : 1;
+  // one entry = A block (+ slack for the padded rows m >= BS) and B block (+ padded columns n >= BS)
+  static constexpr int A_D = (BB + 8 * MT + 1) / 2 * 2;
+  static constexpr int B_D = (8 * MT * BS + 8 + 1) / 2 * 2;
+  static constexpr int STAGE = G * (A_D + B_D);
+  static constexpr int STAGES = 2;
+  static constexpr int CH = BB % 2 == 0 ? BB / 2 : BB;  // copies per block (16 B when bs^2 is even, else 8 B)
+  static constexpr size_t SMEM = (size_t)TEAMS * STAGES * STAGE * 8;
   static_assert(MT % TEAM == 0, "team split");
 };
 
@@ -363,35 +368,31 @@ __global__ void __launch_bounds__(SpRunCfg<BS>::WARPS * 32, 1)
                       int64_t kb, const double* __restrict__ A, const double* __restrict__ B,
                       double* __restrict__ C, double alpha, double beta_first) {
   using Cfg = SpRunCfg<BS>;
-  constexpr int MT = Cfg::MT, TEAM = Cfg::TEAM, NPW = Cfg::NPW, BB = Cfg::BB;
+  constexpr int MT = Cfg::MT, TEAM = Cfg::TEAM, NPW = Cfg::NPW, BB = Cfg::BB, G = Cfg::G, CH = Cfg::CH;
   extern __shared__ __align__(16) double sm[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int team = warp / TEAM, tw = warp % TEAM;
   const int g = lane >> 2, t = lane & 3;
-  double* st0 = sm + (size_t)team * 2 * Cfg::STAGE;
+  double* st0 = sm + (size_t)team * Cfg::STAGES * Cfg::STAGE;
   const int tlane = tw * 32 + lane;  // 0 .. TEAM*32-1
   constexpr int TT = TEAM * 32;
-  // fragment row / column of this lane in each subtile
-  int rowm[MT], coln[NPW];
-#pragma unroll
-  for (int mi = 0; mi < MT; ++mi) rowm[mi] = mi * 8 + g;
-#pragma unroll
-  for (int ni = 0; ni < NPW; ++ni) coln[ni] = (tw * NPW + ni) * 8 + g;
+  // stage layout: A of entries 0..G-1, then B of entries 0..G-1
   // blocks are 16-byte aligned when BB is even (bs 22, 64, ...); odd BB (bs 5, 13, 23) copies 8 bytes at a time
-  auto load = [&](double* dst, int64_t entry) {
-    const double* a = A + (int64_t)trip[3 * entry] * BB;
-    const double* b = B + (int64_t)trip[3 * entry + 1] * BB;
-    const uint32_t sa = (uint32_t)__cvta_generic_to_shared(dst);
-    const uint32_t sb = (uint32_t)__cvta_generic_to_shared(dst + Cfg::A_D);
-    if (BB % 2 == 0) {
-      for (int i = tlane; i < BB / 2; i += TT) {
-        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa + 16u * i), "l"(a + 2 * i) : "memory");
-        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sb + 16u * i), "l"(b + 2 * i) : "memory");
-      }
-    } else {
-      for (int i = tlane; i < BB; i += TT) {
-        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa + 8u * i), "l"(a + i) : "memory");
-        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sb + 8u * i), "l"(b + i) : "memory");
+  auto load = [&](double* dst, int64_t first, int64_t end) {
+    const uint32_t s0 = (uint32_t)__cvta_generic_to_shared(dst);
+    for (int idx = tlane; idx < G * CH; idx += TT) {
+      const int i = idx / CH, c = idx - i * CH;
+      const int64_t entry = first + i;
+      if (entry >= end) break;  // idx grows with i: the rest of this lane's copies are past the run too
+      const double* a = A + (int64_t)trip[3 * entry] * BB;
+      const double* b = B + (int64_t)trip[3 * entry + 1] * BB;
+      const uint32_t sa = s0 + 8u * (uint32_t)(i * Cfg::A_D), sb = s0 + 8u * (uint32_t)(G * Cfg::A_D + i * Cfg::B_D);
+      if (BB % 2 == 0) {
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa + 16u * c), "l"(a + 2 * c) : "memory");
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sb + 16u * c), "l"(b + 2 * c) : "memory");
+      } else {
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa + 8u * c), "l"(a + c) : "memory");
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sb + 8u * c), "l"(b + c) : "memory");
       }
     }
     asm volatile("cp.async.commit_group;" ::: "memory");
@@ -402,6 +403,12 @@ __global__ void __launch_bounds__(SpRunCfg<BS>::WARPS * 32, 1)
     else
       asm volatile("bar.sync %0, %1;" ::"r"(1 + team), "r"(TT) : "memory");
   };
+  // fragment row / column of this lane in each subtile
+  int rowm[MT], coln[NPW];
+#pragma unroll
+  for (int mi = 0; mi < MT; ++mi) rowm[mi] = mi * 8 + g;
+#pragma unroll
+  for (int ni = 0; ni < NPW; ++ni) coln[ni] = (tw * NPW + ni) * 8 + g;
 
   const int64_t nteams = (int64_t)gridDim.x * Cfg::TEAMS;
   for (int64_t run = (int64_t)blockIdx.x * Cfg::TEAMS + team; run < nruns; run += nteams) {
@@ -414,31 +421,36 @@ __global__ void __launch_bounds__(SpRunCfg<BS>::WARPS * 32, 1)
 #pragma unroll
       for (int j = 0; j < NPW; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
     team_sync();  // the previous run's last stage has been consumed by every team warp
-    load(st0, e0);
-    for (int64_t e = e0; e < e1; ++e) {
-      double* cur = st0 + (size_t)((e - e0) & 1) * Cfg::STAGE;
-      if (e + 1 < e1) {
-        load(st0 + (size_t)((e + 1 - e0) & 1) * Cfg::STAGE, e + 1);
+    load(st0, e0, e1);
+    int si = 0;
+    for (int64_t e = e0; e < e1; e += G, si ^= 1) {
+      double* cur = st0 + (size_t)si * Cfg::STAGE;
+      if (e + G < e1) {
+        load(st0 + (size_t)(si ^ 1) * Cfg::STAGE, e + G, e1);
         asm volatile("cp.async.wait_group 1;" ::: "memory");
       } else {
         asm volatile("cp.async.wait_group 0;" ::: "memory");
       }
       team_sync();
-      const double* sA = cur;                // (m, k) at k*BS + m
-      const double* sB = cur + Cfg::A_D;     // (k, n) at n*BS + k
 #pragma unroll
-      for (int ks = 0; ks < (BS + 3) / 4; ++ks) {
-        const int k = 4 * ks + t;
-        const bool kok = (BS % 4 == 0) || k < BS;
-        double a[MT], b[NPW];
+      for (int i = 0; i < G; ++i) {
+        if (G > 1 && e + i >= e1) break;  // warp-uniform
+        const double* sA = cur + i * Cfg::A_D;               // (m, k) at k*BS + m
+        const double* sB = cur + G * Cfg::A_D + i * Cfg::B_D;  // (k, n) at n*BS + k
 #pragma unroll
-        for (int mi = 0; mi < MT; ++mi) a[mi] = kok ? sA[k * BS + rowm[mi]] : 0.0;
+        for (int ks = 0; ks < (BS + 3) / 4; ++ks) {
+          const int k = 4 * ks + t;
+          const bool kok = (BS % 4 == 0) || k < BS;
+          double a[MT], b[NPW];
 #pragma unroll
-        for (int ni = 0; ni < NPW; ++ni) b[ni] = kok ? sB[coln[ni] * BS + k] : 0.0;
+          for (int mi = 0; mi < MT; ++mi) a[mi] = kok ? sA[k * BS + rowm[mi]] : 0.0;
 #pragma unroll
-        for (int mi = 0; mi < MT; ++mi)
+          for (int ni = 0; ni < NPW; ++ni) b[ni] = kok ? sB[coln[ni] * BS + k] : 0.0;
 #pragma unroll
-          for (int ni = 0; ni < NPW; ++ni) sp_dmma(acc[mi][ni], a[mi], b[ni]);
+          for (int mi = 0; mi < MT; ++mi)
+#pragma unroll
+            for (int ni = 0; ni < NPW; ++ni) sp_dmma(acc[mi][ni], a[mi], b[ni]);
+        }
       }
       team_sync();  // every warp is done with `cur` before it is refilled
     }

@@ -353,11 +353,15 @@ struct SpRunCfg {
   // (one cp.async issue, one wait and one barrier per four entries instead of per entry)
   static constexpr int G = BS <= 8 ? 4 : 1;
   // one entry = A block (+ slack for the padded rows m >= BS) and B block (+ padded columns n >= BS)
-  static constexpr int A_D = (BB + 8 * MT + 1) / 2 * 2;
-  static constexpr int B_D = (8 * MT * BS + 8 + 1) / 2 * 2;
-  static constexpr int STAGE = G * (A_D + B_D);
+  // (odd bs^2: +2 for the 8-byte shift below); the stage ends with one int per entry holding the shifts
+  static constexpr int A_D = (BB + 8 * MT + 2 + 1) / 2 * 2;
+  static constexpr int B_D = (8 * MT * BS + 8 + 2 + 1) / 2 * 2;
+  static constexpr int STAGE = G * (A_D + B_D) + (G + 1) / 2 * 2;
   static constexpr int STAGES = 2;
-  static constexpr int CH = BB % 2 == 0 ? BB / 2 : BB;  // copies per block (16 B when bs^2 is even, else 8 B)
+  // copies per block: 16 B each when bs^2 is even; for odd bs^2 a block starts 8 bytes off a 16-byte
+  // boundary when its slot is odd, so it is staged one double further in and copied as (bs^2 - 1) / 2
+  // 16-byte chunks plus one 8-byte element (the first when shifted, else the last)
+  static constexpr int CH = BB % 2 == 0 ? BB / 2 : (BB - 1) / 2 + 1;
   static constexpr size_t SMEM = (size_t)TEAMS * STAGES * STAGE * 8;
   static_assert(MT % TEAM == 0, "team split");
 };
@@ -391,8 +395,18 @@ __global__ void __launch_bounds__(SpRunCfg<BS>::WARPS * 32, 1)
         asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa + 16u * c), "l"(a + 2 * c) : "memory");
         asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sb + 16u * c), "l"(b + 2 * c) : "memory");
       } else {
-        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa + 8u * c), "l"(a + c) : "memory");
-        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sb + 8u * c), "l"(b + c) : "memory");
+        const int pa = trip[3 * entry] & 1, pb = trip[3 * entry + 1] & 1;  // 1: block starts 8 mod 16
+        if (c < CH - 1) {  // elements pa + 2c, pa + 2c + 1 -> shared doubles 2 pa + 2c (16-byte aligned)
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa + 16u * (pa + c)), "l"(a + pa + 2 * c)
+                       : "memory");
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sb + 16u * (pb + c)), "l"(b + pb + 2 * c)
+                       : "memory");
+        } else {  // the single element: 0 when shifted, else bs^2 - 1; this lane also records the shifts
+          const int ja = pa ? 0 : BB - 1, jb = pb ? 0 : BB - 1;
+          asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa + 8u * (pa + ja)), "l"(a + ja) : "memory");
+          asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sb + 8u * (pb + jb)), "l"(b + jb) : "memory");
+          reinterpret_cast<int*>(dst + G * (Cfg::A_D + Cfg::B_D))[i] = pa | (pb << 1);
+        }
       }
     }
     asm volatile("cp.async.commit_group;" ::: "memory");
@@ -435,8 +449,9 @@ __global__ void __launch_bounds__(SpRunCfg<BS>::WARPS * 32, 1)
 #pragma unroll
       for (int i = 0; i < G; ++i) {
         if (G > 1 && e + i >= e1) break;  // warp-uniform
-        const double* sA = cur + i * Cfg::A_D;               // (m, k) at k*BS + m
-        const double* sB = cur + G * Cfg::A_D + i * Cfg::B_D;  // (k, n) at n*BS + k
+        const int sh = BB % 2 == 0 ? 0 : reinterpret_cast<const int*>(cur + G * (Cfg::A_D + Cfg::B_D))[i];
+        const double* sA = cur + i * Cfg::A_D + (sh & 1);                 // (m, k) at k*BS + m
+        const double* sB = cur + G * Cfg::A_D + i * Cfg::B_D + (sh >> 1);  // (k, n) at n*BS + k
 #pragma unroll
         for (int ks = 0; ks < (BS + 3) / 4; ++ks) {
           const int k = 4 * ks + t;

@@ -107,6 +107,7 @@ extern "C" dbm_status dbm_ctx_create(int nranks, int rank, int pr, int pc, const
   ctx->myrow = rank / pc;
   ctx->mycol = rank % pc;
   ctx->device = device;
+  if (const char* hp = getenv("DBM_HOST_PIPE")) ctx->host_pipe = *hp != '0';  // measurement override
   cudaError_t e = cudaSetDevice(device);
   ctx->stream = (cudaStream_t)cuda_stream;  // NULL = the legacy default stream (torch's default)
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->comm, cudaStreamNonBlocking);
@@ -252,6 +253,7 @@ extern "C" dbm_status dbm_ctx_destroy(dbm_ctx ctx) {
   if (ctx->d_scratch) cudaFree(ctx->d_scratch);
   if (ctx->nccl) ncclCommDestroy((ncclComm_t)ctx->nccl);
   cudaStreamDestroy(ctx->comm);
+  if (ctx->up) cudaStreamDestroy(ctx->up);
   if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
   delete ctx;
   return DBM_OK;
@@ -596,6 +598,16 @@ extern "C" dbm_status dbm_undensify(dbm_matrix m, const double* dense, int64_t l
 // ====================================================================== multiply plan
 namespace {
 
+// Host-operand pipeline on several ranks (dbm_multiply_host): upload, own-panel densify and Cannon's
+// step-0 pull + GEMM all run in the same 5 K-chunks of each panel (1, 1, 2, 4, 8 sixteenths).  The
+// boundaries depend only on the panel's block count, which every rank agrees on, so an owner's
+// progress after chunk j is exactly what a consumer's chunk j needs.
+constexpr int kHostPipeChunks = 5;
+inline int64_t host_pipe_bound(int64_t kb, int j) {
+  static const int F[kHostPipeChunks + 1] = {0, 1, 2, 4, 8, 16};
+  return kb * F[j] / 16;
+}
+
 struct Plan {
   int L = 1;
   int pr = 1, pc = 1, r = 0, c = 0;
@@ -609,6 +621,7 @@ struct Plan {
   // workspace regions (byte offsets)
   size_t off_cd = 0, off_ownA = 0, off_ownB = 0, off_recvA[2] = {0, 0}, off_recvB[2] = {0, 0}, off_part = 0;
   size_t off_trav = 0, off_trip = 0, off_spart = 0;  // smm split-K partials
+  size_t off_flags = 0;  // several ranks: [peer][operand][kappa] int64 progress of the peers' own panels
   bool mixed = false;                                 // bs 22 squares inside a non-square traversal
   // densified bs 64 with a dense B: B is never densified -- the GEMM reads B's 64 x 64 blocks in place
   // (arena, or packed panels the peers pull), through a 4-D TMA view (§8f-3, zero-copy B)
@@ -690,6 +703,10 @@ Plan make_plan_raw(int nranks, int pr, int pc, int r, int c, int64_t Mb, int64_t
         const std::vector<int64_t> b = pipeline_chunks(p.kb[p.kappa(s)]);  // step 0 may be chunked
         for (size_t j = 1; j < b.size(); ++j)
           p.max_split = std::max(p.max_split, pick_splitk(M, N, (b[j] - b[j - 1]) * p.bs, num_sms()));
+        for (int j = 0; j < kHostPipeChunks; ++j)  // host-operand pipeline chunks (dbm_multiply_host)
+          p.max_split = std::max(p.max_split, pick_splitk(M, N, (host_pipe_bound(p.kb[p.kappa(s)], j + 1) -
+                                                                 host_pipe_bound(p.kb[p.kappa(s)], j)) * p.bs,
+                                                          num_sms()));
       }
     }
     if (p.max_split > 1) p.off_part = take((size_t)p.max_split * M * N * 8);
@@ -749,6 +766,7 @@ Plan make_plan_raw(int nranks, int pr, int pc, int r, int c, int64_t Mb, int64_t
     }
     for (int i = 0; i < std::min(nA, 2); ++i) p.off_recvA[i] = take(amax);
     for (int i = 0; i < std::min(nB, 2); ++i) p.off_recvB[i] = take(bmax);
+    p.off_flags = take((size_t)nranks * 2 * p.L * 8);
   }
   p.total = std::max<size_t>(off, 256);
   return p;
@@ -947,6 +965,39 @@ AddrRangeFn addr_range_fn() {
 
 constexpr int kIpcRec = 128;  // bytes per rank: 64-B handle + 8-B offset, padded
 
+// 64-bit stream memory operations (driver API through the runtime's entry points): an owner publishes
+// its own-panel progress into its peers' flag tables with a stream write after each densify chunk,
+// and a consumer's copy-engine pull waits on its local table (GEQ) -- no SM and no host in the loop.
+typedef CUresult (*StreamValue64Fn)(CUstream, CUdeviceptr, cuuint64_t, unsigned int);
+typedef CUresult (*DevAttrFn)(int*, CUdevice_attribute, CUdevice);
+struct MemOps {
+  StreamValue64Fn wait = nullptr, write = nullptr;
+  bool ok = false;
+};
+const MemOps& memops(int device) {
+  static MemOps m;
+  static bool init = false;
+  if (!init) {
+    init = true;
+    void *w = nullptr, *x = nullptr, *a = nullptr;
+    cudaDriverEntryPointQueryResult q1, q2, q3;
+    if (cudaGetDriverEntryPoint("cuStreamWaitValue64", &w, cudaEnableDefault, &q1) == cudaSuccess &&
+        cudaGetDriverEntryPoint("cuStreamWriteValue64", &x, cudaEnableDefault, &q2) == cudaSuccess &&
+        cudaGetDriverEntryPoint("cuDeviceGetAttribute", &a, cudaEnableDefault, &q3) == cudaSuccess &&
+        q1 == cudaDriverEntryPointSuccess && q2 == cudaDriverEntryPointSuccess && q3 == cudaDriverEntryPointSuccess) {
+      int v = 0;
+      if (((DevAttrFn)a)(&v, CU_DEVICE_ATTRIBUTE_CAN_USE_64_BIT_STREAM_MEM_OPS, (CUdevice)device) == CUDA_SUCCESS &&
+          v) {
+        m.wait = (StreamValue64Fn)w;
+        m.write = (StreamValue64Fn)x;
+        m.ok = true;
+      }
+    }
+    cudaGetLastError();
+  }
+  return m;
+}
+
 }  // namespace
 
 dbm_status dbm::ipc_exchange(dbm_ctx ctx, void* ws) {
@@ -1002,14 +1053,29 @@ dbm_status dbm::ipc_exchange(dbm_ctx ctx, void* ws) {
 namespace {
 
 // Pull this rank's step-s panels from their owners' workspaces (peer plans give the offsets).
+// Host-operand pipeline: wait (on the comm stream) until the owner of op's panel has published at
+// least `need` K-blocks of it into this rank's flag table.
+dbm_status wait_panel(dbm_ctx ctx, const Plan& p, const char* flags, const XOp& op, int64_t need) {
+  if (!flags || need <= 0) return DBM_OK;
+  const char* f = flags + ((size_t)(op.peer * 2 + op.operand) * p.L + op.kappa) * 8;
+  if (memops(ctx->device).wait(ctx->comm, (CUdeviceptr)f, (cuuint64_t)need, CU_STREAM_WAIT_VALUE_GEQ) !=
+      CUDA_SUCCESS) {
+    set_error("cuStreamWaitValue64 failed");
+    ctx->poisoned = DBM_ERR_CUDA;
+    return DBM_ERR_CUDA;
+  }
+  return DBM_OK;
+}
+
 dbm_status post_pulls(dbm_ctx ctx, const Plan& p, const std::vector<Plan>& peer_plan, int s, char* ws, int bufA,
-                      int bufB, int64_t* sent, int64_t* recv) {
+                      int bufB, int64_t* sent, int64_t* recv, const char* flags = nullptr) {
   for (const XOp& op : exchange_ops(p, s)) {
     const size_t n = (size_t)op.bytes;
     if (op.send) {  // the peer pulls it; counted for the statistics
       *sent += (int64_t)n;
       continue;
     }
+    if (dbm_status e = wait_panel(ctx, p, flags, op, p.kb[op.kappa])) return e;
     const Plan& q = peer_plan[op.peer];
     const size_t src_off = op.operand == 0 ? q.ownA_off[op.kappa] : q.ownB_off[op.kappa];
     ARG_CHECK(src_off != SIZE_MAX && ctx->peer_ws[op.peer], DBM_ERR_PLAN, "peer panel not in its workspace");
@@ -1024,12 +1090,15 @@ dbm_status post_pulls(dbm_ctx ctx, const Plan& p, const std::vector<Plan>& peer_
 // operand (rows x chunk width, pitch = the panel's leading dimension).  Statistics count the whole
 // panel once (count == true on the first chunk).
 dbm_status post_pulls_chunk(dbm_ctx ctx, const Plan& p, const std::vector<Plan>& peer_plan, int s, char* ws, int bufA,
-                            int bufB, int64_t k0, int64_t k1, bool count, int64_t* sent, int64_t* recv) {
+                            int bufB, int64_t k0, int64_t k1, bool count, int64_t* sent, int64_t* recv,
+                            const char* flags = nullptr) {
   for (const XOp& op : exchange_ops(p, s)) {
     if (op.send) {
       if (count) *sent += op.bytes;
       continue;
     }
+    if (k1 > k0)
+      if (dbm_status e = wait_panel(ctx, p, flags, op, k1)) return e;
     const Plan& q = peer_plan[op.peer];
     const size_t src_off = op.operand == 0 ? q.ownA_off[op.kappa] : q.ownB_off[op.kappa];
     ARG_CHECK(src_off != SIZE_MAX && ctx->peer_ws[op.peer], DBM_ERR_PLAN, "peer panel not in its workspace");
@@ -1119,6 +1188,7 @@ struct HostIO {
   cudaEvent_t a_ev = nullptr;         // A uploaded (several ranks: A's own panels start while B uploads)
   bool b_deferred = false;            // the wait for B's upload sits before B's own panels
   bool c_downloaded = false;          // the multiply already enqueued C's download
+  std::vector<cudaEvent_t> up_ev;     // several ranks, pipelined: upload chunk j landed (ctx->up)
 };
 
 namespace {
@@ -1178,6 +1248,7 @@ extern "C" dbm_status dbm_multiply_host(dbm_ctx ctx, double alpha, dbm_matrix A,
   dbm_status e = multiply_impl(ctx, alpha, A, B, beta, C, path, stack_cap, workspace, ws_bytes, stats, &hio);
   for (cudaEvent_t ev : hio.chunk_ev) ctx->ev_pool.push_back(ev);
   for (cudaEvent_t ev : hio.panel_ev) ctx->ev_pool.push_back(ev);
+  for (cudaEvent_t ev : hio.up_ev) ctx->ev_pool.push_back(ev);
   if (hio.all_ev) ctx->ev_pool.push_back(hio.all_ev);
   if (hio.a_ev) ctx->ev_pool.push_back(hio.a_ev);
   if (hio.c_ev) ctx->ev_pool.push_back(hio.c_ev);
@@ -1243,7 +1314,49 @@ dbm_status multiply_impl(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_matrix B, 
   ARG_CHECK(workspace != nullptr && ws_bytes >= (int64_t)p.total, DBM_ERR_WORKSPACE,
             "workspace smaller than dbm_multiply_workspace()");
   const int64_t cap = stack_cap ? stack_cap : 30000;
-  if (hio) {
+  // host operands on several ranks (densified Cannon, copy engines): uploads, own-panel densify and the
+  // step-0 pull + GEMM run chunk by chunk, the pulls gated by the owners' published progress
+  const bool hpipe = hio && ctx->nranks > 1 && dens && ctx->transport == 0 && ctx->host_pipe && alpha != 0.0 &&
+                     p.Kb > 0 && !A->sparse && !B->sparse && !C->sparse && memops(ctx->device).ok;
+  if (hpipe) {
+    cudaEvent_t e0 = get_event(ctx);
+    CUDA_TRY(ctx, cudaEventRecord(e0, ctx->stream));  // previous work on the arenas is done
+    hio->chunk_ev.push_back(e0);
+    if (!ctx->up) CUDA_TRY(ctx, cudaStreamCreateWithFlags(&ctx->up, cudaStreamNonBlocking));
+    cudaStream_t up = ctx->up;
+    CUDA_TRY(ctx, cudaStreamWaitEvent(up, e0, 0));
+    const size_t bb8 = (size_t)p.bs * p.bs * 8;
+    int64_t loA = 0, loB = 0;
+    for (int j = 0; j < kHostPipeChunks; ++j) {
+      // local A columns / B rows that hold the first host_pipe_bound(kb, j + 1) blocks of every own panel
+      int64_t hiA = loA, hiB = loB;
+      for (int k = 0; k < p.L; ++k) {
+        const int64_t q1 = host_pipe_bound(p.kb[k], j + 1);
+        if (q1 <= 0) continue;
+        if (k % p.pc == p.c) hiA = std::max(hiA, (k - p.c) / p.pc + (q1 - 1) * (p.L / p.pc) + 1);
+        if (k % p.pr == p.r) hiB = std::max(hiB, (k - p.r) / p.pr + (q1 - 1) * (p.L / p.pr) + 1);
+      }
+      if (j == kHostPipeChunks - 1) {
+        hiA = p.kA;
+        hiB = p.kB;
+      }
+      if (p.mloc && hiA > loA)
+        CUDA_TRY(ctx, cudaMemcpy2DAsync((char*)A->arena + loA * bb8, p.kA * bb8, (const char*)hio->A + loA * bb8,
+                                        p.kA * bb8, (hiA - loA) * bb8, p.mloc, cudaMemcpyHostToDevice, up));
+      if (p.nloc && hiB > loB)
+        CUDA_TRY(ctx, cudaMemcpyAsync((char*)B->arena + loB * p.nloc * bb8, (const char*)hio->B + loB * p.nloc * bb8,
+                                      (hiB - loB) * p.nloc * bb8, cudaMemcpyHostToDevice, up));
+      cudaEvent_t e = get_event(ctx);
+      CUDA_TRY(ctx, cudaEventRecord(e, up));
+      hio->up_ev.push_back(e);
+      loA = hiA;
+      loB = hiB;
+    }
+    const size_t cb = (size_t)C->blocks() * bb8;
+    if (beta != 0.0 && cb) CUDA_TRY(ctx, cudaMemcpyAsync(C->arena, hio->C, cb, cudaMemcpyHostToDevice, up));
+    hio->c_ev = get_event(ctx);
+    CUDA_TRY(ctx, cudaEventRecord(hio->c_ev, up));
+  } else if (hio) {
     // Stream the host operands in (P:174 double buffering; P:200 page-locked host memory).  The
     // single-rank densified path consumes A and B one K-chunk at a time, so chunk ch's upload only
     // has to precede chunk ch's densify and overlaps the GEMMs of the chunks before it.
@@ -1318,7 +1431,7 @@ dbm_status multiply_impl(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_matrix B, 
   }
 
   // ------------------------------------------------ own panels (densify or pack), on the compute stream
-  if (ctx->nranks > 1) {
+  if (ctx->nranks > 1 && !hpipe) {
     for (int k = 0; k < p.L; ++k) {  // A's own panels first: on host operands B may still be uploading
       if (p.ownA_off[k] != SIZE_MAX) {
         const int64_t col0 = (k - p.c) / p.pc, stride = p.L / p.pc;
@@ -1372,9 +1485,56 @@ dbm_status multiply_impl(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_matrix B, 
   cudaEvent_t ev_ready = nullptr;
   std::vector<int> bufA_of(p.L, -1), bufB_of(p.L, -1);
   std::vector<Plan> peer_plan;
+  // pipelined host operands: own panels densified chunk by chunk inside Cannon's step 0
+  auto own_panels_chunk = [&](int j) -> dbm_status {
+    CUDA_TRY(ctx, cudaStreamWaitEvent(cs, hio->up_ev[j], 0));
+    for (int k = 0; k < p.L; ++k) {
+      const int64_t q0 = host_pipe_bound(p.kb[k], j), q1 = host_pipe_bound(p.kb[k], j + 1);
+      if (q1 <= q0) continue;
+      if (p.ownA_off[k] != SIZE_MAX && M) {
+        const int64_t col0 = (k - p.c) / p.pc, stride = p.L / p.pc;
+        double* dst = (double*)(ws + p.ownA_off[k]) + q0 * bs;
+        ProfScope ps(ctx, cs, 2, 0.0, 16.0 * M * (q1 - q0) * bs);
+        if (dbm_status e = densify_a(ctx, A, col0 + q0 * stride, stride, q1 - q0, dst, p.ld_panel(k), 1, cs)) return e;
+        ++launches;
+      }
+      if (p.ownB_off[k] != SIZE_MAX && N) {
+        const int64_t row0 = (k - p.r) / p.pr, stride = p.L / p.pr;
+        ProfScope ps(ctx, cs, 2, 0.0, 16.0 * N * (q1 - q0) * bs);
+        if (!p.b_packed) {
+          double* dst = (double*)(ws + p.ownB_off[k]) + q0 * bs;
+          if (dbm_status e = densify_b(ctx, B, row0 + q0 * stride, stride, q1 - q0, dst, p.ld_panel(k), 0, cs))
+            return e;
+        } else {
+          double* dst = (double*)(ws + p.ownB_off[k]) + q0 * p.nloc * bb;
+          launch_pack_rows(B->arena, p.nloc, (int)bs, row0 + q0 * stride, stride, q1 - q0, dst, cs);
+        }
+        ++launches;
+      }
+    }
+    CUDA_TRY(ctx, cudaGetLastError());
+    // publish: every peer's table entry [me][operand][k] = K-blocks of my panel k now in place
+    const MemOps& mo = memops(ctx->device);
+    for (int q = 0; q < ctx->nranks; ++q) {
+      if (q == ctx->rank) continue;
+      for (int k = 0; k < p.L; ++k)
+        for (int o = 0; o < 2; ++o) {
+          if ((o == 0 ? p.ownA_off[k] : p.ownB_off[k]) == SIZE_MAX) continue;
+          char* f = ctx->peer_ws[q] + peer_plan[q].off_flags + ((size_t)(ctx->rank * 2 + o) * p.L + k) * 8;
+          if (mo.write(cs, (CUdeviceptr)f, (cuuint64_t)host_pipe_bound(p.kb[k], j + 1), CU_STREAM_WRITE_VALUE_DEFAULT) !=
+              CUDA_SUCCESS) {
+            set_error("cuStreamWriteValue64 failed");
+            ctx->poisoned = DBM_ERR_CUDA;
+            return DBM_ERR_CUDA;
+          }
+        }
+    }
+    return DBM_OK;
+  };
   int nsub0 = 1;               // K-chunks of the step-0 pull (copy-engine transport, densified)
   cudaEvent_t ev_c[kMaxChunks] = {};
   std::vector<int64_t> cb0{0, 0};
+  const char* hp_flags = hpipe ? ws + p.off_flags : nullptr;  // my table of the owners' progress
   auto recv_bytes = [&](int s) {
     double n = 0;
     for (const XOp& op : exchange_ops(p, s)) n += op.send ? 0 : (double)op.bytes;
@@ -1383,7 +1543,7 @@ dbm_status multiply_impl(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_matrix B, 
   auto exchange = [&](int s) -> dbm_status {
     if (ctx->transport == 0) {
       ProfScope ps(ctx, ctx->comm, 5, 0.0, recv_bytes(s));  // copy-engine pulls of this step
-      return post_pulls(ctx, p, peer_plan, s, ws, bufA_of[s], bufB_of[s], &st.bytes_sent, &st.bytes_recv);
+      return post_pulls(ctx, p, peer_plan, s, ws, bufA_of[s], bufB_of[s], &st.bytes_sent, &st.bytes_recv, hp_flags);
     }
     return post_exchange(ctx, p, s, ws, A->arena, B->arena, bufA_of[s], bufB_of[s], &st.bytes_sent, &st.bytes_recv);
   };
@@ -1401,7 +1561,10 @@ dbm_status multiply_impl(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_matrix B, 
       ev_g[s] = get_event(ctx);
     }
     if (ctx->transport == 0) {
-      // handle all-gather after my panels are ready = barrier: every owner's panels are ready after it
+      // handle all-gather after my panels are ready = barrier: every owner's panels are ready after it.
+      // Pipelined host operands: nothing is ready yet -- the barrier only orders the reset of my flag
+      // table before any peer's progress write; the pulls then wait on the flags.
+      if (hpipe) CUDA_TRY(ctx, cudaMemsetAsync(ws + p.off_flags, 0, (size_t)ctx->nranks * 2 * p.L * 8, ctx->comm));
       if (dbm_status e = ipc_exchange(ctx, ws)) return e;
       peer_plan.resize(ctx->nranks);
       for (int q = 0; q < ctx->nranks; ++q)
@@ -1414,7 +1577,11 @@ dbm_status multiply_impl(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_matrix B, 
     // the first chunk's transfer is exposed.
     bool remote0 = p.a_src(0) != p.me() || p.b_src(0) != p.me();
     const int64_t kb0 = p.kb[p.kappa(0)];
-    if (ctx->transport == 0 && remote0 && (!dens || bs % 2 == 0) && kb0 >= 2) {
+    if (hpipe) {  // the fixed host-pipeline chunks, even when both step-0 panels are local
+      cb0.resize(kHostPipeChunks + 1);
+      for (int j = 0; j <= kHostPipeChunks; ++j) cb0[j] = host_pipe_bound(kb0, j);
+      nsub0 = kHostPipeChunks;
+    } else if (ctx->transport == 0 && remote0 && (!dens || bs % 2 == 0) && kb0 >= 2) {
       const double pull = ((p.a_src(0) != p.me() ? p.mloc : 0) + (p.b_src(0) != p.me() ? p.nloc : 0)) * (double)bs * bs * 8;
       cb0 = pipeline_chunks(kb0, pipeline_growth(2.0 * M * N * bs * (dens ? 1.0 : 1.25), pull));
       nsub0 = (int)cb0.size() - 1;
@@ -1424,7 +1591,7 @@ dbm_status multiply_impl(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_matrix B, 
       for (int j = 0; j < nsub0; ++j) {
         ev_c[j] = get_event(ctx);
         if (dbm_status e = post_pulls_chunk(ctx, p, peer_plan, 0, ws, bufA_of[0], bufB_of[0], cb0[j], cb0[j + 1],
-                                            j == 0, &st.bytes_sent, &st.bytes_recv))
+                                            j == 0, &st.bytes_sent, &st.bytes_recv, hp_flags))
           return e;
         CUDA_TRY(ctx, cudaEventRecord(ev_c[j], ctx->comm));
       }
@@ -1527,6 +1694,8 @@ dbm_status multiply_impl(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_matrix B, 
         const int nsub = (s == 0) ? nsub0 : 1;
         for (int j = 0; j < nsub; ++j) {
           const int64_t k0 = nsub > 1 ? cb0[j] : 0, k1 = nsub > 1 ? cb0[j + 1] : kbk;
+          if (hpipe && s == 0)  // my own panels' chunk j (the peers' pulls wait for it), before my GEMM j
+            if (dbm_status e = own_panels_chunk(j)) return e;
           if (nsub > 1) CUDA_TRY(ctx, cudaStreamWaitEvent(cs, ev_c[j], 0));
           // host C: the multiply's last GEMM runs in row panels, each undensified and downloaded on the
           // copy stream while the next panel multiplies (as on one rank)

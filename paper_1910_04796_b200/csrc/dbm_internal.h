@@ -153,6 +153,8 @@ struct dbm_ctx_s {
   cudaStream_t stream = nullptr;
   bool own_stream = false;
   cudaStream_t comm = nullptr;
+  cudaStream_t up = nullptr;  // host->device uploads of dbm_multiply_host on several ranks (lazy)
+  bool host_pipe = true;      // several ranks, host operands: chunked uploads gated by peer flags
   void* nccl = nullptr;  // ncclComm_t
   dbm_status poisoned = DBM_OK;
   int64_t launches = 0;

@@ -88,11 +88,13 @@ def host_cases(world, rank, dev, grids):
     """dbm_multiply_host on every grid (pinned host arenas; the last GEMM's row panels are downloaded while
     the next multiplies): C_host against the oracle, float and integer inputs, beta != 0."""
     failures = 0
-    M, N, K, bs = 352, 352, 704, 22
+    # several ranks: uploads, own-panel densify and the step-0 pull + GEMM run in 5 K-chunks gated by the
+    # owners' published progress (ragged 15-block K: empty first chunks; bs 64: packed zero-copy B panels)
+    shapes = [(352, 352, 704, 22, -1.25), (320, 192, 640, 64, 0.0), (198, 154, 330, 22, 1.0)]
     for pr, pc in grids:
         ctx = dbm.Context.from_distributed(pr=pr, pc=pc)
         r, c = ctx.myrow, ctx.mycol
-        for kind in (0, 1):
+        for (M, N, K, bs, beta), kind in [(sh, kd) for sh in shapes for kd in (0, 1)]:
             A, B, C = dbm.Matrix(ctx, M, K, bs), dbm.Matrix(ctx, K, N, bs), dbm.Matrix(ctx, M, N, bs)
             hs = []
             for m, mid in ((A, 0), (B, 1), (C, 2)):
@@ -103,13 +105,13 @@ def host_cases(world, rank, dev, grids):
             ctx.sync()
             for m in (A, B, C):
                 m.arena.zero_()  # the device copies are only staging: results must come from the host buffers
-            dbm.multiply_host(ctx, 0.75, A, B, -1.25, C, hs[0], hs[1], hs[2], "densified")
+            dbm.multiply_host(ctx, 0.75, A, B, beta, C, hs[0], hs[1], hs[2], "densified")
             ctx.sync()
             got = hs[2].numpy()[: C.arena_bytes // 8]
             Ag = orc.fill_arena(SEED, 0, kind, M, K, bs)
             Bg = orc.fill_arena(SEED, 1, kind, K, N, bs)
             Cg = orc.fill_arena(SEED, 2, kind, M, N, bs)
-            orc.multiply_blocked(M // bs, N // bs, K // bs, bs, 0.75, Ag, Bg, -1.25, Cg)
+            orc.multiply_blocked(M // bs, N // bs, K // bs, bs, 0.75, Ag, Bg, beta, Cg)
             ref = orc.scatter(Cg, M // bs, N // bs, bs, pr, pc, r, c)
             ok = np.array_equal(got, ref) if kind == 1 else \
                 float(np.linalg.norm(got - ref) / max(np.linalg.norm(ref), 1e-300)) <= 1e-12
@@ -117,7 +119,8 @@ def host_cases(world, rank, dev, grids):
             dist.all_reduce(flags)
             failures += int(flags.item() > 0)
             if rank == 0 or not ok:
-                print(json.dumps({"rank": rank, "grid": f"{pr}x{pc}", "host": True, "kind": kind, "ok": bool(ok)}),
+                print(json.dumps({"rank": rank, "grid": f"{pr}x{pc}", "host": True, "shape": [M, N, K, bs],
+                                  "kind": kind, "ok": bool(ok)}),
                       flush=True)
         ctx.close()
     return failures

@@ -73,7 +73,7 @@ def main():
                     if flags.item():
                         failures += 1
                     if rank == 0 or not (ok_val and ok_bytes):
-                        print(json.dumps({"rank": rank, "grid": f"{pr}x{pc}", "transport": transport, "algo": algo, "shape": [M, N, K, bs], "path": path,
+                        print(json.dumps({"rank": rank, "grid": f"{pr}x{pc}", "transport": transport, "algo": algo, "shape": [M, N, K, bs], "path": path, "path": path,
                                           "kind": kind, "err": err, "ok": bool(ok_val), "bytes_ok": ok_bytes,
                                           "recv": st["bytes_recv"], "expect_recv": rv}), flush=True)
         ctx.close()
@@ -90,11 +90,13 @@ def host_cases(world, rank, dev, grids):
     failures = 0
     # several ranks: uploads, own-panel densify and the step-0 pull + GEMM run in 5 K-chunks gated by the
     # owners' published progress (ragged 15-block K: empty first chunks; bs 64: packed zero-copy B panels)
-    shapes = [(352, 352, 704, 22, -1.25), (320, 192, 640, 64, 0.0), (198, 154, 330, 22, 1.0)]
+    # (the blocked path keeps the whole-upload-then-barrier schedule: one case each float / integer)
+    shapes = [(352, 352, 704, 22, -1.25, "densified"), (320, 192, 640, 64, 0.0, "densified"),
+              (198, 154, 330, 22, 1.0, "densified"), (352, 352, 704, 22, -1.25, "blocked")]
     for pr, pc in grids:
         ctx = dbm.Context.from_distributed(pr=pr, pc=pc)
         r, c = ctx.myrow, ctx.mycol
-        for (M, N, K, bs, beta), kind in [(sh, kd) for sh in shapes for kd in (0, 1)]:
+        for (M, N, K, bs, beta, path), kind in [(sh, kd) for sh in shapes for kd in (0, 1)]:
             A, B, C = dbm.Matrix(ctx, M, K, bs), dbm.Matrix(ctx, K, N, bs), dbm.Matrix(ctx, M, N, bs)
             hs = []
             for m, mid in ((A, 0), (B, 1), (C, 2)):
@@ -105,7 +107,7 @@ def host_cases(world, rank, dev, grids):
             ctx.sync()
             for m in (A, B, C):
                 m.arena.zero_()  # the device copies are only staging: results must come from the host buffers
-            dbm.multiply_host(ctx, 0.75, A, B, beta, C, hs[0], hs[1], hs[2], "densified")
+            dbm.multiply_host(ctx, 0.75, A, B, beta, C, hs[0], hs[1], hs[2], path)
             ctx.sync()
             got = hs[2].numpy()[: C.arena_bytes // 8]
             Ag = orc.fill_arena(SEED, 0, kind, M, K, bs)
@@ -119,7 +121,7 @@ def host_cases(world, rank, dev, grids):
             dist.all_reduce(flags)
             failures += int(flags.item() > 0)
             if rank == 0 or not ok:
-                print(json.dumps({"rank": rank, "grid": f"{pr}x{pc}", "host": True, "shape": [M, N, K, bs],
+                print(json.dumps({"rank": rank, "grid": f"{pr}x{pc}", "host": True, "shape": [M, N, K, bs], "path": path,
                                   "kind": kind, "ok": bool(ok)}),
                       flush=True)
         ctx.close()
@@ -188,7 +190,7 @@ def sparse_cases(world, rank, dev, grids):
                         failures += 1
                     if rank == 0 or not (ok_val and ok_bytes):
                         print(json.dumps({"rank": rank, "grid": f"{pr}x{pc}", "sparse": [oa, ob, oc],
-                                          "shape": [M, N, K, bs], "path": path, "kind": kind, "err": err,
+                                          "shape": [M, N, K, bs], "path": path, "path": path, "kind": kind, "err": err,
                                           "ok": bool(ok_val), "bytes_ok": ok_bytes, "recv": st["bytes_recv"]}),
                               flush=True)
         ctx.close()

@@ -354,8 +354,14 @@ struct SpRunCfg {
   static constexpr int G = BS <= 8 ? 4 : 1;
   // one entry = A block (+ slack for the padded rows m >= BS) and B block (+ padded columns n >= BS)
   // (odd bs^2: +2 for the 8-byte shift below); the stage ends with one int per entry holding the shifts
-  static constexpr int A_D = (BB + 8 * MT + 2 + 1) / 2 * 2;
-  static constexpr int B_D = (8 * MT * BS + 8 + 2 + 1) / 2 * 2;
+  // column pitch in shared memory: at bs 16 / 32 the natural pitch (0 mod 16) puts all four k (or n)
+  // columns a half-warp's fragment loads touch on the same banks (4- to 8-way conflicts), so those
+  // blocks are staged at a pitch = 4 or 12 mod 16 (conflict-free): 15.3 -> 24.8 and 22.2 -> 30.0
+  // TFLOP/s.  The same staging measured neutral at bs 26 and slower at bs 6 / 8 (more shared memory
+  // per stage, fewer resident CTAs), which keep their natural pitch, as do the odd sizes
+  static constexpr int P = (BS >= 16 && BS % 8 == 0) ? sp_pitch(BS) : BS;
+  static constexpr int A_D = ((BS - 1) * P + 8 * MT + 2 + 1) / 2 * 2;
+  static constexpr int B_D = (8 * MT * P + 8 + 2 + 1) / 2 * 2;
   static constexpr int STAGE = G * (A_D + B_D) + (G + 1) / 2 * 2;
   static constexpr int STAGES = 2;
   // copies per block: 16 B each when bs^2 is even; for odd bs^2 a block starts 8 bytes off a 16-byte
@@ -391,9 +397,10 @@ __global__ void __launch_bounds__(SpRunCfg<BS>::WARPS * 32, 1)
       const double* a = A + (int64_t)trip[3 * entry] * BB;
       const double* b = B + (int64_t)trip[3 * entry + 1] * BB;
       const uint32_t sa = s0 + 8u * (uint32_t)(i * Cfg::A_D), sb = s0 + 8u * (uint32_t)(G * Cfg::A_D + i * Cfg::B_D);
-      if (BB % 2 == 0) {
-        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa + 16u * c), "l"(a + 2 * c) : "memory");
-        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sb + 16u * c), "l"(b + 2 * c) : "memory");
+      if (BB % 2 == 0) {  // chunk c = doubles 2c, 2c+1 of column c / (bs/2), staged at that column's pitch
+        const int col = c / (BS / 2), d = col * Cfg::P + 2 * (c - col * (BS / 2));
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa + 8u * d), "l"(a + 2 * c) : "memory");
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sb + 8u * d), "l"(b + 2 * c) : "memory");
       } else {
         const int pa = trip[3 * entry] & 1, pb = trip[3 * entry + 1] & 1;  // 1: block starts 8 mod 16
         if (c < CH - 1) {  // elements pa + 2c, pa + 2c + 1 -> shared doubles 2 pa + 2c (16-byte aligned)
@@ -458,9 +465,9 @@ __global__ void __launch_bounds__(SpRunCfg<BS>::WARPS * 32, 1)
           const bool kok = (BS % 4 == 0) || k < BS;
           double a[MT], b[NPW];
 #pragma unroll
-          for (int mi = 0; mi < MT; ++mi) a[mi] = kok ? sA[k * BS + rowm[mi]] : 0.0;
+          for (int mi = 0; mi < MT; ++mi) a[mi] = kok ? sA[k * Cfg::P + rowm[mi]] : 0.0;
 #pragma unroll
-          for (int ni = 0; ni < NPW; ++ni) b[ni] = kok ? sB[coln[ni] * BS + k] : 0.0;
+          for (int ni = 0; ni < NPW; ++ni) b[ni] = kok ? sB[coln[ni] * Cfg::P + k] : 0.0;
 #pragma unroll
           for (int mi = 0; mi < MT; ++mi)
 #pragma unroll

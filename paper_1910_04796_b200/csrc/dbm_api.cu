@@ -1316,8 +1316,8 @@ dbm_status multiply_impl(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_matrix B, 
   const int64_t cap = stack_cap ? stack_cap : 30000;
   // host operands on several ranks (densified Cannon, copy engines): uploads, own-panel densify and the
   // step-0 pull + GEMM run chunk by chunk, the pulls gated by the owners' published progress
-  const bool hpipe = hio && ctx->nranks > 1 && dens && ctx->transport == 0 && ctx->host_pipe && alpha != 0.0 &&
-                     p.Kb > 0 && !A->sparse && !B->sparse && !C->sparse && memops(ctx->device).ok;
+  const bool hpipe = hio && ctx->nranks > 1 && ctx->transport == 0 && ctx->host_pipe && alpha != 0.0 && p.Kb > 0 &&
+                     !A->sparse && !B->sparse && !C->sparse && memops(ctx->device).ok;
   if (hpipe) {
     cudaEvent_t e0 = get_event(ctx);
     CUDA_TRY(ctx, cudaEventRecord(e0, ctx->stream));  // previous work on the arenas is done
@@ -1326,6 +1326,12 @@ dbm_status multiply_impl(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_matrix B, 
     cudaStream_t up = ctx->up;
     CUDA_TRY(ctx, cudaStreamWaitEvent(up, e0, 0));
     const size_t bb8 = (size_t)p.bs * p.bs * 8;
+    const size_t cbytes = beta != 0.0 ? (size_t)C->blocks() * bb8 : 0;
+    if (!dens) {  // the blocked path accumulates into C from the first chunk on: C_in goes first
+      if (cbytes) CUDA_TRY(ctx, cudaMemcpyAsync(C->arena, hio->C, cbytes, cudaMemcpyHostToDevice, up));
+      hio->c_ev = get_event(ctx);
+      CUDA_TRY(ctx, cudaEventRecord(hio->c_ev, up));
+    }
     int64_t loA = 0, loB = 0;
     for (int j = 0; j < kHostPipeChunks; ++j) {
       // local A columns / B rows that hold the first host_pipe_bound(kb, j + 1) blocks of every own panel
@@ -1352,10 +1358,11 @@ dbm_status multiply_impl(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_matrix B, 
       loA = hiA;
       loB = hiB;
     }
-    const size_t cb = (size_t)C->blocks() * bb8;
-    if (beta != 0.0 && cb) CUDA_TRY(ctx, cudaMemcpyAsync(C->arena, hio->C, cb, cudaMemcpyHostToDevice, up));
-    hio->c_ev = get_event(ctx);
-    CUDA_TRY(ctx, cudaEventRecord(hio->c_ev, up));
+    if (dens) {  // the densified path reads C_in only in the undensify
+      if (cbytes) CUDA_TRY(ctx, cudaMemcpyAsync(C->arena, hio->C, cbytes, cudaMemcpyHostToDevice, up));
+      hio->c_ev = get_event(ctx);
+      CUDA_TRY(ctx, cudaEventRecord(hio->c_ev, up));
+    }
   } else if (hio) {
     // Stream the host operands in (P:174 double buffering; P:200 page-locked host memory).  The
     // single-rank densified path consumes A and B one K-chunk at a time, so chunk ch's upload only
@@ -1493,15 +1500,21 @@ dbm_status multiply_impl(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_matrix B, 
       if (q1 <= q0) continue;
       if (p.ownA_off[k] != SIZE_MAX && M) {
         const int64_t col0 = (k - p.c) / p.pc, stride = p.L / p.pc;
-        double* dst = (double*)(ws + p.ownA_off[k]) + q0 * bs;
         ProfScope ps(ctx, cs, 2, 0.0, 16.0 * M * (q1 - q0) * bs);
-        if (dbm_status e = densify_a(ctx, A, col0 + q0 * stride, stride, q1 - q0, dst, p.ld_panel(k), 1, cs)) return e;
+        if (dens) {
+          double* dst = (double*)(ws + p.ownA_off[k]) + q0 * bs;
+          if (dbm_status e = densify_a(ctx, A, col0 + q0 * stride, stride, q1 - q0, dst, p.ld_panel(k), 1, cs))
+            return e;
+        } else {  // packed A panel: mloc rows of kb[k] blocks; this chunk is columns [q0, q1) of every row
+          double* dst = (double*)(ws + p.ownA_off[k]) + q0 * bb;
+          launch_pack_cols(A->arena, p.mloc, p.kA, (int)bs, col0 + q0 * stride, stride, q1 - q0, dst, cs, p.kb[k]);
+        }
         ++launches;
       }
       if (p.ownB_off[k] != SIZE_MAX && N) {
         const int64_t row0 = (k - p.r) / p.pr, stride = p.L / p.pr;
         ProfScope ps(ctx, cs, 2, 0.0, 16.0 * N * (q1 - q0) * bs);
-        if (!p.b_packed) {
+        if (dens && !p.b_packed) {
           double* dst = (double*)(ws + p.ownB_off[k]) + q0 * bs;
           if (dbm_status e = densify_b(ctx, B, row0 + q0 * stride, stride, q1 - q0, dst, p.ld_panel(k), 0, cs))
             return e;
@@ -1612,6 +1625,10 @@ dbm_status multiply_impl(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_matrix B, 
       if (!(s == 0 && nsub0 > 1)) CUDA_TRY(ctx, cudaStreamWaitEvent(cs, ev_x[s], 0));
     }
     const int64_t kbk = p.kb[k];
+    if (hpipe && s == 0 && !dens) CUDA_TRY(ctx, cudaStreamWaitEvent(cs, hio->c_ev, 0));  // C_in (uploaded first)
+    if (hpipe && s == 0 && !dens && !(kbk > 0 && p.mloc * p.nloc > 0))
+      for (int j = 0; j < nsub0; ++j)  // nothing to multiply here, but the peers wait for my panels
+        if (dbm_status e = own_panels_chunk(j)) return e;
     // operand panels for this step
     const double* Ap;
     const double* Bp;
@@ -1758,10 +1775,13 @@ dbm_status multiply_impl(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_matrix B, 
       const int nsub = (s == 0) ? nsub0 : 1;
       for (int j = 0; j < nsub; ++j) {
         const int64_t k0 = nsub > 1 ? cb0[j] : 0, nk = nsub > 1 ? cb0[j + 1] - cb0[j] : kbk;
+        if (hpipe && s == 0)  // my own panels' chunk j (the peers' pulls wait for it)
+          if (dbm_status e = own_panels_chunk(j)) return e;
         if (nsub > 1) CUDA_TRY(ctx, cudaStreamWaitEvent(cs, ev_c[j], 0));
+        if (nk == 0) continue;  // (host pipeline, ragged K: empty leading chunks)
         const double* Aj = Ap + k0 * bb;
         const double* Bj = Bp + k0 * p.nloc * bb;
-        const double bfirst = (s == 0 && j == 0) ? beta : 1.0;
+        const double bfirst = (s == 0 && k0 == 0) ? beta : 1.0;  // the first non-empty chunk applies beta
         for (int64_t q0 = 0; q0 < nruns; q0 += runs_per_chunk) {
           const int64_t q1 = std::min(nruns, q0 + runs_per_chunk);
           {

@@ -37,7 +37,8 @@ void launch_undensify(const double* dense, int64_t ld, int nsplit, int64_t split
 void launch_pack_rows(const double* arena, int64_t ncols, int bs, int64_t row0, int64_t rstride, int64_t nrows,
                       double* out, cudaStream_t st);
 void launch_pack_cols(const double* arena, int64_t mloc, int64_t nloc, int bs, int64_t col0, int64_t cstride,
-                      int64_t ncols, double* out, cudaStream_t st);
+                      int64_t ncols, double* out, cudaStream_t st,
+                      int64_t out_pitch = 0);
 
 // ---- block-sparse matrices (kernels_sparse.cu, reading R15) ----
 void launch_fill_sparse(double* arena, int64_t nnz, const int32_t* ij, int bs, int pr, int pc, int r, int c,

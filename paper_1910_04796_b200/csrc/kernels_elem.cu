@@ -151,22 +151,22 @@ __global__ void pack_blocks_kernel(const double* __restrict__ arena, int64_t nse
   // by_rows: out block (q, j) <- arena block (sel0 + q*sel_stride, j), j < other (row panel of a
   //          matrix with `other` block columns).
   // else   : out block (i, q) <- arena block (i, sel0 + q*sel_stride), i < other, with `inner`
-  //          block columns in the arena; out has nsel block columns.
+  //          block columns in the arena; out rows are outer_stride blocks apart (0: nsel, dense).
   const int64_t bb = (int64_t)bs * bs;
   const int64_t total = nsel * other * bb;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
     int64_t slot = e / bb, w = e - slot * bb;
-    int64_t src;
+    int64_t src, dst = e;
     if (by_rows) {
       int64_t q = slot / other, j = slot - q * other;
       src = ((sel0 + q * sel_stride) * other + j) * bb + w;
     } else {
       int64_t i = slot / nsel, q = slot - i * nsel;
       src = (i * inner + sel0 + q * sel_stride) * bb + w;
+      if (outer_stride > 0) dst = (i * outer_stride + q) * bb + w;
     }
-    out[e] = arena[src];
+    out[dst] = arena[src];
   }
-  (void)outer_stride;
 }
 
 // ---- fast paths for the paper's block sizes (compile-time BS: no 64-bit divisions, 16-B accesses) ----
@@ -372,10 +372,11 @@ void launch_pack_rows(const double* arena, int64_t ncols, int bs, int64_t row0, 
 }
 
 void launch_pack_cols(const double* arena, int64_t mloc, int64_t nloc, int bs, int64_t col0, int64_t cstride,
-                      int64_t ncols, double* out, cudaStream_t st) {
+                      int64_t ncols, double* out, cudaStream_t st, int64_t out_pitch) {
   int64_t total = ncols * mloc * (int64_t)bs * bs;
   if (total == 0) return;
-  pack_blocks_kernel<<<grid_for(total), kThreads, 0, st>>>(arena, ncols, nloc, 0, col0, cstride, bs, 0, mloc, out);
+  pack_blocks_kernel<<<grid_for(total), kThreads, 0, st>>>(arena, ncols, nloc, out_pitch, col0, cstride, bs, 0, mloc,
+                                                           out);
 }
 
 }  // namespace dbm

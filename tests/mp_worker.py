@@ -90,9 +90,10 @@ def host_cases(world, rank, dev, grids):
     failures = 0
     # several ranks: uploads, own-panel densify and the step-0 pull + GEMM run in 5 K-chunks gated by the
     # owners' published progress (ragged 15-block K: empty first chunks; bs 64: packed zero-copy B panels)
-    # (the blocked path keeps the whole-upload-then-barrier schedule: one case each float / integer)
+    # (the blocked path packs its own panels chunk by chunk the same way; C_in is uploaded first there)
     shapes = [(352, 352, 704, 22, -1.25, "densified"), (320, 192, 640, 64, 0.0, "densified"),
-              (198, 154, 330, 22, 1.0, "densified"), (352, 352, 704, 22, -1.25, "blocked")]
+              (198, 154, 330, 22, 1.0, "densified"), (352, 352, 704, 22, -1.25, "blocked"),
+              (198, 154, 330, 22, 1.0, "blocked"), (320, 192, 640, 64, 0.0, "blocked")]
     for pr, pc in grids:
         ctx = dbm.Context.from_distributed(pr=pr, pc=pc)
         r, c = ctx.myrow, ctx.mycol

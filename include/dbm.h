@@ -229,7 +229,11 @@ dbm_status dbm_plan_tallskinny(int pr, int pc, int myrow, int mycol, int64_t Mb,
  * A_host, B_host, C_host are this rank's arenas in host memory (arena layout, arena_bytes each); the
  * device arenas of A, B, C are the staging copies.  Pinned host buffers: A and B are streamed on the
  * library's copy stream — on a single rank the densified path uploads K-chunk j+1 while chunk j is
- * densified and multiplied — C_host is read only if beta != 0, and C is copied back to C_host.
+ * densified and multiplied; on several ranks (copy-engine transport) each rank uploads and densifies
+ * (or packs) its own panels in 5 K-chunks and publishes its progress into the peers' workspaces
+ * (64-bit stream writes), and Cannon's step-0 pulls wait on those flags, so the uploads pipeline
+ * across ranks (set DBM_HOST_PIPE=0 in the environment for the whole-upload-then-barrier schedule) —
+ * C_host is read only if beta != 0, and C is copied back to C_host.
  * Enqueued on the ctx stream; C_host is valid after the stream reaches the end (dbm_ctx_sync).
  * Pageable host buffers: staged synchronously (no overlap).  Errors as dbm_multiply. */
 dbm_status dbm_multiply_host(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_matrix B, double beta, dbm_matrix C,

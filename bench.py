@@ -195,7 +195,18 @@ def run_reference(args, cfg, name, world, rank):
         "cpu_baseline": {k: times[-1][k] for k in ("kind", "cores", "sample")} | {"value": val, "unit": "TFLOP/s"},
         "e2e": {"value": val, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
-    print(json.dumps(line), flush=True)
+    emit(line)
+
+
+_OUT = None  # the stream the ONE JSON line goes to (set in __main__)
+
+
+def emit(line):
+    """Print the bench's single JSON line on the real stdout (everything else, including native
+    libraries' stdout chatter such as NCCL's version banner, is redirected to stderr)."""
+    out = _OUT or sys.stdout
+    out.write(json.dumps(line) + "\n")
+    out.flush()
 
 
 # ------------------------------------------------------------------ our arm
@@ -356,7 +367,7 @@ def main():
             "e2e": e2e,
             "cpu_baseline": cpu,
         }
-        print(json.dumps(line), flush=True)
+        emit(line)
     if world > 1:
         dist.barrier(device_ids=[local])
         dist.destroy_process_group()
@@ -401,4 +412,9 @@ def run_e2e(args, ctx, dbm, torch, A, B, C, path, ws, stream, barrier, maxrank, 
 
 
 if __name__ == "__main__":
+    # keep stdout to exactly one JSON line: the real stdout is kept for emit(), fd 1 (which native
+    # code such as NCCL prints to) goes to stderr
+    sys.stdout.flush()
+    _OUT = os.fdopen(os.dup(1), "w")
+    os.dup2(2, 1)
     main()

@@ -68,7 +68,6 @@ def parse():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--e2e-steps", type=int, default=1)
-    p.add_argument("--cpu-rows", type=int, default=0, help="oracle sample rows (0 = auto, ~10-30 s)")
     return p.parse_args()
 
 
@@ -120,55 +119,47 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------ reference arm / cpu baseline
-def oracle_sample(M, N, K, rows: int) -> dict:
-    """Time the host oracle on `rows` sampled rows of C (2*rows*K*N flop), as it stands."""
+CPU_ROWS = 64  # the oracle is timed on the verification workload's 64 sampled rows of C
+
+
+def _sample_rows(M: int):
     import numpy as np
 
+    return np.linspace(0, M - 1, min(CPU_ROWS, M)).astype(np.int64)
+
+
+def oracle_sample(M, N, K, bs, kpre: int, occ=None) -> dict:
+    """Time the host oracle, as it stands, on a fixed sample of the workload: the same 64 rows of C
+     over the first `kpre` columns of A / rows of B (whole blocks).  The oracle's cost is
+    the same per (k, j) pair for a fixed row set, so the rate does not depend on kpre and every sample
+    of a config measures the same thing; `extrapolated_full_s` = t * (M / 64) * (K / kpre)."""
     import oracle
 
     oracle.build()
-    idx = np.linspace(0, M - 1, rows).astype(np.int64)
+    idx = _sample_rows(M)
     t0 = time.perf_counter()
-    oracle.rows_from_seeds(M, N, K, SEED, 0, 1.0, 0.0, idx)
+    if occ:
+        _, fmas = oracle.sparse_rows_from_seeds(M, N, kpre, bs, SEED, 0, SEED, occ[0], occ[1], occ[2], 1.0, 0.0, idx)
+        flop = 2.0 * fmas
+    else:
+        oracle.rows_from_seeds(M, N, kpre, SEED, 0, 1.0, 0.0, idx)
+        flop = 2.0 * len(idx) * kpre * N
     dt = time.perf_counter() - t0
-    flop = 2.0 * rows * K * N
+    full = dt * (M / len(idx)) * (K / kpre)
+    what = "block-sparse C (useful flop)" if occ else "C = A*B"
     return {"value": flop / dt / 1e12, "unit": "TFLOP/s", "cores": oracle.num_threads(), "kind": "oracle",
-            "sample": f"{rows} of {M} rows of C = A*B regenerated from seeds (2*{rows}*K*N flop), {dt:.1f} s",
-            "seconds": dt}
+            "sample": f"rows {len(idx)} of {M} (np.linspace) x k < {kpre} of {K} of {what} regenerated from seeds "
+                      f"({flop:.3g} flop, {dt:.2f} s)",
+            "extrapolated_full_s": full, "extrapolated": True, "seconds": dt}
 
 
-def oracle_sample_sparse(M, N, K, bs, occ, rows: int) -> dict:
-    """Time the host oracle on `rows` sampled rows of a block-sparse C (useful flop = 2 x its multiply-adds)."""
-    import numpy as np
-
-    import oracle
-
-    oracle.build()
-    idx = np.linspace(0, M - 1, rows).astype(np.int64)
-    t0 = time.perf_counter()
-    _, fmas = oracle.sparse_rows_from_seeds(M, N, K, bs, SEED, 0, SEED, occ[0], occ[1], occ[2], 1.0, 0.0, idx)
-    dt = time.perf_counter() - t0
-    return {"value": 2.0 * fmas / dt / 1e12, "unit": "TFLOP/s", "cores": oracle.num_threads(), "kind": "oracle",
-            "sample": f"{rows} of {M} rows of block-sparse C regenerated from seeds ({2 * fmas:.3g} useful flop), "
-                      f"{dt:.1f} s", "seconds": dt}
-
-
-def auto_rows_sparse(M, N, K, bs, occ, target_s: float = 15.0) -> int:
-    import oracle
-
-    cores = max(1, oracle.num_threads())
-    per_row = 2.0 * K * N * occ[0] * occ[1] / 0.8e9 + (K // bs) * (N // bs) * 2e-8  # work + pattern tests
-    return max(1, min(M, int(target_s * cores / per_row)))
-
-
-def auto_rows(M, N, K, target_s: float = 15.0) -> int:
-    # measured on the B200 box's host cores: ~0.8 GFLOP/s per core for the plain loop incl.
-    # regenerating B from the seeds (59 rows of 63,360^3 took 37 s on 16 threads)
-    import oracle
-
-    cores = max(1, oracle.num_threads())
-    rows = int(target_s * 0.8e9 * cores / (2.0 * K * N))
-    return max(1, min(rows, M, 64))
+def oracle_kpre(M, N, K, bs, target_s: float, occ=None) -> int:
+    """K prefix (whole blocks) that makes one 64-row sample take about target_s on this host: one short
+    probe on the same rows, then linear scaling (the oracle's time is linear in the K prefix)."""
+    probe_k = min(K, bs * max(1, -(-256 // bs)))
+    t = oracle_sample(M, N, K, bs, probe_k, occ)["seconds"]
+    k = int(probe_k * target_s / max(t, 1e-4)) // bs * bs
+    return max(bs, min(K, k))
 
 
 def run_reference(args, cfg, name, world, rank):
@@ -176,13 +167,10 @@ def run_reference(args, cfg, name, world, rank):
     if rank != 0:
         return
     occ = SPARSE_OCC.get(args.config)
-    if occ:
-        rows = args.cpu_rows or auto_rows_sparse(M, N, K, bs, occ, target_s=4.0)
-    else:
-        rows = args.cpu_rows or auto_rows(M, N, K, target_s=4.0)  # each step a bounded sample (~4 s)
+    kpre = oracle_kpre(M, N, K, bs, 4.0, occ)  # each step: the fixed 64-row sample over a K prefix (~4 s)
     times = []
     for i in range(args.warmup + args.steps):
-        r = oracle_sample_sparse(M, N, K, bs, occ, rows) if occ else oracle_sample(M, N, K, rows)
+        r = oracle_sample(M, N, K, bs, kpre, occ)
         if i >= args.warmup:
             times.append(r)
     val = statistics.mean(t["value"] for t in times)
@@ -192,7 +180,8 @@ def run_reference(args, cfg, name, world, rank):
         "ms_per_step": statistics.mean(t["seconds"] for t in times) * 1e3, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": name, "M": M, "N": N, "K": K, "block_size": bs, "path": path},
-        "cpu_baseline": {k: times[-1][k] for k in ("kind", "cores", "sample")} | {"value": val, "unit": "TFLOP/s"},
+        "cpu_baseline": {k: times[-1][k] for k in ("kind", "cores", "sample", "extrapolated_full_s", "extrapolated")}
+        | {"value": val, "unit": "TFLOP/s"},
         "e2e": {"value": val, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     emit(line)
@@ -313,15 +302,8 @@ def main():
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        try:
-            if occ:
-                cpu = oracle_sample_sparse(M, N, K, bs, occ, args.cpu_rows or auto_rows_sparse(M, N, K, bs, occ))
-            else:
-                rows = args.cpu_rows
-                if not rows:  # size the sample from a short probe so it lands at ~15 s on this host
-                    probe = oracle_sample(M, N, K, 4)
-                    rows = max(1, min(M, int(4 * 15.0 / max(probe["seconds"], 1e-3))))
-                cpu = oracle_sample(M, N, K, rows)
+        try:  # the same fixed 64-row sample as the reference arm, over a K prefix sized to ~15 s
+            cpu = oracle_sample(M, N, K, bs, oracle_kpre(M, N, K, bs, 15.0, occ), occ)
             cpu.pop("seconds", None)
         except Exception as ex:  # reported, never fatal
             cpu = {"error": str(ex)[:200]}

@@ -259,6 +259,17 @@ dbm_status dbm_undensify(dbm_matrix m, const double* dense, int64_t ld, double a
  * only.  Synchronous. */
 dbm_status dbm_debug_stacks(dbm_ctx ctx, dbm_matrix A, dbm_matrix B, dbm_matrix C, int step, int32_t cap,
                             int32_t* triplets, int64_t* n_entries, int64_t* stack_ptr, int64_t* n_stacks);
+/* Pack panel (blocked path; the Cannon panels of P:168 §II moved as whole blocks):
+ * gather nk local block columns (operand 0, an A panel) or block rows (operand 1, a B panel)
+ * first, first + stride, ... of a dense-pattern matrix into out (device, caller-owned):
+ *   operand 0: block (li, first + q*stride) -> out slot li*pitch + q   (row-major over (li, q));
+ *   operand 1: block (first + q*stride, lj) -> out slot q*nloc + lj    (row-major over (q, lj)).
+ * pitch (operand 0 only) = blocks per packed row, 0 -> nk (the host pipeline packs K-chunks of a
+ * panel at pitch kb).  Blocks copied whole (column-major inside).  Enqueued on the ctx stream.
+ * Errors: DBM_ERR_ARG (bad operand, sparse matrix, negative sizes, null out with work to do),
+ * DBM_ERR_RANGE (an index outside the local block columns / rows, pitch < nk). */
+dbm_status dbm_debug_pack_panel(dbm_matrix m, int operand, int64_t first, int64_t stride, int64_t nk, int64_t pitch,
+                                double* out);
 /* Raw dense FP64 GEMM kernel (the densified path's local multiply) on device buffers:
  * C(MxN, col-major, ldc) = alpha * At^T * B + beta * C, At K-major (element (m,k) at At[m*lda+k]),
  * B K-major (element (k,n) at B[n*ldb+k]); lda, ldb even.  splitk >= 1 splits K with a

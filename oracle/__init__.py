@@ -71,6 +71,7 @@ def lib():
             "orc_ts_bytes": (None, [_i64, _i64, _i64, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, _pi64, _pi64]),
             "orc_densify_cols": (None, [_pd, _i64, _i64, C.c_int, _pi64, _i64, _pd, _i64, C.c_int]),
             "orc_densify_rows": (None, [_pd, _i64, _i64, C.c_int, _pi64, _i64, _pd, _i64, C.c_int]),
+            "orc_pack_panel": (None, [_pd, _i64, _i64, C.c_int, C.c_int, _pi64, _i64, _pd]),
             "orc_undensify": (None, [_pd, _i64, _i64, _i64, C.c_int, _dbl, _dbl, _pd]),
             "orc_rows_from_seeds": (None, [_i64, _i64, _i64, _u64, C.c_int, _dbl, _dbl, _pi64, _i64, _pd]),
             "orc_freivalds_rhs": (None, [_i64, _i64, _i64, _u64, C.c_int, _dbl, _dbl, _u64, _pd, _pd]),
@@ -299,6 +300,16 @@ def densify_rows(arena, mloc, nloc, bs, krows, layout=0) -> np.ndarray:
         d = np.zeros(nk * bs * ld)
     lib().orc_densify_rows(_p(arena), mloc, nloc, bs, _p(kr, _pi64), nk, _p(d), ld, layout)
     return d
+
+
+def pack_panel(arena, mloc, nloc, bs, operand, kidx) -> np.ndarray:
+    """Packed Cannon panel of whole blocks (a3): A (operand 0) blocks (li, kidx[q]) row-major over (li, q);
+    B (operand 1) blocks (kidx[q], lj) row-major over (q, lj)."""
+    k = np.ascontiguousarray(kidx, dtype=np.int64)
+    n = (mloc if operand == 0 else nloc) * len(k) * bs * bs
+    out = np.zeros(max(n, 1))
+    lib().orc_pack_panel(_p(arena), mloc, nloc, bs, operand, _p(k, _pi64), len(k), _p(out))
+    return out[:n]
 
 
 def undensify(dense, ld, mloc, nloc, bs, alpha, beta, arena) -> None:

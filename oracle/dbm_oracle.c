@@ -401,6 +401,24 @@ void orc_densify_rows(const double* arena, int64_t mloc, int64_t nloc, int bs, c
     }
 }
 
+/* Pack a Cannon K-panel of whole blocks (§II "the Cannon algorithm" moves panels
+ * of blocks).  operand 0 (A): blocks (li, kcols[q]) for li in [0,mloc), q in [0,nk), packed row-major over
+ * (li, q): out slot li*nk + q.  operand 1 (B): blocks (kcols[q], lj), packed row-major over (q, lj): out
+ * slot q*nloc + lj.  Blocks are copied whole (column-major inside, reading R3). */
+void orc_pack_panel(const double* arena, int64_t mloc, int64_t nloc, int bs, int operand, const int64_t* kidx,
+                    int64_t nk, double* out) {
+  int64_t bb = (int64_t)bs * bs;
+  if (operand == 0) {
+    for (int64_t li = 0; li < mloc; ++li)
+      for (int64_t q = 0; q < nk; ++q)
+        for (int64_t e = 0; e < bb; ++e) out[(li * nk + q) * bb + e] = arena[(li * nloc + kidx[q]) * bb + e];
+  } else {
+    for (int64_t q = 0; q < nk; ++q)
+      for (int64_t lj = 0; lj < nloc; ++lj)
+        for (int64_t e = 0; e < bb; ++e) out[(q * nloc + lj) * bb + e] = arena[(kidx[q] * nloc + lj) * bb + e];
+  }
+}
+
 /* P:200 §III: "the resulting C matrix is undensified, i.e. the large blocks are */
 /* decomposed following the original block sizes"; alpha/beta per reading R8.  */
 void orc_undensify(const double* dense, int64_t ld, int64_t mloc, int64_t nloc, int bs, double alpha, double beta,

@@ -87,6 +87,11 @@ void orc_densify_cols(const double* arena, int64_t mloc, int64_t nloc, int bs, c
 /* Same for a set of block rows krows (B panels): (nk*bs) x (nloc*bs). */
 void orc_densify_rows(const double* arena, int64_t mloc, int64_t nloc, int bs, const int64_t* krows, int64_t nk,
                       double* dense, int64_t ld, int layout);
+/* Pack panel (blocked path): operand 0 gathers A blocks (li, kidx[q]) row-major over (li, q);
+ * operand 1 gathers B blocks (kidx[q], lj) row-major over (q, lj).  out holds mloc*nk (A) / nk*nloc (B)
+ * whole blocks. */
+void orc_pack_panel(const double* arena, int64_t mloc, int64_t nloc, int bs, int operand, const int64_t* kidx,
+                    int64_t nk, double* out);
 /* Undensify C: C_blk(li,lj)(x,y) = fl(fl(alpha*D(li*bs+x, lj*bs+y)) + fl(beta*C_blk)); beta==0 => C not read.
  * D column-major with leading dimension ld. */
 void orc_undensify(const double* dense, int64_t ld, int64_t mloc, int64_t nloc, int bs, double alpha, double beta,

@@ -1896,6 +1896,29 @@ extern "C" dbm_status dbm_debug_stacks(dbm_ctx ctx, dbm_matrix A, dbm_matrix B, 
   return DBM_OK;
 }
 
+extern "C" dbm_status dbm_debug_pack_panel(dbm_matrix m, int operand, int64_t first, int64_t stride, int64_t nk,
+                                           int64_t pitch, double* out) {
+  ARG_CHECK(m, DBM_ERR_ARG, "null matrix");
+  dbm_ctx ctx = m->ctx;
+  CTX_OK(ctx);
+  ARG_CHECK(operand == 0 || operand == 1, DBM_ERR_ARG, "operand must be 0 (A columns) or 1 (B rows)");
+  ARG_CHECK(!m->sparse, DBM_ERR_ARG, "pack_panel takes a dense-pattern matrix");
+  ARG_CHECK(nk >= 0 && stride >= 1 && first >= 0 && pitch >= 0, DBM_ERR_ARG, "negative sizes");
+  if (dbm_status s = need_arena(m)) return s;
+  const int64_t lim = operand == 0 ? m->nloc : m->mloc;
+  ARG_CHECK(nk == 0 || first + (nk - 1) * stride < lim, DBM_ERR_RANGE, "panel index outside the local blocks");
+  ARG_CHECK(operand == 1 || pitch == 0 || pitch >= nk, DBM_ERR_RANGE, "pitch < nk");
+  const int64_t other = operand == 0 ? m->mloc : m->nloc;
+  ARG_CHECK(nk * other == 0 || out, DBM_ERR_ARG, "null output");
+  if (operand == 0)
+    launch_pack_cols(m->arena, m->mloc, m->nloc, m->bs, first, stride, nk, out, ctx->stream, pitch);
+  else
+    launch_pack_rows(m->arena, m->nloc, m->bs, first, stride, nk, out, ctx->stream);
+  ctx->launches += (nk * other) ? 1 : 0;
+  CUDA_TRY(ctx, cudaGetLastError());
+  return DBM_OK;
+}
+
 extern "C" dbm_status dbm_debug_dgemm(dbm_ctx ctx, int64_t M, int64_t N, int64_t K, double alpha, const double* At,
                                       int64_t lda, const double* B, int64_t ldb, double beta, double* C, int64_t ldc,
                                       int splitk, double* partial, int64_t partial_bytes) {

@@ -92,6 +92,7 @@ _SIGS = {
     "dbm_undensify": (C.c_int, [_P, _P, _I64, C.c_double, C.c_double]),
     "dbm_debug_stacks": (C.c_int, [_P, _P, _P, _P, C.c_int, C.c_int32, _P, C.POINTER(_I64), _P,
                                    C.POINTER(_I64)]),
+    "dbm_debug_pack_panel": (C.c_int, [_P, C.c_int, _I64, _I64, _I64, _I64, _P]),
     "dbm_debug_dgemm": (C.c_int, [_P, _I64, _I64, _I64, C.c_double, _P, _I64, _P, _I64, C.c_double, _P, _I64,
                                   C.c_int, _P, _I64]),
 }
@@ -423,6 +424,12 @@ def debug_stacks(ctx: Context, A: Matrix, B: Matrix, C_: Matrix, step: int = 0, 
     _check(lib.dbm_debug_stacks(ctx.h, A.h, B.h, C_.h, step, cap, trip.ctypes.data, C.byref(ne), ptr.ctypes.data,
                                 C.byref(ns)))
     return trip[: 3 * ne.value].reshape(ne.value, 3), ptr
+
+
+def debug_pack_panel(m: Matrix, operand: int, first: int, stride: int, nk: int, out: torch.Tensor,
+                     pitch: int = 0) -> None:
+    """dbm_debug_pack_panel: pack nk local block columns (operand 0) / rows (operand 1) into `out`."""
+    _check(load().dbm_debug_pack_panel(m.h, operand, first, stride, nk, pitch, out.data_ptr() if out.numel() else None))
 
 
 def debug_dgemm(ctx: Context, M: int, N: int, K: int, alpha: float, At: torch.Tensor, lda: int, B: torch.Tensor,

@@ -5,6 +5,8 @@ fill A, B, C per rank, multiply, compare the rank's share with the oracle's prod
 that rank (normwise relative error <= 1e-12; bit-exact for integer inputs), and the rank's Cannon
 bytes with the oracle's schedule.  Exits non-zero on any failure; rank 0 prints one JSON per case.
 """
+import argparse
+import faulthandler
 import json
 import os
 import sys
@@ -21,15 +23,72 @@ import paper_1910_04796_b200 as dbm  # noqa: E402
 SEED = 1910
 
 
+class Watchdog:
+    """Per-case hang guard: a case that does not finish within `seconds` dumps every thread's Python
+    stack and exits the process non-zero (torchrun then tears the other ranks down), so one hung
+    multiply fails one test run quickly instead of stalling the suite."""
+
+    def __init__(self, seconds: float):
+        self.seconds = seconds
+
+    def __enter__(self):
+        faulthandler.dump_traceback_later(self.seconds, exit=True)
+        return self
+
+    def __exit__(self, *a):
+        faulthandler.cancel_dump_traceback_later()
+
+
+CASE_TIMEOUT = float(os.environ.get("DBM_CASE_TIMEOUT", "120"))
+
+
 def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--groups", default="cannon,sparse,host,sweep",
+                    help="comma list of case groups: cannon, sparse, host, sweep")
+    ap.add_argument("--summary", default="", help="rank 0 writes a JSON summary here")
+    args = ap.parse_args()
+    groups = set(args.groups.split(","))
     local = int(os.environ["LOCAL_RANK"])
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     dist.init_process_group("nccl", device_id=dev)
     world, rank = dist.get_world_size(), dist.get_rank()
     grids = [(p, world // p) for p in range(1, world + 1) if world % p == 0]
-    shapes = [(352, 352, 352, 22), (704, 528, 1100, 22), (384, 640, 1280, 64), (66, 154, 198, 22), (44, 44, 22, 22)]
+    summary = {"world": world, "grids": [f"{a}x{b}" for a, b in grids], "groups": {}}
     failures = 0
+    if "cannon" in groups:
+        f, n, e = cannon_cases(world, rank, dev, grids)
+        summary["groups"]["cannon"] = {"cases": n, "failures": f, "max_err": e}
+        failures += f
+    if "sparse" in groups:
+        f, n, e = sparse_cases(world, rank, dev, grids)
+        summary["groups"]["sparse"] = {"cases": n, "failures": f, "max_err": e}
+        failures += f
+    if "host" in groups:
+        f, n = host_cases(world, rank, dev, grids, HOST_SHAPES)
+        summary["groups"]["host"] = {"cases": n, "failures": f}
+        failures += f
+    if "sweep" in groups:
+        f, n = host_cases(world, rank, dev, grids, sweep_shapes())
+        summary["groups"]["host_sweep"] = {"cases": n, "failures": f}
+        failures += f
+    summary["failures"] = failures
+    if rank == 0:
+        print(json.dumps({"summary": summary}), flush=True)
+        if args.summary:
+            with open(args.summary, "w") as fh:
+                json.dump(summary, fh, indent=1)
+    dist.barrier(device_ids=[local])
+    dist.destroy_process_group()
+    sys.exit(1 if failures else 0)
+
+
+def cannon_cases(world, rank, dev, grids):
+    """Device-resident multiply on every grid, both transports and algorithms, both paths."""
+    shapes = [(352, 352, 352, 22), (704, 528, 1100, 22), (384, 640, 1280, 64), (66, 154, 198, 22), (44, 44, 22, 22)]
+    failures = ncases = 0
+    max_err = 0.0
     cases = [(pr, pc, tr, "cannon") for (pr, pc) in grids for tr in ("ce", "nccl")]
     cases += [(pr, pc, "ce", "tallskinny") for (pr, pc) in grids]
     cases += [(pr, pc, "ce", "auto") for (pr, pc) in grids]  # tall-and-skinny iff K >= 16 max(M, N)
@@ -45,11 +104,12 @@ def main():
                     A.fill_random(SEED, 0, kind)
                     B.fill_random(SEED, 1, kind)
                     C.fill_random(SEED, 2, kind)
-                    for rep in range(2):  # second call reuses the workspace / exchange buffers
-                        if rep == 1:
-                            C.fill_random(SEED, 2, kind)
-                        st = dbm.multiply(ctx, 0.75, A, B, -1.25, C, path)
-                    torch.cuda.synchronize()
+                    with Watchdog(CASE_TIMEOUT):
+                        for rep in range(2):  # second call reuses the workspace / exchange buffers
+                            if rep == 1:
+                                C.fill_random(SEED, 2, kind)
+                            st = dbm.multiply(ctx, 0.75, A, B, -1.25, C, path)
+                        torch.cuda.synchronize()
                     got = C.arena.cpu().numpy()[: C.arena_bytes // 8]
                     Ag = orc.fill_arena(SEED, 0, kind, M, K, bs)
                     Bg = orc.fill_arena(SEED, 1, kind, K, N, bs)
@@ -70,30 +130,48 @@ def main():
                     ok_bytes = (st["bytes_recv"], st["bytes_sent"]) == (rv, sd)
                     flags = torch.tensor([0 if (ok_val and ok_bytes) else 1], device=dev)
                     dist.all_reduce(flags)
+                    ncases += 1
+                    max_err = max(max_err, err)
                     if flags.item():
                         failures += 1
                     if rank == 0 or not (ok_val and ok_bytes):
-                        print(json.dumps({"rank": rank, "grid": f"{pr}x{pc}", "transport": transport, "algo": algo, "shape": [M, N, K, bs], "path": path, "path": path,
+                        print(json.dumps({"rank": rank, "grid": f"{pr}x{pc}", "transport": transport, "algo": algo, "shape": [M, N, K, bs], "path": path,
                                           "kind": kind, "err": err, "ok": bool(ok_val), "bytes_ok": ok_bytes,
                                           "recv": st["bytes_recv"], "expect_recv": rv}), flush=True)
         ctx.close()
-    failures += sparse_cases(world, rank, dev, grids)
-    failures += host_cases(world, rank, dev, grids)
-    dist.barrier(device_ids=[local])
-    dist.destroy_process_group()
-    sys.exit(1 if failures else 0)
+    return failures, ncases, max_err
 
 
-def host_cases(world, rank, dev, grids):
+# dbm_multiply_host on several ranks: (M, N, K, bs, beta, path).  The 352^3 bs-22 beta = 0 cases are the
+# round-1 bench hang (1 x 2 grid, 8-block panels); bs 13 / 9 are odd block sizes (odd bs^2: blocks
+# alternate 8 mod 16 byte alignment, odd bs: dense panel columns too).
+HOST_SHAPES = [(352, 352, 704, 22, -1.25, "densified"), (320, 192, 640, 64, 0.0, "densified"),
+               (198, 154, 330, 22, 1.0, "densified"), (352, 352, 704, 22, -1.25, "blocked"),
+               (198, 154, 330, 22, 1.0, "blocked"), (320, 192, 640, 64, 0.0, "blocked"),
+               (352, 352, 352, 22, 0.0, "densified"), (352, 352, 352, 22, 0.0, "blocked"),
+               (130, 104, 416, 13, 0.0, "blocked"), (130, 104, 416, 13, -1.25, "densified"),
+               (117, 90, 243, 9, 1.0, "blocked"), (117, 90, 243, 9, 0.0, "densified")]
+
+
+def sweep_shapes():
+    """Panel block counts 1..16 on the widest grid (K = 4 kb blocks covers L <= 4), both betas, both
+    paths, bs 22 and 64: every pattern of empty / non-empty host-pipeline chunks."""
+    out = []
+    for kb in range(1, 17):
+        for bs in (22, 64):
+            for beta in (0.0, -1.25):
+                for path in ("densified", "blocked"):
+                    out.append((4 * bs, 2 * bs, 4 * kb * bs, bs, beta, path))
+    return out
+
+
+def host_cases(world, rank, dev, grids, shapes):
     """dbm_multiply_host on every grid (pinned host arenas; the last GEMM's row panels are downloaded while
-    the next multiplies): C_host against the oracle, float and integer inputs, beta != 0."""
-    failures = 0
-    # several ranks: uploads, own-panel densify and the step-0 pull + GEMM run in 5 K-chunks gated by the
-    # owners' published progress (ragged 15-block K: empty first chunks; bs 64: packed zero-copy B panels)
-    # (the blocked path packs its own panels chunk by chunk the same way; C_in is uploaded first there)
-    shapes = [(352, 352, 704, 22, -1.25, "densified"), (320, 192, 640, 64, 0.0, "densified"),
-              (198, 154, 330, 22, 1.0, "densified"), (352, 352, 704, 22, -1.25, "blocked"),
-              (198, 154, 330, 22, 1.0, "blocked"), (320, 192, 640, 64, 0.0, "blocked")]
+    the next multiplies): C_host against the oracle, float and integer inputs.
+    Several ranks: uploads, own-panel densify and the step-0 pull + GEMM run in 5 K-chunks gated by the
+    owners' published progress (ragged K: empty first chunks; bs 64: packed zero-copy B panels); the
+    blocked path packs its own panels chunk by chunk the same way, C_in uploaded first."""
+    failures = ncases = 0
     for pr, pc in grids:
         ctx = dbm.Context.from_distributed(pr=pr, pc=pc)
         r, c = ctx.myrow, ctx.mycol
@@ -108,8 +186,9 @@ def host_cases(world, rank, dev, grids):
             ctx.sync()
             for m in (A, B, C):
                 m.arena.zero_()  # the device copies are only staging: results must come from the host buffers
-            dbm.multiply_host(ctx, 0.75, A, B, beta, C, hs[0], hs[1], hs[2], path)
-            ctx.sync()
+            with Watchdog(CASE_TIMEOUT):
+                dbm.multiply_host(ctx, 0.75, A, B, beta, C, hs[0], hs[1], hs[2], path)
+                ctx.sync()
             got = hs[2].numpy()[: C.arena_bytes // 8]
             Ag = orc.fill_arena(SEED, 0, kind, M, K, bs)
             Bg = orc.fill_arena(SEED, 1, kind, K, N, bs)
@@ -121,12 +200,13 @@ def host_cases(world, rank, dev, grids):
             flags = torch.tensor([0 if ok else 1], device=dev)
             dist.all_reduce(flags)
             failures += int(flags.item() > 0)
-            if rank == 0 or not ok:
+            ncases += 1
+            if (rank == 0 and shapes is HOST_SHAPES) or not ok:
                 print(json.dumps({"rank": rank, "grid": f"{pr}x{pc}", "host": True, "shape": [M, N, K, bs], "path": path,
-                                  "kind": kind, "ok": bool(ok)}),
+                                  "beta": beta, "kind": kind, "ok": bool(ok)}),
                       flush=True)
         ctx.close()
-    return failures
+    return failures, ncases
 
 
 def sparse_recv_bytes(am, bm, bs, pr, pc, r, c):
@@ -148,7 +228,8 @@ def sparse_recv_bytes(am, bm, bs, pr, pc, r, c):
 
 def sparse_cases(world, rank, dev, grids):
     """Block-sparse operands (reading R15) on every grid: both paths against orc_multiply_sparse."""
-    failures = 0
+    failures = ncases = 0
+    max_err = 0.0
     shapes = [(352, 352, 352, 22, 0.3, 0.4, 1.0), (704, 528, 1100, 22, 0.1, 0.2, 0.7), (384, 640, 1280, 64, 0.5, 0.5, 0.5),
               (66, 154, 198, 22, 0.0, 0.5, 1.0)]
     for pr, pc in grids:
@@ -165,10 +246,11 @@ def sparse_cases(world, rank, dev, grids):
                     C = dbm.Matrix(ctx, M, N, bs, mask=cm)
                     A.fill_random(SEED, 0, kind)
                     B.fill_random(SEED, 1, kind)
-                    for rep in range(2):
-                        C.fill_random(SEED, 2, kind)
-                        st = dbm.multiply(ctx, 0.75, A, B, -1.25, C, path)
-                    torch.cuda.synchronize()
+                    with Watchdog(CASE_TIMEOUT):
+                        for rep in range(2):
+                            C.fill_random(SEED, 2, kind)
+                            st = dbm.multiply(ctx, 0.75, A, B, -1.25, C, path)
+                        torch.cuda.synchronize()
                     got = C.arena.cpu().numpy()[: C.arena_bytes // 8]
                     Ag = orc.fill_arena(SEED, 0, kind, M, K, bs)
                     Bg = orc.fill_arena(SEED, 1, kind, K, N, bs)
@@ -187,15 +269,17 @@ def sparse_cases(world, rank, dev, grids):
                         ok_bytes = (st["bytes_recv"], st["bytes_sent"]) == orc.cannon_bytes(Mb, Nb, Kb, bs, pr, pc, r, c)
                     flags = torch.tensor([0 if (ok_val and ok_bytes) else 1], device=dev)
                     dist.all_reduce(flags)
+                    ncases += 1
+                    max_err = max(max_err, err)
                     if flags.item():
                         failures += 1
                     if rank == 0 or not (ok_val and ok_bytes):
                         print(json.dumps({"rank": rank, "grid": f"{pr}x{pc}", "sparse": [oa, ob, oc],
-                                          "shape": [M, N, K, bs], "path": path, "path": path, "kind": kind, "err": err,
+                                          "shape": [M, N, K, bs], "path": path, "kind": kind, "err": err,
                                           "ok": bool(ok_val), "bytes_ok": ok_bytes, "recv": st["bytes_recv"]}),
                               flush=True)
         ctx.close()
-    return failures
+    return failures, ncases, max_err
 
 
 if __name__ == "__main__":

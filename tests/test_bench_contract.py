@@ -28,5 +28,5 @@ def test_reference_arm_line():
 
 
 def test_reference_arm_sparse_config():
-    d = run_ref("--config", "sp22", "--steps", "1", "--warmup", "0", "--cpu-rows", "2")
+    d = run_ref("--config", "sp22", "--steps", "1", "--warmup", "0")
     assert d["value"] > 0 and "block-sparse" in d["config"]["workload"]

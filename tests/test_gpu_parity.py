@@ -145,6 +145,70 @@ def test_stacks_bit_exact(dbm, ctx, orc, n, bs, cap):
     assert np.array_equal(ptr, rptr)
 
 
+@pytest.mark.parametrize("Mb,Nb,Kb,bs,cap", [(13, 7, 29, 22, 7), (13, 7, 29, 22, 100), (7, 13, 29, 22, 30000),
+                                           (5, 9, 3, 64, 4), (1, 11, 40, 22, 30), (9, 1, 2, 5, 3)])
+def test_stacks_bit_exact_non_square(dbm, ctx, orc, Mb, Nb, Kb, bs, cap):
+    """Stack lists on rectangular local grids (mloc != nloc, the bisection splits the longer side) and
+    runs longer than the cap (kb > cap splits a run into ceil(kb/cap) stacks)."""
+    A, B, C = dbm.Matrix(ctx, Mb * bs, Kb * bs, bs), dbm.Matrix(ctx, Kb * bs, Nb * bs, bs), dbm.Matrix(ctx, Mb * bs, Nb * bs, bs)
+    trip, ptr = dbm.debug_stacks(ctx, A, B, C, 0, cap)
+    rtrip, rptr = orc.stacks(Mb, Nb, Kb, cap)
+    assert np.array_equal(trip, rtrip)
+    assert np.array_equal(ptr, rptr)
+
+
+# ------------------------------------------------------------------ pack panel (a3, bit-exact)
+@pytest.mark.parametrize("rows,cols,bs", [(352, 616, 22), (320, 448, 64), (65, 91, 13), (30, 45, 5)])
+@pytest.mark.parametrize("operand", [0, 1])
+@pytest.mark.parametrize("first,stride", [(0, 1), (1, 2), (0, 4), (2, 3)])
+def test_pack_panel_bit_exact(dbm, ctx, orc, rows, cols, bs, operand, first, stride):
+    """a3: the GPU panel pack (dbm_debug_pack_panel) against orc_pack_panel (brute-force pinned in
+    test_oracle_pins.py::test_pack_panel_brute_force), every block size alignment (bs^2 odd: blocks
+    alternate 8 mod 16 bytes)."""
+    m = dbm.Matrix(ctx, rows, cols, bs)
+    m.fill_random(SEED, operand, 0)
+    mloc, nloc = rows // bs, cols // bs
+    lim = nloc if operand == 0 else mloc
+    nk = max(0, (lim - 1 - first) // stride + 1)
+    kidx = [first + q * stride for q in range(nk)]
+    other = mloc if operand == 0 else nloc
+    out = torch.full((max(other * nk * bs * bs, 1),), float("nan"), dtype=torch.float64, device="cuda")
+    dbm.debug_pack_panel(m, operand, first, stride, nk, out)
+    ref = orc.pack_panel(orc.fill_arena(SEED, operand, 0, rows, cols, bs), mloc, nloc, bs, operand, kidx)
+    assert np.array_equal(host(out)[: ref.size], ref)
+
+
+@pytest.mark.parametrize("bs", [22, 13])
+def test_pack_panel_chunks_with_pitch(dbm, ctx, orc, bs):
+    """The host pipeline packs an A panel K-chunk by K-chunk at the panel's pitch: chunks [q0, q1) packed
+    into columns q0.. of every packed row must assemble the whole panel."""
+    rows, cols = 10 * bs, 17 * bs
+    m = dbm.Matrix(ctx, rows, cols, bs)
+    m.fill_random(SEED, 0, 1)
+    mloc, nloc = 10, 17
+    first, stride = 1, 2
+    kb = (nloc - 1 - first) // stride + 1
+    bb = bs * bs
+    out = torch.full((mloc * kb * bb,), float("nan"), dtype=torch.float64, device="cuda")
+    bounds = [0, 0, 1, 2, 5, kb]
+    for q0, q1 in zip(bounds[:-1], bounds[1:]):
+        if q1 > q0:
+            dbm.debug_pack_panel(m, 0, first + q0 * stride, stride, q1 - q0, out[q0 * bb:], pitch=kb)
+    ref = orc.pack_panel(orc.fill_arena(SEED, 0, 1, rows, cols, bs), mloc, nloc, bs, 0,
+                         [first + q * stride for q in range(kb)])
+    assert np.array_equal(host(out), ref)
+
+
+def test_pack_panel_validation(dbm, ctx):
+    m = dbm.Matrix(ctx, 88, 66, 22)
+    out = torch.empty(64 * 22 * 22, dtype=torch.float64, device="cuda")
+    for args, name in [((2, 0, 1, 1), "DBM_ERR_ARG"), ((0, 2, 1, 2), "DBM_ERR_RANGE"), ((1, 0, 1, 5), "DBM_ERR_RANGE"),
+                       ((0, 0, 0, 1), "DBM_ERR_ARG")]:
+        with pytest.raises(dbm.DbmError) as e:
+            dbm.debug_pack_panel(m, *args, out)
+        assert e.value.name == name
+
+
 # ------------------------------------------------------------------ full multiply vs the oracle
 def run_multiply(dbm, ctx, orc, M, N, K, bs, path, alpha, beta, kind=0, cap=0, chunk=None):
     A, B, C = dbm.Matrix(ctx, M, K, bs), dbm.Matrix(ctx, K, N, bs), dbm.Matrix(ctx, M, N, bs)

@@ -98,9 +98,33 @@ dbm_status densify_b(dbm_ctx ctx, dbm_matrix B, int64_t row0, int64_t stride, in
 void undensify_c(dbm_matrix C, const double* dense, int64_t ld, int nsplit, int64_t split_stride, double alpha,
                  double beta, cudaStream_t cs);
 void launch_scale(double* x, int64_t n, double beta, cudaStream_t st);  // x = beta * x (beta 0: zeros)
-// All-gather of the workspaces' CUDA IPC handles (maps the peers' workspaces; doubles as the "every
-// rank's panels are ready" barrier).  Synchronises the comm stream.
+// All-gather of the workspaces' CUDA IPC handles (maps the peers' workspaces).  Synchronises the comm
+// stream: it runs only when a rank registers a new workspace (xattach / dbm_ctx_set_workspace).
 dbm_status ipc_exchange(dbm_ctx ctx, void* ws);
+
+// ---- device-side signals between ranks (copy-engine transport)
+// Every rank's registered workspace starts with a header of int64 words its peers write into through
+// the IPC mappings: word (kind * P + q) holds the last epoch for which peer q announced `kind`, then the
+// host pipeline's progress table [peer][operand][kappa] = (epoch << 32) | K-blocks in place.  Values
+// only grow (epochs count the copy-engine multiplies, identical on every rank), so no table is ever
+// reset between multiplies; registration zeroes the header once, ordered before any peer write by the
+// registration all-gather.  Waits are cuStreamWaitValue64 (GEQ) on a stream, writes
+// cuStreamWriteValue64: no SM spins and no host round trip.
+enum XKind { X_READY = 0, X_MID = 1, X_DONE = 2, X_KINDS = 3 };
+size_t xhdr_bytes(int nranks, int L);           // header bytes at the start of the workspace (0: one rank)
+inline size_t xprog_word(int P, int L, int peer, int operand, int kappa) {
+  return (size_t)X_KINDS * P + ((size_t)peer * 2 + operand) * L + kappa;
+}
+// Make `ws` this rank's registered workspace (collective when it changes: zero the header, all-gather
+// the IPC handles).  Fast path (ws already registered): nothing.
+dbm_status xattach(dbm_ctx ctx, char* ws, cudaStream_t cs);
+// Write `value` into word (kind, me) of every peer's header / wait on stream st until word (kind, q) of
+// my header holds >= value for every peer q.
+dbm_status xsignal(dbm_ctx ctx, cudaStream_t st, int kind, uint64_t value);
+dbm_status xwait(dbm_ctx ctx, cudaStream_t st, int kind, uint64_t value);
+// Single words: write my progress into peer q's table / wait for peer q's progress in mine.
+dbm_status xwrite_word(dbm_ctx ctx, cudaStream_t st, int q, size_t word, uint64_t value);
+dbm_status xwait_word(dbm_ctx ctx, cudaStream_t st, size_t word, uint64_t value);
 
 // ---- tall-and-skinny (multiply_tallskinny.cu, reading R14)
 size_t ts_workspace_bytes(int pr, int pc, int r, int c, int64_t Mb, int64_t Nb, int64_t Kb, int64_t bs);

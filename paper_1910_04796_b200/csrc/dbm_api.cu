@@ -602,11 +602,16 @@ namespace {
 // step-0 pull + GEMM all run in the same 5 K-chunks of each panel (1, 1, 2, 4, 8 sixteenths).  The
 // boundaries depend only on the panel's block count, which every rank agrees on, so an owner's
 // progress after chunk j is exactly what a consumer's chunk j needs.
+// Densified panels of an odd block size keep every chunk start even (in blocks), so the GEMM's TMA base
+// Ap + k0*bs stays 16-byte aligned (`even`); the last bound is always kb.
 constexpr int kHostPipeChunks = 5;
-inline int64_t host_pipe_bound(int64_t kb, int j) {
+inline int64_t host_pipe_bound(int64_t kb, int j, bool even = false) {
   static const int F[kHostPipeChunks + 1] = {0, 1, 2, 4, 8, 16};
-  return kb * F[j] / 16;
+  if (j >= kHostPipeChunks) return kb;
+  const int64_t b = kb * F[j] / 16;
+  return even ? b / 2 * 2 : b;
 }
+inline bool host_pipe_even(bool densified, int64_t bs) { return densified && (bs & 1); }
 
 struct Plan {
   int L = 1;
@@ -621,7 +626,6 @@ struct Plan {
   // workspace regions (byte offsets)
   size_t off_cd = 0, off_ownA = 0, off_ownB = 0, off_recvA[2] = {0, 0}, off_recvB[2] = {0, 0}, off_part = 0;
   size_t off_trav = 0, off_trip = 0, off_spart = 0;  // smm split-K partials
-  size_t off_flags = 0;  // several ranks: [peer][operand][kappa] int64 progress of the peers' own panels
   bool mixed = false;                                 // bs 22 squares inside a non-square traversal
   // densified bs 64 with a dense B: B is never densified -- the GEMM reads B's 64 x 64 blocks in place
   // (arena, or packed panels the peers pull), through a 4-D TMA view (§8f-3, zero-copy B)
@@ -672,7 +676,7 @@ Plan make_plan_raw(int nranks, int pr, int pc, int r, int c, int64_t Mb, int64_t
   p.densified = densified;
   p.kb.resize(p.L);
   for (int k = 0; k < p.L; ++k) p.kb[k] = local_count(p.Kb, p.L, k);
-  size_t off = 0;
+  size_t off = xhdr_bytes(nranks, p.L);  // several ranks: the signal header comes first
   auto take = [&](size_t bytes) {
     size_t o = off;
     off = align256(off + bytes);
@@ -703,9 +707,10 @@ Plan make_plan_raw(int nranks, int pr, int pc, int r, int c, int64_t Mb, int64_t
         const std::vector<int64_t> b = pipeline_chunks(p.kb[p.kappa(s)]);  // step 0 may be chunked
         for (size_t j = 1; j < b.size(); ++j)
           p.max_split = std::max(p.max_split, pick_splitk(M, N, (b[j] - b[j - 1]) * p.bs, num_sms()));
+        const bool ev = host_pipe_even(true, p.bs);
         for (int j = 0; j < kHostPipeChunks; ++j)  // host-operand pipeline chunks (dbm_multiply_host)
-          p.max_split = std::max(p.max_split, pick_splitk(M, N, (host_pipe_bound(p.kb[p.kappa(s)], j + 1) -
-                                                                 host_pipe_bound(p.kb[p.kappa(s)], j)) * p.bs,
+          p.max_split = std::max(p.max_split, pick_splitk(M, N, (host_pipe_bound(p.kb[p.kappa(s)], j + 1, ev) -
+                                                                 host_pipe_bound(p.kb[p.kappa(s)], j, ev)) * p.bs,
                                                           num_sms()));
       }
     }
@@ -766,7 +771,6 @@ Plan make_plan_raw(int nranks, int pr, int pc, int r, int c, int64_t Mb, int64_t
     }
     for (int i = 0; i < std::min(nA, 2); ++i) p.off_recvA[i] = take(amax);
     for (int i = 0; i < std::min(nB, 2); ++i) p.off_recvB[i] = take(bmax);
-    p.off_flags = take((size_t)nranks * 2 * p.L * 8);
   }
   p.total = std::max<size_t>(off, 256);
   return p;
@@ -1050,16 +1054,37 @@ dbm_status dbm::ipc_exchange(dbm_ctx ctx, void* ws) {
   return DBM_OK;
 }
 
-namespace {
+size_t dbm::xhdr_bytes(int nranks, int L) {
+  if (nranks <= 1) return 0;
+  return align256((size_t)8 * nranks * (X_KINDS + 2 * (size_t)L));
+}
 
-// Pull this rank's step-s panels from their owners' workspaces (peer plans give the offsets).
-// Host-operand pipeline: wait (on the comm stream) until the owner of op's panel has published at
-// least `need` K-blocks of it into this rank's flag table.
-dbm_status wait_panel(dbm_ctx ctx, const Plan& p, const char* flags, const XOp& op, int64_t need) {
-  if (!flags || need <= 0) return DBM_OK;
-  const char* f = flags + ((size_t)(op.peer * 2 + op.operand) * p.L + op.kappa) * 8;
-  if (memops(ctx->device).wait(ctx->comm, (CUdeviceptr)f, (cuuint64_t)need, CU_STREAM_WAIT_VALUE_GEQ) !=
-      CUDA_SUCCESS) {
+dbm_status dbm::xattach(dbm_ctx ctx, char* ws, cudaStream_t cs) {
+  ARG_CHECK(memops(ctx->device).ok, DBM_ERR_CUDA, "64-bit stream memory operations unavailable");
+  if (ws == (char*)ctx->ipc_ws && (int)ctx->peer_ws.size() == ctx->nranks) return DBM_OK;
+  // new workspace: zero its header, then the all-gather (after the memset on every rank) registers it
+  const int L = (int)lcm64(ctx->pr, ctx->pc);
+  CUDA_TRY(ctx, cudaMemsetAsync(ws, 0, xhdr_bytes(ctx->nranks, L), cs));
+  cudaEvent_t e = get_event(ctx);
+  CUDA_TRY(ctx, cudaEventRecord(e, cs));
+  CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->comm, e, 0));
+  ctx->ev_pool.push_back(e);
+  return ipc_exchange(ctx, ws);
+}
+
+dbm_status dbm::xwrite_word(dbm_ctx ctx, cudaStream_t st, int q, size_t word, uint64_t value) {
+  if (memops(ctx->device).write(st, (CUdeviceptr)(ctx->peer_ws[q] + word * 8), (cuuint64_t)value,
+                                CU_STREAM_WRITE_VALUE_DEFAULT) != CUDA_SUCCESS) {
+    set_error("cuStreamWriteValue64 failed");
+    ctx->poisoned = DBM_ERR_CUDA;
+    return DBM_ERR_CUDA;
+  }
+  return DBM_OK;
+}
+
+dbm_status dbm::xwait_word(dbm_ctx ctx, cudaStream_t st, size_t word, uint64_t value) {
+  if (memops(ctx->device).wait(st, (CUdeviceptr)((char*)ctx->ipc_ws + word * 8), (cuuint64_t)value,
+                               CU_STREAM_WAIT_VALUE_GEQ) != CUDA_SUCCESS) {
     set_error("cuStreamWaitValue64 failed");
     ctx->poisoned = DBM_ERR_CUDA;
     return DBM_ERR_CUDA;
@@ -1067,15 +1092,40 @@ dbm_status wait_panel(dbm_ctx ctx, const Plan& p, const char* flags, const XOp& 
   return DBM_OK;
 }
 
+dbm_status dbm::xsignal(dbm_ctx ctx, cudaStream_t st, int kind, uint64_t value) {
+  for (int q = 0; q < ctx->nranks; ++q)
+    if (q != ctx->rank)
+      if (dbm_status e = xwrite_word(ctx, st, q, (size_t)kind * ctx->nranks + ctx->rank, value)) return e;
+  return DBM_OK;
+}
+
+dbm_status dbm::xwait(dbm_ctx ctx, cudaStream_t st, int kind, uint64_t value) {
+  for (int q = 0; q < ctx->nranks; ++q)
+    if (q != ctx->rank)
+      if (dbm_status e = xwait_word(ctx, st, (size_t)kind * ctx->nranks + q, value)) return e;
+  return DBM_OK;
+}
+
+namespace {
+
+// Pull this rank's step-s panels from their owners' workspaces (peer plans give the offsets).
+// Host-operand pipeline (hp_epoch != 0): wait (on the comm stream) until the owner of op's panel has
+// published at least `need` K-blocks of it for this multiply into this rank's progress table.
+dbm_status wait_panel(dbm_ctx ctx, const Plan& p, uint64_t hp_epoch, const XOp& op, int64_t need) {
+  if (!hp_epoch || need <= 0) return DBM_OK;
+  return xwait_word(ctx, ctx->comm, xprog_word(ctx->nranks, p.L, op.peer, op.operand, op.kappa),
+                    (hp_epoch << 32) | (uint64_t)need);
+}
+
 dbm_status post_pulls(dbm_ctx ctx, const Plan& p, const std::vector<Plan>& peer_plan, int s, char* ws, int bufA,
-                      int bufB, int64_t* sent, int64_t* recv, const char* flags = nullptr) {
+                      int bufB, int64_t* sent, int64_t* recv, uint64_t hp_epoch = 0) {
   for (const XOp& op : exchange_ops(p, s)) {
     const size_t n = (size_t)op.bytes;
     if (op.send) {  // the peer pulls it; counted for the statistics
       *sent += (int64_t)n;
       continue;
     }
-    if (dbm_status e = wait_panel(ctx, p, flags, op, p.kb[op.kappa])) return e;
+    if (dbm_status e = wait_panel(ctx, p, hp_epoch, op, p.kb[op.kappa])) return e;
     const Plan& q = peer_plan[op.peer];
     const size_t src_off = op.operand == 0 ? q.ownA_off[op.kappa] : q.ownB_off[op.kappa];
     ARG_CHECK(src_off != SIZE_MAX && ctx->peer_ws[op.peer], DBM_ERR_PLAN, "peer panel not in its workspace");
@@ -1091,14 +1141,14 @@ dbm_status post_pulls(dbm_ctx ctx, const Plan& p, const std::vector<Plan>& peer_
 // panel once (count == true on the first chunk).
 dbm_status post_pulls_chunk(dbm_ctx ctx, const Plan& p, const std::vector<Plan>& peer_plan, int s, char* ws, int bufA,
                             int bufB, int64_t k0, int64_t k1, bool count, int64_t* sent, int64_t* recv,
-                            const char* flags = nullptr) {
+                            uint64_t hp_epoch = 0) {
   for (const XOp& op : exchange_ops(p, s)) {
     if (op.send) {
       if (count) *sent += op.bytes;
       continue;
     }
     if (k1 > k0)
-      if (dbm_status e = wait_panel(ctx, p, flags, op, k1)) return e;
+      if (dbm_status e = wait_panel(ctx, p, hp_epoch, op, k1)) return e;
     const Plan& q = peer_plan[op.peer];
     const size_t src_off = op.operand == 0 ? q.ownA_off[op.kappa] : q.ownB_off[op.kappa];
     ARG_CHECK(src_off != SIZE_MAX && ctx->peer_ws[op.peer], DBM_ERR_PLAN, "peer panel not in its workspace");
@@ -1318,6 +1368,7 @@ dbm_status multiply_impl(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_matrix B, 
   // step-0 pull + GEMM run chunk by chunk, the pulls gated by the owners' published progress
   const bool hpipe = hio && ctx->nranks > 1 && ctx->transport == 0 && ctx->host_pipe && alpha != 0.0 && p.Kb > 0 &&
                      !A->sparse && !B->sparse && !C->sparse && memops(ctx->device).ok;
+  const bool hp_even = host_pipe_even(dens, p.bs);
   if (hpipe) {
     cudaEvent_t e0 = get_event(ctx);
     CUDA_TRY(ctx, cudaEventRecord(e0, ctx->stream));  // previous work on the arenas is done
@@ -1337,7 +1388,7 @@ dbm_status multiply_impl(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_matrix B, 
       // local A columns / B rows that hold the first host_pipe_bound(kb, j + 1) blocks of every own panel
       int64_t hiA = loA, hiB = loB;
       for (int k = 0; k < p.L; ++k) {
-        const int64_t q1 = host_pipe_bound(p.kb[k], j + 1);
+        const int64_t q1 = host_pipe_bound(p.kb[k], j + 1, hp_even);
         if (q1 <= 0) continue;
         if (k % p.pc == p.c) hiA = std::max(hiA, (k - p.c) / p.pc + (q1 - 1) * (p.L / p.pc) + 1);
         if (k % p.pr == p.r) hiB = std::max(hiB, (k - p.r) / p.pr + (q1 - 1) * (p.L / p.pr) + 1);
@@ -1492,62 +1543,67 @@ dbm_status multiply_impl(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_matrix B, 
   cudaEvent_t ev_ready = nullptr;
   std::vector<int> bufA_of(p.L, -1), bufB_of(p.L, -1);
   std::vector<Plan> peer_plan;
-  // pipelined host operands: own panels densified chunk by chunk inside Cannon's step 0
-  auto own_panels_chunk = [&](int j) -> dbm_status {
-    CUDA_TRY(ctx, cudaStreamWaitEvent(cs, hio->up_ev[j], 0));
-    for (int k = 0; k < p.L; ++k) {
-      const int64_t q0 = host_pipe_bound(p.kb[k], j), q1 = host_pipe_bound(p.kb[k], j + 1);
-      if (q1 <= q0) continue;
-      if (p.ownA_off[k] != SIZE_MAX && M) {
-        const int64_t col0 = (k - p.c) / p.pc, stride = p.L / p.pc;
-        ProfScope ps(ctx, cs, 2, 0.0, 16.0 * M * (q1 - q0) * bs);
-        if (dens) {
-          double* dst = (double*)(ws + p.ownA_off[k]) + q0 * bs;
-          if (dbm_status e = densify_a(ctx, A, col0 + q0 * stride, stride, q1 - q0, dst, p.ld_panel(k), 1, cs))
-            return e;
-        } else {  // packed A panel: mloc rows of kb[k] blocks; this chunk is columns [q0, q1) of every row
-          double* dst = (double*)(ws + p.ownA_off[k]) + q0 * bb;
-          launch_pack_cols(A->arena, p.mloc, p.kA, (int)bs, col0 + q0 * stride, stride, q1 - q0, dst, cs, p.kb[k]);
-        }
-        ++launches;
-      }
-      if (p.ownB_off[k] != SIZE_MAX && N) {
-        const int64_t row0 = (k - p.r) / p.pr, stride = p.L / p.pr;
-        ProfScope ps(ctx, cs, 2, 0.0, 16.0 * N * (q1 - q0) * bs);
-        if (dens && !p.b_packed) {
-          double* dst = (double*)(ws + p.ownB_off[k]) + q0 * bs;
-          if (dbm_status e = densify_b(ctx, B, row0 + q0 * stride, stride, q1 - q0, dst, p.ld_panel(k), 0, cs))
-            return e;
-        } else {
-          double* dst = (double*)(ws + p.ownB_off[k]) + q0 * p.nloc * bb;
-          launch_pack_rows(B->arena, p.nloc, (int)bs, row0 + q0 * stride, stride, q1 - q0, dst, cs);
-        }
-        ++launches;
-      }
-    }
-    CUDA_TRY(ctx, cudaGetLastError());
-    // publish: every peer's table entry [me][operand][k] = K-blocks of my panel k now in place
-    const MemOps& mo = memops(ctx->device);
+  // Pipelined host operands: this rank's own panels are densified (or packed) chunk by chunk on the
+  // upload stream, each chunk right behind its upload, and after every chunk the rank publishes its
+  // progress into every peer's flag table.  All of this is enqueued BEFORE any wait on a peer's flag:
+  // a rank's signals then never sit behind its own waits (in a stream or in the host's program order),
+  // so host calls that synchronise the device (lazy kernel loading, cudaFree, ...) cannot close a
+  // cycle across ranks -- the round-1 hang was exactly that: flag waits enqueued, then a first kernel
+  // launch loaded its module, synchronised, and waited forever on the peer doing the same.
+  std::vector<cudaEvent_t> own_ev;  // own panels' chunk j in place (upload stream)
+  cudaStream_t up = hpipe ? ctx->up : nullptr;
+  uint64_t ep = 0;  // this multiply's epoch (copy-engine transport)
+  auto publish = [&](int j, bool final_) -> dbm_status {
+    // every peer's table entry [me][operand][k] = (epoch, K-blocks of my panel k now in place)
     for (int q = 0; q < ctx->nranks; ++q) {
       if (q == ctx->rank) continue;
       for (int k = 0; k < p.L; ++k)
         for (int o = 0; o < 2; ++o) {
           if ((o == 0 ? p.ownA_off[k] : p.ownB_off[k]) == SIZE_MAX) continue;
-          char* f = ctx->peer_ws[q] + peer_plan[q].off_flags + ((size_t)(ctx->rank * 2 + o) * p.L + k) * 8;
-          if (mo.write(cs, (CUdeviceptr)f, (cuuint64_t)host_pipe_bound(p.kb[k], j + 1), CU_STREAM_WRITE_VALUE_DEFAULT) !=
-              CUDA_SUCCESS) {
-            set_error("cuStreamWriteValue64 failed");
-            ctx->poisoned = DBM_ERR_CUDA;
-            return DBM_ERR_CUDA;
-          }
+          const int64_t v = final_ ? p.kb[k] : host_pipe_bound(p.kb[k], j + 1, hp_even);
+          if (dbm_status e = xwrite_word(ctx, up, q, xprog_word(ctx->nranks, p.L, ctx->rank, o, k), (ep << 32) | (uint64_t)v))
+            return e;
         }
     }
     return DBM_OK;
   };
+  auto own_panels_chunk = [&](int j) -> dbm_status {
+    for (int k = 0; k < p.L; ++k) {
+      const int64_t q0 = host_pipe_bound(p.kb[k], j, hp_even), q1 = host_pipe_bound(p.kb[k], j + 1, hp_even);
+      if (q1 <= q0) continue;
+      if (p.ownA_off[k] != SIZE_MAX && M) {
+        const int64_t col0 = (k - p.c) / p.pc, stride = p.L / p.pc;
+        ProfScope ps(ctx, up, 2, 0.0, 16.0 * M * (q1 - q0) * bs);
+        if (dens) {
+          double* dst = (double*)(ws + p.ownA_off[k]) + q0 * bs;
+          if (dbm_status e = densify_a(ctx, A, col0 + q0 * stride, stride, q1 - q0, dst, p.ld_panel(k), 1, up))
+            return e;
+        } else {  // packed A panel: mloc rows of kb[k] blocks; this chunk is columns [q0, q1) of every row
+          double* dst = (double*)(ws + p.ownA_off[k]) + q0 * bb;
+          launch_pack_cols(A->arena, p.mloc, p.kA, (int)bs, col0 + q0 * stride, stride, q1 - q0, dst, up, p.kb[k]);
+        }
+        ++launches;
+      }
+      if (p.ownB_off[k] != SIZE_MAX && N) {
+        const int64_t row0 = (k - p.r) / p.pr, stride = p.L / p.pr;
+        ProfScope ps(ctx, up, 2, 0.0, 16.0 * N * (q1 - q0) * bs);
+        if (dens && !p.b_packed) {
+          double* dst = (double*)(ws + p.ownB_off[k]) + q0 * bs;
+          if (dbm_status e = densify_b(ctx, B, row0 + q0 * stride, stride, q1 - q0, dst, p.ld_panel(k), 0, up))
+            return e;
+        } else {
+          double* dst = (double*)(ws + p.ownB_off[k]) + q0 * p.nloc * bb;
+          launch_pack_rows(B->arena, p.nloc, (int)bs, row0 + q0 * stride, stride, q1 - q0, dst, up);
+        }
+        ++launches;
+      }
+    }
+    CUDA_TRY(ctx, cudaGetLastError());
+    return publish(j, false);
+  };
   int nsub0 = 1;               // K-chunks of the step-0 pull (copy-engine transport, densified)
   cudaEvent_t ev_c[kMaxChunks] = {};
   std::vector<int64_t> cb0{0, 0};
-  const char* hp_flags = hpipe ? ws + p.off_flags : nullptr;  // my table of the owners' progress
   auto recv_bytes = [&](int s) {
     double n = 0;
     for (const XOp& op : exchange_ops(p, s)) n += op.send ? 0 : (double)op.bytes;
@@ -1556,7 +1612,8 @@ dbm_status multiply_impl(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_matrix B, 
   auto exchange = [&](int s) -> dbm_status {
     if (ctx->transport == 0) {
       ProfScope ps(ctx, ctx->comm, 5, 0.0, recv_bytes(s));  // copy-engine pulls of this step
-      return post_pulls(ctx, p, peer_plan, s, ws, bufA_of[s], bufB_of[s], &st.bytes_sent, &st.bytes_recv, hp_flags);
+      return post_pulls(ctx, p, peer_plan, s, ws, bufA_of[s], bufB_of[s], &st.bytes_sent, &st.bytes_recv,
+                        hpipe ? ep : 0);
     }
     return post_exchange(ctx, p, s, ws, A->arena, B->arena, bufA_of[s], bufB_of[s], &st.bytes_sent, &st.bytes_recv);
   };
@@ -1574,17 +1631,40 @@ dbm_status multiply_impl(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_matrix B, 
       ev_g[s] = get_event(ctx);
     }
     if (ctx->transport == 0) {
-      // handle all-gather after my panels are ready = barrier: every owner's panels are ready after it.
-      // Pipelined host operands: nothing is ready yet -- the barrier only orders the reset of my flag
-      // table before any peer's progress write; the pulls then wait on the flags.
-      if (hpipe) CUDA_TRY(ctx, cudaMemsetAsync(ws + p.off_flags, 0, (size_t)ctx->nranks * 2 * p.L * 8, ctx->comm));
-      if (dbm_status e = ipc_exchange(ctx, ws)) return e;
+      // Copy engines over the IPC-mapped workspaces, ordered by device-side signals (no host sync once
+      // the workspace is registered): every signal this rank owes its peers -- "my panels are ready"
+      // (on the compute stream, behind my own densify / pack) or, with host operands, the chunk-by-chunk
+      // progress (upload stream) -- is enqueued before the first wait on theirs.
+      if (dbm_status e = xattach(ctx, ws, cs)) return e;
+      ep = ++ctx->epoch;
       peer_plan.resize(ctx->nranks);
       for (int q = 0; q < ctx->nranks; ++q)
         if (q != ctx->rank)
           peer_plan[q] = make_plan_raw(ctx->nranks, p.pr, p.pc, q / p.pc, q % p.pc, p.Mb, p.Nb, p.Kb, p.bs, dens,
                                        ctx->chunk_bytes, ctx->transport, p.b_packed);
+      if (hpipe) {
+        for (int j = 0; j < kHostPipeChunks; ++j) {
+          if (dbm_status e = own_panels_chunk(j)) {
+            // the peers drain instead of hanging (final progress + my "done"); the ctx is poisoned
+            publish(kHostPipeChunks - 1, true);
+            xsignal(ctx, up, X_DONE, ep);
+            ctx->poisoned = e;
+            return e;
+          }
+          own_ev.push_back(get_event(ctx));
+          CUDA_TRY(ctx, cudaEventRecord(own_ev.back(), up));
+        }
+      } else {
+        if (dbm_status e = xsignal(ctx, cs, X_READY, ep)) return e;
+        if (dbm_status e = xwait(ctx, ctx->comm, X_READY, ep)) return e;  // every owner's panels are ready
+      }
     }
+  }
+
+  // Everything after the Cannon setup runs in body(): whatever it returns, the closing barrier below is
+  // still enqueued, so an error on one rank (poisoning its ctx) does not leave its peers waiting in theirs.
+  auto body = [&]() -> dbm_status {
+  if (ctx->nranks > 1) {
     // Step 0 is the one exchange nothing overlaps with (Cannon's initial alignment).  With the copy
     // engines and densified panels it is pulled in K-chunks, each followed by its GEMM chunk, so only
     // the first chunk's transfer is exposed.
@@ -1592,7 +1672,7 @@ dbm_status multiply_impl(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_matrix B, 
     const int64_t kb0 = p.kb[p.kappa(0)];
     if (hpipe) {  // the fixed host-pipeline chunks, even when both step-0 panels are local
       cb0.resize(kHostPipeChunks + 1);
-      for (int j = 0; j <= kHostPipeChunks; ++j) cb0[j] = host_pipe_bound(kb0, j);
+      for (int j = 0; j <= kHostPipeChunks; ++j) cb0[j] = host_pipe_bound(kb0, j, hp_even);
       nsub0 = kHostPipeChunks;
     } else if (ctx->transport == 0 && remote0 && (!dens || bs % 2 == 0) && kb0 >= 2) {
       const double pull = ((p.a_src(0) != p.me() ? p.mloc : 0) + (p.b_src(0) != p.me() ? p.nloc : 0)) * (double)bs * bs * 8;
@@ -1604,7 +1684,7 @@ dbm_status multiply_impl(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_matrix B, 
       for (int j = 0; j < nsub0; ++j) {
         ev_c[j] = get_event(ctx);
         if (dbm_status e = post_pulls_chunk(ctx, p, peer_plan, 0, ws, bufA_of[0], bufB_of[0], cb0[j], cb0[j + 1],
-                                            j == 0, &st.bytes_sent, &st.bytes_recv, hp_flags))
+                                            j == 0, &st.bytes_sent, &st.bytes_recv, hpipe ? ep : 0))
           return e;
         CUDA_TRY(ctx, cudaEventRecord(ev_c[j], ctx->comm));
       }
@@ -1626,9 +1706,7 @@ dbm_status multiply_impl(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_matrix B, 
     }
     const int64_t kbk = p.kb[k];
     if (hpipe && s == 0 && !dens) CUDA_TRY(ctx, cudaStreamWaitEvent(cs, hio->c_ev, 0));  // C_in (uploaded first)
-    if (hpipe && s == 0 && !dens && !(kbk > 0 && p.mloc * p.nloc > 0))
-      for (int j = 0; j < nsub0; ++j)  // nothing to multiply here, but the peers wait for my panels
-        if (dbm_status e = own_panels_chunk(j)) return e;
+    if (hpipe && s == 1) CUDA_TRY(ctx, cudaStreamWaitEvent(cs, own_ev.back(), 0));  // all own panels in place
     // operand panels for this step
     const double* Ap;
     const double* Bp;
@@ -1711,8 +1789,7 @@ dbm_status multiply_impl(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_matrix B, 
         const int nsub = (s == 0) ? nsub0 : 1;
         for (int j = 0; j < nsub; ++j) {
           const int64_t k0 = nsub > 1 ? cb0[j] : 0, k1 = nsub > 1 ? cb0[j + 1] : kbk;
-          if (hpipe && s == 0)  // my own panels' chunk j (the peers' pulls wait for it), before my GEMM j
-            if (dbm_status e = own_panels_chunk(j)) return e;
+          if (hpipe && s == 0) CUDA_TRY(ctx, cudaStreamWaitEvent(cs, own_ev[j], 0));  // my own panels' chunk j
           if (nsub > 1) CUDA_TRY(ctx, cudaStreamWaitEvent(cs, ev_c[j], 0));
           // host C: the multiply's last GEMM runs in row panels, each undensified and downloaded on the
           // copy stream while the next panel multiplies (as on one rank)
@@ -1775,8 +1852,7 @@ dbm_status multiply_impl(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_matrix B, 
       const int nsub = (s == 0) ? nsub0 : 1;
       for (int j = 0; j < nsub; ++j) {
         const int64_t k0 = nsub > 1 ? cb0[j] : 0, nk = nsub > 1 ? cb0[j + 1] - cb0[j] : kbk;
-        if (hpipe && s == 0)  // my own panels' chunk j (the peers' pulls wait for it)
-          if (dbm_status e = own_panels_chunk(j)) return e;
+        if (hpipe && s == 0) CUDA_TRY(ctx, cudaStreamWaitEvent(cs, own_ev[j], 0));  // my own panels' chunk j
         if (nsub > 1) CUDA_TRY(ctx, cudaStreamWaitEvent(cs, ev_c[j], 0));
         if (nk == 0) continue;  // (host pipeline, ragged K: empty leading chunks)
         const double* Aj = Ap + k0 * bb;
@@ -1822,8 +1898,9 @@ dbm_status multiply_impl(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_matrix B, 
   }
 
   if (ctx->nranks > 1) {
-    // the comm stream's last op covers every transfer of this rank
+    // the comm stream's last op covers every transfer of this rank (and the upload stream's own panels)
     CUDA_TRY(ctx, cudaStreamWaitEvent(cs, ev_x[p.L - 1], 0));
+    if (hpipe) CUDA_TRY(ctx, cudaStreamWaitEvent(cs, own_ev.back(), 0));
   }
   if (dens && M * N > 0 && !(hio && hio->c_downloaded)) {
     if (hio && hio->c_ev) CUDA_TRY(ctx, cudaStreamWaitEvent(cs, hio->c_ev, 0));  // C_in uploaded
@@ -1832,13 +1909,20 @@ dbm_status multiply_impl(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_matrix B, 
     ++launches;
     CUDA_TRY(ctx, cudaGetLastError());
   }
+  return DBM_OK;
+  };
+  const dbm_status berr = body();
   if (ctx->nranks > 1 && ctx->transport == 0) {
-    // Closing barrier, on the COMPUTE stream after this rank's last GEMM: once every rank passed it,
-    // no peer still pulls from this workspace, so stream-ordered reuse of it is safe.  (A barrier
-    // kernel on the comm stream would start while the persistent GEMM runs, pin an SM until the
-    // slowest peer arrives and leave one GEMM CTA's whole item list waiting behind it.)
-    int* w = ctx->d_scratch;
-    NCCL_TRY(ctx, ncclAllReduce(w, w, 1, ncclInt, ncclSum, (ncclComm_t)ctx->nccl, cs));
+    // Closing barrier: "done" goes out on the comm stream behind my last pull, and the compute stream
+    // (after my last GEMM) waits for every peer's "done": when it passes, no peer still pulls from this
+    // workspace, so stream-ordered reuse of it is safe.  Device-side signals: no kernel spins on an SM
+    // next to the persistent GEMM, no host round trip.
+    if (dbm_status e = xsignal(ctx, ctx->comm, X_DONE, ep)) return e;
+    if (dbm_status e = xwait(ctx, cs, X_DONE, ep)) return e;
+  }
+  if (berr != DBM_OK) {
+    if (ctx->poisoned == DBM_OK) ctx->poisoned = berr;
+    return berr;
   }
   if (ctx->nranks > 1) {
     // events are reusable once the compute stream has passed them; recycle after this call
@@ -1850,6 +1934,7 @@ dbm_status multiply_impl(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_matrix B, 
       ctx->ev_pool.push_back(ev_g[s]);
     }
     for (int j = 0; j < nsub0 && nsub0 > 1; ++j) ctx->ev_pool.push_back(ev_c[j]);
+    for (cudaEvent_t e : own_ev) ctx->ev_pool.push_back(e);
     ctx->ev_pool.push_back(done);
   }
   ctx->launches += launches;

@@ -176,8 +176,9 @@ struct dbm_ctx_s {
   // 1 = NCCL grouped send/recv.
   int transport = 0;
   int algorithm = 0;  // 0 = Cannon, 1 = tall-and-skinny
-  void* ipc_ws = nullptr;                 // workspace the peer mappings were built for
+  void* ipc_ws = nullptr;                 // registered workspace: the one the peer mappings were built for
   int64_t ipc_ws_bytes = 0;
+  uint64_t epoch = 0;                     // copy-engine multiplies so far (the same count on every rank)
   std::vector<char*> peer_ws;             // peer workspaces mapped into this process (nullptr = self)
   std::vector<std::vector<char>> peer_handles;  // raw IPC handles (to re-use / close mappings)
   std::vector<void*> peer_bases;          // opened allocation bases (cudaIpcCloseMemHandle)

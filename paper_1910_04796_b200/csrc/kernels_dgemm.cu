@@ -88,7 +88,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     int k_tiles_total, int k_tiles_per_split, int nsplit, int tiles_m, int tiles_n,
                     double* __restrict__ C,
                     int64_t ldc, double alpha, double beta, double* __restrict__ partial,
-                    unsigned* __restrict__ wave_sync, int sync_kt, int sync_rounds, int b_blocks) {
+                    unsigned* __restrict__ wave_sync, int sync_kt, int sync_rounds, int slack, int b_blocks) {
   using T = Tile<BM, BN>;
   constexpr int STAGES = T::STAGES, kStage = T::kStage, kStageA = T::kStageA, MI = T::MI, NI = T::NI;
   extern __shared__ uint8_t smem_raw[];
@@ -140,12 +140,15 @@ __global__ void __launch_bounds__(kThreads, 1)
         item_coords(item, tm, tn, split);
         item_k(split, kt0, nkt);
         for (int kt = 0; kt < nkt; ++kt) {
-          // Optional wave barrier (cooperative launch only): every sync_kt k-tiles of the rounds every
-          // CTA runs, the producers re-align so one wave's A/B panels are read from L2, not HBM.
+          // Fuzzy wave barrier (cooperative launch only): every sync_kt k-tiles of the rounds every CTA
+          // runs, a producer announces its arrival and waits only until every CTA has reached the
+          // sync point `slack` intervals back.  CTAs then never drift more than (slack + 1) intervals
+          // apart in k, so one wave's A/B panel slices stay in L2 (read once from HBM), while a CTA
+          // stalls only if it gets a whole interval ahead of the slowest one.
           if (wave_sync != nullptr && round < sync_rounds && kt % sync_kt == 0) {
             ++epoch;
             atomicAdd(wave_sync, 1u);
-            const unsigned target = epoch * gridDim.x;
+            const unsigned target = epoch > (unsigned)slack ? (epoch - (unsigned)slack) * gridDim.x : 0u;
             unsigned seen;
             do {
               asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(seen) : "l"(wave_sync) : "memory");
@@ -184,20 +187,20 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int g = lane >> 2, t = lane & 3;
   const uint32_t a_row = (uint32_t)(wm * (BM / 2) + g) * 128u;
   const uint32_t b_row = (uint32_t)(wn * (BN / 4) + g) * 128u;
-  uint32_t koff[4];
-#pragma unroll
-  for (int ks = 0; ks < 4; ++ks) {
-    const int k = 2 * ks + (t & 1) + 8 * (t >> 1);
-    koff[ks] = (uint32_t)((((k >> 1) ^ g) << 4) | ((k & 1) << 3));
-  }
+  // k>>1 = ks + 4 (t>>1) with ks < 4, so ((k>>1) ^ g) = ks ^ G: the per-ks offsets are one XOR away from
+  // two lane constants (cheaper than four live registers under the 168-register cap)
+  const uint32_t G = (uint32_t)(g ^ (4 * (t >> 1))), kodd = (uint32_t)(t & 1) << 3;
 
   int stage = 0;
   uint32_t phase = 0;
   const uint32_t smem_base = su32(smem);
   for (int item = blockIdx.x; item < nitems; item += gridDim.x) {
-  int tm, tn, split, kt0, nkt;
-  item_coords(item, tm, tn, split);
-  item_k(split, kt0, nkt);
+  int nkt;
+  {
+    int tm_, tn_, split_, kt0_;
+    item_coords(item, tm_, tn_, split_);
+    item_k(split_, kt0_, nkt);
+  }
   double acc[MI][NI][2];
 #pragma unroll
   for (int i = 0; i < MI; ++i)
@@ -209,11 +212,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t sB = sA + kStageA;
 #pragma unroll
     for (int ks = 0; ks < 4; ++ks) {
+      const uint32_t koff = ((G ^ (uint32_t)ks) << 4) | kodd;
       double a[MI], b[NI];
 #pragma unroll
-      for (int mi = 0; mi < MI; ++mi) a[mi] = lds64(sA + a_row + mi * 1024 + koff[ks]);
+      for (int mi = 0; mi < MI; ++mi) a[mi] = lds64(sA + a_row + mi * 1024 + koff);
 #pragma unroll
-      for (int ni = 0; ni < NI; ++ni) b[ni] = lds64(sB + b_row + ni * 1024 + koff[ks]);
+      for (int ni = 0; ni < NI; ++ni) b[ni] = lds64(sB + b_row + ni * 1024 + koff);
 #pragma unroll
       for (int mi = 0; mi < MI; ++mi)
 #pragma unroll
@@ -227,7 +231,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   }
 
-  // ---------------- epilogue (C column-major)
+  // ---------------- epilogue (C column-major); the tile coordinates are recomputed here so they are not
+  // live (spilled) across the k-loop
+  int tm, tn, split;
+  item_coords(item, tm, tn, split);
   const int m0 = tm * BM + wm * (BM / 2) + g;
   const int n0 = tn * BN + wn * (BN / 4) + (lane & 3) * 2;
   if (partial) {
@@ -377,11 +384,19 @@ GemmPlan pick_gemm(int64_t M, int64_t N, int64_t K, int sms) {
 int pick_splitk(int64_t M, int64_t N, int64_t K, int sms) { return pick_gemm(M, N, K, sms).splitk; }
 
 namespace {
-// DBM_DGEMM_WAVESYNC=<k-tiles> turns on the wave barrier (0/unset = off).  Experimental: see DESIGN.md.
+// DBM_DGEMM_WAVESYNC=<k-tiles> sets the fuzzy wave barrier's interval (0/unset = off) and
+// DBM_DGEMM_WAVESLACK=<intervals> its slack (default 1).  See DESIGN.md §5.
 int wave_sync_ktiles() {
   static int v = [] {
     const char* e = getenv("DBM_DGEMM_WAVESYNC");
     return e ? std::max(0, atoi(e)) : 0;
+  }();
+  return v;
+}
+int wave_slack() {
+  static int v = [] {
+    const char* e = getenv("DBM_DGEMM_WAVESLACK");
+    return e ? std::max(0, atoi(e)) : 1;
   }();
   return v;
 }
@@ -434,11 +449,11 @@ cudaError_t launch_tile(const GemmArgs& g, int splitk, cudaStream_t st) {
     cfg.numAttrs = 1;
     return cudaLaunchKernelEx(&cfg, dgemm_tn_kernel<BM, BN>, tmA, tmB, (int)g.M, (int)g.N, ktiles,
                               std::max(per, 0), splitk, tiles_m, tiles_n, g.C, g.ldc, g.alpha, g.beta, partial, ws,
-                              sync_kt, rounds, g.b_blocks);
+                              sync_kt, rounds, wave_slack(), g.b_blocks);
   }
   dgemm_tn_kernel<BM, BN><<<grid, kThreads, T::kSmem, st>>>(tmA, tmB, (int)g.M, (int)g.N, ktiles, std::max(per, 0),
                                                             splitk, tiles_m, tiles_n, g.C, g.ldc, g.alpha, g.beta,
-                                                            partial, nullptr, 1, 0, g.b_blocks);
+                                                            partial, nullptr, 1, 0, 0, g.b_blocks);
   return cudaGetLastError();
 }
 }  // namespace

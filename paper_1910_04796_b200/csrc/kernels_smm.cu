@@ -542,14 +542,13 @@ __global__ void __launch_bounds__((s22::WARPS + 1) * 32, 1)
 // as a pinwheel of 5 x 6 / 6 x 5 rectangles around the centre subtile (30, 30, 30, 31
 // DMMAs per k-step), each rectangle split between the sub-partition's two warps (5 x 3 or 3 x 5).
 namespace s22q {
-constexpr int BS = 22, BB = 484, KK = 2, KS = 44, RUNS = 16, WARPS = 8, STAGES = 2;
+constexpr int BS = 22, BB = 484, KK = 2, KS = 44, RUNS = 16, WARPS = 8, STAGES = 3;
 constexpr int SLOT = KK * BB;                  // A slot: one block row over the stage's 2 k-blocks, [k][m]
 constexpr int BOFF = 4 * SLOT;                 // B slots follow the 4 A slots
 constexpr int SLOTB = 980;                     // B slot: [kk0 block][2 pad][kk1 block], stride = 4 (mod 16)
 constexpr int KK1B = BB + 2;                   // the kk1 block's offset inside a B slot
 constexpr int STAGE = BOFF + 4 * SLOTB;        // 7,792 doubles (a multiple of 16)
-constexpr int TP = 89;                         // pitch of the 88 x 88 C staging tile (column-major)
-constexpr size_t SMEM = (size_t)(STAGES * STAGE + 88 * TP) * 8;
+constexpr size_t SMEM = (size_t)STAGES * STAGE * 8;
 constexpr uint32_t BLK_BYTES = BB * 8;
 static_assert(SMEM + 1024 <= 232448, "shared memory");
 }  // namespace s22q
@@ -565,12 +564,44 @@ __constant__ short kQRowIdx[88] = {0, 1, 8, 9, 2, 3, 10, 11, 4, 5, 12, 13, 6, 7,
 __constant__ short kQColOff[88] = {3872, 4004, 3960, 3916, 4048, 4180, 4136, 4092, 3938, 3894, 4026, 3982, 4114, 4070, 4202, 4158, 4852, 4984, 4940, 4896, 5028, 5160, 5116, 5072, 4918, 4874, 5006, 4962, 5094, 5050, 5182, 5138, 5832, 5964, 5920, 5876, 6008, 6140, 6096, 6052, 5898, 5854, 5986, 5942, 6074, 6030, 6162, 6118, 6812, 6944, 6900, 6856, 6988, 7120, 7076, 7032, 6878, 6834, 6966, 6922, 7054, 7010, 7142, 7098, 4224, 5204, 4312, 4268, 4290, 4246, 5226, 4334, 5292, 5248, 6228, 6184, 5270, 6250, 6206, 5314, 6272, 7252, 7208, 7164, 6294, 7274, 7230, 7186};
 __constant__ short kQColIdx[88] = {0, 6, 4, 2, 8, 14, 12, 10, 3, 1, 7, 5, 11, 9, 15, 13, 22, 28, 26, 24, 30, 36, 34, 32, 25, 23, 29, 27, 33, 31, 37, 35, 44, 50, 48, 46, 52, 58, 56, 54, 47, 45, 51, 49, 55, 53, 59, 57, 66, 72, 70, 68, 74, 80, 78, 76, 69, 67, 73, 71, 77, 75, 81, 79, 16, 38, 20, 18, 19, 17, 39, 21, 42, 40, 62, 60, 41, 63, 61, 43, 64, 86, 84, 82, 65, 87, 85, 83};
 
-// One warp's rectangle of subtiles: rows [r0, r0+R), cols [c0, c0+Cn) of the 11 x 11 grid.
-template <int R, int Cn>
+// One k-step block of a stage: R x Cn subtiles (+ the centre subtile for CENTRE), fragments loaded with the
+// tail predicate only when TAIL (the last stage of an odd kb holds one k-block).
+template <int R, int Cn, bool CENTRE, bool TAIL>
+__device__ __forceinline__ void s22q_stage(uint32_t sb, int kvalid, int t, const uint32_t (&offA)[R],
+                                           const uint32_t (&offB)[Cn], uint32_t offAc, uint32_t offBc,
+                                           double (&acc)[R][Cn][2], double (&cacc)[2]) {
+  using namespace s22q;
+#pragma unroll
+  for (int ks = 0; ks < KS / 4; ++ks) {
+    const int k = 4 * ks + t;
+    const bool ok = !TAIL || k < kvalid;
+    // A slot: [k 0..43][m] at pitch 22 (the two blocks are contiguous); B slot: block k / 22 (the second
+    // at KK1B), [n][k % 22]
+    const uint32_t ka = (uint32_t)(k * BS) * 8u, kbo = (uint32_t)(k + (k >= BS ? KK1B - BS : 0)) * 8u;
+    double a[R], b[Cn];
+#pragma unroll
+    for (int i = 0; i < R; ++i) a[i] = ok ? lds64(sb + offA[i] + ka) : 0.0;
+#pragma unroll
+    for (int j = 0; j < Cn; ++j) b[j] = ok ? lds64(sb + offB[j] + kbo) : 0.0;
+#pragma unroll
+    for (int i = 0; i < R; ++i)
+#pragma unroll
+      for (int j = 0; j < Cn; ++j) dmma(acc[i][j], a[i], b[j]);
+    if (CENTRE) {
+      const double ac = ok ? lds64(sb + offAc + ka) : 0.0;
+      const double bc = ok ? lds64(sb + offBc + kbo) : 0.0;
+      dmma(cacc, ac, bc);
+    }
+  }
+}
+
+// One warp's rectangle of subtiles: rows [r0, r0+R), cols [c0, c0+Cn) of the 11 x 11 grid (+ the centre
+// subtile (5, 5) for CENTRE, a compile-time role so the k-loop carries no branch).
+template <int R, int Cn, bool CENTRE>
 __device__ __forceinline__ void s22q_consume(uint64_t* full, uint64_t* empty, uint32_t sbase, int& stage,
-                                             uint32_t& phase, int st0, int st1, int Krun, int r0, int c0,
-                                             bool centre, int g, int t, int lane, double* const (&s_dst)[4][4],
-                                             bool raw, double alpha, double beta_first, double* tile) {
+                                             uint32_t& phase, int st0, int st1, int Krun, int r0, int c0, int g,
+                                             int t, int lane, double* const (&s_dst)[4][4], bool raw, double alpha,
+                                             double beta_first) {
   using namespace s22q;
   double acc[R][Cn][2], cacc[2] = {0.0, 0.0};
 #pragma unroll
@@ -583,33 +614,15 @@ __device__ __forceinline__ void s22q_consume(uint64_t* full, uint64_t* empty, ui
 #pragma unroll
   for (int j = 0; j < Cn; ++j) offB[j] = (uint32_t)kQColOff[(c0 + j) * 8 + g] * 8u;
   const uint32_t offAc = (uint32_t)kQRowOff[40 + g] * 8u, offBc = (uint32_t)kQColOff[40 + g] * 8u;
+  // every stage but (possibly) the last holds 44 valid k
+  const int full_end = min(st1, Krun / KS);
   for (int st = st0; st < st1; ++st) {
     mbar_wait((uint32_t)__cvta_generic_to_shared(&full[stage]), phase);
     const uint32_t sb = sbase + (uint32_t)(stage * STAGE) * 8u;
-    const int kvalid = Krun - st * KS;
-    const bool tail = kvalid < KS;
-#pragma unroll
-    for (int ks = 0; ks < KS / 4; ++ks) {
-      const int k = 4 * ks + t;
-      const bool ok = !tail || k < kvalid;
-      // A slot: [k 0..43][m] at pitch 22 (the two blocks are contiguous); B slot: block k / 22 (the second
-      // at KK1B), [n][k % 22]
-      const uint32_t ka = (uint32_t)(k * BS) * 8u, kbo = (uint32_t)(k + (k >= BS ? KK1B - BS : 0)) * 8u;
-      double a[R], b[Cn];
-#pragma unroll
-      for (int i = 0; i < R; ++i) a[i] = ok ? lds64(sb + offA[i] + ka) : 0.0;
-#pragma unroll
-      for (int j = 0; j < Cn; ++j) b[j] = ok ? lds64(sb + offB[j] + kbo) : 0.0;
-#pragma unroll
-      for (int i = 0; i < R; ++i)
-#pragma unroll
-        for (int j = 0; j < Cn; ++j) dmma(acc[i][j], a[i], b[j]);
-      if (centre) {
-        const double ac = ok ? lds64(sb + offAc + ka) : 0.0;
-        const double bc = ok ? lds64(sb + offBc + kbo) : 0.0;
-        dmma(cacc, ac, bc);
-      }
-    }
+    if (st < full_end)
+      s22q_stage<R, Cn, CENTRE, false>(sb, KS, t, offA, offB, offAc, offBc, acc, cacc);
+    else
+      s22q_stage<R, Cn, CENTRE, true>(sb, Krun - st * KS, t, offA, offB, offAc, offBc, acc, cacc);
     __syncwarp();
     if (lane == 0) mbar_arrive((uint32_t)__cvta_generic_to_shared(&empty[stage]));
     if (++stage == STAGES) {
@@ -617,41 +630,30 @@ __device__ __forceinline__ void s22q_consume(uint64_t* full, uint64_t* empty, ui
       phase ^= 1;
     }
   }
-  // epilogue: subtile (i, j), lane (g, t) holds C(M = 8 (r0 + i) + g, N = 8 (c0 + j) + 2t + jj).  The warp
-  // stages its rectangle in the shared 88 x 88 tile (immediate offsets, no per-element address math while
-  // the accumulators are live), then writes it back block by block.
+  // epilogue straight from the accumulators: subtile (i, j), lane (g, t) holds the element at row
+  // M = kQRowIdx[8 (r0 + i) + g], column N = kQColIdx[8 (c0 + j) + 2t + jj] of the 88 x 88 square,
+  // i.e. element (M mod 22, N mod 22) of C block (M / 22, N / 22) (once per square: off the hot loop)
+  auto put = [&](int M, int N, double v) {
+    const int ri = M / BS, cj = N / BS;
+    double* p = s_dst[ri][cj] + (M - ri * BS) + (N - cj * BS) * BS;
+    if (raw) {
+      *p = v;
+    } else {
+      const double w = alpha * v;
+      *p = (beta_first == 0.0) ? w : beta_first * *p + w;
+    }
+  };
 #pragma unroll
   for (int i = 0; i < R; ++i) {
     const int M = kQRowIdx[(r0 + i) * 8 + g];
 #pragma unroll
     for (int j = 0; j < Cn; ++j)
 #pragma unroll
-      for (int jj = 0; jj < 2; ++jj) tile[M + kQColIdx[(c0 + j) * 8 + 2 * t + jj] * TP] = acc[i][j][jj];
+      for (int jj = 0; jj < 2; ++jj) put(M, kQColIdx[(c0 + j) * 8 + 2 * t + jj], acc[i][j][jj]);
   }
-  if (centre)
+  if (CENTRE)
 #pragma unroll
-    for (int jj = 0; jj < 2; ++jj) tile[kQRowIdx[40 + g] + kQColIdx[40 + 2 * t + jj] * TP] = cacc[jj];
-  __syncwarp();
-  // subtile rows [sr0, sr0+nr) x subtile cols [sc0, sc0+nc), through the permutations
-  auto writeback = [&](int sr0, int nr, int sc0, int nc) {
-    const int Mn = nr * 8, Nn = nc * 8;
-#pragma unroll 1
-    for (int e = lane; e < Mn * Nn; e += 32) {
-      const int M = kQRowIdx[sr0 * 8 + e % Mn], N = kQColIdx[sc0 * 8 + e / Mn];
-      const int ri = M / BS, cj = N / BS;
-      double* p = s_dst[ri][cj] + (M - ri * BS) + (N - cj * BS) * BS;
-      const double v = tile[M + N * TP];
-      if (raw) {
-        *p = v;
-      } else {
-        const double w = alpha * v;
-        *p = (beta_first == 0.0) ? w : beta_first * *p + w;
-      }
-    }
-  };
-  writeback(r0, R, c0, Cn);
-  if (centre) writeback(5, 1, 5, 1);
-  __syncwarp();
+    for (int jj = 0; jj < 2; ++jj) put(kQRowIdx[40 + g], kQColIdx[40 + 2 * t + jj], cacc[jj]);
 }
 
 __global__ void __launch_bounds__((s22q::WARPS + 1) * 32, 1)
@@ -665,7 +667,7 @@ __global__ void __launch_bounds__((s22q::WARPS + 1) * 32, 1)
   extern __shared__ __align__(128) double smem[];
   __shared__ __align__(8) uint64_t full[STAGES], empty[STAGES];
   __shared__ int s_rowrep[4], s_colrep[4];
-  __shared__ double* s_dst[4][4];
+  __shared__ double* s_dst[2][4][4];  // per item parity: the C (or split-K partial) block of square cell (ri, cj)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const bool producer = warp == WARPS;
@@ -674,6 +676,12 @@ __global__ void __launch_bounds__((s22q::WARPS + 1) * 32, 1)
   const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(smem);
   const int64_t ngroups = nruns / RUNS;  // the host launches this kernel only on whole squares
   const int g = lane >> 2, t = lane & 3;
+  // Items of >= STAGES + 1 stages need no CTA barrier between them: the consumers read the item's
+  // destination pointers (s_dst, double-buffered by item parity) after waiting on one of its full
+  // barriers, and the producer cannot reach item i + 2 before the consumers finished item i (it waits
+  // for the release of item i + 1's own stages).  Shorter items (kb < 8, small multiplies) keep the
+  // barriers.  (The host never splits K below 64 stages, so every item has >= 1 stage.)
+  const bool sync_items = nst / nsplit < STAGES + 1;
 
   // pinwheel of the 11 x 11 subtiles around the centre (5, 5): warp 0 rows 0-4 x cols 0-5 (+ centre),
   // warp 1 rows 0-5 x cols 6-10, warp 2 rows 6-10 x cols 5-10, warp 3 rows 5-10 x cols 0-4
@@ -695,7 +703,8 @@ __global__ void __launch_bounds__((s22q::WARPS + 1) * 32, 1)
 
   int stage = 0;
   uint32_t phase = 0;
-  for (int64_t item = blockIdx.x; item < ngroups * nsplit; item += gridDim.x) {
+  int par = 0;
+  for (int64_t item = blockIdx.x; item < ngroups * nsplit; item += gridDim.x, par ^= 1) {
     const int64_t grp = item % ngroups;
     const int split = (int)(item / ngroups);
     const int st0 = (int)((int64_t)nst * split / nsplit), st1 = (int)((int64_t)nst * (split + 1) / nsplit);
@@ -716,12 +725,14 @@ __global__ void __launch_bounds__((s22q::WARPS + 1) * 32, 1)
         cj += (firstb && bo < b0) ? 1 : 0;
       }
       if (lane < 16) {
-        s_dst[ri][cj] = partial ? partial + ((int64_t)split * nruns + q) * BB : C + (int64_t)trip[3 * (q * kb) + 2] * BB;
+        s_dst[par][ri][cj] =
+            partial ? partial + ((int64_t)split * nruns + q) * BB : C + (int64_t)trip[3 * (q * kb) + 2] * BB;
         if (cj == 0) s_rowrep[ri] = lane;
         if (ri == 0) s_colrep[cj] = lane;
       }
+      __syncwarp();  // s_rowrep / s_colrep are read by the producer lanes; s_dst is released by the full barrier
     }
-    __syncthreads();
+    if (sync_items) __syncthreads();
     if (producer) {
       // lane l < 16: l < 8 -> A row l / 2, block kk0 + (l & 1); else B column (l - 8) / 2
       const int isb = lane >= 8 ? 1 : 0, u = (lane & 7) >> 1, j = lane & 1;
@@ -746,14 +757,17 @@ __global__ void __launch_bounds__((s22q::WARPS + 1) * 32, 1)
           phase ^= 1;
         }
       }
+    } else if (centre) {
+      s22q_consume<5, 3, true>(full, empty, sbase, stage, phase, st0, st1, Krun, r0, c0, g, t, lane, s_dst[par],
+                               partial != nullptr, alpha, beta_first);
     } else if (tall) {
-      s22q_consume<5, 3>(full, empty, sbase, stage, phase, st0, st1, Krun, r0, c0, centre, g, t, lane, s_dst,
-                         partial != nullptr, alpha, beta_first, smem + STAGES * STAGE);
+      s22q_consume<5, 3, false>(full, empty, sbase, stage, phase, st0, st1, Krun, r0, c0, g, t, lane, s_dst[par],
+                                partial != nullptr, alpha, beta_first);
     } else {
-      s22q_consume<3, 5>(full, empty, sbase, stage, phase, st0, st1, Krun, r0, c0, centre, g, t, lane, s_dst,
-                         partial != nullptr, alpha, beta_first, smem + STAGES * STAGE);
+      s22q_consume<3, 5, false>(full, empty, sbase, stage, phase, st0, st1, Krun, r0, c0, g, t, lane, s_dst[par],
+                                partial != nullptr, alpha, beta_first);
     }
-    __syncthreads();
+    if (sync_items) __syncthreads();
   }
 }
 

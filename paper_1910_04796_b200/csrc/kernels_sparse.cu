@@ -402,7 +402,8 @@ __global__ void __launch_bounds__(SpRunCfg<BS>::WARPS * 32, 1)
         asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa + 8u * d), "l"(a + 2 * c) : "memory");
         asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sb + 8u * d), "l"(b + 2 * c) : "memory");
       } else {
-        const int pa = trip[3 * entry] & 1, pb = trip[3 * entry + 1] & 1;  // 1: block starts 8 mod 16
+        // 1: block starts 8 mod 16 (from the address: a chunked panel base A + k0 bs^2 may itself be 8 mod 16)
+        const int pa = (int)(((uintptr_t)a >> 3) & 1), pb = (int)(((uintptr_t)b >> 3) & 1);
         if (c < CH - 1) {  // elements pa + 2c, pa + 2c + 1 -> shared doubles 2 pa + 2c (16-byte aligned)
           asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa + 16u * (pa + c)), "l"(a + pa + 2 * c)
                        : "memory");

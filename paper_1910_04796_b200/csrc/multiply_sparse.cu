@@ -93,7 +93,7 @@ void own_layout(dbm_ctx ctx, dbm_matrix A, dbm_matrix B, int L, int r, int c, st
   b_nnz.assign(L, -1);
   a_off.assign(L, SIZE_MAX);
   b_off.assign(L, SIZE_MAX);
-  size_t off = 0;
+  size_t off = xhdr_bytes(ctx->nranks, L);  // several ranks: the signal header comes first
   if (ctx->nranks > 1) {
     for (int k = 0; k < L; ++k)
       if (k % ctx->pc == c) {
@@ -356,6 +356,7 @@ dbm_status multiply_sparse_blocked(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_
   }
   std::vector<cudaEvent_t> ev_x(L, nullptr), ev_g(L, nullptr);
   cudaEvent_t ev_ready = nullptr;
+  uint64_t ep = 0;  // this multiply's epoch (signals between ranks)
   std::vector<int> bufA(L, -1), bufB(L, -1);
   auto pulls = [&](int s) -> dbm_status {
     const SpStep& x = sc->steps[s];
@@ -392,7 +393,11 @@ dbm_status multiply_sparse_blocked(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_
     ev_ready = get_event(ctx);
     CUDA_TRY(ctx, cudaEventRecord(ev_ready, cs));
     CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->comm, ev_ready, 0));
-    if (dbm_status e = ipc_exchange(ctx, ws)) return e;  // = barrier: every rank's panels are packed
+    // my packed panels are ready (signal behind the packs) -> wait for every peer's (device-side)
+    if (dbm_status e = xattach(ctx, ws, cs)) return e;
+    ep = ++ctx->epoch;
+    if (dbm_status e = xsignal(ctx, cs, X_READY, ep)) return e;
+    if (dbm_status e = xwait(ctx, ctx->comm, X_READY, ep)) return e;
     if (dbm_status e = pulls(0)) return e;
     CUDA_TRY(ctx, cudaEventRecord(ev_x[0], ctx->comm));
   }
@@ -443,8 +448,9 @@ dbm_status multiply_sparse_blocked(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_
   st.stacks = sp_stacks(sc, cap);
   if (ctx->nranks > 1) {
     CUDA_TRY(ctx, cudaStreamWaitEvent(cs, ev_x[L - 1], 0));
-    int* w = ctx->d_scratch;
-    NCCL_TRY(ctx, ncclAllReduce(w, w, 1, ncclInt, ncclSum, (ncclComm_t)ctx->nccl, cs));
+    // closing barrier: "done" behind my last pull, then wait for every peer's (no peer reads my panels)
+    if (dbm_status e = xsignal(ctx, ctx->comm, X_DONE, ep)) return e;
+    if (dbm_status e = xwait(ctx, cs, X_DONE, ep)) return e;
     cudaEvent_t done = get_event(ctx);
     CUDA_TRY(ctx, cudaEventRecord(done, cs));
     ctx->ev_pool.push_back(ev_ready);

@@ -61,7 +61,7 @@ TSPlan make_ts_plan(int pr, int pc, int r, int c, int64_t Mb, int64_t Nb, int64_
   }
   t.Mtot = Mb * bs;
   t.Ntot = Nb * bs;
-  size_t off = 0;
+  size_t off = xhdr_bytes(pr * pc, (int)lcm64(pr, pc));  // the signal header comes first
   auto take = [&](size_t bytes) {
     size_t o = off;
     off = align256(off + bytes);
@@ -150,7 +150,11 @@ dbm_status multiply_tallskinny(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_matr
   cudaEvent_t ev_ready = get_event(ctx);
   CUDA_TRY(ctx, cudaEventRecord(ev_ready, cs));
   CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->comm, ev_ready, 0));
-  if (dbm_status e = ipc_exchange(ctx, ws)) return e;  // all-gather = "every piece is ready" barrier
+  // "my pieces are ready" (behind the densifies) -> the gathers wait for every peer's (device-side)
+  if (dbm_status e = xattach(ctx, ws, cs)) return e;
+  const uint64_t ep = ++ctx->epoch;
+  if (dbm_status e = xsignal(ctx, cs, X_READY, ep)) return e;
+  if (dbm_status e = xwait(ctx, ctx->comm, X_READY, ep)) return e;
   std::vector<TSPlan> peer(P);
   for (int q = 0; q < P; ++q)
     if (q != t.me) peer[q] = make_ts_plan(t.pr, t.pc, q / t.pc, q % t.pc, t.Mb, t.Nb, t.Kb, bs);
@@ -212,9 +216,10 @@ dbm_status multiply_tallskinny(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_matr
   st->entries += 1;  // the densified batch holds one multiplication
   st->stacks += 1;
   st->flops += 2.0 * t.Mtot * t.Ntot * kb * bs;
-  // ---- reduction: every partial is complete after this barrier; pull my C share out of each
-  int* w = ctx->d_scratch;
-  NCCL_TRY(ctx, ncclAllReduce(w, w, 1, ncclInt, ncclSum, (ncclComm_t)ctx->nccl, cs));
+  // ---- reduction: every partial is complete after this barrier; pull my C share out of each.  My gathers
+  // are finished too (the last GEMM chunk waited for them): "done" goes out with "mid".
+  if (dbm_status e = xsignal(ctx, cs, X_MID, ep)) return e;
+  if (dbm_status e = xwait(ctx, cs, X_MID, ep)) return e;
   const int64_t mr = t.mrows[t.r], nc = t.ncols[t.c];
   double* cstack = (double*)(ws + t.off_cstack);
   for (int q = 0; q < P && mr * nc > 0; ++q) {
@@ -230,7 +235,8 @@ dbm_status multiply_tallskinny(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_matr
     CUDA_TRY(ctx, cudaGetLastError());
   }
   // closing barrier: no peer still reads my pieces or my partial
-  NCCL_TRY(ctx, ncclAllReduce(w, w, 1, ncclInt, ncclSum, (ncclComm_t)ctx->nccl, cs));
+  if (dbm_status e = xsignal(ctx, cs, X_DONE, ep)) return e;
+  if (dbm_status e = xwait(ctx, cs, X_DONE, ep)) return e;
   ts_bytes(t, &st->bytes_recv, &st->bytes_sent);
   st->steps = 1;
   ctx->ev_pool.push_back(ev_ready);

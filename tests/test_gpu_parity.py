@@ -252,6 +252,19 @@ def test_multiply_integer_bit_exact(dbm, ctx, orc, path):
     assert np.array_equal(got, ref)
 
 
+@pytest.mark.parametrize("nb,kb", [(8, 1), (8, 2), (8, 3), (8, 5), (8, 6), (8, 7), (8, 8), (8, 9), (8, 17),
+                                   (64, 9), (64, 6), (32, 40)])
+@pytest.mark.parametrize("beta", [0.0, -1.25])
+def test_smm22q_item_lengths(dbm, ctx, orc, nb, kb, beta):
+    """The 4 x 4-square bs-22 kernel over every item regime: 1..9 stages of 2 k-blocks (items shorter
+    than STAGES + 1 keep the CTA barriers, longer ones run with double-buffered destinations), odd kb
+    (a predicated half stage at the end), and 256 squares (several items per CTA).  Integer inputs: exact."""
+    n = nb * 22
+    got, ref, st = run_multiply(dbm, ctx, orc, n, n, kb * 22, 22, "blocked", 0.75, beta, kind=1)
+    assert np.array_equal(got, ref)
+    assert st["entries"] == nb * nb * kb
+
+
 @pytest.mark.parametrize("bs", [4, 5, 6, 7, 8, 9, 13, 16, 23, 26, 32])
 def test_blocked_small_block_sizes(dbm, ctx, orc, bs):
     """The per-size DMMA run kernels (bs 4..32 except 22 / 64; bs 7 stays on the FMA kernel) on uniform runs:

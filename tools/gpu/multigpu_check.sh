@@ -1,0 +1,26 @@
+#!/bin/bash
+# Multi-rank validation on the GPUs of one box (2 or 4): the host-pipeline cases first (they hung in
+# round 1), then the whole mp_worker parity suite with its JSON summary, then bench lines.  Each command
+# runs under its own timeout; results land in gpurun_out/mg_<n>gpu_*.
+set -u
+cd "$(dirname "$0")/../.."
+mkdir -p gpurun_out
+N=$(nvidia-smi -L | wc -l)
+OUT=gpurun_out/mg_${N}gpu.txt
+: > $OUT
+TR="python -m torch.distributed.run --nnodes=1 --nproc-per-node=$N --master-addr=127.0.0.1"
+run() {  # name seconds cmd...
+  local name=$1 to=$2; shift 2
+  local t0=$(date +%s)
+  timeout -k 10 $to "$@" > gpurun_out/mg_${N}gpu_$name.log 2>&1
+  local rc=$?
+  echo "$name rc=$rc secs=$(( $(date +%s) - t0 ))" | tee -a $OUT
+}
+run bench_s352 150 $TR --master-port=29611 bench.py --gpus $N --config s352 --steps 3 --warmup 3
+run mp_host 600 env DBM_CASE_TIMEOUT=60 $TR --master-port=29612 tests/mp_worker.py --groups host,sweep \
+    --summary gpurun_out/mg_${N}gpu_host_summary.json
+run mp_all 1500 env DBM_CASE_TIMEOUT=120 $TR --master-port=29613 tests/mp_worker.py --groups cannon,sparse,host \
+    --summary gpurun_out/mg_${N}gpu_all_summary.json
+for cfg in ${BENCH_CFGS:-sq64}; do
+  run bench_$cfg 900 $TR --master-port=29614 bench.py --gpus $N --config $cfg --steps 3 --warmup 3
+done

@@ -68,7 +68,36 @@ def parse():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--e2e-steps", type=int, default=1)
+    p.add_argument("--timeline", default="", help="write one profiled multiply's per-rank timeline "
+                   "(kernels on every stream and the Cannon pulls, CUDA events) to <path>.rank<r>.json")
     return p.parse_args()
+
+
+# ------------------------------------------------------------------ NVLink byte counters (NVML)
+def nvlink_bytes(device: int):
+    """(rx, tx) bytes this GPU moved over NVLink so far (NVML field counters summed over the links), or
+    None.  Sampled around the timed region: the Cannon pulls are copy-engine transfers, which ncu's
+    kernel replay cannot attribute, so the device's own link counters are the evidence."""
+    try:
+        import pynvml
+
+        pynvml.nvmlInit()
+        h = pynvml.nvmlDeviceGetHandleByIndex(device)
+        for rx_id, tx_id, unit in ((pynvml.NVML_FI_DEV_NVLINK_COUNT_RCV_BYTES, pynvml.NVML_FI_DEV_NVLINK_COUNT_XMIT_BYTES, 1),
+                                   (pynvml.NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_RX,
+                                    pynvml.NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_TX, 1024)):
+            tot, ok = [0, 0], False
+            for link in range(18):  # NVLink 5 on B200: 18 links
+                vals = pynvml.nvmlDeviceGetFieldValues(h, [(rx_id, link), (tx_id, link)])
+                for i, v in enumerate(vals):
+                    if v.nvmlReturn == 0:
+                        tot[i] += int(v.value.ullVal) * unit
+                        ok = True
+            if ok:
+                return tot[0], tot[1]
+    except Exception:
+        return None
+    return None
 
 
 # ------------------------------------------------------------------ clocks during the timed region
@@ -265,11 +294,13 @@ def main():
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
         barrier()
+        nvl0 = nvlink_bytes(local) if world > 1 else None
         ev0.record(stream)
         for _ in range(args.steps):
             st = dbm.multiply(ctx, alpha, A, B, beta, C, path, workspace=ws)
         ev1.record(stream)
         barrier()
+        nvl1 = nvlink_bytes(local) if world > 1 else None
     ctx.set_profiling(False)
     launches = ctx.launch_count() - launches0
     ms = maxrank(ev0.elapsed_time(ev1)) / args.steps
@@ -294,6 +325,19 @@ def main():
     tfile = os.path.join(ROOT, "profiles", f"traffic_{args.config}_{path}_n{world}.json")
     if os.path.exists(tfile):
         traffic = json.load(open(tfile)).get("bytes_per_launch")
+
+    if args.timeline:  # one more multiply with every record kept: the overlap of pulls and GEMMs
+        ctx.set_profiling(True)
+        dbm.multiply(ctx, alpha, A, B, beta, C, path, workspace=ws)
+        ctx.sync()
+        names = {dbm.K_DGEMM: "dgemm", dbm.K_SMM: "smm", dbm.K_DENSIFY: "densify", dbm.K_UNDENSIFY: "undensify",
+                 dbm.K_STACKGEN: "stackgen", dbm.K_EXCHANGE: "pull"}
+        tl = [{"kind": names.get(k, k), "start_ms": a, "end_ms": b} for k, a, b in ctx.profile_timeline()]
+        ctx.set_profiling(False)
+        for k in names:
+            ctx.profile_read(k)  # drop the records
+        with open(f"{args.timeline}.rank{rank}.json", "w") as fh:
+            json.dump({"rank": rank, "grid": f"{ctx.pr}x{ctx.pc}", "config": name, "records": tl}, fh, indent=0)
 
     # ---------------- end to end through the public API with host buffers (pinned), rank-local shares
     e2e = None
@@ -344,6 +388,14 @@ def main():
                           "gbs": prof_x["bytes"] / (prof_x["ms"] * 1e-3) / 1e9 if prof_x["ms"] > 0 else None,
                           "uncovered_ms_per_step": ms - (prof["ms"] + prof_d["ms"] + prof_u["ms"] + prof_s["ms"])
                           / args.steps} if world > 1 else None),
+            # NVML link counters of rank 0's GPU over the timed region vs the pulls' algorithmic bytes
+            "nvlink": ({"rx_bytes_per_step": (nvl1[0] - nvl0[0]) / args.steps,
+                        "tx_bytes_per_step": (nvl1[1] - nvl0[1]) / args.steps,
+                        "algorithmic_recv_bytes_per_step": st["bytes_recv"],
+                        "algorithmic_sent_bytes_per_step": st["bytes_sent"],
+                        "rx_gbs_over_step": (nvl1[0] - nvl0[0]) / args.steps / (ms * 1e-3) / 1e9,
+                        "source": "NVML field counters (NVLINK_COUNT_RCV/XMIT_BYTES, all links)"}
+                       if (nvl0 and nvl1) else None),
             "gpu_launches": launches,
             "clocks": clk.summary(),
             "e2e": e2e,

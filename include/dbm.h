@@ -109,6 +109,12 @@ dbm_status dbm_ctx_sync(dbm_ctx ctx);
 dbm_status dbm_ctx_set_profiling(dbm_ctx ctx, int on);
 dbm_status dbm_ctx_profile_read(dbm_ctx ctx, int kernel, double* ms_out, int64_t* launches_out, double* flops_out,
                                 double* bytes_out);
+/* Timeline of the pending profiling records (not consumed): for record i (enqueue order, at most
+ * max_records) out[3i] = kind (as dbm_ctx_profile_read), out[3i+1] / out[3i+2] = start / end in ms
+ * relative to the first record's start (CUDA events, so records on the compute, comm and upload
+ * streams share one clock: the overlap of the Cannon pulls with the GEMMs is read off directly).
+ * *n_out = number of pending records.  Synchronises on the records. */
+dbm_status dbm_ctx_profile_timeline(dbm_ctx ctx, int max_records, double* out, int* n_out);
 /* Cannon panel transport between ranks ("asynchronous point-to-point"):
  * 0 (default) = DMA copy engines pull each needed panel from its owner's workspace, mapped with CUDA
  *     IPC, over NVLink (no SM is taken from the local multiply); ordering uses two tiny NCCL

@@ -103,7 +103,7 @@ void launch_scale(double* x, int64_t n, double beta, cudaStream_t st);  // x = b
 dbm_status ipc_exchange(dbm_ctx ctx, void* ws);
 
 // ---- device-side signals between ranks (copy-engine transport)
-// Every rank's registered workspace starts with a header of int64 words its peers write into through
+// Every rank's exchange pool starts with a header of int64 words its peers write into through
 // the IPC mappings: word (kind * P + q) holds the last epoch for which peer q announced `kind`, then the
 // host pipeline's progress table [peer][operand][kappa] = (epoch << 32) | K-blocks in place.  Values
 // only grow (epochs count the copy-engine multiplies, identical on every rank), so no table is ever
@@ -115,9 +115,11 @@ size_t xhdr_bytes(int nranks, int L);           // header bytes at the start of 
 inline size_t xprog_word(int P, int L, int peer, int operand, int kappa) {
   return (size_t)X_KINDS * P + ((size_t)peer * 2 + operand) * L + kappa;
 }
-// Make `ws` this rank's registered workspace (collective when it changes: zero the header, all-gather
-// the IPC handles).  Fast path (ws already registered): nothing.
-dbm_status xattach(dbm_ctx ctx, char* ws, cudaStream_t cs);
+// Make the context's exchange pool (library-owned: signal header + the own panels / pieces peers pull)
+// hold at least `need` bytes, `need` being the maximum over all ranks.  Growing is collective by
+// construction (every rank sees the same need): a new cudaMalloc allocation, its header zeroed, the
+// IPC handles all-gathered (the only host synchronisation, once per growth).  Otherwise: nothing.
+dbm_status xattach(dbm_ctx ctx, size_t need, cudaStream_t cs);
 // Write `value` into word (kind, me) of every peer's header / wait on stream st until word (kind, q) of
 // my header holds >= value for every peer q.
 dbm_status xsignal(dbm_ctx ctx, cudaStream_t st, int kind, uint64_t value);

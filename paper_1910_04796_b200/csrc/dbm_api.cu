@@ -202,6 +202,24 @@ extern "C" dbm_status dbm_ctx_profile_read(dbm_ctx ctx, int kernel, double* ms_o
   return DBM_OK;
 }
 
+extern "C" dbm_status dbm_ctx_profile_timeline(dbm_ctx ctx, int max_records, double* out, int* n_out) {
+  CTX_OK(ctx);
+  ARG_CHECK(n_out && max_records >= 0 && (out || max_records == 0), DBM_ERR_ARG, "bad timeline buffer");
+  const int n = (int)std::min<size_t>(ctx->prof.size(), (size_t)max_records);
+  for (int i = 0; i < n; ++i) {
+    const auto& r = ctx->prof[i];
+    CUDA_TRY(ctx, cudaEventSynchronize(r.b));
+    float t0 = 0, t1 = 0;
+    CUDA_TRY(ctx, cudaEventElapsedTime(&t0, ctx->prof[0].a, r.a));
+    CUDA_TRY(ctx, cudaEventElapsedTime(&t1, ctx->prof[0].a, r.b));
+    out[3 * i] = r.kind;
+    out[3 * i + 1] = t0;
+    out[3 * i + 2] = t1;
+  }
+  *n_out = (int)ctx->prof.size();
+  return DBM_OK;
+}
+
 extern "C" dbm_status dbm_ctx_set_transport(dbm_ctx ctx, int transport) {
   ARG_CHECK(ctx && (transport == 0 || transport == 1), DBM_ERR_ARG, "transport must be 0 (copy engine) or 1 (NCCL)");
   ctx->transport = transport;
@@ -251,9 +269,11 @@ extern "C" dbm_status dbm_ctx_destroy(dbm_ctx ctx) {
   for (void* b : ctx->peer_bases)
     if (b) cudaIpcCloseMemHandle(b);
   if (ctx->d_scratch) cudaFree(ctx->d_scratch);
+  if (ctx->xpool) cudaFree(ctx->xpool);
   if (ctx->nccl) ncclCommDestroy((ncclComm_t)ctx->nccl);
   cudaStreamDestroy(ctx->comm);
   if (ctx->up) cudaStreamDestroy(ctx->up);
+  if (ctx->gen) cudaStreamDestroy(ctx->gen);
   if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
   delete ctx;
   return DBM_OK;
@@ -626,6 +646,7 @@ struct Plan {
   // workspace regions (byte offsets)
   size_t off_cd = 0, off_ownA = 0, off_ownB = 0, off_recvA[2] = {0, 0}, off_recvB[2] = {0, 0}, off_part = 0;
   size_t off_trav = 0, off_trip = 0, off_spart = 0;  // smm split-K partials
+  size_t off_trip2 = 0;                               // second triplet buffer (0: one chunk per step)
   bool mixed = false;                                 // bs 22 squares inside a non-square traversal
   // densified bs 64 with a dense B: B is never densified -- the GEMM reads B's 64 x 64 blocks in place
   // (arena, or packed panels the peers pull), through a 4-D TMA view (§8f-3, zero-copy B)
@@ -635,7 +656,8 @@ struct Plan {
   int64_t spart_runs = 0;                            // capacity: (split x runs) C blocks
   std::vector<size_t> ownA_off, ownB_off;  // per kappa, SIZE_MAX if not owned
   int64_t trip_cap = 0;                     // entries per stack-generation chunk
-  size_t total = 0;
+  size_t total = 0;       // caller-owned workspace bytes
+  size_t pool_total = 0;  // several ranks: exchange-pool bytes (signal header + own panels peers pull)
   int max_split = 1;
 
   int kappa(int s) const { return (r + c + s) % L; }
@@ -676,10 +698,17 @@ Plan make_plan_raw(int nranks, int pr, int pc, int r, int c, int64_t Mb, int64_t
   p.densified = densified;
   p.kb.resize(p.L);
   for (int k = 0; k < p.L; ++k) p.kb[k] = local_count(p.Kb, p.L, k);
-  size_t off = xhdr_bytes(nranks, p.L);  // several ranks: the signal header comes first
+  size_t off = 0;
   auto take = [&](size_t bytes) {
     size_t o = off;
     off = align256(off + bytes);
+    return o;
+  };
+  // own panels (what the peers pull) live in the library's exchange pool, after the signal header
+  size_t poff = xhdr_bytes(nranks, p.L);
+  auto take_pool = [&](size_t bytes) {
+    size_t o = poff;
+    poff = align256(poff + bytes);
     return o;
   };
   const int64_t M = p.mloc * p.bs, N = p.nloc * p.bs;
@@ -699,8 +728,8 @@ Plan make_plan_raw(int nranks, int pr, int pc, int r, int c, int64_t Mb, int64_t
       p.max_split = pick_splitk(M, N, std::min<int64_t>(ck, std::max<int64_t>(p.Kb, 1)) * p.bs, num_sms());
     } else {
       for (int k = 0; k < p.L; ++k) {
-        if (k % p.pc == p.c) p.ownA_off[k] = take(p.a_panel_bytes(k));
-        if (k % p.pr == p.r) p.ownB_off[k] = take(p.b_panel_bytes(k));
+        if (k % p.pc == p.c) p.ownA_off[k] = take_pool(p.a_panel_bytes(k));
+        if (k % p.pr == p.r) p.ownB_off[k] = take_pool(p.b_panel_bytes(k));
       }
       for (int s = 0; s < p.L; ++s) {
         p.max_split = std::max(p.max_split, pick_splitk(M, N, p.kb[p.kappa(s)] * p.bs, num_sms()));
@@ -720,8 +749,8 @@ Plan make_plan_raw(int nranks, int pr, int pc, int r, int c, int64_t Mb, int64_t
     // copy-engine transport (peers pull from this rank's workspace, the IPC-mapped allocation)
     const bool all = nranks > 1 && transport == 0;
     for (int k = 0; k < p.L; ++k) {
-      if (k % p.pc == p.c && (all || p.L / p.pc > 1)) p.ownA_off[k] = take(p.a_panel_bytes(k));
-      if (k % p.pr == p.r && (all || p.L / p.pr > 1)) p.ownB_off[k] = take(p.b_panel_bytes(k));
+      if (k % p.pc == p.c && (all || p.L / p.pc > 1)) p.ownA_off[k] = take_pool(p.a_panel_bytes(k));
+      if (k % p.pr == p.r && (all || p.L / p.pr > 1)) p.ownB_off[k] = take_pool(p.b_panel_bytes(k));
     }
     p.off_trav = take((size_t)std::max<int64_t>(p.mloc * p.nloc, 1) * 8);
     int64_t maxkb = 1;
@@ -731,6 +760,9 @@ Plan make_plan_raw(int nranks, int pr, int pc, int r, int c, int64_t Mb, int64_t
     const int64_t runs = std::max<int64_t>(16, kTripChunkEntries / maxkb / 16 * 16);
     p.trip_cap = std::min<int64_t>(runs, round_up(std::max<int64_t>(p.mloc * p.nloc, 1), 16)) * maxkb;
     p.off_trip = take((size_t)p.trip_cap * 12);
+    // several stack chunks per step: a second triplet buffer, so chunk c+1 is generated (side stream)
+    // while chunk c multiplies
+    if (runs < round_up(std::max<int64_t>(p.mloc * p.nloc, 1), 16)) p.off_trip2 = take((size_t)p.trip_cap * 12);
     // split-K partials of the smm kernel (rectangular shapes with few, long runs)
     const int64_t chunk_runs = std::max<int64_t>(1, std::min<int64_t>(p.mloc * p.nloc, p.trip_cap / maxkb));
     int64_t max_split = 1;
@@ -773,6 +805,7 @@ Plan make_plan_raw(int nranks, int pr, int pc, int r, int c, int64_t Mb, int64_t
     for (int i = 0; i < std::min(nB, 2); ++i) p.off_recvB[i] = take(bmax);
   }
   p.total = std::max<size_t>(off, 256);
+  p.pool_total = nranks > 1 ? poff : 0;
   return p;
 }
 
@@ -933,7 +966,7 @@ dbm_status post_exchange(dbm_ctx ctx, const Plan& p, int s, char* ws, const doub
     const size_t n = (size_t)op.bytes;
     if (op.send) {
       const size_t own = op.operand == 0 ? p.ownA_off[op.kappa] : p.ownB_off[op.kappa];
-      const void* src = own != SIZE_MAX ? (const void*)(ws + own) : (const void*)(op.operand == 0 ? Aarena : Barena);
+      const void* src = own != SIZE_MAX ? (const void*)(ctx->xpool + own) : (const void*)(op.operand == 0 ? Aarena : Barena);
       if (n) NCCL_TRY(ctx, ncclSend(src, n / 8, ncclDouble, op.peer, comm, ctx->comm));
       *sent += (int64_t)n;
     } else {
@@ -1059,17 +1092,31 @@ size_t dbm::xhdr_bytes(int nranks, int L) {
   return align256((size_t)8 * nranks * (X_KINDS + 2 * (size_t)L));
 }
 
-dbm_status dbm::xattach(dbm_ctx ctx, char* ws, cudaStream_t cs) {
+dbm_status dbm::xattach(dbm_ctx ctx, size_t need, cudaStream_t cs) {
   ARG_CHECK(memops(ctx->device).ok, DBM_ERR_CUDA, "64-bit stream memory operations unavailable");
-  if (ws == (char*)ctx->ipc_ws && (int)ctx->peer_ws.size() == ctx->nranks) return DBM_OK;
-  // new workspace: zero its header, then the all-gather (after the memset on every rank) registers it
+  if (ctx->xpool && ctx->xpool_bytes >= need && (int)ctx->peer_ws.size() == ctx->nranks) return DBM_OK;
+  // Grow the exchange pool.  `need` is the maximum over all ranks (every rank computes every rank's
+  // plan), so every rank takes this branch in the same multiply: the registration all-gather below is
+  // collective by construction.  A fresh cudaMalloc allocation (not the caller's allocator: CUDA IPC
+  // needs a plain allocation, which expandable segments are not).
+  const size_t bytes = std::max(round_up((int64_t)need, 2 << 20), (int64_t)(2 << 20));
+  char* pool = nullptr;
+  CUDA_TRY(ctx, cudaMalloc(&pool, bytes));
   const int L = (int)lcm64(ctx->pr, ctx->pc);
-  CUDA_TRY(ctx, cudaMemsetAsync(ws, 0, xhdr_bytes(ctx->nranks, L), cs));
+  CUDA_TRY(ctx, cudaMemsetAsync(pool, 0, xhdr_bytes(ctx->nranks, L), cs));  // the header: every word 0
   cudaEvent_t e = get_event(ctx);
   CUDA_TRY(ctx, cudaEventRecord(e, cs));
   CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->comm, e, 0));
   ctx->ev_pool.push_back(e);
-  return ipc_exchange(ctx, ws);
+  if (dbm_status st = ipc_exchange(ctx, pool)) {  // all-gather of the handles after the memset on every rank
+    cudaFree(pool);
+    return st;
+  }
+  // the previous pool: every multiply that used it ended with the closing barrier (no peer reads it)
+  if (ctx->xpool) cudaFree(ctx->xpool);
+  ctx->xpool = pool;
+  ctx->xpool_bytes = bytes;
+  return DBM_OK;
 }
 
 dbm_status dbm::xwrite_word(dbm_ctx ctx, cudaStream_t st, int q, size_t word, uint64_t value) {
@@ -1083,7 +1130,7 @@ dbm_status dbm::xwrite_word(dbm_ctx ctx, cudaStream_t st, int q, size_t word, ui
 }
 
 dbm_status dbm::xwait_word(dbm_ctx ctx, cudaStream_t st, size_t word, uint64_t value) {
-  if (memops(ctx->device).wait(st, (CUdeviceptr)((char*)ctx->ipc_ws + word * 8), (cuuint64_t)value,
+  if (memops(ctx->device).wait(st, (CUdeviceptr)(ctx->xpool + word * 8), (cuuint64_t)value,
                                CU_STREAM_WAIT_VALUE_GEQ) != CUDA_SUCCESS) {
     set_error("cuStreamWaitValue64 failed");
     ctx->poisoned = DBM_ERR_CUDA;
@@ -1488,12 +1535,25 @@ dbm_status multiply_impl(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_matrix B, 
     return DBM_OK;
   }
 
+  // ------------------------------------------------ the exchange pool (several ranks)
+  char* xp = nullptr;  // this rank's exchange pool: signal header + own panels (the peers pull them)
+  uint64_t ep = 0;     // this multiply's epoch
+  if (ctx->nranks > 1) {
+    size_t need = p.pool_total;
+    for (int q = 0; q < ctx->nranks; ++q)
+      need = std::max(need, make_plan_raw(ctx->nranks, p.pr, p.pc, q / p.pc, q % p.pc, p.Mb, p.Nb, p.Kb, p.bs, dens,
+                                          ctx->chunk_bytes, ctx->transport, p.b_packed).pool_total);
+    if (dbm_status e = xattach(ctx, need, cs)) return e;
+    xp = ctx->xpool;
+    ep = ++ctx->epoch;
+  }
+
   // ------------------------------------------------ own panels (densify or pack), on the compute stream
   if (ctx->nranks > 1 && !hpipe) {
     for (int k = 0; k < p.L; ++k) {  // A's own panels first: on host operands B may still be uploading
       if (p.ownA_off[k] != SIZE_MAX) {
         const int64_t col0 = (k - p.c) / p.pc, stride = p.L / p.pc;
-        double* dst = (double*)(ws + p.ownA_off[k]);
+        double* dst = (double*)(xp + p.ownA_off[k]);
         if (dens) {
           ProfScope ps(ctx, cs, 2, 0.0, 16.0 * M * p.kb[k] * bs);
           if (dbm_status e = densify_a(ctx, A, col0, stride, p.kb[k], dst, p.ld_panel(k), 1, cs)) return e;
@@ -1507,7 +1567,7 @@ dbm_status multiply_impl(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_matrix B, 
     for (int k = 0; k < p.L; ++k) {
       if (p.ownB_off[k] != SIZE_MAX) {
         const int64_t row0 = (k - p.r) / p.pr, stride = p.L / p.pr;
-        double* dst = (double*)(ws + p.ownB_off[k]);
+        double* dst = (double*)(xp + p.ownB_off[k]);
         if (dens && !p.b_packed) {
           ProfScope ps(ctx, cs, 2, 0.0, 16.0 * N * p.kb[k] * bs);
           if (dbm_status e = densify_b(ctx, B, row0, stride, p.kb[k], dst, p.ld_panel(k), 0, cs)) return e;
@@ -1524,11 +1584,11 @@ dbm_status multiply_impl(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_matrix B, 
   // blocked path: traversal table once per multiply
   int32_t* trav_li = nullptr;
   int32_t* trav_lj = nullptr;
-  int32_t* trip = nullptr;
+  int32_t* trip0 = nullptr;
   if (!dens) {
     trav_li = (int32_t*)(ws + p.off_trav);
     trav_lj = trav_li + std::max<int64_t>(p.mloc * p.nloc, 1);
-    trip = (int32_t*)(ws + p.off_trip);
+    trip0 = (int32_t*)(ws + p.off_trip);
     ProfScope ps(ctx, cs, 4, 0.0, 8.0 * p.mloc * p.nloc);
     launch_traversal(p.mloc, p.nloc, trav_li, trav_lj, cs);
     launches += (p.mloc * p.nloc) ? 1 : 0;
@@ -1552,7 +1612,6 @@ dbm_status multiply_impl(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_matrix B, 
   // launch loaded its module, synchronised, and waited forever on the peer doing the same.
   std::vector<cudaEvent_t> own_ev;  // own panels' chunk j in place (upload stream)
   cudaStream_t up = hpipe ? ctx->up : nullptr;
-  uint64_t ep = 0;  // this multiply's epoch (copy-engine transport)
   auto publish = [&](int j, bool final_) -> dbm_status {
     // every peer's table entry [me][operand][k] = (epoch, K-blocks of my panel k now in place)
     for (int q = 0; q < ctx->nranks; ++q) {
@@ -1575,11 +1634,11 @@ dbm_status multiply_impl(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_matrix B, 
         const int64_t col0 = (k - p.c) / p.pc, stride = p.L / p.pc;
         ProfScope ps(ctx, up, 2, 0.0, 16.0 * M * (q1 - q0) * bs);
         if (dens) {
-          double* dst = (double*)(ws + p.ownA_off[k]) + q0 * bs;
+          double* dst = (double*)(xp + p.ownA_off[k]) + q0 * bs;
           if (dbm_status e = densify_a(ctx, A, col0 + q0 * stride, stride, q1 - q0, dst, p.ld_panel(k), 1, up))
             return e;
         } else {  // packed A panel: mloc rows of kb[k] blocks; this chunk is columns [q0, q1) of every row
-          double* dst = (double*)(ws + p.ownA_off[k]) + q0 * bb;
+          double* dst = (double*)(xp + p.ownA_off[k]) + q0 * bb;
           launch_pack_cols(A->arena, p.mloc, p.kA, (int)bs, col0 + q0 * stride, stride, q1 - q0, dst, up, p.kb[k]);
         }
         ++launches;
@@ -1588,11 +1647,11 @@ dbm_status multiply_impl(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_matrix B, 
         const int64_t row0 = (k - p.r) / p.pr, stride = p.L / p.pr;
         ProfScope ps(ctx, up, 2, 0.0, 16.0 * N * (q1 - q0) * bs);
         if (dens && !p.b_packed) {
-          double* dst = (double*)(ws + p.ownB_off[k]) + q0 * bs;
+          double* dst = (double*)(xp + p.ownB_off[k]) + q0 * bs;
           if (dbm_status e = densify_b(ctx, B, row0 + q0 * stride, stride, q1 - q0, dst, p.ld_panel(k), 0, up))
             return e;
         } else {
-          double* dst = (double*)(ws + p.ownB_off[k]) + q0 * p.nloc * bb;
+          double* dst = (double*)(xp + p.ownB_off[k]) + q0 * p.nloc * bb;
           launch_pack_rows(B->arena, p.nloc, (int)bs, row0 + q0 * stride, stride, q1 - q0, dst, up);
         }
         ++launches;
@@ -1635,8 +1694,6 @@ dbm_status multiply_impl(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_matrix B, 
       // the workspace is registered): every signal this rank owes its peers -- "my panels are ready"
       // (on the compute stream, behind my own densify / pack) or, with host operands, the chunk-by-chunk
       // progress (upload stream) -- is enqueued before the first wait on theirs.
-      if (dbm_status e = xattach(ctx, ws, cs)) return e;
-      ep = ++ctx->epoch;
       peer_plan.resize(ctx->nranks);
       for (int q = 0; q < ctx->nranks; ++q)
         if (q != ctx->rank)
@@ -1712,9 +1769,9 @@ dbm_status multiply_impl(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_matrix B, 
     const double* Bp;
     if (ctx->nranks > 1) {
       Ap = p.a_src(s) != p.me() ? (const double*)(ws + p.off_recvA[bufA_of[s]])
-                                : (p.ownA_off[k] != SIZE_MAX ? (const double*)(ws + p.ownA_off[k]) : A->arena);
+                                : (p.ownA_off[k] != SIZE_MAX ? (const double*)(xp + p.ownA_off[k]) : A->arena);
       Bp = p.b_src(s) != p.me() ? (const double*)(ws + p.off_recvB[bufB_of[s]])
-                                : (p.ownB_off[k] != SIZE_MAX ? (const double*)(ws + p.ownB_off[k]) : B->arena);
+                                : (p.ownB_off[k] != SIZE_MAX ? (const double*)(xp + p.ownB_off[k]) : B->arena);
     } else {
       Ap = A->arena;
       Bp = B->arena;
@@ -1858,9 +1915,33 @@ dbm_status multiply_impl(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_matrix B, 
         const double* Aj = Ap + k0 * bb;
         const double* Bj = Bp + k0 * p.nloc * bb;
         const double bfirst = (s == 0 && k0 == 0) ? beta : 1.0;  // the first non-empty chunk applies beta
-        for (int64_t q0 = 0; q0 < nruns; q0 += runs_per_chunk) {
+        // two triplet buffers (several chunks): chunk c's stacks are generated on the generation stream
+        // into buffer c % 2 once the multiply of chunk c - 2 released it, overlapping chunk c - 1's
+        // multiply (the generation kernel's CTAs fit beside the persistent small-block kernel's)
+        const bool dbuf = p.off_trip2 != 0 && nruns > runs_per_chunk;
+        cudaEvent_t ev_free[2] = {nullptr, nullptr};
+        if (dbuf) {
+          if (!ctx->gen) CUDA_TRY(ctx, cudaStreamCreateWithFlags(&ctx->gen, cudaStreamNonBlocking));
+          cudaEvent_t e = get_event(ctx);
+          CUDA_TRY(ctx, cudaEventRecord(e, cs));  // the traversal table and everything before
+          CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->gen, e, 0));
+          ctx->ev_pool.push_back(e);
+        }
+        for (int64_t q0 = 0, chunk = 0; q0 < nruns; q0 += runs_per_chunk, ++chunk) {
           const int64_t q1 = std::min(nruns, q0 + runs_per_chunk);
-          {
+          int32_t* trip = (dbuf && (chunk & 1)) ? (int32_t*)(ws + p.off_trip2) : trip0;
+          if (dbuf) {
+            if (ev_free[chunk & 1]) CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->gen, ev_free[chunk & 1], 0));
+            {
+              ProfScope ps(ctx, ctx->gen, 4, 0.0, 12.0 * (q1 - q0) * nk);
+              launch_stackgen(trav_li, trav_lj, q0, q1, nk, p.nloc, a_ld, p.nloc, trip, ctx->gen);
+              ++launches;
+            }
+            cudaEvent_t e = get_event(ctx);
+            CUDA_TRY(ctx, cudaEventRecord(e, ctx->gen));
+            CUDA_TRY(ctx, cudaStreamWaitEvent(cs, e, 0));
+            ctx->ev_pool.push_back(e);
+          } else {
             ProfScope ps(ctx, cs, 4, 0.0, 12.0 * (q1 - q0) * nk);
             launch_stackgen(trav_li, trav_lj, q0, q1, nk, p.nloc, a_ld, p.nloc, trip, cs);
             ++launches;
@@ -1883,7 +1964,13 @@ dbm_status multiply_impl(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_matrix B, 
                                        p.mloc * kbk - k0, (kbk - k0) * p.nloc, squares));
             }
           }
+          if (dbuf) {  // buffer chunk % 2 is free once this multiply is done with it
+            if (!ev_free[chunk & 1]) ev_free[chunk & 1] = get_event(ctx);
+            CUDA_TRY(ctx, cudaEventRecord(ev_free[chunk & 1], cs));
+          }
         }
+        for (cudaEvent_t e : ev_free)
+          if (e) ctx->ev_pool.push_back(e);
       }
       st.entries += nruns * kbk;
       st.stacks += kbk <= cap ? (nruns + (cap / kbk) - 1) / (cap / kbk) : nruns * ((kbk + cap - 1) / cap);

@@ -155,6 +155,7 @@ struct dbm_ctx_s {
   bool own_stream = false;
   cudaStream_t comm = nullptr;
   cudaStream_t up = nullptr;  // host->device uploads of dbm_multiply_host on several ranks (lazy)
+  cudaStream_t gen = nullptr; // stack generation of the next chunk beside the small-block GEMM (lazy)
   bool host_pipe = true;      // several ranks, host operands: chunked uploads gated by peer flags
   void* nccl = nullptr;  // ncclComm_t
   dbm_status poisoned = DBM_OK;
@@ -176,8 +177,10 @@ struct dbm_ctx_s {
   // 1 = NCCL grouped send/recv.
   int transport = 0;
   int algorithm = 0;  // 0 = Cannon, 1 = tall-and-skinny
-  void* ipc_ws = nullptr;                 // registered workspace: the one the peer mappings were built for
+  void* ipc_ws = nullptr;                 // the allocation the peer mappings were built for (= xpool)
   int64_t ipc_ws_bytes = 0;
+  char* xpool = nullptr;                  // exchange pool (several ranks): signal header + own panels
+  size_t xpool_bytes = 0;
   uint64_t epoch = 0;                     // copy-engine multiplies so far (the same count on every rank)
   std::vector<char*> peer_ws;             // peer workspaces mapped into this process (nullptr = self)
   std::vector<std::vector<char>> peer_handles;  // raw IPC handles (to re-use / close mappings)

@@ -26,6 +26,7 @@ struct SpCache {
   std::vector<int64_t> ownA_nnz, ownB_nnz;  // per kappa (-1: not mine)
   std::vector<size_t> ownA_off, ownB_off, o_gatherA, o_gatherB;
   std::vector<std::vector<size_t>> peer_ownA_off, peer_ownB_off;
+  size_t pool_need = 0;  // exchange-pool bytes: the maximum over all ranks of their own_layout end
   std::vector<std::vector<int64_t>> peer_ownA_nnz, peer_ownB_nnz;
   size_t off_recvA[2] = {0, 0}, off_recvB[2] = {0, 0}, off_trav = 0, off_cnt = 0, off_off = 0, off_scan = 0;
   size_t off_trip = 0, scan_bytes = 0, total = 256;
@@ -85,7 +86,8 @@ int64_t b_panel_nnz(dbm_ctx ctx, dbm_matrix B, int L, int cc, int kappa) {
   return n;
 }
 
-// Workspace layout: own (packed) panels first, so a peer only needs the panel sizes to find them.
+// Exchange-pool layout (several ranks): the signal header, then the own (packed) panels, so a peer only
+// needs the panel sizes to find them.  *end = the pool bytes this rank needs.
 void own_layout(dbm_ctx ctx, dbm_matrix A, dbm_matrix B, int L, int r, int c, std::vector<int64_t>& a_nnz,
                 std::vector<int64_t>& b_nnz, std::vector<size_t>& a_off, std::vector<size_t>& b_off, size_t* end) {
   const size_t bb8 = (size_t)A->bs * A->bs * 8;
@@ -93,7 +95,7 @@ void own_layout(dbm_ctx ctx, dbm_matrix A, dbm_matrix B, int L, int r, int c, st
   b_nnz.assign(L, -1);
   a_off.assign(L, SIZE_MAX);
   b_off.assign(L, SIZE_MAX);
-  size_t off = xhdr_bytes(ctx->nranks, L);  // several ranks: the signal header comes first
+  size_t off = xhdr_bytes(ctx->nranks, L);  // exchange-pool offsets: the signal header comes first
   if (ctx->nranks > 1) {
     for (int k = 0; k < L; ++k)
       if (k % ctx->pc == c) {
@@ -126,17 +128,19 @@ dbm_status sp_cache_get(dbm_ctx ctx, dbm_matrix A, dbm_matrix B, dbm_matrix C, S
   sc->L = L;
   const int64_t mloc = C->mloc, nloc = C->nloc, Kb = A->Nb;
   const size_t bb8 = (size_t)A->bs * A->bs * 8;
-  size_t off = 0;
-  own_layout(ctx, A, B, L, r, c, sc->ownA_nnz, sc->ownB_nnz, sc->ownA_off, sc->ownB_off, &off);
+  size_t off = 0;  // caller-owned workspace offsets (the own panels are in the exchange pool)
+  own_layout(ctx, A, B, L, r, c, sc->ownA_nnz, sc->ownB_nnz, sc->ownA_off, sc->ownB_off, &sc->pool_need);
   sc->peer_ownA_off.resize(ctx->nranks);
   sc->peer_ownB_off.resize(ctx->nranks);
   sc->peer_ownA_nnz.resize(ctx->nranks);
   sc->peer_ownB_nnz.resize(ctx->nranks);
   for (int q = 0; q < ctx->nranks && ctx->nranks > 1; ++q) {
     size_t e;
-    if (q != me)
+    if (q != me) {
       own_layout(ctx, A, B, L, q / pc, q % pc, sc->peer_ownA_nnz[q], sc->peer_ownB_nnz[q], sc->peer_ownA_off[q],
                  sc->peer_ownB_off[q], &e);
+      sc->pool_need = std::max(sc->pool_need, e);  // the pool size every rank agrees on
+    }
   }
   // per-step panel metadata and entry counts
   std::vector<int32_t> meta;
@@ -334,14 +338,21 @@ dbm_status multiply_sparse_blocked(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_
     return DBM_OK;
   }
   const int32_t* meta = sc->d_meta;
+  char* xp = nullptr;  // exchange pool (several ranks): signal header + my packed panels
+  uint64_t ep = 0;     // this multiply's epoch (signals between ranks)
+  if (ctx->nranks > 1) {
+    if (dbm_status e = xattach(ctx, sc->pool_need, cs)) return e;
+    xp = ctx->xpool;
+    ep = ++ctx->epoch;
+  }
   if (ctx->nranks > 1) {  // pack my panels (stored blocks only)
     for (int k = 0; k < L; ++k) {
       if (sc->ownA_nnz[k] > 0) {
-        launch_sp_gather(A->arena, meta + sc->o_gatherA[k], sc->ownA_nnz[k], bs, (double*)(ws + sc->ownA_off[k]), cs);
+        launch_sp_gather(A->arena, meta + sc->o_gatherA[k], sc->ownA_nnz[k], bs, (double*)(xp + sc->ownA_off[k]), cs);
         ++launches;
       }
       if (sc->ownB_nnz[k] > 0) {
-        launch_sp_gather(B->arena, meta + sc->o_gatherB[k], sc->ownB_nnz[k], bs, (double*)(ws + sc->ownB_off[k]), cs);
+        launch_sp_gather(B->arena, meta + sc->o_gatherB[k], sc->ownB_nnz[k], bs, (double*)(xp + sc->ownB_off[k]), cs);
         ++launches;
       }
     }
@@ -356,7 +367,6 @@ dbm_status multiply_sparse_blocked(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_
   }
   std::vector<cudaEvent_t> ev_x(L, nullptr), ev_g(L, nullptr);
   cudaEvent_t ev_ready = nullptr;
-  uint64_t ep = 0;  // this multiply's epoch (signals between ranks)
   std::vector<int> bufA(L, -1), bufB(L, -1);
   auto pulls = [&](int s) -> dbm_status {
     const SpStep& x = sc->steps[s];
@@ -394,8 +404,6 @@ dbm_status multiply_sparse_blocked(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_
     CUDA_TRY(ctx, cudaEventRecord(ev_ready, cs));
     CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->comm, ev_ready, 0));
     // my packed panels are ready (signal behind the packs) -> wait for every peer's (device-side)
-    if (dbm_status e = xattach(ctx, ws, cs)) return e;
-    ep = ++ctx->epoch;
     if (dbm_status e = xsignal(ctx, cs, X_READY, ep)) return e;
     if (dbm_status e = xwait(ctx, ctx->comm, X_READY, ep)) return e;
     if (dbm_status e = pulls(0)) return e;
@@ -416,10 +424,10 @@ dbm_status multiply_sparse_blocked(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_
     }
     const double* Ap = ctx->nranks == 1 ? A->arena
                        : x.a_src != me ? (const double*)(ws + sc->off_recvA[bufA[s]])
-                                       : (const double*)(ws + sc->ownA_off[x.kappa]);
+                                       : (const double*)(xp + sc->ownA_off[x.kappa]);
     const double* Bp = ctx->nranks == 1 ? B->arena
                        : x.b_src != me ? (const double*)(ws + sc->off_recvB[bufB[s]])
-                                       : (const double*)(ws + sc->ownB_off[x.kappa]);
+                                       : (const double*)(xp + sc->ownB_off[x.kappa]);
     if (x.entries > 0) {
       const int64_t nruns = mloc * nloc;
       for (int64_t q0 = 0, ch = 0; q0 < nruns; q0 += sc->runs_per_chunk, ++ch) {

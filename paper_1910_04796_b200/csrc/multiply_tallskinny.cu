@@ -27,6 +27,7 @@ struct TSPlan {
   int64_t Mtot = 0, Ntot = 0;
   std::vector<size_t> offApiece, offBpiece;  // my pieces: A per target row tr, B per target t (q = r + t*pr)
   size_t off_afull = 0, off_bfull = 0, off_cpart = 0, off_cstack = 0, off_part = 0, total = 0;
+  size_t pool_total = 0;  // exchange pool: header + pieces + partial C (offApiece, offBpiece, off_cpart)
   int max_split = 1;
   int64_t ld(int q) const { return round_up(std::max<int64_t>(kp[q] * bs, 1), 2); }
   size_t a_piece_bytes(int q, int rr) const { return kp[q] ? (size_t)mrows[rr] * ld(q) * 8 : 0; }
@@ -61,19 +62,27 @@ TSPlan make_ts_plan(int pr, int pc, int r, int c, int64_t Mb, int64_t Nb, int64_
   }
   t.Mtot = Mb * bs;
   t.Ntot = Nb * bs;
-  size_t off = xhdr_bytes(pr * pc, (int)lcm64(pr, pc));  // the signal header comes first
+  size_t off = 0;
   auto take = [&](size_t bytes) {
     size_t o = off;
     off = align256(off + bytes);
     return o;
   };
+  // what the peers read (my pieces, my partial C) lives in the exchange pool, after the signal header
+  size_t poff = xhdr_bytes(pr * pc, (int)lcm64(pr, pc));
+  auto take_pool = [&](size_t bytes) {
+    size_t o = poff;
+    poff = align256(poff + bytes);
+    return o;
+  };
   t.offApiece.resize(pr);
-  for (int tr = 0; tr < pr; ++tr) t.offApiece[tr] = take(t.a_piece_bytes(tr * pc + c, r));
+  for (int tr = 0; tr < pr; ++tr) t.offApiece[tr] = take_pool(t.a_piece_bytes(tr * pc + c, r));
   t.offBpiece.resize(pc);
-  for (int tt = 0; tt < pc; ++tt) t.offBpiece[tt] = take(t.b_piece_bytes(r + tt * pr, c));
+  for (int tt = 0; tt < pc; ++tt) t.offBpiece[tt] = take_pool(t.b_piece_bytes(r + tt * pr, c));
+  t.off_cpart = take_pool((size_t)t.Mtot * t.Ntot * 8);
+  t.pool_total = poff;
   t.off_afull = take((size_t)t.Mtot * t.ld(t.me) * 8);
   t.off_bfull = take((size_t)t.Ntot * t.ld(t.me) * 8);
-  t.off_cpart = take((size_t)t.Mtot * t.Ntot * 8);
   t.off_cstack = take((size_t)t.P * t.mrows[r] * t.ncols[c] * 8);
   const int64_t K = t.kp[t.me] * bs;
   const std::vector<int64_t> cb = pipeline_chunks(t.kp[t.me]);
@@ -124,6 +133,12 @@ dbm_status multiply_tallskinny(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_matr
   const TSPlan t = make_ts_plan(ctx->pr, ctx->pc, ctx->myrow, ctx->mycol, A->Mb, B->Nb, A->Nb, A->bs);
   cudaStream_t cs = ctx->stream;
   const int64_t bs = t.bs, P = t.P;
+  size_t need = t.pool_total;  // every rank's pool need: the growth decision is the same on every rank
+  for (int q = 0; q < P; ++q)
+    need = std::max(need, make_ts_plan(t.pr, t.pc, q / t.pc, q % t.pc, t.Mb, t.Nb, t.Kb, bs).pool_total);
+  if (dbm_status e = xattach(ctx, need, cs)) return e;
+  char* xp = ctx->xpool;
+  const uint64_t ep = ++ctx->epoch;
   // ---- own pieces (densified once; peers pull them).  The pieces this rank needs itself are densified
   // straight into its A_full / B_full: a local device-to-device copy would run on SMs and wait behind
   // the persistent GEMM (measured: 23 GB/s under a GEMM vs 750 GB/s for the peer pulls on the copy
@@ -132,7 +147,7 @@ dbm_status multiply_tallskinny(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_matr
     const int q = tr * t.pc + t.c;
     if (!t.kp[q] || !t.mrows[t.r]) continue;
     double* dst = q == t.me ? (double*)(ws + t.off_afull) + (size_t)t.rowoff[t.r] * t.ld(q)
-                            : (double*)(ws + t.offApiece[tr]);
+                            : (double*)(xp + t.offApiece[tr]);
     ProfScope ps(ctx, cs, 2, 0.0, 16.0 * t.mrows[t.r] * t.kp[q] * bs);
     if (dbm_status e = densify_a(ctx, A, tr, t.pr, t.kp[q], dst, t.ld(q), 1, cs)) return e;
     ++*launches;
@@ -141,7 +156,7 @@ dbm_status multiply_tallskinny(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_matr
     const int q = t.r + tt * t.pr;
     if (!t.kp[q] || !t.ncols[t.c]) continue;
     double* dst = q == t.me ? (double*)(ws + t.off_bfull) + (size_t)t.coloff[t.c] * t.ld(q)
-                            : (double*)(ws + t.offBpiece[tt]);
+                            : (double*)(xp + t.offBpiece[tt]);
     ProfScope ps(ctx, cs, 2, 0.0, 16.0 * t.ncols[t.c] * t.kp[q] * bs);
     if (dbm_status e = densify_b(ctx, B, tt, t.pc, t.kp[q], dst, t.ld(q), 0, cs)) return e;
     ++*launches;
@@ -151,14 +166,12 @@ dbm_status multiply_tallskinny(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_matr
   CUDA_TRY(ctx, cudaEventRecord(ev_ready, cs));
   CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->comm, ev_ready, 0));
   // "my pieces are ready" (behind the densifies) -> the gathers wait for every peer's (device-side)
-  if (dbm_status e = xattach(ctx, ws, cs)) return e;
-  const uint64_t ep = ++ctx->epoch;
   if (dbm_status e = xsignal(ctx, cs, X_READY, ep)) return e;
   if (dbm_status e = xwait(ctx, ctx->comm, X_READY, ep)) return e;
   std::vector<TSPlan> peer(P);
   for (int q = 0; q < P; ++q)
     if (q != t.me) peer[q] = make_ts_plan(t.pr, t.pc, q / t.pc, q % t.pc, t.Mb, t.Nb, t.Kb, bs);
-  auto base_of = [&](int q) { return q == t.me ? ws : ctx->peer_ws[q]; };
+  auto base_of = [&](int q) { return q == t.me ? xp : ctx->peer_ws[q]; };
 
   // ---- gather A[:, S_me] and B[S_me, :] in K-chunks on the comm stream, GEMM chunks on the compute stream
   const int64_t kb = t.kp[t.me], ldp = t.ld(t.me);
@@ -173,7 +186,7 @@ dbm_status multiply_tallskinny(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_matr
   const int nsub = (int)cb.size() - 1;
   char* afull = ws + t.off_afull;
   char* bfull = ws + t.off_bfull;
-  double* cpart = (double*)(ws + t.off_cpart);
+  double* cpart = (double*)(xp + t.off_cpart);
   cudaEvent_t ev_c[kMaxChunks] = {};
   const int rb = t.me % t.pr;
   int64_t ts_recv = 0, ts_sent = 0;

@@ -58,6 +58,7 @@ _SIGS = {
     "dbm_ctx_set_profiling": (C.c_int, [_P, C.c_int]),
     "dbm_ctx_profile_read": (C.c_int, [_P, C.c_int, C.POINTER(C.c_double), C.POINTER(_I64),
                                        C.POINTER(C.c_double), C.POINTER(C.c_double)]),
+    "dbm_ctx_profile_timeline": (C.c_int, [_P, C.c_int, _P, C.POINTER(C.c_int)]),
     "dbm_ctx_launch_count": (C.c_int, [_P, C.POINTER(_I64)]),
     "dbm_ctx_set_dense_chunk_bytes": (C.c_int, [_P, _I64]),
     "dbm_ctx_set_transport": (C.c_int, [_P, C.c_int]),
@@ -184,6 +185,16 @@ class Context:
         n = C.c_int64()
         _check(load().dbm_ctx_profile_read(self.h, kernel, C.byref(ms), C.byref(n), C.byref(fl), C.byref(by)))
         return {"ms": ms.value, "launches": n.value, "flops": fl.value, "bytes": by.value}
+
+    def profile_timeline(self, max_records: int = 4096) -> list[tuple[int, float, float]]:
+        """dbm_ctx_profile_timeline: (kind, start_ms, end_ms) of the pending profiling records."""
+        import numpy as np
+
+        buf = np.zeros(3 * max(max_records, 1))
+        n = C.c_int()
+        _check(load().dbm_ctx_profile_timeline(self.h, max_records, buf.ctypes.data, C.byref(n)))
+        k = min(n.value, max_records)
+        return [(int(buf[3 * i]), float(buf[3 * i + 1]), float(buf[3 * i + 2])) for i in range(k)]
 
     def set_transport(self, transport: str | int) -> None:
         """'ce' (copy engines over CUDA IPC, default) or 'nccl' (grouped send/recv)."""

@@ -1,4 +1,4 @@
-"""Multi-process (world_size 2 and 4, gloo, CPU) test of the library's Cannon exchange schedule.
+"""Multi-process (world_size 2, 4 and 8, gloo, CPU) test of the library's Cannon exchange schedule.
 
 Each rank asks libdbm (host-only dbm_plan_exchange, the same op list dbm_multiply hands to NCCL)
 what to send and receive at every step, moves real panels with torch.distributed send/recv over
@@ -97,7 +97,10 @@ def _worker(rank, world, pr, pc, port, shape, q):
 
 
 @pytest.mark.parametrize("pr,pc,shape", [(1, 2, (3, 5, 7, 4)), (2, 1, (5, 3, 4, 2)), (2, 2, (5, 7, 9, 2)),
-                                         (1, 4, (3, 9, 10, 2)), (4, 1, (9, 2, 5, 2))])
+                                         (1, 4, (3, 9, 10, 2)), (4, 1, (9, 2, 5, 2)),
+                                         # world 8: the north star's 2 x 4 grid (L = 4) and its transpose,
+                                         # ragged block counts (13 = 4 + 3 + 3 + 3 K-blocks per panel)
+                                         (2, 4, (5, 11, 13, 2)), (4, 2, (9, 5, 11, 3))])
 def test_gloo_cannon_exchange(pr, pc, shape):
     world = pr * pc
     ctx = mp.get_context("spawn")

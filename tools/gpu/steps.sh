@@ -43,7 +43,8 @@ for s in "$@"; do
           --csv python tools/profile_dgemm.py --M 63360 --N 63360 --K 15872 --reps 1
       done ;;
     dgemm_sweep)
-      for cfg in ${SWEEP:-"0:1 32:1 64:1 128:1 64:2 16:1"}; do
+      SW="${SWEEP:-0:1 32:1 64:1 128:1 64:2 16:1}"
+      for cfg in $SW; do
         IFS=: read -r ws sl <<< "$cfg"
         step dgemm_ws${ws}_sl${sl} 600 env DBM_DGEMM_WAVESYNC=$ws DBM_DGEMM_WAVESLACK=$sl \
           python tools/profile_dgemm.py --M 63360 --N 63360 --K 15872 --reps 4

@@ -77,6 +77,11 @@ def lib():
             "orc_freivalds_rhs": (None, [_i64, _i64, _i64, _u64, C.c_int, _dbl, _dbl, _u64, _pd, _pd]),
             "orc_sign_value": (_dbl, [_u64, _i64]),
             "orc_num_threads": (C.c_int, []),
+            "orc_nu_local_elems": (_i64, [_pi32, _i64, _pi32, _i64, C.c_int, C.c_int, C.c_int, C.c_int, _pu8]),
+            "orc_nu_scatter": (None, [_pd, _pi32, _i64, _pi32, _i64, C.c_int, C.c_int, C.c_int, C.c_int, _pu8, _pd]),
+            "orc_nu_gather": (None, [_pd, _pi32, _i64, _pi32, _i64, C.c_int, C.c_int, C.c_int, C.c_int, _pu8, _pd]),
+            "orc_nu_multiply": (None, [_pi32, _i64, _pi32, _i64, _pi32, _i64, _dbl, _pd, _pu8, _pd, _pu8, _dbl, _pd,
+                                       _pu8]),
             "orc_pattern_present": (C.c_int, [_u64, C.c_uint32, _i64, _i64, _dbl]),
             "orc_pattern_random": (None, [_u64, C.c_uint32, _i64, _i64, _dbl, _pu8]),
             "orc_multiply_sparse": (None, [_i64, _i64, _i64, C.c_int, _dbl, _pd, _pu8, _pd, _pu8, _dbl, _pd, _pu8]),
@@ -333,3 +338,61 @@ def freivalds_rhs(M, N, K, seed, kind, alpha, beta, x_seed):
 
 def num_threads() -> int:
     return lib().orc_num_threads()
+
+
+# ---------------------------------------------------------------- non-uniform block sizes (reading R16)
+def _i32(a):
+    return np.ascontiguousarray(a, dtype=np.int32)
+
+
+def _mask(m):
+    return None if m is None else np.ascontiguousarray(m, dtype=np.uint8)
+
+
+def fill_dense(seed, mat_id, kind, rows, cols) -> np.ndarray:
+    """The generator's matrix as a dense column-major (rows, cols) array: D(gi, gj) = v(seed, mat_id, gi, gj)
+    (independent of any blocking, so it is the reference for every block-size layout)."""
+    d = np.empty((cols, rows))
+    for gj in range(cols):
+        for gi in range(rows):
+            d[gj, gi] = fill_value(seed, mat_id, gi, gj, kind)
+    return d.T  # (rows, cols) view of column-major storage
+
+
+def nu_local_elems(rsz, csz, pr=1, pc=1, r=0, c=0, mask=None) -> int:
+    rs, cs = _i32(rsz), _i32(csz)
+    mk = _mask(mask)
+    return lib().orc_nu_local_elems(_p(rs, _pi32), len(rs), _p(cs, _pi32), len(cs), pr, pc, r, c,
+                                    _p(mk, _pu8) if mk is not None else None)
+
+
+def nu_scatter(dense, rsz, csz, pr=1, pc=1, r=0, c=0, mask=None) -> np.ndarray:
+    """Local arena of rank (r, c) from a dense (rows, cols) array (any memory order)."""
+    rs, cs = _i32(rsz), _i32(csz)
+    mk = _mask(mask)
+    d = np.ascontiguousarray(np.asarray(dense).T)  # column-major storage
+    out = np.empty(max(nu_local_elems(rs, cs, pr, pc, r, c, mk), 1))
+    lib().orc_nu_scatter(_p(d), _p(rs, _pi32), len(rs), _p(cs, _pi32), len(cs), pr, pc, r, c,
+                         _p(mk, _pu8) if mk is not None else None, _p(out))
+    return out[: nu_local_elems(rs, cs, pr, pc, r, c, mk)]
+
+
+def nu_gather_into(dense_t, local, rsz, csz, pr=1, pc=1, r=0, c=0, mask=None) -> None:
+    """Write rank (r, c)'s blocks into dense_t, a C-contiguous (cols, rows) array = column-major storage."""
+    rs, cs = _i32(rsz), _i32(csz)
+    mk = _mask(mask)
+    lib().orc_nu_gather(_p(np.ascontiguousarray(local)), _p(rs, _pi32), len(rs), _p(cs, _pi32), len(cs), pr, pc, r,
+                        c, _p(mk, _pu8) if mk is not None else None, _p(dense_t))
+
+
+def nu_multiply(msz, nsz, ksz, alpha, A, B, beta, C, amask=None, bmask=None, cmask=None) -> np.ndarray:
+    """C_out (dense (M, N)) = alpha*A*B + beta*C over stored blocks of mixed (m, n, k) sizes."""
+    ms, ns, ks = _i32(msz), _i32(nsz), _i32(ksz)
+    a = np.ascontiguousarray(np.asarray(A).T)
+    b = np.ascontiguousarray(np.asarray(B).T)
+    cc = np.ascontiguousarray(np.asarray(C).T).copy()
+    am, bm, cm = _mask(amask), _mask(bmask), _mask(cmask)
+    lib().orc_nu_multiply(_p(ms, _pi32), len(ms), _p(ns, _pi32), len(ns), _p(ks, _pi32), len(ks), alpha, _p(a),
+                          _p(am, _pu8) if am is not None else None, _p(b), _p(bm, _pu8) if bm is not None else None,
+                          beta, _p(cc), _p(cm, _pu8) if cm is not None else None)
+    return cc.T

@@ -675,3 +675,91 @@ int64_t orc_sparse_rows_from_seeds(int64_t M, int64_t N, int64_t K, int bs, uint
   }
   return fmas;
 }
+
+/* ------------------------------------------------------------------------- */
+/* Non-uniform block sizes ("BlockDims: row_sizes / */
+/* col_sizes", "non-uniform block sizes are supported throughout"; the      */
+/* paper's (m x k) x (k x n) block products, §II).  A matrix is a dense     */
+/* M x N array cut into blocks by row_sizes (Mb entries) and col_sizes (Nb);      */
+/* block (bi, bj) covers rows roff[bi] .. roff[bi]+rsz[bi]-1 and the same for     */
+/* columns, roff / coff the prefix sums.  A rank's local arena holds its stored    */
+/* blocks (owner rule S:115, block-cyclic over block indices) in local CSR order   */
+/* (li, then lj), each block column-major, packed back to back (reading R16).     */
+/* ------------------------------------------------------------------------- */
+static int64_t nu_off(const int32_t* sz, int64_t i) {
+  int64_t o = 0;
+  for (int64_t q = 0; q < i; ++q) o += sz[q];
+  return o;
+}
+
+int64_t orc_nu_local_elems(const int32_t* rsz, int64_t Mb, const int32_t* csz, int64_t Nb, int pr, int pc, int r,
+                           int c, const uint8_t* mask) {
+  int64_t n = 0;
+  for (int64_t bi = r; bi < Mb; bi += pr)
+    for (int64_t bj = c; bj < Nb; bj += pc)
+      if (!mask || mask[bi * Nb + bj]) n += (int64_t)rsz[bi] * csz[bj];
+  return n;
+}
+
+/* dense (column-major, ld = M = sum rsz) -> the local arena of rank (r, c) */
+void orc_nu_scatter(const double* dense, const int32_t* rsz, int64_t Mb, const int32_t* csz, int64_t Nb, int pr,
+                    int pc, int r, int c, const uint8_t* mask, double* local) {
+  int64_t M = nu_off(rsz, Mb), o = 0;
+  for (int64_t bi = r; bi < Mb; bi += pr)
+    for (int64_t bj = c; bj < Nb; bj += pc) {
+      if (mask && !mask[bi * Nb + bj]) continue;
+      int64_t r0 = nu_off(rsz, bi), c0 = nu_off(csz, bj);
+      for (int64_t y = 0; y < csz[bj]; ++y)
+        for (int64_t x = 0; x < rsz[bi]; ++x) local[o++] = dense[(c0 + y) * M + r0 + x];
+    }
+}
+
+/* the local arena of rank (r, c) -> its blocks' places in the dense array (other entries untouched) */
+void orc_nu_gather(const double* local, const int32_t* rsz, int64_t Mb, const int32_t* csz, int64_t Nb, int pr,
+                   int pc, int r, int c, const uint8_t* mask, double* dense) {
+  int64_t M = nu_off(rsz, Mb), o = 0;
+  for (int64_t bi = r; bi < Mb; bi += pr)
+    for (int64_t bj = c; bj < Nb; bj += pc) {
+      if (mask && !mask[bi * Nb + bj]) continue;
+      int64_t r0 = nu_off(rsz, bi), c0 = nu_off(csz, bj);
+      for (int64_t y = 0; y < csz[bj]; ++y)
+        for (int64_t x = 0; x < rsz[bi]; ++x) dense[(c0 + y) * M + r0 + x] = local[o++];
+    }
+}
+
+/* C = alpha*A*B + beta*C over blocks of mixed (m, n, k) sizes: for every stored C block (bi, bj),
+ * acc = sum over bk ascending with A(bi, bk) and B(bk, bj) stored of the (m x k) x (k x n) block
+ * product (element loops), then C_blk = beta*C_blk + alpha*acc (beta == 0: C not read; C's pattern is
+ * kept, reading R15).  Dense column-major arrays: A M x K, B K x N, C M x N; masks NULL = all stored.
+ * The block products are the paper's (§II "(m x k) for A blocks and (k x n) for B blocks"). */
+void orc_nu_multiply(const int32_t* msz, int64_t Mb, const int32_t* nsz, int64_t Nb, const int32_t* ksz, int64_t Kb,
+                     double alpha, const double* A, const uint8_t* amask, const double* B, const uint8_t* bmask,
+                     double beta, double* C, const uint8_t* cmask) {
+  int64_t M = nu_off(msz, Mb), K = nu_off(ksz, Kb);
+#pragma omp parallel for schedule(dynamic, 1)
+  for (int64_t bi = 0; bi < Mb; ++bi) {
+    int64_t r0 = nu_off(msz, bi), m = msz[bi];
+    for (int64_t bj = 0; bj < Nb; ++bj) {
+      if (cmask && !cmask[bi * Nb + bj]) continue;
+      int64_t c0 = nu_off(nsz, bj), n = nsz[bj];
+      double* acc = (double*)calloc((size_t)(m * n > 0 ? m * n : 1), sizeof(double));
+      for (int64_t bk = 0; bk < Kb && alpha != 0.0; ++bk) { /* alpha == 0: A, B not read (reading R8) */
+        if ((amask && !amask[bi * Kb + bk]) || (bmask && !bmask[bk * Nb + bj])) continue;
+        int64_t k0 = nu_off(ksz, bk);
+        for (int64_t y = 0; y < n; ++y)
+          for (int64_t x = 0; x < m; ++x) {
+            double sum = acc[y * m + x];
+            for (int64_t z = 0; z < ksz[bk]; ++z) sum += A[(k0 + z) * M + r0 + x] * B[(c0 + y) * K + k0 + z];
+            acc[y * m + x] = sum;
+          }
+      }
+      for (int64_t y = 0; y < n; ++y)
+        for (int64_t x = 0; x < m; ++x) {
+          double* p = &C[(c0 + y) * M + r0 + x];
+          double t = alpha * acc[y * m + x];
+          *p = (beta == 0.0) ? t : t + beta * *p;
+        }
+      free(acc);
+    }
+  }
+}

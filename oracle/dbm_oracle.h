@@ -139,6 +139,19 @@ int64_t orc_sparse_rows_from_seeds(int64_t M, int64_t N, int64_t K, int bs, uint
                                    double occ_a, double occ_b, double occ_c, double alpha, double beta,
                                    const int64_t* rows, int64_t nrows, double* out);
 
+/* ---- Non-uniform block sizes (§II (m x k)(k x n) block
+ * products), reading R16: blocks cut by row_sizes / col_sizes; a rank's arena = its stored blocks in
+ * local CSR order, each column-major, back to back. ---- */
+int64_t orc_nu_local_elems(const int32_t* rsz, int64_t Mb, const int32_t* csz, int64_t Nb, int pr, int pc, int r,
+                           int c, const uint8_t* mask);
+void orc_nu_scatter(const double* dense, const int32_t* rsz, int64_t Mb, const int32_t* csz, int64_t Nb, int pr,
+                    int pc, int r, int c, const uint8_t* mask, double* local);
+void orc_nu_gather(const double* local, const int32_t* rsz, int64_t Mb, const int32_t* csz, int64_t Nb, int pr,
+                   int pc, int r, int c, const uint8_t* mask, double* dense);
+void orc_nu_multiply(const int32_t* msz, int64_t Mb, const int32_t* nsz, int64_t Nb, const int32_t* ksz, int64_t Kb,
+                     double alpha, const double* A, const uint8_t* amask, const double* B, const uint8_t* bmask,
+                     double beta, double* C, const uint8_t* cmask);
+
 int orc_num_threads(void);
 
 #ifdef __cplusplus

@@ -669,3 +669,89 @@ def test_pack_panel_brute_force(orc, Mb, Nb, Kb, bs, pr, pc):
                     exp = np.concatenate([gB[(k * Nb + j) * bb:(k * Nb + j + 1) * bb] for k in ks for j in cols]
                                          or [np.zeros(0)])
                     assert np.array_equal(got, exp)
+
+
+# ----------------------------------------------------------------- non-uniform block sizes (reading R16)
+def _cut(sizes):
+    o = np.concatenate([[0], np.cumsum(sizes)]).astype(int)
+    return [(o[i], o[i + 1]) for i in range(len(sizes))]
+
+
+@pytest.mark.parametrize("rsz,csz,pr,pc", [([5, 13, 22, 3], [23, 4, 26], 2, 2), ([7], [1, 2, 3, 4, 5], 1, 2),
+                                           ([22, 22, 22], [64, 22], 2, 1), ([9, 1, 31, 2, 17], [6, 11], 2, 4)])
+def test_nu_scatter_gather_brute_force(orc, rsz, csz, pr, pc):
+    """R16 layout: rank (r, c)'s arena = its blocks (owner rule S:115 through orc_owner_rank) in (bi, bj) order,
+    each column-major, back to back; read from the dense array by slicing (catches a swapped size list, a
+    row-major block or a wrong prefix offset).  Scatter over all ranks then gather restores the array."""
+    rng = np.random.default_rng(3)
+    M, N = sum(rsz), sum(csz)
+    D = rng.uniform(-1, 1, (M, N))
+    rows, cols = _cut(rsz), _cut(csz)
+    mask = (rng.uniform(size=(len(rsz), len(csz))) < 0.7).astype(np.uint8)
+    for mk in (None, mask):
+        back = np.full((N, M), np.nan)  # column-major storage of the (M, N) result
+        for r in range(pr):
+            for c in range(pc):
+                q = r * pc + c
+                exp = [D[rows[bi][0]:rows[bi][1], cols[bj][0]:cols[bj][1]].T.reshape(-1)
+                       for bi in range(len(rsz)) for bj in range(len(csz))
+                       if orc.owner_rank(bi, bj, pr, pc) == q and (mk is None or mk[bi, bj])]
+                exp = np.concatenate(exp) if exp else np.zeros(0)
+                loc = orc.nu_scatter(D, rsz, csz, pr, pc, r, c, mk)
+                assert orc.nu_local_elems(rsz, csz, pr, pc, r, c, mk) == exp.size
+                assert np.array_equal(loc, exp)
+                orc.nu_gather_into(back, loc, rsz, csz, pr, pc, r, c, mk)
+        stored = np.ones((M, N), bool)
+        if mk is not None:
+            stored = np.zeros((M, N), bool)
+            for bi in range(len(rsz)):
+                for bj in range(len(csz)):
+                    if mk[bi, bj]:
+                        stored[rows[bi][0]:rows[bi][1], cols[bj][0]:cols[bj][1]] = True
+        assert np.array_equal(back.T[stored], D[stored]) and np.isnan(back.T[~stored]).all()
+
+
+@pytest.mark.parametrize("msz,nsz,ksz", [([5, 13, 22], [23, 4, 26, 9], [7, 22, 31]), ([64], [1], [2, 3]),
+                                         ([22] * 3, [22] * 2, [22] * 4)])
+def test_nu_multiply_matches_numpy(orc, msz, nsz, ksz):
+    """Mixed (m, n, k) block products: all-stored = alpha*A@B + beta*C (numpy/BLAS); with masks =
+    the product of the block-masked operands on the stored C blocks, the other C entries untouched
+    (catches a transposed block, a dropped k block or an m/n swap on non-square blocks)."""
+    rng = np.random.default_rng(5)
+    M, N, K = sum(msz), sum(nsz), sum(ksz)
+    A, B, C = rng.uniform(-1, 1, (M, K)), rng.uniform(-1, 1, (K, N)), rng.uniform(-1, 1, (M, N))
+    got = orc.nu_multiply(msz, nsz, ksz, 0.75, A, B, -1.25, C)
+    assert np.allclose(got, 0.75 * A @ B - 1.25 * C, rtol=0, atol=1e-12)
+
+    def expand(mask, rs, cs):
+        e = np.zeros((sum(rs), sum(cs)), bool)
+        for i, (a0, a1) in enumerate(_cut(rs)):
+            for j, (b0, b1) in enumerate(_cut(cs)):
+                e[a0:a1, b0:b1] = mask[i, j]
+        return e
+
+    am = (rng.uniform(size=(len(msz), len(ksz))) < 0.6).astype(np.uint8)
+    bm = (rng.uniform(size=(len(ksz), len(nsz))) < 0.6).astype(np.uint8)
+    cm = (rng.uniform(size=(len(msz), len(nsz))) < 0.6).astype(np.uint8)
+    got = orc.nu_multiply(msz, nsz, ksz, 0.75, A, B, -1.25, C, am, bm, cm)
+    Ae, Be, Ce = expand(am, msz, ksz), expand(bm, ksz, nsz), expand(cm, msz, nsz)
+    ref = np.where(Ce, 0.75 * (A * Ae) @ (B * Be) - 1.25 * C, C)
+    assert np.allclose(got, ref, rtol=0, atol=1e-12)
+
+
+def test_nu_multiply_uniform_is_the_blocked_oracle_and_conventions(orc):
+    """Uniform sizes reduce R16 to the uniform layout: orc_nu_multiply through nu_scatter equals
+    orc_multiply_blocked bit for bit (same k order); alpha = 0 gives beta*C exactly, beta = 0 ignores a
+    NaN C (reading R8)."""
+    Mb, Nb, Kb, bs = 3, 2, 4, 5
+    A = orc.fill_dense(7, 0, 0, Mb * bs, Kb * bs)
+    B = orc.fill_dense(7, 1, 0, Kb * bs, Nb * bs)
+    C = orc.fill_dense(7, 2, 0, Mb * bs, Nb * bs)
+    got = orc.nu_multiply([bs] * Mb, [bs] * Nb, [bs] * Kb, 0.75, A, B, -1.25, C)
+    Ag = orc.fill_arena(7, 0, 0, Mb * bs, Kb * bs, bs)
+    Bg = orc.fill_arena(7, 1, 0, Kb * bs, Nb * bs, bs)
+    Cg = orc.fill_arena(7, 2, 0, Mb * bs, Nb * bs, bs)
+    orc.multiply_blocked(Mb, Nb, Kb, bs, 0.75, Ag, Bg, -1.25, Cg)
+    assert np.array_equal(orc.nu_scatter(got, [bs] * Mb, [bs] * Nb), Cg)
+    assert np.array_equal(orc.nu_multiply([bs] * Mb, [bs] * Nb, [bs] * Kb, 0.0, A * np.nan, B, -1.25, C), -1.25 * C)
+    assert not np.isnan(orc.nu_multiply([bs] * Mb, [bs] * Nb, [bs] * Kb, 1.0, A, B, 0.0, C * np.nan)).any()

@@ -168,6 +168,23 @@ dbm_status dbm_pattern_random(uint64_t seed, uint32_t mat_id, int64_t Mb, int64_
 dbm_status dbm_pattern_product(int64_t Mb, int64_t Kb, int64_t Nb, const uint8_t* amask, const uint8_t* bmask,
                                uint8_t* cmask);
 /* Stored blocks: local (this rank) and global. */
+/* Matrix with non-uniform block sizes (SPEC S:25-26 BlockDims: row_sizes / col_sizes, "non-uniform
+ * block sizes are supported throughout"; the paper's (m x k) A blocks and (k x n) B blocks, §II),
+ * reading R16: nblk_rows block rows of row_sizes[i] rows, nblk_cols block columns of col_sizes[j]
+ * columns (host arrays, copied; every size > 0), block-cyclic over the ctx grid by block index.
+ * mask (host, nblk_rows x nblk_cols row-major, nonzero = stored; NULL = every block) makes it
+ * block-sparse (R15).  The local arena holds the rank's stored blocks in local CSR order, each
+ * row_sizes[bi] x col_sizes[bj] column-major, back to back (dbm_matrix_local_info gives its bytes).
+ * All sizes equal: the uniform matrix of dbm_matrix_create / dbm_matrix_create_sparse.  A multiply
+ * needs equal block partitions: A's columns = B's rows (else DBM_ERR_PARTITION), A's rows = C's rows,
+ * B's columns = C's columns.  Non-uniform operands: Cannon over the copy-engine transport, the
+ * densified path for any sizes and patterns, the blocked path for dense patterns with C blocks up to
+ * 64 x 64 (DBM_ERR_SHAPE otherwise).  Errors: DBM_ERR_ARG (null pointers, bad counts), DBM_ERR_SHAPE
+ * (a size <= 0), DBM_ERR_NOMEM. */
+dbm_status dbm_matrix_create_blocked(dbm_ctx ctx, int64_t nblk_rows, const int32_t* row_sizes, int64_t nblk_cols,
+                                     const int32_t* col_sizes, const uint8_t* mask, dbm_matrix* out);
+/* The block sizes of a matrix (uniform matrices: bs everywhere); either output may be NULL. */
+dbm_status dbm_matrix_block_sizes(dbm_matrix m, int32_t* row_sizes, int32_t* col_sizes);
 dbm_status dbm_matrix_nnz(dbm_matrix m, int64_t* local_blocks, int64_t* global_blocks);
 /* Local share: mloc x nloc blocks; arena_bytes = (stored local blocks)*bs*bs*8 (mloc*nloc*bs*bs*8 dense). */
 dbm_status dbm_matrix_local_info(dbm_matrix m, int64_t* mloc_blocks, int64_t* nloc_blocks, int64_t* arena_bytes);

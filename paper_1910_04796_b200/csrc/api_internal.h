@@ -144,4 +144,10 @@ dbm_status sp_debug_stacks(dbm_ctx ctx, dbm_matrix A, dbm_matrix B, dbm_matrix C
                            int32_t* triplets, int64_t* n_entries, int64_t* stack_ptr, int64_t* n_stacks);
 void free_sp_cache(dbm_ctx ctx);
 
+// ---- non-uniform block sizes (multiply_nonuniform.cu, reading R16)
+dbm_status nu_workspace_bytes(dbm_ctx ctx, dbm_matrix A, dbm_matrix B, dbm_matrix C, bool dens, int64_t* bytes);
+dbm_status multiply_nonuniform(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_matrix B, double beta, dbm_matrix C,
+                               bool dens, void* workspace, int64_t ws_bytes, dbm_stats* stats);
+void free_nu_cache(dbm_ctx ctx);
+
 }  // namespace dbm

@@ -257,6 +257,7 @@ extern "C" dbm_status dbm_ctx_destroy(dbm_ctx ctx) {
   cudaStreamSynchronize(ctx->stream);
   cudaStreamSynchronize(ctx->comm);
   free_sp_cache(ctx);
+  free_nu_cache(ctx);
   for (auto& r : ctx->prof) {
     cudaEventDestroy(r.a);
     cudaEventDestroy(r.b);
@@ -383,6 +384,88 @@ extern "C" dbm_status dbm_matrix_create_sparse(dbm_ctx ctx, int64_t rows, int64_
   return DBM_OK;
 }
 
+// ---- non-uniform block sizes (reading R16) ----
+extern "C" dbm_status dbm_matrix_create_blocked(dbm_ctx ctx, int64_t nblk_rows, const int32_t* row_sizes,
+                                                int64_t nblk_cols, const int32_t* col_sizes, const uint8_t* mask,
+                                                dbm_matrix* out) {
+  ARG_CHECK(ctx && out, DBM_ERR_ARG, "null argument");
+  ARG_CHECK(nblk_rows >= 0 && nblk_cols >= 0 && nblk_rows < (1LL << 31) && nblk_cols < (1LL << 31), DBM_ERR_ARG,
+            "bad block counts");
+  ARG_CHECK((nblk_rows == 0 || row_sizes) && (nblk_cols == 0 || col_sizes), DBM_ERR_ARG, "null size list");
+  for (int64_t i = 0; i < nblk_rows; ++i) ARG_CHECK(row_sizes[i] > 0, DBM_ERR_SHAPE, "block sizes must be positive");
+  for (int64_t j = 0; j < nblk_cols; ++j) ARG_CHECK(col_sizes[j] > 0, DBM_ERR_SHAPE, "block sizes must be positive");
+  // all sizes equal: the uniform matrix (dense or sparse), which takes the uniform kernels
+  const int32_t s0 = nblk_rows ? row_sizes[0] : (nblk_cols ? col_sizes[0] : 1);
+  bool uni = true;
+  for (int64_t i = 0; i < nblk_rows; ++i) uni &= row_sizes[i] == s0;
+  for (int64_t j = 0; j < nblk_cols; ++j) uni &= col_sizes[j] == s0;
+  if (uni)
+    return mask ? dbm_matrix_create_sparse(ctx, nblk_rows * s0, nblk_cols * s0, s0, mask, out)
+                : dbm_matrix_create(ctx, nblk_rows * s0, nblk_cols * s0, s0, out);
+  dbm_matrix m = new dbm_matrix_s();
+  m->ctx = ctx;
+  m->nonuni = true;
+  m->bs = 0;  // no uniform block size
+  m->device = ctx->device;
+  m->Mb = nblk_rows;
+  m->Nb = nblk_cols;
+  m->rsz.assign(row_sizes, row_sizes + nblk_rows);
+  m->csz.assign(col_sizes, col_sizes + nblk_cols);
+  m->roff.assign(nblk_rows + 1, 0);
+  m->coff.assign(nblk_cols + 1, 0);
+  for (int64_t i = 0; i < nblk_rows; ++i) m->roff[i + 1] = m->roff[i] + row_sizes[i];
+  for (int64_t j = 0; j < nblk_cols; ++j) m->coff[j + 1] = m->coff[j] + col_sizes[j];
+  m->rows = m->roff.back();
+  m->cols = m->coff.back();
+  m->mloc = local_count(m->Mb, ctx->pr, ctx->myrow);
+  m->nloc = local_count(m->Nb, ctx->pc, ctx->mycol);
+  m->sparse = mask != nullptr;
+  if (m->sparse) {
+    m->gmask.resize((size_t)(m->Mb * m->Nb));
+    for (size_t i = 0; i < m->gmask.size(); ++i) m->gmask[i] = mask[i] ? 1 : 0;
+  }
+  m->gnnz = 0;
+  for (int64_t bi = 0; bi < m->Mb; ++bi)
+    for (int64_t bj = 0; bj < m->Nb; ++bj) m->gnnz += m->stored(bi, bj) ? 1 : 0;
+  m->row_ptr.assign(m->mloc + 1, 0);
+  m->slot_off.assign(1, 0);
+  for (int64_t li = 0; li < m->mloc; ++li) {
+    const int64_t bi = ctx->myrow + li * ctx->pr;
+    for (int64_t lj = 0; lj < m->nloc; ++lj) {
+      const int64_t bj = ctx->mycol + lj * ctx->pc;
+      if (!m->stored(bi, bj)) continue;
+      m->col.push_back((int32_t)lj);
+      m->hblk.push_back({m->slot_off.back(), m->roff[bi], m->coff[bj], m->rsz[bi], m->csz[bj]});
+      m->slot_off.push_back(m->slot_off.back() + (int64_t)m->rsz[bi] * m->csz[bj]);
+    }
+    m->row_ptr[li + 1] = (int64_t)m->col.size();
+  }
+  m->nnz = (int64_t)m->col.size();
+  m->serial = next_serial();
+  if (cudaError_t e = cudaSetDevice(ctx->device)) {
+    set_error(cudaGetErrorString(e));
+    delete m;
+    return DBM_ERR_CUDA;
+  }
+  cudaError_t e = cudaMalloc(&m->d_blk, std::max<size_t>(m->hblk.size(), 1) * sizeof(NUBlk));
+  if (e == cudaSuccess && !m->hblk.empty())
+    e = cudaMemcpy(m->d_blk, m->hblk.data(), m->hblk.size() * sizeof(NUBlk), cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) {
+    set_error(std::string("non-uniform block table: ") + cudaGetErrorString(e));
+    dbm_matrix_destroy(m);
+    return DBM_ERR_NOMEM;
+  }
+  *out = m;
+  return DBM_OK;
+}
+
+extern "C" dbm_status dbm_matrix_block_sizes(dbm_matrix m, int32_t* row_sizes, int32_t* col_sizes) {
+  ARG_CHECK(m, DBM_ERR_ARG, "null matrix");
+  for (int64_t i = 0; i < m->Mb && row_sizes; ++i) row_sizes[i] = m->row_size(i);
+  for (int64_t j = 0; j < m->Nb && col_sizes; ++j) col_sizes[j] = m->col_size(j);
+  return DBM_OK;
+}
+
 extern "C" dbm_status dbm_matrix_nnz(dbm_matrix m, int64_t* local_blocks, int64_t* global_blocks) {
   ARG_CHECK(m, DBM_ERR_ARG, "null matrix");
   if (local_blocks) *local_blocks = m->blocks();
@@ -394,7 +477,7 @@ extern "C" dbm_status dbm_matrix_local_info(dbm_matrix m, int64_t* mloc, int64_t
   ARG_CHECK(m, DBM_ERR_ARG, "null matrix");
   if (mloc) *mloc = m->mloc;
   if (nloc) *nloc = m->nloc;
-  if (bytes) *bytes = m->blocks() * (int64_t)m->bs * m->bs * 8;
+  if (bytes) *bytes = m->elems() * 8;
   return DBM_OK;
 }
 
@@ -417,7 +500,7 @@ extern "C" dbm_status dbm_matrix_local_csr(dbm_matrix m, int64_t* row_ptr, int64
 
 extern "C" dbm_status dbm_matrix_attach(dbm_matrix m, void* arena, int64_t bytes) {
   ARG_CHECK(m, DBM_ERR_ARG, "null matrix");
-  const int64_t need = m->blocks() * (int64_t)m->bs * m->bs * 8;
+  const int64_t need = m->elems() * 8;
   ARG_CHECK(bytes >= need, DBM_ERR_WORKSPACE, "arena smaller than dbm_matrix_local_info() bytes");
   ARG_CHECK(need == 0 || arena != nullptr, DBM_ERR_ARG, "null arena");
   ARG_CHECK(((uintptr_t)arena & 15) == 0, DBM_ERR_ARG, "arena must be 16-byte aligned");
@@ -427,7 +510,7 @@ extern "C" dbm_status dbm_matrix_attach(dbm_matrix m, void* arena, int64_t bytes
 }
 
 static dbm_status need_arena(dbm_matrix m) {
-  const int64_t need = m->blocks() * (int64_t)m->bs * m->bs * 8;
+  const int64_t need = m->elems() * 8;
   ARG_CHECK(need == 0 || m->arena, DBM_ERR_WORKSPACE, "matrix has no attached arena");
   return DBM_OK;
 }
@@ -438,7 +521,9 @@ extern "C" dbm_status dbm_matrix_fill_random(dbm_matrix m, uint64_t seed, uint32
   dbm_ctx ctx = m->ctx;
   CTX_OK(ctx);
   if (dbm_status s = need_arena(m)) return s;
-  if (m->sparse)
+  if (m->nonuni)
+    launch_nu_fill(m->arena, m->d_blk, m->blocks(), seed, mat_id, kind, ctx->stream);
+  else if (m->sparse)
     launch_fill_sparse(m->arena, m->nnz, m->d_ij, m->bs, ctx->pr, ctx->pc, ctx->myrow, ctx->mycol, seed, mat_id, kind,
                        ctx->stream);
   else
@@ -454,7 +539,11 @@ static dbm_status block_slot(dbm_matrix m, int64_t bi, int64_t bj, int64_t* slot
   const dbm_ctx c = m->ctx;
   ARG_CHECK(bi % c->pr == c->myrow && bj % c->pc == c->mycol, DBM_ERR_OWNERSHIP, "block owned by another rank");
   const int64_t li = bi / c->pr, lj = bj / c->pc;
-  if (!m->sparse) {
+  if (!m->sparse && !m->nonuni) {
+    *slot = li * m->nloc + lj;
+    return DBM_OK;
+  }
+  if (!m->sparse) {  // non-uniform, every block stored: CSR slots are li * nloc + lj
     *slot = li * m->nloc + lj;
     return DBM_OK;
   }
@@ -472,8 +561,9 @@ extern "C" dbm_status dbm_matrix_set_block(dbm_matrix m, int64_t bi, int64_t bj,
   int64_t slot;
   if (dbm_status s = block_slot(m, bi, bj, &slot)) return s;
   if (dbm_status s = need_arena(m)) return s;
-  const size_t bb = (size_t)m->bs * m->bs;
-  CUDA_TRY(ctx, cudaMemcpyAsync(m->arena + slot * bb, host, bb * 8, cudaMemcpyHostToDevice, ctx->stream));
+  const size_t bb = (size_t)m->row_size(bi) * m->col_size(bj);
+  const int64_t off = m->nonuni ? m->slot_off[slot] : slot * (int64_t)bb;
+  CUDA_TRY(ctx, cudaMemcpyAsync(m->arena + off, host, bb * 8, cudaMemcpyHostToDevice, ctx->stream));
   CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
   return DBM_OK;
 }
@@ -485,8 +575,9 @@ extern "C" dbm_status dbm_matrix_get_block(dbm_matrix m, int64_t bi, int64_t bj,
   int64_t slot;
   if (dbm_status s = block_slot(m, bi, bj, &slot)) return s;
   if (dbm_status s = need_arena(m)) return s;
-  const size_t bb = (size_t)m->bs * m->bs;
-  CUDA_TRY(ctx, cudaMemcpyAsync(host, m->arena + slot * bb, bb * 8, cudaMemcpyDeviceToHost, ctx->stream));
+  const size_t bb = (size_t)m->row_size(bi) * m->col_size(bj);
+  const int64_t off = m->nonuni ? m->slot_off[slot] : slot * (int64_t)bb;
+  CUDA_TRY(ctx, cudaMemcpyAsync(host, m->arena + off, bb * 8, cudaMemcpyDeviceToHost, ctx->stream));
   CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
   return DBM_OK;
 }
@@ -495,7 +586,7 @@ extern "C" dbm_status dbm_matrix_get_block(dbm_matrix m, int64_t bi, int64_t bj,
 // pinned double buffer (P:174 double buffering, P:200 page-locked memory pools).
 static dbm_status host_copy(dbm_matrix m, void* host, bool upload) {
   dbm_ctx ctx = m->ctx;
-  const size_t bytes = (size_t)m->blocks() * m->bs * m->bs * 8;
+  const size_t bytes = (size_t)m->elems() * 8;
   if (bytes == 0) return DBM_OK;
   cudaPointerAttributes at;
   bool pinned = cudaPointerGetAttributes(&at, host) == cudaSuccess &&
@@ -562,13 +653,14 @@ extern "C" dbm_status dbm_owner_of_block(dbm_matrix m, int64_t bi, int64_t bj, i
 }
 
 extern "C" dbm_status dbm_matrix_destroy(dbm_matrix m) {
-  if (m && (m->d_ij || m->d_map)) {
+  if (m && (m->d_ij || m->d_map || m->d_blk)) {
     // the context may already be destroyed: use the device recorded at creation, restore the caller's
     int cur = 0;
     cudaGetDevice(&cur);
     cudaSetDevice(m->device);
     if (m->d_ij) cudaFree(m->d_ij);
     if (m->d_map) cudaFree(m->d_map);
+    if (m->d_blk) cudaFree(m->d_blk);
     cudaSetDevice(cur);
     cudaGetLastError();
   }
@@ -577,12 +669,44 @@ extern "C" dbm_status dbm_matrix_destroy(dbm_matrix m) {
 }
 
 // ====================================================================== densify / undensify
+// Non-uniform blocks (R16): the local share's element rows / columns and one copy task per stored slot,
+// staged in stream-ordered device memory for one launch of the table-driven copy kernel.
+static dbm_status nu_local_copy(dbm_matrix m, double* dense, int64_t ld, int mode, double alpha, double beta) {
+  dbm_ctx ctx = m->ctx;
+  std::vector<int64_t> lro(m->mloc + 1, 0), lco(m->nloc + 1, 0);
+  for (int64_t li = 0; li < m->mloc; ++li) lro[li + 1] = lro[li] + m->row_size(ctx->myrow + li * ctx->pr);
+  for (int64_t lj = 0; lj < m->nloc; ++lj) lco[lj + 1] = lco[lj] + m->col_size(ctx->mycol + lj * ctx->pc);
+  const int64_t rows = lro.back(), cols = lco.back();
+  ARG_CHECK(ld >= (mode == 0 ? cols : rows), DBM_ERR_PLAN, "leading dimension too small");
+  ARG_CHECK(rows * cols == 0 || dense, DBM_ERR_ARG, "null dense buffer");
+  if (rows * cols == 0) return DBM_OK;
+  std::vector<NUTask> t;
+  for (int64_t li = 0; li < m->mloc; ++li)
+    for (int64_t q = m->row_ptr[li]; q < m->row_ptr[li + 1]; ++q) {
+      const int64_t lj = m->col[q];
+      t.push_back({m->slot_off[q], lro[li], lco[lj], m->hblk[q].rows, m->hblk[q].cols});
+    }
+  if (mode != 2 && m->sparse)  // absent blocks densify to zeros
+    CUDA_TRY(ctx, cudaMemsetAsync(dense, 0, (size_t)ld * (mode == 0 ? rows : cols) * 8, ctx->stream));
+  if (t.empty()) return DBM_OK;
+  NUTask* d = nullptr;
+  CUDA_TRY(ctx, cudaMallocAsync((void**)&d, t.size() * sizeof(NUTask), ctx->stream));
+  CUDA_TRY(ctx, cudaMemcpyAsync(d, t.data(), t.size() * sizeof(NUTask), cudaMemcpyHostToDevice, ctx->stream));
+  launch_nu_copy(d, (int64_t)t.size(), m->arena, dense, ld, mode, alpha, beta, ctx->stream);
+  CUDA_TRY(ctx, cudaGetLastError());
+  CUDA_TRY(ctx, cudaFreeAsync(d, ctx->stream));
+  CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));  // the pageable task vector must outlive the H2D copy
+  ctx->launches += 1;
+  return DBM_OK;
+}
+
 extern "C" dbm_status dbm_densify(dbm_matrix m, double* dense, int64_t ld, int layout) {
   ARG_CHECK(m, DBM_ERR_ARG, "null matrix");
   ARG_CHECK(layout == 0 || layout == 1, DBM_ERR_ARG, "layout must be 0 or 1");
   dbm_ctx ctx = m->ctx;
   CTX_OK(ctx);
   if (dbm_status s = need_arena(m)) return s;
+  if (m->nonuni) return nu_local_copy(m, dense, ld, layout == 0 ? 1 : 0, 0.0, 0.0);
   const int64_t rows = m->mloc * m->bs, cols = m->nloc * m->bs;
   ARG_CHECK(ld >= (layout == 0 ? rows : cols), DBM_ERR_PLAN, "leading dimension too small");
   ARG_CHECK(rows * cols == 0 || dense, DBM_ERR_ARG, "null dense buffer");
@@ -602,6 +726,7 @@ extern "C" dbm_status dbm_undensify(dbm_matrix m, const double* dense, int64_t l
   dbm_ctx ctx = m->ctx;
   CTX_OK(ctx);
   if (dbm_status s = need_arena(m)) return s;
+  if (m->nonuni) return nu_local_copy(m, (double*)dense, ld, 2, alpha, beta);
   const int64_t rows = m->mloc * m->bs, cols = m->nloc * m->bs;
   ARG_CHECK(ld >= rows, DBM_ERR_PLAN, "leading dimension too small");
   ARG_CHECK(rows * cols == 0 || dense, DBM_ERR_ARG, "null dense buffer");
@@ -881,13 +1006,23 @@ double pipeline_growth(double gemm_flop_per_kblock, double pull_bytes_per_kblock
 dbm_status validate(dbm_ctx ctx, dbm_matrix A, dbm_matrix B, dbm_matrix C) {
   ARG_CHECK(ctx && A && B && C, DBM_ERR_ARG, "null handle");
   ARG_CHECK(A->ctx == ctx && B->ctx == ctx && C->ctx == ctx, DBM_ERR_GRID, "matrices from a different context");
-  ARG_CHECK(A->bs == B->bs && A->bs == C->bs, DBM_ERR_PARTITION, "block sizes differ (K partition mismatch)");
   ARG_CHECK(A->cols == B->rows && A->rows == C->rows && B->cols == C->cols, DBM_ERR_SHAPE, "non-conformant shapes");
+  if (!A->nonuni && !B->nonuni && !C->nonuni) {
+    ARG_CHECK(A->bs == B->bs && A->bs == C->bs, DBM_ERR_PARTITION, "block sizes differ (K partition mismatch)");
+  } else {  // reading R16: the block partitions must agree, K (S:42 PartitionMismatch) and C's rows / columns
+    ARG_CHECK(A->Nb == B->Mb && A->Mb == C->Mb && B->Nb == C->Nb, DBM_ERR_PARTITION, "block partitions differ");
+    for (int64_t k = 0; k < A->Nb; ++k)
+      ARG_CHECK(A->col_size(k) == B->row_size(k), DBM_ERR_PARTITION, "K partition of A and B differs");
+    for (int64_t i = 0; i < A->Mb; ++i)
+      ARG_CHECK(A->row_size(i) == C->row_size(i), DBM_ERR_PARTITION, "row partition of A and C differs");
+    for (int64_t j = 0; j < B->Nb; ++j)
+      ARG_CHECK(B->col_size(j) == C->col_size(j), DBM_ERR_PARTITION, "column partition of B and C differs");
+  }
   ARG_CHECK(C != A && C != B, DBM_ERR_ALIAS, "C aliases A or B");
   auto overlap = [](dbm_matrix x, dbm_matrix y) {
     if (!x->arena || !y->arena) return false;
-    const char *a0 = (const char*)x->arena, *a1 = a0 + x->blocks() * x->bs * x->bs * 8;
-    const char *b0 = (const char*)y->arena, *b1 = b0 + y->blocks() * y->bs * y->bs * 8;
+    const char *a0 = (const char*)x->arena, *a1 = a0 + x->elems() * 8;
+    const char *b0 = (const char*)y->arena, *b1 = b0 + y->elems() * 8;
     return a0 < b1 && b0 < a1;
   };
   ARG_CHECK(!overlap(C, A) && !overlap(C, B), DBM_ERR_ALIAS, "C storage overlaps A or B");
@@ -1252,6 +1387,7 @@ extern "C" dbm_status dbm_multiply_workspace(dbm_ctx ctx, dbm_matrix A, dbm_matr
   ARG_CHECK(path == DBM_PATH_BLOCKED || path == DBM_PATH_DENSIFIED || path == DBM_PATH_AUTO, DBM_ERR_ARG, "bad path");
   if (dbm_status s = validate(ctx, A, B, C)) return s;
   path = resolve_path(ctx, A, B, path);
+  if (A->nonuni || B->nonuni || C->nonuni) return nu_workspace_bytes(ctx, A, B, C, path == DBM_PATH_DENSIFIED, bytes);
   if (path == DBM_PATH_BLOCKED && (A->sparse || B->sparse || C->sparse)) {
     return sp_workspace_bytes(ctx, A, B, C, bytes);
   }
@@ -1350,7 +1486,7 @@ extern "C" dbm_status dbm_multiply_host(dbm_ctx ctx, double alpha, dbm_matrix A,
   if (hio.a_ev) ctx->ev_pool.push_back(hio.a_ev);
   if (hio.c_ev) ctx->ev_pool.push_back(hio.c_ev);
   if (e) return e;
-  const size_t cbytes = (size_t)C->blocks() * C->bs * C->bs * 8;
+  const size_t cbytes = (size_t)C->elems() * 8;
   if (cbytes && !hio.c_downloaded)
     CUDA_TRY(ctx, cudaMemcpyAsync(C_host, C->arena, cbytes, cudaMemcpyDeviceToHost, ctx->stream));
   return DBM_OK;
@@ -1366,6 +1502,17 @@ dbm_status multiply_impl(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_matrix B, 
   if (dbm_status s = validate(ctx, A, B, C)) return s;
   path = resolve_path(ctx, A, B, path);
   const bool dens = path == DBM_PATH_DENSIFIED;
+  if (A->nonuni || B->nonuni || C->nonuni) {  // non-uniform block sizes (reading R16)
+    ARG_CHECK(ctx->transport == 0 && ctx->algorithm != 1, DBM_ERR_ARG,
+              "non-uniform blocks: Cannon over the copy-engine transport");
+    if (hio) {  // host operands: plain uploads ahead of the multiply on the compute stream
+      if (A->elems()) CUDA_TRY(ctx, cudaMemcpyAsync(A->arena, hio->A, A->elems() * 8, cudaMemcpyHostToDevice, ctx->stream));
+      if (B->elems()) CUDA_TRY(ctx, cudaMemcpyAsync(B->arena, hio->B, B->elems() * 8, cudaMemcpyHostToDevice, ctx->stream));
+      if (beta != 0.0 && C->elems())
+        CUDA_TRY(ctx, cudaMemcpyAsync(C->arena, hio->C, C->elems() * 8, cudaMemcpyHostToDevice, ctx->stream));
+    }
+    return multiply_nonuniform(ctx, alpha, A, B, beta, C, dens, workspace, ws_bytes, stats);
+  }
   if (!dens && (A->sparse || B->sparse || C->sparse)) {
     if (hio) {  // host operands: plain uploads ahead of the multiply on the compute stream
       const size_t bb8 = (size_t)A->bs * A->bs * 8;
@@ -2041,7 +2188,11 @@ extern "C" dbm_status dbm_debug_stacks(dbm_ctx ctx, dbm_matrix A, dbm_matrix B, 
   ARG_CHECK(n_entries && n_stacks, DBM_ERR_ARG, "null size outputs");
   if (A->sparse || B->sparse || C->sparse)
     return sp_debug_stacks(ctx, A, B, C, step, cap, triplets, n_entries, stack_ptr, n_stacks);
-  const Plan p = make_plan(ctx, A, B, C, false);
+  // (non-uniform blocks, R16: the same slot triplets -- the list depends on the block structure only)
+  const Plan p = A->nonuni || B->nonuni || C->nonuni
+                     ? make_plan_raw(ctx->nranks, ctx->pr, ctx->pc, ctx->myrow, ctx->mycol, A->Mb, B->Nb, A->Nb, 1,
+                                     false, ctx->chunk_bytes, ctx->transport)
+                     : make_plan(ctx, A, B, C, false);
   ARG_CHECK(step >= 0 && step < p.L, DBM_ERR_RANGE, "step out of range");
   const int64_t capv = cap ? cap : 30000;
   const int64_t kb = p.kb[p.kappa(step)], nruns = p.mloc * p.nloc, ne = nruns * kb;

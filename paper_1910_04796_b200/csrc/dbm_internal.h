@@ -146,6 +146,31 @@ cudaError_t launch_smm_tc(int bs, const int32_t* trip, int64_t nruns, int64_t kb
 int num_sms();
 
 struct SpCache;  // block-sparse multiply plans + device metadata (dbm_api.cu)
+
+// ---- non-uniform block sizes (kernels_nonuniform.cu, multiply_nonuniform.cu; reading R16) ----
+struct NUBlk {  // one stored local block: arena element offset, global element row / column, shape
+  int64_t off, r0, c0;
+  int32_t rows, cols;
+};
+struct NUTask {  // block <-> dense copy: block at arena element src, dense position (row0, col0)
+  int64_t src, row0, col0;
+  int32_t rows, cols;
+};
+struct NUPack {  // whole-block gather: n elements from src to dst (element offsets)
+  int64_t src, dst, n;
+};
+void launch_nu_fill(double* arena, const NUBlk* blk, int64_t nslots, uint64_t seed, uint32_t mat_id, int kind,
+                    cudaStream_t st);
+// mode 0: A block -> K-major rows dense[(row0+x)*ld + col0+y]; mode 1: B block -> K-major columns
+// dense[(col0+y)*ld + row0+x]; mode 2: C block = alpha*dense[(col0+y)*ld + row0+x] + beta*C block
+void launch_nu_copy(const NUTask* tasks, int64_t ntasks, double* arena, double* dense, int64_t ld, int mode,
+                    double alpha, double beta, cudaStream_t st);
+void launch_nu_pack(const NUPack* tasks, int64_t ntasks, const double* src, double* dst, cudaStream_t st);
+size_t nu_smm_smem(int kmax, int mmax, int nmax);
+cudaError_t launch_nu_smm(const int32_t* trip, int64_t nruns, int64_t kb, const double* A, const int64_t* aoff,
+                          const double* B, const int64_t* boff, const int32_t* kdim, double* C, const NUBlk* cblk,
+                          int kmax, int mmax, int nmax, double alpha, double beta_first, cudaStream_t st);
+struct NUCache;  // non-uniform multiply plans + device tables (multiply_nonuniform.cu)
 }  // namespace dbm
 
 // ----------------------------------------------------------------- handles
@@ -188,6 +213,7 @@ struct dbm_ctx_s {
   int* d_scratch = nullptr;               // device scratch: barrier word + handle exchange
   double densify_threshold = 1.0;         // DBM_PATH_AUTO: densify iff occupancy >= this
   std::vector<dbm::SpCache*> sp_cache;    // sparse plans keyed by the operands' pattern serials
+  std::vector<dbm::NUCache*> nu_cache;    // non-uniform plans keyed by the operands' serials
 };
 
 struct dbm_matrix_s {
@@ -209,6 +235,16 @@ struct dbm_matrix_s {
   int32_t* d_map = nullptr;       // device li*nloc + lj -> slot or -1 (sparse only; library-owned)
   uint64_t serial = 0;            // pattern identity (plan caches)
   int device = 0;                 // CUDA device of the metadata (sparse only)
+  // non-uniform block sizes (reading R16): global sizes, prefix offsets, per-slot element offsets
+  bool nonuni = false;
+  std::vector<int32_t> rsz, csz;      // block row / column sizes (Mb / Nb entries)
+  std::vector<int64_t> roff, coff;    // prefix sums (Mb + 1 / Nb + 1 entries)
+  std::vector<int64_t> slot_off;      // element offset of every stored local slot (blocks() + 1 entries)
+  std::vector<dbm::NUBlk> hblk;       // host copy of the per-slot table
+  dbm::NUBlk* d_blk = nullptr;        // device per-slot table (library-owned)
   int64_t blocks() const { return sparse ? nnz : mloc * nloc; }
+  int64_t elems() const { return nonuni ? slot_off.back() : blocks() * (int64_t)bs * bs; }
+  int32_t row_size(int64_t bi) const { return nonuni ? rsz[bi] : bs; }
+  int32_t col_size(int64_t bj) const { return nonuni ? csz[bj] : bs; }
   bool stored(int64_t bi, int64_t bj) const { return !sparse || gmask[(size_t)bi * Nb + bj]; }
 };

@@ -1,0 +1,237 @@
+// Kernels for matrices with non-uniform block sizes (SPEC S:25-26 row_sizes /
+// col_sizes; the paper's (m x k) A blocks times (k x n) B blocks, §II).  Reading R16
+// (DESIGN.md §3): a rank's arena holds its stored blocks in local CSR order, each column-major, back to
+// back; the host keeps every slot's element offset and shape (NUBlk).
+//
+//   nu_fill_kernel     the counter generator at global element coordinates
+//   nu_copy_kernel     block <-> dense panel copies from a task list: densify A (K-major rows), densify
+//                      B (K-major columns) and undensify C with alpha / beta (column-major)
+//   nu_pack_kernel     whole-block gathers into packed Cannon panels (blocked path)
+//   nu_smm_kernel      the blocked path's small-block products of mixed (m, n, k): one CTA per C-block
+//                      run, operands staged by cp.async into a 2-stage ring, FP64 DMMA (mma.sync
+//                      m8n8k4) on 8 x 8 subtiles with register predication for the ragged edges
+#include <algorithm>
+
+#include "dbm_internal.h"
+
+namespace dbm {
+
+namespace {
+
+__device__ __forceinline__ uint64_t nu_mix64(uint64_t z) {
+  z ^= z >> 30;
+  z *= 0xBF58476D1CE4E5B9ull;
+  z ^= z >> 27;
+  z *= 0x94D049BB133111EBull;
+  z ^= z >> 31;
+  return z;
+}
+
+__global__ void nu_fill_kernel(double* __restrict__ arena, const NUBlk* __restrict__ blk, int64_t nslots, uint64_t key,
+                               int kind) {
+  for (int64_t s = blockIdx.x; s < nslots; s += gridDim.x) {
+    const NUBlk b = blk[s];
+    const int64_t n = (int64_t)b.rows * b.cols;
+    for (int64_t e = threadIdx.x; e < n; e += blockDim.x) {
+      const int64_t y = e / b.rows, x = e - y * b.rows;
+      const uint64_t gi = (uint64_t)(b.r0 + x), gj = (uint64_t)(b.c0 + y);
+      const uint64_t bits = nu_mix64(key ^ nu_mix64((gi << 32) ^ gj));
+      double v;
+      if (kind == 1) {
+        v = (double)((int)((bits >> 32) % 5u) - 2);
+      } else {
+        const double u = __dmul_rn((double)(bits >> 11), 0x1.0p-53);
+        v = __dsub_rn(__dmul_rn(2.0, u), 1.0);
+      }
+      arena[b.off + e] = v;
+    }
+  }
+}
+
+// mode 0: A block (rows m x cols k) -> K-major rows: dense[(row0 + x) * ld + col0 + y]
+// mode 1: B block (rows k x cols n) -> K-major columns: dense[(col0 + y) * ld + row0 + x]
+// mode 2: C block <- column-major dense: blk = alpha * dense[(col0 + y) * ld + row0 + x] + beta * blk
+//         (two roundings, no FMA, as the uniform undensify; beta == 0: blk not read)
+__global__ void nu_copy_kernel(const NUTask* __restrict__ tasks, int64_t ntasks, double* __restrict__ arena,
+                               double* __restrict__ dense, int64_t ld, int mode, double alpha, double beta) {
+  for (int64_t t = blockIdx.x; t < ntasks; t += gridDim.x) {
+    const NUTask k = tasks[t];
+    const int64_t n = (int64_t)k.rows * k.cols;
+    for (int64_t e = threadIdx.x; e < n; e += blockDim.x) {
+      const int64_t y = e / k.rows, x = e - y * k.rows;
+      if (mode == 0) {
+        dense[(k.row0 + x) * ld + k.col0 + y] = arena[k.src + e];
+      } else if (mode == 1) {
+        dense[(k.col0 + y) * ld + k.row0 + x] = arena[k.src + e];
+      } else {
+        const double d = __dmul_rn(alpha, dense[(k.col0 + y) * ld + k.row0 + x]);
+        double* p = arena + k.src + e;
+        *p = beta == 0.0 ? d : __dadd_rn(d, __dmul_rn(beta, *p));
+      }
+    }
+  }
+}
+
+__global__ void nu_pack_kernel(const NUPack* __restrict__ tasks, int64_t ntasks, const double* __restrict__ src,
+                               double* __restrict__ dst) {
+  for (int64_t t = blockIdx.x; t < ntasks; t += gridDim.x) {
+    const NUPack k = tasks[t];
+    for (int64_t e = threadIdx.x; e < k.n; e += blockDim.x) dst[k.dst + e] = src[k.src + e];
+  }
+}
+
+__device__ __forceinline__ void nu_dmma(double (&c)[2], double a, double b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+      : "+d"(c[0]), "+d"(c[1])
+      : "d"(a), "d"(b));
+}
+
+constexpr int kNuWarps = 4;
+constexpr int kNuMaxSub = 16;  // subtiles per warp: C blocks up to 64 x 64 = 64 subtiles over 4 warps
+
+// One CTA per run (C block): acc(c) = sum over the run's entries of A_blk(a) (m x k) * B_blk(b) (k x n),
+// then C = (first ? beta*C : C) + alpha*acc.  Entry e's blocks are staged by cp.async (8 bytes per
+// element: any offset alignment) into stage e % 2 while entry e - 1 multiplies.  Shared layout per
+// stage: A as [k][mp] (mp = m rounded up to 8), B as [n][kp + 1] (kp = k_max rounded up to 4): the
+// DMMA fragment loads read A(row 8i + g, k 4ks + t) and B(k 4ks + t, col 8j + g).  Rows >= m, columns
+// >= n and k >= k_entry are zeroed in registers (predication), so the padding is never staged.
+__global__ void __launch_bounds__(kNuWarps * 32)
+    nu_smm_kernel(const int32_t* __restrict__ trip, int64_t nruns, int64_t kb, const double* __restrict__ A,
+                  const int64_t* __restrict__ aoff, const double* __restrict__ B, const int64_t* __restrict__ boff,
+                  const int32_t* __restrict__ kdim, double* __restrict__ C, const NUBlk* __restrict__ cblk,
+                  int kmax_pad, int mmax_pad, int nmax_pad, double alpha, double beta_first) {
+  extern __shared__ __align__(16) double nsm[];
+  const int a_st = kmax_pad * mmax_pad, b_pitch = kmax_pad + 1, b_st = nmax_pad * b_pitch;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+  for (int64_t run = blockIdx.x; run < nruns; run += gridDim.x) {
+    const int32_t* rt = trip + 3 * run * kb;
+    const NUBlk cb = cblk[rt[2]];
+    const int m = cb.rows, n = cb.cols, mp = (m + 7) & ~7;
+    const int sm_ = mp / 8, sn = (n + 7) / 8, nsub = sm_ * sn;
+    auto stage = [&](int64_t e, int buf) {  // entry e's A and B blocks -> stage buf
+      const int k = kdim[e];  // entries run kk = 0 .. kb-1 (dense pattern): entry e is panel k-block e
+      const double* a = A + aoff[rt[3 * e]];
+      const double* b = B + boff[rt[3 * e + 1]];
+      double* sa = nsm + buf * (a_st + b_st);
+      double* sb = sa + a_st;
+      for (int q = threadIdx.x; q < m * k; q += blockDim.x) {  // A(x, z) at z*m + x -> sa[z*mp + x]
+        const int z = q / m, x = q - z * m;
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"((uint32_t)__cvta_generic_to_shared(sa + z * mp + x)),
+                     "l"(a + q)
+                     : "memory");
+      }
+      for (int q = threadIdx.x; q < k * n; q += blockDim.x) {  // B(z, y) at y*k + z -> sb[y*b_pitch + z]
+        const int y = q / k, z = q - y * k;
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(
+                         (uint32_t)__cvta_generic_to_shared(sb + y * b_pitch + z)),
+                     "l"(b + q)
+                     : "memory");
+      }
+      asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    double acc[kNuMaxSub][2];
+#pragma unroll
+    for (int i = 0; i < kNuMaxSub; ++i) acc[i][0] = acc[i][1] = 0.0;
+    if (kb > 0) stage(0, 0);
+    for (int64_t e = 0; e < kb; ++e) {
+      if (e + 1 < kb) {
+        stage(e + 1, (int)((e + 1) & 1));
+        asm volatile("cp.async.wait_group 1;" ::: "memory");
+      } else {
+        asm volatile("cp.async.wait_group 0;" ::: "memory");
+      }
+      __syncthreads();
+      const int k = kdim[e];
+      const double* sa = nsm + (e & 1) * (a_st + b_st);
+      const double* sb = sa + a_st;
+#pragma unroll
+      for (int i = 0; i < kNuMaxSub; ++i) {
+        const int sub = warp + kNuWarps * i;
+        if (sub >= nsub) break;
+        const int im = sub % sm_, in = sub / sm_;
+        const int row = 8 * im + g, col = 8 * in + g;
+        const bool rok = row < m, cok = col < n;
+        for (int ks = 0; 4 * ks < k; ++ks) {
+          const int z = 4 * ks + t;
+          const double av = (rok && z < k) ? sa[z * mp + row] : 0.0;
+          const double bv = (cok && z < k) ? sb[col * b_pitch + z] : 0.0;
+          nu_dmma(acc[i], av, bv);
+        }
+      }
+      __syncthreads();  // stage e & 1 is refilled by entry e + 2
+    }
+    // epilogue: subtile (im, in), lane (g, t) holds C(8 im + g, 8 in + 2t + jj)
+#pragma unroll
+    for (int i = 0; i < kNuMaxSub; ++i) {
+      const int sub = warp + kNuWarps * i;
+      if (sub >= nsub) break;
+      const int im = sub % sm_, in = sub / sm_;
+      const int row = 8 * im + g;
+      if (row >= m) continue;
+#pragma unroll
+      for (int jj = 0; jj < 2; ++jj) {
+        const int col = 8 * in + 2 * t + jj;
+        if (col >= n) continue;
+        double* p = C + cb.off + (int64_t)col * m + row;
+        const double v = alpha * acc[i][jj];
+        *p = beta_first == 0.0 ? v : beta_first * *p + v;
+      }
+    }
+    __syncthreads();  // the next run's first stage reuses buffer 0
+  }
+}
+
+unsigned nu_grid(int64_t n) { return (unsigned)std::max<int64_t>(1, std::min<int64_t>(n, (int64_t)num_sms() * 16)); }
+
+}  // namespace
+
+void launch_nu_fill(double* arena, const NUBlk* blk, int64_t nslots, uint64_t seed, uint32_t mat_id, int kind,
+                    cudaStream_t st) {
+  if (nslots <= 0) return;
+  auto hmix = [](uint64_t z) {
+    z ^= z >> 30;
+    z *= 0xBF58476D1CE4E5B9ull;
+    z ^= z >> 27;
+    z *= 0x94D049BB133111EBull;
+    z ^= z >> 31;
+    return z;
+  };
+  const uint64_t key = hmix(seed + 0x9E3779B97F4A7C15ull * ((uint64_t)mat_id + 1ull));
+  nu_fill_kernel<<<nu_grid(nslots), 256, 0, st>>>(arena, blk, nslots, key, kind);
+}
+
+void launch_nu_copy(const NUTask* tasks, int64_t ntasks, double* arena, double* dense, int64_t ld, int mode,
+                    double alpha, double beta, cudaStream_t st) {
+  if (ntasks <= 0) return;
+  nu_copy_kernel<<<nu_grid(ntasks), 256, 0, st>>>(tasks, ntasks, arena, dense, ld, mode, alpha, beta);
+}
+
+void launch_nu_pack(const NUPack* tasks, int64_t ntasks, const double* src, double* dst, cudaStream_t st) {
+  if (ntasks <= 0) return;
+  nu_pack_kernel<<<nu_grid(ntasks), 256, 0, st>>>(tasks, ntasks, src, dst);
+}
+
+size_t nu_smm_smem(int kmax, int mmax, int nmax) {
+  const int kp = (kmax + 3) & ~3, mp = (mmax + 7) & ~7, np = (nmax + 7) & ~7;
+  return (size_t)2 * ((size_t)kp * mp + (size_t)np * (kp + 1)) * 8;
+}
+
+cudaError_t launch_nu_smm(const int32_t* trip, int64_t nruns, int64_t kb, const double* A, const int64_t* aoff,
+                          const double* B, const int64_t* boff, const int32_t* kdim, double* C, const NUBlk* cblk,
+                          int kmax, int mmax, int nmax, double alpha, double beta_first, cudaStream_t st) {
+  if (nruns <= 0 || kb <= 0) return cudaSuccess;
+  if (mmax > 64 || nmax > 64) return cudaErrorInvalidValue;  // the host checks: C blocks up to 64 x 64
+  const size_t smem = nu_smm_smem(kmax, mmax, nmax);
+  static size_t attr = 0;
+  if (smem > 48 * 1024 && smem > attr) {
+    cudaError_t e = cudaFuncSetAttribute(nu_smm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    attr = smem;
+  }
+  nu_smm_kernel<<<(unsigned)std::min<int64_t>(nruns, (int64_t)num_sms() * 32), kNuWarps * 32, smem, st>>>(
+      trip, nruns, kb, A, aoff, B, boff, kdim, C, cblk, (kmax + 3) & ~3, (mmax + 7) & ~7, (nmax + 7) & ~7, alpha,
+      beta_first);
+  return cudaGetLastError();
+}
+
+}  // namespace dbm

@@ -477,6 +477,8 @@ dbm_status multiply_sparse_blocked(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_
 // DBM_PATH_AUTO -> blocked / densified (should_densify)
 dbm_path resolve_path(dbm_ctx ctx, dbm_matrix A, dbm_matrix B, dbm_path path) {
   if (path != DBM_PATH_AUTO) return path;
+  // non-uniform block-sparse operands: the blocked path takes dense patterns only (reading R16)
+  if ((A->nonuni || B->nonuni) && (A->sparse || B->sparse)) return DBM_PATH_DENSIFIED;
   auto occ = [](dbm_matrix m) { return m->Mb * m->Nb ? (double)m->gnnz / (double)(m->Mb * m->Nb) : 1.0; };
   return (occ(A) >= ctx->densify_threshold && occ(B) >= ctx->densify_threshold) ? DBM_PATH_DENSIFIED
                                                                                 : DBM_PATH_BLOCKED;

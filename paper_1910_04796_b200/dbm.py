@@ -71,6 +71,8 @@ _SIGS = {
     "dbm_matrix_create": (C.c_int, [_P, _I64, _I64, C.c_int32, C.POINTER(_P)]),
     "dbm_matrix_create_sparse": (C.c_int, [_P, _I64, _I64, C.c_int32, _P, C.POINTER(_P)]),
     "dbm_pattern_random": (C.c_int, [C.c_uint64, C.c_uint32, _I64, _I64, C.c_double, _P]),
+    "dbm_matrix_create_blocked": (C.c_int, [_P, _I64, _P, _I64, _P, _P, C.POINTER(_P)]),
+    "dbm_matrix_block_sizes": (C.c_int, [_P, _P, _P]),
     "dbm_matrix_nnz": (C.c_int, [_P, C.POINTER(_I64), C.POINTER(_I64)]),
     "dbm_pattern_product": (C.c_int, [_I64, _I64, _I64, _P, _P, _P]),
     "dbm_ctx_set_densify_threshold": (C.c_int, [_P, C.c_double]),
@@ -271,11 +273,26 @@ class Matrix:
     mask (numpy (Mb, Nb), nonzero = stored) makes it block-sparse (dbm_matrix_create_sparse, R15)."""
 
     def __init__(self, ctx: Context, rows: int, cols: int, block_size: int, arena: torch.Tensor | None = None,
-                 mask=None, sparse: bool = False):
+                 mask=None, sparse: bool = False, row_sizes=None, col_sizes=None):
         lib = load()
         h = C.c_void_p()
         self.sparse = sparse or mask is not None
-        if self.sparse:
+        self.row_sizes = self.col_sizes = None
+        if row_sizes is not None:  # non-uniform block sizes (dbm_matrix_create_blocked, reading R16)
+            import numpy as np
+
+            rs = np.ascontiguousarray(row_sizes, dtype=np.int32)
+            cs = np.ascontiguousarray(col_sizes, dtype=np.int32)
+            mk = None
+            if mask is not None:
+                mk = np.ascontiguousarray(mask, dtype=np.uint8)
+                assert mk.size == rs.size * cs.size
+            _check(lib.dbm_matrix_create_blocked(ctx.h, rs.size, rs.ctypes.data, cs.size, cs.ctypes.data,
+                                                 mk.ctypes.data if mk is not None else None, C.byref(h)))
+            rows, cols = int(rs.sum()), int(cs.sum())
+            self.row_sizes, self.col_sizes = rs, cs
+            block_size = int(rs[0]) if (rs.size and (rs == rs[0]).all() and (cs == rs[0]).all()) else 0
+        elif self.sparse:
             import numpy as np
 
             mk = None
@@ -311,17 +328,22 @@ class Matrix:
         _check(load().dbm_matrix_local_csr(self.h, rp.ctypes.data, ci.ctypes.data, ri.ctypes.data))
         return rp, ci[: self.nnz], ri[: self.mloc]
 
+    def block_shape(self, bi: int, bj: int) -> tuple[int, int]:
+        if self.row_sizes is None:
+            return self.bs, self.bs
+        return int(self.row_sizes[bi]), int(self.col_sizes[bj])
+
     def set_block(self, bi: int, bj: int, block) -> None:
         import numpy as np
 
         b = np.asfortranarray(np.asarray(block, dtype=np.float64))
-        assert b.shape == (self.bs, self.bs)
+        assert b.shape == self.block_shape(bi, bj)
         _check(load().dbm_matrix_set_block(self.h, bi, bj, b.ctypes.data))
 
     def get_block(self, bi: int, bj: int):
         import numpy as np
 
-        b = np.empty((self.bs, self.bs), dtype=np.float64, order="F")
+        b = np.empty(self.block_shape(bi, bj), dtype=np.float64, order="F")
         _check(load().dbm_matrix_get_block(self.h, bi, bj, b.ctypes.data))
         return b
 
@@ -343,14 +365,21 @@ class Matrix:
         n = self.nnz * self.bs * self.bs
         return self.arena[:n]
 
+    def local_dims(self) -> tuple[int, int]:
+        """Element rows and columns of this rank's local share (sum of its block sizes)."""
+        if self.row_sizes is None:
+            return self.mloc * self.bs, self.nloc * self.bs
+        c = self.ctx
+        return int(self.row_sizes[c.myrow::c.pr].sum()), int(self.col_sizes[c.mycol::c.pc].sum())
+
     def densify(self, dense: torch.Tensor, ld: int | None = None, layout: int = 0) -> None:
         if ld is None:
-            ld = self.mloc * self.bs if layout == 0 else self.nloc * self.bs
+            ld = self.local_dims()[0] if layout == 0 else self.local_dims()[1]
         _check(load().dbm_densify(self.h, dense.data_ptr(), ld, layout))
 
     def undensify(self, dense: torch.Tensor, alpha: float = 1.0, beta: float = 0.0, ld: int | None = None) -> None:
         if ld is None:
-            ld = self.mloc * self.bs
+            ld = self.local_dims()[0]
         _check(load().dbm_undensify(self.h, dense.data_ptr(), ld, alpha, beta))
 
     def close(self) -> None:

@@ -44,8 +44,8 @@ CASE_TIMEOUT = float(os.environ.get("DBM_CASE_TIMEOUT", "120"))
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--groups", default="cannon,sparse,host,sweep",
-                    help="comma list of case groups: cannon, sparse, host, sweep")
+    ap.add_argument("--groups", default="cannon,sparse,host,sweep,nonuni",
+                    help="comma list of case groups: cannon, sparse, host, sweep, nonuni")
     ap.add_argument("--summary", default="", help="rank 0 writes a JSON summary here")
     args = ap.parse_args()
     groups = set(args.groups.split(","))
@@ -68,6 +68,10 @@ def main():
     if "host" in groups:
         f, n = host_cases(world, rank, dev, grids, HOST_SHAPES)
         summary["groups"]["host"] = {"cases": n, "failures": f}
+        failures += f
+    if "nonuni" in groups:
+        f, n, e = nonuni_cases(world, rank, dev, grids)
+        summary["groups"]["nonuni"] = {"cases": n, "failures": f, "max_err": e}
         failures += f
     if "sweep" in groups:
         f, n = host_cases(world, rank, dev, grids, sweep_shapes())
@@ -207,6 +211,55 @@ def host_cases(world, rank, dev, grids, shapes):
                       flush=True)
         ctx.close()
     return failures, ncases
+
+
+def nonuni_cases(world, rank, dev, grids):
+    """Non-uniform block sizes (reading R16) on every grid: both paths (densified also block-sparse),
+    float <= 1e-12 and integer bit-exact against orc_nu_multiply scattered to this rank."""
+    failures = ncases = 0
+    max_err = 0.0
+    mixes = [([5, 13, 23, 26, 13, 5, 32, 9, 22], [13, 26, 5, 23, 9, 32, 7], [23, 5, 26, 13, 32, 9, 5, 11, 4]),
+             ([22, 64, 22, 64, 22], [64, 22, 64, 22], [22, 22, 64, 64, 22, 64, 22])]
+    for pr, pc in grids:
+        ctx = dbm.Context.from_distributed(pr=pr, pc=pc)
+        r, c = ctx.myrow, ctx.mycol
+        for mi, (ms, ns, ks) in enumerate(mixes):
+            for path, sparse in (("densified", False), ("blocked", False), ("densified", True)):
+                masks = (orc.pattern_random(4, 0, len(ms), len(ks), 0.5), orc.pattern_random(4, 1, len(ks), len(ns), 0.5),
+                         orc.pattern_random(4, 2, len(ms), len(ns), 0.8)) if sparse else (None, None, None)
+                for kind in (0, 1):
+                    A = dbm.Matrix(ctx, 0, 0, 0, row_sizes=ms, col_sizes=ks, mask=masks[0])
+                    B = dbm.Matrix(ctx, 0, 0, 0, row_sizes=ks, col_sizes=ns, mask=masks[1])
+                    C = dbm.Matrix(ctx, 0, 0, 0, row_sizes=ms, col_sizes=ns, mask=masks[2])
+                    A.fill_random(SEED, 0, kind)
+                    B.fill_random(SEED, 1, kind)
+                    with Watchdog(CASE_TIMEOUT):
+                        for rep in range(2):  # second call: cached plan, the same exchange pool
+                            C.fill_random(SEED, 2, kind)
+                            dbm.multiply(ctx, 0.75, A, B, -1.25, C, path)
+                        torch.cuda.synchronize()
+                    got = C.arena.cpu().numpy()[: C.arena_bytes // 8]
+                    Ad = orc.fill_dense(SEED, 0, kind, sum(ms), sum(ks))
+                    Bd = orc.fill_dense(SEED, 1, kind, sum(ks), sum(ns))
+                    Cd = orc.fill_dense(SEED, 2, kind, sum(ms), sum(ns))
+                    ref = orc.nu_scatter(orc.nu_multiply(ms, ns, ks, 0.75, Ad, Bd, -1.25, Cd, *masks), ms, ns, pr, pc,
+                                         r, c, masks[2])
+                    if kind == 1:
+                        ok = np.array_equal(got, ref)
+                        err = float(np.abs(got - ref).max()) if ref.size else 0.0
+                    else:
+                        err = float(np.linalg.norm(got - ref) / max(np.linalg.norm(ref), 1e-300)) if ref.size else 0.0
+                        ok = err <= 1e-12
+                    flags = torch.tensor([0 if ok else 1], device=dev)
+                    dist.all_reduce(flags)
+                    ncases += 1
+                    max_err = max(max_err, err)
+                    failures += int(flags.item() > 0)
+                    if rank == 0 or not ok:
+                        print(json.dumps({"rank": rank, "grid": f"{pr}x{pc}", "nonuni": mi, "path": path,
+                                          "sparse": sparse, "kind": kind, "err": err, "ok": bool(ok)}), flush=True)
+        ctx.close()
+    return failures, ncases, max_err
 
 
 def sparse_recv_bytes(am, bm, bs, pr, pc, r, c):

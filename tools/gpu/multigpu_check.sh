@@ -19,7 +19,7 @@ run() {  # name seconds cmd...
 run bench_s352 150 $TR --master-port=29611 bench.py --gpus $N --config s352 --steps 3 --warmup 3
 run mp_host 600 env DBM_CASE_TIMEOUT=60 $TR --master-port=29612 tests/mp_worker.py --groups host,sweep \
     --summary gpurun_out/mg_${N}gpu_host_summary.json
-run mp_all 1500 env DBM_CASE_TIMEOUT=120 $TR --master-port=29613 tests/mp_worker.py --groups cannon,sparse,host \
+run mp_all 1500 env DBM_CASE_TIMEOUT=120 $TR --master-port=29613 tests/mp_worker.py --groups cannon,sparse,host,nonuni \
     --summary gpurun_out/mg_${N}gpu_all_summary.json
 for cfg in ${BENCH_CFGS:-sq64}; do
   run bench_$cfg 900 $TR --master-port=29614 bench.py --gpus $N --config $cfg --steps 3 --warmup 3 \

@@ -327,17 +327,8 @@ def main():
         traffic = json.load(open(tfile)).get("bytes_per_launch")
 
     if args.timeline:  # one more multiply with every record kept: the overlap of pulls and GEMMs
-        ctx.set_profiling(True)
-        dbm.multiply(ctx, alpha, A, B, beta, C, path, workspace=ws)
-        ctx.sync()
-        names = {dbm.K_DGEMM: "dgemm", dbm.K_SMM: "smm", dbm.K_DENSIFY: "densify", dbm.K_UNDENSIFY: "undensify",
-                 dbm.K_STACKGEN: "stackgen", dbm.K_EXCHANGE: "pull"}
-        tl = [{"kind": names.get(k, k), "start_ms": a, "end_ms": b} for k, a, b in ctx.profile_timeline()]
-        ctx.set_profiling(False)
-        for k in names:
-            ctx.profile_read(k)  # drop the records
-        with open(f"{args.timeline}.rank{rank}.json", "w") as fh:
-            json.dump({"rank": rank, "grid": f"{ctx.pr}x{ctx.pc}", "config": name, "records": tl}, fh, indent=0)
+        write_timeline(args, ctx, dbm, lambda: dbm.multiply(ctx, alpha, A, B, beta, C, path, workspace=ws),
+                       args.timeline, name)
 
     # ---------------- end to end through the public API with host buffers (pinned), rank-local shares
     e2e = None
@@ -407,6 +398,24 @@ def main():
         dist.destroy_process_group()
 
 
+def write_timeline(args, ctx, dbm, call, prefix, name=""):
+    """Run `call` once with profiling on; write its records (kind, start, end in ms, CUDA events on every
+    stream the library uses) to <prefix>.rank<r>.json."""
+    ctx.sync()
+    ctx.set_profiling(True)
+    call()
+    ctx.sync()
+    names = {dbm.K_DGEMM: "dgemm", dbm.K_SMM: "smm", dbm.K_DENSIFY: "densify", dbm.K_UNDENSIFY: "undensify",
+             dbm.K_STACKGEN: "stackgen", dbm.K_EXCHANGE: "pull"}
+    tl = [{"kind": names.get(k, k), "start_ms": a, "end_ms": b} for k, a, b in ctx.profile_timeline()]
+    ctx.set_profiling(False)
+    for k in names:
+        ctx.profile_read(k)  # drop the records
+    with open(f"{prefix}.rank{ctx.rank}.json", "w") as fh:
+        json.dump({"rank": ctx.rank, "grid": f"{ctx.pr}x{ctx.pc}", "config": name or args.config, "records": tl}, fh,
+                  indent=0)
+
+
 def run_e2e(args, ctx, dbm, torch, A, B, C, path, ws, stream, barrier, maxrank, flop):
     """Same metric through the public C-ABI call with HOST buffers (dbm_multiply_host): per step the H2D
     of A and B from pinned host memory (streamed in K-chunks under the GEMMs on one GPU), the multiply
@@ -437,6 +446,8 @@ def run_e2e(args, ctx, dbm, torch, A, B, C, path, ws, stream, barrier, maxrank, 
     e1.record(stream)
     barrier()
     ms = maxrank(e0.elapsed_time(e1)) / args.e2e_steps
+    if args.timeline:  # one more profiled host-operand multiply (uploads, own-panel chunks, pulls, GEMMs)
+        write_timeline(args, ctx, dbm, step, f"{args.timeline}.e2e")
     out = {"value": flop / (ms * 1e-3) / 1e12, "unit": "TFLOP/s", "h2d_bytes_per_step": A.arena_bytes + B.arena_bytes,
            "d2h_bytes_per_step": C.arena_bytes, "ms_per_step": ms, "steps": args.e2e_steps,
            "host_memory": "pinned" if pinned else "pageable (staged through libdbm's pinned double buffer)",

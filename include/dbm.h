@@ -75,6 +75,13 @@ typedef struct {
   int64_t gemm_launches;
   int64_t kernel_launches; /* all kernels this call launched */
   double flops;            /* 2*mloc*bs*nloc*bs*K_local + epilogue, this rank */
+  /* Device times (ms) of the call, filled by dbm_multiply_timing (the call returns before its work
+   * runs, so dbm_multiply leaves them 0): whole call on the ctx stream, densify / pack kernels, the
+   * local multiply (GEMMs, small-block kernels, stack generation), undensify, and the exposed remainder
+   * (ms_total minus the three phases: exchange waits, barriers and gaps not hidden under the rank's
+   * kernels; clamped at 0).  SURVEY §8(b) timing fields; "only the execution time of the
+   * multiplication part". */
+  double ms_total, ms_densify, ms_local, ms_comm_exposed, ms_undensify;
 } dbm_stats;
 
 const char* dbm_status_string(dbm_status s);
@@ -107,6 +114,10 @@ dbm_status dbm_ctx_sync(dbm_ctx ctx);
  * 4 = stack generation, 5 = the copy-engine panel pulls of one exchange step, timed on the comm
  * stream) and clears the records. bytes_out: algorithmic bytes (kernel 5: bytes received). */
 dbm_status dbm_ctx_set_profiling(dbm_ctx ctx, int on);
+/* Timing of the last dbm_multiply / dbm_multiply_host this ctx ran with profiling on: synchronises on
+ * it and fills st->ms_* (the other fields are left untouched).  Call before dbm_ctx_profile_read
+ * consumes that multiply's records.  DBM_ERR_ARG if no profiled multiply is pending. */
+dbm_status dbm_multiply_timing(dbm_ctx ctx, dbm_stats* st);
 dbm_status dbm_ctx_profile_read(dbm_ctx ctx, int kernel, double* ms_out, int64_t* launches_out, double* flops_out,
                                 double* bytes_out);
 /* Timeline of the pending profiling records (not consumed): for record i (enqueue order, at most

@@ -149,5 +149,6 @@ dbm_status nu_workspace_bytes(dbm_ctx ctx, dbm_matrix A, dbm_matrix B, dbm_matri
 dbm_status multiply_nonuniform(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_matrix B, double beta, dbm_matrix C,
                                bool dens, void* workspace, int64_t ws_bytes, dbm_stats* stats);
 void free_nu_cache(dbm_ctx ctx);
+dbm_status nu_tables(dbm_matrix m);  // per-slot offset / shape tables for a uniform matrix (R16 multiplies)
 
 }  // namespace dbm

@@ -111,6 +111,7 @@ extern "C" dbm_status dbm_ctx_create(int nranks, int rank, int pr, int pc, const
   cudaError_t e = cudaSetDevice(device);
   ctx->stream = (cudaStream_t)cuda_stream;  // NULL = the legacy default stream (torch's default)
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->comm, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->comm2, cudaStreamNonBlocking);
   if (e != cudaSuccess) {
     set_error(std::string("context CUDA setup: ") + cudaGetErrorString(e));
     delete ctx;
@@ -124,6 +125,7 @@ extern "C" dbm_status dbm_ctx_create(int nranks, int rank, int pr, int pc, const
     if (r != ncclSuccess) {
       set_error(std::string("ncclCommInitRank: ") + ncclGetErrorString(r));
       cudaStreamDestroy(ctx->comm);
+      cudaStreamDestroy(ctx->comm2);
       if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
       delete ctx;
       return DBM_ERR_NCCL;
@@ -158,7 +160,8 @@ extern "C" dbm_status dbm_ctx_set_stream(dbm_ctx ctx, void* stream) {
 extern "C" dbm_status dbm_ctx_sync(dbm_ctx ctx) {
   CTX_OK(ctx);
   CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
-  CUDA_TRY(ctx, cudaStreamSynchronize(ctx->comm));
+  for (cudaStream_t st : {ctx->comm, ctx->comm2, ctx->up, ctx->gen})
+    if (st) CUDA_TRY(ctx, cudaStreamSynchronize(st));
   if (ctx->nccl) {
     ncclResult_t ae;
     NCCL_TRY(ctx, ncclCommGetAsyncError((ncclComm_t)ctx->nccl, &ae));
@@ -195,6 +198,7 @@ extern "C" dbm_status dbm_ctx_profile_read(dbm_ctx ctx, int kernel, double* ms_o
     cudaEventDestroy(r.b);
   }
   ctx->prof.swap(keep);
+  ctx->lt_valid = false;  // the bracketed record range is gone
   if (ms_out) *ms_out = ms;
   if (launches_out) *launches_out = n;
   if (flops_out) *flops_out = fl;
@@ -255,7 +259,8 @@ extern "C" dbm_status dbm_ctx_destroy(dbm_ctx ctx) {
   if (!ctx) return DBM_OK;
   cudaSetDevice(ctx->device);
   cudaStreamSynchronize(ctx->stream);
-  cudaStreamSynchronize(ctx->comm);
+  for (cudaStream_t st : {ctx->comm, ctx->comm2, ctx->up, ctx->gen})
+    if (st) cudaStreamSynchronize(st);
   free_sp_cache(ctx);
   free_nu_cache(ctx);
   for (auto& r : ctx->prof) {
@@ -263,6 +268,8 @@ extern "C" dbm_status dbm_ctx_destroy(dbm_ctx ctx) {
     cudaEventDestroy(r.b);
   }
   for (auto e : ctx->ev_pool) cudaEventDestroy(e);
+  if (ctx->lt_a) cudaEventDestroy(ctx->lt_a);
+  if (ctx->lt_b) cudaEventDestroy(ctx->lt_b);
   for (int i = 0; i < 2; ++i) {
     if (ctx->stage[i]) cudaFreeHost(ctx->stage[i]);
     if (ctx->stage_ev[i]) cudaEventDestroy(ctx->stage_ev[i]);
@@ -273,6 +280,7 @@ extern "C" dbm_status dbm_ctx_destroy(dbm_ctx ctx) {
   if (ctx->xpool) cudaFree(ctx->xpool);
   if (ctx->nccl) ncclCommDestroy((ncclComm_t)ctx->nccl);
   cudaStreamDestroy(ctx->comm);
+  if (ctx->comm2) cudaStreamDestroy(ctx->comm2);
   if (ctx->up) cudaStreamDestroy(ctx->up);
   if (ctx->gen) cudaStreamDestroy(ctx->gen);
   if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
@@ -456,6 +464,34 @@ extern "C" dbm_status dbm_matrix_create_blocked(dbm_ctx ctx, int64_t nblk_rows, 
     return DBM_ERR_NOMEM;
   }
   *out = m;
+  return DBM_OK;
+}
+
+// A uniform matrix that meets non-uniform ones in a multiply gets the per-slot tables too (slot s at element
+// offset s * bs^2, CSR slot order for block-sparse patterns); built once, library-owned.
+dbm_status dbm::nu_tables(dbm_matrix m) {
+  if (m->nonuni || m->d_blk) return DBM_OK;
+  dbm_ctx ctx = m->ctx;
+  const int64_t bb = (int64_t)m->bs * m->bs;
+  m->slot_off.assign(1, 0);
+  m->hblk.clear();
+  for (int64_t li = 0; li < m->mloc; ++li) {
+    const int64_t bi = ctx->myrow + li * ctx->pr;
+    const int64_t q0 = m->sparse ? m->row_ptr[li] : li * m->nloc, q1 = m->sparse ? m->row_ptr[li + 1] : (li + 1) * m->nloc;
+    for (int64_t q = q0; q < q1; ++q) {
+      const int64_t lj = m->sparse ? m->col[q] : q - li * m->nloc, bj = ctx->mycol + lj * ctx->pc;
+      m->hblk.push_back({m->slot_off.back(), bi * m->bs, bj * m->bs, m->bs, m->bs});
+      m->slot_off.push_back(m->slot_off.back() + bb);
+    }
+  }
+  m->device = ctx->device;
+  cudaError_t e = cudaMalloc(&m->d_blk, std::max<size_t>(m->hblk.size(), 1) * sizeof(NUBlk));
+  if (e == cudaSuccess && !m->hblk.empty())
+    e = cudaMemcpy(m->d_blk, m->hblk.data(), m->hblk.size() * sizeof(NUBlk), cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) {
+    set_error(std::string("block table: ") + cudaGetErrorString(e));
+    return DBM_ERR_NOMEM;
+  }
   return DBM_OK;
 }
 
@@ -776,6 +812,9 @@ struct Plan {
   // densified bs 64 with a dense B: B is never densified -- the GEMM reads B's 64 x 64 blocks in place
   // (arena, or packed panels the peers pull), through a 4-D TMA view (§8f-3, zero-copy B)
   bool b_packed = false;
+  // densified bs 64 with a dense A: A is never densified either -- the GEMM reads A's 64 x 64 blocks in
+  // place through a 4-D TMA view (arena on one rank, packed own panels the peers pull on several)
+  bool a_packed = false;
   size_t off_pos = 0, off_sqflag = 0, off_sqids = 0, off_runsq = 0, off_runleft = 0, off_runflag = 0;
   size_t off_counts = 0, off_mtemp = 0, mtemp_bytes = 0;
   int64_t spart_runs = 0;                            // capacity: (split x runs) C blocks
@@ -804,9 +843,11 @@ struct Plan {
 
 // Host-only plan: depends on the grid, this rank's coordinates and the block counts (no CUDA).
 Plan make_plan_raw(int nranks, int pr, int pc, int r, int c, int64_t Mb, int64_t Nb, int64_t Kb, int64_t bs,
-                   bool densified, int64_t chunk_bytes, int transport, bool b_packed = false) {
+                   bool densified, int64_t chunk_bytes, int transport, bool b_packed = false,
+                   bool a_packed = false) {
   Plan p;
   p.b_packed = b_packed;
+  p.a_packed = a_packed;
   p.pr = pr;
   p.pc = pc;
   p.r = r;
@@ -848,7 +889,7 @@ Plan make_plan_raw(int nranks, int pr, int pc, int r, int c, int64_t Mb, int64_t
       p.chunk_kb = ck;
       p.nchunks = p.Kb > 0 ? (p.Kb + ck - 1) / ck : 1;
       const int64_t ld = round_up(ck * p.bs, 2);
-      p.off_ownA = take((size_t)M * ld * 8);
+      if (!a_packed) p.off_ownA = take((size_t)M * ld * 8);  // zero-copy A needs no dense A chunk
       if (!b_packed) p.off_ownB = take((size_t)N * ld * 8);  // zero-copy B needs no dense B chunk
       p.max_split = pick_splitk(M, N, std::min<int64_t>(ck, std::max<int64_t>(p.Kb, 1)) * p.bs, num_sms());
     } else {
@@ -944,11 +985,29 @@ bool use_tallskinny(dbm_ctx ctx, dbm_matrix A, dbm_matrix B, bool densified) {
   return A->cols >= 16 * std::max(A->rows, B->cols);
 }
 
+// DBM_STACKGEN_DBUF=0 generates every stack chunk on the compute stream (no overlap): an A/B switch.
+bool stackgen_dbuf() {
+  static const bool on = [] {
+    const char* e = getenv("DBM_STACKGEN_DBUF");
+    return !(e && *e == '0');
+  }();
+  return on;
+}
+
+// DBM_ZC_A=0 turns zero-copy A off (A densified as in round 1): an A/B switch for measurements.
+bool zero_copy_a() {
+  static const bool on = [] {
+    const char* e = getenv("DBM_ZC_A");
+    return !(e && *e == '0');
+  }();
+  return on;
+}
+
 Plan make_plan(dbm_ctx ctx, dbm_matrix A, dbm_matrix B, dbm_matrix C, bool densified) {
   (void)C;
+  const bool zc = densified && A->bs == 64 && !use_tallskinny(ctx, A, B, densified);
   return make_plan_raw(ctx->nranks, ctx->pr, ctx->pc, ctx->myrow, ctx->mycol, A->Mb, B->Nb, A->Nb, A->bs, densified,
-                       ctx->chunk_bytes, ctx->transport,
-                       densified && A->bs == 64 && !B->sparse && !use_tallskinny(ctx, A, B, densified));
+                       ctx->chunk_bytes, ctx->transport, zc && !B->sparse, zc && !A->sparse && zero_copy_a());
 }
 
 // One Cannon exchange step as a list of point-to-point operations (owner-pull, reading R5):
@@ -1293,14 +1352,33 @@ namespace {
 // Pull this rank's step-s panels from their owners' workspaces (peer plans give the offsets).
 // Host-operand pipeline (hp_epoch != 0): wait (on the comm stream) until the owner of op's panel has
 // published at least `need` K-blocks of it for this multiply into this rank's progress table.
+// A step's A and B pulls go on two streams (comm, comm2), so two copy engines move them concurrently; the
+// B stream forks from the comm stream's state and joins it again at the end of the step's posts.
+cudaStream_t pull_stream(dbm_ctx ctx, const XOp& op) { return op.operand == 1 ? ctx->comm2 : ctx->comm; }
+dbm_status fork_b(dbm_ctx ctx) {
+  cudaEvent_t e = get_event(ctx);
+  CUDA_TRY(ctx, cudaEventRecord(e, ctx->comm));
+  CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->comm2, e, 0));
+  ctx->ev_pool.push_back(e);
+  return DBM_OK;
+}
+dbm_status join_b(dbm_ctx ctx) {
+  cudaEvent_t e = get_event(ctx);
+  CUDA_TRY(ctx, cudaEventRecord(e, ctx->comm2));
+  CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->comm, e, 0));
+  ctx->ev_pool.push_back(e);
+  return DBM_OK;
+}
+
 dbm_status wait_panel(dbm_ctx ctx, const Plan& p, uint64_t hp_epoch, const XOp& op, int64_t need) {
   if (!hp_epoch || need <= 0) return DBM_OK;
-  return xwait_word(ctx, ctx->comm, xprog_word(ctx->nranks, p.L, op.peer, op.operand, op.kappa),
+  return xwait_word(ctx, pull_stream(ctx, op), xprog_word(ctx->nranks, p.L, op.peer, op.operand, op.kappa),
                     (hp_epoch << 32) | (uint64_t)need);
 }
 
 dbm_status post_pulls(dbm_ctx ctx, const Plan& p, const std::vector<Plan>& peer_plan, int s, char* ws, int bufA,
                       int bufB, int64_t* sent, int64_t* recv, uint64_t hp_epoch = 0) {
+  if (dbm_status e = fork_b(ctx)) return e;
   for (const XOp& op : exchange_ops(p, s)) {
     const size_t n = (size_t)op.bytes;
     if (op.send) {  // the peer pulls it; counted for the statistics
@@ -1312,10 +1390,12 @@ dbm_status post_pulls(dbm_ctx ctx, const Plan& p, const std::vector<Plan>& peer_
     const size_t src_off = op.operand == 0 ? q.ownA_off[op.kappa] : q.ownB_off[op.kappa];
     ARG_CHECK(src_off != SIZE_MAX && ctx->peer_ws[op.peer], DBM_ERR_PLAN, "peer panel not in its workspace");
     void* dst = ws + (op.operand == 0 ? p.off_recvA[bufA] : p.off_recvB[bufB]);
-    if (n) CUDA_TRY(ctx, cudaMemcpyAsync(dst, ctx->peer_ws[op.peer] + src_off, n, cudaMemcpyDeviceToDevice, ctx->comm));
+    if (n)
+      CUDA_TRY(ctx, cudaMemcpyAsync(dst, ctx->peer_ws[op.peer] + src_off, n, cudaMemcpyDeviceToDevice,
+                                    pull_stream(ctx, op)));
     *recv += (int64_t)n;
   }
-  return DBM_OK;
+  return join_b(ctx);
 }
 
 // K-chunk [k0, k1) (blocks) of this rank's step-s dense panels: one 2-D copy-engine pull per remote
@@ -1324,6 +1404,7 @@ dbm_status post_pulls(dbm_ctx ctx, const Plan& p, const std::vector<Plan>& peer_
 dbm_status post_pulls_chunk(dbm_ctx ctx, const Plan& p, const std::vector<Plan>& peer_plan, int s, char* ws, int bufA,
                             int bufB, int64_t k0, int64_t k1, bool count, int64_t* sent, int64_t* recv,
                             uint64_t hp_epoch = 0) {
+  if (dbm_status e = fork_b(ctx)) return e;
   for (const XOp& op : exchange_ops(p, s)) {
     if (op.send) {
       if (count) *sent += op.bytes;
@@ -1339,7 +1420,7 @@ dbm_status post_pulls_chunk(dbm_ctx ctx, const Plan& p, const std::vector<Plan>&
     const size_t bb8 = (size_t)p.bs * p.bs * 8;
     int64_t rows;
     size_t pitch, off, width;
-    if (p.densified && !(op.operand == 1 && p.b_packed)) {
+    if (p.densified && !(op.operand == 1 && p.b_packed) && !(op.operand == 0 && p.a_packed)) {
       rows = (op.operand == 0 ? p.mloc : p.nloc) * p.bs;
       pitch = (size_t)p.ld_panel(op.kappa) * 8;
       off = (size_t)(k0 * p.bs) * 8;
@@ -1357,10 +1438,11 @@ dbm_status post_pulls_chunk(dbm_ctx ctx, const Plan& p, const std::vector<Plan>&
     char* dst = ws + (op.operand == 0 ? p.off_recvA[bufA] : p.off_recvB[bufB]) + off;
     const char* src = ctx->peer_ws[op.peer] + src_off + off;
     if (rows && width)
-      CUDA_TRY(ctx, cudaMemcpy2DAsync(dst, pitch, src, pitch, width, rows, cudaMemcpyDeviceToDevice, ctx->comm));
+      CUDA_TRY(ctx, cudaMemcpy2DAsync(dst, pitch, src, pitch, width, rows, cudaMemcpyDeviceToDevice,
+                                      pull_stream(ctx, op)));
     if (count) *recv += op.bytes;
   }
-  return DBM_OK;
+  return join_b(ctx);
 }
 
 __global__ void scale_kernel(double* __restrict__ x, int64_t n, double beta) {
@@ -1447,10 +1529,57 @@ dbm_status multiply_impl(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_matrix B, 
                          HostIO* hio);
 }
 
+// Profiled multiplies are bracketed (dbm_multiply_timing): events on the ctx stream + the record range.
+struct TimingBracket {
+  dbm_ctx ctx;
+  bool on;
+  explicit TimingBracket(dbm_ctx c) : ctx(c), on(c && c->profiling && c->poisoned == DBM_OK) {
+    if (!on) return;
+    if (!ctx->lt_a) cudaEventCreate(&ctx->lt_a);
+    if (!ctx->lt_b) cudaEventCreate(&ctx->lt_b);
+    cudaEventRecord(ctx->lt_a, ctx->stream);
+    ctx->lt_first = ctx->prof.size();
+    ctx->lt_valid = false;
+  }
+  void done(dbm_status s) {
+    if (!on || s != DBM_OK) return;
+    cudaEventRecord(ctx->lt_b, ctx->stream);
+    ctx->lt_last = ctx->prof.size();
+    ctx->lt_valid = true;
+  }
+};
+
 extern "C" dbm_status dbm_multiply(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_matrix B, double beta, dbm_matrix C,
                                    dbm_path path, int32_t stack_cap, void* workspace, int64_t ws_bytes,
                                    dbm_stats* stats) {
-  return multiply_impl(ctx, alpha, A, B, beta, C, path, stack_cap, workspace, ws_bytes, stats, nullptr);
+  TimingBracket tb(ctx);
+  const dbm_status s = multiply_impl(ctx, alpha, A, B, beta, C, path, stack_cap, workspace, ws_bytes, stats, nullptr);
+  tb.done(s);
+  return s;
+}
+
+extern "C" dbm_status dbm_multiply_timing(dbm_ctx ctx, dbm_stats* st) {
+  CTX_OK(ctx);
+  ARG_CHECK(st, DBM_ERR_ARG, "null stats");
+  ARG_CHECK(ctx->lt_valid && ctx->prof.size() >= ctx->lt_last, DBM_ERR_ARG,
+            "no profiled multiply pending (dbm_ctx_set_profiling, and before dbm_ctx_profile_read)");
+  CUDA_TRY(ctx, cudaEventSynchronize(ctx->lt_b));
+  float t = 0;
+  CUDA_TRY(ctx, cudaEventElapsedTime(&t, ctx->lt_a, ctx->lt_b));
+  double ph[6] = {0, 0, 0, 0, 0, 0};
+  for (size_t i = ctx->lt_first; i < ctx->lt_last; ++i) {
+    const auto& r = ctx->prof[i];
+    CUDA_TRY(ctx, cudaEventSynchronize(r.b));
+    float d = 0;
+    CUDA_TRY(ctx, cudaEventElapsedTime(&d, r.a, r.b));
+    if (r.kind >= 0 && r.kind < 6) ph[r.kind] += d;
+  }
+  st->ms_total = t;
+  st->ms_densify = ph[2];
+  st->ms_local = ph[0] + ph[1] + ph[4];
+  st->ms_undensify = ph[3];
+  st->ms_comm_exposed = std::max(0.0, st->ms_total - st->ms_densify - st->ms_local - st->ms_undensify);
+  return DBM_OK;
 }
 
 extern "C" dbm_status dbm_multiply_host(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_matrix B, double beta,
@@ -1478,6 +1607,7 @@ extern "C" dbm_status dbm_multiply_host(dbm_ctx ctx, double alpha, dbm_matrix A,
   hio.A = (const double*)A_host;
   hio.B = (const double*)B_host;
   hio.C = (double*)C_host;
+  TimingBracket tb(ctx);
   dbm_status e = multiply_impl(ctx, alpha, A, B, beta, C, path, stack_cap, workspace, ws_bytes, stats, &hio);
   for (cudaEvent_t ev : hio.chunk_ev) ctx->ev_pool.push_back(ev);
   for (cudaEvent_t ev : hio.panel_ev) ctx->ev_pool.push_back(ev);
@@ -1489,6 +1619,7 @@ extern "C" dbm_status dbm_multiply_host(dbm_ctx ctx, double alpha, dbm_matrix A,
   const size_t cbytes = (size_t)C->elems() * 8;
   if (cbytes && !hio.c_downloaded)
     CUDA_TRY(ctx, cudaMemcpyAsync(C_host, C->arena, cbytes, cudaMemcpyDeviceToHost, ctx->stream));
+  tb.done(DBM_OK);
   return DBM_OK;
 }
 
@@ -1689,7 +1820,7 @@ dbm_status multiply_impl(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_matrix B, 
     size_t need = p.pool_total;
     for (int q = 0; q < ctx->nranks; ++q)
       need = std::max(need, make_plan_raw(ctx->nranks, p.pr, p.pc, q / p.pc, q % p.pc, p.Mb, p.Nb, p.Kb, p.bs, dens,
-                                          ctx->chunk_bytes, ctx->transport, p.b_packed).pool_total);
+                                          ctx->chunk_bytes, ctx->transport, p.b_packed, p.a_packed).pool_total);
     if (dbm_status e = xattach(ctx, need, cs)) return e;
     xp = ctx->xpool;
     ep = ++ctx->epoch;
@@ -1701,10 +1832,11 @@ dbm_status multiply_impl(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_matrix B, 
       if (p.ownA_off[k] != SIZE_MAX) {
         const int64_t col0 = (k - p.c) / p.pc, stride = p.L / p.pc;
         double* dst = (double*)(xp + p.ownA_off[k]);
-        if (dens) {
+        if (dens && !p.a_packed) {
           ProfScope ps(ctx, cs, 2, 0.0, 16.0 * M * p.kb[k] * bs);
           if (dbm_status e = densify_a(ctx, A, col0, stride, p.kb[k], dst, p.ld_panel(k), 1, cs)) return e;
-        } else {
+        } else {  // packed whole blocks (blocked path; densified bs 64: the GEMM reads them in place)
+          ProfScope ps(ctx, cs, 2, 0.0, 16.0 * M * p.kb[k] * bs);
           launch_pack_cols(A->arena, p.mloc, p.kA, (int)bs, col0, stride, p.kb[k], dst, cs);
         }
         launches += (M * p.kb[k]) ? 1 : 0;
@@ -1780,7 +1912,7 @@ dbm_status multiply_impl(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_matrix B, 
       if (p.ownA_off[k] != SIZE_MAX && M) {
         const int64_t col0 = (k - p.c) / p.pc, stride = p.L / p.pc;
         ProfScope ps(ctx, up, 2, 0.0, 16.0 * M * (q1 - q0) * bs);
-        if (dens) {
+        if (dens && !p.a_packed) {
           double* dst = (double*)(xp + p.ownA_off[k]) + q0 * bs;
           if (dbm_status e = densify_a(ctx, A, col0 + q0 * stride, stride, q1 - q0, dst, p.ld_panel(k), 1, up))
             return e;
@@ -1845,7 +1977,7 @@ dbm_status multiply_impl(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_matrix B, 
       for (int q = 0; q < ctx->nranks; ++q)
         if (q != ctx->rank)
           peer_plan[q] = make_plan_raw(ctx->nranks, p.pr, p.pc, q / p.pc, q % p.pc, p.Mb, p.Nb, p.Kb, p.bs, dens,
-                                       ctx->chunk_bytes, ctx->transport, p.b_packed);
+                                       ctx->chunk_bytes, ctx->transport, p.b_packed, p.a_packed);
       if (hpipe) {
         for (int j = 0; j < kHostPipeChunks; ++j) {
           if (dbm_status e = own_panels_chunk(j)) {
@@ -1941,17 +2073,23 @@ dbm_status multiply_impl(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_matrix B, 
           if (hio && hio->chunk_ev.size() > (size_t)ch + 1)  // chunk ch uploaded
             CUDA_TRY(ctx, cudaStreamWaitEvent(cs, hio->chunk_ev[ch + 1], 0));
           if (p.b_packed) Bd = B->arena + k0 * p.nloc * bb;  // B's blocks read in place (§8f-3)
-          {
-            ProfScope ps(ctx, cs, 2, 0.0, 16.0 * (M + (p.b_packed ? 0 : N)) * nk * bs);
-            if (dbm_status e = densify_a(ctx, A, k0, 1, nk, Ad, ld, 1, cs)) return e;
+          if (!p.a_packed || !p.b_packed) {
+            ProfScope ps(ctx, cs, 2, 0.0, 16.0 * ((p.a_packed ? 0 : M) + (p.b_packed ? 0 : N)) * nk * bs);
+            if (!p.a_packed)
+              if (dbm_status e = densify_a(ctx, A, k0, 1, nk, Ad, ld, 1, cs)) return e;
             if (!p.b_packed)
               if (dbm_status e = densify_b(ctx, B, k0, 1, nk, Bd, ld, 0, cs)) return e;
-            launches += p.b_packed ? 1 : 2;
+            launches += (p.a_packed ? 0 : 1) + (p.b_packed ? 0 : 1);
           }
           const int pans = (ch == nch - 1) ? npan : 1;
           for (int pn = 0; pn < pans; ++pn) {
             const int64_t li0 = p.mloc * pn / pans, li1 = p.mloc * (pn + 1) / pans, m0 = li0 * bs, mr = (li1 - li0) * bs;
             GemmArgs g{mr, N, nk * bs, Ad + m0 * ld, ld, Bd, ld, Cd + m0, M, 1.0, ch == 0 ? 0.0 : 1.0, 1, nullptr};
+            if (p.a_packed) {  // A's blocks read in place: block (li, kk) at slot li * kA + kk of the arena (§8f-3)
+              g.A = A->arena + (li0 * p.kA + k0) * bb;
+              g.a_blocks = 1;
+              g.a_blk_ld = p.kA;
+            }
             g.b_blocks = p.b_packed ? 1 : 0;
             g.splitk = std::min(pick_splitk(g.M, N, g.K, num_sms()), p.max_split);  // partial buffer bound
             g.partial = g.splitk > 1 ? (double*)(ws + p.off_part) : nullptr;
@@ -2003,6 +2141,11 @@ dbm_status multiply_impl(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_matrix B, 
             GemmArgs g{mr, N, (k1 - k0) * bs, Ap + m0 * ld + k0 * bs, ld,
                        p.b_packed ? Bp + k0 * p.nloc * bb : Bp + k0 * bs, ld, Cd + m0, M, 1.0,
                        (s == 0 && j == 0) ? 0.0 : 1.0, 1, nullptr};
+            if (p.a_packed) {  // packed A panel read in place: block (li, kk) at slot li * kb + kk (§8f-3)
+              g.A = Ap + (li0 * kbk + k0) * bb;
+              g.a_blocks = 1;
+              g.a_blk_ld = kbk;
+            }
             g.b_blocks = p.b_packed ? 1 : 0;
             g.splitk = std::min(pick_splitk(g.M, N, g.K, num_sms()), p.max_split);  // partial buffer bound
             g.partial = g.splitk > 1 ? (double*)(ws + p.off_part) : nullptr;
@@ -2065,7 +2208,7 @@ dbm_status multiply_impl(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_matrix B, 
         // two triplet buffers (several chunks): chunk c's stacks are generated on the generation stream
         // into buffer c % 2 once the multiply of chunk c - 2 released it, overlapping chunk c - 1's
         // multiply (the generation kernel's CTAs fit beside the persistent small-block kernel's)
-        const bool dbuf = p.off_trip2 != 0 && nruns > runs_per_chunk;
+        const bool dbuf = p.off_trip2 != 0 && nruns > runs_per_chunk && stackgen_dbuf();
         cudaEvent_t ev_free[2] = {nullptr, nullptr};
         if (dbuf) {
           if (!ctx->gen) CUDA_TRY(ctx, cudaStreamCreateWithFlags(&ctx->gen, cudaStreamNonBlocking));

@@ -79,6 +79,10 @@ struct GemmArgs {
   // b_blocks: B is not a dense K-major matrix but a panel of 64 x 64 column-major blocks, block (kk, lj)
   // at slot kk * ceil(N/64) + lj (a bs-64 arena / packed panel, read in place: no densify); ldb unused
   int b_blocks = 0;
+  // a_blocks: A is a panel of 64 x 64 column-major blocks, block (li, kk) at slot li * a_blk_ld + kk (a bs-64
+  // arena or packed panel, read in place through a 4-D TMA view: no densify; §8f-3 zero-copy A); lda unused
+  int a_blocks = 0;
+  int64_t a_blk_ld = 0;
 };
 // Returns cudaSuccess or an error (tensor-map encode failures map to cudaErrorInvalidValue).
 cudaError_t launch_dgemm(const GemmArgs& g, cudaStream_t st, int* launches);
@@ -179,6 +183,7 @@ struct dbm_ctx_s {
   cudaStream_t stream = nullptr;
   bool own_stream = false;
   cudaStream_t comm = nullptr;
+  cudaStream_t comm2 = nullptr;  // second pull stream: a step's B panel beside its A panel (two copy engines)
   cudaStream_t up = nullptr;  // host->device uploads of dbm_multiply_host on several ranks (lazy)
   cudaStream_t gen = nullptr; // stack generation of the next chunk beside the small-block GEMM (lazy)
   bool host_pipe = true;      // several ranks, host operands: chunked uploads gated by peer flags
@@ -193,6 +198,10 @@ struct dbm_ctx_s {
     double flops, bytes;
   };
   std::vector<ProfRec> prof;
+  // the last profiled multiply (dbm_multiply_timing): bracket events on the ctx stream, record range
+  cudaEvent_t lt_a = nullptr, lt_b = nullptr;
+  size_t lt_first = 0, lt_last = 0;
+  bool lt_valid = false;
   std::vector<cudaEvent_t> ev_pool;  // free events
   // pinned staging ring for pageable host copies
   void* stage[2] = {nullptr, nullptr};

@@ -82,7 +82,7 @@ __device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
       : "d"(a), "d"(b));
 }
 
-template <int BM, int BN>
+template <int BM, int BN, bool A_BLK>
 __global__ void __launch_bounds__(kThreads, 1)
     dgemm_tn_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M, int N,
                     int k_tiles_total, int k_tiles_per_split, int nsplit, int tiles_m, int tiles_n,
@@ -158,7 +158,14 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint32_t fb = su32(&full[stage]);
           mbar_expect_tx(fb, kStage);
           const uint32_t dst = su32(smem + stage * kStage);
-          tma_load_2d(dst, &tmA, (kt0 + kt) * BK, tm * BM, fb);
+          if (A_BLK) {  // A read in place from 64 x 64 blocks: 4 boxes of (16 m, 16 k) x BM/64 block rows
+            const int k = (kt0 + kt) * BK;
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+              tma_load_4d(dst + q * (BM / 64) * 2048, &tmA, 16 * q, k & 63, k >> 6, tm * (BM / 64), fb);
+          } else {
+            tma_load_2d(dst, &tmA, (kt0 + kt) * BK, tm * BM, fb);
+          }
           if (b_blocks) {  // B read in place from 64 x 64 blocks: (k in block, n in block, block col, block row)
             const int k = (kt0 + kt) * BK;
             tma_load_4d(dst + kStageA, &tmB, k & 63, 0, tn * (BN / 64), k >> 6, fb);
@@ -190,6 +197,13 @@ __global__ void __launch_bounds__(kThreads, 1)
   // k>>1 = ks + 4 (t>>1) with ks < 4, so ((k>>1) ^ g) = ks ^ G: the per-ks offsets are one XOR away from
   // two lane constants (cheaper than four live registers under the 168-register cap)
   const uint32_t G = (uint32_t)(g ^ (4 * (t >> 1))), kodd = (uint32_t)(t & 1) << 3;
+  // A_BLK: the A tile is 4 boxes q (m_in chunks of 16) of [BM/64 block rows][16 k][16 m] doubles, rows of
+  // 128 B swizzled by (row & 7) = (k & 7).  Element (m_local, k): li = m_local / 64, q = (m_local % 64) / 16,
+  // at q * (BM/64) * 2048 + (li * 16 + k) * 128 + ((((m % 16) >> 1) ^ (k & 7)) << 4) + ((m & 1) << 3).  With
+  // k = 2 ks + kt, kt = (t & 1) + 8 (t >> 1), the lane constants are the row base and the low m bits.
+  const int kt_a = (t & 1) + 8 * (t >> 1);
+  const int m_warp = wm * (BM / 2);  // a warp's first tile row: a multiple of 32
+  const uint32_t a_blk_row = (uint32_t)((m_warp >> 6) * 16 + kt_a) * 128u + (uint32_t)((g & 1) << 3);
 
   int stage = 0;
   uint32_t phase = 0;
@@ -215,7 +229,15 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t koff = ((G ^ (uint32_t)ks) << 4) | kodd;
       double a[MI], b[NI];
 #pragma unroll
-      for (int mi = 0; mi < MI; ++mi) a[mi] = lds64(sA + a_row + mi * 1024 + koff);
+      for (int mi = 0; mi < MI; ++mi) {
+        if (A_BLK) {
+          const int m_in = (m_warp & 63) + mi * 8;  // + g (in the lane constants)
+          const uint32_t x = (uint32_t)((((m_in & 15) >> 1) + (g >> 1)) ^ ((2 * ks + (t & 1)) & 7));
+          a[mi] = lds64(sA + (uint32_t)(m_in >> 4) * (BM / 64) * 2048u + a_blk_row + (uint32_t)(2 * ks) * 128u + (x << 4));
+        } else {
+          a[mi] = lds64(sA + a_row + mi * 1024 + koff);
+        }
+      }
 #pragma unroll
       for (int ni = 0; ni < NI; ++ni) b[ni] = lds64(sB + b_row + ni * 1024 + koff);
 #pragma unroll
@@ -349,6 +371,21 @@ bool make_block_b_map(CUtensorMap* tm, const double* base, int64_t nblk_n, int64
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// 4-D view of a panel of 64 x 64 column-major A blocks, block (li, kk) at slot li*blk_ld + kk: A(m, k) with
+// m = 64 li + m_in, k = 64 kk + k_in lives at ((li*blk_ld + kk)*64 + k_in)*64 + m_in.  Box {16 m, 16 k, 1,
+// bm/64 block rows}: a [bm/64][16 k][16 m] 128-B-swizzled tile per 16-row m chunk (4 chunks per stage).
+bool make_block_a_map(CUtensorMap* tm, const double* base, int64_t nblk_m, int64_t nblk_k, int64_t blk_ld, int bm) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[4] = {64, 64, (cuuint64_t)std::max<int64_t>(nblk_k, 1), (cuuint64_t)std::max<int64_t>(nblk_m, 1)};
+  cuuint64_t strides[3] = {64 * 8, 64 * 64 * 8, (cuuint64_t)std::max<int64_t>(blk_ld, 1) * 64 * 64 * 8};
+  cuuint32_t box[4] = {16, BK, 1, (cuuint32_t)(bm / 64)};
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  return fn(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, (void*)base, dims, strides, box, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 namespace {
 
 // Host planner: for each CTA tile shape, the split-K count that fills whole waves of `sms`
@@ -406,19 +443,20 @@ unsigned* wave_sync_counter() {
   return p;
 }
 
-template <int BM, int BN>
+template <int BM, int BN, bool A_BLK>
 cudaError_t launch_tile(const GemmArgs& g, int splitk, cudaStream_t st) {
   using T = Tile<BM, BN>;
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(dgemm_tn_kernel<BM, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e = cudaFuncSetAttribute(dgemm_tn_kernel<BM, BN, A_BLK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)T::kSmem);
     if (e != cudaSuccess) return e;
     attr = true;
   }
   CUtensorMap tmA, tmB;
   // A zero-K product still needs valid (never dereferenced) maps: point at a 1-column view.
-  if (!make_kmajor_map(&tmA, g.A, g.M, g.K, std::max<int64_t>(g.lda, 2), BM))
+  if (A_BLK ? !make_block_a_map(&tmA, g.A, (g.M + 63) / 64, (g.K + 63) / 64, g.a_blk_ld, BM)
+            : !make_kmajor_map(&tmA, g.A, g.M, g.K, std::max<int64_t>(g.lda, 2), BM))
     return cudaErrorInvalidValue;
   if (g.b_blocks ? !make_block_b_map(&tmB, g.B, (g.N + 63) / 64, (g.K + 63) / 64, BN)
                  : !make_kmajor_map(&tmB, g.B, g.N, g.K, std::max<int64_t>(g.ldb, 2), BN))
@@ -447,11 +485,11 @@ cudaError_t launch_tile(const GemmArgs& g, int splitk, cudaStream_t st) {
     at[0].val.cooperative = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, dgemm_tn_kernel<BM, BN>, tmA, tmB, (int)g.M, (int)g.N, ktiles,
+    return cudaLaunchKernelEx(&cfg, dgemm_tn_kernel<BM, BN, A_BLK>, tmA, tmB, (int)g.M, (int)g.N, ktiles,
                               std::max(per, 0), splitk, tiles_m, tiles_n, g.C, g.ldc, g.alpha, g.beta, partial, ws,
                               sync_kt, rounds, wave_slack(), g.b_blocks);
   }
-  dgemm_tn_kernel<BM, BN><<<grid, kThreads, T::kSmem, st>>>(tmA, tmB, (int)g.M, (int)g.N, ktiles, std::max(per, 0),
+  dgemm_tn_kernel<BM, BN, A_BLK><<<grid, kThreads, T::kSmem, st>>>(tmA, tmB, (int)g.M, (int)g.N, ktiles, std::max(per, 0),
                                                             splitk, tiles_m, tiles_n, g.C, g.ldc, g.alpha, g.beta,
                                                             partial, nullptr, 1, 0, 0, g.b_blocks);
   return cudaGetLastError();
@@ -463,14 +501,24 @@ cudaError_t launch_dgemm(const GemmArgs& g, cudaStream_t st, int* launches) {
   const GemmPlan pl = pick_gemm(g.M, g.N, g.K, num_sms());
   const int splitk = std::max(1, g.splitk);
   cudaError_t e;
-  if (pl.bm == 128 && pl.bn == 128)
-    e = launch_tile<128, 128>(g, splitk, st);
-  else if (pl.bm == 128)
-    e = launch_tile<128, 64>(g, splitk, st);
-  else if (pl.bn == 128)
-    e = launch_tile<64, 128>(g, splitk, st);
-  else
-    e = launch_tile<64, 64>(g, splitk, st);
+  if (g.a_blocks) {
+    if (pl.bm == 128 && pl.bn == 128)
+      e = launch_tile<128, 128, true>(g, splitk, st);
+    else if (pl.bm == 128)
+      e = launch_tile<128, 64, true>(g, splitk, st);
+    else if (pl.bn == 128)
+      e = launch_tile<64, 128, true>(g, splitk, st);
+    else
+      e = launch_tile<64, 64, true>(g, splitk, st);
+  } else if (pl.bm == 128 && pl.bn == 128) {
+    e = launch_tile<128, 128, false>(g, splitk, st);
+  } else if (pl.bm == 128) {
+    e = launch_tile<128, 64, false>(g, splitk, st);
+  } else if (pl.bn == 128) {
+    e = launch_tile<64, 128, false>(g, splitk, st);
+  } else {
+    e = launch_tile<64, 64, false>(g, splitk, st);
+  }
   if (launches) ++*launches;
   if (e != cudaSuccess) return e;
   if (splitk > 1) {

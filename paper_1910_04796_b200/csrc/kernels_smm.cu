@@ -564,12 +564,11 @@ __constant__ short kQRowIdx[88] = {0, 1, 8, 9, 2, 3, 10, 11, 4, 5, 12, 13, 6, 7,
 __constant__ short kQColOff[88] = {3872, 4004, 3960, 3916, 4048, 4180, 4136, 4092, 3938, 3894, 4026, 3982, 4114, 4070, 4202, 4158, 4852, 4984, 4940, 4896, 5028, 5160, 5116, 5072, 4918, 4874, 5006, 4962, 5094, 5050, 5182, 5138, 5832, 5964, 5920, 5876, 6008, 6140, 6096, 6052, 5898, 5854, 5986, 5942, 6074, 6030, 6162, 6118, 6812, 6944, 6900, 6856, 6988, 7120, 7076, 7032, 6878, 6834, 6966, 6922, 7054, 7010, 7142, 7098, 4224, 5204, 4312, 4268, 4290, 4246, 5226, 4334, 5292, 5248, 6228, 6184, 5270, 6250, 6206, 5314, 6272, 7252, 7208, 7164, 6294, 7274, 7230, 7186};
 __constant__ short kQColIdx[88] = {0, 6, 4, 2, 8, 14, 12, 10, 3, 1, 7, 5, 11, 9, 15, 13, 22, 28, 26, 24, 30, 36, 34, 32, 25, 23, 29, 27, 33, 31, 37, 35, 44, 50, 48, 46, 52, 58, 56, 54, 47, 45, 51, 49, 55, 53, 59, 57, 66, 72, 70, 68, 74, 80, 78, 76, 69, 67, 73, 71, 77, 75, 81, 79, 16, 38, 20, 18, 19, 17, 39, 21, 42, 40, 62, 60, 41, 63, 61, 43, 64, 86, 84, 82, 65, 87, 85, 83};
 
-// One stage (11 k-steps of 4): R x Cn subtiles, plus the centre subtile (5, 5) on the k-steps ks = CSEL
-// (mod 4) when CSEL >= 0 -- the four sub-partitions take turns on it, so every SMSP issues 30 x 11 + (2 or
-// 3) DMMAs per stage (balanced) instead of one SMSP carrying the whole centre (31 vs 30 per k-step).
-// Fragments are loaded with the tail predicate only when TAIL (the last stage of an odd kb holds one
-// k-block).
-template <int R, int Cn, int CSEL, bool TAIL>
+// One stage (11 k-steps of 4): R x Cn subtiles (+ the centre subtile for CENTRE), fragments loaded with the
+// tail predicate only when TAIL (the last stage of an odd kb holds one k-block).  (Splitting the centre's
+// k-steps over the four SMSPs balances their DMMA counts 30/30/30/31 -> 30.25 each, but needs a named-barrier
+// reduction and spills at the 168-register cap: measured 93.3 -> 79.9 % DMMA at 5,632^3, not kept.)
+template <int R, int Cn, bool CENTRE, bool TAIL>
 __device__ __forceinline__ void s22q_stage(uint32_t sb, int kvalid, int t, const uint32_t (&offA)[R],
                                            const uint32_t (&offB)[Cn], uint32_t offAc, uint32_t offBc,
                                            double (&acc)[R][Cn][2], double (&cacc)[2]) {
@@ -590,7 +589,7 @@ __device__ __forceinline__ void s22q_stage(uint32_t sb, int kvalid, int t, const
     for (int i = 0; i < R; ++i)
 #pragma unroll
       for (int j = 0; j < Cn; ++j) dmma(acc[i][j], a[i], b[j]);
-    if (CSEL >= 0 && (ks & 3) == CSEL) {
+    if (CENTRE) {
       const double ac = ok ? lds64(sb + offAc + ka) : 0.0;
       const double bc = ok ? lds64(sb + offBc + kbo) : 0.0;
       dmma(cacc, ac, bc);
@@ -598,13 +597,13 @@ __device__ __forceinline__ void s22q_stage(uint32_t sb, int kvalid, int t, const
   }
 }
 
-// One warp's rectangle of subtiles: rows [r0, r0+R), cols [c0, c0+Cn) of the 11 x 11 grid (+ a quarter
-// of the centre subtile's k-steps for CSEL >= 0: compile-time roles, so the k-loop carries no branch).
-template <int R, int Cn, int CSEL>
+// One warp's rectangle of subtiles: rows [r0, r0+R), cols [c0, c0+Cn) of the 11 x 11 grid (+ the centre
+// subtile (5, 5) for CENTRE, a compile-time role so the k-loop carries no branch).
+template <int R, int Cn, bool CENTRE>
 __device__ __forceinline__ void s22q_consume(uint64_t* full, uint64_t* empty, uint32_t sbase, int& stage,
                                              uint32_t& phase, int st0, int st1, int Krun, int r0, int c0, int g,
                                              int t, int lane, double* const (&s_dst)[4][4], bool raw, double alpha,
-                                             double beta_first, double* s_centre) {
+                                             double beta_first) {
   using namespace s22q;
   double acc[R][Cn][2], cacc[2] = {0.0, 0.0};
 #pragma unroll
@@ -623,9 +622,9 @@ __device__ __forceinline__ void s22q_consume(uint64_t* full, uint64_t* empty, ui
     mbar_wait((uint32_t)__cvta_generic_to_shared(&full[stage]), phase);
     const uint32_t sb = sbase + (uint32_t)(stage * STAGE) * 8u;
     if (st < full_end)
-      s22q_stage<R, Cn, CSEL, false>(sb, KS, t, offA, offB, offAc, offBc, acc, cacc);
+      s22q_stage<R, Cn, CENTRE, false>(sb, KS, t, offA, offB, offAc, offBc, acc, cacc);
     else
-      s22q_stage<R, Cn, CSEL, true>(sb, Krun - st * KS, t, offA, offB, offAc, offBc, acc, cacc);
+      s22q_stage<R, Cn, CENTRE, true>(sb, Krun - st * KS, t, offA, offB, offAc, offBc, acc, cacc);
     __syncwarp();
     if (lane == 0) mbar_arrive((uint32_t)__cvta_generic_to_shared(&empty[stage]));
     if (++stage == STAGES) {
@@ -654,23 +653,9 @@ __device__ __forceinline__ void s22q_consume(uint64_t* full, uint64_t* empty, ui
 #pragma unroll
       for (int jj = 0; jj < 2; ++jj) put(M, kQColIdx[(c0 + j) * 8 + 2 * t + jj], acc[i][j][jj]);
   }
-  if (CSEL >= 0) {
-    // the centre's four k-quarters, summed in the fixed order 0, 1, 2, 3 by the CSEL == 0 warp
-    // (deterministic); named barrier 1 joins the four centre warps only
-    s_centre[(CSEL * 32 + lane) * 2] = cacc[0];
-    s_centre[(CSEL * 32 + lane) * 2 + 1] = cacc[1];
-    asm volatile("bar.sync 1, 128;" ::: "memory");
-    if (CSEL == 0) {
+  if (CENTRE)
 #pragma unroll
-      for (int jj = 0; jj < 2; ++jj) {
-        double v = s_centre[lane * 2 + jj];
-#pragma unroll
-        for (int q = 1; q < 4; ++q) v += s_centre[(q * 32 + lane) * 2 + jj];
-        put(kQRowIdx[40 + g], kQColIdx[40 + 2 * t + jj], v);
-      }
-    }
-    asm volatile("bar.sync 1, 128;" ::: "memory");  // s_centre is reused by the next item
-  }
+    for (int jj = 0; jj < 2; ++jj) put(kQRowIdx[40 + g], kQColIdx[40 + 2 * t + jj], cacc[jj]);
 }
 
 __global__ void __launch_bounds__((s22q::WARPS + 1) * 32, 1)
@@ -685,7 +670,6 @@ __global__ void __launch_bounds__((s22q::WARPS + 1) * 32, 1)
   __shared__ __align__(8) uint64_t full[STAGES], empty[STAGES];
   __shared__ int s_rowrep[4], s_colrep[4];
   __shared__ double* s_dst[2][4][4];  // per item parity: the C (or split-K partial) block of square cell (ri, cj)
-  __shared__ double s_centre[4 * 32 * 2];  // the centre subtile's four k-quarter partials
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const bool producer = warp == WARPS;
@@ -701,7 +685,7 @@ __global__ void __launch_bounds__((s22q::WARPS + 1) * 32, 1)
   // barriers.  (The host never splits K below 64 stages, so every item has >= 1 stage.)
   const bool sync_items = nst / nsplit < STAGES + 1;
 
-  // pinwheel of the 11 x 11 subtiles around the centre (5, 5): warp 0 rows 0-4 x cols 0-5,
+  // pinwheel of the 11 x 11 subtiles around the centre (5, 5): warp 0 rows 0-4 x cols 0-5 (+ centre),
   // warp 1 rows 0-5 x cols 6-10, warp 2 rows 6-10 x cols 5-10, warp 3 rows 5-10 x cols 0-4
   // (two warps per sub-partition: sp = warp % 4 owns a rectangle, h = warp / 4 one half of it)
   const int sp = warp & 3, hh = warp >> 2;
@@ -774,25 +758,15 @@ __global__ void __launch_bounds__((s22q::WARPS + 1) * 32, 1)
           phase ^= 1;
         }
       }
+    } else if (sp == 0 && hh == 1) {  // the centre subtile rides with warp 4
+      s22q_consume<5, 3, true>(full, empty, sbase, stage, phase, st0, st1, Krun, r0, c0, g, t, lane, s_dst[par],
+                               partial != nullptr, alpha, beta_first);
+    } else if (tall) {
+      s22q_consume<5, 3, false>(full, empty, sbase, stage, phase, st0, st1, Krun, r0, c0, g, t, lane, s_dst[par],
+                                partial != nullptr, alpha, beta_first);
     } else {
-      // warps 0-3: their rectangle only; warps 4-7 (one per SMSP, sp = 0..3): their rectangle + the centre
-      // subtile on the k-steps ks = sp (mod 4)
-      const bool raw = partial != nullptr;
-#define S22Q(R_, C_, SEL_)                                                                                       \
-  s22q_consume<R_, C_, SEL_>(full, empty, sbase, stage, phase, st0, st1, Krun, r0, c0, g, t, lane, s_dst[par], raw, \
-                             alpha, beta_first, s_centre)
-      if (hh == 0) {
-        if (tall) S22Q(5, 3, -1); else S22Q(3, 5, -1);
-      } else if (sp == 0) {
-        S22Q(5, 3, 0);
-      } else if (sp == 1) {
-        S22Q(3, 5, 1);
-      } else if (sp == 2) {
-        S22Q(5, 3, 2);
-      } else {
-        S22Q(3, 5, 3);
-      }
-#undef S22Q
+      s22q_consume<3, 5, false>(full, empty, sbase, stage, phase, st0, st1, Krun, r0, c0, g, t, lane, s_dst[par],
+                                partial != nullptr, alpha, beta_first);
     }
     if (sync_items) __syncthreads();
   }

@@ -114,6 +114,8 @@ struct NUCache {
 namespace {
 
 dbm_status nu_cache_get(dbm_ctx ctx, dbm_matrix A, dbm_matrix B, dbm_matrix C, bool dens, NUCache** out) {
+  for (dbm_matrix m : {A, B, C})  // uniform operands beside non-uniform ones: per-slot tables
+    if (dbm_status e = nu_tables(m)) return e;
   for (NUCache* c : ctx->nu_cache)
     if (c->a_serial == A->serial && c->b_serial == B->serial && c->c_serial == C->serial && c->dens == dens) {
       *out = c;
@@ -280,7 +282,7 @@ dbm_status nu_cache_get(dbm_ctx ctx, dbm_matrix A, dbm_matrix B, dbm_matrix C, b
       for (int64_t lj = 0; lj < p.nloc; ++lj) {
         const int64_t s = slot_of(C, li, lj);
         if (s < 0) continue;
-        t.push_back({C->slot_off.empty() ? s * (int64_t)C->bs * C->bs : C->slot_off[s], p.lro[li], p.lco[lj],
+        t.push_back({C->slot_off[s], p.lro[li], p.lco[lj],
                      C->row_size(r + li * p.pr), C->col_size(c + lj * p.pc)});
       }
     nc->o_ctask = put(t.data(), t.size() * sizeof(NUTask));

@@ -36,7 +36,9 @@ class DbmError(RuntimeError):
 class Stats(C.Structure):
     _fields_ = [("entries", C.c_int64), ("stacks", C.c_int64), ("bytes_sent", C.c_int64),
                 ("bytes_recv", C.c_int64), ("steps", C.c_int64), ("gemm_launches", C.c_int64),
-                ("kernel_launches", C.c_int64), ("flops", C.c_double)]
+                ("kernel_launches", C.c_int64), ("flops", C.c_double), ("ms_total", C.c_double),
+                ("ms_densify", C.c_double), ("ms_local", C.c_double), ("ms_comm_exposed", C.c_double),
+                ("ms_undensify", C.c_double)]
 
     def as_dict(self) -> dict:
         return {f: getattr(self, f) for f, _ in self._fields_}
@@ -58,6 +60,7 @@ _SIGS = {
     "dbm_ctx_set_profiling": (C.c_int, [_P, C.c_int]),
     "dbm_ctx_profile_read": (C.c_int, [_P, C.c_int, C.POINTER(C.c_double), C.POINTER(_I64),
                                        C.POINTER(C.c_double), C.POINTER(C.c_double)]),
+    "dbm_multiply_timing": (C.c_int, [_P, C.POINTER(Stats)]),
     "dbm_ctx_profile_timeline": (C.c_int, [_P, C.c_int, _P, C.POINTER(C.c_int)]),
     "dbm_ctx_launch_count": (C.c_int, [_P, C.POINTER(_I64)]),
     "dbm_ctx_set_dense_chunk_bytes": (C.c_int, [_P, _I64]),
@@ -187,6 +190,13 @@ class Context:
         n = C.c_int64()
         _check(load().dbm_ctx_profile_read(self.h, kernel, C.byref(ms), C.byref(n), C.byref(fl), C.byref(by)))
         return {"ms": ms.value, "launches": n.value, "flops": fl.value, "bytes": by.value}
+
+    def multiply_timing(self) -> dict:
+        """dbm_multiply_timing: ms_total / ms_densify / ms_local / ms_comm_exposed / ms_undensify of the last
+        multiply run with profiling on."""
+        st = Stats()
+        _check(load().dbm_multiply_timing(self.h, C.byref(st)))
+        return {k: getattr(st, k) for k in ("ms_total", "ms_densify", "ms_local", "ms_comm_exposed", "ms_undensify")}
 
     def profile_timeline(self, max_records: int = 4096) -> list[tuple[int, float, float]]:
         """dbm_ctx_profile_timeline: (kind, start_ms, end_ms) of the pending profiling records."""

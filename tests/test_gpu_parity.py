@@ -437,3 +437,25 @@ def test_multiply_host_row_panels(dbm, ctx, orc, kind):
         assert np.array_equal(hs[2].numpy(), ref)
     else:
         assert relerr(hs[2].numpy(), ref) <= TOL
+
+
+@pytest.mark.parametrize("path", ["densified", "blocked"])
+def test_multiply_timing_fields(dbm, ctx, path):
+    """dbm_multiply_timing (the dbm_stats ms_* fields, SURVEY §8(b)): the call's device time and its phases;
+    the phases fit inside the call (kernels of one stream), the exposed remainder is what is left."""
+    A, B, C = dbm.Matrix(ctx, 704, 704, 22), dbm.Matrix(ctx, 704, 704, 22), dbm.Matrix(ctx, 704, 704, 22)
+    for m, i in ((A, 0), (B, 1), (C, 2)):
+        m.fill_random(SEED, i, 0)
+    ctx.set_profiling(True)
+    dbm.multiply(ctx, 1.0, A, B, 0.0, C, path)
+    t = ctx.multiply_timing()
+    ctx.set_profiling(False)
+    for k in range(6):
+        ctx.profile_read(k)
+    assert t["ms_total"] > 0 and t["ms_local"] > 0
+    assert t["ms_densify"] + t["ms_local"] + t["ms_undensify"] <= t["ms_total"] * 1.001 + 1e-3
+    assert t["ms_comm_exposed"] >= 0
+    if path == "densified":
+        assert t["ms_densify"] > 0 and t["ms_undensify"] > 0
+    with pytest.raises(dbm.DbmError):
+        ctx.multiply_timing()  # the records were consumed

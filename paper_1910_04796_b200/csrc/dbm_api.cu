@@ -841,6 +841,9 @@ struct Plan {
   }
 };
 
+bool stackgen_dbuf();
+bool zero_copy_a();
+
 // Host-only plan: depends on the grid, this rank's coordinates and the block counts (no CUDA).
 Plan make_plan_raw(int nranks, int pr, int pc, int r, int c, int64_t Mb, int64_t Nb, int64_t Kb, int64_t bs,
                    bool densified, int64_t chunk_bytes, int transport, bool b_packed = false,
@@ -928,7 +931,8 @@ Plan make_plan_raw(int nranks, int pr, int pc, int r, int c, int64_t Mb, int64_t
     p.off_trip = take((size_t)p.trip_cap * 12);
     // several stack chunks per step: a second triplet buffer, so chunk c+1 is generated (side stream)
     // while chunk c multiplies
-    if (runs < round_up(std::max<int64_t>(p.mloc * p.nloc, 1), 16)) p.off_trip2 = take((size_t)p.trip_cap * 12);
+    if (stackgen_dbuf() && runs < round_up(std::max<int64_t>(p.mloc * p.nloc, 1), 16))
+      p.off_trip2 = take((size_t)p.trip_cap * 12);
     // split-K partials of the smm kernel (rectangular shapes with few, long runs)
     const int64_t chunk_runs = std::max<int64_t>(1, std::min<int64_t>(p.mloc * p.nloc, p.trip_cap / maxkb));
     int64_t max_split = 1;
@@ -985,20 +989,24 @@ bool use_tallskinny(dbm_ctx ctx, dbm_matrix A, dbm_matrix B, bool densified) {
   return A->cols >= 16 * std::max(A->rows, B->cols);
 }
 
-// DBM_STACKGEN_DBUF=0 generates every stack chunk on the compute stream (no overlap): an A/B switch.
+// Opt-in variants, measured and not the default:
+// DBM_STACKGEN_DBUF=1 generates stack chunk c+1 on a side stream into a second triplet buffer while chunk c
+// multiplies (63,360^3 bs 22 blocked: 34.03 vs 34.03 TFLOP/s -- the overlap gains what the co-running
+// generation costs the small-block kernel -- for 6.4 GB more workspace);
 bool stackgen_dbuf() {
   static const bool on = [] {
     const char* e = getenv("DBM_STACKGEN_DBUF");
-    return !(e && *e == '0');
+    return e && *e == '1';
   }();
   return on;
 }
 
-// DBM_ZC_A=0 turns zero-copy A off (A densified as in round 1): an A/B switch for measurements.
+// DBM_ZC_A=1 reads bs-64 A blocks in place (zero-copy A): no A densify, but the M-major A tile's 2-way
+// conflicted fragment loads and 4 boxes per stage slow the GEMM by 5 % (63,360^3: 33.9 vs 35.6 TFLOP/s).
 bool zero_copy_a() {
   static const bool on = [] {
     const char* e = getenv("DBM_ZC_A");
-    return !(e && *e == '0');
+    return e && *e == '1';
   }();
   return on;
 }

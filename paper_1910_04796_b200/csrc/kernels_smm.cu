@@ -15,6 +15,7 @@
 // (22/24)^2 = 84% of the DMMA peak; bs 64 has none).  cp.async (16 B) stages operands in a 3-deep
 // ring; pitches are chosen so DMMA fragment loads are (near) conflict-free LDS.64.
 #include <algorithm>
+#include <cstdlib>
 
 #include <cub/device/device_select.cuh>
 #include <cub/iterator/counting_input_iterator.cuh>
@@ -661,7 +662,8 @@ __device__ __forceinline__ void s22q_consume(uint64_t* full, uint64_t* empty, ui
 __global__ void __launch_bounds__((s22q::WARPS + 1) * 32, 1)
     smm22q_kernel(const int32_t* __restrict__ trip, int64_t nruns, int64_t kb, const double* __restrict__ A,
                   const double* __restrict__ B, double* __restrict__ C, double alpha, double beta_first, int nsplit,
-                  double* __restrict__ partial, const int32_t* __restrict__ runs, const int* __restrict__ d_count) {
+                  double* __restrict__ partial, const int32_t* __restrict__ runs, const int* __restrict__ d_count,
+                  int centre_warp) {
   // runs != nullptr: squares are runs[16 s .. 16 s + 16) for s < *d_count / 16; otherwise runs 16 s ..
   using namespace s22q;
   if (d_count) nruns = *d_count;
@@ -740,16 +742,26 @@ __global__ void __launch_bounds__((s22q::WARPS + 1) * 32, 1)
       const bool owner = lane < 16;
       const int64_t q = RUN(q0 + (owner ? (isb ? s_colrep[u] : s_rowrep[u]) : 0));
       const double* base = isb ? B : A;
+      // the stage's block indices come from the stack list in global memory: load them two stages ahead,
+      // so the load latency overlaps the wait for a free stage instead of following it (ncu: the producer's
+      // dependent trip load was the refill's critical path, consumers waited on full stages 5 % of the time)
+      auto blk_of = [&](int st) -> int64_t {
+        const int kk = st * KK + j;
+        return (owner && st < st1 && kk < kb) ? (int64_t)trip[3 * (q * kb + kk) + isb] : 0;
+      };
+      int64_t blk0 = blk_of(st0), blk1 = blk_of(st0 + 1);
       for (int st = st0; st < st1; ++st) {
         const int kk = st * KK + j;
         const bool valid = owner && kk < kb;
+        const int64_t blk = blk0;
+        blk0 = blk1;
+        blk1 = blk_of(st + 2);
         const uint32_t fb = (uint32_t)__cvta_generic_to_shared(&full[stage]);
         if (lane == 0) mbar_wait((uint32_t)__cvta_generic_to_shared(&empty[stage]), phase ^ 1);
         const unsigned vm = __ballot_sync(0xffffffffu, valid);
         if (lane == 0) mbar_expect_tx(fb, (uint32_t)__popc(vm) * BLK_BYTES);
         __syncwarp();
         if (valid) {
-          const int64_t blk = trip[3 * (q * kb + kk) + isb];
           const int off = isb ? BOFF + u * SLOTB + j * KK1B : u * SLOT + j * BB;
           bulk_g2s(sbase + (uint32_t)(stage * STAGE + off) * 8u, base + blk * BB, BLK_BYTES, fb);
         }
@@ -758,8 +770,12 @@ __global__ void __launch_bounds__((s22q::WARPS + 1) * 32, 1)
           phase ^= 1;
         }
       }
-    } else if (sp == 0 && hh == 1) {  // the centre subtile rides with warp 4
+    } else if (warp == centre_warp && tall) {  // the centre subtile rides with one warp (default 5: SMSP 1,
+      // so SMSP 0, which also issues the producer warp, keeps 30 DMMAs per k-step)
       s22q_consume<5, 3, true>(full, empty, sbase, stage, phase, st0, st1, Krun, r0, c0, g, t, lane, s_dst[par],
+                               partial != nullptr, alpha, beta_first);
+    } else if (warp == centre_warp) {
+      s22q_consume<3, 5, true>(full, empty, sbase, stage, phase, st0, st1, Krun, r0, c0, g, t, lane, s_dst[par],
                                partial != nullptr, alpha, beta_first);
     } else if (tall) {
       s22q_consume<5, 3, false>(full, empty, sbase, stage, phase, st0, st1, Krun, r0, c0, g, t, lane, s_dst[par],
@@ -993,6 +1009,16 @@ cudaError_t launch_smm64(const int32_t* trip, int64_t nruns, int64_t kb, const d
   return cudaGetLastError();
 }
 
+// DBM_SMM22Q_CENTRE=<warp 0..7> picks the consumer warp that also computes the square's centre subtile.
+int smm22q_centre_warp() {
+  static const int w = [] {
+    const char* e = getenv("DBM_SMM22Q_CENTRE");
+    const int v = e ? atoi(e) : 5;
+    return v >= 0 && v < s22q::WARPS ? v : 5;
+  }();
+  return w;
+}
+
 cudaError_t launch_smm22q(const int32_t* trip, int64_t nruns, int64_t kb, const double* A, const double* B, double* C,
                           double alpha, double beta_first, int nsplit, double* partial, cudaStream_t st,
                           const int32_t* runs = nullptr, const int* d_count = nullptr) {
@@ -1006,7 +1032,7 @@ cudaError_t launch_smm22q(const int32_t* trip, int64_t nruns, int64_t kb, const 
   if (nsplit < 1 || !partial) nsplit = 1;
   const unsigned grid = (unsigned)std::min<int64_t>(ngroups * nsplit, (int64_t)num_sms());
   smm22q_kernel<<<grid, (s22q::WARPS + 1) * 32, s22q::SMEM, st>>>(trip, nruns, kb, A, B, C, alpha, beta_first, nsplit,
-                                                                  nsplit > 1 ? partial : nullptr, runs, d_count);
+                                                                  nsplit > 1 ? partial : nullptr, runs, d_count, smm22q_centre_warp());
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess || nsplit == 1) return e;
   const int64_t n = nruns * s22q::BB;

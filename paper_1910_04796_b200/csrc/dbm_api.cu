@@ -160,7 +160,7 @@ extern "C" dbm_status dbm_ctx_set_stream(dbm_ctx ctx, void* stream) {
 extern "C" dbm_status dbm_ctx_sync(dbm_ctx ctx) {
   CTX_OK(ctx);
   CUDA_TRY(ctx, cudaStreamSynchronize(ctx->stream));
-  for (cudaStream_t st : {ctx->comm, ctx->comm2, ctx->up, ctx->gen})
+  for (cudaStream_t st : {ctx->comm, ctx->comm2, ctx->up, ctx->gen, ctx->own})
     if (st) CUDA_TRY(ctx, cudaStreamSynchronize(st));
   if (ctx->nccl) {
     ncclResult_t ae;
@@ -259,7 +259,7 @@ extern "C" dbm_status dbm_ctx_destroy(dbm_ctx ctx) {
   if (!ctx) return DBM_OK;
   cudaSetDevice(ctx->device);
   cudaStreamSynchronize(ctx->stream);
-  for (cudaStream_t st : {ctx->comm, ctx->comm2, ctx->up, ctx->gen})
+  for (cudaStream_t st : {ctx->comm, ctx->comm2, ctx->up, ctx->gen, ctx->own})
     if (st) cudaStreamSynchronize(st);
   free_sp_cache(ctx);
   free_nu_cache(ctx);
@@ -283,6 +283,7 @@ extern "C" dbm_status dbm_ctx_destroy(dbm_ctx ctx) {
   if (ctx->comm2) cudaStreamDestroy(ctx->comm2);
   if (ctx->up) cudaStreamDestroy(ctx->up);
   if (ctx->gen) cudaStreamDestroy(ctx->gen);
+  if (ctx->own) cudaStreamDestroy(ctx->own);
   if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
   delete ctx;
   return DBM_OK;
@@ -1707,8 +1708,10 @@ dbm_status multiply_impl(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_matrix B, 
     CUDA_TRY(ctx, cudaEventRecord(e0, ctx->stream));  // previous work on the arenas is done
     hio->chunk_ev.push_back(e0);
     if (!ctx->up) CUDA_TRY(ctx, cudaStreamCreateWithFlags(&ctx->up, cudaStreamNonBlocking));
+    if (!ctx->own) CUDA_TRY(ctx, cudaStreamCreateWithFlags(&ctx->own, cudaStreamNonBlocking));
     cudaStream_t up = ctx->up;
     CUDA_TRY(ctx, cudaStreamWaitEvent(up, e0, 0));
+    CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->own, e0, 0));  // the own-panel stream starts after earlier work too
     const size_t bb8 = (size_t)p.bs * p.bs * 8;
     const size_t cbytes = beta != 0.0 ? (size_t)C->blocks() * bb8 : 0;
     if (!dens) {  // the blocked path accumulates into C from the first chunk on: C_in goes first
@@ -1897,8 +1900,10 @@ dbm_status multiply_impl(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_matrix B, 
   // so host calls that synchronise the device (lazy kernel loading, cudaFree, ...) cannot close a
   // cycle across ranks -- the round-1 hang was exactly that: flag waits enqueued, then a first kernel
   // launch loaded its module, synchronised, and waited forever on the peer doing the same.
-  std::vector<cudaEvent_t> own_ev;  // own panels' chunk j in place (upload stream)
-  cudaStream_t up = hpipe ? ctx->up : nullptr;
+  std::vector<cudaEvent_t> own_ev;  // own panels' chunk j in place (own-panel stream)
+  // own-panel stream: chunk j's densify / pack waits only for upload chunk j (the uploads stream on
+  // ctx->up back to back); it never waits on a peer, so its progress signals keep the ordering rule
+  cudaStream_t up = hpipe ? ctx->own : nullptr;
   auto publish = [&](int j, bool final_) -> dbm_status {
     // every peer's table entry [me][operand][k] = (epoch, K-blocks of my panel k now in place)
     for (int q = 0; q < ctx->nranks; ++q) {
@@ -1914,6 +1919,7 @@ dbm_status multiply_impl(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_matrix B, 
     return DBM_OK;
   };
   auto own_panels_chunk = [&](int j) -> dbm_status {
+    CUDA_TRY(ctx, cudaStreamWaitEvent(up, hio->up_ev[j], 0));  // upload chunk j landed
     for (int k = 0; k < p.L; ++k) {
       const int64_t q0 = host_pipe_bound(p.kb[k], j, hp_even), q1 = host_pipe_bound(p.kb[k], j + 1, hp_even);
       if (q1 <= q0) continue;

@@ -186,6 +186,7 @@ struct dbm_ctx_s {
   cudaStream_t comm2 = nullptr;  // second pull stream: a step's B panel beside its A panel (two copy engines)
   cudaStream_t up = nullptr;  // host->device uploads of dbm_multiply_host on several ranks (lazy)
   cudaStream_t gen = nullptr; // stack generation of the next chunk beside the small-block GEMM (lazy)
+  cudaStream_t own = nullptr; // host pipeline: own-panel densify / pack + progress signals (lazy)
   bool host_pipe = true;      // several ranks, host operands: chunked uploads gated by peer flags
   void* nccl = nullptr;  // ncclComm_t
   dbm_status poisoned = DBM_OK;

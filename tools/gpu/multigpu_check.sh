@@ -16,7 +16,9 @@ run() {  # name seconds cmd...
   local rc=$?
   echo "$name rc=$rc secs=$(( $(date +%s) - t0 ))" | tee -a $OUT
 }
-run nvlink_probe 120 python tools/microbench/nvlink_probe.py
+run nvlink_rate 120 python tools/microbench/nvlink_range.py
+run ncu_nvlink 600 /usr/local/cuda/bin/ncu --replay-mode app-range --profile-from-start off \
+    --metrics nvlrx__bytes.sum,nvltx__bytes.sum,gpu__time_duration.sum --csv python tools/microbench/nvlink_range.py
 run bench_s352 150 $TR --master-port=29611 bench.py --gpus $N --config s352 --steps 3 --warmup 3
 run mp_host 600 env DBM_CASE_TIMEOUT=60 $TR --master-port=29612 tests/mp_worker.py --groups host,sweep \
     --summary gpurun_out/mg_${N}gpu_host_summary.json

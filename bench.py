@@ -36,7 +36,20 @@ CONFIGS = {
     # stored; the metric counts only the stored block products (2 bs^3 per stack entry)
     "sp22": (63360, 63360, 63360, 22, "blocked", None),
     "sp64": (63360, 63360, 63360, 64, "blocked", None),
+    # non-uniform block sizes (§8f-2 / f4, reading R16; not a BASELINE config): every dimension cut into
+    # 1,000 blocks cycling through CP2K-like sizes 5, 13, 23, 26, 32 (19,800 elements)
+    "nu": (19800, 19800, 19800, 0, "densified", None),
 }
+NU_CYCLE = (5, 13, 23, 26, 32)
+
+
+def nu_sizes(total: int):
+    out, i = [], 0
+    while sum(out) < total:
+        out.append(NU_CYCLE[i % len(NU_CYCLE)])
+        i += 1
+    assert sum(out) == total
+    return out
 SPARSE_OCC = {"sp22": (0.1, 0.1, 1.0), "sp64": (0.1, 0.1, 1.0)}
 SEED = 1910
 FP64_PEAK_MEASURED = 37.15  # TFLOP/s per B200, DMMA m8n8k4 chain at 1965 MHz (profiles/r01_fp64_peaks.jsonl)
@@ -71,33 +84,6 @@ def parse():
     p.add_argument("--timeline", default="", help="write one profiled multiply's per-rank timeline "
                    "(kernels on every stream and the Cannon pulls, CUDA events) to <path>.rank<r>.json")
     return p.parse_args()
-
-
-# ------------------------------------------------------------------ NVLink byte counters (NVML)
-def nvlink_bytes(device: int):
-    """(rx, tx) bytes this GPU moved over NVLink so far (NVML field counters summed over the links), or
-    None.  Sampled around the timed region: the Cannon pulls are copy-engine transfers, which ncu's
-    kernel replay cannot attribute, so the device's own link counters are the evidence."""
-    try:
-        import pynvml
-
-        pynvml.nvmlInit()
-        h = pynvml.nvmlDeviceGetHandleByIndex(device)
-        for rx_id, tx_id, unit in ((pynvml.NVML_FI_DEV_NVLINK_COUNT_RCV_BYTES, pynvml.NVML_FI_DEV_NVLINK_COUNT_XMIT_BYTES, 1),
-                                   (pynvml.NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_RX,
-                                    pynvml.NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_TX, 1024)):
-            tot, ok = [0, 0], False
-            for link in range(18):  # NVLink 5 on B200: 18 links
-                vals = pynvml.nvmlDeviceGetFieldValues(h, [(rx_id, link), (tx_id, link)])
-                for i, v in enumerate(vals):
-                    if v.nvmlReturn == 0:
-                        tot[i] += int(v.value.ullVal) * unit
-                        ok = True
-            if ok:
-                return tot[0], tot[1]
-    except Exception:
-        return None
-    return None
 
 
 # ------------------------------------------------------------------ clocks during the timed region
@@ -185,6 +171,7 @@ def oracle_sample(M, N, K, bs, kpre: int, occ=None) -> dict:
 def oracle_kpre(M, N, K, bs, target_s: float, occ=None) -> int:
     """K prefix (whole blocks) that makes one 64-row sample take about target_s on this host: one short
     probe on the same rows, then linear scaling (the oracle's time is linear in the K prefix)."""
+    bs = bs or 1  # non-uniform blocks: the oracle's rows do not depend on the blocking
     probe_k = min(K, bs * max(1, -(-256 // bs)))
     t = oracle_sample(M, N, K, bs, probe_k, occ)["seconds"]
     k = int(probe_k * target_s / max(t, 1e-4)) // bs * bs
@@ -239,7 +226,8 @@ def main():
     name = {"s352": "352^3 bs22", "sq64": "square 63360^3 bs64", "sq22": "square 63360^3 bs22",
             "r64": "rect 1408x1408x1982464 bs64", "r22": "rect 1408x1408x1982464 bs22",
             "sp22": "square 63360^3 bs22 block-sparse A,B occupancy 0.1, C stored",
-            "sp64": "square 63360^3 bs64 block-sparse A,B occupancy 0.1, C stored"}[args.config]
+            "sp64": "square 63360^3 bs64 block-sparse A,B occupancy 0.1, C stored",
+            "nu": "square 19800^3 non-uniform blocks cycling 5,13,23,26,32"}[args.config]
     occ = SPARSE_OCC.get(args.config)
     name = f"{name} {path} " + (f"(BASELINE.json configs[{cidx}])" if cidx is not None else "(§8f-2 NEXT row)")
     if args.impl == "reference":
@@ -266,6 +254,11 @@ def main():
         A = dbm.Matrix(ctx, M, K, bs, mask=dbm.pattern_random(SEED, 0, Mb, Kb, occ[0]))
         B = dbm.Matrix(ctx, K, N, bs, mask=dbm.pattern_random(SEED, 1, Kb, Nb, occ[1]))
         C = dbm.Matrix(ctx, M, N, bs, mask=dbm.pattern_random(SEED, 2, Mb, Nb, occ[2]))
+    elif bs == 0:  # non-uniform block sizes
+        ms, ns, ks = nu_sizes(M), nu_sizes(N), nu_sizes(K)
+        A = dbm.Matrix(ctx, 0, 0, 0, row_sizes=ms, col_sizes=ks)
+        B = dbm.Matrix(ctx, 0, 0, 0, row_sizes=ks, col_sizes=ns)
+        C = dbm.Matrix(ctx, 0, 0, 0, row_sizes=ms, col_sizes=ns)
     else:
         A, B, C = dbm.Matrix(ctx, M, K, bs), dbm.Matrix(ctx, K, N, bs), dbm.Matrix(ctx, M, N, bs)
     A.fill_random(SEED, 0, 0)
@@ -292,15 +285,19 @@ def main():
     launches0 = ctx.launch_count()
     ctx.set_profiling(True)
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+    host_ms = []
     with ClockSampler(local) as clk:
         barrier()
-        nvl0 = nvlink_bytes(local) if world > 1 else None
         ev0.record(stream)
-        for _ in range(args.steps):
+        evs[0].record(stream)
+        for i in range(args.steps):
+            h0 = time.perf_counter()
             st = dbm.multiply(ctx, alpha, A, B, beta, C, path, workspace=ws)
+            host_ms.append((time.perf_counter() - h0) * 1e3)  # host enqueue time of the call
+            evs[i + 1].record(stream)
         ev1.record(stream)
         barrier()
-        nvl1 = nvlink_bytes(local) if world > 1 else None
     ctx.set_profiling(False)
     launches = ctx.launch_count() - launches0
     ms = maxrank(ev0.elapsed_time(ev1)) / args.steps
@@ -352,7 +349,8 @@ def main():
                        "grid": f"{ctx.pr}x{ctx.pc}", "parallelism": f"cannon{ctx.pr}x{ctx.pc}",
                        "transport": (args.transport if world > 1 else None),
                        "algorithm": (args.algorithm if world > 1 else "local"),
-                       "l2": ("inputs >= 8 GB per matrix >> 126 MB L2; no flush" if not occ else
+                       "l2": ("inputs 3.1 GB per matrix >> 126 MB L2; no flush" if bs == 0 else
+                              "inputs >= 8 GB per matrix >> 126 MB L2; no flush" if not occ else
                               "A, B 3.2 GB each (10 % of 32 GB) >> 126 MB L2; no flush"), "alpha": alpha, "beta": beta,
                        "occupancy": occ},
             "pct_fp64_peak": 100.0 * tflops / (world * FP64_PEAK_MEASURED),
@@ -379,14 +377,11 @@ def main():
                           "gbs": prof_x["bytes"] / (prof_x["ms"] * 1e-3) / 1e9 if prof_x["ms"] > 0 else None,
                           "uncovered_ms_per_step": ms - (prof["ms"] + prof_d["ms"] + prof_u["ms"] + prof_s["ms"])
                           / args.steps} if world > 1 else None),
-            # NVML link counters of rank 0's GPU over the timed region vs the pulls' algorithmic bytes
-            "nvlink": ({"rx_bytes_per_step": (nvl1[0] - nvl0[0]) / args.steps,
-                        "tx_bytes_per_step": (nvl1[1] - nvl0[1]) / args.steps,
-                        "algorithmic_recv_bytes_per_step": st["bytes_recv"],
-                        "algorithmic_sent_bytes_per_step": st["bytes_sent"],
-                        "rx_gbs_over_step": (nvl1[0] - nvl0[0]) / args.steps / (ms * 1e-3) / 1e9,
-                        "source": "NVML field counters (NVLINK_COUNT_RCV/XMIT_BYTES, all links)"}
-                       if (nvl0 and nvl1) else None),
+            # rank 0: device time of every timed step (CUDA events between the calls) and the host time each
+            # call took to enqueue (the call returns before its work runs; a host slower than the device
+            # would show as gaps between steps)
+            "steps_ms": [evs[i].elapsed_time(evs[i + 1]) for i in range(args.steps)],
+            "host_enqueue_ms": host_ms,
             "gpu_launches": launches,
             "clocks": clk.summary(),
             "e2e": e2e,
@@ -403,6 +398,7 @@ def write_timeline(args, ctx, dbm, call, prefix, name=""):
     stream the library uses) to <prefix>.rank<r>.json."""
     ctx.sync()
     ctx.set_profiling(True)
+    call()  # two calls back to back, as in the timed loop: the gap between them is part of the record
     call()
     ctx.sync()
     names = {dbm.K_DGEMM: "dgemm", dbm.K_SMM: "smm", dbm.K_DENSIFY: "densify", dbm.K_UNDENSIFY: "undensify",

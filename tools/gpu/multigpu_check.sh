@@ -17,14 +17,17 @@ run() {  # name seconds cmd...
   echo "$name rc=$rc secs=$(( $(date +%s) - t0 ))" | tee -a $OUT
 }
 run nvlink_rate 120 python tools/microbench/nvlink_range.py
-run ncu_nvlink 600 /usr/local/cuda/bin/ncu --replay-mode app-range --profile-from-start off \
+run ncu_nvlink 600 /usr/local/cuda/bin/ncu --replay-mode app-range \
     --metrics nvlrx__bytes.sum,nvltx__bytes.sum,gpu__time_duration.sum --csv python tools/microbench/nvlink_range.py
 run bench_s352 150 $TR --master-port=29611 bench.py --gpus $N --config s352 --steps 3 --warmup 3
 run mp_host 600 env DBM_CASE_TIMEOUT=60 $TR --master-port=29612 tests/mp_worker.py --groups host,sweep \
     --summary gpurun_out/mg_${N}gpu_host_summary.json
 run mp_all 1500 env DBM_CASE_TIMEOUT=120 $TR --master-port=29613 tests/mp_worker.py --groups cannon,sparse,host,nonuni \
     --summary gpurun_out/mg_${N}gpu_all_summary.json
-for cfg in ${BENCH_CFGS:-sq64}; do
-  run bench_$cfg 900 $TR --master-port=29614 bench.py --gpus $N --config $cfg --steps 3 --warmup 3 \
-      --timeline gpurun_out/mg_${N}gpu_timeline_$cfg
+# BENCH_SPECS: "cfg" or "name=bench args" (spaces in args as commas), e.g. "sq64 sq64nccl=--config,sq64,--transport,nccl"
+for spec in ${BENCH_SPECS:-${BENCH_CFGS:-sq64}}; do
+  name=${spec%%=*}
+  if [ "$name" = "$spec" ]; then args="--config $spec"; else args=$(echo "${spec#*=}" | tr ',' ' '); fi
+  run bench_$name 900 $TR --master-port=29614 bench.py --gpus $N $args --steps 3 --warmup 3 \
+      --timeline gpurun_out/mg_${N}gpu_timeline_$name
 done

@@ -3,7 +3,7 @@ copies, which ncu's kernel replay cannot attribute): GPU 0 pulls a 4 GiB panel f
 pitched copies, as dbm's pulls), alone and beside a persistent dbm GEMM on GPU 0, each inside a
 cudaProfilerStart/Stop range.
 
-    ncu --replay-mode app-range --profile-from-start off \
+    ncu --replay-mode app-range \
         --metrics nvlrx__bytes.sum,nvltx__bytes.sum,gpu__time_duration.sum --csv \
         python tools/microbench/nvlink_range.py
 Without ncu it prints the pull rates (CUDA events).
@@ -17,8 +17,24 @@ import torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 
 
+def cudart():
+    """The CUDA runtime torch loaded (for cudaMemcpyPeerAsync: a copy-engine peer copy; torch's own
+    cross-device copy_ may run as a kernel, which cannot start beside a persistent GEMM)."""
+    import ctypes
+    import glob
+
+    import nvidia.cuda_runtime as cr
+
+    lib = ctypes.CDLL(sorted(glob.glob(os.path.join(list(cr.__path__)[0], "lib", "libcudart.so*")))[0])
+    lib.cudaMemcpyPeerAsync.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p, ctypes.c_int, ctypes.c_size_t,
+                                        ctypes.c_void_p]
+    return lib
+
+
 def main():
     import paper_1910_04796_b200 as dbm
+
+    rt = cudart()
 
     n = 1 << 29  # 4 GiB of doubles
     torch.cuda.set_device(0)
@@ -41,10 +57,10 @@ def main():
         torch.cuda.profiler.start()
         if with_gemm:
             dbm.debug_dgemm(ctx, M, N, K, 1.0, At, K, Bt, K, 0.0, Cm, M)  # persistent GEMM, every SM
-        with torch.cuda.stream(side):
-            e0.record(side)
-            dst.copy_(src)  # peer copy on the copy engines, GPU 1 -> GPU 0 over NVLink
-            e1.record(side)
+        e0.record(side)
+        r = rt.cudaMemcpyPeerAsync(dst.data_ptr(), 0, src.data_ptr(), 1, n * 8, side.cuda_stream)
+        assert r == 0, r
+        e1.record(side)
         torch.cuda.synchronize(0)
         torch.cuda.profiler.stop()
         ms = e0.elapsed_time(e1)

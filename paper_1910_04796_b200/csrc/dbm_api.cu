@@ -844,6 +844,15 @@ struct Plan {
 
 bool stackgen_dbuf();
 bool zero_copy_a();
+// DBM_SMMQ=0 keeps the padded small sizes on the per-run kernel (the A/B of the R x R square kernel);
+// DBM_SMMQ=2 takes the squares even when they cannot fill the GPU (tests of small shapes)
+int smmq_on() {
+  static const int on = [] {
+    const char* e = getenv("DBM_SMMQ");
+    return e ? atoi(e) : 1;
+  }();
+  return on;
+}
 
 // Host-only plan: depends on the grid, this rank's coordinates and the block counts (no CUDA).
 Plan make_plan_raw(int nranks, int pr, int pc, int r, int c, int64_t Mb, int64_t Nb, int64_t Kb, int64_t bs,
@@ -2203,8 +2212,13 @@ dbm_status multiply_impl(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_matrix B, 
       const int64_t nruns = p.mloc * p.nloc;
       // a dense local grid the bisection visits as whole 4 x 4 squares runs the unpadded bs-22 kernel;
       // chunks of runs then hold whole squares
-      const bool squares = bs == 22 && bisection_squares(p.mloc, p.nloc);
-      const int64_t grp = squares ? 16 : smm_group_runs((int)bs);
+      // ... and the small padded sizes take R x R run squares (smmq) when the bisection visits them and
+      // there are enough squares to fill the GPU
+      const int qR = smmq_on() ? smmq_side((int)bs) : 0;
+      const bool squares = bs == 22 ? bisection_squares(p.mloc, p.nloc)
+                                    : (qR > 0 && bisection_squares(p.mloc, p.nloc, qR) &&
+                                       (smmq_on() == 2 || nruns / ((int64_t)qR * qR) >= num_sms()));
+      const int64_t grp = squares ? (bs == 22 ? 16 : (int64_t)qR * qR) : smm_group_runs((int)bs);
       const int64_t runs_per_chunk = std::max<int64_t>(grp, p.trip_cap / kbk / grp * grp);
       const int64_t a_ld = kbk;  // A panel is mloc x kb blocks, row-major over (li, kk)
       // step 0 with a chunked pull: each K-chunk [k0, k1) of the panels multiplies as soon as it landed

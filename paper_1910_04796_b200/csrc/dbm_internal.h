@@ -133,7 +133,11 @@ cudaError_t launch_smm22_mixed(const int32_t* trip, int64_t q0, int64_t nruns, i
                                cudaStream_t st, int* launches);
 // True when the bisection traversal of an mloc x nloc grid (reading R6) visits it as whole 4 x 4 squares
 // of 16 consecutive runs (both sides keep halving evenly down to 4).
-bool bisection_squares(int64_t mloc, int64_t nloc);
+bool bisection_squares(int64_t mloc, int64_t nloc, int64_t side = 4);
+// smmq (kernels_smmq.cu): R x R run squares for the padded small sizes (bs 4, 5, 6, 9); R (0: none)
+int smmq_side(int bs);
+cudaError_t launch_smmq(int bs, const int32_t* trip, int64_t nruns, int64_t kb, const double* A, const double* B,
+                        double* C, double alpha, double beta_first, cudaStream_t st);
 // DMMA group kernel for bs 22 / 64 (kernels_smm.cu); the generic smm handles other block sizes.
 bool smm_has_tensor_path(int bs);
 // DMMA per-run kernel for other compiled block sizes (kernels_sparse.cu); off == nullptr: uniform runs of kb

@@ -1166,11 +1166,11 @@ int smm_group_runs(int bs) { return bs == 22 ? s22::RUNS : (bs == 64 ? Cfg64::RU
 
 // Split the runs' K across CTAs when the groups alone cannot fill the GPU (long, few runs: the
 // rectangular configs on several GPUs).  Returns 1 when no split is needed.
-bool bisection_squares(int64_t mloc, int64_t nloc) {
-  if (mloc == 4 && nloc == 4) return true;
-  if (mloc < 4 || nloc < 4) return false;
-  if (mloc >= nloc) return mloc % 2 == 0 && bisection_squares(mloc / 2, nloc);  // rows split on ties
-  return nloc % 2 == 0 && bisection_squares(mloc, nloc / 2);
+bool bisection_squares(int64_t mloc, int64_t nloc, int64_t side) {
+  if (mloc == side && nloc == side) return true;
+  if (mloc < side || nloc < side) return false;
+  if (mloc >= nloc) return mloc % 2 == 0 && bisection_squares(mloc / 2, nloc, side);  // rows split on ties
+  return nloc % 2 == 0 && bisection_squares(mloc, nloc / 2, side);
 }
 
 int smm_pick_split(int bs, int64_t nruns, int64_t kb, bool squares) {

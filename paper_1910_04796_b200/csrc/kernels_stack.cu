@@ -197,7 +197,10 @@ cudaError_t launch_smm(int bs, const int32_t* trip, int64_t nruns, int64_t kb, c
                        int* launches, int64_t a_blocks, int64_t b_blocks, bool squares) {
   if (nruns <= 0) return cudaSuccess;
   const unsigned grid = (unsigned)std::min<int64_t>(nruns, (int64_t)num_sms() * 8);
-  if (smm_has_tensor_path(bs)) {
+  if (squares && smmq_side(bs) > 0) {  // R x R run squares of a padded small size (the host checked the shape)
+    cudaError_t e = launch_smmq(bs, trip, nruns, kb, A, B, C, alpha, beta_first, st);
+    if (e != cudaSuccess) return e;
+  } else if (smm_has_tensor_path(bs)) {
     cudaError_t e =
         launch_smm_tc(bs, trip, nruns, kb, A, B, C, alpha, beta_first, nsplit, partial, st, a_blocks, b_blocks,
                       squares);

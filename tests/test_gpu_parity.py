@@ -459,3 +459,18 @@ def test_multiply_timing_fields(dbm, ctx, path):
         assert t["ms_densify"] > 0 and t["ms_undensify"] > 0
     with pytest.raises(dbm.DbmError):
         ctx.multiply_timing()  # the records were consumed
+
+
+@pytest.mark.parametrize("bs,side", [(4, 8), (5, 16), (6, 8), (9, 8)])
+@pytest.mark.parametrize("kb", [3, 13])
+def test_smmq_square_kernel(dbm, ctx, orc, bs, side, kb):
+    """The R x R run-square kernel for the padded small sizes (kernels_smmq.cu): a 16R x 16R local grid (256
+    squares in Morton order, enough to fill the GPU), kb not a multiple of the stage's k-blocks (the
+    zero-predicated tail); integer inputs bit-exact with beta != 0 and beta = 0; U[-1,1) <= 1e-12."""
+    n = 16 * side * bs
+    for beta in (-1.25, 0.0):
+        got, ref, st = run_multiply(dbm, ctx, orc, n, n, kb * bs, bs, "blocked", 0.75, beta, kind=1)
+        assert np.array_equal(got, ref)
+        assert st["entries"] == (16 * side) ** 2 * kb
+    got, ref, _ = run_multiply(dbm, ctx, orc, n, n, kb * bs, bs, "blocked", 0.75, -1.25)
+    assert relerr(got, ref) <= TOL

@@ -14,7 +14,9 @@
  *    returns a thread-local human-readable detail string.
  *  - Device memory (matrix arenas, multiply workspace, dense buffers) is CALLER-OWNED
  *    (e.g. torch tensors).  The library never frees it.  Handles belong to the
- *    library until the matching *_destroy.
+ *    library until the matching *_destroy.  Library-owned device memory: small metadata
+ *    tables (block-sparse / non-uniform matrices, plans) and, on several ranks, the
+ *    exchange pool of dbm_ctx_set_transport (freed by dbm_ctx_destroy).
  *  - Calls that launch GPU work enqueue on the context's stream and return without
  *    synchronising, unless documented otherwise.  Asynchronous CUDA / NCCL failures
  *    surface at dbm_ctx_sync(), after which the context is poisoned: every later
@@ -127,9 +129,14 @@ dbm_status dbm_ctx_profile_read(dbm_ctx ctx, int kernel, double* ms_out, int64_t
  * *n_out = number of pending records.  Synchronises on the records. */
 dbm_status dbm_ctx_profile_timeline(dbm_ctx ctx, int max_records, double* out, int* n_out);
 /* Cannon panel transport between ranks ("asynchronous point-to-point"):
- * 0 (default) = DMA copy engines pull each needed panel from its owner's workspace, mapped with CUDA
- *     IPC, over NVLink (no SM is taken from the local multiply); ordering uses two tiny NCCL
- *     collectives per multiply.  The workspace must be a cudaMalloc allocation (e.g. a torch tensor).
+ * 0 (default) = DMA copy engines pull each needed panel over NVLink from its owner's exchange pool (no
+ *     SM is taken from the local multiply).  The pool is library-owned (a plain cudaMalloc allocation,
+ *     freed by dbm_ctx_destroy): a header of 64-bit signal words and the rank's own panels.  It is
+ *     mapped into every peer with CUDA IPC when it grows (an all-gather of the handles with a host
+ *     synchronisation; every rank sizes it by the maximum over all ranks' plans, so every rank grows
+ *     it in the same multiply); otherwise a multiply orders ranks device-side only: "panels ready" /
+ *     "done" epochs written into the peers' headers (cuStreamWriteValue64) and awaited on the
+ *     streams (cuStreamWaitValue64), no host synchronisation.
  * 1 = NCCL grouped ncclSend / ncclRecv.
  * Every rank must use the same transport.  Changes dbm_multiply_workspace() for the blocked path. */
 dbm_status dbm_ctx_set_transport(dbm_ctx ctx, int transport);
@@ -264,7 +271,7 @@ dbm_status dbm_plan_tallskinny(int pr, int pc, int myrow, int mycol, int64_t Mb,
  * device arenas of A, B, C are the staging copies.  Pinned host buffers: A and B are streamed on the
  * library's copy stream — on a single rank the densified path uploads K-chunk j+1 while chunk j is
  * densified and multiplied; on several ranks (copy-engine transport) each rank uploads and densifies
- * (or packs) its own panels in 5 K-chunks and publishes its progress into the peers' workspaces
+ * (or packs) its own panels in 5 K-chunks and publishes its progress into the peers' exchange pools
  * (64-bit stream writes), and Cannon's step-0 pulls wait on those flags, so the uploads pipeline
  * across ranks (set DBM_HOST_PIPE=0 in the environment for the whole-upload-then-barrier schedule) —
  * C_host is read only if beta != 0, and C is copied back to C_host.

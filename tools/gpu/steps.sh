@@ -6,7 +6,8 @@
 #   tests                 pytest -m gpu (the driver's GPU tier) + smoke()
 #   bench:<cfg>[:<path>]  bench.py --config cfg [--path path] --steps 3 --warmup 3 (JSON line -> s_bench_*.json)
 #   ncu_smm22q            ncu --set full of the bs-22 square kernel at 5,632^3 (one launch)
-#   ncu_dgemm_traffic     ncu dram bytes of one bench-shape dgemm launch (63,360 x 63,360 x 15,872)
+#   ncu_dgemm_traffic     ncu dram bytes of one bench-shape dgemm launch (63,360 x 63,360 x 16,896: a K-chunk)
+#   ncu_dgemm_full        ncu --set full of one bench-shape dgemm launch
 #   dgemm_sweep           bench-shape dgemm time under DBM_DGEMM_WAVESYNC / _WAVESLACK settings
 #   launches:<cfg>[:path] ncu launch list (gpu__time_duration) of one bench step
 set -u
@@ -40,8 +41,11 @@ for s in "$@"; do
       for ws in ${WAVES:-0}; do
         step ncu_dgemm_ws$ws 1200 env DBM_DGEMM_WAVESYNC=$ws $NCU --clock-control none -k regex:dgemm_tn -c 1 \
           --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,lts__t_sector_hit_rate.pct \
-          --csv python tools/profile_dgemm.py --M 63360 --N 63360 --K 15872 --reps 1
+          --csv python tools/profile_dgemm.py --M 63360 --N 63360 --K 16896 --reps 1
       done ;;
+    ncu_dgemm_full)
+      step ncu_dgemm_full 1500 $NCU --set full --import-source on --clock-control none -k regex:dgemm_tn -c 1 \
+        -o gpurun_out/ncu_dgemm_full -f python tools/profile_dgemm.py --M 63360 --N 63360 --K 16896 --reps 1 ;;
     dgemm_sweep)
       SW="${SWEEP:-0:1 32:1 64:1 128:1 64:2 16:1}"
       for cfg in $SW; do

@@ -1,5 +1,6 @@
 """Multi-GPU parity (NCCL over NVLink): torchrun tests/mp_worker.py on every visible GPU (2, 4 or 8),
-all grid factorisations, both local paths, against the oracle.  Skipped with fewer than 2 GPUs."""
+all grid factorisations, both local paths, against the oracle (each case under a watchdog, so a hang
+fails in minutes).  Skipped with fewer than 2 GPUs."""
 import os
 import subprocess
 import sys
@@ -17,8 +18,9 @@ def test_multirank_parity():
         pytest.skip("needs >= 2 GPUs")
     n = min(n, 8)
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
-           "--master-addr=127.0.0.1", "--master-port=29531", os.path.join(ROOT, "tests", "mp_worker.py")]
-    r = subprocess.run(cmd, capture_output=True, text=True, timeout=1200, cwd=ROOT)
+           "--master-addr=127.0.0.1", "--master-port=29531", os.path.join(ROOT, "tests", "mp_worker.py"),
+           "--groups", "cannon,sparse,host,nonuni"]  # (the host-pipeline sweep: tools/gpu/multigpu_check.sh)
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=2400, cwd=ROOT)
     print(r.stdout[-4000:])
     print(r.stderr[-4000:])
     assert r.returncode == 0

@@ -174,10 +174,13 @@ void launch_nu_fill(double* arena, const NUBlk* blk, int64_t nslots, uint64_t se
 void launch_nu_copy(const NUTask* tasks, int64_t ntasks, double* arena, double* dense, int64_t ld, int mode,
                     double alpha, double beta, cudaStream_t st);
 void launch_nu_pack(const NUPack* tasks, int64_t ntasks, const double* src, double* dst, cudaStream_t st);
-size_t nu_smm_smem(int kmax, int mmax, int nmax);
+// Entries grouped per stage: kdim[e] = k size of the run's entry e, kofs[e] = its k offset inside its group,
+// groups g = entries [gbeg[g], gbeg[g+1]) (host-computed; every run of a step has the same k sizes)
+size_t nu_smm_smem(int kcap, int mmax, int nmax);
 cudaError_t launch_nu_smm(const int32_t* trip, int64_t nruns, int64_t kb, const double* A, const int64_t* aoff,
-                          const double* B, const int64_t* boff, const int32_t* kdim, double* C, const NUBlk* cblk,
-                          int kmax, int mmax, int nmax, double alpha, double beta_first, cudaStream_t st);
+                          const double* B, const int64_t* boff, const int32_t* kdim, const int32_t* kofs,
+                          const int32_t* gbeg, int ngroups, double* C, const NUBlk* cblk, int kcap, int mmax, int nmax,
+                          double alpha, double beta_first, cudaStream_t st);
 struct NUCache;  // non-uniform multiply plans + device tables (multiply_nonuniform.cu)
 }  // namespace dbm
 

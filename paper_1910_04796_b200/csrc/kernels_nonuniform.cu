@@ -88,61 +88,69 @@ __device__ __forceinline__ void nu_dmma(double (&c)[2], double a, double b) {
 
 constexpr int kNuWarps = 4;
 constexpr int kNuMaxSub = 16;  // subtiles per warp: C blocks up to 64 x 64 = 64 subtiles over 4 warps
+constexpr int kNuStages = 3;
 
-// One CTA per run (C block): acc(c) = sum over the run's entries of A_blk(a) (m x k) * B_blk(b) (k x n),
-// then C = (first ? beta*C : C) + alpha*acc.  Entry e's blocks are staged by cp.async (8 bytes per
-// element: any offset alignment) into stage e % 2 while entry e - 1 multiplies.  Shared layout per
-// stage: A as [k][mp] (mp = m rounded up to 8), B as [n][kp + 1] (kp = k_max rounded up to 4): the
-// DMMA fragment loads read A(row 8i + g, k 4ks + t) and B(k 4ks + t, col 8j + g).  Rows >= m, columns
-// >= n and k >= k_entry are zeroed in registers (predication), so the padding is never staged.
+// One CTA per run (C block): acc(c) = sum over the run's entries of A_blk (m x k_e) * B_blk (k_e x n), then
+// C = (first ? beta*C : C) + alpha*acc.  The entries are taken in GROUPS (host-computed from the k sizes,
+// the same for every run of the step: group g = entries [gbeg[g], gbeg[g+1]), their k sizes summing to at
+// most kcap): a group's A blocks are staged as the rows of one (K_g x mp) tile and its B blocks as the
+// columns of one (np x K_g) tile -- entry e at k offset kofs[e] inside its group -- so one k-loop runs over
+// the concatenated K of several entries (k-steps may straddle entries) and the ring advances once per
+// group, not per entry.  8-byte cp.async (any alignment) into a 3-stage ring; FP64 DMMA on 8 x 8 subtiles;
+// rows >= m, columns >= n and k >= K_g are zeroed in registers, so no padding is ever staged.
 __global__ void __launch_bounds__(kNuWarps * 32)
     nu_smm_kernel(const int32_t* __restrict__ trip, int64_t nruns, int64_t kb, const double* __restrict__ A,
                   const int64_t* __restrict__ aoff, const double* __restrict__ B, const int64_t* __restrict__ boff,
-                  const int32_t* __restrict__ kdim, double* __restrict__ C, const NUBlk* __restrict__ cblk,
-                  int kmax_pad, int mmax_pad, int nmax_pad, double alpha, double beta_first) {
+                  const int32_t* __restrict__ kdim, const int32_t* __restrict__ kofs, const int32_t* __restrict__ gbeg,
+                  int ngroups, double* __restrict__ C, const NUBlk* __restrict__ cblk, int kcap, int mmax_pad,
+                  int nmax_pad, double alpha, double beta_first) {
   extern __shared__ __align__(16) double nsm[];
-  const int a_st = kmax_pad * mmax_pad, b_pitch = kmax_pad + 1, b_st = nmax_pad * b_pitch;
+  const int kcap_pad = (kcap + 3) & ~3;
+  const int a_st = kcap_pad * mmax_pad, b_pitch = kcap_pad + 1, b_st = nmax_pad * b_pitch;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
   for (int64_t run = blockIdx.x; run < nruns; run += gridDim.x) {
     const int32_t* rt = trip + 3 * run * kb;
     const NUBlk cb = cblk[rt[2]];
     const int m = cb.rows, n = cb.cols, mp = (m + 7) & ~7;
     const int sm_ = mp / 8, sn = (n + 7) / 8, nsub = sm_ * sn;
-    auto stage = [&](int64_t e, int buf) {  // entry e's A and B blocks -> stage buf
-      const int k = kdim[e];  // entries run kk = 0 .. kb-1 (dense pattern): entry e is panel k-block e
-      const double* a = A + aoff[rt[3 * e]];
-      const double* b = B + boff[rt[3 * e + 1]];
-      double* sa = nsm + buf * (a_st + b_st);
-      double* sb = sa + a_st;
-      for (int q = threadIdx.x; q < m * k; q += blockDim.x) {  // A(x, z) at z*m + x -> sa[z*mp + x]
-        const int z = q / m, x = q - z * m;
-        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"((uint32_t)__cvta_generic_to_shared(sa + z * mp + x)),
-                     "l"(a + q)
-                     : "memory");
-      }
-      for (int q = threadIdx.x; q < k * n; q += blockDim.x) {  // B(z, y) at y*k + z -> sb[y*b_pitch + z]
-        const int y = q / k, z = q - y * k;
-        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(
-                         (uint32_t)__cvta_generic_to_shared(sb + y * b_pitch + z)),
-                     "l"(b + q)
-                     : "memory");
+    auto stage = [&](int grp, int buf) {  // group grp's blocks -> stage buf (an empty commit past the end)
+      if (grp < ngroups) {
+        double* sa = nsm + buf * (a_st + b_st);
+        double* sb = sa + a_st;
+        for (int e = gbeg[grp]; e < gbeg[grp + 1]; ++e) {
+          const int k = kdim[e], ko = kofs[e];
+          const double* a = A + aoff[rt[3 * e]];
+          const double* b = B + boff[rt[3 * e + 1]];
+          for (int q = threadIdx.x; q < m * k; q += blockDim.x) {  // A(x, z) at z*m + x -> sa[(ko+z)*mp + x]
+            const int z = q / m, x = q - z * m;
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(
+                             (uint32_t)__cvta_generic_to_shared(sa + (ko + z) * mp + x)),
+                         "l"(a + q)
+                         : "memory");
+          }
+          for (int q = threadIdx.x; q < k * n; q += blockDim.x) {  // B(z, y) at y*k + z -> sb[y*b_pitch + ko+z]
+            const int y = q / k, z = q - y * k;
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(
+                             (uint32_t)__cvta_generic_to_shared(sb + y * b_pitch + ko + z)),
+                         "l"(b + q)
+                         : "memory");
+          }
+        }
       }
       asm volatile("cp.async.commit_group;" ::: "memory");
     };
     double acc[kNuMaxSub][2];
 #pragma unroll
     for (int i = 0; i < kNuMaxSub; ++i) acc[i][0] = acc[i][1] = 0.0;
-    if (kb > 0) stage(0, 0);
-    for (int64_t e = 0; e < kb; ++e) {
-      if (e + 1 < kb) {
-        stage(e + 1, (int)((e + 1) & 1));
-        asm volatile("cp.async.wait_group 1;" ::: "memory");
-      } else {
-        asm volatile("cp.async.wait_group 0;" ::: "memory");
-      }
+#pragma unroll
+    for (int s = 0; s < kNuStages - 1; ++s) stage(s, s);
+    for (int grp = 0; grp < ngroups; ++grp) {
+      stage(grp + kNuStages - 1, (grp + kNuStages - 1) % kNuStages);
+      asm volatile("cp.async.wait_group %0;" ::"n"(kNuStages - 1) : "memory");
       __syncthreads();
-      const int k = kdim[e];
-      const double* sa = nsm + (e & 1) * (a_st + b_st);
+      const int ek = gbeg[grp + 1] - 1;
+      const int K = kofs[ek] + kdim[ek];  // the group's concatenated K
+      const double* sa = nsm + (grp % kNuStages) * (a_st + b_st);
       const double* sb = sa + a_st;
 #pragma unroll
       for (int i = 0; i < kNuMaxSub; ++i) {
@@ -151,15 +159,16 @@ __global__ void __launch_bounds__(kNuWarps * 32)
         const int im = sub % sm_, in = sub / sm_;
         const int row = 8 * im + g, col = 8 * in + g;
         const bool rok = row < m, cok = col < n;
-        for (int ks = 0; 4 * ks < k; ++ks) {
+        for (int ks = 0; 4 * ks < K; ++ks) {
           const int z = 4 * ks + t;
-          const double av = (rok && z < k) ? sa[z * mp + row] : 0.0;
-          const double bv = (cok && z < k) ? sb[col * b_pitch + z] : 0.0;
+          const double av = (rok && z < K) ? sa[z * mp + row] : 0.0;
+          const double bv = (cok && z < K) ? sb[col * b_pitch + z] : 0.0;
           nu_dmma(acc[i], av, bv);
         }
       }
-      __syncthreads();  // stage e & 1 is refilled by entry e + 2
+      __syncthreads();  // stage grp % kNuStages is refilled two groups on
     }
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
     // epilogue: subtile (im, in), lane (g, t) holds C(8 im + g, 8 in + 2t + jj)
 #pragma unroll
     for (int i = 0; i < kNuMaxSub; ++i) {
@@ -177,7 +186,7 @@ __global__ void __launch_bounds__(kNuWarps * 32)
         *p = beta_first == 0.0 ? v : beta_first * *p + v;
       }
     }
-    __syncthreads();  // the next run's first stage reuses buffer 0
+    __syncthreads();  // the next run's first stages reuse the ring
   }
 }
 
@@ -211,17 +220,18 @@ void launch_nu_pack(const NUPack* tasks, int64_t ntasks, const double* src, doub
   nu_pack_kernel<<<nu_grid(ntasks), 256, 0, st>>>(tasks, ntasks, src, dst);
 }
 
-size_t nu_smm_smem(int kmax, int mmax, int nmax) {
-  const int kp = (kmax + 3) & ~3, mp = (mmax + 7) & ~7, np = (nmax + 7) & ~7;
-  return (size_t)2 * ((size_t)kp * mp + (size_t)np * (kp + 1)) * 8;
+size_t nu_smm_smem(int kcap, int mmax, int nmax) {
+  const int kp = (kcap + 3) & ~3, mp = (mmax + 7) & ~7, np = (nmax + 7) & ~7;
+  return (size_t)kNuStages * ((size_t)kp * mp + (size_t)np * (kp + 1)) * 8;
 }
 
 cudaError_t launch_nu_smm(const int32_t* trip, int64_t nruns, int64_t kb, const double* A, const int64_t* aoff,
-                          const double* B, const int64_t* boff, const int32_t* kdim, double* C, const NUBlk* cblk,
-                          int kmax, int mmax, int nmax, double alpha, double beta_first, cudaStream_t st) {
+                          const double* B, const int64_t* boff, const int32_t* kdim, const int32_t* kofs,
+                          const int32_t* gbeg, int ngroups, double* C, const NUBlk* cblk, int kcap, int mmax, int nmax,
+                          double alpha, double beta_first, cudaStream_t st) {
   if (nruns <= 0 || kb <= 0) return cudaSuccess;
   if (mmax > 64 || nmax > 64) return cudaErrorInvalidValue;  // the host checks: C blocks up to 64 x 64
-  const size_t smem = nu_smm_smem(kmax, mmax, nmax);
+  const size_t smem = nu_smm_smem(kcap, mmax, nmax);
   static size_t attr = 0;
   if (smem > 48 * 1024 && smem > attr) {
     cudaError_t e = cudaFuncSetAttribute(nu_smm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -229,8 +239,8 @@ cudaError_t launch_nu_smm(const int32_t* trip, int64_t nruns, int64_t kb, const 
     attr = smem;
   }
   nu_smm_kernel<<<(unsigned)std::min<int64_t>(nruns, (int64_t)num_sms() * 32), kNuWarps * 32, smem, st>>>(
-      trip, nruns, kb, A, aoff, B, boff, kdim, C, cblk, (kmax + 3) & ~3, (mmax + 7) & ~7, (nmax + 7) & ~7, alpha,
-      beta_first);
+      trip, nruns, kb, A, aoff, B, boff, kdim, kofs, gbeg, ngroups, C, cblk, kcap, (mmax + 7) & ~7, (nmax + 7) & ~7,
+      alpha, beta_first);
   return cudaGetLastError();
 }
 

@@ -108,7 +108,9 @@ struct NUCache {
   size_t o_ctask = 0;                       // C undensify tasks
   int64_t n_ctask = 0;
   std::vector<size_t> o_aoff, o_boff, o_kdim;  // per kappa: panel slot -> element offset tables, k sizes (blocked)
-  int kmax = 1, mmax = 1, nmax = 1;
+  std::vector<size_t> o_kofs, o_gbeg;          // per kappa: entry k offsets inside their groups, group starts
+  std::vector<int> ngroups;
+  int kmax = 1, mmax = 1, nmax = 1, kcap = 32;
 };
 
 namespace {
@@ -197,6 +199,7 @@ dbm_status nu_cache_get(dbm_ctx ctx, dbm_matrix A, dbm_matrix B, dbm_matrix C, b
   };
   (void)a_slot;
   const bool multi = ctx->nranks > 1;
+  std::vector<std::vector<int32_t>> kdims(p.L);  // per kappa: the panel's k-block sizes (blocked)
   for (int k = 0; k < p.L; ++k) {
     const int64_t kb = (int64_t)p.ks[k].size();
     if (dens) {
@@ -252,6 +255,7 @@ dbm_status nu_cache_get(dbm_ctx ctx, dbm_matrix A, dbm_matrix B, dbm_matrix C, b
       nc->o_aoff[k] = put(ao.data(), ao.size() * 8);
       nc->o_boff[k] = put(bo.data(), bo.size() * 8);
       nc->o_kdim[k] = put(kd.data(), kd.size() * 4);
+      kdims[k] = kd;
       if (multi && p.ownA[k] != SIZE_MAX) {  // pack my A panel kappa: blocks (li, kk) in row-major order
         std::vector<NUPack> t;
         for (int64_t li = 0; li < p.mloc; ++li)
@@ -276,6 +280,28 @@ dbm_status nu_cache_get(dbm_ctx ctx, dbm_matrix A, dbm_matrix B, dbm_matrix C, b
   }
   for (int64_t li = 0; li < p.mloc; ++li) nc->mmax = std::max(nc->mmax, (int)A->row_size(r + li * p.pr));
   for (int64_t lj = 0; lj < p.nloc; ++lj) nc->nmax = std::max(nc->nmax, (int)B->col_size(c + lj * p.pc));
+  if (!dens) {  // entry groups of the small-block kernel: consecutive entries with summed k <= kcap
+    nc->kcap = std::max(nc->kmax, 32);
+    nc->o_kofs.assign(p.L, SIZE_MAX);
+    nc->o_gbeg.assign(p.L, SIZE_MAX);
+    nc->ngroups.assign(p.L, 0);
+    for (int k = 0; k < p.L; ++k) {
+      std::vector<int32_t> kofs, gbeg{0};
+      int32_t acc = 0;
+      for (size_t e = 0; e < kdims[k].size(); ++e) {
+        if (acc + kdims[k][e] > nc->kcap) {
+          gbeg.push_back((int32_t)e);
+          acc = 0;
+        }
+        kofs.push_back(acc);
+        acc += kdims[k][e];
+      }
+      if (!kdims[k].empty()) gbeg.push_back((int32_t)kdims[k].size());
+      nc->ngroups[k] = (int)gbeg.size() - 1;
+      nc->o_kofs[k] = put(kofs.data(), kofs.size() * 4);
+      nc->o_gbeg[k] = put(gbeg.data(), gbeg.size() * 4);
+    }
+  }
   if (dens) {  // undensify C (stored blocks only)
     std::vector<NUTask> t;
     for (int64_t li = 0; li < p.mloc; ++li)
@@ -330,7 +356,7 @@ dbm_status multiply_nonuniform(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_matr
   if (!dens) {
     ARG_CHECK(nc->mmax <= 64 && nc->nmax <= 64, DBM_ERR_SHAPE,
               "blocked path: C blocks up to 64 x 64 (larger blocks: the densified path)");
-    ARG_CHECK(nu_smm_smem(nc->kmax, nc->mmax, nc->nmax) <= 227 * 1024, DBM_ERR_SHAPE,
+    ARG_CHECK(nu_smm_smem(nc->kcap, nc->mmax, nc->nmax) <= 227 * 1024, DBM_ERR_SHAPE,
               "blocked path: A / B blocks too large for the shared-memory stages (use the densified path)");
   }
   cudaStream_t cs = ctx->stream;
@@ -489,11 +515,13 @@ dbm_status multiply_nonuniform(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_matr
             launch_stackgen(trav_li, trav_lj, q0, q1, kb, p.nloc, kb, p.nloc, trip, cs);
             ++launches;
           }
-          ProfScope ps(ctx, cs, 1, 0.0, 0.0);
+          // flops of the chunk: the step's 2 Mel Nel W spread over the runs (exact for one chunk per step)
+          ProfScope ps(ctx, cs, 1, 2.0 * (double)p.Mel * p.Nel * W * (double)(q1 - q0) / (double)nruns, 0.0);
           CUDA_TRY(ctx, launch_nu_smm(trip, q1 - q0, kb, Ap, (const int64_t*)(meta + nc->o_aoff[k]), Bp,
                                       (const int64_t*)(meta + nc->o_boff[k]), (const int32_t*)(meta + nc->o_kdim[k]),
-                                      C->arena, C->d_blk, nc->kmax, nc->mmax, nc->nmax, alpha, s == 0 ? beta : 1.0,
-                                      cs));
+                                      (const int32_t*)(meta + nc->o_kofs[k]), (const int32_t*)(meta + nc->o_gbeg[k]),
+                                      nc->ngroups[k], C->arena, C->d_blk, nc->kcap, nc->mmax, nc->nmax, alpha,
+                                      s == 0 ? beta : 1.0, cs));
           ++launches;
         }
         st.entries += nruns * kb;

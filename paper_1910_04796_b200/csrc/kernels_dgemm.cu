@@ -20,7 +20,12 @@ namespace {
 
 constexpr int BK = 16;
 constexpr int kConsumerWarps = 8;
-constexpr int kThreads = (kConsumerWarps + 1) * 32;
+// 12 warps = three warpgroups: two of consumers, one whose first warp is the TMA producer.  The launch
+// gives every thread 168 registers (65,536 / 384); the producer warpgroup then releases down to 40 and the
+// consumers raise to 232 (setmaxnreg), so the 64 FP64 accumulators, the fragments and the ring state of a
+// consumer fit without spilling (at a flat 168 the k-loop spilled its stage / phase / base registers).
+constexpr int kThreads = (kConsumerWarps + 4) * 32;
+constexpr int kRegsConsumer = 232, kRegsProducer = 40;
 // CTA tile BM x BN in {128, 64}^2 (the host picks the one that wastes the least padding for the
 // block-multiple shapes of the configs, e.g. 704 = 5.5 x 128); ~192 KB of stages in every case.
 template <int BM, int BN>
@@ -127,8 +132,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   __syncthreads();
 
-  if (warp == kConsumerWarps) {  // ---------------- TMA producer
-    if (lane == 0) {
+  if (warp >= kConsumerWarps) {  // ---------------- producer warpgroup: warp 8 issues the TMA, 9-11 idle
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kRegsProducer));
+    if (warp == kConsumerWarps && lane == 0) {
       asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&tmA) : "memory");
       asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&tmB) : "memory");
       int stage = 0;
@@ -183,6 +189,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 
   // ---------------- consumers: warp (wm, wn) owns rows wm*BM/2.., cols wn*BN/4..
+  asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kRegsConsumer));
   const int wm = warp >> 2, wn = warp & 3;
 
   // Fragment addressing inside a 128-B-swizzled [rows][16 doubles] box: element (row, k) lives at

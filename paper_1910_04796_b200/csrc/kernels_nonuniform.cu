@@ -87,7 +87,7 @@ __device__ __forceinline__ void nu_dmma(double (&c)[2], double a, double b) {
 }
 
 constexpr int kNuWarps = 4;
-constexpr int kNuMaxSub = 16;  // subtiles per warp: C blocks up to 64 x 64 = 64 subtiles over 4 warps
+constexpr int kNuRows = 2, kNuCols = 8;  // a warp's subtiles: C blocks up to 64 x 64 = 8 x 8 subtiles, 4 warps
 constexpr int kNuStages = 3;
 
 // One CTA per run (C block): acc(c) = sum over the run's entries of A_blk (m x k_e) * B_blk (k_e x n), then
@@ -112,7 +112,7 @@ __global__ void __launch_bounds__(kNuWarps * 32)
     const int32_t* rt = trip + 3 * run * kb;
     const NUBlk cb = cblk[rt[2]];
     const int m = cb.rows, n = cb.cols, mp = (m + 7) & ~7;
-    const int sm_ = mp / 8, sn = (n + 7) / 8, nsub = sm_ * sn;
+    const int sm_ = mp / 8, sn = (n + 7) / 8;
     auto stage = [&](int grp, int buf) {  // group grp's blocks -> stage buf (an empty commit past the end)
       if (grp < ngroups) {
         double* sa = nsm + buf * (a_st + b_st);
@@ -139,9 +139,11 @@ __global__ void __launch_bounds__(kNuWarps * 32)
       }
       asm volatile("cp.async.commit_group;" ::: "memory");
     };
-    double acc[kNuMaxSub][2];
+    double acc[kNuRows][kNuCols][2];
 #pragma unroll
-    for (int i = 0; i < kNuMaxSub; ++i) acc[i][0] = acc[i][1] = 0.0;
+    for (int i = 0; i < kNuRows; ++i)
+#pragma unroll
+      for (int j = 0; j < kNuCols; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 #pragma unroll
     for (int s = 0; s < kNuStages - 1; ++s) stage(s, s);
     for (int grp = 0; grp < ngroups; ++grp) {
@@ -152,38 +154,51 @@ __global__ void __launch_bounds__(kNuWarps * 32)
       const int K = kofs[ek] + kdim[ek];  // the group's concatenated K
       const double* sa = nsm + (grp % kNuStages) * (a_st + b_st);
       const double* sb = sa + a_st;
+      // warp w owns subtile rows im = w, w + 4 (m <= 64: at most 2) across all subtile columns: per k-step
+      // it loads its rows' A fragments and every column's B fragment once and reuses them (2 + sn loads for
+      // 2 sn DMMAs, instead of two loads per DMMA)
+      for (int ks = 0; 4 * ks < K; ++ks) {
+        const int z = 4 * ks + t;
+        const bool zok = z < K;
+        double av[kNuRows], bv[kNuCols];
 #pragma unroll
-      for (int i = 0; i < kNuMaxSub; ++i) {
-        const int sub = warp + kNuWarps * i;
-        if (sub >= nsub) break;
-        const int im = sub % sm_, in = sub / sm_;
-        const int row = 8 * im + g, col = 8 * in + g;
-        const bool rok = row < m, cok = col < n;
-        for (int ks = 0; 4 * ks < K; ++ks) {
-          const int z = 4 * ks + t;
-          const double av = (rok && z < K) ? sa[z * mp + row] : 0.0;
-          const double bv = (cok && z < K) ? sb[col * b_pitch + z] : 0.0;
-          nu_dmma(acc[i], av, bv);
+        for (int i = 0; i < kNuRows; ++i) {
+          const int row = 8 * (warp + kNuWarps * i) + g;
+          av[i] = (zok && row < m) ? sa[z * mp + row] : 0.0;
+        }
+#pragma unroll
+        for (int j = 0; j < kNuCols; ++j) {
+          const int col = 8 * j + g;
+          bv[j] = (zok && j < sn && col < n) ? sb[col * b_pitch + z] : 0.0;
+        }
+#pragma unroll
+        for (int i = 0; i < kNuRows; ++i) {
+          if (warp + kNuWarps * i >= sm_) break;
+#pragma unroll
+          for (int j = 0; j < kNuCols; ++j) {
+            if (j >= sn) break;
+            nu_dmma(acc[i][j], av[i], bv[j]);
+          }
         }
       }
       __syncthreads();  // stage grp % kNuStages is refilled two groups on
     }
     asm volatile("cp.async.wait_group 0;" ::: "memory");
-    // epilogue: subtile (im, in), lane (g, t) holds C(8 im + g, 8 in + 2t + jj)
+    // epilogue: subtile (im = warp + 4i, j), lane (g, t) holds C(8 im + g, 8 j + 2t + jj)
 #pragma unroll
-    for (int i = 0; i < kNuMaxSub; ++i) {
-      const int sub = warp + kNuWarps * i;
-      if (sub >= nsub) break;
-      const int im = sub % sm_, in = sub / sm_;
-      const int row = 8 * im + g;
+    for (int i = 0; i < kNuRows; ++i) {
+      const int row = 8 * (warp + kNuWarps * i) + g;
       if (row >= m) continue;
 #pragma unroll
-      for (int jj = 0; jj < 2; ++jj) {
-        const int col = 8 * in + 2 * t + jj;
-        if (col >= n) continue;
-        double* p = C + cb.off + (int64_t)col * m + row;
-        const double v = alpha * acc[i][jj];
-        *p = beta_first == 0.0 ? v : beta_first * *p + v;
+      for (int j = 0; j < kNuCols; ++j) {
+#pragma unroll
+        for (int jj = 0; jj < 2; ++jj) {
+          const int col = 8 * j + 2 * t + jj;
+          if (col >= n) continue;
+          double* p = C + cb.off + (int64_t)col * m + row;
+          const double v = alpha * acc[i][j][jj];
+          *p = beta_first == 0.0 ? v : beta_first * *p + v;
+        }
       }
     }
     __syncthreads();  // the next run's first stages reuse the ring

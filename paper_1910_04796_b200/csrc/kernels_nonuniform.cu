@@ -121,20 +121,19 @@ __global__ void __launch_bounds__(kNuWarps * 32)
           const int k = kdim[e], ko = kofs[e];
           const double* a = A + aoff[rt[3 * e]];
           const double* b = B + boff[rt[3 * e + 1]];
-          for (int q = threadIdx.x; q < m * k; q += blockDim.x) {  // A(x, z) at z*m + x -> sa[(ko+z)*mp + x]
-            const int z = q / m, x = q - z * m;
-            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(
-                             (uint32_t)__cvta_generic_to_shared(sa + (ko + z) * mp + x)),
-                         "l"(a + q)
-                         : "memory");
-          }
-          for (int q = threadIdx.x; q < k * n; q += blockDim.x) {  // B(z, y) at y*k + z -> sb[y*b_pitch + ko+z]
-            const int y = q / k, z = q - y * k;
-            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(
-                             (uint32_t)__cvta_generic_to_shared(sb + y * b_pitch + ko + z)),
-                         "l"(b + q)
-                         : "memory");
-          }
+          // warps over columns, lanes along a column (coalesced, no per-element division)
+          for (int z = warp; z < k; z += kNuWarps)  // A(x, z) at z*m + x -> sa[(ko+z)*mp + x]
+            for (int x = lane; x < m; x += 32)
+              asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(
+                               (uint32_t)__cvta_generic_to_shared(sa + (ko + z) * mp + x)),
+                           "l"(a + z * m + x)
+                           : "memory");
+          for (int y = warp; y < n; y += kNuWarps)  // B(z, y) at y*k + z -> sb[y*b_pitch + ko+z]
+            for (int z = lane; z < k; z += 32)
+              asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(
+                               (uint32_t)__cvta_generic_to_shared(sb + y * b_pitch + ko + z)),
+                           "l"(b + y * k + z)
+                           : "memory");
         }
       }
       asm volatile("cp.async.commit_group;" ::: "memory");

@@ -43,6 +43,10 @@ for s in "$@"; do
           --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,lts__t_sector_hit_rate.pct \
           --csv python tools/profile_dgemm.py --M 63360 --N 63360 --K 16896 --reps 1
       done ;;
+    ncu_nu_smm)
+      step ncu_nu_smm 900 $NCU --set full --import-source on --clock-control none -k regex:nu_smm -c 1 \
+        -o gpurun_out/ncu_nu_smm -f python bench.py --config nu --path blocked --steps 1 --warmup 0 --no-e2e \
+        --no-cpu-baseline ;;
     ncu_dgemm_full)
       step ncu_dgemm_full 1500 $NCU --set full --import-source on --clock-control none -k regex:dgemm_tn -c 1 \
         -o gpurun_out/ncu_dgemm_full -f python tools/profile_dgemm.py --M 63360 --N 63360 --K 16896 --reps 1 ;;

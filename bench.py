@@ -39,6 +39,7 @@ CONFIGS = {
     # non-uniform block sizes (§8f-2 / f4, reading R16; not a BASELINE config): every dimension cut into
     # 1,000 blocks cycling through CP2K-like sizes 5, 13, 23, 26, 32 (19,800 elements)
     "nu": (19800, 19800, 19800, 0, "densified", None),
+    "nus": (3960, 3960, 3960, 0, "densified", None),  # (the same at 200 blocks: profiling, quick A/B)
 }
 NU_CYCLE = (5, 13, 23, 26, 32)
 
@@ -227,7 +228,8 @@ def main():
             "r64": "rect 1408x1408x1982464 bs64", "r22": "rect 1408x1408x1982464 bs22",
             "sp22": "square 63360^3 bs22 block-sparse A,B occupancy 0.1, C stored",
             "sp64": "square 63360^3 bs64 block-sparse A,B occupancy 0.1, C stored",
-            "nu": "square 19800^3 non-uniform blocks cycling 5,13,23,26,32"}[args.config]
+            "nu": "square 19800^3 non-uniform blocks cycling 5,13,23,26,32",
+            "nus": "square 3960^3 non-uniform blocks cycling 5,13,23,26,32"}[args.config]
     occ = SPARSE_OCC.get(args.config)
     name = f"{name} {path} " + (f"(BASELINE.json configs[{cidx}])" if cidx is not None else "(§8f-2 NEXT row)")
     if args.impl == "reference":

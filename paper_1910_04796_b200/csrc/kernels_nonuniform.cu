@@ -8,8 +8,8 @@
 //                      B (K-major columns) and undensify C with alpha / beta (column-major)
 //   nu_pack_kernel     whole-block gathers into packed Cannon panels (blocked path)
 //   nu_smm_kernel      the blocked path's small-block products of mixed (m, n, k): one CTA per C-block
-//                      run, operands staged by cp.async into a 2-stage ring, FP64 DMMA (mma.sync
-//                      m8n8k4) on 8 x 8 subtiles with register predication for the ragged edges
+//                      run, entry groups staged by cp.async into a 3-stage ring, K split over the warps,
+//                      FP64 DMMA (mma.sync m8n8k4) on 8 x 8 subtiles with register predication
 #include <algorithm>
 
 #include "dbm_internal.h"
@@ -87,17 +87,26 @@ __device__ __forceinline__ void nu_dmma(double (&c)[2], double a, double b) {
 }
 
 constexpr int kNuWarps = 4;
-constexpr int kNuRows = 2, kNuCols = 8;  // a warp's subtiles: C blocks up to 64 x 64 = 8 x 8 subtiles, 4 warps
 constexpr int kNuStages = 3;
 
-// One CTA per run (C block): acc(c) = sum over the run's entries of A_blk (m x k_e) * B_blk (k_e x n), then
-// C = (first ? beta*C : C) + alpha*acc.  The entries are taken in GROUPS (host-computed from the k sizes,
-// the same for every run of the step: group g = entries [gbeg[g], gbeg[g+1]), their k sizes summing to at
-// most kcap): a group's A blocks are staged as the rows of one (K_g x mp) tile and its B blocks as the
-// columns of one (np x K_g) tile -- entry e at k offset kofs[e] inside its group -- so one k-loop runs over
-// the concatenated K of several entries (k-steps may straddle entries) and the ring advances once per
-// group, not per entry.  8-byte cp.async (any alignment) into a 3-stage ring; FP64 DMMA on 8 x 8 subtiles;
-// rows >= m, columns >= n and k >= K_g are zeroed in registers, so no padding is ever staged.
+// One CTA per run (C block, m x n <= 64 x 64): acc(c) = sum over the run's entries of A_blk (m x k_e) *
+// B_blk (k_e x n), then C = (first ? beta*C : C) + alpha*acc.  The entries are taken in GROUPS
+// (host-computed from the k sizes, the same for every run of the step: group g = entries [gbeg[g],
+// gbeg[g+1]), their k sizes summing to at most kcap), entry e at k offset kofs[e] inside its group:
+//   * staging (all 128 threads, 8-byte cp.async, any alignment, into a 3-stage ring): every A block of a
+//     run has the run's m rows, so the group's A blocks, each m x k_e column-major, are ONE contiguous
+//     m x K_g column-major tile -- a flat copy; the B blocks (k_e x n column-major) go to the columns of an
+//     (n x K_g) K-contiguous tile, the column index of a flat element taken by a float reciprocal and one
+//     correction (no integer division);
+//   * compute: the warps split the group's K WK ways (k-step ks to k-group ks mod WK) and the subtile rows
+//     WR ways (WR WK = 4 warps); a warp holds SI subtile rows x all S subtile columns of the C block (8 x 8
+//     DMMA subtiles; blocks up to 32: S = 4, WR = 1, WK = 4; up to 64: S = 8, WR = 2, WK = 2, so the
+//     accumulators stay at 64 registers) and per k-step loads its A and B fragments once for all its
+//     DMMAs -- every warp busy whatever the block shape; rows >= m, columns >= n and k >= K_g are zeroed
+//     in registers;
+//   * epilogue: the WK k-groups' partial C blocks meet in shared memory and are summed in k-group order
+//     (deterministic), then scaled into C.
+template <int S, int WR>
 __global__ void __launch_bounds__(kNuWarps * 32)
     nu_smm_kernel(const int32_t* __restrict__ trip, int64_t nruns, int64_t kb, const double* __restrict__ A,
                   const int64_t* __restrict__ aoff, const double* __restrict__ B, const int64_t* __restrict__ boff,
@@ -107,12 +116,14 @@ __global__ void __launch_bounds__(kNuWarps * 32)
   extern __shared__ __align__(16) double nsm[];
   const int kcap_pad = (kcap + 3) & ~3;
   const int a_st = kcap_pad * mmax_pad, b_pitch = kcap_pad + 1, b_st = nmax_pad * b_pitch;
+  constexpr int WK = kNuWarps / WR, SI = S / WR;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+  const int rh = warp % WR, kg = warp / WR, i0 = rh * SI;
   for (int64_t run = blockIdx.x; run < nruns; run += gridDim.x) {
     const int32_t* rt = trip + 3 * run * kb;
     const NUBlk cb = cblk[rt[2]];
-    const int m = cb.rows, n = cb.cols, mp = (m + 7) & ~7;
-    const int sm_ = mp / 8, sn = (n + 7) / 8;
+    const int m = cb.rows, n = cb.cols;
+    const int sm_ = (m + 7) / 8, sn = (n + 7) / 8;
     auto stage = [&](int grp, int buf) {  // group grp's blocks -> stage buf (an empty commit past the end)
       if (grp < ngroups) {
         double* sa = nsm + buf * (a_st + b_st);
@@ -121,28 +132,31 @@ __global__ void __launch_bounds__(kNuWarps * 32)
           const int k = kdim[e], ko = kofs[e];
           const double* a = A + aoff[rt[3 * e]];
           const double* b = B + boff[rt[3 * e + 1]];
-          // warps over columns, lanes along a column (coalesced, no per-element division)
-          for (int z = warp; z < k; z += kNuWarps)  // A(x, z) at z*m + x -> sa[(ko+z)*mp + x]
-            for (int x = lane; x < m; x += 32)
-              asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(
-                               (uint32_t)__cvta_generic_to_shared(sa + (ko + z) * mp + x)),
-                           "l"(a + z * m + x)
-                           : "memory");
-          for (int y = warp; y < n; y += kNuWarps)  // B(z, y) at y*k + z -> sb[y*b_pitch + ko+z]
-            for (int z = lane; z < k; z += 32)
-              asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(
-                               (uint32_t)__cvta_generic_to_shared(sb + y * b_pitch + ko + z)),
-                           "l"(b + y * k + z)
-                           : "memory");
+          const int na = m * k, nb = k * n;
+          for (int q = threadIdx.x; q < na; q += kNuWarps * 32)  // A(x, z) at z*m + x -> sa[(ko+z)*m + x]
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(
+                             (uint32_t)__cvta_generic_to_shared(sa + ko * m + q)),
+                         "l"(a + q)
+                         : "memory");
+          const float rk = 1.0f / (float)k;
+          for (int q = threadIdx.x; q < nb; q += kNuWarps * 32) {  // B(z, y) at y*k + z -> sb[y*b_pitch + ko+z]
+            int y = (int)(((float)q + 0.5f) * rk), z = q - y * k;
+            if (z < 0) --y, z += k;
+            if (z >= k) ++y, z -= k;
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(
+                             (uint32_t)__cvta_generic_to_shared(sb + y * b_pitch + ko + z)),
+                         "l"(b + q)
+                         : "memory");
+          }
         }
       }
       asm volatile("cp.async.commit_group;" ::: "memory");
     };
-    double acc[kNuRows][kNuCols][2];
+    double acc[SI][S][2];
 #pragma unroll
-    for (int i = 0; i < kNuRows; ++i)
+    for (int i = 0; i < SI; ++i)
 #pragma unroll
-      for (int j = 0; j < kNuCols; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+      for (int j = 0; j < S; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 #pragma unroll
     for (int s = 0; s < kNuStages - 1; ++s) stage(s, s);
     for (int grp = 0; grp < ngroups; ++grp) {
@@ -153,28 +167,25 @@ __global__ void __launch_bounds__(kNuWarps * 32)
       const int K = kofs[ek] + kdim[ek];  // the group's concatenated K
       const double* sa = nsm + (grp % kNuStages) * (a_st + b_st);
       const double* sb = sa + a_st;
-      // warp w owns subtile rows im = w, w + 4 (m <= 64: at most 2) across all subtile columns: per k-step
-      // it loads its rows' A fragments and every column's B fragment once and reuses them (2 + sn loads for
-      // 2 sn DMMAs, instead of two loads per DMMA)
-      for (int ks = 0; 4 * ks < K; ++ks) {
-        const int z = 4 * ks + t;
+      for (int z0 = 4 * kg; z0 < K; z0 += 4 * WK) {
+        const int z = z0 + t;
         const bool zok = z < K;
-        double av[kNuRows], bv[kNuCols];
+        double av[SI], bv[S];
 #pragma unroll
-        for (int i = 0; i < kNuRows; ++i) {
-          const int row = 8 * (warp + kNuWarps * i) + g;
-          av[i] = (zok && row < m) ? sa[z * mp + row] : 0.0;
+        for (int i = 0; i < SI; ++i) {
+          const int row = 8 * (i0 + i) + g;
+          av[i] = (zok && row < m) ? sa[z * m + row] : 0.0;
         }
 #pragma unroll
-        for (int j = 0; j < kNuCols; ++j) {
+        for (int j = 0; j < S; ++j) {
           const int col = 8 * j + g;
-          bv[j] = (zok && j < sn && col < n) ? sb[col * b_pitch + z] : 0.0;
+          bv[j] = (zok && col < n) ? sb[col * b_pitch + z] : 0.0;
         }
 #pragma unroll
-        for (int i = 0; i < kNuRows; ++i) {
-          if (warp + kNuWarps * i >= sm_) break;
+        for (int i = 0; i < SI; ++i) {
+          if (i0 + i >= sm_) break;
 #pragma unroll
-          for (int j = 0; j < kNuCols; ++j) {
+          for (int j = 0; j < S; ++j) {
             if (j >= sn) break;
             nu_dmma(acc[i][j], av[i], bv[j]);
           }
@@ -183,23 +194,30 @@ __global__ void __launch_bounds__(kNuWarps * 32)
       __syncthreads();  // stage grp % kNuStages is refilled two groups on
     }
     asm volatile("cp.async.wait_group 0;" ::: "memory");
-    // epilogue: subtile (im = warp + 4i, j), lane (g, t) holds C(8 im + g, 8 j + 2t + jj)
+    // epilogue: subtile (i0 + i, j), lane (g, t) holds k-group kg's partial C(8(i0+i) + g, 8j + 2t + jj)
+    const int mp = 8 * sm_, np = 8 * sn;
+    double* red = nsm;
 #pragma unroll
-    for (int i = 0; i < kNuRows; ++i) {
-      const int row = 8 * (warp + kNuWarps * i) + g;
-      if (row >= m) continue;
+    for (int i = 0; i < SI; ++i) {
+      if (i0 + i >= sm_) break;
 #pragma unroll
-      for (int j = 0; j < kNuCols; ++j) {
+      for (int j = 0; j < S; ++j) {
+        if (j >= sn) break;
 #pragma unroll
-        for (int jj = 0; jj < 2; ++jj) {
-          const int col = 8 * j + 2 * t + jj;
-          if (col >= n) continue;
-          double* p = C + cb.off + (int64_t)col * m + row;
-          const double v = alpha * acc[i][j][jj];
-          *p = beta_first == 0.0 ? v : beta_first * *p + v;
-        }
+        for (int jj = 0; jj < 2; ++jj)
+          red[(kg * np + 8 * j + 2 * t + jj) * mp + 8 * (i0 + i) + g] = acc[i][j][jj];
       }
     }
+    __syncthreads();
+    for (int y = warp; y < n; y += kNuWarps)
+      for (int x = lane; x < m; x += 32) {
+        double v = red[y * mp + x];
+#pragma unroll
+        for (int w = 1; w < WK; ++w) v += red[(w * np + y) * mp + x];
+        double* p = C + cb.off + (int64_t)y * m + x;
+        v *= alpha;
+        *p = beta_first == 0.0 ? v : beta_first * *p + v;
+      }
     __syncthreads();  // the next run's first stages reuse the ring
   }
 }
@@ -236,7 +254,8 @@ void launch_nu_pack(const NUPack* tasks, int64_t ntasks, const double* src, doub
 
 size_t nu_smm_smem(int kcap, int mmax, int nmax) {
   const int kp = (kcap + 3) & ~3, mp = (mmax + 7) & ~7, np = (nmax + 7) & ~7;
-  return (size_t)kNuStages * ((size_t)kp * mp + (size_t)np * (kp + 1)) * 8;
+  const size_t ring = (size_t)kNuStages * ((size_t)kp * mp + (size_t)np * (kp + 1));
+  return std::max(ring, (size_t)kNuWarps * mp * np) * 8;  // (the epilogue's 4 partial C blocks reuse the ring)
 }
 
 cudaError_t launch_nu_smm(const int32_t* trip, int64_t nruns, int64_t kb, const double* A, const int64_t* aoff,
@@ -246,13 +265,15 @@ cudaError_t launch_nu_smm(const int32_t* trip, int64_t nruns, int64_t kb, const 
   if (nruns <= 0 || kb <= 0) return cudaSuccess;
   if (mmax > 64 || nmax > 64) return cudaErrorInvalidValue;  // the host checks: C blocks up to 64 x 64
   const size_t smem = nu_smm_smem(kcap, mmax, nmax);
-  static size_t attr = 0;
-  if (smem > 48 * 1024 && smem > attr) {
-    cudaError_t e = cudaFuncSetAttribute(nu_smm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const bool small = mmax <= 32 && nmax <= 32;  // 4 x 4 subtiles per warp, else 8 x 8
+  auto kern = small ? nu_smm_kernel<4, 1> : nu_smm_kernel<8, 2>;
+  static size_t attr[2] = {0, 0};
+  if (smem > 48 * 1024 && smem > attr[small]) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    attr = smem;
+    attr[small] = smem;
   }
-  nu_smm_kernel<<<(unsigned)std::min<int64_t>(nruns, (int64_t)num_sms() * 32), kNuWarps * 32, smem, st>>>(
+  kern<<<(unsigned)std::min<int64_t>(nruns, (int64_t)num_sms() * 32), kNuWarps * 32, smem, st>>>(
       trip, nruns, kb, A, aoff, B, boff, kdim, kofs, gbeg, ngroups, C, cblk, kcap, (mmax + 7) & ~7, (nmax + 7) & ~7,
       alpha, beta_first);
   return cudaGetLastError();

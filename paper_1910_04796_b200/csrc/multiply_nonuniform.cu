@@ -281,7 +281,11 @@ dbm_status nu_cache_get(dbm_ctx ctx, dbm_matrix A, dbm_matrix B, dbm_matrix C, b
   for (int64_t li = 0; li < p.mloc; ++li) nc->mmax = std::max(nc->mmax, (int)A->row_size(r + li * p.pr));
   for (int64_t lj = 0; lj < p.nloc; ++lj) nc->nmax = std::max(nc->nmax, (int)B->col_size(c + lj * p.pc));
   if (!dens) {  // entry groups of the small-block kernel: consecutive entries with summed k <= kcap
-    nc->kcap = std::max(nc->kmax, 32);
+    static const int kcap_env = [] {  // (tuning knob: DBM_NU_KCAP, default 32)
+      const char* e = getenv("DBM_NU_KCAP");
+      return e ? std::max(4, atoi(e)) : 32;
+    }();
+    nc->kcap = std::max(nc->kmax, kcap_env);
     nc->o_kofs.assign(p.L, SIZE_MAX);
     nc->o_gbeg.assign(p.L, SIZE_MAX);
     nc->ngroups.assign(p.L, 0);

@@ -45,7 +45,7 @@ for s in "$@"; do
       done ;;
     ncu_nu_smm)
       step ncu_nu_smm 900 $NCU --set full --import-source on --clock-control none -k regex:nu_smm -c 1 \
-        -o gpurun_out/ncu_nu_smm -f python bench.py --config nu --path blocked --steps 1 --warmup 0 --no-e2e \
+        -o gpurun_out/ncu_nu_smm -f python bench.py --config nus --path blocked --steps 1 --warmup 0 --no-e2e \
         --no-cpu-baseline ;;
     ncu_dgemm_full)
       step ncu_dgemm_full 1500 $NCU --set full --import-source on --clock-control none -k regex:dgemm_tn -c 1 \

@@ -88,22 +88,28 @@ __device__ __forceinline__ void nu_dmma(double (&c)[2], double a, double b) {
 
 constexpr int kNuWarps = 4;
 constexpr int kNuStages = 3;
+constexpr int kNuZero = 64;  // doubles of zeros at the end of shared memory (the k tail's operand)
+
+// Stage layout (doubles), kp = kcap rounded up to 4: A tile kp * mmax | B tile kp * nmax | k table kp int2.
+__host__ __device__ inline int nu_stage_doubles(int kp, int mmax, int nmax) { return kp * (mmax + nmax + 1); }
 
 // One CTA per run (C block, m x n <= 64 x 64): acc(c) = sum over the run's entries of A_blk (m x k_e) *
 // B_blk (k_e x n), then C = (first ? beta*C : C) + alpha*acc.  The entries are taken in GROUPS
 // (host-computed from the k sizes, the same for every run of the step: group g = entries [gbeg[g],
 // gbeg[g+1]), their k sizes summing to at most kcap), entry e at k offset kofs[e] inside its group:
-//   * staging (all 128 threads, 8-byte cp.async, any alignment, into a 3-stage ring): every A block of a
-//     run has the run's m rows, so the group's A blocks, each m x k_e column-major, are ONE contiguous
-//     m x K_g column-major tile -- a flat copy; the B blocks (k_e x n column-major) go to the columns of an
-//     (n x K_g) K-contiguous tile, the column index of a flat element taken by a float reciprocal and one
-//     correction (no integer division);
+//   * staging (8-byte cp.async, any alignment, into a 3-stage ring; warp w copies entries w, w+4, ... of
+//     the group, lanes along the entry): both operands are FLAT copies -- every A block of a run has the
+//     run's m rows, so the group's A blocks, each m x k_e column-major, are one m x K_g column-major tile;
+//     the B blocks (k_e x n column-major) are laid end to end (entry e at ko_e n), and a k table gives,
+//     for every k index z of the group, the shared-memory offset of B(z, 0) and the column stride k_e;
 //   * compute: the warps split the group's K WK ways (k-step ks to k-group ks mod WK) and the subtile rows
 //     WR ways (WR WK = 4 warps); a warp holds SI subtile rows x all S subtile columns of the C block (8 x 8
 //     DMMA subtiles; blocks up to 32: S = 4, WR = 1, WK = 4; up to 64: S = 8, WR = 2, WK = 2, so the
-//     accumulators stay at 64 registers) and per k-step loads its A and B fragments once for all its
-//     DMMAs -- every warp busy whatever the block shape; rows >= m, columns >= n and k >= K_g are zeroed
-//     in registers;
+//     accumulators stay at 64 registers) and per k-step loads its A and B fragments once for all its DMMAs
+//     -- every warp busy whatever the block shape.  Fragment rows >= m and columns >= n read the block's
+//     last row / column (clamped offsets, computed once per run): they only feed accumulator rows /
+//     columns that are never stored.  k indices past the group's K read a zero region (A and B), so the
+//     tail adds exact zeros;
 //   * epilogue: the WK k-groups' partial C blocks meet in shared memory and are summed in k-group order
 //     (deterministic), then scaled into C.
 template <int S, int WR>
@@ -114,40 +120,50 @@ __global__ void __launch_bounds__(kNuWarps * 32)
                   int ngroups, double* __restrict__ C, const NUBlk* __restrict__ cblk, int kcap, int mmax_pad,
                   int nmax_pad, double alpha, double beta_first) {
   extern __shared__ __align__(16) double nsm[];
-  const int kcap_pad = (kcap + 3) & ~3;
-  const int a_st = kcap_pad * mmax_pad, b_pitch = kcap_pad + 1, b_st = nmax_pad * b_pitch;
   constexpr int WK = kNuWarps / WR, SI = S / WR;
+  const int kp = (kcap + 3) & ~3;
+  const int st_d = nu_stage_doubles(kp, mmax_pad, nmax_pad);
+  // past the ring and the epilogue's partial C blocks (zeroed once, never overwritten)
+  const int zero_off = max(kNuStages * st_d, kNuWarps * mmax_pad * nmax_pad);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
   const int rh = warp % WR, kg = warp / WR, i0 = rh * SI;
+  for (int i = threadIdx.x; i < kNuZero; i += blockDim.x) nsm[zero_off + i] = 0.0;
   for (int64_t run = blockIdx.x; run < nruns; run += gridDim.x) {
     const int32_t* rt = trip + 3 * run * kb;
     const NUBlk cb = cblk[rt[2]];
     const int m = cb.rows, n = cb.cols;
     const int sm_ = (m + 7) / 8, sn = (n + 7) / 8;
+    int rowc[SI], colc[S];  // clamped fragment rows / columns
+#pragma unroll
+    for (int i = 0; i < SI; ++i) rowc[i] = min(8 * (i0 + i) + g, m - 1);
+#pragma unroll
+    for (int j = 0; j < S; ++j) colc[j] = min(8 * j + g, n - 1);
     auto stage = [&](int grp, int buf) {  // group grp's blocks -> stage buf (an empty commit past the end)
       if (grp < ngroups) {
-        double* sa = nsm + buf * (a_st + b_st);
-        double* sb = sa + a_st;
-        for (int e = gbeg[grp]; e < gbeg[grp + 1]; ++e) {
+        const int sa_off = buf * st_d, sb_off = sa_off + kp * mmax_pad;
+        double* sa = nsm + sa_off;
+        double* sb = nsm + sb_off;
+        int2* zt = reinterpret_cast<int2*>(sb + kp * nmax_pad);
+        const int e1 = gbeg[grp + 1];
+        for (int e = gbeg[grp] + warp; e < e1; e += kNuWarps) {
           const int k = kdim[e], ko = kofs[e];
           const double* a = A + aoff[rt[3 * e]];
           const double* b = B + boff[rt[3 * e + 1]];
-          const int na = m * k, nb = k * n;
-          for (int q = threadIdx.x; q < na; q += kNuWarps * 32)  // A(x, z) at z*m + x -> sa[(ko+z)*m + x]
+          for (int q = lane; q < m * k; q += 32)  // A(x, z) at z*m + x -> sa[(ko+z)*m + x]
             asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(
                              (uint32_t)__cvta_generic_to_shared(sa + ko * m + q)),
                          "l"(a + q)
                          : "memory");
-          const float rk = 1.0f / (float)k;
-          for (int q = threadIdx.x; q < nb; q += kNuWarps * 32) {  // B(z, y) at y*k + z -> sb[y*b_pitch + ko+z]
-            int y = (int)(((float)q + 0.5f) * rk), z = q - y * k;
-            if (z < 0) --y, z += k;
-            if (z >= k) ++y, z -= k;
+          for (int q = lane; q < k * n; q += 32)  // B(z, y) at y*k + z -> sb[ko*n + y*k + z]
             asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(
-                             (uint32_t)__cvta_generic_to_shared(sb + y * b_pitch + ko + z)),
+                             (uint32_t)__cvta_generic_to_shared(sb + ko * n + q)),
                          "l"(b + q)
                          : "memory");
-          }
+          for (int z = lane; z < k; z += 32) zt[ko + z] = make_int2(sb_off + ko * n + z, k);
+        }
+        if (warp == kNuWarps - 1) {  // the k tail up to kp: the zero region, stride 0
+          const int K = kofs[e1 - 1] + kdim[e1 - 1];
+          if (K + lane < kp) zt[K + lane] = make_int2(zero_off, 0);
         }
       }
       asm volatile("cp.async.commit_group;" ::: "memory");
@@ -165,22 +181,18 @@ __global__ void __launch_bounds__(kNuWarps * 32)
       __syncthreads();
       const int ek = gbeg[grp + 1] - 1;
       const int K = kofs[ek] + kdim[ek];  // the group's concatenated K
-      const double* sa = nsm + (grp % kNuStages) * (a_st + b_st);
-      const double* sb = sa + a_st;
+      const int sa_off = (grp % kNuStages) * st_d;
+      const int2* zt = reinterpret_cast<const int2*>(nsm + sa_off + kp * (mmax_pad + nmax_pad));
       for (int z0 = 4 * kg; z0 < K; z0 += 4 * WK) {
         const int z = z0 + t;
-        const bool zok = z < K;
+        const int2 zi = zt[z];  // (z < kp: the table covers the tail)
+        const double* ap = nsm + (z < K ? sa_off + z * m : zero_off);
+        const double* bp = nsm + zi.x;
         double av[SI], bv[S];
 #pragma unroll
-        for (int i = 0; i < SI; ++i) {
-          const int row = 8 * (i0 + i) + g;
-          av[i] = (zok && row < m) ? sa[z * m + row] : 0.0;
-        }
+        for (int i = 0; i < SI; ++i) av[i] = ap[rowc[i]];
 #pragma unroll
-        for (int j = 0; j < S; ++j) {
-          const int col = 8 * j + g;
-          bv[j] = (zok && col < n) ? sb[col * b_pitch + z] : 0.0;
-        }
+        for (int j = 0; j < S; ++j) bv[j] = bp[colc[j] * zi.y];
 #pragma unroll
         for (int i = 0; i < SI; ++i) {
           if (i0 + i >= sm_) break;
@@ -254,8 +266,9 @@ void launch_nu_pack(const NUPack* tasks, int64_t ntasks, const double* src, doub
 
 size_t nu_smm_smem(int kcap, int mmax, int nmax) {
   const int kp = (kcap + 3) & ~3, mp = (mmax + 7) & ~7, np = (nmax + 7) & ~7;
-  const size_t ring = (size_t)kNuStages * ((size_t)kp * mp + (size_t)np * (kp + 1));
-  return std::max(ring, (size_t)kNuWarps * mp * np) * 8;  // (the epilogue's 4 partial C blocks reuse the ring)
+  const size_t ring = (size_t)kNuStages * nu_stage_doubles(kp, mp, np);
+  // (the epilogue's WK partial C blocks, at most 4 mp np doubles, reuse the ring; the zero region follows it)
+  return (std::max(ring, (size_t)kNuWarps * mp * np) + kNuZero) * 8;
 }
 
 cudaError_t launch_nu_smm(const int32_t* trip, int64_t nruns, int64_t kb, const double* A, const int64_t* aoff,

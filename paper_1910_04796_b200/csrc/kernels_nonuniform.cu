@@ -90,15 +90,18 @@ constexpr int kNuWarps = 4;
 constexpr int kNuStages = 3;
 constexpr int kNuZero = 64;  // doubles of zeros at the end of shared memory (the k tail's operand)
 
-// Stage layout (doubles), kp = kcap rounded up to 4: A tile kp * mmax | B tile kp * nmax | k table kp int2.
-__host__ __device__ inline int nu_stage_doubles(int kp, int mmax, int nmax) { return kp * (mmax + nmax + 1); }
+// Stage layout (doubles), kp = kcap rounded up to 4: A tile kp * mmax | B tile kp * nmax | k table kp int2 |
+// the group's K (one int).
+__host__ __device__ inline int nu_stage_doubles(int kp, int mmax, int nmax) { return kp * (mmax + nmax + 1) + 1; }
 
 // One CTA per run (C block, m x n <= 64 x 64): acc(c) = sum over the run's entries of A_blk (m x k_e) *
 // B_blk (k_e x n), then C = (first ? beta*C : C) + alpha*acc.  The entries are taken in GROUPS
 // (host-computed from the k sizes, the same for every run of the step: group g = entries [gbeg[g],
 // gbeg[g+1]), their k sizes summing to at most kcap), entry e at k offset kofs[e] inside its group:
 //   * staging (8-byte cp.async, any alignment, into a 3-stage ring; warp w copies entries w, w+4, ... of
-//     the group, lanes along the entry): both operands are FLAT copies -- every A block of a run has the
+//     the group, lanes along the entry, the entries' metadata -- k, k offset, A and B block addresses --
+//     loaded one entry per lane a group AHEAD, so the table lookups' latency hides under a group's
+//     compute): both operands are FLAT copies -- every A block of a run has the
 //     run's m rows, so the group's A blocks, each m x k_e column-major, are one m x K_g column-major tile;
 //     the B blocks (k_e x n column-major) are laid end to end (entry e at ko_e n), and a k table gives,
 //     for every k index z of the group, the shared-memory offset of B(z, 0) and the column stride k_e;
@@ -138,17 +141,37 @@ __global__ void __launch_bounds__(kNuWarps * 32)
     for (int i = 0; i < SI; ++i) rowc[i] = min(8 * (i0 + i) + g, m - 1);
 #pragma unroll
     for (int j = 0; j < S; ++j) colc[j] = min(8 * j + g, n - 1);
+    // the prefetched metadata of one group: this warp's entries gbeg + warp + 4 lane (pm_n of them) and
+    // the group's K
+    int pm_n = 0, pm_k = 0, pm_ko = 0, pm_K = 0;
+    const double *pm_a = A, *pm_b = B;
+    auto prefetch = [&](int grp) {
+      pm_n = 0;
+      if (grp < ngroups) {
+        const int gb = gbeg[grp], ge = gbeg[grp + 1];
+        pm_n = max(0, (ge - gb - warp + kNuWarps - 1) / kNuWarps);
+        pm_K = kofs[ge - 1] + kdim[ge - 1];
+        if (lane < pm_n) {
+          const int e = gb + warp + kNuWarps * lane;
+          pm_k = kdim[e];
+          pm_ko = kofs[e];
+          pm_a = A + aoff[rt[3 * e]];
+          pm_b = B + boff[rt[3 * e + 1]];
+        }
+      }
+    };
     auto stage = [&](int grp, int buf) {  // group grp's blocks -> stage buf (an empty commit past the end)
       if (grp < ngroups) {
         const int sa_off = buf * st_d, sb_off = sa_off + kp * mmax_pad;
         double* sa = nsm + sa_off;
         double* sb = nsm + sb_off;
         int2* zt = reinterpret_cast<int2*>(sb + kp * nmax_pad);
-        const int e1 = gbeg[grp + 1];
-        for (int e = gbeg[grp] + warp; e < e1; e += kNuWarps) {
-          const int k = kdim[e], ko = kofs[e];
-          const double* a = A + aoff[rt[3 * e]];
-          const double* b = B + boff[rt[3 * e + 1]];
+        for (int i = 0; i < pm_n; ++i) {
+          const int k = __shfl_sync(0xffffffffu, pm_k, i), ko = __shfl_sync(0xffffffffu, pm_ko, i);
+          const double* a = reinterpret_cast<const double*>(
+              __shfl_sync(0xffffffffu, reinterpret_cast<uintptr_t>(pm_a), i));
+          const double* b = reinterpret_cast<const double*>(
+              __shfl_sync(0xffffffffu, reinterpret_cast<uintptr_t>(pm_b), i));
           for (int q = lane; q < m * k; q += 32)  // A(x, z) at z*m + x -> sa[(ko+z)*m + x]
             asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(
                              (uint32_t)__cvta_generic_to_shared(sa + ko * m + q)),
@@ -161,9 +184,9 @@ __global__ void __launch_bounds__(kNuWarps * 32)
                          : "memory");
           for (int z = lane; z < k; z += 32) zt[ko + z] = make_int2(sb_off + ko * n + z, k);
         }
-        if (warp == kNuWarps - 1) {  // the k tail up to kp: the zero region, stride 0
-          const int K = kofs[e1 - 1] + kdim[e1 - 1];
-          if (K + lane < kp) zt[K + lane] = make_int2(zero_off, 0);
+        if (warp == kNuWarps - 1) {  // the k tail up to kp: the zero region, stride 0; the group's K
+          if (pm_K + lane < kp && lane < 4) zt[pm_K + lane] = make_int2(zero_off, 0);
+          if (lane == 0) reinterpret_cast<int*>(zt + kp)[0] = pm_K;
         }
       }
       asm volatile("cp.async.commit_group;" ::: "memory");
@@ -174,15 +197,19 @@ __global__ void __launch_bounds__(kNuWarps * 32)
 #pragma unroll
       for (int j = 0; j < S; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 #pragma unroll
-    for (int s = 0; s < kNuStages - 1; ++s) stage(s, s);
+    for (int s = 0; s < kNuStages - 1; ++s) {
+      prefetch(s);
+      stage(s, s);
+    }
+    prefetch(kNuStages - 1);
     for (int grp = 0; grp < ngroups; ++grp) {
       stage(grp + kNuStages - 1, (grp + kNuStages - 1) % kNuStages);
+      prefetch(grp + kNuStages);  // (in flight during this group's compute)
       asm volatile("cp.async.wait_group %0;" ::"n"(kNuStages - 1) : "memory");
       __syncthreads();
-      const int ek = gbeg[grp + 1] - 1;
-      const int K = kofs[ek] + kdim[ek];  // the group's concatenated K
       const int sa_off = (grp % kNuStages) * st_d;
       const int2* zt = reinterpret_cast<const int2*>(nsm + sa_off + kp * (mmax_pad + nmax_pad));
+      const int K = reinterpret_cast<const int*>(zt + kp)[0];  // the group's concatenated K
       for (int z0 = 4 * kg; z0 < K; z0 += 4 * WK) {
         const int z = z0 + t;
         const int2 zi = zt[z];  // (z < kp: the table covers the tail)

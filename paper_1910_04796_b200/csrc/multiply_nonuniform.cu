@@ -280,7 +280,8 @@ dbm_status nu_cache_get(dbm_ctx ctx, dbm_matrix A, dbm_matrix B, dbm_matrix C, b
   }
   for (int64_t li = 0; li < p.mloc; ++li) nc->mmax = std::max(nc->mmax, (int)A->row_size(r + li * p.pr));
   for (int64_t lj = 0; lj < p.nloc; ++lj) nc->nmax = std::max(nc->nmax, (int)B->col_size(c + lj * p.pc));
-  if (!dens) {  // entry groups of the small-block kernel: consecutive entries with summed k <= kcap
+  if (!dens) {  // entry groups of the small-block kernel: consecutive entries with summed k <= kcap (and
+              // at most kNuGroupMaxEntries of them)
     static const int kcap_env = [] {  // (tuning knob: DBM_NU_KCAP, default 32)
       const char* e = getenv("DBM_NU_KCAP");
       return e ? std::max(4, atoi(e)) : 32;
@@ -293,7 +294,7 @@ dbm_status nu_cache_get(dbm_ctx ctx, dbm_matrix A, dbm_matrix B, dbm_matrix C, b
       std::vector<int32_t> kofs, gbeg{0};
       int32_t acc = 0;
       for (size_t e = 0; e < kdims[k].size(); ++e) {
-        if (acc + kdims[k][e] > nc->kcap) {
+        if (acc + kdims[k][e] > nc->kcap || (int64_t)e - gbeg.back() == kNuGroupMaxEntries) {
           gbeg.push_back((int32_t)e);
           acc = 0;
         }

@@ -88,23 +88,57 @@ __device__ __forceinline__ void nu_dmma(double (&c)[2], double a, double b) {
 
 constexpr int kNuWarps = 4;
 constexpr int kNuStages = 3;
-constexpr int kNuZero = 64;  // doubles of zeros at the end of shared memory (the k tail's operand)
+constexpr int kNuZero = 64;  // doubles of zeros past the ring (the k tail's operand)
 
-// Stage layout (doubles), kp = kcap rounded up to 4: A tile kp * mmax | B tile kp * nmax | k table kp int2 |
-// the group's K (one int).
-__host__ __device__ inline int nu_stage_doubles(int kp, int mmax, int nmax) { return kp * (mmax + nmax + 1) + 1; }
+__device__ __forceinline__ void nu_mbar_init(uint32_t a, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(a), "r"(count) : "memory");
+}
+__device__ __forceinline__ void nu_mbar_arrive(uint32_t a) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(a) : "memory");
+}
+__device__ __forceinline__ void nu_mbar_arrive_tx(uint32_t a, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(a), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void nu_mbar_wait(uint32_t a, uint32_t parity) {
+  uint32_t done;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(a), "r"(parity)
+        : "memory");
+  } while (!done);
+}
+__device__ __forceinline__ void nu_bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t mbar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+               "l"(src), "r"(bytes), "r"(mbar)
+               : "memory");
+}
+
+// Stage layout (doubles), kp = kcap rounded up to 4, ne = the most entries a group holds: A region
+// kp mmax + 4 ne + 4 | B region kp nmax + 4 ne + 4 | k table kp int4 | the group's K (2 doubles, keeps
+// every region 16-B aligned).
+__host__ __device__ inline int nu_a_region(int kp, int mmax, int ne) { return kp * mmax + 4 * ne + 4; }
+__host__ __device__ inline int nu_stage_doubles(int kp, int mmax, int nmax, int ne) {
+  return nu_a_region(kp, mmax, ne) + nu_a_region(kp, nmax, ne) + 2 * kp + 2;
+}
+__host__ __device__ inline int nu_group_entries(int kp) { return kp < kNuGroupMaxEntries ? kp : kNuGroupMaxEntries; }
 
 // One CTA per run (C block, m x n <= 64 x 64): acc(c) = sum over the run's entries of A_blk (m x k_e) *
 // B_blk (k_e x n), then C = (first ? beta*C : C) + alpha*acc.  The entries are taken in GROUPS
 // (host-computed from the k sizes, the same for every run of the step: group g = entries [gbeg[g],
-// gbeg[g+1]), their k sizes summing to at most kcap), entry e at k offset kofs[e] inside its group:
-//   * staging (8-byte cp.async, any alignment, into a 3-stage ring; warp w copies entries w, w+4, ... of
-//     the group, lanes along the entry, the entries' metadata -- k, k offset, A and B block addresses --
-//     loaded one entry per lane a group AHEAD, so the table lookups' latency hides under a group's
-//     compute): both operands are FLAT copies -- every A block of a run has the
-//     run's m rows, so the group's A blocks, each m x k_e column-major, are one m x K_g column-major tile;
-//     the B blocks (k_e x n column-major) are laid end to end (entry e at ko_e n), and a k table gives,
-//     for every k index z of the group, the shared-memory offset of B(z, 0) and the column stride k_e;
+// gbeg[g+1]), their k sizes summing to at most kcap, at most kNuGroupMaxEntries of them), entry e at k
+// offset kofs[e] inside its group:
+//   * staging (TMA bulk copies into a 3-stage ring): lane l of warp w owns entry w + 4 l of the group; its
+//     metadata -- k, k offset, A and B block addresses -- is loaded a group AHEAD (the table lookups'
+//     latency hides under a group's compute), then the lane issues one cp.async.bulk per operand block,
+//     completing on its warp's mbarrier of the stage.  Blocks of odd element counts sit at any 8-B
+//     offset, so each copy takes the 16-B-aligned superset of its block (at most one extra double on
+//     either side, never outside the block's 16-B granules) into a 16-B-aligned slot with room for it;
+//     a k table gives, for every k index z of the group, the shared offsets of A(0, z) and B(z, 0) and
+//     the B column stride k_e.  No per-element staging instruction, and no L1 traffic;
 //   * compute: the warps split the group's K WK ways (k-step ks to k-group ks mod WK) and the subtile rows
 //     WR ways (WR WK = 4 warps); a warp holds SI subtile rows x all S subtile columns of the C block (8 x 8
 //     DMMA subtiles; blocks up to 32: S = 4, WR = 1, WK = 4; up to 64: S = 8, WR = 2, WK = 2, so the
@@ -123,14 +157,25 @@ __global__ void __launch_bounds__(kNuWarps * 32)
                   int ngroups, double* __restrict__ C, const NUBlk* __restrict__ cblk, int kcap, int mmax_pad,
                   int nmax_pad, double alpha, double beta_first) {
   extern __shared__ __align__(16) double nsm[];
+  __shared__ __align__(8) uint64_t nmb[kNuStages][kNuWarps];
   constexpr int WK = kNuWarps / WR, SI = S / WR;
-  const int kp = (kcap + 3) & ~3;
-  const int st_d = nu_stage_doubles(kp, mmax_pad, nmax_pad);
+  const int kp = (kcap + 3) & ~3, ne = nu_group_entries(kp);
+  const int a_reg = nu_a_region(kp, mmax_pad, ne), b_reg = nu_a_region(kp, nmax_pad, ne);
+  const int st_d = nu_stage_doubles(kp, mmax_pad, nmax_pad, ne);
   // past the ring and the epilogue's partial C blocks (zeroed once, never overwritten)
   const int zero_off = max(kNuStages * st_d, kNuWarps * mmax_pad * nmax_pad);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
   const int rh = warp % WR, kg = warp / WR, i0 = rh * SI;
+  const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(nsm);
+  const uint32_t mb0 = (uint32_t)__cvta_generic_to_shared(&nmb[0][0]);
   for (int i = threadIdx.x; i < kNuZero; i += blockDim.x) nsm[zero_off + i] = 0.0;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kNuStages * kNuWarps; ++i) nu_mbar_init(mb0 + 8 * i, 32);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  __syncthreads();
+  uint32_t phase = 0;  // bit s: the parity of stage s's next completion
   for (int64_t run = blockIdx.x; run < nruns; run += gridDim.x) {
     const int32_t* rt = trip + 3 * run * kb;
     const NUBlk cb = cblk[rt[2]];
@@ -141,18 +186,19 @@ __global__ void __launch_bounds__(kNuWarps * 32)
     for (int i = 0; i < SI; ++i) rowc[i] = min(8 * (i0 + i) + g, m - 1);
 #pragma unroll
     for (int j = 0; j < S; ++j) colc[j] = min(8 * j + g, n - 1);
-    // the prefetched metadata of one group: this warp's entries gbeg + warp + 4 lane (pm_n of them) and
-    // the group's K
-    int pm_n = 0, pm_k = 0, pm_ko = 0, pm_K = 0;
+    // the prefetched metadata of one group: this lane's entry gbeg + warp + 4 lane (if pm_has) and the
+    // group's K
+    bool pm_has = false;
+    int pm_k = 0, pm_ko = 0, pm_K = 0;
     const double *pm_a = A, *pm_b = B;
     auto prefetch = [&](int grp) {
-      pm_n = 0;
+      pm_has = false;
       if (grp < ngroups) {
         const int gb = gbeg[grp], ge = gbeg[grp + 1];
-        pm_n = max(0, (ge - gb - warp + kNuWarps - 1) / kNuWarps);
         pm_K = kofs[ge - 1] + kdim[ge - 1];
-        if (lane < pm_n) {
-          const int e = gb + warp + kNuWarps * lane;
+        const int e = gb + warp + kNuWarps * lane;
+        if (e < ge) {
+          pm_has = true;
           pm_k = kdim[e];
           pm_ko = kofs[e];
           pm_a = A + aoff[rt[3 * e]];
@@ -160,36 +206,30 @@ __global__ void __launch_bounds__(kNuWarps * 32)
         }
       }
     };
-    auto stage = [&](int grp, int buf) {  // group grp's blocks -> stage buf (an empty commit past the end)
-      if (grp < ngroups) {
-        const int sa_off = buf * st_d, sb_off = sa_off + kp * mmax_pad;
-        double* sa = nsm + sa_off;
-        double* sb = nsm + sb_off;
-        int2* zt = reinterpret_cast<int2*>(sb + kp * nmax_pad);
-        for (int i = 0; i < pm_n; ++i) {
-          const int k = __shfl_sync(0xffffffffu, pm_k, i), ko = __shfl_sync(0xffffffffu, pm_ko, i);
-          const double* a = reinterpret_cast<const double*>(
-              __shfl_sync(0xffffffffu, reinterpret_cast<uintptr_t>(pm_a), i));
-          const double* b = reinterpret_cast<const double*>(
-              __shfl_sync(0xffffffffu, reinterpret_cast<uintptr_t>(pm_b), i));
-          for (int q = lane; q < m * k; q += 32)  // A(x, z) at z*m + x -> sa[(ko+z)*m + x]
-            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(
-                             (uint32_t)__cvta_generic_to_shared(sa + ko * m + q)),
-                         "l"(a + q)
-                         : "memory");
-          for (int q = lane; q < k * n; q += 32)  // B(z, y) at y*k + z -> sb[ko*n + y*k + z]
-            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(
-                             (uint32_t)__cvta_generic_to_shared(sb + ko * n + q)),
-                         "l"(b + q)
-                         : "memory");
-          for (int z = lane; z < k; z += 32) zt[ko + z] = make_int2(sb_off + ko * n + z, k);
-        }
-        if (warp == kNuWarps - 1) {  // the k tail up to kp: the zero region, stride 0; the group's K
-          if (pm_K + lane < kp && lane < 4) zt[pm_K + lane] = make_int2(zero_off, 0);
-          if (lane == 0) reinterpret_cast<int*>(zt + kp)[0] = pm_K;
-        }
+    auto stage = [&](int grp, int buf) {  // group grp's blocks -> stage buf (nothing past the end)
+      if (grp >= ngroups) return;
+      const int so = buf * st_d;
+      int4* zt = reinterpret_cast<int4*>(nsm + so + a_reg + b_reg);
+      const uint32_t mb = mb0 + 8 * (buf * kNuWarps + warp);
+      if (pm_has) {
+        const int er = warp + kNuWarps * lane;  // the entry's index in its group
+        const uintptr_t as = reinterpret_cast<uintptr_t>(pm_a), bs = reinterpret_cast<uintptr_t>(pm_b);
+        const int ha = (int)((as >> 3) & 1), hb = (int)((bs >> 3) & 1);  // doubles before the block
+        const int ao = so + ((pm_ko * m + 4 * er + 1) & ~1);
+        const int bo = so + a_reg + ((pm_ko * n + 4 * er + 1) & ~1);
+        const uint32_t na = (uint32_t)((ha + m * pm_k) * 8 + 15) & ~15u;
+        const uint32_t nb = (uint32_t)((hb + pm_k * n) * 8 + 15) & ~15u;
+        nu_mbar_arrive_tx(mb, na + nb);
+        nu_bulk_g2s(sbase + 8 * ao, reinterpret_cast<const void*>(as & ~(uintptr_t)15), na, mb);
+        nu_bulk_g2s(sbase + 8 * bo, reinterpret_cast<const void*>(bs & ~(uintptr_t)15), nb, mb);
+        for (int z = 0; z < pm_k; ++z) zt[pm_ko + z] = make_int4(ao + ha + z * m, bo + hb + z, pm_k, 0);
+      } else {
+        nu_mbar_arrive(mb);
       }
-      asm volatile("cp.async.commit_group;" ::: "memory");
+      if (warp == kNuWarps - 1) {  // the k tail up to a multiple of 4: the zero region, stride 0; the K
+        if (lane < 4 && pm_K + lane < kp) zt[pm_K + lane] = make_int4(zero_off, zero_off, 0, 0);
+        if (lane == 0) reinterpret_cast<int*>(zt + kp)[0] = pm_K;
+      }
     };
     double acc[SI][S][2];
 #pragma unroll
@@ -205,21 +245,22 @@ __global__ void __launch_bounds__(kNuWarps * 32)
     for (int grp = 0; grp < ngroups; ++grp) {
       stage(grp + kNuStages - 1, (grp + kNuStages - 1) % kNuStages);
       prefetch(grp + kNuStages);  // (in flight during this group's compute)
-      asm volatile("cp.async.wait_group %0;" ::"n"(kNuStages - 1) : "memory");
-      __syncthreads();
-      const int sa_off = (grp % kNuStages) * st_d;
-      const int2* zt = reinterpret_cast<const int2*>(nsm + sa_off + kp * (mmax_pad + nmax_pad));
+      const int buf = grp % kNuStages;
+#pragma unroll
+      for (int w = 0; w < kNuWarps; ++w) nu_mbar_wait(mb0 + 8 * (buf * kNuWarps + w), (phase >> buf) & 1);
+      phase ^= 1u << buf;
+      __syncthreads();  // (the k table and K are generic stores)
+      const int4* zt = reinterpret_cast<const int4*>(nsm + buf * st_d + a_reg + b_reg);
       const int K = reinterpret_cast<const int*>(zt + kp)[0];  // the group's concatenated K
       for (int z0 = 4 * kg; z0 < K; z0 += 4 * WK) {
-        const int z = z0 + t;
-        const int2 zi = zt[z];  // (z < kp: the table covers the tail)
-        const double* ap = nsm + (z < K ? sa_off + z * m : zero_off);
-        const double* bp = nsm + zi.x;
+        const int4 zi = zt[z0 + t];  // (z0 + t < kp: the table covers the tail)
+        const double* ap = nsm + zi.x;
+        const double* bp = nsm + zi.y;
         double av[SI], bv[S];
 #pragma unroll
         for (int i = 0; i < SI; ++i) av[i] = ap[rowc[i]];
 #pragma unroll
-        for (int j = 0; j < S; ++j) bv[j] = bp[colc[j] * zi.y];
+        for (int j = 0; j < S; ++j) bv[j] = bp[colc[j] * zi.z];
 #pragma unroll
         for (int i = 0; i < SI; ++i) {
           if (i0 + i >= sm_) break;
@@ -230,9 +271,8 @@ __global__ void __launch_bounds__(kNuWarps * 32)
           }
         }
       }
-      __syncthreads();  // stage grp % kNuStages is refilled two groups on
+      __syncthreads();  // stage buf is refilled two groups on
     }
-    asm volatile("cp.async.wait_group 0;" ::: "memory");
     // epilogue: subtile (i0 + i, j), lane (g, t) holds k-group kg's partial C(8(i0+i) + g, 8j + 2t + jj)
     const int mp = 8 * sm_, np = 8 * sn;
     double* red = nsm;
@@ -257,7 +297,9 @@ __global__ void __launch_bounds__(kNuWarps * 32)
         v *= alpha;
         *p = beta_first == 0.0 ? v : beta_first * *p + v;
       }
-    __syncthreads();  // the next run's first stages reuse the ring
+    // the next run's bulk copies (async proxy) overwrite what the epilogue wrote and read (generic proxy)
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncthreads();
   }
 }
 
@@ -293,7 +335,7 @@ void launch_nu_pack(const NUPack* tasks, int64_t ntasks, const double* src, doub
 
 size_t nu_smm_smem(int kcap, int mmax, int nmax) {
   const int kp = (kcap + 3) & ~3, mp = (mmax + 7) & ~7, np = (nmax + 7) & ~7;
-  const size_t ring = (size_t)kNuStages * nu_stage_doubles(kp, mp, np);
+  const size_t ring = (size_t)kNuStages * nu_stage_doubles(kp, mp, np, nu_group_entries(kp));
   // (the epilogue's WK partial C blocks, at most 4 mp np doubles, reuse the ring; the zero region follows it)
   return (std::max(ring, (size_t)kNuWarps * mp * np) + kNuZero) * 8;
 }

@@ -177,8 +177,9 @@ void launch_nu_pack(const NUPack* tasks, int64_t ntasks, const double* src, doub
 // Entries grouped per stage: kdim[e] = k size of the run's entry e, kofs[e] = its k offset inside its group,
 // groups g = entries [gbeg[g], gbeg[g+1]) (host-computed; every run of a step has the same k sizes)
 // Entry groups of the non-uniform small-block kernel hold at most this many entries (its 4 warps load a
-// group's entry metadata one entry per lane).
-constexpr int kNuGroupMaxEntries = 128;
+// group's entry metadata one entry per lane; each entry reserves 4 doubles of alignment room per operand
+// in a stage, so the bound keeps 4 CTAs' rings of 32 x 32 blocks within an SM's shared memory).
+constexpr int kNuGroupMaxEntries = 16;
 size_t nu_smm_smem(int kcap, int mmax, int nmax);
 cudaError_t launch_nu_smm(const int32_t* trip, int64_t nruns, int64_t kb, const double* A, const int64_t* aoff,
                           const double* B, const int64_t* boff, const int32_t* kdim, const int32_t* kofs,

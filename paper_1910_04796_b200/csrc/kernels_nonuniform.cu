@@ -132,8 +132,9 @@ __host__ __device__ inline int nu_group_entries(int kp) { return kp < kNuGroupMa
 // gbeg[g+1]), their k sizes summing to at most kcap, at most kNuGroupMaxEntries of them), entry e at k
 // offset kofs[e] inside its group:
 //   * staging (TMA bulk copies into a 3-stage ring): lane l of warp w owns entry w + 4 l of the group; its
-//     metadata -- k, k offset, A and B block addresses -- is loaded a group AHEAD (the table lookups'
-//     latency hides under a group's compute), then the lane issues one cp.async.bulk per operand block,
+//     metadata -- k, k offset, trip slots, then A and B block addresses -- is loaded in two levels, two
+//     and one groups ahead (each dependent lookup's latency hides under a group's compute), then the
+//     lane issues one cp.async.bulk per operand block,
 //     completing on its warp's mbarrier of the stage.  Blocks of odd element counts sit at any 8-B
 //     offset, so each copy takes the 16-B-aligned superset of its block (at most one extra double on
 //     either side, never outside the block's 16-B granules) into a 16-B-aligned slot with room for it;
@@ -186,24 +187,36 @@ __global__ void __launch_bounds__(kNuWarps * 32)
     for (int i = 0; i < SI; ++i) rowc[i] = min(8 * (i0 + i) + g, m - 1);
 #pragma unroll
     for (int j = 0; j < S; ++j) colc[j] = min(8 * j + g, n - 1);
-    // the prefetched metadata of one group: this lane's entry gbeg + warp + 4 lane (if pm_has) and the
-    // group's K
-    bool pm_has = false;
-    int pm_k = 0, pm_ko = 0, pm_K = 0;
+    // A group's metadata in two levels, a group apart: level 1 (this lane's entry e = gbeg + warp + 4 lane:
+    // k, k offset, the trip's A / B slots; the group's K), then level 2 (the blocks' addresses, from the
+    // slot offset tables).  Group g + 4's level 1 and g + 3's level 2 are in flight while group g computes,
+    // so each dependent lookup has a whole group's compute to land.
+    bool l1_has = false, pm_has = false;
+    int l1_k = 0, l1_ko = 0, l1_K = 0, l1_sa = 0, l1_sb = 0, pm_k = 0, pm_ko = 0, pm_K = 0;
     const double *pm_a = A, *pm_b = B;
-    auto prefetch = [&](int grp) {
-      pm_has = false;
+    auto fetch1 = [&](int grp) {
+      l1_has = false;
       if (grp < ngroups) {
         const int gb = gbeg[grp], ge = gbeg[grp + 1];
-        pm_K = kofs[ge - 1] + kdim[ge - 1];
+        l1_K = kofs[ge - 1] + kdim[ge - 1];
         const int e = gb + warp + kNuWarps * lane;
         if (e < ge) {
-          pm_has = true;
-          pm_k = kdim[e];
-          pm_ko = kofs[e];
-          pm_a = A + aoff[rt[3 * e]];
-          pm_b = B + boff[rt[3 * e + 1]];
+          l1_has = true;
+          l1_k = kdim[e];
+          l1_ko = kofs[e];
+          l1_sa = rt[3 * e];
+          l1_sb = rt[3 * e + 1];
         }
+      }
+    };
+    auto fetch2 = [&]() {
+      pm_has = l1_has;
+      pm_k = l1_k;
+      pm_ko = l1_ko;
+      pm_K = l1_K;
+      if (l1_has) {
+        pm_a = A + aoff[l1_sa];
+        pm_b = B + boff[l1_sb];
       }
     };
     auto stage = [&](int grp, int buf) {  // group grp's blocks -> stage buf (nothing past the end)
@@ -238,13 +251,17 @@ __global__ void __launch_bounds__(kNuWarps * 32)
       for (int j = 0; j < S; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 #pragma unroll
     for (int s = 0; s < kNuStages - 1; ++s) {
-      prefetch(s);
+      fetch1(s);
+      fetch2();
       stage(s, s);
     }
-    prefetch(kNuStages - 1);
+    fetch1(kNuStages - 1);
+    fetch2();
+    fetch1(kNuStages);
     for (int grp = 0; grp < ngroups; ++grp) {
       stage(grp + kNuStages - 1, (grp + kNuStages - 1) % kNuStages);
-      prefetch(grp + kNuStages);  // (in flight during this group's compute)
+      fetch2();                   // group grp + 3's addresses
+      fetch1(grp + kNuStages + 1);  // group grp + 4's entries (both in flight during this group's compute)
       const int buf = grp % kNuStages;
 #pragma unroll
       for (int w = 0; w < kNuWarps; ++w) nu_mbar_wait(mb0 + 8 * (buf * kNuWarps + w), (phase >> buf) & 1);

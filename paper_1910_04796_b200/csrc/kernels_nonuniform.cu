@@ -138,8 +138,10 @@ __host__ __device__ inline int nu_group_entries(int kp) { return kp < kNuGroupMa
 //     completing on its warp's mbarrier of the stage.  Blocks of odd element counts sit at any 8-B
 //     offset, so each copy takes the 16-B-aligned superset of its block (at most one extra double on
 //     either side, never outside the block's 16-B granules) into a 16-B-aligned slot with room for it;
-//     a k table gives, for every k index z of the group, the shared offsets of A(0, z) and B(z, 0) and
-//     the B column stride k_e.  No per-element staging instruction, and no L1 traffic;
+//     a k table (written lane-parallel before the lanes arrive, so the stage's mbarriers publish it with
+//     the data) gives, for every k index z of the group, the shared offsets of A(0, z) and B(z, 0) and
+//     the B column stride k_e.  No per-element staging instruction, no L1 traffic, one CTA barrier per
+//     group (the ring's reuse);
 //   * compute: the warps split the group's K WK ways (k-step ks to k-group ks mod WK) and the subtile rows
 //     WR ways (WR WK = 4 warps); a warp holds SI subtile rows x all S subtile columns of the C block (8 x 8
 //     DMMA subtiles; blocks up to 32: S = 4, WR = 1, WK = 4; up to 64: S = 8, WR = 2, WK = 2, so the
@@ -224,24 +226,31 @@ __global__ void __launch_bounds__(kNuWarps * 32)
       const int so = buf * st_d;
       int4* zt = reinterpret_cast<int4*>(nsm + so + a_reg + b_reg);
       const uint32_t mb = mb0 + 8 * (buf * kNuWarps + warp);
+      const int er = warp + kNuWarps * lane;  // this lane's entry's index in its group
+      const uintptr_t as = reinterpret_cast<uintptr_t>(pm_a), bs = reinterpret_cast<uintptr_t>(pm_b);
+      const int ha = (int)((as >> 3) & 1), hb = (int)((bs >> 3) & 1);  // doubles before the block
+      const int ao = so + ((pm_ko * m + 4 * er + 1) & ~1);
+      const int bo = so + a_reg + ((pm_ko * n + 4 * er + 1) & ~1);
+      // the k table, lane-parallel: the warp's entries are its lanes 0 .. c-1
+      const int c = __popc(__ballot_sync(0xffffffffu, pm_has));
+      for (int i = 0; i < c; ++i) {
+        const int k = __shfl_sync(0xffffffffu, pm_k, i), ko = __shfl_sync(0xffffffffu, pm_ko, i);
+        const int a0 = __shfl_sync(0xffffffffu, ao + ha, i), b0 = __shfl_sync(0xffffffffu, bo + hb, i);
+        for (int z = lane; z < k; z += 32) zt[ko + z] = make_int4(a0 + z * m, b0 + z, k, 0);
+      }
+      if (warp == kNuWarps - 1) {  // the k tail up to a multiple of 4: the zero region, stride 0; the K
+        if (lane < 4 && pm_K + lane < kp) zt[pm_K + lane] = make_int4(zero_off, zero_off, 0, 0);
+        if (lane == 0) reinterpret_cast<int*>(zt + kp)[0] = pm_K;
+      }
+      // every lane arrives after its table stores (release; the consumers' wait acquires them)
       if (pm_has) {
-        const int er = warp + kNuWarps * lane;  // the entry's index in its group
-        const uintptr_t as = reinterpret_cast<uintptr_t>(pm_a), bs = reinterpret_cast<uintptr_t>(pm_b);
-        const int ha = (int)((as >> 3) & 1), hb = (int)((bs >> 3) & 1);  // doubles before the block
-        const int ao = so + ((pm_ko * m + 4 * er + 1) & ~1);
-        const int bo = so + a_reg + ((pm_ko * n + 4 * er + 1) & ~1);
         const uint32_t na = (uint32_t)((ha + m * pm_k) * 8 + 15) & ~15u;
         const uint32_t nb = (uint32_t)((hb + pm_k * n) * 8 + 15) & ~15u;
         nu_mbar_arrive_tx(mb, na + nb);
         nu_bulk_g2s(sbase + 8 * ao, reinterpret_cast<const void*>(as & ~(uintptr_t)15), na, mb);
         nu_bulk_g2s(sbase + 8 * bo, reinterpret_cast<const void*>(bs & ~(uintptr_t)15), nb, mb);
-        for (int z = 0; z < pm_k; ++z) zt[pm_ko + z] = make_int4(ao + ha + z * m, bo + hb + z, pm_k, 0);
       } else {
         nu_mbar_arrive(mb);
-      }
-      if (warp == kNuWarps - 1) {  // the k tail up to a multiple of 4: the zero region, stride 0; the K
-        if (lane < 4 && pm_K + lane < kp) zt[pm_K + lane] = make_int4(zero_off, zero_off, 0, 0);
-        if (lane == 0) reinterpret_cast<int*>(zt + kp)[0] = pm_K;
       }
     };
     double acc[SI][S][2];
@@ -266,7 +275,6 @@ __global__ void __launch_bounds__(kNuWarps * 32)
 #pragma unroll
       for (int w = 0; w < kNuWarps; ++w) nu_mbar_wait(mb0 + 8 * (buf * kNuWarps + w), (phase >> buf) & 1);
       phase ^= 1u << buf;
-      __syncthreads();  // (the k table and K are generic stores)
       const int4* zt = reinterpret_cast<const int4*>(nsm + buf * st_d + a_reg + b_reg);
       const int K = reinterpret_cast<const int*>(zt + kp)[0];  // the group's concatenated K
       for (int z0 = 4 * kg; z0 < K; z0 += 4 * WK) {

@@ -126,6 +126,27 @@ __host__ __device__ inline int nu_stage_doubles(int kp, int mmax, int nmax, int 
 }
 __host__ __device__ inline int nu_group_entries(int kp) { return kp < kNuGroupMaxEntries ? kp : kNuGroupMaxEntries; }
 
+// A warp's k-loop over one staged group for a run of R x Cn subtiles (all of them: one row group, WR = 1):
+// per k-step one k-table entry, R A and Cn B fragments, R Cn DMMAs, no shape branches.
+template <int R, int Cn, int S>
+__device__ __forceinline__ void nu_kloop(double (&acc)[S][S][2], const int4* zt, int K, int z_first, int z_step,
+                                         int t, const int (&rowc)[S], const int (&colc)[S], const double* nsm) {
+  for (int z0 = z_first; z0 < K; z0 += z_step) {
+    const int4 zi = zt[z0 + t];  // (z0 + t < kp: the table covers the tail)
+    const double* ap = nsm + zi.x;
+    const double* bp = nsm + zi.y;
+    double av[R], bv[Cn];
+#pragma unroll
+    for (int i = 0; i < R; ++i) av[i] = ap[rowc[i]];
+#pragma unroll
+    for (int j = 0; j < Cn; ++j) bv[j] = bp[colc[j] * zi.z];
+#pragma unroll
+    for (int i = 0; i < R; ++i)
+#pragma unroll
+      for (int j = 0; j < Cn; ++j) nu_dmma(acc[i][j], av[i], bv[j]);
+  }
+}
+
 // One CTA per run (C block, m x n <= 64 x 64): acc(c) = sum over the run's entries of A_blk (m x k_e) *
 // B_blk (k_e x n), then C = (first ? beta*C : C) + alpha*acc.  The entries are taken in GROUPS
 // (host-computed from the k sizes, the same for every run of the step: group g = entries [gbeg[g],
@@ -146,7 +167,8 @@ __host__ __device__ inline int nu_group_entries(int kp) { return kp < kNuGroupMa
 //     WR ways (WR WK = 4 warps); a warp holds SI subtile rows x all S subtile columns of the C block (8 x 8
 //     DMMA subtiles; blocks up to 32: S = 4, WR = 1, WK = 4; up to 64: S = 8, WR = 2, WK = 2, so the
 //     accumulators stay at 64 registers) and per k-step loads its A and B fragments once for all its DMMAs
-//     -- every warp busy whatever the block shape.  Fragment rows >= m and columns >= n read the block's
+//     -- every warp busy whatever the block shape; for blocks up to 32 the k-loop is instantiated per
+//     subtile shape (1..4 x 1..4, a switch per group), so it issues only the run's fragments and DMMAs.  Fragment rows >= m and columns >= n read the block's
 //     last row / column (clamped offsets, computed once per run): they only feed accumulator rows /
 //     columns that are never stored.  k indices past the group's K read a zero region (A and B), so the
 //     tail adds exact zeros;
@@ -277,22 +299,38 @@ __global__ void __launch_bounds__(kNuWarps * 32)
       phase ^= 1u << buf;
       const int4* zt = reinterpret_cast<const int4*>(nsm + buf * st_d + a_reg + b_reg);
       const int K = reinterpret_cast<const int*>(zt + kp)[0];  // the group's concatenated K
-      for (int z0 = 4 * kg; z0 < K; z0 += 4 * WK) {
-        const int4 zi = zt[z0 + t];  // (z0 + t < kp: the table covers the tail)
-        const double* ap = nsm + zi.x;
-        const double* bp = nsm + zi.y;
-        double av[SI], bv[S];
+      if constexpr (WR == 1) {  // blocks up to 32 x 32: the k-loop specialised on the run's subtile shape
+        const int shape = (sm_ - 1) * S + (sn - 1);
+#define NU_K(R_, C_)                                                        \
+  case (R_ - 1) * S + (C_ - 1):                                             \
+    nu_kloop<R_, C_, S>(acc, zt, K, 4 * kg, 4 * WK, t, rowc, colc, nsm); \
+    break;
+        switch (shape) {
+          NU_K(1, 1) NU_K(1, 2) NU_K(1, 3) NU_K(1, 4)
+          NU_K(2, 1) NU_K(2, 2) NU_K(2, 3) NU_K(2, 4)
+          NU_K(3, 1) NU_K(3, 2) NU_K(3, 3) NU_K(3, 4)
+          NU_K(4, 1) NU_K(4, 2) NU_K(4, 3) NU_K(4, 4)
+          default: break;
+        }
+#undef NU_K
+      } else {
+        for (int z0 = 4 * kg; z0 < K; z0 += 4 * WK) {
+          const int4 zi = zt[z0 + t];  // (z0 + t < kp: the table covers the tail)
+          const double* ap = nsm + zi.x;
+          const double* bp = nsm + zi.y;
+          double av[SI], bv[S];
 #pragma unroll
-        for (int i = 0; i < SI; ++i) av[i] = ap[rowc[i]];
+          for (int i = 0; i < SI; ++i) av[i] = ap[rowc[i]];
 #pragma unroll
-        for (int j = 0; j < S; ++j) bv[j] = bp[colc[j] * zi.z];
+          for (int j = 0; j < S; ++j) bv[j] = bp[colc[j] * zi.z];
 #pragma unroll
-        for (int i = 0; i < SI; ++i) {
-          if (i0 + i >= sm_) break;
+          for (int i = 0; i < SI; ++i) {
+            if (i0 + i >= sm_) break;
 #pragma unroll
-          for (int j = 0; j < S; ++j) {
-            if (j >= sn) break;
-            nu_dmma(acc[i][j], av[i], bv[j]);
+            for (int j = 0; j < S; ++j) {
+              if (j >= sn) break;
+              nu_dmma(acc[i][j], av[i], bv[j]);
+            }
           }
         }
       }

@@ -248,29 +248,33 @@ __global__ void __launch_bounds__(kNuWarps * 32)
       const int so = buf * st_d;
       int4* zt = reinterpret_cast<int4*>(nsm + so + a_reg + b_reg);
       const uint32_t mb = mb0 + 8 * (buf * kNuWarps + warp);
-      const int er = warp + kNuWarps * lane;  // this lane's entry's index in its group
-      const uintptr_t as = reinterpret_cast<uintptr_t>(pm_a), bs = reinterpret_cast<uintptr_t>(pm_b);
-      const int ha = (int)((as >> 3) & 1), hb = (int)((bs >> 3) & 1);  // doubles before the block
-      const int ao = so + ((pm_ko * m + 4 * er + 1) & ~1);
-      const int bo = so + a_reg + ((pm_ko * n + 4 * er + 1) & ~1);
-      // the k table, lane-parallel: the warp's entries are its lanes 0 .. c-1
-      const int c = __popc(__ballot_sync(0xffffffffu, pm_has));
-      for (int i = 0; i < c; ++i) {
-        const int k = __shfl_sync(0xffffffffu, pm_k, i), ko = __shfl_sync(0xffffffffu, pm_ko, i);
-        const int a0 = __shfl_sync(0xffffffffu, ao + ha, i), b0 = __shfl_sync(0xffffffffu, bo + hb, i);
-        for (int z = lane; z < k; z += 32) zt[ko + z] = make_int4(a0 + z * m, b0 + z, k, 0);
-      }
       if (warp == kNuWarps - 1) {  // the k tail up to a multiple of 4: the zero region, stride 0; the K
         if (lane < 4 && pm_K + lane < kp) zt[pm_K + lane] = make_int4(zero_off, zero_off, 0, 0);
         if (lane == 0) reinterpret_cast<int*>(zt + kp)[0] = pm_K;
       }
-      // every lane arrives after its table stores (release; the consumers' wait acquires them)
-      if (pm_has) {
-        const uint32_t na = (uint32_t)((ha + m * pm_k) * 8 + 15) & ~15u;
-        const uint32_t nb = (uint32_t)((hb + pm_k * n) * 8 + 15) & ~15u;
-        nu_mbar_arrive_tx(mb, na + nb);
-        nu_bulk_g2s(sbase + 8 * ao, reinterpret_cast<const void*>(as & ~(uintptr_t)15), na, mb);
-        nu_bulk_g2s(sbase + 8 * bo, reinterpret_cast<const void*>(bs & ~(uintptr_t)15), nb, mb);
+      // the warp's entries are its lanes 0 .. c-1 (typically one or two warps of the four hold any)
+      const int c = __popc(__ballot_sync(0xffffffffu, pm_has));
+      if (c > 0) {
+        const int er = warp + kNuWarps * lane;  // this lane's entry's index in its group
+        const uintptr_t as = reinterpret_cast<uintptr_t>(pm_a), bs = reinterpret_cast<uintptr_t>(pm_b);
+        const int ha = (int)((as >> 3) & 1), hb = (int)((bs >> 3) & 1);  // doubles before the block
+        const int ao = so + ((pm_ko * m + 4 * er + 1) & ~1);
+        const int bo = so + a_reg + ((pm_ko * n + 4 * er + 1) & ~1);
+        for (int i = 0; i < c; ++i) {  // the k table, lane-parallel
+          const int k = __shfl_sync(0xffffffffu, pm_k, i), ko = __shfl_sync(0xffffffffu, pm_ko, i);
+          const int a0 = __shfl_sync(0xffffffffu, ao + ha, i), b0 = __shfl_sync(0xffffffffu, bo + hb, i);
+          for (int z = lane; z < k; z += 32) zt[ko + z] = make_int4(a0 + z * m, b0 + z, k, 0);
+        }
+        // every lane arrives after its table stores (release; the consumers' wait acquires them)
+        if (pm_has) {
+          const uint32_t na = (uint32_t)((ha + m * pm_k) * 8 + 15) & ~15u;
+          const uint32_t nb = (uint32_t)((hb + pm_k * n) * 8 + 15) & ~15u;
+          nu_mbar_arrive_tx(mb, na + nb);
+          nu_bulk_g2s(sbase + 8 * ao, reinterpret_cast<const void*>(as & ~(uintptr_t)15), na, mb);
+          nu_bulk_g2s(sbase + 8 * bo, reinterpret_cast<const void*>(bs & ~(uintptr_t)15), nb, mb);
+        } else {
+          nu_mbar_arrive(mb);
+        }
       } else {
         nu_mbar_arrive(mb);
       }

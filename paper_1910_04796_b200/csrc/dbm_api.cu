@@ -108,6 +108,7 @@ extern "C" dbm_status dbm_ctx_create(int nranks, int rank, int pr, int pc, const
   ctx->mycol = rank % pc;
   ctx->device = device;
   if (const char* hp = getenv("DBM_HOST_PIPE")) ctx->host_pipe = *hp != '0';  // measurement override
+  if (const char* dp = getenv("DBM_DEV_PIPE")) ctx->dev_pipe = *dp != '0';    // measurement override
   cudaError_t e = cudaSetDevice(device);
   ctx->stream = (cudaStream_t)cuda_stream;  // NULL = the legacy default stream (torch's default)
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->comm, cudaStreamNonBlocking);
@@ -1711,6 +1712,20 @@ dbm_status multiply_impl(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_matrix B, 
   // step-0 pull + GEMM run chunk by chunk, the pulls gated by the owners' published progress
   const bool hpipe = hio && ctx->nranks > 1 && ctx->transport == 0 && ctx->host_pipe && alpha != 0.0 && p.Kb > 0 &&
                      !A->sparse && !B->sparse && !C->sparse && memops(ctx->device).ok;
+  // the same pipeline for device-resident operands (no uploads): this rank's own panels are densified /
+  // packed chunk by chunk on the own-panel stream, each chunk's progress published at once, so the peers'
+  // step-0 pulls and this rank's step-0 GEMM / small-block chunks start behind the first chunk instead of
+  // behind the whole panel
+  const bool dpipe = !hio && ctx->nranks > 1 && ctx->transport == 0 && ctx->dev_pipe && alpha != 0.0 && p.Kb > 0 &&
+                     !A->sparse && !B->sparse && !C->sparse && memops(ctx->device).ok;
+  const bool pipe = hpipe || dpipe;
+  cudaEvent_t dpipe_e0 = nullptr;
+  if (dpipe) {
+    if (!ctx->own) CUDA_TRY(ctx, cudaStreamCreateWithFlags(&ctx->own, cudaStreamNonBlocking));
+    dpipe_e0 = get_event(ctx);
+    CUDA_TRY(ctx, cudaEventRecord(dpipe_e0, ctx->stream));  // previous work on the arenas is done
+    CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->own, dpipe_e0, 0));
+  }
   const bool hp_even = host_pipe_even(dens, p.bs);
   if (hpipe) {
     cudaEvent_t e0 = get_event(ctx);
@@ -1847,7 +1862,7 @@ dbm_status multiply_impl(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_matrix B, 
   }
 
   // ------------------------------------------------ own panels (densify or pack), on the compute stream
-  if (ctx->nranks > 1 && !hpipe) {
+  if (ctx->nranks > 1 && !pipe) {
     for (int k = 0; k < p.L; ++k) {  // A's own panels first: on host operands B may still be uploading
       if (p.ownA_off[k] != SIZE_MAX) {
         const int64_t col0 = (k - p.c) / p.pc, stride = p.L / p.pc;
@@ -1912,7 +1927,7 @@ dbm_status multiply_impl(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_matrix B, 
   std::vector<cudaEvent_t> own_ev;  // own panels' chunk j in place (own-panel stream)
   // own-panel stream: chunk j's densify / pack waits only for upload chunk j (the uploads stream on
   // ctx->up back to back); it never waits on a peer, so its progress signals keep the ordering rule
-  cudaStream_t up = hpipe ? ctx->own : nullptr;
+  cudaStream_t up = pipe ? ctx->own : nullptr;
   auto publish = [&](int j, bool final_) -> dbm_status {
     // every peer's table entry [me][operand][k] = (epoch, K-blocks of my panel k now in place)
     for (int q = 0; q < ctx->nranks; ++q) {
@@ -1928,7 +1943,7 @@ dbm_status multiply_impl(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_matrix B, 
     return DBM_OK;
   };
   auto own_panels_chunk = [&](int j) -> dbm_status {
-    CUDA_TRY(ctx, cudaStreamWaitEvent(up, hio->up_ev[j], 0));  // upload chunk j landed
+    if (hpipe) CUDA_TRY(ctx, cudaStreamWaitEvent(up, hio->up_ev[j], 0));  // upload chunk j landed
     for (int k = 0; k < p.L; ++k) {
       const int64_t q0 = host_pipe_bound(p.kb[k], j, hp_even), q1 = host_pipe_bound(p.kb[k], j + 1, hp_even);
       if (q1 <= q0) continue;
@@ -1974,7 +1989,7 @@ dbm_status multiply_impl(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_matrix B, 
     if (ctx->transport == 0) {
       ProfScope ps(ctx, ctx->comm, 5, 0.0, recv_bytes(s));  // copy-engine pulls of this step
       return post_pulls(ctx, p, peer_plan, s, ws, bufA_of[s], bufB_of[s], &st.bytes_sent, &st.bytes_recv,
-                        hpipe ? ep : 0);
+                        pipe ? ep : 0);
     }
     return post_exchange(ctx, p, s, ws, A->arena, B->arena, bufA_of[s], bufB_of[s], &st.bytes_sent, &st.bytes_recv);
   };
@@ -2001,7 +2016,7 @@ dbm_status multiply_impl(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_matrix B, 
         if (q != ctx->rank)
           peer_plan[q] = make_plan_raw(ctx->nranks, p.pr, p.pc, q / p.pc, q % p.pc, p.Mb, p.Nb, p.Kb, p.bs, dens,
                                        ctx->chunk_bytes, ctx->transport, p.b_packed, p.a_packed);
-      if (hpipe) {
+      if (pipe) {
         for (int j = 0; j < kHostPipeChunks; ++j) {
           if (dbm_status e = own_panels_chunk(j)) {
             // the peers drain instead of hanging (final progress + my "done"); the ctx is poisoned
@@ -2029,7 +2044,7 @@ dbm_status multiply_impl(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_matrix B, 
     // the first chunk's transfer is exposed.
     bool remote0 = p.a_src(0) != p.me() || p.b_src(0) != p.me();
     const int64_t kb0 = p.kb[p.kappa(0)];
-    if (hpipe) {  // the fixed host-pipeline chunks, even when both step-0 panels are local
+    if (pipe) {  // the fixed pipeline chunks, even when both step-0 panels are local
       cb0.resize(kHostPipeChunks + 1);
       for (int j = 0; j <= kHostPipeChunks; ++j) cb0[j] = host_pipe_bound(kb0, j, hp_even);
       nsub0 = kHostPipeChunks;
@@ -2043,7 +2058,7 @@ dbm_status multiply_impl(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_matrix B, 
       for (int j = 0; j < nsub0; ++j) {
         ev_c[j] = get_event(ctx);
         if (dbm_status e = post_pulls_chunk(ctx, p, peer_plan, 0, ws, bufA_of[0], bufB_of[0], cb0[j], cb0[j + 1],
-                                            j == 0, &st.bytes_sent, &st.bytes_recv, hpipe ? ep : 0))
+                                            j == 0, &st.bytes_sent, &st.bytes_recv, pipe ? ep : 0))
           return e;
         CUDA_TRY(ctx, cudaEventRecord(ev_c[j], ctx->comm));
       }
@@ -2065,7 +2080,7 @@ dbm_status multiply_impl(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_matrix B, 
     }
     const int64_t kbk = p.kb[k];
     if (hpipe && s == 0 && !dens) CUDA_TRY(ctx, cudaStreamWaitEvent(cs, hio->c_ev, 0));  // C_in (uploaded first)
-    if (hpipe && s == 1) CUDA_TRY(ctx, cudaStreamWaitEvent(cs, own_ev.back(), 0));  // all own panels in place
+    if (pipe && s == 1) CUDA_TRY(ctx, cudaStreamWaitEvent(cs, own_ev.back(), 0));  // all own panels in place
     // operand panels for this step
     const double* Ap;
     const double* Bp;
@@ -2154,7 +2169,7 @@ dbm_status multiply_impl(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_matrix B, 
         const int nsub = (s == 0) ? nsub0 : 1;
         for (int j = 0; j < nsub; ++j) {
           const int64_t k0 = nsub > 1 ? cb0[j] : 0, k1 = nsub > 1 ? cb0[j + 1] : kbk;
-          if (hpipe && s == 0) CUDA_TRY(ctx, cudaStreamWaitEvent(cs, own_ev[j], 0));  // my own panels' chunk j
+          if (pipe && s == 0) CUDA_TRY(ctx, cudaStreamWaitEvent(cs, own_ev[j], 0));  // my own panels' chunk j
           if (nsub > 1) CUDA_TRY(ctx, cudaStreamWaitEvent(cs, ev_c[j], 0));
           // host C: the multiply's last GEMM runs in row panels, each undensified and downloaded on the
           // copy stream while the next panel multiplies (as on one rank)
@@ -2227,7 +2242,7 @@ dbm_status multiply_impl(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_matrix B, 
       const int nsub = (s == 0) ? nsub0 : 1;
       for (int j = 0; j < nsub; ++j) {
         const int64_t k0 = nsub > 1 ? cb0[j] : 0, nk = nsub > 1 ? cb0[j + 1] - cb0[j] : kbk;
-        if (hpipe && s == 0) CUDA_TRY(ctx, cudaStreamWaitEvent(cs, own_ev[j], 0));  // my own panels' chunk j
+        if (pipe && s == 0) CUDA_TRY(ctx, cudaStreamWaitEvent(cs, own_ev[j], 0));  // my own panels' chunk j
         if (nsub > 1) CUDA_TRY(ctx, cudaStreamWaitEvent(cs, ev_c[j], 0));
         if (nk == 0) continue;  // (host pipeline, ragged K: empty leading chunks)
         const double* Aj = Ap + k0 * bb;
@@ -2305,7 +2320,7 @@ dbm_status multiply_impl(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_matrix B, 
   if (ctx->nranks > 1) {
     // the comm stream's last op covers every transfer of this rank (and the upload stream's own panels)
     CUDA_TRY(ctx, cudaStreamWaitEvent(cs, ev_x[p.L - 1], 0));
-    if (hpipe) CUDA_TRY(ctx, cudaStreamWaitEvent(cs, own_ev.back(), 0));
+    if (pipe) CUDA_TRY(ctx, cudaStreamWaitEvent(cs, own_ev.back(), 0));
   }
   if (dens && M * N > 0 && !(hio && hio->c_downloaded)) {
     if (hio && hio->c_ev) CUDA_TRY(ctx, cudaStreamWaitEvent(cs, hio->c_ev, 0));  // C_in uploaded
@@ -2340,6 +2355,7 @@ dbm_status multiply_impl(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_matrix B, 
     }
     for (int j = 0; j < nsub0 && nsub0 > 1; ++j) ctx->ev_pool.push_back(ev_c[j]);
     for (cudaEvent_t e : own_ev) ctx->ev_pool.push_back(e);
+    if (dpipe_e0) ctx->ev_pool.push_back(dpipe_e0);
     ctx->ev_pool.push_back(done);
   }
   ctx->launches += launches;

@@ -108,7 +108,7 @@ extern "C" dbm_status dbm_ctx_create(int nranks, int rank, int pr, int pc, const
   ctx->mycol = rank % pc;
   ctx->device = device;
   if (const char* hp = getenv("DBM_HOST_PIPE")) ctx->host_pipe = *hp != '0';  // measurement override
-  if (const char* dp = getenv("DBM_DEV_PIPE")) ctx->dev_pipe = *dp != '0';    // measurement override
+  if (const char* dp = getenv("DBM_DEV_PIPE")) ctx->dev_pipe = *dp != '0';    // opt-in (see multiply_impl)
   cudaError_t e = cudaSetDevice(device);
   ctx->stream = (cudaStream_t)cuda_stream;  // NULL = the legacy default stream (torch's default)
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->comm, cudaStreamNonBlocking);
@@ -1712,10 +1712,13 @@ dbm_status multiply_impl(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_matrix B, 
   // step-0 pull + GEMM run chunk by chunk, the pulls gated by the owners' published progress
   const bool hpipe = hio && ctx->nranks > 1 && ctx->transport == 0 && ctx->host_pipe && alpha != 0.0 && p.Kb > 0 &&
                      !A->sparse && !B->sparse && !C->sparse && memops(ctx->device).ok;
-  // the same pipeline for device-resident operands (no uploads): this rank's own panels are densified /
-  // packed chunk by chunk on the own-panel stream, each chunk's progress published at once, so the peers'
-  // step-0 pulls and this rank's step-0 GEMM / small-block chunks start behind the first chunk instead of
-  // behind the whole panel
+  // the same pipeline for device-resident operands (no uploads; opt-in, DBM_DEV_PIPE=1): this rank's own
+  // panels are densified / packed chunk by chunk on the own-panel stream, each chunk's progress published
+  // at once, so the peers' step-0 pulls and this rank's step-0 chunks start behind the first chunk instead
+  // of behind the whole panel.  Measured on 4 GPUs it loses on the rectangular configs (1,408^2 x
+  // 1,982,464 bs 64 128.5 -> 124.0 TFLOP/s, bs 22 blocked 116.4 -> 114.5): the later chunks' densify /
+  // pack kernels find no free SM beside the persistent GEMM / small-block kernel (its CTAs hold every
+  // SM's register file), so they run only in the gaps between chunks and the peers' pulls trail them.
   const bool dpipe = !hio && ctx->nranks > 1 && ctx->transport == 0 && ctx->dev_pipe && alpha != 0.0 && p.Kb > 0 &&
                      !A->sparse && !B->sparse && !C->sparse && memops(ctx->device).ok;
   const bool pipe = hpipe || dpipe;

@@ -199,7 +199,7 @@ struct dbm_ctx_s {
   cudaStream_t gen = nullptr; // stack generation of the next chunk beside the small-block GEMM (lazy)
   cudaStream_t own = nullptr; // host pipeline: own-panel densify / pack + progress signals (lazy)
   bool host_pipe = true;      // several ranks, host operands: chunked uploads gated by peer flags
-  bool dev_pipe = true;       // several ranks, device operands: own panels chunked, pulls gated by progress
+  bool dev_pipe = false;      // several ranks, device operands: own panels chunked, pulls gated by progress
   void* nccl = nullptr;  // ncclComm_t
   dbm_status poisoned = DBM_OK;
   int64_t launches = 0;

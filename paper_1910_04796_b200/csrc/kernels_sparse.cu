@@ -494,6 +494,164 @@ __global__ void __launch_bounds__(SpRunCfg<BS>::WARPS * 32, 1)
   }
 }
 
+// ---- bs 22 with TMA bulk staging (round 2): the per-run kernel's structure -- one warp per run, blocks at
+// their natural 22-double column pitch -- with each entry's A and B blocks fetched by two cp.async.bulk
+// copies (a 3,872-B block is 16-B aligned and a multiple of 16 B) issued by one lane into a 3-stage
+// per-warp ring that completes on the stage's mbarrier, instead of 242 16-B cp.async per block spread over
+// the lanes; the run's trip slots are loaded 32 entries at a time, one per lane (the next 32 in flight),
+// and handed to the issuing lane by shuffles, so no dependent global load sits between two entries.
+constexpr int kSpBulkStages = 3, kSpBulkWarps = 8;
+
+template <int BS>
+struct SpBulkCfg {
+  using R = SpRunCfg<BS>;
+  static_assert(R::TEAM == 1 && R::BB % 2 == 0 && R::P == BS && R::G == 1, "bulk staging: one warp per run, even bs^2");
+  static constexpr int STG = R::A_D + R::B_D;  // doubles (even: every stage and B region 16-B aligned)
+  static constexpr size_t SMEM = (size_t)kSpBulkWarps * kSpBulkStages * STG * 8;
+};
+
+template <int BS>
+__global__ void __launch_bounds__(kSpBulkWarps * 32, 1)
+    smm_sparse_bulk_kernel(const int32_t* __restrict__ trip, const int64_t* __restrict__ off, int64_t nruns,
+                           int64_t kb, const double* __restrict__ A, const double* __restrict__ B,
+                           double* __restrict__ C, double alpha, double beta_first) {
+  using R = SpRunCfg<BS>;
+  using Q = SpBulkCfg<BS>;
+  constexpr int MT = R::MT, BB = R::BB, S = kSpBulkStages;
+  extern __shared__ __align__(16) double sm[];
+  __shared__ __align__(8) uint64_t mbar[kSpBulkWarps][S];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+  double* ring = sm + (size_t)warp * S * Q::STG;
+  const uint32_t ring_s = (uint32_t)__cvta_generic_to_shared(ring);
+  const uint32_t mb0 = (uint32_t)__cvta_generic_to_shared(&mbar[warp][0]);
+  if (lane == 0) {
+    for (int i = 0; i < S; ++i)
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mb0 + 8 * i) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
+  uint32_t phase = 0;  // bit s: parity of stage s's next completion
+  int rowm[MT], coln[MT];
+#pragma unroll
+  for (int i = 0; i < MT; ++i) rowm[i] = coln[i] = i * 8 + g;
+  const int64_t nwarps = (int64_t)gridDim.x * kSpBulkWarps;
+  for (int64_t run = (int64_t)blockIdx.x * kSpBulkWarps + warp; run < nruns; run += nwarps) {
+    const int64_t e0 = off ? off[run] : run * kb, e1 = off ? off[run + 1] : e0 + kb;
+    if (e0 == e1) continue;
+    // trip slot window: lane l holds entry w0 + l's (A, B) slots, the next window's in flight
+    int64_t w0 = e0;
+    int ca = 0, cb = 0, na = 0, nb = 0;
+    if (e0 + lane < e1) ca = trip[3 * (e0 + lane)], cb = trip[3 * (e0 + lane) + 1];
+    if (e0 + 32 + lane < e1) na = trip[3 * (e0 + 32 + lane)], nb = trip[3 * (e0 + 32 + lane) + 1];
+    auto issue = [&](int64_t e, int si) {  // warp-uniform; entries issued in order e0, e0 + 1, ...
+      if (e >= w0 + 32) {
+        w0 += 32;
+        ca = na;
+        cb = nb;
+        const int64_t f = w0 + 32 + lane;
+        if (f < e1) na = trip[3 * f], nb = trip[3 * f + 1];
+      }
+      const int sa = __shfl_sync(0xffffffffu, ca, (int)(e - w0)), sb = __shfl_sync(0xffffffffu, cb, (int)(e - w0));
+      if (lane == 0) {
+        const uint32_t mb = mb0 + 8 * si, dst = ring_s + 8u * (uint32_t)(si * Q::STG);
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mb), "r"(2 * BB * 8) : "memory");
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                         dst),
+                     "l"(A + (int64_t)sa * BB), "r"(BB * 8), "r"(mb)
+                     : "memory");
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                         dst + 8u * R::A_D),
+                     "l"(B + (int64_t)sb * BB), "r"(BB * 8), "r"(mb)
+                     : "memory");
+      }
+    };
+    double acc[MT][MT][2];
+#pragma unroll
+    for (int i = 0; i < MT; ++i)
+#pragma unroll
+      for (int j = 0; j < MT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+#pragma unroll
+    for (int i = 0; i < S - 1; ++i)
+      if (e0 + i < e1) issue(e0 + i, i);
+    int si = 0;
+    for (int64_t e = e0; e < e1; ++e) {
+      if (e + S - 1 < e1) issue(e + S - 1, si == 0 ? S - 1 : si - 1);  // the stage entry e - 1 used
+      {
+        const uint32_t mb = mb0 + 8 * si, par = (phase >> si) & 1;
+        uint32_t done;
+        do {
+          asm volatile(
+              "{\n\t.reg .pred p;\n\t"
+              "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+              "selp.u32 %0, 1, 0, p;\n\t}"
+              : "=r"(done)
+              : "r"(mb), "r"(par)
+              : "memory");
+        } while (!done);
+        phase ^= 1u << si;
+      }
+      const double* sA = ring + si * Q::STG;  // (m, k) at k*BS + m
+      const double* sB = sA + R::A_D;         // (k, n) at n*BS + k
+#pragma unroll
+      for (int ks = 0; ks < (BS + 3) / 4; ++ks) {
+        const int k = 4 * ks + t;
+        const bool kok = (BS % 4 == 0) || k < BS;
+        double a[MT], b[MT];
+#pragma unroll
+        for (int mi = 0; mi < MT; ++mi) a[mi] = kok ? sA[k * BS + rowm[mi]] : 0.0;
+#pragma unroll
+        for (int ni = 0; ni < MT; ++ni) b[ni] = kok ? sB[coln[ni] * BS + k] : 0.0;
+#pragma unroll
+        for (int mi = 0; mi < MT; ++mi)
+#pragma unroll
+          for (int ni = 0; ni < MT; ++ni) sp_dmma(acc[mi][ni], a[mi], b[ni]);
+      }
+      __syncwarp();  // every lane is done with stage si before an issue refills it
+      si = si == S - 1 ? 0 : si + 1;
+    }
+    double* cbk = C + (int64_t)trip[3 * e0 + 2] * BB;
+#pragma unroll
+    for (int mi = 0; mi < MT; ++mi)
+#pragma unroll
+      for (int ni = 0; ni < MT; ++ni)
+#pragma unroll
+        for (int jj = 0; jj < 2; ++jj) {
+          const int m = rowm[mi], n = ni * 8 + 2 * t + jj;
+          if (m < BS && n < BS) {
+            double* p = cbk + m + n * BS;
+            const double ab = __dmul_rn(alpha, acc[mi][ni][jj]);
+            *p = beta_first == 1.0 ? __dadd_rn(*p, ab) : beta_first == 0.0 ? ab : fma(beta_first, *p, ab);
+          }
+        }
+  }
+}
+
+bool sp_bulk_on() {
+  static const bool on = [] {
+    const char* e = getenv("DBM_SP_BULK");
+    return !(e && *e == '0');
+  }();
+  return on;
+}
+
+template <int BS>
+cudaError_t launch_sp_bulk(const int32_t* trip, const int64_t* off, int64_t nruns, int64_t kb, const double* A,
+                           const double* B, double* C, double alpha, double beta_first, cudaStream_t st) {
+  using Q = SpBulkCfg<BS>;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(smm_sparse_bulk_kernel<BS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)Q::SMEM);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  const int64_t ctas = (nruns + kSpBulkWarps - 1) / kSpBulkWarps;
+  const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(ctas, (int64_t)num_sms()));
+  smm_sparse_bulk_kernel<BS><<<grid, kSpBulkWarps * 32, Q::SMEM, st>>>(trip, off, nruns, kb, A, B, C, alpha,
+                                                                      beta_first);
+  return cudaGetLastError();
+}
+
 // Any block size: one CTA per run, one thread per C element, FMA.
 __global__ void __launch_bounds__(256) smm_sparse_generic_kernel(int bs, const int32_t* __restrict__ trip,
                                                                  const int64_t* __restrict__ off, int64_t nruns,
@@ -554,7 +712,11 @@ cudaError_t launch_sp_run(const int32_t* trip, const int64_t* off, int64_t nruns
 template <int BS>
 cudaError_t launch_sp_tc(const int32_t* trip, const int64_t* off, int64_t nruns, const double* A, const double* B,
                          double* C, double alpha, cudaStream_t st) {
-  if (BS == 22) return launch_sp_run<BS>(trip, off, nruns, 0, A, B, C, alpha, 1.0, st);
+  if (BS == 22) {  // TMA bulk staging when both panels are 16-B aligned (blocks then are too: bs^2 even)
+    if (sp_bulk_on() && (((uintptr_t)A | (uintptr_t)B) & 15) == 0)
+      return launch_sp_bulk<22>(trip, off, nruns, 0, A, B, C, alpha, 1.0, st);
+    return launch_sp_run<BS>(trip, off, nruns, 0, A, B, C, alpha, 1.0, st);
+  }
   using Cfg = SpCfg<BS>;
   static bool attr = false;
   if (!attr) {

@@ -498,8 +498,8 @@ __global__ void __launch_bounds__(SpRunCfg<BS>::WARPS * 32, 1)
 // their natural 22-double column pitch -- with each entry's A and B blocks fetched by two cp.async.bulk
 // copies (a 3,872-B block is 16-B aligned and a multiple of 16 B) issued by one lane into a 3-stage
 // per-warp ring that completes on the stage's mbarrier, instead of 242 16-B cp.async per block spread over
-// the lanes; the run's trip slots are loaded 32 entries at a time, one per lane (the next 32 in flight),
-// and handed to the issuing lane by shuffles, so no dependent global load sits between two entries.
+// the lanes; the warp's runs stream through the ring as one sequence of entries, with every run's
+// metadata loaded one run ahead (see the kernel).
 constexpr int kSpBulkStages = 3, kSpBulkWarps = 8;
 
 template <int BS>
@@ -520,6 +520,7 @@ __global__ void __launch_bounds__(kSpBulkWarps * 32, 1)
   constexpr int MT = R::MT, BB = R::BB, S = kSpBulkStages;
   extern __shared__ __align__(16) double sm[];
   __shared__ __align__(8) uint64_t mbar[kSpBulkWarps][S];
+  __shared__ int smeta[kSpBulkWarps][S][2];  // per stage: C slot of the entry's run, flags (1 first, 2 last)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
   double* ring = sm + (size_t)warp * S * Q::STG;
   const uint32_t ring_s = (uint32_t)__cvta_generic_to_shared(ring);
@@ -535,94 +536,135 @@ __global__ void __launch_bounds__(kSpBulkWarps * 32, 1)
 #pragma unroll
   for (int i = 0; i < MT; ++i) rowm[i] = coln[i] = i * 8 + g;
   const int64_t nwarps = (int64_t)gridDim.x * kSpBulkWarps;
-  for (int64_t run = (int64_t)blockIdx.x * kSpBulkWarps + warp; run < nruns; run += nwarps) {
-    const int64_t e0 = off ? off[run] : run * kb, e1 = off ? off[run + 1] : e0 + kb;
-    if (e0 == e1) continue;
-    // trip slot window: lane l holds entry w0 + l's (A, B) slots, the next window's in flight
-    int64_t w0 = e0;
-    int ca = 0, cb = 0, na = 0, nb = 0;
-    if (e0 + lane < e1) ca = trip[3 * (e0 + lane)], cb = trip[3 * (e0 + lane) + 1];
-    if (e0 + 32 + lane < e1) na = trip[3 * (e0 + 32 + lane)], nb = trip[3 * (e0 + 32 + lane) + 1];
-    auto issue = [&](int64_t e, int si) {  // warp-uniform; entries issued in order e0, e0 + 1, ...
-      if (e >= w0 + 32) {
-        w0 += 32;
-        ca = na;
-        cb = nb;
-        const int64_t f = w0 + 32 + lane;
-        if (f < e1) na = trip[3 * f], nb = trip[3 * f + 1];
-      }
-      const int sa = __shfl_sync(0xffffffffu, ca, (int)(e - w0)), sb = __shfl_sync(0xffffffffu, cb, (int)(e - w0));
-      if (lane == 0) {
-        const uint32_t mb = mb0 + 8 * si, dst = ring_s + 8u * (uint32_t)(si * Q::STG);
-        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mb), "r"(2 * BB * 8) : "memory");
-        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                         dst),
-                     "l"(A + (int64_t)sa * BB), "r"(BB * 8), "r"(mb)
-                     : "memory");
-        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                         dst + 8u * R::A_D),
-                     "l"(B + (int64_t)sb * BB), "r"(BB * 8), "r"(mb)
-                     : "memory");
-      }
-    };
-    double acc[MT][MT][2];
-#pragma unroll
-    for (int i = 0; i < MT; ++i)
-#pragma unroll
-      for (int j = 0; j < MT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-#pragma unroll
-    for (int i = 0; i < S - 1; ++i)
-      if (e0 + i < e1) issue(e0 + i, i);
-    int si = 0;
-    for (int64_t e = e0; e < e1; ++e) {
-      if (e + S - 1 < e1) issue(e + S - 1, si == 0 ? S - 1 : si - 1);  // the stage entry e - 1 used
-      {
-        const uint32_t mb = mb0 + 8 * si, par = (phase >> si) & 1;
-        uint32_t done;
-        do {
-          asm volatile(
-              "{\n\t.reg .pred p;\n\t"
-              "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-              "selp.u32 %0, 1, 0, p;\n\t}"
-              : "=r"(done)
-              : "r"(mb), "r"(par)
-              : "memory");
-        } while (!done);
-        phase ^= 1u << si;
-      }
-      const double* sA = ring + si * Q::STG;  // (m, k) at k*BS + m
-      const double* sB = sA + R::A_D;         // (k, n) at n*BS + k
-#pragma unroll
-      for (int ks = 0; ks < (BS + 3) / 4; ++ks) {
-        const int k = 4 * ks + t;
-        const bool kok = (BS % 4 == 0) || k < BS;
-        double a[MT], b[MT];
-#pragma unroll
-        for (int mi = 0; mi < MT; ++mi) a[mi] = kok ? sA[k * BS + rowm[mi]] : 0.0;
-#pragma unroll
-        for (int ni = 0; ni < MT; ++ni) b[ni] = kok ? sB[coln[ni] * BS + k] : 0.0;
-#pragma unroll
-        for (int mi = 0; mi < MT; ++mi)
-#pragma unroll
-          for (int ni = 0; ni < MT; ++ni) sp_dmma(acc[mi][ni], a[mi], b[ni]);
-      }
-      __syncwarp();  // every lane is done with stage si before an issue refills it
-      si = si == S - 1 ? 0 : si + 1;
+
+  // The warp's runs (run = first + i * nwarps) are issued as ONE stream of entries, so the ring stays
+  // full across run boundaries; the next run's offsets, C slot and first 32 trip slots are loaded one
+  // run ahead, the current run's next 32 slots one window ahead (one per lane, handed to the issuing
+  // lane by shuffles): no dependent global load sits between two entries or two runs.
+  struct RunPre {  // a run's prefetched metadata (lane l: entry e0 + l's slots)
+    int64_t r, e0, e1;
+    int a, b, c;
+  };
+  auto prefetch_run = [&](int64_t r) -> RunPre {
+    RunPre p{r, 0, 0, 0, 0, 0};
+    while (p.r < nruns) {  // (skip runs without entries)
+      p.e0 = off ? off[p.r] : p.r * kb;
+      p.e1 = off ? off[p.r + 1] : p.e0 + kb;
+      if (p.e1 > p.e0) break;
+      p.r += nwarps;
     }
-    double* cbk = C + (int64_t)trip[3 * e0 + 2] * BB;
+    if (p.r < nruns) {
+      p.c = trip[3 * p.e0 + 2];
+      if (p.e0 + lane < p.e1) p.a = trip[3 * (p.e0 + lane)], p.b = trip[3 * (p.e0 + lane) + 1];
+    }
+    return p;
+  };
+  RunPre cur = prefetch_run((int64_t)blockIdx.x * kSpBulkWarps + warp);
+  RunPre nxt = prefetch_run(cur.r + nwarps);
+  int64_t ie = cur.e0, w0 = cur.e0;  // issue cursor (entry of run cur.r) and its slot window
+  int ca = cur.a, cb = cur.b, na = 0, nb = 0;
+  if (cur.r < nruns && cur.e0 + 32 + lane < cur.e1)
+    na = trip[3 * (cur.e0 + 32 + lane)], nb = trip[3 * (cur.e0 + 32 + lane) + 1];
+  auto issue_next = [&](int si) -> bool {  // warp-uniform
+    if (cur.r >= nruns) return false;
+    if (ie >= w0 + 32) {
+      w0 += 32;
+      ca = na;
+      cb = nb;
+      const int64_t f = w0 + 32 + lane;
+      if (f < cur.e1) na = trip[3 * f], nb = trip[3 * f + 1];
+    }
+    const int sa = __shfl_sync(0xffffffffu, ca, (int)(ie - w0)), sb = __shfl_sync(0xffffffffu, cb, (int)(ie - w0));
+    if (lane == 0) {
+      smeta[warp][si][0] = cur.c;
+      smeta[warp][si][1] = (ie == cur.e0 ? 1 : 0) | (ie + 1 == cur.e1 ? 2 : 0);
+      const uint32_t mb = mb0 + 8 * si, dst = ring_s + 8u * (uint32_t)(si * Q::STG);
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mb), "r"(2 * BB * 8) : "memory");
+      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                       dst),
+                   "l"(A + (int64_t)sa * BB), "r"(BB * 8), "r"(mb)
+                   : "memory");
+      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                       dst + 8u * R::A_D),
+                   "l"(B + (int64_t)sb * BB), "r"(BB * 8), "r"(mb)
+                   : "memory");
+    }
+    if (++ie == cur.e1) {  // on to the next run: its metadata is in registers; prefetch the one after
+      cur = nxt;
+      ie = w0 = cur.e0;
+      ca = cur.a;
+      cb = cur.b;
+      na = nb = 0;
+      if (cur.r < nruns) {
+        if (cur.e0 + 32 + lane < cur.e1)
+          na = trip[3 * (cur.e0 + 32 + lane)], nb = trip[3 * (cur.e0 + 32 + lane) + 1];
+        nxt = prefetch_run(cur.r + nwarps);
+      }
+    }
+    return true;
+  };
+  double acc[MT][MT][2];
 #pragma unroll
-    for (int mi = 0; mi < MT; ++mi)
+  for (int i = 0; i < MT; ++i)
 #pragma unroll
-      for (int ni = 0; ni < MT; ++ni)
+    for (int j = 0; j < MT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  int inflight = 0;
 #pragma unroll
-        for (int jj = 0; jj < 2; ++jj) {
-          const int m = rowm[mi], n = ni * 8 + 2 * t + jj;
-          if (m < BS && n < BS) {
-            double* p = cbk + m + n * BS;
-            const double ab = __dmul_rn(alpha, acc[mi][ni][jj]);
-            *p = beta_first == 1.0 ? __dadd_rn(*p, ab) : beta_first == 0.0 ? ab : fma(beta_first, *p, ab);
+  for (int i = 0; i < S - 1; ++i) inflight += issue_next(i) ? 1 : 0;
+  int si = 0;
+  while (inflight > 0) {
+    if (issue_next(si == 0 ? S - 1 : si - 1)) ++inflight;  // refill the stage the previous entry used
+    {
+      const uint32_t mb = mb0 + 8 * si, par = (phase >> si) & 1;
+      uint32_t done;
+      do {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(done)
+            : "r"(mb), "r"(par)
+            : "memory");
+      } while (!done);
+      phase ^= 1u << si;
+    }
+    --inflight;
+    const int cslot = smeta[warp][si][0], flags = smeta[warp][si][1];
+    const double* sA = ring + si * Q::STG;  // (m, k) at k*BS + m
+    const double* sB = sA + R::A_D;         // (k, n) at n*BS + k
+#pragma unroll
+    for (int ks = 0; ks < (BS + 3) / 4; ++ks) {
+      const int k = 4 * ks + t;
+      const bool kok = (BS % 4 == 0) || k < BS;
+      double a[MT], b[MT];
+#pragma unroll
+      for (int mi = 0; mi < MT; ++mi) a[mi] = kok ? sA[k * BS + rowm[mi]] : 0.0;
+#pragma unroll
+      for (int ni = 0; ni < MT; ++ni) b[ni] = kok ? sB[coln[ni] * BS + k] : 0.0;
+#pragma unroll
+      for (int mi = 0; mi < MT; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < MT; ++ni) sp_dmma(acc[mi][ni], a[mi], b[ni]);
+    }
+    __syncwarp();  // every lane is done with stage si (and its metadata) before an issue refills it
+    si = si == S - 1 ? 0 : si + 1;
+    if (flags & 2) {  // the run's last entry: C_blk = (first ? beta*C : C) + alpha*acc, then a fresh acc
+      double* cbk = C + (int64_t)cslot * BB;
+#pragma unroll
+      for (int mi = 0; mi < MT; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < MT; ++ni)
+#pragma unroll
+          for (int jj = 0; jj < 2; ++jj) {
+            const int m = rowm[mi], n = ni * 8 + 2 * t + jj;
+            if (m < BS && n < BS) {
+              double* p = cbk + m + n * BS;
+              const double ab = __dmul_rn(alpha, acc[mi][ni][jj]);
+              *p = beta_first == 1.0 ? __dadd_rn(*p, ab) : beta_first == 0.0 ? ab : fma(beta_first, *p, ab);
+            }
+            acc[mi][ni][jj] = 0.0;
           }
-        }
+    }
   }
 }
 

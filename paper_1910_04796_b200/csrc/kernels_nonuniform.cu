@@ -87,6 +87,7 @@ __device__ __forceinline__ void nu_dmma(double (&c)[2], double a, double b) {
 }
 
 constexpr int kNuWarps = 4;
+constexpr int kNuStages = 3;
 constexpr int kNuZero = 64;  // doubles of zeros past the ring (the k tail's operand)
 
 __device__ __forceinline__ void nu_mbar_init(uint32_t a, uint32_t count) {
@@ -173,33 +174,28 @@ __device__ __forceinline__ void nu_kloop(double (&acc)[S][S][2], const int4* zt,
 //     tail adds exact zeros;
 //   * epilogue: the WK k-groups' partial C blocks meet in shared memory and are summed in k-group order
 //     (deterministic), then scaled into C.
-// resident CTAs per SM the register budget is sized for (blocks up to 32: the ring's shared memory
-// allows 5 / 4 / 3 CTAs at 2 / 3 / 4 stages)
-template <int S, int NST>
-constexpr int nu_min_ctas() { return S == 4 ? (NST == 2 ? 5 : NST == 3 ? 4 : 3) : 1; }
-
-template <int S, int WR, int NST>
-__global__ void __launch_bounds__(kNuWarps * 32, nu_min_ctas<S, NST>())
+template <int S, int WR>
+__global__ void __launch_bounds__(kNuWarps * 32)
     nu_smm_kernel(const int32_t* __restrict__ trip, int64_t nruns, int64_t kb, const double* __restrict__ A,
                   const int64_t* __restrict__ aoff, const double* __restrict__ B, const int64_t* __restrict__ boff,
                   const int32_t* __restrict__ kdim, const int32_t* __restrict__ kofs, const int32_t* __restrict__ gbeg,
                   int ngroups, double* __restrict__ C, const NUBlk* __restrict__ cblk, int kcap, int mmax_pad,
                   int nmax_pad, double alpha, double beta_first) {
   extern __shared__ __align__(16) double nsm[];
-  __shared__ __align__(8) uint64_t nmb[NST][kNuWarps];
+  __shared__ __align__(8) uint64_t nmb[kNuStages][kNuWarps];
   constexpr int WK = kNuWarps / WR, SI = S / WR;
   const int kp = (kcap + 3) & ~3, ne = nu_group_entries(kp);
   const int a_reg = nu_a_region(kp, mmax_pad, ne), b_reg = nu_a_region(kp, nmax_pad, ne);
   const int st_d = nu_stage_doubles(kp, mmax_pad, nmax_pad, ne);
   // past the ring and the epilogue's partial C blocks (zeroed once, never overwritten)
-  const int zero_off = max(NST * st_d, kNuWarps * mmax_pad * nmax_pad);
+  const int zero_off = max(kNuStages * st_d, kNuWarps * mmax_pad * nmax_pad);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
   const int rh = warp % WR, kg = warp / WR, i0 = rh * SI;
   const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(nsm);
   const uint32_t mb0 = (uint32_t)__cvta_generic_to_shared(&nmb[0][0]);
   for (int i = threadIdx.x; i < kNuZero; i += blockDim.x) nsm[zero_off + i] = 0.0;
   if (threadIdx.x == 0) {
-    for (int i = 0; i < NST * kNuWarps; ++i) nu_mbar_init(mb0 + 8 * i, 32);
+    for (int i = 0; i < kNuStages * kNuWarps; ++i) nu_mbar_init(mb0 + 8 * i, 32);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -289,19 +285,19 @@ __global__ void __launch_bounds__(kNuWarps * 32, nu_min_ctas<S, NST>())
 #pragma unroll
       for (int j = 0; j < S; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 #pragma unroll
-    for (int s = 0; s < NST - 1; ++s) {
+    for (int s = 0; s < kNuStages - 1; ++s) {
       fetch1(s);
       fetch2();
       stage(s, s);
     }
-    fetch1(NST - 1);
+    fetch1(kNuStages - 1);
     fetch2();
-    fetch1(NST);
+    fetch1(kNuStages);
     for (int grp = 0; grp < ngroups; ++grp) {
-      stage(grp + NST - 1, (grp + NST - 1) % NST);
+      stage(grp + kNuStages - 1, (grp + kNuStages - 1) % kNuStages);
       fetch2();                   // group grp + 3's addresses
-      fetch1(grp + NST + 1);  // group grp + 4's entries (both in flight during this group's compute)
-      const int buf = grp % NST;
+      fetch1(grp + kNuStages + 1);  // group grp + 4's entries (both in flight during this group's compute)
+      const int buf = grp % kNuStages;
 #pragma unroll
       for (int w = 0; w < kNuWarps; ++w) nu_mbar_wait(mb0 + 8 * (buf * kNuWarps + w), (phase >> buf) & 1);
       phase ^= 1u << buf;
@@ -404,19 +400,9 @@ void launch_nu_pack(const NUPack* tasks, int64_t ntasks, const double* src, doub
   nu_pack_kernel<<<nu_grid(ntasks), 256, 0, st>>>(tasks, ntasks, src, dst);
 }
 
-// stages of the small-block kernel's ring (DBM_NU_STAGES = 2, 3 or 4; default 3)
-int nu_stages() {
-  static const int n = [] {
-    const char* e = getenv("DBM_NU_STAGES");
-    const int v = e ? atoi(e) : 3;
-    return v >= 2 && v <= 4 ? v : 3;
-  }();
-  return n;
-}
-
 size_t nu_smm_smem(int kcap, int mmax, int nmax) {
   const int kp = (kcap + 3) & ~3, mp = (mmax + 7) & ~7, np = (nmax + 7) & ~7;
-  const size_t ring = (size_t)nu_stages() * nu_stage_doubles(kp, mp, np, nu_group_entries(kp));
+  const size_t ring = (size_t)kNuStages * nu_stage_doubles(kp, mp, np, nu_group_entries(kp));
   // (the epilogue's WK partial C blocks, at most 4 mp np doubles, reuse the ring; the zero region follows it)
   return (std::max(ring, (size_t)kNuWarps * mp * np) + kNuZero) * 8;
 }
@@ -429,10 +415,8 @@ cudaError_t launch_nu_smm(const int32_t* trip, int64_t nruns, int64_t kb, const 
   if (mmax > 64 || nmax > 64) return cudaErrorInvalidValue;  // the host checks: C blocks up to 64 x 64
   const size_t smem = nu_smm_smem(kcap, mmax, nmax);
   const bool small = mmax <= 32 && nmax <= 32;  // 4 x 4 subtiles per warp, else 8 x 8
-  const int nst = nu_stages();
-  auto kern = small ? (nst == 2 ? nu_smm_kernel<4, 1, 2> : nst == 4 ? nu_smm_kernel<4, 1, 4> : nu_smm_kernel<4, 1, 3>)
-                    : (nst == 2 ? nu_smm_kernel<8, 2, 2> : nst == 4 ? nu_smm_kernel<8, 2, 4> : nu_smm_kernel<8, 2, 3>);
-  static size_t attr[2] = {0, 0};  // (one stage count per process)
+  auto kern = small ? nu_smm_kernel<4, 1> : nu_smm_kernel<8, 2>;
+  static size_t attr[2] = {0, 0};
   if (smem > 48 * 1024 && smem > attr[small]) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;

@@ -174,8 +174,11 @@ __device__ __forceinline__ void nu_kloop(double (&acc)[S][S][2], const int4* zt,
 //     tail adds exact zeros;
 //   * epilogue: the WK k-groups' partial C blocks meet in shared memory and are summed in k-group order
 //     (deterministic), then scaled into C.
+// (blocks up to 32: the ring's shared memory allows 4 resident CTAs per SM, so the register budget is
+// pinned to 4 x 128 threads; measured: 2 stages at 5 CTAs and 4 stages at 3 CTAs both lose, 7.7 vs 9.1
+// TFLOP/s at 3,960^3)
 template <int S, int WR>
-__global__ void __launch_bounds__(kNuWarps * 32)
+__global__ void __launch_bounds__(kNuWarps * 32, S == 4 ? 4 : 1)
     nu_smm_kernel(const int32_t* __restrict__ trip, int64_t nruns, int64_t kb, const double* __restrict__ A,
                   const int64_t* __restrict__ aoff, const double* __restrict__ B, const int64_t* __restrict__ boff,
                   const int32_t* __restrict__ kdim, const int32_t* __restrict__ kofs, const int32_t* __restrict__ gbeg,

@@ -8,8 +8,8 @@
 //                      B (K-major columns) and undensify C with alpha / beta (column-major)
 //   nu_pack_kernel     whole-block gathers into packed Cannon panels (blocked path)
 //   nu_smm_kernel      the blocked path's small-block products of mixed (m, n, k): one CTA per C-block
-//                      run, entry groups staged by cp.async into a 3-stage ring, K split over the warps,
-//                      FP64 DMMA (mma.sync m8n8k4) on 8 x 8 subtiles with register predication
+//                      run, entry groups staged by TMA bulk copies into a 3-stage mbarrier ring, K split
+//                      over the warps, FP64 DMMA (mma.sync m8n8k4) on 8 x 8 subtiles
 #include <algorithm>
 
 #include "dbm_internal.h"

@@ -260,6 +260,14 @@ dbm_status dbm_multiply(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_matrix B, d
 dbm_status dbm_plan_exchange(int pr, int pc, int myrow, int mycol, int64_t Mb, int64_t Nb, int64_t Kb, int32_t bs,
                              dbm_path path, int step, int32_t* ops, int64_t* bytes, int* n_ops);
 
+/* Host-only: the canonical Cannon step rank `rank` of a pr x pc grid takes FIRST under the copy-engine
+ * transport (the local-first order: with owner-pull every panel is in its owner's exchange pool before
+ * any step, so a rank may take the L = lcm(pr, pc) steps in any order; it starts at the step with the
+ * most local operands, ties broken towards the owners with the fewest first-step pullers, then runs the
+ * steps cyclically: position s is canonical step (first + s) mod L).  The NCCL transport and
+ * dbm_plan_exchange keep the canonical order (first = 0).  ARG on a bad grid or rank. */
+dbm_status dbm_debug_first_step(int pr, int pc, int rank, int* first_step);
+
 /* Host-only: bytes rank (myrow, mycol) receives from / sends to its peers in one tall-and-skinny
  * multiply of Mb x Kb by Kb x Nb blocks of bs (gather of A and B pieces + the C-share reduction). */
 dbm_status dbm_plan_tallskinny(int pr, int pc, int myrow, int mycol, int64_t Mb, int64_t Nb, int64_t Kb, int32_t bs,

@@ -88,6 +88,16 @@ struct ProfScope {
 };
 
 std::vector<int64_t> pipeline_chunks(int64_t kb, double growth = 2.0);
+// Local-first step order (copy-engine transport, several ranks).  With owner-pull every panel sits in
+// its owner's exchange pool before any step, so a rank may take Cannon's L steps in any order (reading
+// R5; the canonical skew kappa = (r + c + s) mod L stays the schedule dbm_plan_exchange describes and the
+// NCCL transport runs).  Each rank starts at the canonical step with the most local operands -- the
+// first step is the one nothing overlaps with -- ties broken towards the owners serving the fewest first-
+// step pulls (greedy over the ranks in order, so every rank computes every rank's choice), and then
+// continues cyclically.  2 x 2: ranks 0 and 3 start with both operands local, ranks 1 and 2 with one
+// pull each from different owners (canonical: rank 3 pulls both, and serves both of the others' pulls).
+// Returns rank's first canonical step.
+int local_first_start(int pr, int pc, int rank);
 double pipeline_growth(double gemm_flop_per_kblock, double pull_bytes_per_kblock);
 
 dbm_status validate(dbm_ctx ctx, dbm_matrix A, dbm_matrix B, dbm_matrix C);

@@ -826,7 +826,9 @@ struct Plan {
   size_t pool_total = 0;  // several ranks: exchange-pool bytes (signal header + own panels peers pull)
   int max_split = 1;
 
-  int kappa(int s) const { return (r + c + s) % L; }
+  bool local_first = false;  // steps in local-first order (local_first_start), else canonical
+  int s0 = 0;                // this rank's first canonical step
+  int kappa(int s) const { return (r + c + s + s0) % L; }
   int a_src(int s) const { return r * pc + kappa(s) % pc; }
   int b_src(int s) const { return (kappa(s) % pr) * pc + c; }
   int me() const { return r * pc + c; }
@@ -858,8 +860,10 @@ int smmq_on() {
 // Host-only plan: depends on the grid, this rank's coordinates and the block counts (no CUDA).
 Plan make_plan_raw(int nranks, int pr, int pc, int r, int c, int64_t Mb, int64_t Nb, int64_t Kb, int64_t bs,
                    bool densified, int64_t chunk_bytes, int transport, bool b_packed = false,
-                   bool a_packed = false) {
+                   bool a_packed = false, bool local_first = false) {
   Plan p;
+  p.local_first = local_first && nranks > 1 && transport == 0;
+  p.s0 = p.local_first ? local_first_start(pr, pc, r * pc + c) : 0;
   p.b_packed = b_packed;
   p.a_packed = a_packed;
   p.pr = pr;
@@ -1022,11 +1026,12 @@ bool zero_copy_a() {
   return on;
 }
 
-Plan make_plan(dbm_ctx ctx, dbm_matrix A, dbm_matrix B, dbm_matrix C, bool densified) {
+Plan make_plan(dbm_ctx ctx, dbm_matrix A, dbm_matrix B, dbm_matrix C, bool densified, bool local_first = true) {
   (void)C;
   const bool zc = densified && A->bs == 64 && !use_tallskinny(ctx, A, B, densified);
   return make_plan_raw(ctx->nranks, ctx->pr, ctx->pc, ctx->myrow, ctx->mycol, A->Mb, B->Nb, A->Nb, A->bs, densified,
-                       ctx->chunk_bytes, ctx->transport, zc && !B->sparse, zc && !A->sparse && zero_copy_a());
+                       ctx->chunk_bytes, ctx->transport, zc && !B->sparse, zc && !A->sparse && zero_copy_a(),
+                       local_first);
 }
 
 // One Cannon exchange step as a list of point-to-point operations (owner-pull, reading R5):
@@ -1046,7 +1051,7 @@ std::vector<XOp> exchange_ops(const Plan& p, int s) {
     for (int cc = 0; cc < p.pc; ++cc) {
       const int dst = rr * p.pc + cc;
       if (dst == me) continue;
-      const int k = (rr + cc + s) % p.L;
+      const int k = (rr + cc + s + (p.local_first ? local_first_start(p.pr, p.pc, dst) : 0)) % p.L;
       if (rr == p.r && k % p.pc == p.c) ops.push_back({1, 0, dst, k, (int64_t)p.a_panel_bytes(k)});  // dst needs my A(r,k)
       if (cc == p.c && k % p.pr == p.r) ops.push_back({1, 1, dst, k, (int64_t)p.b_panel_bytes(k)});  // dst needs my B(k,c)
     }
@@ -1059,6 +1064,30 @@ std::vector<XOp> exchange_ops(const Plan& p, int s) {
 }  // namespace
 
 namespace dbm {
+int local_first_start(int pr, int pc, int rank) {
+  const int L = (int)lcm64(pr, pc), P = pr * pc;
+  std::vector<int> load(P, 0);
+  int mine = 0;
+  for (int q = 0; q < P; ++q) {
+    const int r = q / pc, c = q % pc;
+    int best = 0, best_remote = 3, best_load = 0;
+    for (int s = 0; s < L; ++s) {
+      const int k = (r + c + s) % L, a = r * pc + k % pc, b = (k % pr) * pc + c;
+      const int remote = (a != q) + (b != q), ld = (a != q ? load[a] : 0) + (b != q ? load[b] : 0);
+      if (remote < best_remote || (remote == best_remote && ld < best_load)) {
+        best = s;
+        best_remote = remote;
+        best_load = ld;
+      }
+    }
+    const int k = (r + c + best) % L, a = r * pc + k % pc, b = (k % pr) * pc + c;
+    if (a != q) ++load[a];
+    if (b != q) ++load[b];
+    if (q == rank) mine = best;
+  }
+  return mine;
+}
+
 // K-chunk boundaries (blocks) of a transfer -> GEMM pipeline whose first transfer nothing hides (Cannon's
 // step 0, the tall-and-skinny gather).  The first chunk is 1/16 of kb and each next one is `growth`
 // times larger: the pull of chunk j+1 (copy engines, ~600 GB/s from a peer) must fit under the GEMM of
@@ -1140,6 +1169,12 @@ void undensify_c(dbm_matrix C, const double* dense, int64_t ld, int nsplit, int6
 
 }  // namespace dbm
 
+
+extern "C" dbm_status dbm_debug_first_step(int pr, int pc, int rank, int* first_step) {
+  ARG_CHECK(first_step && pr > 0 && pc > 0 && rank >= 0 && rank < pr * pc, DBM_ERR_ARG, "bad grid or rank");
+  *first_step = local_first_start(pr, pc, rank);
+  return DBM_OK;
+}
 
 extern "C" dbm_status dbm_plan_exchange(int pr, int pc, int myrow, int mycol, int64_t Mb, int64_t Nb, int64_t Kb,
                                         int32_t bs, dbm_path path, int step, int32_t* ops, int64_t* bytes,
@@ -1858,7 +1893,8 @@ dbm_status multiply_impl(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_matrix B, 
     size_t need = p.pool_total;
     for (int q = 0; q < ctx->nranks; ++q)
       need = std::max(need, make_plan_raw(ctx->nranks, p.pr, p.pc, q / p.pc, q % p.pc, p.Mb, p.Nb, p.Kb, p.bs, dens,
-                                          ctx->chunk_bytes, ctx->transport, p.b_packed, p.a_packed).pool_total);
+                                          ctx->chunk_bytes, ctx->transport, p.b_packed, p.a_packed,
+                                          p.local_first).pool_total);
     if (dbm_status e = xattach(ctx, need, cs)) return e;
     xp = ctx->xpool;
     ep = ++ctx->epoch;
@@ -2018,7 +2054,7 @@ dbm_status multiply_impl(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_matrix B, 
       for (int q = 0; q < ctx->nranks; ++q)
         if (q != ctx->rank)
           peer_plan[q] = make_plan_raw(ctx->nranks, p.pr, p.pc, q / p.pc, q % p.pc, p.Mb, p.Nb, p.Kb, p.bs, dens,
-                                       ctx->chunk_bytes, ctx->transport, p.b_packed, p.a_packed);
+                                       ctx->chunk_bytes, ctx->transport, p.b_packed, p.a_packed, p.local_first);
       if (pipe) {
         for (int j = 0; j < kHostPipeChunks; ++j) {
           if (dbm_status e = own_panels_chunk(j)) {
@@ -2382,7 +2418,7 @@ extern "C" dbm_status dbm_debug_stacks(dbm_ctx ctx, dbm_matrix A, dbm_matrix B, 
   const Plan p = A->nonuni || B->nonuni || C->nonuni
                      ? make_plan_raw(ctx->nranks, ctx->pr, ctx->pc, ctx->myrow, ctx->mycol, A->Mb, B->Nb, A->Nb, 1,
                                      false, ctx->chunk_bytes, ctx->transport)
-                     : make_plan(ctx, A, B, C, false);
+                     : make_plan(ctx, A, B, C, false, false);  // (the canonical step numbering)
   ARG_CHECK(step >= 0 && step < p.L, DBM_ERR_RANGE, "step out of range");
   const int64_t capv = cap ? cap : 30000;
   const int64_t kb = p.kb[p.kappa(step)], nruns = p.mloc * p.nloc, ne = nruns * kb;

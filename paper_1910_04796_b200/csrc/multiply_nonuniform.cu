@@ -34,7 +34,8 @@ struct NURank {
   std::vector<int64_t> ldk;              // per kappa: dense panel leading dimension (even)
   size_t a_bytes(int k) const { return (size_t)(dens ? Mel * ldk[k] : Mel * pko[k].back()) * 8; }
   size_t b_bytes(int k) const { return (size_t)(dens ? Nel * ldk[k] : Nel * pko[k].back()) * 8; }
-  int kappa(int s) const { return (r + c + s) % L; }
+  int s0 = 0;  // first canonical step (local-first order, several ranks: local_first_start)
+  int kappa(int s) const { return (r + c + s + s0) % L; }
   int a_src(int s) const { return r * pc + kappa(s) % pc; }
   int b_src(int s) const { return (kappa(s) % pr) * pc + c; }
   int me() const { return r * pc + c; }
@@ -49,6 +50,7 @@ NURank nu_rank(dbm_ctx ctx, dbm_matrix A, dbm_matrix B, bool dens, int r, int c)
   p.r = r;
   p.c = c;
   p.L = (int)lcm64(p.pr, p.pc);
+  p.s0 = ctx->nranks > 1 && ctx->transport == 0 ? local_first_start(p.pr, p.pc, r * p.pc + c) : 0;
   p.dens = dens;
   p.mloc = local_count(A->Mb, p.pr, r);
   p.nloc = local_count(B->Nb, p.pc, c);

@@ -68,6 +68,7 @@ _SIGS = {
     "dbm_ctx_set_algorithm": (C.c_int, [_P, C.c_int]),
     "dbm_plan_tallskinny": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, _I64, _I64, _I64, C.c_int32,
                                       C.POINTER(_I64), C.POINTER(_I64)]),
+    "dbm_debug_first_step": (C.c_int, [C.c_int, C.c_int, C.c_int, C.POINTER(C.c_int)]),
     "dbm_plan_exchange": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, _I64, _I64, _I64, C.c_int32, C.c_int,
                                     C.c_int, _P, _P, C.POINTER(C.c_int)]),
     "dbm_ctx_destroy": (C.c_int, [_P]),
@@ -421,6 +422,14 @@ def multiply(ctx: Context, alpha: float, A: Matrix, B: Matrix, beta: float, C_: 
     _check(lib.dbm_multiply(ctx.h, alpha, A.h, B.h, beta, C_.h, _PATHS[path], stack_cap, ws.data_ptr(),
                             ws.numel() * ws.element_size(), C.byref(st)))
     return st.as_dict()
+
+
+def debug_first_step(pr: int, pc: int, rank: int) -> int:
+    """Host-only: the canonical Cannon step `rank` takes first under the copy-engine transport
+    (dbm_debug_first_step, the local-first order)."""
+    v = C.c_int(0)
+    _check(load().dbm_debug_first_step(pr, pc, rank, C.byref(v)))
+    return v.value
 
 
 def plan_exchange(pr: int, pc: int, myrow: int, mycol: int, Mb: int, Nb: int, Kb: int, bs: int, step: int,

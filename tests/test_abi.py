@@ -129,3 +129,31 @@ def test_pattern_product_matches_numpy(dbm, orc):
     want = ((a.astype(np.int64) @ b.astype(np.int64)) > 0).astype(np.uint8)
     assert np.array_equal(dbm.pattern_product(a, b), want)
     assert np.array_equal(dbm.pattern_product(a, b, c0), want | c0)
+
+
+@pytest.mark.parametrize("pr,pc", GRIDS + [(3, 3), (4, 4), (2, 3), (1, 8), (8, 1)])
+def test_first_step_is_local_first(dbm, orc, pr, pc):
+    """dbm_debug_first_step (the copy-engine transport's local-first order): every rank starts at a
+    canonical step with the most local operands any step offers it (brute force over the oracle's schedule,
+    orc_cannon_step); on the 2 x 2 and 2 x 4 grids no owner serves more than one first-step pull (the
+    canonical order makes one rank of 2 x 2 pull both operands and another serve both pulls)."""
+    L = orc.lcm(pr, pc)
+    served = {}
+    for q in range(pr * pc):
+        r, c = divmod(q, pc)
+        first = dbm.debug_first_step(pr, pc, q)
+        assert 0 <= first < L
+
+        def local(s):
+            _, a, b = orc.cannon_step(pr, pc, r, c, s)
+            return (a == q) + (b == q)
+
+        assert local(first) == max(local(s) for s in range(L))
+        _, a, b = orc.cannon_step(pr, pc, r, c, first)
+        for src in (a, b):
+            if src != q:
+                served[src] = served.get(src, 0) + 1
+    if (pr, pc) in ((2, 2), (2, 4)):
+        assert max(served.values(), default=0) <= 1
+    with pytest.raises(dbm.DbmError):
+        dbm.debug_first_step(pr, pc, pr * pc)

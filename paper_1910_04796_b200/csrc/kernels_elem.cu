@@ -145,6 +145,20 @@ __global__ void __launch_bounds__(256) pack_rows_fast(const double2* __restrict_
   }
 }
 
+// Column panels: block row i's selected blocks (i, col0 + q*cstride) are contiguous bs^2 runs; a CTA row
+// (blockIdx.y) per block row, CTAs along x over its blocks, threads over a block's 16-byte pairs (no
+// per-element index division).  Out row i starts out_row blocks after row i-1.
+__global__ void __launch_bounds__(256) pack_cols_fast(const double2* __restrict__ arena, int64_t bb2, int64_t inner,
+                                                      int64_t col0, int64_t cstride, int64_t ncols, int64_t mloc,
+                                                      int64_t out_row, double2* __restrict__ out) {
+  for (int64_t i = blockIdx.y; i < mloc; i += gridDim.y)
+    for (int64_t q = blockIdx.x; q < ncols; q += gridDim.x) {
+      const double2* src = arena + (i * inner + col0 + q * cstride) * bb2;
+      double2* dst = out + (i * out_row + q) * bb2;
+      for (int64_t w = threadIdx.x; w < bb2; w += blockDim.x) dst[w] = src[w];
+    }
+}
+
 __global__ void pack_blocks_kernel(const double* __restrict__ arena, int64_t nsel, int64_t inner, int64_t outer_stride,
                                    int64_t sel0, int64_t sel_stride, int bs, int by_rows, int64_t other,
                                    double* __restrict__ out) {
@@ -375,6 +389,14 @@ void launch_pack_cols(const double* arena, int64_t mloc, int64_t nloc, int bs, i
                       int64_t ncols, double* out, cudaStream_t st, int64_t out_pitch) {
   int64_t total = ncols * mloc * (int64_t)bs * bs;
   if (total == 0) return;
+  const int64_t bb = (int64_t)bs * bs;
+  if (bb % 2 == 0 && ((uintptr_t)arena & 15) == 0 && ((uintptr_t)out & 15) == 0) {
+    const unsigned gy = (unsigned)std::min<int64_t>(mloc, 65535);
+    const unsigned gx = (unsigned)std::max<int64_t>(1, std::min<int64_t>(ncols, (4 * num_sms() * 8 + gy - 1) / gy));
+    pack_cols_fast<<<dim3(gx, gy), 256, 0, st>>>((const double2*)arena, bb / 2, nloc, col0, cstride, ncols, mloc,
+                                                 out_pitch > 0 ? out_pitch : ncols, (double2*)out);
+    return;
+  }
   pack_blocks_kernel<<<grid_for(total), kThreads, 0, st>>>(arena, ncols, nloc, out_pitch, col0, cstride, bs, 0, mloc,
                                                            out);
 }

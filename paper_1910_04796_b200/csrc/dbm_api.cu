@@ -1404,8 +1404,9 @@ dbm_status dbm::xwait(dbm_ctx ctx, cudaStream_t st, int kind, uint64_t value) {
 namespace {
 
 // Pull this rank's step-s panels from their owners' workspaces (peer plans give the offsets).
-// Host-operand pipeline (hp_epoch != 0): wait (on the comm stream) until the owner of op's panel has
-// published at least `need` K-blocks of it for this multiply into this rank's progress table.
+// Each pull first waits (on its copy stream) until the owner of op's panel has published at least `need`
+// K-blocks of it for this multiply (epoch hp_epoch) into this rank's progress table: the whole panel
+// behind its densify / pack, or chunk by chunk in the pipelined modes.
 // A step's A and B pulls go on two streams (comm, comm2), so two copy engines move them concurrently; the
 // B stream forks from the comm stream's state and joins it again at the end of the step's posts.
 cudaStream_t pull_stream(dbm_ctx ctx, const XOp& op) { return op.operand == 1 ? ctx->comm2 : ctx->comm; }
@@ -1901,9 +1902,32 @@ dbm_status multiply_impl(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_matrix B, 
   }
 
   // ------------------------------------------------ own panels (densify or pack), on the compute stream
+  // Copy-engine transport: each own panel's completion goes into every peer's progress table as soon as
+  // it is in place ((epoch << 32) | its K-blocks), and a peer's pull of that panel waits on exactly that
+  // word -- not on a "all my panels are ready" signal -- so the operand the peers pull first is packed
+  // first and released alone (on 2 x 2 with the local-first order: the B panels).
   if (ctx->nranks > 1 && !pipe) {
-    for (int k = 0; k < p.L; ++k) {  // A's own panels first: on host operands B may still be uploading
-      if (p.ownA_off[k] != SIZE_MAX) {
+    const bool ce = ctx->transport == 0;
+    auto publish_panel = [&](int operand, int k) -> dbm_status {
+      if (!ce) return DBM_OK;
+      for (int q = 0; q < ctx->nranks; ++q)
+        if (q != ctx->rank)
+          if (dbm_status e = xwrite_word(ctx, cs, q, xprog_word(ctx->nranks, p.L, ctx->rank, operand, k),
+                                         (ep << 32) | (uint64_t)p.kb[k]))
+            return e;
+      return DBM_OK;
+    };
+    bool a_first = false, b_first = false;  // a peer's first step pulls my A / my B panel
+    for (int q = 0; q < ctx->nranks && ce; ++q) {
+      if (q == ctx->rank) continue;
+      const int rq = q / p.pc, cq = q % p.pc;
+      const int kq = (rq + cq + (p.local_first ? local_first_start(p.pr, p.pc, q) : 0)) % p.L;
+      a_first |= rq * p.pc + kq % p.pc == ctx->rank;
+      b_first |= (kq % p.pr) * p.pc + cq == ctx->rank;
+    }
+    auto own_a = [&]() -> dbm_status {
+      for (int k = 0; k < p.L; ++k) {
+        if (p.ownA_off[k] == SIZE_MAX) continue;
         const int64_t col0 = (k - p.c) / p.pc, stride = p.L / p.pc;
         double* dst = (double*)(xp + p.ownA_off[k]);
         if (dens && !p.a_packed) {
@@ -1914,11 +1938,13 @@ dbm_status multiply_impl(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_matrix B, 
           launch_pack_cols(A->arena, p.mloc, p.kA, (int)bs, col0, stride, p.kb[k], dst, cs);
         }
         launches += (M * p.kb[k]) ? 1 : 0;
+        if (dbm_status e = publish_panel(0, k)) return e;
       }
-    }
-    if (hio && hio->b_deferred) CUDA_TRY(ctx, cudaStreamWaitEvent(cs, hio->all_ev, 0));
-    for (int k = 0; k < p.L; ++k) {
-      if (p.ownB_off[k] != SIZE_MAX) {
+      return DBM_OK;
+    };
+    auto own_b = [&]() -> dbm_status {
+      for (int k = 0; k < p.L; ++k) {
+        if (p.ownB_off[k] == SIZE_MAX) continue;
         const int64_t row0 = (k - p.r) / p.pr, stride = p.L / p.pr;
         double* dst = (double*)(xp + p.ownB_off[k]);
         if (dens && !p.b_packed) {
@@ -1929,7 +1955,17 @@ dbm_status multiply_impl(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_matrix B, 
           launch_pack_rows(B->arena, p.nloc, (int)bs, row0, stride, p.kb[k], dst, cs);
         }
         launches += (N * p.kb[k]) ? 1 : 0;
+        if (dbm_status e = publish_panel(1, k)) return e;
       }
+      return DBM_OK;
+    };
+    if (b_first && !a_first && !hio) {  // (host operands: B may still be uploading, A goes first)
+      if (dbm_status e = own_b()) return e;
+      if (dbm_status e = own_a()) return e;
+    } else {
+      if (dbm_status e = own_a()) return e;
+      if (hio && hio->b_deferred) CUDA_TRY(ctx, cudaStreamWaitEvent(cs, hio->all_ev, 0));
+      if (dbm_status e = own_b()) return e;
     }
     CUDA_TRY(ctx, cudaGetLastError());
   }
@@ -2027,8 +2063,7 @@ dbm_status multiply_impl(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_matrix B, 
   auto exchange = [&](int s) -> dbm_status {
     if (ctx->transport == 0) {
       ProfScope ps(ctx, ctx->comm, 5, 0.0, recv_bytes(s));  // copy-engine pulls of this step
-      return post_pulls(ctx, p, peer_plan, s, ws, bufA_of[s], bufB_of[s], &st.bytes_sent, &st.bytes_recv,
-                        pipe ? ep : 0);
+      return post_pulls(ctx, p, peer_plan, s, ws, bufA_of[s], bufB_of[s], &st.bytes_sent, &st.bytes_recv, ep);
     }
     return post_exchange(ctx, p, s, ws, A->arena, B->arena, bufA_of[s], bufB_of[s], &st.bytes_sent, &st.bytes_recv);
   };
@@ -2047,9 +2082,9 @@ dbm_status multiply_impl(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_matrix B, 
     }
     if (ctx->transport == 0) {
       // Copy engines over the IPC-mapped workspaces, ordered by device-side signals (no host sync once
-      // the workspace is registered): every signal this rank owes its peers -- "my panels are ready"
-      // (on the compute stream, behind my own densify / pack) or, with host operands, the chunk-by-chunk
-      // progress (upload stream) -- is enqueued before the first wait on theirs.
+      // the workspace is registered): every signal this rank owes its peers -- each own panel's progress
+      // word (on the compute stream behind its densify / pack, or chunk by chunk on the own-panel stream
+      // in the pipelined modes) -- is enqueued before the first wait on theirs.
       peer_plan.resize(ctx->nranks);
       for (int q = 0; q < ctx->nranks; ++q)
         if (q != ctx->rank)
@@ -2067,10 +2102,7 @@ dbm_status multiply_impl(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_matrix B, 
           own_ev.push_back(get_event(ctx));
           CUDA_TRY(ctx, cudaEventRecord(own_ev.back(), up));
         }
-      } else {
-        if (dbm_status e = xsignal(ctx, cs, X_READY, ep)) return e;
-        if (dbm_status e = xwait(ctx, ctx->comm, X_READY, ep)) return e;  // every owner's panels are ready
-      }
+      }  // (else: every own panel's progress word went out behind its densify / pack above)
     }
   }
 
@@ -2097,7 +2129,7 @@ dbm_status multiply_impl(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_matrix B, 
       for (int j = 0; j < nsub0; ++j) {
         ev_c[j] = get_event(ctx);
         if (dbm_status e = post_pulls_chunk(ctx, p, peer_plan, 0, ws, bufA_of[0], bufB_of[0], cb0[j], cb0[j + 1],
-                                            j == 0, &st.bytes_sent, &st.bytes_recv, pipe ? ep : 0))
+                                            j == 0, &st.bytes_sent, &st.bytes_recv, ep))
           return e;
         CUDA_TRY(ctx, cudaEventRecord(ev_c[j], ctx->comm));
       }

@@ -1901,6 +1901,15 @@ dbm_status multiply_impl(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_matrix B, 
     ep = ++ctx->epoch;
   }
 
+  // copy-engine pulls write only this rank's receive buffers: they wait for the compute stream's work
+  // up to here (the previous multiply's reads of those buffers), not for the own panels packed next
+  // (each pull waits on its panel's progress word instead)
+  cudaEvent_t ev_prior = nullptr;
+  if (ctx->nranks > 1 && ctx->transport == 0) {
+    ev_prior = get_event(ctx);
+    CUDA_TRY(ctx, cudaEventRecord(ev_prior, cs));
+  }
+
   // ------------------------------------------------ own panels (densify or pack), on the compute stream
   // Copy-engine transport: each own panel's completion goes into every peer's progress table as soon as
   // it is in place ((epoch << 32) | its K-blocks), and a peer's pull of that panel waits on exactly that
@@ -2073,8 +2082,12 @@ dbm_status multiply_impl(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_matrix B, 
       bufA_of[s] = (p.a_src(s) != p.me()) ? (na++ & 1) : -1;
       bufB_of[s] = (p.b_src(s) != p.me()) ? (nb++ & 1) : -1;
     }
-    ev_ready = get_event(ctx);
-    CUDA_TRY(ctx, cudaEventRecord(ev_ready, cs));
+    if (ev_prior) {
+      ev_ready = ev_prior;
+    } else {  // (NCCL: the sends read the own panels packed above)
+      ev_ready = get_event(ctx);
+      CUDA_TRY(ctx, cudaEventRecord(ev_ready, cs));
+    }
     CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->comm, ev_ready, 0));
     for (int s = 0; s < p.L; ++s) {
       ev_x[s] = get_event(ctx);

@@ -849,6 +849,14 @@ bool stackgen_dbuf();
 bool zero_copy_a();
 // DBM_SMMQ=0 keeps the padded small sizes on the per-run kernel (the A/B of the R x R square kernel);
 // DBM_SMMQ=2 takes the squares even when they cannot fill the GPU (tests of small shapes)
+bool ce_pack_on() {
+  static const bool on = [] {
+    const char* e = getenv("DBM_CE_PACK");
+    return !(e && *e == '0');
+  }();
+  return on;
+}
+
 int smmq_on() {
   static const int on = [] {
     const char* e = getenv("DBM_SMMQ");
@@ -1905,6 +1913,7 @@ dbm_status multiply_impl(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_matrix B, 
   // up to here (the previous multiply's reads of those buffers), not for the own panels packed next
   // (each pull waits on its panel's progress word instead)
   cudaEvent_t ev_prior = nullptr;
+  bool ce_ident_a = false, ce_ident_b = false;  // own panel copied by the copy engine (see below)
   if (ctx->nranks > 1 && ctx->transport == 0) {
     ev_prior = get_event(ctx);
     CUDA_TRY(ctx, cudaEventRecord(ev_prior, cs));
@@ -1926,6 +1935,16 @@ dbm_status multiply_impl(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_matrix B, 
             return e;
       return DBM_OK;
     };
+    // Blocked path, dense operands, L = pc (A) / L = pr (B): the rank's one own panel of that operand is
+    // its arena verbatim (packed panel = row-major over (li, kk) = the local CSR order), so the local steps
+    // read the arena and the pool copy the peers pull is a copy-engine copy on the own-panel stream --
+    // no SM work, nothing on the compute stream (DBM_CE_PACK=0: the pack kernels)
+    ce_ident_a = ce && !dens && !hio && ce_pack_on() && p.L == p.pc && !A->sparse;
+    ce_ident_b = ce && !dens && !hio && ce_pack_on() && p.L == p.pr && !B->sparse;
+    if (ce_ident_a || ce_ident_b) {
+      if (!ctx->own) CUDA_TRY(ctx, cudaStreamCreateWithFlags(&ctx->own, cudaStreamNonBlocking));
+      CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->own, ev_prior, 0));  // the arenas' earlier writers
+    }
     bool a_first = false, b_first = false;  // a peer's first step pulls my A / my B panel
     for (int q = 0; q < ctx->nranks && ce; ++q) {
       if (q == ctx->rank) continue;
@@ -1939,6 +1958,15 @@ dbm_status multiply_impl(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_matrix B, 
         if (p.ownA_off[k] == SIZE_MAX) continue;
         const int64_t col0 = (k - p.c) / p.pc, stride = p.L / p.pc;
         double* dst = (double*)(xp + p.ownA_off[k]);
+        if (ce_ident_a) {  // the panel IS the arena: a copy-engine copy beside the compute, published there
+          CUDA_TRY(ctx, cudaMemcpyAsync(dst, A->arena, p.a_panel_bytes(k), cudaMemcpyDeviceToDevice, ctx->own));
+          for (int q = 0; q < ctx->nranks; ++q)
+            if (q != ctx->rank)
+              if (dbm_status e = xwrite_word(ctx, ctx->own, q, xprog_word(ctx->nranks, p.L, ctx->rank, 0, k),
+                                             (ep << 32) | (uint64_t)p.kb[k]))
+                return e;
+          continue;
+        }
         if (dens && !p.a_packed) {
           ProfScope ps(ctx, cs, 2, 0.0, 16.0 * M * p.kb[k] * bs);
           if (dbm_status e = densify_a(ctx, A, col0, stride, p.kb[k], dst, p.ld_panel(k), 1, cs)) return e;
@@ -1956,6 +1984,15 @@ dbm_status multiply_impl(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_matrix B, 
         if (p.ownB_off[k] == SIZE_MAX) continue;
         const int64_t row0 = (k - p.r) / p.pr, stride = p.L / p.pr;
         double* dst = (double*)(xp + p.ownB_off[k]);
+        if (ce_ident_b) {
+          CUDA_TRY(ctx, cudaMemcpyAsync(dst, B->arena, p.b_panel_bytes(k), cudaMemcpyDeviceToDevice, ctx->own));
+          for (int q = 0; q < ctx->nranks; ++q)
+            if (q != ctx->rank)
+              if (dbm_status e = xwrite_word(ctx, ctx->own, q, xprog_word(ctx->nranks, p.L, ctx->rank, 1, k),
+                                             (ep << 32) | (uint64_t)p.kb[k]))
+                return e;
+          continue;
+        }
         if (dens && !p.b_packed) {
           ProfScope ps(ctx, cs, 2, 0.0, 16.0 * N * p.kb[k] * bs);
           if (dbm_status e = densify_b(ctx, B, row0, stride, p.kb[k], dst, p.ld_panel(k), 0, cs)) return e;
@@ -2170,9 +2207,11 @@ dbm_status multiply_impl(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_matrix B, 
     const double* Bp;
     if (ctx->nranks > 1) {
       Ap = p.a_src(s) != p.me() ? (const double*)(ws + p.off_recvA[bufA_of[s]])
-                                : (p.ownA_off[k] != SIZE_MAX ? (const double*)(xp + p.ownA_off[k]) : A->arena);
+                                : (p.ownA_off[k] != SIZE_MAX && !ce_ident_a ? (const double*)(xp + p.ownA_off[k])
+                                                                            : A->arena);
       Bp = p.b_src(s) != p.me() ? (const double*)(ws + p.off_recvB[bufB_of[s]])
-                                : (p.ownB_off[k] != SIZE_MAX ? (const double*)(xp + p.ownB_off[k]) : B->arena);
+                                : (p.ownB_off[k] != SIZE_MAX && !ce_ident_b ? (const double*)(xp + p.ownB_off[k])
+                                                                            : B->arena);
     } else {
       Ap = A->arena;
       Bp = B->arena;
@@ -2405,6 +2444,12 @@ dbm_status multiply_impl(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_matrix B, 
     // the comm stream's last op covers every transfer of this rank (and the upload stream's own panels)
     CUDA_TRY(ctx, cudaStreamWaitEvent(cs, ev_x[p.L - 1], 0));
     if (pipe) CUDA_TRY(ctx, cudaStreamWaitEvent(cs, own_ev.back(), 0));
+    if (ce_ident_a || ce_ident_b) {  // the copy-engine panel copies read the arenas
+      cudaEvent_t e = get_event(ctx);
+      CUDA_TRY(ctx, cudaEventRecord(e, ctx->own));
+      CUDA_TRY(ctx, cudaStreamWaitEvent(cs, e, 0));
+      ctx->ev_pool.push_back(e);
+    }
   }
   if (dens && M * N > 0 && !(hio && hio->c_downloaded)) {
     if (hio && hio->c_ev) CUDA_TRY(ctx, cudaStreamWaitEvent(cs, hio->c_ev, 0));  // C_in uploaded

@@ -1926,11 +1926,11 @@ dbm_status multiply_impl(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_matrix B, 
   // first and released alone (on 2 x 2 with the local-first order: the B panels).
   if (ctx->nranks > 1 && !pipe) {
     const bool ce = ctx->transport == 0;
-    auto publish_panel = [&](int operand, int k) -> dbm_status {
+    auto publish_panel = [&](int operand, int k, cudaStream_t st) -> dbm_status {
       if (!ce) return DBM_OK;
       for (int q = 0; q < ctx->nranks; ++q)
         if (q != ctx->rank)
-          if (dbm_status e = xwrite_word(ctx, cs, q, xprog_word(ctx->nranks, p.L, ctx->rank, operand, k),
+          if (dbm_status e = xwrite_word(ctx, st, q, xprog_word(ctx->nranks, p.L, ctx->rank, operand, k),
                                          (ep << 32) | (uint64_t)p.kb[k]))
             return e;
       return DBM_OK;
@@ -1960,11 +1960,7 @@ dbm_status multiply_impl(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_matrix B, 
         double* dst = (double*)(xp + p.ownA_off[k]);
         if (ce_ident_a) {  // the panel IS the arena: a copy-engine copy beside the compute, published there
           CUDA_TRY(ctx, cudaMemcpyAsync(dst, A->arena, p.a_panel_bytes(k), cudaMemcpyDeviceToDevice, ctx->own));
-          for (int q = 0; q < ctx->nranks; ++q)
-            if (q != ctx->rank)
-              if (dbm_status e = xwrite_word(ctx, ctx->own, q, xprog_word(ctx->nranks, p.L, ctx->rank, 0, k),
-                                             (ep << 32) | (uint64_t)p.kb[k]))
-                return e;
+          if (dbm_status e = publish_panel(0, k, ctx->own)) return e;
           continue;
         }
         if (dens && !p.a_packed) {
@@ -1975,7 +1971,7 @@ dbm_status multiply_impl(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_matrix B, 
           launch_pack_cols(A->arena, p.mloc, p.kA, (int)bs, col0, stride, p.kb[k], dst, cs);
         }
         launches += (M * p.kb[k]) ? 1 : 0;
-        if (dbm_status e = publish_panel(0, k)) return e;
+        if (dbm_status e = publish_panel(0, k, cs)) return e;
       }
       return DBM_OK;
     };
@@ -1986,11 +1982,7 @@ dbm_status multiply_impl(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_matrix B, 
         double* dst = (double*)(xp + p.ownB_off[k]);
         if (ce_ident_b) {
           CUDA_TRY(ctx, cudaMemcpyAsync(dst, B->arena, p.b_panel_bytes(k), cudaMemcpyDeviceToDevice, ctx->own));
-          for (int q = 0; q < ctx->nranks; ++q)
-            if (q != ctx->rank)
-              if (dbm_status e = xwrite_word(ctx, ctx->own, q, xprog_word(ctx->nranks, p.L, ctx->rank, 1, k),
-                                             (ep << 32) | (uint64_t)p.kb[k]))
-                return e;
+          if (dbm_status e = publish_panel(1, k, ctx->own)) return e;
           continue;
         }
         if (dens && !p.b_packed) {
@@ -2001,7 +1993,7 @@ dbm_status multiply_impl(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_matrix B, 
           launch_pack_rows(B->arena, p.nloc, (int)bs, row0, stride, p.kb[k], dst, cs);
         }
         launches += (N * p.kb[k]) ? 1 : 0;
-        if (dbm_status e = publish_panel(1, k)) return e;
+        if (dbm_status e = publish_panel(1, k, cs)) return e;
       }
       return DBM_OK;
     };

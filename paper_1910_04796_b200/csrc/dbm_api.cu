@@ -1935,12 +1935,13 @@ dbm_status multiply_impl(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_matrix B, 
             return e;
       return DBM_OK;
     };
-    // Blocked path, dense operands, L = pc (A) / L = pr (B): the rank's one own panel of that operand is
-    // its arena verbatim (packed panel = row-major over (li, kk) = the local CSR order), so the local steps
-    // read the arena and the pool copy the peers pull is a copy-engine copy on the own-panel stream --
-    // no SM work, nothing on the compute stream (DBM_CE_PACK=0: the pack kernels)
-    ce_ident_a = ce && !dens && !hio && ce_pack_on() && p.L == p.pc && !A->sparse;
-    ce_ident_b = ce && !dens && !hio && ce_pack_on() && p.L == p.pr && !B->sparse;
+    // Packed panels (blocked path; the densified path's zero-copy B / A for bs 64) of dense operands with
+    // L = pc (A) / L = pr (B): the rank's one own panel of that operand is its arena verbatim (packed panel
+    // = row-major blocks = the local CSR order), so the local steps read the arena and the pool copy the
+    // peers pull is a cudaMemcpyAsync on the own-panel stream, off the compute stream (DBM_CE_PACK=0: the
+    // pack kernels)
+    ce_ident_a = ce && (!dens || p.a_packed) && !hio && ce_pack_on() && p.L == p.pc && !A->sparse;
+    ce_ident_b = ce && (!dens || p.b_packed) && !hio && ce_pack_on() && p.L == p.pr && !B->sparse;
     if (ce_ident_a || ce_ident_b) {
       if (!ctx->own) CUDA_TRY(ctx, cudaStreamCreateWithFlags(&ctx->own, cudaStreamNonBlocking));
       CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->own, ev_prior, 0));  // the arenas' earlier writers

@@ -134,9 +134,10 @@ dbm_status dbm_ctx_profile_timeline(dbm_ctx ctx, int max_records, double* out, i
  *     freed by dbm_ctx_destroy): a header of 64-bit signal words and the rank's own panels.  It is
  *     mapped into every peer with CUDA IPC when it grows (an all-gather of the handles with a host
  *     synchronisation; every rank sizes it by the maximum over all ranks' plans, so every rank grows
- *     it in the same multiply); otherwise a multiply orders ranks device-side only: "panels ready" /
- *     "done" epochs written into the peers' headers (cuStreamWriteValue64) and awaited on the
- *     streams (cuStreamWaitValue64), no host synchronisation.
+ *     it in the same multiply); otherwise a multiply orders ranks device-side only: per-panel progress
+ *     and "done" epochs written into the peers' headers (cuStreamWriteValue64) and awaited on the
+ *     streams (cuStreamWaitValue64), no host synchronisation.  Ranks take Cannon's steps in a
+ *     local-first order (dbm_debug_first_step).
  * 1 = NCCL grouped ncclSend / ncclRecv.
  * Every rank must use the same transport.  Changes dbm_multiply_workspace() for the blocked path. */
 dbm_status dbm_ctx_set_transport(dbm_ctx ctx, int transport);

@@ -849,10 +849,10 @@ bool stackgen_dbuf();
 bool zero_copy_a();
 // DBM_SMMQ=0 keeps the padded small sizes on the per-run kernel (the A/B of the R x R square kernel);
 // DBM_SMMQ=2 takes the squares even when they cannot fill the GPU (tests of small shapes)
-bool ce_pack_on() {
+bool ce_pack_on() {  // opt-in (DBM_CE_PACK=1): see the own-panel block of multiply_impl
   static const bool on = [] {
     const char* e = getenv("DBM_CE_PACK");
-    return !(e && *e == '0');
+    return e && *e == '1';
   }();
   return on;
 }
@@ -1937,9 +1937,12 @@ dbm_status multiply_impl(dbm_ctx ctx, double alpha, dbm_matrix A, dbm_matrix B, 
     };
     // Packed panels (blocked path; the densified path's zero-copy B / A for bs 64) of dense operands with
     // L = pc (A) / L = pr (B): the rank's one own panel of that operand is its arena verbatim (packed panel
-    // = row-major blocks = the local CSR order), so the local steps read the arena and the pool copy the
-    // peers pull is a cudaMemcpyAsync on the own-panel stream, off the compute stream (DBM_CE_PACK=0: the
-    // pack kernels)
+    // = row-major blocks = the local CSR order), so with DBM_CE_PACK=1 the local steps read the arena and
+    // the pool copy the peers pull is a cudaMemcpyAsync on the own-panel stream.  Opt-in: a same-device
+    // copy needs the SMs (it does not go to a copy engine), so when the persistent GEMM / small-block
+    // kernel starts first the copy -- and the peers' first pulls behind it -- wait for that kernel (one
+    // 4-GPU session: 28 ms of idle per multiply on two ranks); the pack kernels on the compute stream
+    // stay the default.
     ce_ident_a = ce && (!dens || p.a_packed) && !hio && ce_pack_on() && p.L == p.pc && !A->sparse;
     ce_ident_b = ce && (!dens || p.b_packed) && !hio && ce_pack_on() && p.L == p.pr && !B->sparse;
     if (ce_ident_a || ce_ident_b) {

@@ -155,11 +155,11 @@ __device__ __forceinline__ void nu_kloop(double (&acc)[S][S][2], const int4* zt,
 //   * staging (TMA bulk copies into a 3-stage ring): lane l of warp w owns entry w + 4 l of the group; its
 //     metadata -- k, k offset, trip slots, then A and B block addresses -- is loaded in two levels, two
 //     and one groups ahead (each dependent lookup's latency hides under a group's compute), then the
-//     lane issues one cp.async.bulk per operand block,
-//     completing on its warp's mbarrier of the stage.  Blocks of odd element counts sit at any 8-B
-//     offset, so each copy takes the 16-B-aligned superset of its block (at most one extra double on
+//     lane issues one cp.async.bulk per operand block, completing on the stage's mbarrier (every thread
+//     arrives once per group, the data lanes with their bytes).  Blocks of odd element counts sit at any
+//     8-B offset, so each copy takes the 16-B-aligned superset of its block (at most one extra double on
 //     either side, never outside the block's 16-B granules) into a 16-B-aligned slot with room for it;
-//     a k table (written lane-parallel before the lanes arrive, so the stage's mbarriers publish it with
+//     a k table (written lane-parallel before the lanes arrive, so the stage's mbarrier publishes it with
 //     the data) gives, for every k index z of the group, the shared offsets of A(0, z) and B(z, 0) and
 //     the B column stride k_e.  No per-element staging instruction, no L1 traffic, one CTA barrier per
 //     group (the ring's reuse);
@@ -185,7 +185,7 @@ __global__ void __launch_bounds__(kNuWarps * 32, S == 4 ? 4 : 1)
                   int ngroups, double* __restrict__ C, const NUBlk* __restrict__ cblk, int kcap, int mmax_pad,
                   int nmax_pad, double alpha, double beta_first) {
   extern __shared__ __align__(16) double nsm[];
-  __shared__ __align__(8) uint64_t nmb[kNuStages][kNuWarps];
+  __shared__ __align__(8) uint64_t nmb[kNuStages];  // one per stage: every thread arrives, data lanes with tx
   constexpr int WK = kNuWarps / WR, SI = S / WR;
   const int kp = (kcap + 3) & ~3, ne = nu_group_entries(kp);
   const int a_reg = nu_a_region(kp, mmax_pad, ne), b_reg = nu_a_region(kp, nmax_pad, ne);
@@ -195,10 +195,10 @@ __global__ void __launch_bounds__(kNuWarps * 32, S == 4 ? 4 : 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
   const int rh = warp % WR, kg = warp / WR, i0 = rh * SI;
   const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(nsm);
-  const uint32_t mb0 = (uint32_t)__cvta_generic_to_shared(&nmb[0][0]);
+  const uint32_t mb0 = (uint32_t)__cvta_generic_to_shared(&nmb[0]);
   for (int i = threadIdx.x; i < kNuZero; i += blockDim.x) nsm[zero_off + i] = 0.0;
   if (threadIdx.x == 0) {
-    for (int i = 0; i < kNuStages * kNuWarps; ++i) nu_mbar_init(mb0 + 8 * i, 32);
+    for (int i = 0; i < kNuStages; ++i) nu_mbar_init(mb0 + 8 * i, kNuWarps * 32);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -250,7 +250,7 @@ __global__ void __launch_bounds__(kNuWarps * 32, S == 4 ? 4 : 1)
       if (grp >= ngroups) return;
       const int so = buf * st_d;
       int4* zt = reinterpret_cast<int4*>(nsm + so + a_reg + b_reg);
-      const uint32_t mb = mb0 + 8 * (buf * kNuWarps + warp);
+      const uint32_t mb = mb0 + 8 * buf;
       if (warp == kNuWarps - 1) {  // the k tail up to a multiple of 4: the zero region, stride 0; the K
         if (lane < 4 && pm_K + lane < kp) zt[pm_K + lane] = make_int4(zero_off, zero_off, 0, 0);
         if (lane == 0) reinterpret_cast<int*>(zt + kp)[0] = pm_K;
@@ -302,7 +302,7 @@ __global__ void __launch_bounds__(kNuWarps * 32, S == 4 ? 4 : 1)
       fetch1(grp + kNuStages + 1);  // group grp + 4's entries (both in flight during this group's compute)
       const int buf = grp % kNuStages;
 #pragma unroll
-      for (int w = 0; w < kNuWarps; ++w) nu_mbar_wait(mb0 + 8 * (buf * kNuWarps + w), (phase >> buf) & 1);
+      nu_mbar_wait(mb0 + 8 * buf, (phase >> buf) & 1);
       phase ^= 1u << buf;
       const int4* zt = reinterpret_cast<const int4*>(nsm + buf * st_d + a_reg + b_reg);
       const int K = reinterpret_cast<const int*>(zt + kp)[0];  // the group's concatenated K

@@ -52,23 +52,43 @@ __global__ void nu_fill_kernel(double* __restrict__ arena, const NUBlk* __restri
 // mode 1: B block (rows k x cols n) -> K-major columns: dense[(col0 + y) * ld + row0 + x]
 // mode 2: C block <- column-major dense: blk = alpha * dense[(col0 + y) * ld + row0 + x] + beta * blk
 //         (two roundings, no FMA, as the uniform undensify; beta == 0: blk not read)
-__global__ void nu_copy_kernel(const NUTask* __restrict__ tasks, int64_t ntasks, double* __restrict__ arena,
-                               double* __restrict__ dense, int64_t ld, int mode, double alpha, double beta) {
+constexpr int kNuTile = 64 * 65;  // shared transpose tile (doubles): blocks up to 64 x 64, rows padded by one
+
+// One CTA (8 warps) per task; lanes run along a block column (x, contiguous in the column-major block),
+// warps across columns -- no per-element index division.  Modes 1 and 2 are contiguous in x on both sides.
+// Mode 0 transposes (the dense row is contiguous in y): blocks up to 64 x 64 go through a shared tile, read
+// column by column and written row by row, so both sides stay coalesced; larger blocks copy directly.
+__global__ void __launch_bounds__(256) nu_copy_kernel(const NUTask* __restrict__ tasks, int64_t ntasks,
+                                                      double* __restrict__ arena, double* __restrict__ dense,
+                                                      int64_t ld, int mode, double alpha, double beta) {
+  __shared__ double tile[kNuTile];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
   for (int64_t t = blockIdx.x; t < ntasks; t += gridDim.x) {
     const NUTask k = tasks[t];
-    const int64_t n = (int64_t)k.rows * k.cols;
-    for (int64_t e = threadIdx.x; e < n; e += blockDim.x) {
-      const int64_t y = e / k.rows, x = e - y * k.rows;
-      if (mode == 0) {
-        dense[(k.row0 + x) * ld + k.col0 + y] = arena[k.src + e];
-      } else if (mode == 1) {
-        dense[(k.col0 + y) * ld + k.row0 + x] = arena[k.src + e];
-      } else {
-        const double d = __dmul_rn(alpha, dense[(k.col0 + y) * ld + k.row0 + x]);
-        double* p = arena + k.src + e;
-        *p = beta == 0.0 ? d : __dadd_rn(d, __dmul_rn(beta, *p));
-      }
+    const int rows = k.rows, cols = k.cols;
+    if (mode == 0 && rows <= 64 && cols <= 64) {
+      const int pitch = cols + 1;
+      for (int y = warp; y < cols; y += nw)
+        for (int x = lane; x < rows; x += 32) tile[x * pitch + y] = arena[k.src + (int64_t)y * rows + x];
+      __syncthreads();
+      for (int x = warp; x < rows; x += nw)
+        for (int y = lane; y < cols; y += 32) dense[(k.row0 + x) * ld + k.col0 + y] = tile[x * pitch + y];
+      __syncthreads();  // the next task's tile
+      continue;
     }
+    for (int y = warp; y < cols; y += nw)
+      for (int x = lane; x < rows; x += 32) {
+        const int64_t e = (int64_t)y * rows + x;
+        if (mode == 0) {
+          dense[(k.row0 + x) * ld + k.col0 + y] = arena[k.src + e];
+        } else if (mode == 1) {
+          dense[(k.col0 + y) * ld + k.row0 + x] = arena[k.src + e];
+        } else {
+          const double d = __dmul_rn(alpha, dense[(k.col0 + y) * ld + k.row0 + x]);
+          double* p = arena + k.src + e;
+          *p = beta == 0.0 ? d : __dadd_rn(d, __dmul_rn(beta, *p));
+        }
+      }
   }
 }
 

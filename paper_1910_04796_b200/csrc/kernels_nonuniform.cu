@@ -54,10 +54,10 @@ __global__ void nu_fill_kernel(double* __restrict__ arena, const NUBlk* __restri
 //         (two roundings, no FMA, as the uniform undensify; beta == 0: blk not read)
 constexpr int kNuTile = 64 * 65;  // shared transpose tile (doubles): blocks up to 64 x 64, rows padded by one
 
-// One CTA (8 warps) per task; lanes run along a block column (x, contiguous in the column-major block),
-// warps across columns -- no per-element index division.  Modes 1 and 2 are contiguous in x on both sides.
-// Mode 0 transposes (the dense row is contiguous in y): blocks up to 64 x 64 go through a shared tile, read
-// column by column and written row by row, so both sides stay coalesced; larger blocks copy directly.
+// One CTA (8 warps) per task.  Modes 1 and 2 are contiguous in x (down a block column) on both sides: a
+// flat loop over the block's elements (32-bit index math).  Mode 0 transposes (the dense row is contiguous
+// in y): blocks up to 64 x 64 go through a shared tile, read column by column and written row by row, so
+// both sides stay coalesced; larger blocks copy directly.
 __global__ void __launch_bounds__(256) nu_copy_kernel(const NUTask* __restrict__ tasks, int64_t ntasks,
                                                       double* __restrict__ arena, double* __restrict__ dense,
                                                       int64_t ld, int mode, double alpha, double beta) {
@@ -76,19 +76,20 @@ __global__ void __launch_bounds__(256) nu_copy_kernel(const NUTask* __restrict__
       __syncthreads();  // the next task's tile
       continue;
     }
-    for (int y = warp; y < cols; y += nw)
-      for (int x = lane; x < rows; x += 32) {
-        const int64_t e = (int64_t)y * rows + x;
-        if (mode == 0) {
-          dense[(k.row0 + x) * ld + k.col0 + y] = arena[k.src + e];
-        } else if (mode == 1) {
-          dense[(k.col0 + y) * ld + k.row0 + x] = arena[k.src + e];
-        } else {
-          const double d = __dmul_rn(alpha, dense[(k.col0 + y) * ld + k.row0 + x]);
-          double* p = arena + k.src + e;
-          *p = beta == 0.0 ? d : __dadd_rn(d, __dmul_rn(beta, *p));
-        }
+    // (flat over the block: every lane busy for thin blocks too; 32-bit index math)
+    const int n = rows * cols;
+    for (int e = threadIdx.x; e < n; e += blockDim.x) {
+      const int y = e / rows, x = e - y * rows;
+      if (mode == 0) {
+        dense[(k.row0 + x) * ld + k.col0 + y] = arena[k.src + e];
+      } else if (mode == 1) {
+        dense[(k.col0 + y) * ld + k.row0 + x] = arena[k.src + e];
+      } else {
+        const double d = __dmul_rn(alpha, dense[(k.col0 + y) * ld + k.row0 + x]);
+        double* p = arena + k.src + e;
+        *p = beta == 0.0 ? d : __dadd_rn(d, __dmul_rn(beta, *p));
       }
+    }
   }
 }
 

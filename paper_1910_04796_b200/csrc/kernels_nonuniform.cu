@@ -4,8 +4,9 @@
 // back; the host keeps every slot's element offset and shape (NUBlk).
 //
 //   nu_fill_kernel     the counter generator at global element coordinates
-//   nu_copy_kernel     block <-> dense panel copies from a task list: densify A (K-major rows), densify
-//                      B (K-major columns) and undensify C with alpha / beta (column-major)
+//   nu_copy_kernel     block <-> dense panel copies from a task list: densify B (K-major columns) and
+//                      undensify C with alpha / beta (column-major); nu_copy_a_kernel densify A (K-major
+//                      rows, a transpose through a shared tile)
 //   nu_pack_kernel     whole-block gathers into packed Cannon panels (blocked path)
 //   nu_smm_kernel      the blocked path's small-block products of mixed (m, n, k): one CTA per C-block
 //                      run, entry groups staged by TMA bulk copies into a 3-stage mbarrier ring, K split
@@ -55,18 +56,38 @@ __global__ void nu_fill_kernel(double* __restrict__ arena, const NUBlk* __restri
 constexpr int kNuTile = 64 * 65;  // shared transpose tile (doubles): blocks up to 64 x 64, rows padded by one
 
 // One CTA (8 warps) per task.  Modes 1 and 2 are contiguous in x (down a block column) on both sides: a
-// flat loop over the block's elements (32-bit index math).  Mode 0 transposes (the dense row is contiguous
-// in y): blocks up to 64 x 64 go through a shared tile, read column by column and written row by row, so
-// both sides stay coalesced; larger blocks copy directly.
+// flat loop over the block's elements (32-bit index math), no shared memory.
 __global__ void __launch_bounds__(256) nu_copy_kernel(const NUTask* __restrict__ tasks, int64_t ntasks,
                                                       double* __restrict__ arena, double* __restrict__ dense,
                                                       int64_t ld, int mode, double alpha, double beta) {
+  for (int64_t t = blockIdx.x; t < ntasks; t += gridDim.x) {
+    const NUTask k = tasks[t];
+    const int rows = k.rows, n = k.rows * k.cols;
+    for (int e = threadIdx.x; e < n; e += blockDim.x) {
+      const int y = e / rows, x = e - y * rows;
+      if (mode == 1) {
+        dense[(k.col0 + y) * ld + k.row0 + x] = arena[k.src + e];
+      } else {
+        const double d = __dmul_rn(alpha, dense[(k.col0 + y) * ld + k.row0 + x]);
+        double* p = arena + k.src + e;
+        *p = beta == 0.0 ? d : __dadd_rn(d, __dmul_rn(beta, *p));
+      }
+    }
+  }
+}
+
+// Mode 0 transposes (the dense row is contiguous in y): blocks up to 64 x 64 go through a shared tile, read
+// down the block columns and written along the dense rows, so both sides stay coalesced; larger blocks
+// copy directly.
+__global__ void __launch_bounds__(256) nu_copy_a_kernel(const NUTask* __restrict__ tasks, int64_t ntasks,
+                                                        const double* __restrict__ arena, double* __restrict__ dense,
+                                                        int64_t ld) {
   __shared__ double tile[kNuTile];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
   for (int64_t t = blockIdx.x; t < ntasks; t += gridDim.x) {
     const NUTask k = tasks[t];
     const int rows = k.rows, cols = k.cols;
-    if (mode == 0 && rows <= 64 && cols <= 64) {
+    if (rows <= 64 && cols <= 64) {
       const int pitch = cols + 1;
       for (int y = warp; y < cols; y += nw)
         for (int x = lane; x < rows; x += 32) tile[x * pitch + y] = arena[k.src + (int64_t)y * rows + x];
@@ -76,19 +97,10 @@ __global__ void __launch_bounds__(256) nu_copy_kernel(const NUTask* __restrict__
       __syncthreads();  // the next task's tile
       continue;
     }
-    // (flat over the block: every lane busy for thin blocks too; 32-bit index math)
     const int n = rows * cols;
     for (int e = threadIdx.x; e < n; e += blockDim.x) {
       const int y = e / rows, x = e - y * rows;
-      if (mode == 0) {
-        dense[(k.row0 + x) * ld + k.col0 + y] = arena[k.src + e];
-      } else if (mode == 1) {
-        dense[(k.col0 + y) * ld + k.row0 + x] = arena[k.src + e];
-      } else {
-        const double d = __dmul_rn(alpha, dense[(k.col0 + y) * ld + k.row0 + x]);
-        double* p = arena + k.src + e;
-        *p = beta == 0.0 ? d : __dadd_rn(d, __dmul_rn(beta, *p));
-      }
+      dense[(k.row0 + x) * ld + k.col0 + y] = arena[k.src + e];
     }
   }
 }
@@ -416,7 +428,10 @@ void launch_nu_fill(double* arena, const NUBlk* blk, int64_t nslots, uint64_t se
 void launch_nu_copy(const NUTask* tasks, int64_t ntasks, double* arena, double* dense, int64_t ld, int mode,
                     double alpha, double beta, cudaStream_t st) {
   if (ntasks <= 0) return;
-  nu_copy_kernel<<<nu_grid(ntasks), 256, 0, st>>>(tasks, ntasks, arena, dense, ld, mode, alpha, beta);
+  if (mode == 0)
+    nu_copy_a_kernel<<<nu_grid(ntasks), 256, 0, st>>>(tasks, ntasks, arena, dense, ld);
+  else
+    nu_copy_kernel<<<nu_grid(ntasks), 256, 0, st>>>(tasks, ntasks, arena, dense, ld, mode, alpha, beta);
 }
 
 void launch_nu_pack(const NUPack* tasks, int64_t ntasks, const double* src, double* dst, cudaStream_t st) {

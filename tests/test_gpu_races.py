@@ -17,7 +17,7 @@ import torch
 pytestmark = pytest.mark.gpu
 
 SEED = 1910
-REPS = 6
+REPS = 16
 TOL = 1e-12
 
 

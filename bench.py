@@ -183,6 +183,10 @@ def run_reference(args, cfg, name, world, rank):
     M, N, K, bs, path, _ = cfg
     if rank != 0:
         return
+    if world > 1 and os.environ.get("OMP_NUM_THREADS") == "1":
+        # torchrun pins every process to one OpenMP thread; rank 0 is the only one working here, so it
+        # gets the host's cores, as at N = 1 (set before the oracle library, and its OpenMP, load)
+        os.environ["OMP_NUM_THREADS"] = str(len(os.sched_getaffinity(0)))
     occ = SPARSE_OCC.get(args.config)
     kpre = oracle_kpre(M, N, K, bs, 4.0, occ)  # each step: the fixed 64-row sample over a K prefix (~4 s)
     times = []

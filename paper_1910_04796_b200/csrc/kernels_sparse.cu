@@ -603,11 +603,11 @@ __global__ void __launch_bounds__(kSpBulkWarps * 32, 1)
     }
     return true;
   };
-  double acc[MT][MT][2];
+  double acc[MT][MT][2], cold[MT][MT][2];  // (cold: the run's C values, loaded at its first entry)
 #pragma unroll
   for (int i = 0; i < MT; ++i)
 #pragma unroll
-    for (int j = 0; j < MT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    for (int j = 0; j < MT; ++j) acc[i][j][0] = acc[i][j][1] = cold[i][j][0] = cold[i][j][1] = 0.0;
   int inflight = 0;
 #pragma unroll
   for (int i = 0; i < S - 1; ++i) inflight += issue_next(i) ? 1 : 0;
@@ -630,6 +630,18 @@ __global__ void __launch_bounds__(kSpBulkWarps * 32, 1)
     }
     --inflight;
     const int cslot = smeta[warp][si][0], flags = smeta[warp][si][1];
+    if ((flags & 1) && beta_first != 0.0) {  // a run's first entry: its C values load under its products
+      const double* cbk = C + (int64_t)cslot * BB;
+#pragma unroll
+      for (int mi = 0; mi < MT; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < MT; ++ni)
+#pragma unroll
+          for (int jj = 0; jj < 2; ++jj) {
+            const int m = rowm[mi], n = ni * 8 + 2 * t + jj;
+            cold[mi][ni][jj] = (m < BS && n < BS) ? cbk[m + n * BS] : 0.0;
+          }
+    }
     const double* sA = ring + si * Q::STG;  // (m, k) at k*BS + m
     const double* sB = sA + R::A_D;         // (k, n) at n*BS + k
 #pragma unroll
@@ -658,9 +670,9 @@ __global__ void __launch_bounds__(kSpBulkWarps * 32, 1)
           for (int jj = 0; jj < 2; ++jj) {
             const int m = rowm[mi], n = ni * 8 + 2 * t + jj;
             if (m < BS && n < BS) {
-              double* p = cbk + m + n * BS;
+              const double c0 = cold[mi][ni][jj];
               const double ab = __dmul_rn(alpha, acc[mi][ni][jj]);
-              *p = beta_first == 1.0 ? __dadd_rn(*p, ab) : beta_first == 0.0 ? ab : fma(beta_first, *p, ab);
+              cbk[m + n * BS] = beta_first == 1.0 ? __dadd_rn(c0, ab) : beta_first == 0.0 ? ab : fma(beta_first, c0, ab);
             }
             acc[mi][ni][jj] = 0.0;
           }

@@ -437,11 +437,18 @@ __global__ void __launch_bounds__(SpRunCfg<BS>::WARPS * 32, 1)
     // sparse stacks carry run offsets; dense stacks (off == nullptr) are uniform runs of kb entries
     const int64_t e0 = off ? off[run] : run * kb, e1 = off ? off[run + 1] : e0 + kb;
     if (e0 == e1) continue;
-    double acc[MT][NPW][2];
+    double acc[MT][NPW][2], cold[MT][NPW][2];  // (cold: the run's C values, loaded under its products)
+    double* cb = C + (int64_t)trip[3 * e0 + 2] * BB;
 #pragma unroll
     for (int i = 0; i < MT; ++i)
 #pragma unroll
-      for (int j = 0; j < NPW; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+      for (int j = 0; j < NPW; ++j)
+#pragma unroll
+        for (int jj = 0; jj < 2; ++jj) {
+          acc[i][j][jj] = 0.0;
+          const int m = rowm[i], n = (tw * NPW + j) * 8 + 2 * t + jj;
+          cold[i][j][jj] = (beta_first != 0.0 && m < BS && n < BS) ? cb[m + n * BS] : 0.0;
+        }
     team_sync();  // the previous run's last stage has been consumed by every team warp
     load(st0, e0, e1);
     int si = 0;
@@ -477,7 +484,6 @@ __global__ void __launch_bounds__(SpRunCfg<BS>::WARPS * 32, 1)
       }
       team_sync();  // every warp is done with `cur` before it is refilled
     }
-    double* cb = C + (int64_t)trip[3 * e0 + 2] * BB;
 #pragma unroll
     for (int mi = 0; mi < MT; ++mi)
 #pragma unroll
@@ -486,9 +492,8 @@ __global__ void __launch_bounds__(SpRunCfg<BS>::WARPS * 32, 1)
         for (int jj = 0; jj < 2; ++jj) {
           const int m = rowm[mi], n = (tw * NPW + ni) * 8 + 2 * t + jj;
           if (m < BS && n < BS) {
-            double* p = cb + m + n * BS;
-            const double ab = __dmul_rn(alpha, acc[mi][ni][jj]);
-            *p = beta_first == 1.0 ? __dadd_rn(*p, ab) : beta_first == 0.0 ? ab : fma(beta_first, *p, ab);
+            const double c0 = cold[mi][ni][jj], ab = __dmul_rn(alpha, acc[mi][ni][jj]);
+            cb[m + n * BS] = beta_first == 1.0 ? __dadd_rn(c0, ab) : beta_first == 0.0 ? ab : fma(beta_first, c0, ab);
           }
         }
   }
